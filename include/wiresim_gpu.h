@@ -1,0 +1,189 @@
+/*
+ * wiresim_gpu.h — C ABI of the B200-native Wire-Cell signal-simulation hot path
+ * (rasterize -> scatter-add -> FFT convolution), a drop-in for the
+ * raster/scatter/convolve section of the reference `wiresim` library
+ * (/root/reference/proj). Plain C types only: pointers, sizes, PODs. No
+ * exceptions cross this boundary; every call returns a ws_status and leaves a
+ * thread-local message readable with ws_last_error().
+ *
+ * Reference interfaces each entry point replaces (file:line under proj/):
+ *
+ *   ws_plane_create        build_response(GridSpec, ResponseParams)     include/wiresim/spectral.hpp:43
+ *                          (spectral.cpp:87-139; precomputed once per plane
+ *                          instead of once per run_simulation, pipeline.cpp:417)
+ *                          + convolve's support check                   src/spectral.cpp:147-153
+ *   ws_rasterize           rasterize_depo over all depos + scatter_add_parallel
+ *                          include/wiresim/rasterize.hpp:74-76, scatter.hpp:25-26
+ *                          (pipeline.cpp:374-413)
+ *   ws_convolve            convolve(ChargeGrid, ResponseKernel, workers)  include/wiresim/spectral.hpp:47
+ *   ws_simulate_plane      run_simulation(SimConfig, vector<Depo>) up to the
+ *                          pre-noise frame                               include/wiresim/pipeline.hpp:104
+ *                          (pipeline.cpp:345-419)
+ *   ws_simulate_event      N independent planes (one plane per run)
+ *   ws_noise_digitize      add_noise + digitize                          include/wiresim/spectral.hpp:61-65
+ *
+ * Data layout (identical to the reference's):
+ *   ws_depo     == wiresim::Depo       (core.hpp:63-70), 48 B AoS
+ *   ws_grid_spec== wiresim::GridSpec   (core.hpp:40-58)
+ *   frames      row-major padded grid, row = wire, column = tick (core.hpp:17-35,
+ *               94-107), padded_wires x padded_ticks; float32 on this side.
+ *
+ * Functions suffixed _device take device pointers and are asynchronous on the
+ * context's stream; the others take host pointers and return when the result
+ * is in host memory. There is no CPU fallback: without a usable sm_100 device
+ * every call fails with WS_ECUDA.
+ */
+#ifndef WIRESIM_GPU_H
+#define WIRESIM_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WS_ABI_VERSION 1
+
+typedef enum ws_status {
+    WS_OK = 0,
+    WS_EINVAL = 1,   /* std::invalid_argument in the reference */
+    WS_ERANGE = 2,   /* std::out_of_range */
+    WS_EDOMAIN = 3,  /* std::domain_error (e.g. drift_depo behind the plane) */
+    WS_ERUNTIME = 4, /* std::runtime_error */
+    WS_ECUDA = 5,    /* CUDA runtime / device failure (no CPU fallback) */
+    WS_ENOMEM = 6
+} ws_status;
+
+typedef struct ws_grid_spec {
+    uint64_t n_wires, n_ticks, pad_wires, pad_ticks;
+    double pitch;    /* mm per wire */
+    double tick;     /* us per tick */
+    double origin_x; /* mm, low edge of wire 0 */
+    double origin_t; /* us, low edge of tick 0 */
+} ws_grid_spec;
+
+typedef struct ws_depo {
+    int64_t id;     /* RNG stream key */
+    double t;       /* us */
+    double x;       /* mm */
+    int64_t q;      /* electrons */
+    double sigma_t; /* us */
+    double sigma_x; /* mm */
+} ws_depo;
+
+enum { WS_INDUCTION = 0, WS_COLLECTION = 1 };
+
+typedef struct ws_response {
+    int32_t plane_kind; /* WS_INDUCTION | WS_COLLECTION */
+    int32_t shaper_order;
+    double field_sigma_t;  /* us; 0 = single-bin delta */
+    double shaper_peaking; /* us; 0 = single-sample delta */
+    double gain;           /* output units per electron */
+    const double* wire_weights; /* odd length, centred on lag 0 */
+    uint64_t n_wire_weights;
+} ws_response;
+
+typedef struct ws_drift {
+    int32_t enabled;
+    int32_t reserved;
+    double response_plane_x, drift_speed, diffusion_long, diffusion_tran;
+} ws_drift;
+
+enum { WS_RNG_SUBSTREAM = 0, /* reference xoshiro256** substream(seed, depo.id), rng.cpp:64-76 */
+       WS_RNG_PHILOX = 1 };  /* shared Philox4x32-10 stream keyed by (seed, depo.id) */
+
+typedef struct ws_sim_options {
+    int32_t fluctuate;   /* 0: S = q * p (fp32, fixed-point accumulated); 1: binomial fluctuation */
+    int32_t approx;      /* fluctuation sampler: 0 exact binomial (fluctuate), 1 Gaussian approx (fluctuate_approx) */
+    int32_t rng_mode;    /* WS_RNG_* */
+    int32_t reserved;
+    uint64_t seed;       /* SimConfig::rng.seed */
+    ws_drift drift;      /* SimConfig::drift */
+} ws_sim_options;
+
+typedef struct ws_timing {
+    float prepare_ms;    /* sample: footprints + erf integrals (+ drift) */
+    float fluctuate_ms;  /* fluctuation walk + integer scatter (0 when off) */
+    float bin_ms;        /* depo -> wire-band binning */
+    float convolve_ms;   /* fused accumulate + FFT convolution */
+    float total_ms;      /* device time of the whole call */
+    int32_t reserved;
+    int64_t clipped_patches; /* TimingReport::clipped_patch_count */
+    int64_t clipped_charge;  /* SimResult::clipped_charge */
+} ws_timing;
+
+typedef struct ws_plane_info {
+    uint64_t padded_wires, padded_ticks;
+    uint64_t fft_length;     /* real transform length along ticks (== padded_ticks when circular) */
+    int32_t folded;          /* 1 if the circular wrap is folded from a longer linear transform */
+    int32_t n_radix_passes;
+    int64_t support_ticks, support_wires; /* ResponseKernel::support_* */
+    int64_t lo_lag, n_lags;               /* combined time kernel lags [lo_lag, lo_lag + n_lags) */
+} ws_plane_info;
+
+typedef struct ws_ctx ws_ctx;
+typedef struct ws_plane ws_plane;
+
+const char* ws_last_error(void);
+int ws_abi_version(void);
+
+/* Context: one device, one stream, reusable device workspace. Not thread-safe;
+ * use one context per host thread. `stream` (cudaStream_t) may be NULL to
+ * create a private non-blocking stream. */
+int ws_ctx_create(int device, void* stream, ws_ctx** out);
+int ws_ctx_destroy(ws_ctx* ctx);
+int ws_ctx_synchronize(ws_ctx* ctx);
+void* ws_ctx_stream(ws_ctx* ctx);
+/* Number of CUDA kernels this context has launched so far. */
+uint64_t ws_ctx_launch_count(const ws_ctx* ctx);
+
+/* Plane: geometry + response precomputed on the device (response spectrum,
+ * FFT plan, twiddles). Validation mirrors build_response and convolve. */
+int ws_plane_create(ws_ctx* ctx, const ws_grid_spec* grid, const ws_response* response, double n_sigma,
+                    ws_plane** out);
+int ws_plane_destroy(ws_plane* plane);
+int ws_plane_get_info(const ws_plane* plane, ws_plane_info* info);
+/* Combined time-domain kernel samples (n_lags doubles, lag lo_lag first). */
+int ws_plane_get_kernel(const ws_plane* plane, double* out, uint64_t cap);
+
+/* Charge grid only (raster + scatter), device pointers. charge: padded
+ * float32 frame; with fluctuation the values are exact integers. */
+int ws_rasterize_device(ws_plane* plane, const ws_depo* depos, uint64_t n, const ws_sim_options* opt,
+                        float* charge, ws_timing* timing);
+/* Convolution of an existing charge grid (float32, padded) into a frame. */
+int ws_convolve_device(ws_plane* plane, const float* charge, float* frame);
+
+/* raster -> scatter -> convolve for one plane, device pointers, asynchronous.
+ * charge (nullable) additionally receives the charge grid. timing (nullable)
+ * is filled at the next ws_ctx_synchronize. */
+int ws_simulate_plane_device(ws_plane* plane, const ws_depo* depos, uint64_t n, const ws_sim_options* opt,
+                             float* frame, float* charge, ws_timing* timing);
+
+/* Host-buffer drop-in for run_simulation's hot section: depos and frame in
+ * host memory (pinned recommended), synchronous. */
+int ws_simulate_plane(ws_plane* plane, const ws_depo* depos, uint64_t n, const ws_sim_options* opt, float* frame,
+                      float* charge, ws_timing* timing);
+
+/* Several independent planes (e.g. U, V, W of one event) in one batch of
+ * launches. Arrays have n_planes entries; all planes must share the context. */
+int ws_simulate_event_device(ws_ctx* ctx, uint32_t n_planes, ws_plane* const* planes, const ws_depo* const* depos,
+                             const uint64_t* n_depos, const ws_sim_options* opt, float* const* frames,
+                             ws_timing* timing);
+int ws_simulate_event(ws_ctx* ctx, uint32_t n_planes, ws_plane* const* planes, const ws_depo* const* depos,
+                      const uint64_t* n_depos, const ws_sim_options* opt, float* const* frames, ws_timing* timing);
+
+/* Pinned host memory for the host-buffer entry points (cudaMallocHost). */
+int ws_host_alloc(uint64_t bytes, void** out);
+int ws_host_free(void* p);
+
+/* Synthetic depos placed uniformly inside the active grid, the reference's
+ * gen_depos (pipeline.cpp:264-294, DepoGenRanges defaults pipeline.hpp:83-87)
+ * without the CSV round trip (its %.17g text is exact). ranges6 = {q_min,
+ * q_max, sigma_t_min, sigma_t_max, sigma_x_min, sigma_x_max} or NULL. */
+int ws_gen_depos_uniform(uint64_t n, uint64_t seed, const ws_grid_spec* grid, const double* ranges6, ws_depo* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WIRESIM_GPU_H */

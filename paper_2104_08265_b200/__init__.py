@@ -1,0 +1,21 @@
+"""B200-native Wire-Cell signal-simulation hot path (arXiv 2104.08265).
+
+rasterize -> scatter-add -> FFT convolution behind the C ABI in
+include/wiresim_gpu.h; this package is the Python mirror of the reference's
+C++ interface (see api.py) plus the synthetic workloads used by bench.py.
+"""
+from ._lib import DEPO_DTYPE, WsError  # noqa: F401
+from .api import (  # noqa: F401
+    Context,
+    DriftParams,
+    GridSpec,
+    Plane,
+    ResponseParams,
+    RngConfig,
+    SimConfig,
+    SimResult,
+    gen_depos,
+    run_simulation,
+    simulate_event,
+    simulate_event_device,
+)

@@ -1,0 +1,263 @@
+"""Host-side mirror of the reference's C++ interface for the hot path.
+
+Types and field names follow /root/reference/proj/include/wiresim:
+``GridSpec`` (core.hpp:40-58), ``ResponseParams`` (spectral.hpp:18-26),
+``DriftParams`` (rasterize.hpp:16-23), ``RngConfig``/``SimConfig``
+(pipeline.hpp:24-50), ``Depo`` arrays (core.hpp:63-70, as a numpy structured
+array with the same 48-byte layout), and ``run_simulation``-shaped entry points
+(pipeline.hpp:104) that stop at the pre-noise frame M = IFT(R . FT(S)) — the
+raster -> scatter -> convolve section this library replaces.
+
+Everything runs through libwsgpu.so (include/wiresim_gpu.h); there is no CPU
+fallback. Errors raise ``WsError`` carrying the reference exception category
+(WS_EINVAL ~ std::invalid_argument, WS_EDOMAIN ~ std::domain_error, ...).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import DEPO_DTYPE, WsError, check
+
+
+@dataclass
+class GridSpec:
+    n_wires: int = 1000
+    n_ticks: int = 6000
+    pad_wires: int = 100
+    pad_ticks: int = 100
+    pitch: float = 5.0
+    tick: float = 0.5
+    origin_x: float = 0.0
+    origin_t: float = 0.0
+
+    def padded_wires(self) -> int:
+        return self.n_wires + 2 * self.pad_wires
+
+    def padded_ticks(self) -> int:
+        return self.n_ticks + 2 * self.pad_ticks
+
+    def to_c(self) -> _lib.GridSpecC:
+        return _lib.GridSpecC(self.n_wires, self.n_ticks, self.pad_wires, self.pad_ticks, self.pitch, self.tick,
+                              self.origin_x, self.origin_t)
+
+
+@dataclass
+class ResponseParams:
+    plane_kind: str = "collection"  # "induction" | "collection"
+    field_sigma_t: float = 1.0
+    shaper_peaking: float = 2.0
+    shaper_order: int = 2
+    gain: float = 14.0
+    wire_weights: Sequence[float] = (1.0,)
+
+    def to_c(self):
+        ww = np.ascontiguousarray(np.asarray(self.wire_weights, dtype=np.float64))
+        r = _lib.ResponseC(_lib.WS_COLLECTION if self.plane_kind == "collection" else _lib.WS_INDUCTION,
+                           self.shaper_order, self.field_sigma_t, self.shaper_peaking, self.gain,
+                           ww.ctypes.data_as(C.POINTER(C.c_double)), ww.size)
+        return r, ww
+
+
+@dataclass
+class DriftParams:
+    response_plane_x: float = 0.0
+    drift_speed: float = 1.6
+    diffusion_long: float = 0.0068
+    diffusion_tran: float = 0.0088
+    enabled: bool = False
+
+
+@dataclass
+class RngConfig:
+    mode: str = "substream"  # "substream" (reference xoshiro) | "philox" (shared counter stream)
+    seed: int = 12345
+
+
+@dataclass
+class SimConfig:
+    grid: GridSpec = field(default_factory=GridSpec)
+    drift: DriftParams = field(default_factory=DriftParams)
+    response: ResponseParams = field(default_factory=ResponseParams)
+    n_sigma: float = 3.0
+    rng: RngConfig = field(default_factory=RngConfig)
+    fluctuate: bool = True       # the reference always fluctuates (rasterize.cpp:182-202)
+    approx: bool = False         # fluctuate_approx sampler (rasterize.cpp:159-170)
+
+    def options(self) -> _lib.SimOptionsC:
+        d = self.drift
+        return _lib.SimOptionsC(
+            int(self.fluctuate), int(self.approx),
+            _lib.WS_RNG_PHILOX if self.rng.mode == "philox" else _lib.WS_RNG_SUBSTREAM, 0, self.rng.seed,
+            _lib.DriftC(int(d.enabled), 0, d.response_plane_x, d.drift_speed, d.diffusion_long, d.diffusion_tran))
+
+
+def as_depos(depos) -> np.ndarray:
+    a = np.ascontiguousarray(depos)
+    if a.dtype != DEPO_DTYPE:
+        a = np.ascontiguousarray(a.astype(DEPO_DTYPE))
+    return a
+
+
+class Context:
+    """One device + stream + workspace (ws_ctx)."""
+
+    def __init__(self, device: int = 0, stream: int | None = None):
+        self.lib = _lib.load()
+        h = C.c_void_p()
+        check(self.lib.ws_ctx_create(device, C.c_void_p(stream) if stream else None, C.byref(h)))
+        self.handle = h
+        self.device = device
+
+    def synchronize(self):
+        check(self.lib.ws_ctx_synchronize(self.handle))
+
+    @property
+    def stream(self) -> int:
+        return self.lib.ws_ctx_stream(self.handle) or 0
+
+    @property
+    def launch_count(self) -> int:
+        return int(self.lib.ws_ctx_launch_count(self.handle))
+
+    def close(self):
+        if self.handle:
+            self.lib.ws_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Plane:
+    """Geometry + response, precomputed on the device (ws_plane)."""
+
+    def __init__(self, ctx: Context, grid: GridSpec, response: ResponseParams, n_sigma: float = 3.0):
+        self.ctx, self.grid, self.response, self.n_sigma = ctx, grid, response, n_sigma
+        self.lib = ctx.lib
+        r, self._ww = response.to_c()
+        g = grid.to_c()
+        h = C.c_void_p()
+        check(self.lib.ws_plane_create(ctx.handle, C.byref(g), C.byref(r), n_sigma, C.byref(h)))
+        self.handle = h
+        info = _lib.PlaneInfoC()
+        check(self.lib.ws_plane_get_info(h, C.byref(info)))
+        self.info = {k: getattr(info, k) for k, _ in info._fields_}
+        self.shape = (int(info.padded_wires), int(info.padded_ticks))
+
+    def kernel(self) -> np.ndarray:
+        k = np.zeros(int(self.info["n_lags"]), dtype=np.float64)
+        check(self.lib.ws_plane_get_kernel(self.handle, k.ctypes.data, k.size))
+        return k
+
+    # ---- host-buffer entry points (synchronous)
+    def simulate(self, depos, config: SimConfig, want_charge: bool = False, frame_out: np.ndarray | None = None):
+        d = as_depos(depos)
+        frame = frame_out if frame_out is not None else np.empty(self.shape, dtype=np.float32)
+        charge = np.empty(self.shape, dtype=np.float32) if want_charge else None
+        t = _lib.TimingC()
+        opt = config.options()
+        check(self.lib.ws_simulate_plane(self.handle, d.ctypes.data, len(d), C.byref(opt), frame.ctypes.data,
+                                         charge.ctypes.data if charge is not None else None, C.byref(t)))
+        return SimResult(frame=frame, charge=charge, timing=t.as_dict())
+
+    # ---- device entry points (torch tensors; asynchronous on the context stream)
+    def simulate_device(self, depos_dev, n: int, config: SimConfig, frame_dev, charge_dev=None, timing=None):
+        opt = config.options()
+        check(self.lib.ws_simulate_plane_device(self.handle, _ptr(depos_dev), n, C.byref(opt), _ptr(frame_dev),
+                                                _ptr(charge_dev), C.byref(timing) if timing is not None else None))
+
+    def rasterize_device(self, depos_dev, n: int, config: SimConfig, charge_dev, timing=None):
+        opt = config.options()
+        check(self.lib.ws_rasterize_device(self.handle, _ptr(depos_dev), n, C.byref(opt), _ptr(charge_dev),
+                                           C.byref(timing) if timing is not None else None))
+
+    def convolve_device(self, charge_dev, frame_dev):
+        check(self.lib.ws_convolve_device(self.handle, _ptr(charge_dev), _ptr(frame_dev)))
+
+    def close(self):
+        if self.handle:
+            self.lib.ws_plane_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _ptr(x):
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return C.c_void_p(x)
+    if hasattr(x, "data_ptr"):
+        return C.c_void_p(x.data_ptr())
+    if isinstance(x, np.ndarray):
+        return C.c_void_p(x.ctypes.data)
+    raise TypeError(f"cannot take a pointer of {type(x)}")
+
+
+@dataclass
+class SimResult:
+    frame: np.ndarray            # pre-noise measurement M (float32, padded)
+    charge: np.ndarray | None    # charge grid S (float32, padded)
+    timing: dict
+
+
+def simulate_event(ctx: Context, planes: Sequence[Plane], depos: Sequence, config: SimConfig,
+                   frames: Sequence[np.ndarray] | None = None):
+    """Independent planes of one event through one batch of launches (host buffers)."""
+    n = len(planes)
+    ds = [as_depos(d) for d in depos]
+    frames = list(frames) if frames is not None else [np.empty(p.shape, dtype=np.float32) for p in planes]
+    PArr = C.c_void_p * n
+    parr = PArr(*[p.handle.value for p in planes])
+    darr = PArr(*[d.ctypes.data for d in ds])
+    narr = (C.c_uint64 * n)(*[len(d) for d in ds])
+    farr = PArr(*[f.ctypes.data for f in frames])
+    t = _lib.TimingC()
+    opt = config.options()
+    check(ctx.lib.ws_simulate_event(ctx.handle, n, parr, darr, narr, C.byref(opt), farr, C.byref(t)))
+    return frames, t.as_dict()
+
+
+def simulate_event_device(ctx: Context, planes: Sequence[Plane], depos_dev: Sequence, n_depos: Sequence[int],
+                          config: SimConfig, frames_dev: Sequence, timing=None):
+    n = len(planes)
+    PArr = C.c_void_p * n
+    parr = PArr(*[p.handle.value for p in planes])
+    darr = PArr(*[_ptr(d).value for d in depos_dev])
+    narr = (C.c_uint64 * n)(*n_depos)
+    farr = PArr(*[_ptr(f).value for f in frames_dev])
+    opt = config.options()
+    check(ctx.lib.ws_simulate_event_device(ctx.handle, n, parr, darr, narr, C.byref(opt), farr,
+                                           C.byref(timing) if timing is not None else None))
+
+
+def run_simulation(config: SimConfig, depos, device: int = 0, ctx: Context | None = None) -> SimResult:
+    """run_simulation (pipeline.hpp:104) up to the pre-noise frame, on the GPU."""
+    ctx = ctx or Context(device)
+    plane = Plane(ctx, config.grid, config.response, config.n_sigma)
+    try:
+        return plane.simulate(depos, config, want_charge=True)
+    finally:
+        plane.close()
+
+
+def gen_depos(n: int, seed: int, grid: GridSpec, ranges: Sequence[float] | None = None) -> np.ndarray:
+    """The reference's gen_depos (pipeline.cpp:264-294), same xoshiro stream."""
+    lib = _lib.load()
+    out = np.zeros(n, dtype=DEPO_DTYPE)
+    g = grid.to_c()
+    r = None if ranges is None else np.ascontiguousarray(ranges, dtype=np.float64)
+    check(lib.ws_gen_depos_uniform(n, seed, C.byref(g), r.ctypes.data if r is not None else None, out.ctypes.data))
+    return out

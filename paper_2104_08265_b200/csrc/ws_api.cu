@@ -1,0 +1,844 @@
+// C-ABI host layer (include/wiresim_gpu.h): contexts, planes (response
+// spectrum + FFT plan precomputed once per geometry), workspace management and
+// the launch sequence of one event. No exceptions cross the ABI; no CPU
+// fallback exists — every path launches the kernels in ws_sample.cu and
+// ws_conv.cu or fails with WS_ECUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "ws_common.cuh"
+#include "wiresim_gpu.h"
+
+using wsb::EventDesc;
+using wsb::PlaneDesc;
+using wsb::UnitRec;
+
+extern "C" cudaError_t wsb_launch_sample(const EventDesc& ev, UnitRec* recs, uint32_t* pool, uint32_t pool_cap,
+                                         uint32_t* pool_ctr, uint32_t* band_count, unsigned* err, cudaStream_t s);
+extern "C" cudaError_t wsb_launch_scan(const uint32_t* count, uint32_t* off, uint32_t* fill, uint32_t n,
+                                       cudaStream_t s);
+extern "C" cudaError_t wsb_launch_fill(const EventDesc& ev, const UnitRec* recs, const uint32_t* off, uint32_t* fill,
+                                       uint32_t* list, cudaStream_t s);
+extern "C" cudaError_t wsb_launch_fluctuate(const EventDesc& ev, const UnitRec* recs, const uint32_t* pool,
+                                            const uint32_t* order, cudaStream_t s);
+extern "C" cudaError_t wsb_launch_conv(const EventDesc& ev, const UnitRec* recs, const uint32_t* pool,
+                                       const uint32_t* band_off, const uint32_t* band_list, int flags,
+                                       size_t smem_bytes, cudaStream_t stream);
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const char* fmt, ...)
+{
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define WS_CUDA(call)                                                                            \
+    do {                                                                                         \
+        const cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess)                                                                   \
+            return set_err(WS_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
+                           __LINE__);                                                            \
+    } while (0)
+
+constexpr double kTwoPi = 6.283185307179586476925286766559;
+constexpr double kInvSqrt2 = 0.70710678118654752440084436210485;
+constexpr int kStatSlots = 64;
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t cap = 0;  // elements
+    cudaError_t reserve(size_t n)
+    {
+        if (n <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        const size_t want = std::max<size_t>(n, 1);
+        cudaError_t e = cudaMalloc(&p, want * sizeof(T));
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    void release()
+    {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+}  // namespace
+
+// per-call device scratch header: [pool_ctr, err, pad, pad] u32 + stats i64[2*kMaxPlanes]
+struct ScratchHeader {
+    uint32_t pool_ctr;
+    uint32_t err;
+    uint32_t pad[2];
+    long long stats[2 * wsb::kMaxPlanes];
+};
+
+struct PendingCall {
+    ws_timing* timing;
+    int slot;
+    int n_planes;
+    cudaEvent_t ev[6];
+    int fluctuate;
+};
+
+struct ws_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    uint64_t launches = 0;
+    DevBuf<UnitRec> recs;
+    DevBuf<uint32_t> pool;
+    DevBuf<uint32_t> band_count, band_off, band_fill, band_list;
+    DevBuf<ScratchHeader> header;
+    DevBuf<ws_depo> depos;
+    DevBuf<float> frames, charges;
+    ScratchHeader* host_slots = nullptr;  // pinned, kStatSlots
+    int next_slot = 0;
+    std::vector<PendingCall> pending;
+    std::vector<cudaEvent_t> event_pool;
+    size_t pool_hint = 0;
+    int sm_count = 0;
+};
+
+struct ws_plane {
+    ws_ctx* ctx = nullptr;
+    ws_grid_spec grid{};
+    double n_sigma = 3.0;
+    int W = 0, N = 0, Np = 0, M = 0, folded = 0, h = 0;
+    long lo_lag = 0, n_lags = 0, support_ticks = 0, support_wires = 0;
+    std::vector<double> kernel;  // combined time-domain kernel
+    std::vector<int> radix;
+    double* d_ww = nullptr;
+    float2* d_H = nullptr;
+    float2* d_tw = nullptr;
+    float2* d_rtw = nullptr;
+    int ww_is_one = 0;
+    int rows_per_band = 4;
+    int n_bands = 0;
+    size_t smem = 0;
+};
+
+namespace {
+
+cudaEvent_t take_event(ws_ctx* c)
+{
+    if (!c->event_pool.empty()) {
+        cudaEvent_t e = c->event_pool.back();
+        c->event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// ---------------------------------------------------------------- response --
+// Host restatement of the response builder's time-domain kernel
+// (spectral.cpp:34-83 field/shaper samples, :98-113 combination and supports),
+// with the same validation (:89-92, :117-121). The frequency-domain values are
+// produced below for the row transform instead of a 2D fft_2d (:137).
+
+double gauss_pdf(double t, double sigma)
+{
+    const double z = t / sigma;
+    return std::exp(-0.5 * z * z) / (sigma * std::sqrt(kTwoPi));
+}
+
+void bin_integrals(double center, double sigma, double lo_edge, double spacing, size_t n, double* vals)
+{
+    for (size_t i = 0; i < n; ++i) vals[i] = 0.0;
+    if (n == 0) return;
+    if (sigma <= 0.0) {
+        long idx = (long)std::floor((center - lo_edge) / spacing);
+        idx = std::clamp<long>(idx, 0, (long)n - 1);
+        vals[idx] = 1.0;
+        return;
+    }
+    const double inv = kInvSqrt2 / sigma;
+    double prev = std::erf((lo_edge - center) * inv);
+    for (size_t i = 0; i < n; ++i) {
+        const double next = std::erf((lo_edge + (double)(i + 1) * spacing - center) * inv);
+        vals[i] = 0.5 * (next - prev);
+        prev = next;
+    }
+}
+
+int build_kernel(const ws_grid_spec& g, const ws_response& r, std::vector<double>& combined, long& lo_lag,
+                 long& support_ticks, long& support_wires)
+{
+    if (r.shaper_order < 1) return set_err(WS_EINVAL, "build_response: shaper_order must be >= 1");
+    if (!r.wire_weights || r.n_wire_weights == 0 || r.n_wire_weights % 2 == 0)
+        return set_err(WS_EINVAL, "build_response: wire_weights must have odd length");
+    const double tick = g.tick;
+    std::vector<double> f;
+    long half = 0;
+    if (r.field_sigma_t <= 0.0) {
+        f = {1.0};
+    } else {
+        const double sigma = r.field_sigma_t;
+        half = (long)std::ceil(8.0 * sigma / tick);
+        const size_t n = (size_t)(2 * half + 1);
+        f.assign(n, 0.0);
+        if (r.plane_kind == WS_COLLECTION) {
+            bin_integrals(0.0, sigma, (-(double)half - 0.5) * tick, tick, n, f.data());
+            double sum = 0.0;
+            for (double v : f) sum += v;
+            for (double& v : f) v /= sum;
+        } else {
+            double pos = 0.0;
+            for (size_t i = 0; i < n; ++i) {
+                const double lo = ((double)i - (double)half - 0.5) * tick;
+                f[i] = gauss_pdf(lo + tick, sigma) - gauss_pdf(lo, sigma);
+                if (f[i] > 0.0) pos += f[i];
+            }
+            for (double& v : f) v /= pos;
+        }
+    }
+    std::vector<double> s;
+    if (r.shaper_peaking <= 0.0) {
+        s = {1.0};
+    } else {
+        const double tau = r.shaper_peaking;
+        const int order = r.shaper_order;
+        for (long k = 0;; ++k) {
+            const double t = (double)k * tick;
+            const double z = t / tau;
+            const double v = std::pow(z, order) * std::exp(-(double)order * (z - 1.0));
+            s.push_back(v);
+            if (t > tau && v < 1e-14) break;
+            if (k > 2000000) return set_err(WS_ERUNTIME, "build_response: shaper tail does not decay");
+        }
+    }
+    double shaper_sum = 0.0;
+    for (double v : s) shaper_sum += v;
+    const double amplitude = r.gain / shaper_sum;
+    const size_t n_lags = f.size() + s.size() - 1;
+    combined.assign(n_lags, 0.0);
+    for (size_t i = 0; i < f.size(); ++i)
+        for (size_t j = 0; j < s.size(); ++j) combined[i + j] += f[i] * s[j] * amplitude;
+    lo_lag = -half;
+    support_ticks = std::max<long>(-lo_lag, lo_lag + (long)n_lags - 1);
+    support_wires = (long)(r.n_wire_weights / 2);
+    const uint64_t W = g.n_wires + 2 * g.pad_wires, N = g.n_ticks + 2 * g.pad_ticks;
+    if (n_lags > N)
+        return set_err(WS_EINVAL, "build_response: kernel time support %zu exceeds the padded tick count %llu", n_lags,
+                       (unsigned long long)N);
+    if (r.n_wire_weights > W) return set_err(WS_EINVAL, "build_response: wire_weights exceed the padded wire count");
+    return WS_OK;
+}
+
+bool smooth7(long n)
+{
+    if (n < 1) return false;
+    for (long p : {2L, 3L, 5L, 7L})
+        while (n % p == 0) n /= p;
+    return n == 1;
+}
+
+std::vector<int> plan_radices(int m)
+{
+    std::vector<int> r;
+    while (m % 8 == 0) { r.push_back(8); m /= 8; }
+    while (m % 4 == 0) { r.push_back(4); m /= 4; }
+    while (m % 2 == 0) { r.push_back(2); m /= 2; }
+    while (m % 7 == 0) { r.push_back(7); m /= 7; }
+    while (m % 5 == 0) { r.push_back(5); m /= 5; }
+    while (m % 3 == 0) { r.push_back(3); m /= 3; }
+    return r;
+}
+
+int validate_grid(const ws_grid_spec* g)
+{
+    if (!g) return set_err(WS_EINVAL, "GridSpec: null");
+    if (g->n_wires < 1 || g->n_ticks < 1) return set_err(WS_EINVAL, "GridSpec: active grid must be at least 1x1");
+    if (!(g->pitch > 0.0)) return set_err(WS_EINVAL, "GridSpec: pitch must be > 0");
+    if (!(g->tick > 0.0)) return set_err(WS_EINVAL, "GridSpec: tick must be > 0");
+    const uint64_t W = g->n_wires + 2 * g->pad_wires, N = g->n_ticks + 2 * g->pad_ticks;
+    if (W > (1u << 30) || N > (1u << 30)) return set_err(WS_EINVAL, "GridSpec: padded grid too large");
+    return WS_OK;
+}
+
+PlaneDesc plane_desc(const ws_plane* p)
+{
+    PlaneDesc d{};
+    d.W = p->W;
+    d.N = p->N;
+    d.pad_w = (int)p->grid.pad_wires;
+    d.pad_t = (int)p->grid.pad_ticks;
+    d.pitch = p->grid.pitch;
+    d.tick = p->grid.tick;
+    d.origin_x = p->grid.origin_x;
+    d.origin_t = p->grid.origin_t;
+    d.n_sigma = p->n_sigma;
+    d.h = p->h;
+    d.ww_is_one = p->ww_is_one;
+    d.folded = p->folded;
+    d.Np = p->Np;
+    d.M = p->M;
+    d.lo_lag = (int)p->lo_lag;
+    d.hi_lag = (int)(p->lo_lag + p->n_lags - 1);
+    d.npass = (int)p->radix.size();
+    for (size_t i = 0; i < p->radix.size(); ++i) d.radix[i] = p->radix[i];
+    d.ww = p->d_ww;
+    d.H = p->d_H;
+    d.tw = p->d_tw;
+    d.rtw = p->d_rtw;
+    d.rows_per_band = p->rows_per_band;
+    d.n_bands = p->n_bands;
+    return d;
+}
+
+int check_opts(const ws_sim_options* o)
+{
+    if (!o) return set_err(WS_EINVAL, "options: null");
+    if (o->rng_mode != WS_RNG_SUBSTREAM && o->rng_mode != WS_RNG_PHILOX)
+        return set_err(WS_EINVAL, "options: unknown rng mode %d", o->rng_mode);
+    if (o->drift.enabled && !(o->drift.drift_speed > 0.0))
+        return set_err(WS_EINVAL, "drift_depo: drift_speed must be > 0");
+    return WS_OK;
+}
+
+// Launch one group of <= kMaxPlanes planes. frames/charges are device
+// pointers (frames[i] may be null when only charge is wanted).
+int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* const* depos, const uint64_t* n_depos,
+              const ws_sim_options* opt, float* const* frames, float* const* charges, const float* const* charge_in,
+              ws_timing* timing)
+{
+    cudaStream_t s = c->stream;
+    EventDesc ev{};
+    ev.n_planes = (int)n;
+    ev.fluctuate = opt ? opt->fluctuate : 0;
+    ev.approx = opt ? opt->approx : 0;
+    ev.rng_mode = opt ? opt->rng_mode : 0;
+    ev.seed = opt ? opt->seed : 0;
+    ev.drift_enabled = opt ? opt->drift.enabled : 0;
+    if (ev.drift_enabled) {
+        ev.drift_plane_x = opt->drift.response_plane_x;
+        ev.drift_speed = opt->drift.drift_speed;
+        ev.drift_dl = opt->drift.diffusion_long;
+        ev.drift_dt = opt->drift.diffusion_tran;
+    }
+    const bool from_grid = charge_in != nullptr;
+    ev.mode = (from_grid || ev.fluctuate) ? 1 : 0;
+    uint32_t units = 0, bands = 0;
+    int need_raw = 0;
+    size_t smem = 0;
+    bool want_frame = false;
+    for (uint32_t i = 0; i < n; ++i) {
+        ws_plane* p = planes[i];
+        PlaneDesc d = plane_desc(p);
+        d.depos = depos ? depos[i] : nullptr;
+        d.n_units = depos ? (uint32_t)n_depos[i] : 0u;
+        d.unit_base = units;
+        d.band_base = bands;
+        d.frame = frames ? frames[i] : nullptr;
+        d.charge_out = charges ? charges[i] : nullptr;
+        d.charge_in = from_grid ? charge_in[i] : (ev.fluctuate ? charges[i] : nullptr);
+        d.stats = nullptr;
+        ev.p[i] = d;
+        units += d.n_units;
+        bands += (uint32_t)p->n_bands;
+        need_raw = need_raw || !p->ww_is_one;
+        smem = std::max(smem, p->smem);
+        want_frame = want_frame || d.frame != nullptr;
+    }
+    ev.total_units = units;
+    ev.total_bands = bands;
+
+    // workspace
+    const size_t pool_need = std::max<size_t>(c->pool_hint, (size_t)units * 96 + 4096);
+    WS_CUDA(c->recs.reserve(units));
+    WS_CUDA(c->pool.reserve(pool_need));
+    WS_CUDA(c->band_count.reserve(bands + 1));
+    WS_CUDA(c->band_off.reserve(bands + 1));
+    WS_CUDA(c->band_fill.reserve(bands + 1));
+    int max_h = 0;
+    for (uint32_t i = 0; i < n; ++i) max_h = std::max(max_h, planes[i]->h);
+    WS_CUDA(c->band_list.reserve(c->pool.cap + (size_t)units * (2 * max_h + 2) + 16));
+    WS_CUDA(c->header.reserve(1));
+    ScratchHeader* hdr = c->header.p;
+    for (uint32_t i = 0; i < n; ++i) ev.p[i].stats = &hdr->stats[2 * i];
+
+    PendingCall pc{};
+    pc.timing = timing;
+    pc.n_planes = (int)n;
+    pc.fluctuate = ev.fluctuate;
+    for (int k = 0; k < 6; ++k) pc.ev[k] = take_event(c);
+
+    WS_CUDA(cudaEventRecord(pc.ev[0], s));
+    WS_CUDA(cudaMemsetAsync(hdr, 0, sizeof(ScratchHeader), s));
+    if (ev.mode == 0) WS_CUDA(cudaMemsetAsync(c->band_count.p, 0, sizeof(uint32_t) * (bands + 1), s));
+    if (ev.fluctuate && !from_grid)
+        for (uint32_t i = 0; i < n; ++i)
+            WS_CUDA(cudaMemsetAsync(ev.p[i].charge_out, 0, sizeof(float) * (size_t)ev.p[i].W * ev.p[i].N, s));
+    if (!from_grid) {
+        WS_CUDA(wsb_launch_sample(ev, c->recs.p, c->pool.p, (uint32_t)std::min<size_t>(c->pool.cap, 0xffffffffu),
+                                  &hdr->pool_ctr, c->band_count.p, &hdr->err, s));
+        c->launches += units ? 1 : 0;
+    }
+    WS_CUDA(cudaEventRecord(pc.ev[1], s));
+    if (ev.fluctuate && !from_grid) {
+        WS_CUDA(wsb_launch_fluctuate(ev, c->recs.p, c->pool.p, nullptr, s));
+        c->launches += units ? 1 : 0;
+    }
+    WS_CUDA(cudaEventRecord(pc.ev[2], s));
+    if (ev.mode == 0) {
+        WS_CUDA(wsb_launch_scan(c->band_count.p, c->band_off.p, c->band_fill.p, bands, s));
+        WS_CUDA(wsb_launch_fill(ev, c->recs.p, c->band_off.p, c->band_fill.p, c->band_list.p, s));
+        c->launches += 1 + (units ? 1 : 0);
+    }
+    WS_CUDA(cudaEventRecord(pc.ev[3], s));
+    if (ev.mode == 0 && charges && need_raw) {
+        // the charge grid is the un-stencilled S: one extra accumulate-only pass
+        WS_CUDA(wsb_launch_conv(ev, c->recs.p, c->pool.p, c->band_off.p, c->band_list.p, 2, smem, s));
+        c->launches += bands ? 1 : 0;
+    }
+    if (want_frame || (ev.mode == 0 && charges && !need_raw)) {
+        WS_CUDA(wsb_launch_conv(ev, c->recs.p, c->pool.p, c->band_off.p, c->band_list.p, want_frame ? 1 : 0, smem, s));
+        c->launches += bands ? 1 : 0;
+    }
+    WS_CUDA(cudaEventRecord(pc.ev[4], s));
+    // per-call copy of the header into a pinned slot, read at synchronize
+    if ((int)c->pending.size() >= kStatSlots) {
+        // too many calls in flight: drain
+        WS_CUDA(cudaStreamSynchronize(s));
+    }
+    pc.slot = c->next_slot;
+    c->next_slot = (c->next_slot + 1) % kStatSlots;
+    WS_CUDA(cudaMemcpyAsync(&c->host_slots[pc.slot], hdr, sizeof(ScratchHeader), cudaMemcpyDeviceToHost, s));
+    WS_CUDA(cudaEventRecord(pc.ev[5], s));
+    c->pending.push_back(pc);
+    return WS_OK;
+}
+
+int finish_pending(ws_ctx* c)
+{
+    WS_CUDA(cudaStreamSynchronize(c->stream));
+    int rc = WS_OK;
+    for (PendingCall& pc : c->pending) {
+        const ScratchHeader& h = c->host_slots[pc.slot];
+        if (rc == WS_OK) {
+            if (h.err & wsb::kErrDomain) rc = set_err(WS_EDOMAIN, "drift_depo: a depo is behind the response plane");
+            else if (h.err & wsb::kErrCharge) rc = set_err(WS_EINVAL, "fluctuate: charge must be >= 0");
+            else if (h.err & wsb::kErrPool) {
+                c->pool_hint = std::max<size_t>(c->pool.cap * 2, (size_t)h.pool_ctr + 4096);
+                rc = set_err(WS_ERANGE, "workspace: patch pool overflow (%u doubles needed); grown, re-run the call",
+                             h.pool_ctr);
+            }
+        }
+        if (pc.timing) {
+            ws_timing& t = *pc.timing;
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, pc.ev[0], pc.ev[1]);
+            t.prepare_ms = ms;
+            cudaEventElapsedTime(&ms, pc.ev[1], pc.ev[2]);
+            t.fluctuate_ms = ms;
+            cudaEventElapsedTime(&ms, pc.ev[2], pc.ev[3]);
+            t.bin_ms = ms;
+            cudaEventElapsedTime(&ms, pc.ev[3], pc.ev[4]);
+            t.convolve_ms = ms;
+            cudaEventElapsedTime(&ms, pc.ev[0], pc.ev[4]);
+            t.total_ms = ms;
+            t.clipped_charge = 0;
+            t.clipped_patches = 0;
+            for (int i = 0; i < pc.n_planes; ++i) {
+                t.clipped_charge += h.stats[2 * i];
+                t.clipped_patches += h.stats[2 * i + 1];
+            }
+        }
+        for (int k = 0; k < 6; ++k) c->event_pool.push_back(pc.ev[k]);
+    }
+    c->pending.clear();
+    return rc;
+}
+
+int check_plane_set(ws_ctx* ctx, uint32_t n, ws_plane* const* planes)
+{
+    if (!ctx) return set_err(WS_EINVAL, "null context");
+    if (n == 0) return WS_OK;
+    if (!planes) return set_err(WS_EINVAL, "null plane array");
+    for (uint32_t i = 0; i < n; ++i)
+        if (!planes[i] || planes[i]->ctx != ctx) return set_err(WS_EINVAL, "plane %u does not belong to the context", i);
+    return WS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ws_last_error(void) { return g_err.c_str(); }
+int ws_set_error_message(int code, const char* msg) { return set_err(code, "%s", msg); }
+int ws_abi_version(void) { return WS_ABI_VERSION; }
+
+int ws_ctx_create(int device, void* stream, ws_ctx** out)
+{
+    if (!out) return set_err(WS_EINVAL, "null out pointer");
+    *out = nullptr;
+    int n = 0;
+    WS_CUDA(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) return set_err(WS_ECUDA, "device %d not present (%d devices)", device, n);
+    cudaDeviceProp prop{};
+    WS_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) return set_err(WS_ECUDA, "device %d is sm_%d%d; this build targets sm_100a", device, prop.major, prop.minor);
+    WS_CUDA(cudaSetDevice(device));
+    ws_ctx* c = new ws_ctx();
+    c->device = device;
+    c->sm_count = prop.multiProcessorCount;
+    if (stream) {
+        c->stream = (cudaStream_t)stream;
+    } else {
+        cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) {
+            delete c;
+            return set_err(WS_ECUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
+        }
+        c->own_stream = true;
+    }
+    cudaError_t e = cudaMallocHost(&c->host_slots, sizeof(ScratchHeader) * kStatSlots);
+    if (e != cudaSuccess) {
+        delete c;
+        return set_err(WS_ECUDA, "cudaMallocHost: %s", cudaGetErrorString(e));
+    }
+    *out = c;
+    return WS_OK;
+}
+
+int ws_ctx_destroy(ws_ctx* c)
+{
+    if (!c) return WS_OK;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    c->recs.release();
+    c->pool.release();
+    c->band_count.release();
+    c->band_off.release();
+    c->band_fill.release();
+    c->band_list.release();
+    c->header.release();
+    c->depos.release();
+    c->frames.release();
+    c->charges.release();
+    for (PendingCall& pc : c->pending)
+        for (cudaEvent_t e : pc.ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
+    if (c->host_slots) cudaFreeHost(c->host_slots);
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return WS_OK;
+}
+
+int ws_ctx_synchronize(ws_ctx* c)
+{
+    if (!c) return set_err(WS_EINVAL, "null context");
+    WS_CUDA(cudaSetDevice(c->device));
+    return finish_pending(c);
+}
+
+void* ws_ctx_stream(ws_ctx* c) { return c ? (void*)c->stream : nullptr; }
+uint64_t ws_ctx_launch_count(const ws_ctx* c) { return c ? c->launches : 0; }
+
+int ws_plane_create(ws_ctx* ctx, const ws_grid_spec* grid, const ws_response* response, double n_sigma, ws_plane** out)
+{
+    if (!ctx || !out || !response) return set_err(WS_EINVAL, "null argument");
+    *out = nullptr;
+    if (int rc = validate_grid(grid)) return rc;
+    if (!(n_sigma > 0.0)) return set_err(WS_EINVAL, "map_depo_to_grid: n_sigma must be > 0");
+    WS_CUDA(cudaSetDevice(ctx->device));
+    ws_plane* p = new ws_plane();
+    p->ctx = ctx;
+    p->grid = *grid;
+    p->n_sigma = n_sigma;
+    p->W = (int)(grid->n_wires + 2 * grid->pad_wires);
+    p->N = (int)(grid->n_ticks + 2 * grid->pad_ticks);
+    if (int rc = build_kernel(*grid, *response, p->kernel, p->lo_lag, p->support_ticks, p->support_wires)) {
+        delete p;
+        return rc;
+    }
+    p->n_lags = (long)p->kernel.size();
+    // convolve's wrap check (spectral.cpp:147-153)
+    if (p->support_ticks > (long)grid->pad_ticks || p->support_wires > (long)grid->pad_wires) {
+        const int rc = set_err(WS_EINVAL,
+                               "convolve: kernel support (%ld wires, %ld ticks) exceeds the padding; pad_wires >= %ld "
+                               "and pad_ticks >= %ld required",
+                               p->support_wires, p->support_ticks, p->support_wires, p->support_ticks);
+        delete p;
+        return rc;
+    }
+    if ((int)response->n_wire_weights > wsb::kMaxWireWeights) {
+        delete p;
+        return set_err(WS_EINVAL, "wire_weights: at most %d taps supported", wsb::kMaxWireWeights);
+    }
+    p->h = (int)(response->n_wire_weights / 2);
+    p->ww_is_one = (response->n_wire_weights == 1 && response->wire_weights[0] == 1.0) ? 1 : 0;
+    // transform length: the padded tick count itself when it is even and
+    // 7-smooth (exact circular convolution), else the smallest even 7-smooth
+    // length holding the linear convolution, whose tails are folded back
+    // (same circular result).
+    if (p->N % 2 == 0 && smooth7(p->N)) {
+        p->Np = p->N;
+        p->folded = 0;
+    } else {
+        long L = p->N + p->n_lags - 1;
+        if (L % 2) ++L;
+        while (!smooth7(L)) L += 2;
+        p->Np = (int)L;
+        p->folded = 1;
+    }
+    p->M = p->Np / 2;
+    if (p->M > wsb::kMaxFftHalf) {
+        delete p;
+        return set_err(WS_EINVAL, "padded_ticks %d needs a %d-point transform; at most %d supported", p->N, p->Np,
+                       2 * wsb::kMaxFftHalf);
+    }
+    p->radix = plan_radices(p->M);
+    if ((int)p->radix.size() > wsb::kMaxPasses) {
+        delete p;
+        return set_err(WS_EINVAL, "transform plan too deep");
+    }
+    // response spectrum H[k] = (1/M) sum_lag c_lag exp(-2 pi i k lag / Np), k <= M
+    const int Np = p->Np, M = p->M;
+    std::vector<double> cs(Np), sn(Np);
+    for (int m = 0; m < Np; ++m) {
+        const double a = -kTwoPi * (double)m / (double)Np;
+        cs[m] = std::cos(a);
+        sn[m] = std::sin(a);
+    }
+    std::vector<float2> H(M + 1), tw(M), rtw(M / 2 + 1);
+    for (int k = 0; k <= M; ++k) {
+        double re = 0.0, im = 0.0;
+        for (long i = 0; i < p->n_lags; ++i) {
+            long lag = (p->lo_lag + i) % Np;
+            if (lag < 0) lag += Np;
+            const long idx = (long)(((long long)k * lag) % Np);
+            re += p->kernel[i] * cs[idx];
+            im += p->kernel[i] * sn[idx];
+        }
+        H[k] = make_float2((float)(re / M), (float)(im / M));
+    }
+    for (int m = 0; m < M; ++m) tw[m] = make_float2((float)cs[2 * m], (float)sn[2 * m]);
+    for (int k = 0; k <= M / 2; ++k) rtw[k] = make_float2((float)cs[k], (float)sn[k]);
+    std::vector<double> ww(response->wire_weights, response->wire_weights + response->n_wire_weights);
+    cudaError_t e = cudaSuccess;
+    e = e ? e : cudaMalloc(&p->d_H, sizeof(float2) * (M + 1));
+    e = e ? e : cudaMalloc(&p->d_tw, sizeof(float2) * M);
+    e = e ? e : cudaMalloc(&p->d_rtw, sizeof(float2) * (M / 2 + 1));
+    e = e ? e : cudaMalloc(&p->d_ww, sizeof(double) * ww.size());
+    e = e ? e : cudaMemcpy(p->d_H, H.data(), sizeof(float2) * (M + 1), cudaMemcpyHostToDevice);
+    e = e ? e : cudaMemcpy(p->d_tw, tw.data(), sizeof(float2) * M, cudaMemcpyHostToDevice);
+    e = e ? e : cudaMemcpy(p->d_rtw, rtw.data(), sizeof(float2) * (M / 2 + 1), cudaMemcpyHostToDevice);
+    e = e ? e : cudaMemcpy(p->d_ww, ww.data(), sizeof(double) * ww.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        ws_plane_destroy(p);
+        return set_err(WS_ECUDA, "plane upload: %s", cudaGetErrorString(e));
+    }
+    p->n_bands = (p->W + p->rows_per_band - 1) / p->rows_per_band;
+    p->smem = (size_t)8 * (size_t)std::max(p->N, p->Np);
+    if (p->smem > 227 * 1024) {
+        ws_plane_destroy(p);
+        return set_err(WS_EINVAL, "padded_ticks too large for the shared-memory row transform");
+    }
+    *out = p;
+    return WS_OK;
+}
+
+int ws_plane_destroy(ws_plane* p)
+{
+    if (!p) return WS_OK;
+    if (p->ctx) cudaSetDevice(p->ctx->device);
+    if (p->d_H) cudaFree(p->d_H);
+    if (p->d_tw) cudaFree(p->d_tw);
+    if (p->d_rtw) cudaFree(p->d_rtw);
+    if (p->d_ww) cudaFree(p->d_ww);
+    delete p;
+    return WS_OK;
+}
+
+int ws_plane_get_info(const ws_plane* p, ws_plane_info* info)
+{
+    if (!p || !info) return set_err(WS_EINVAL, "null argument");
+    info->padded_wires = (uint64_t)p->W;
+    info->padded_ticks = (uint64_t)p->N;
+    info->fft_length = (uint64_t)p->Np;
+    info->folded = p->folded;
+    info->n_radix_passes = (int32_t)p->radix.size();
+    info->support_ticks = p->support_ticks;
+    info->support_wires = p->support_wires;
+    info->lo_lag = p->lo_lag;
+    info->n_lags = p->n_lags;
+    return WS_OK;
+}
+
+int ws_plane_get_kernel(const ws_plane* p, double* out, uint64_t cap)
+{
+    if (!p || !out) return set_err(WS_EINVAL, "null argument");
+    if (cap < p->kernel.size()) return set_err(WS_ERANGE, "kernel has %zu lags", p->kernel.size());
+    std::copy(p->kernel.begin(), p->kernel.end(), out);
+    return WS_OK;
+}
+
+int ws_simulate_event_device(ws_ctx* ctx, uint32_t n_planes, ws_plane* const* planes, const ws_depo* const* depos,
+                             const uint64_t* n_depos, const ws_sim_options* opt, float* const* frames,
+                             ws_timing* timing)
+{
+    if (int rc = check_plane_set(ctx, n_planes, planes)) return rc;
+    if (int rc = check_opts(opt)) return rc;
+    WS_CUDA(cudaSetDevice(ctx->device));
+    std::vector<float*> charges(n_planes, nullptr);
+    if (opt->fluctuate) {
+        size_t total = 0;
+        for (uint32_t i = 0; i < n_planes; ++i) total += (size_t)planes[i]->W * planes[i]->N;
+        WS_CUDA(ctx->charges.reserve(total));
+        size_t off = 0;
+        for (uint32_t i = 0; i < n_planes; ++i) {
+            charges[i] = ctx->charges.p + off;
+            off += (size_t)planes[i]->W * planes[i]->N;
+        }
+    }
+    for (uint32_t g = 0; g < n_planes; g += wsb::kMaxPlanes) {
+        const uint32_t n = std::min<uint32_t>(wsb::kMaxPlanes, n_planes - g);
+        const int rc = run_group(ctx, n, planes + g, depos + g, n_depos + g, opt, frames + g,
+                                 opt->fluctuate ? charges.data() + g : nullptr, nullptr, g == 0 ? timing : nullptr);
+        if (rc) return rc;
+    }
+    return WS_OK;
+}
+
+int ws_simulate_plane_device(ws_plane* p, const ws_depo* depos, uint64_t n, const ws_sim_options* opt, float* frame,
+                             float* charge, ws_timing* timing)
+{
+    if (!p) return set_err(WS_EINVAL, "null plane");
+    if (int rc = check_opts(opt)) return rc;
+    ws_ctx* c = p->ctx;
+    WS_CUDA(cudaSetDevice(c->device));
+    float* ch = charge;
+    if (opt->fluctuate && !ch) {
+        WS_CUDA(c->charges.reserve((size_t)p->W * p->N));
+        ch = c->charges.p;
+    }
+    ws_plane* planes[1] = {p};
+    const ws_depo* dp[1] = {depos};
+    uint64_t nd[1] = {n};
+    float* fr[1] = {frame};
+    float* chs[1] = {ch};
+    return run_group(c, 1, planes, dp, nd, opt, fr, ch ? chs : nullptr, nullptr, timing);
+}
+
+int ws_rasterize_device(ws_plane* p, const ws_depo* depos, uint64_t n, const ws_sim_options* opt, float* charge,
+                        ws_timing* timing)
+{
+    if (!p || !charge) return set_err(WS_EINVAL, "null argument");
+    if (int rc = check_opts(opt)) return rc;
+    WS_CUDA(cudaSetDevice(p->ctx->device));
+    ws_plane* planes[1] = {p};
+    const ws_depo* dp[1] = {depos};
+    uint64_t nd[1] = {n};
+    float* chs[1] = {charge};
+    return run_group(p->ctx, 1, planes, dp, nd, opt, nullptr, chs, nullptr, timing);
+}
+
+int ws_convolve_device(ws_plane* p, const float* charge, float* frame)
+{
+    if (!p || !charge || !frame) return set_err(WS_EINVAL, "null argument");
+    WS_CUDA(cudaSetDevice(p->ctx->device));
+    ws_sim_options o{};
+    ws_plane* planes[1] = {p};
+    float* fr[1] = {frame};
+    const float* ci[1] = {charge};
+    return run_group(p->ctx, 1, planes, nullptr, nullptr, &o, fr, nullptr, ci, nullptr);
+}
+
+int ws_simulate_event(ws_ctx* ctx, uint32_t n_planes, ws_plane* const* planes, const ws_depo* const* depos,
+                      const uint64_t* n_depos, const ws_sim_options* opt, float* const* frames, ws_timing* timing)
+{
+    if (int rc = check_plane_set(ctx, n_planes, planes)) return rc;
+    if (int rc = check_opts(opt)) return rc;
+    WS_CUDA(cudaSetDevice(ctx->device));
+    if (int rc = finish_pending(ctx)) return rc;
+    // host validation the reference does at ingestion / drift time
+    size_t units = 0, cells = 0;
+    for (uint32_t i = 0; i < n_planes; ++i) {
+        units += n_depos[i];
+        cells += (size_t)planes[i]->W * planes[i]->N;
+    }
+    WS_CUDA(ctx->depos.reserve(units));
+    WS_CUDA(ctx->frames.reserve(cells));
+    std::vector<const ws_depo*> dd(n_planes);
+    std::vector<float*> ff(n_planes);
+    size_t uo = 0, co = 0;
+    for (uint32_t i = 0; i < n_planes; ++i) {
+        dd[i] = ctx->depos.p + uo;
+        ff[i] = ctx->frames.p + co;
+        if (n_depos[i])
+            WS_CUDA(cudaMemcpyAsync(ctx->depos.p + uo, depos[i], sizeof(ws_depo) * n_depos[i], cudaMemcpyHostToDevice,
+                                    ctx->stream));
+        uo += n_depos[i];
+        co += (size_t)planes[i]->W * planes[i]->N;
+    }
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        if (int rc = ws_simulate_event_device(ctx, n_planes, planes, dd.data(), n_depos, opt, ff.data(), timing))
+            return rc;
+        const int rc = finish_pending(ctx);
+        if (rc == WS_ERANGE) continue;  // pool grown; re-run
+        if (rc) return rc;
+        break;
+    }
+    co = 0;
+    for (uint32_t i = 0; i < n_planes; ++i) {
+        const size_t nc = (size_t)planes[i]->W * planes[i]->N;
+        if (frames && frames[i])
+            WS_CUDA(cudaMemcpyAsync(frames[i], ctx->frames.p + co, sizeof(float) * nc, cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+        co += nc;
+    }
+    WS_CUDA(cudaStreamSynchronize(ctx->stream));
+    return WS_OK;
+}
+
+int ws_simulate_plane(ws_plane* p, const ws_depo* depos, uint64_t n, const ws_sim_options* opt, float* frame,
+                      float* charge, ws_timing* timing)
+{
+    if (!p) return set_err(WS_EINVAL, "null plane");
+    if (int rc = check_opts(opt)) return rc;
+    ws_ctx* c = p->ctx;
+    WS_CUDA(cudaSetDevice(c->device));
+    if (int rc = finish_pending(c)) return rc;
+    const size_t cells = (size_t)p->W * p->N;
+    WS_CUDA(c->depos.reserve(n));
+    WS_CUDA(c->frames.reserve(cells));
+    if (charge || opt->fluctuate) WS_CUDA(c->charges.reserve(cells));
+    if (n) WS_CUDA(cudaMemcpyAsync(c->depos.p, depos, sizeof(ws_depo) * n, cudaMemcpyHostToDevice, c->stream));
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        if (int rc = ws_simulate_plane_device(p, c->depos.p, n, opt, frame ? c->frames.p : nullptr,
+                                              (charge || opt->fluctuate) ? c->charges.p : nullptr, timing))
+            return rc;
+        const int rc = finish_pending(c);
+        if (rc == WS_ERANGE) continue;
+        if (rc) return rc;
+        break;
+    }
+    if (frame) WS_CUDA(cudaMemcpyAsync(frame, c->frames.p, sizeof(float) * cells, cudaMemcpyDeviceToHost, c->stream));
+    if (charge) WS_CUDA(cudaMemcpyAsync(charge, c->charges.p, sizeof(float) * cells, cudaMemcpyDeviceToHost, c->stream));
+    WS_CUDA(cudaStreamSynchronize(c->stream));
+    return WS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,270 @@
+// Shared device-side definitions for the B200 signal-simulation hot path.
+//
+// Layout of one "event" launch: up to kMaxPlanes independent planes (each a
+// run_simulation-equivalent), their depos concatenated into
+// "units" (one unit = one depo on one plane). Plane descriptors travel as a
+// kernel parameter (EventDesc) so a launch needs no host->device copy.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "wiresim_gpu.h"
+
+namespace wsb {
+
+constexpr int kMaxPlanes = 8;
+constexpr int kMaxPasses = 12;
+constexpr int kMaxWireWeights = 33;  // 2h+1 <= 33 taps of cross-wire coupling
+constexpr int kConvThreads = 512;
+constexpr int kMaxFftHalf = 12288;   // M = N'/2 <= 12288 (N' <= 24576 ticks)
+constexpr double kFixScale = 4294967296.0;          // 2^32: fixed-point electrons
+constexpr double kFixInv = 1.0 / 4294967296.0;
+
+// Per-unit footprint record written by the sample kernel.
+struct __align__(16) UnitRec {
+    int32_t w0;    // first wire (padded index) of the clipped footprint; -1 = empty
+    int32_t t0;    // first tick (padded index)
+    int32_t n_w;   // wires
+    int32_t n_t;   // ticks
+    uint32_t pool; // offset (in doubles) of [wv(n_w) | tv(n_t)] in the pool
+    int32_t plane;
+    double a;      // fluct off: q / total; fluct on: unused
+};
+
+// Device view of one plane for one launch.
+struct PlaneDesc {
+    // geometry (GridSpec, core.hpp:40-58)
+    int32_t W, N;              // padded wires, padded ticks
+    int32_t pad_w, pad_t;
+    double pitch, tick, origin_x, origin_t;
+    double n_sigma;
+    // response
+    int32_t h;                 // wire-weight half width
+    int32_t ww_is_one;         // wire_weights == {1.0}: S' == S
+    int32_t folded;            // circular wrap folded from a length-Np linear transform
+    int32_t Np, M;             // real FFT length, complex half length
+    int32_t lo_lag, hi_lag;    // combined kernel lags
+    int32_t npass;
+    int32_t radix[kMaxPasses];
+    const double* ww;          // 2h+1 wire weights
+    const float2* H;           // M+1 response spectrum bins, pre-scaled by 1/M
+    const float2* tw;          // exp(-2 pi i m / M), m < M
+    const float2* rtw;         // exp(-2 pi i k / Np), k <= M/2
+    // per call
+    const ws_depo* depos;
+    uint32_t n_units;
+    uint32_t unit_base;        // first unit index of this plane
+    uint32_t band_base;        // first band index of this plane
+    int32_t rows_per_band;
+    int32_t n_bands;
+    float* frame;              // out: M (nullable when only the charge grid is wanted)
+    float* charge_out;         // out: S (nullable)
+    const float* charge_in;    // in: S (mode "grid")
+    long long* stats;          // [0] clipped_charge, [1] clipped_patches
+};
+
+struct EventDesc {
+    int32_t n_planes;
+    int32_t fluctuate;
+    int32_t approx;
+    int32_t rng_mode;
+    uint64_t seed;
+    int32_t drift_enabled;
+    int32_t mode;              // conv source: 0 accumulate from band lists, 1 charge grid
+    double drift_plane_x, drift_speed, drift_dl, drift_dt;
+    uint32_t total_units;
+    uint32_t total_bands;
+    PlaneDesc p[kMaxPlanes];
+};
+
+// Error / overflow flags shared by kernels (device scalar words).
+enum : unsigned { kErrPool = 1u, kErrDomain = 2u, kErrCharge = 4u, kErrRange = 8u };
+
+__device__ __forceinline__ int plane_of_unit(const EventDesc& ev, uint32_t u)
+{
+    int p = 0;
+#pragma unroll 1
+    for (int i = 1; i < ev.n_planes; ++i)
+        if (u >= ev.p[i].unit_base) p = i;
+    return p;
+}
+
+// ------------------------------------------------------------------ RNG --
+// xoshiro256** / splitmix64, bit-identical to rng.cpp:18-76.
+__device__ __forceinline__ uint64_t splitmix64_next(uint64_t& s)
+{
+    uint64_t z = (s += 0x9e3779b97f4a7c15ULL);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ uint64_t rotl64(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+
+struct Rng {
+    int mode;      // 0 substream (xoshiro), 1 philox
+    uint64_t s0, s1, s2, s3;
+    uint32_t key0, key1, id0, id1;
+    uint32_t draw;
+    double spare;
+    bool have_spare;
+
+    __device__ void init(int m, uint64_t seed, uint64_t id)
+    {
+        mode = m;
+        have_spare = false;
+        spare = 0.0;
+        draw = 0;
+        if (m == WS_RNG_SUBSTREAM) {
+            // substream (rng.cpp:64-76)
+            uint64_t sm = seed, tag = id;
+            (void)splitmix64_next(tag);
+            sm ^= splitmix64_next(tag);
+            s0 = splitmix64_next(sm);
+            s1 = splitmix64_next(sm);
+            s2 = splitmix64_next(sm);
+            s3 = splitmix64_next(sm);
+            if ((s0 | s1 | s2 | s3) == 0) s0 = 0x9e3779b97f4a7c15ULL;
+        } else {
+            key0 = (uint32_t)seed;
+            key1 = (uint32_t)(seed >> 32);
+            id0 = (uint32_t)id;
+            id1 = (uint32_t)(id >> 32);
+        }
+    }
+
+    __device__ __forceinline__ uint64_t next_xoshiro()
+    {
+        const uint64_t result = rotl64(s1 * 5, 7) * 9;
+        const uint64_t t = s1 << 17;
+        s2 ^= s0;
+        s3 ^= s1;
+        s1 ^= s2;
+        s0 ^= s3;
+        s2 ^= t;
+        s3 = rotl64(s3, 45);
+        return result;
+    }
+
+    // Philox4x32-10; draw i -> ctr (i>>1, id lo, id hi, 0), words 2(i&1), 2(i&1)+1.
+    __device__ __forceinline__ uint64_t next_philox()
+    {
+        const uint32_t i = draw++;
+        uint32_t c0 = i >> 1, c1 = id0, c2 = id1, c3 = 0u;
+        uint32_t k0 = key0, k1 = key1;
+#pragma unroll
+        for (int r = 0; r < 10; ++r) {
+            const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+            const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+            const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+            c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+        return (i & 1u) ? ((uint64_t)c2 << 32 | c3) : ((uint64_t)c0 << 32 | c1);
+    }
+
+    // uniform01 (rng.cpp:51-54)
+    __device__ __forceinline__ double uniform()
+    {
+        const uint64_t x = mode == WS_RNG_SUBSTREAM ? next_xoshiro() : next_philox();
+        return (double)(x >> 11) * 0x1.0p-53;
+    }
+
+    // StreamSource::normal (rng.hpp:78-90) + box_muller (rng.cpp:56-62)
+    __device__ double normal()
+    {
+        if (have_spare) {
+            have_spare = false;
+            return spare;
+        }
+        const double u1 = __dsub_rn(1.0, uniform());
+        const double u2 = uniform();
+        const double r = sqrt(__dmul_rn(-2.0, log(u1)));
+        const double a = __dmul_rn(6.283185307179586476925286766559, u2);
+        double sn, cs;
+        sincos(a, &sn, &cs);
+        spare = __dmul_rn(r, sn);
+        have_spare = true;
+        return __dmul_rn(r, cs);
+    }
+};
+
+// exp with a correctly rounded subnormal range. CUDA's exp loses the
+// subnormal results that glibc returns (e.g. the lgamma-seeded pmf at
+// n*log1p(-p) ~ -744, rng.cpp:152-162); scale into the normal range, then let
+// one IEEE multiply round into the subnormal grid.
+__device__ __forceinline__ double exp_ref(double x)
+{
+    if (x >= -708.0) return exp(x);
+    const double kLn2Hi = 0x1.62e42fefa3800p-1, kLn2Lo = 0x1.ef35793c7673p-45;
+    const double y = exp(__dadd_rn(__dadd_rn(x, 512.0 * kLn2Hi), 512.0 * kLn2Lo));
+    return __dmul_rn(y, 0x1p-512);
+}
+
+// --------------------------------------------------------------- binomial --
+// invert_binomial_cdf (rng.cpp:146-170), operation order kept with explicit
+// round-to-nearest intrinsics (no FMA contraction).
+__device__ __forceinline__ int64_t invert_binomial_cdf(int64_t n, double p, double u)
+{
+    const double odds = __ddiv_rn(p, __dsub_rn(1.0, p));
+    int64_t k = 0;
+    double pmf;
+    const double log_pmf0 = __dmul_rn((double)n, log1p(-p));
+    if (log_pmf0 > -700.0) {
+        pmf = exp_ref(log_pmf0);
+    } else {
+        const double mean = __dmul_rn((double)n, p);
+        const double sd = sqrt(__dmul_rn(mean, __dsub_rn(1.0, p)));
+        const int64_t k0 = (int64_t)__dsub_rn(mean, __dmul_rn(30.0, sd));
+        k = k0 > 0 ? k0 : 0;
+        const double nd = (double)n, kd = (double)k;
+        double e = __dsub_rn(lgamma(__dadd_rn(nd, 1.0)), lgamma(__dadd_rn(kd, 1.0)));
+        e = __dsub_rn(e, lgamma(__dadd_rn(__dsub_rn(nd, kd), 1.0)));
+        e = __dadd_rn(e, __dmul_rn(kd, log(p)));
+        e = __dadd_rn(e, __dmul_rn(__dsub_rn(nd, kd), log1p(-p)));
+        pmf = exp_ref(e);
+    }
+    double cdf = pmf;
+    while (cdf <= u && k < n) {
+        pmf = __dmul_rn(pmf, __ddiv_rn(__dmul_rn(odds, (double)(n - k)), (double)(k + 1)));
+        ++k;
+        cdf = __dadd_rn(cdf, pmf);
+    }
+    return k;
+}
+
+// binomial (rng.cpp:174-193); p in [0,1] guaranteed by the caller's clamp.
+__device__ __forceinline__ int64_t binomial(int64_t n, double p, Rng& src)
+{
+    if (n == 0 || p == 0.0) return 0;
+    if (p == 1.0) return n;
+    const double mean = __dmul_rn((double)n, p);
+    const double var = __dmul_rn(mean, __dsub_rn(1.0, p));
+    const double q1 = __dsub_rn(1.0, p);
+    const double mn = (q1 < p) ? q1 : p;
+    if (__dmul_rn((double)n, mn) > 1e6) {
+        const double k = round(__dadd_rn(mean, __dmul_rn(sqrt(var), src.normal())));
+        if (k < 0.0) return 0;
+        if (k > (double)n) return n;
+        return (int64_t)k;
+    }
+    const double u = src.uniform();
+    if (p > 0.5) return n - invert_binomial_cdf(n, q1, u);
+    return invert_binomial_cdf(n, p, u);
+}
+
+// fluctuate_approx draw (rasterize.cpp:161-169)
+__device__ __forceinline__ int64_t binomial_approx(int64_t n, double p, Rng& src)
+{
+    if (p <= 0.0) return 0;
+    if (p >= 1.0) return n;
+    const double mean = __dmul_rn((double)n, p);
+    const double k = round(__dadd_rn(mean, __dmul_rn(sqrt(__dmul_rn(mean, __dsub_rn(1.0, p))), src.normal())));
+    if (k < 0.0) return 0;
+    if (k > (double)n) return n;
+    return (int64_t)k;
+}
+
+}  // namespace wsb

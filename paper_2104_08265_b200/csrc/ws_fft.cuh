@@ -1,0 +1,234 @@
+// Shared-memory mixed-radix Stockham FFT (complex fp32) for one tick row.
+//
+// Replaces the reference's recursive double FFT (fft.cpp:116-161) on the hot
+// path. The transform length M is 7-smooth (radix 2,3,4,5,7,8 passes), planned
+// on the host (ws_api.cu: plan_radices). One CTA transforms one row in place:
+// passes ping-pong between two M-element buffers (16*M bytes of shared memory,
+// exactly the footprint of the row's int64 accumulator, which they alias).
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace wsb {
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) { return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+// multiply by -i
+__device__ __forceinline__ float2 cmul_mi(float2 a) { return make_float2(a.y, -a.x); }
+
+// Forward DFT of size R in registers: X_k = sum_n x_n exp(-2 pi i n k / R).
+template <int R>
+struct Dft;
+
+template <>
+struct Dft<2> {
+    static __device__ __forceinline__ void run(float2* v)
+    {
+        const float2 a = v[0], b = v[1];
+        v[0] = cadd(a, b);
+        v[1] = csub(a, b);
+    }
+};
+
+template <>
+struct Dft<4> {
+    static __device__ __forceinline__ void run(float2* v)
+    {
+        const float2 s02 = cadd(v[0], v[2]), d02 = csub(v[0], v[2]);
+        const float2 s13 = cadd(v[1], v[3]), d13 = cmul_mi(csub(v[1], v[3]));
+        v[0] = cadd(s02, s13);
+        v[2] = csub(s02, s13);
+        v[1] = cadd(d02, d13);
+        v[3] = csub(d02, d13);
+    }
+};
+
+template <>
+struct Dft<8> {
+    static __device__ __forceinline__ void run(float2* v)
+    {
+        constexpr float r = 0.70710678118654752440f;
+        // radix-2 over pairs (n, n+4), then twiddle, then two radix-4
+        float2 a[4], b[4];
+#pragma unroll
+        for (int n = 0; n < 4; ++n) {
+            a[n] = cadd(v[n], v[n + 4]);
+            b[n] = csub(v[n], v[n + 4]);
+        }
+        // b[n] *= exp(-2 pi i n / 8)
+        b[1] = make_float2(r * (b[1].x + b[1].y), r * (b[1].y - b[1].x));
+        b[2] = cmul_mi(b[2]);
+        b[3] = make_float2(r * (b[3].y - b[3].x), -r * (b[3].x + b[3].y));
+        Dft<4>::run(a);
+        Dft<4>::run(b);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            v[2 * k] = a[k];
+            v[2 * k + 1] = b[k];
+        }
+    }
+};
+
+// Odd prime radix via the symmetric-pair form: with a_m = x_m + x_{R-m},
+// b_m = x_m - x_{R-m}: X_k = x_0 + sum_m a_m cos(2 pi k m / R) - i sum_m b_m sin(...).
+template <int R>
+struct OddDft {
+    static __device__ __forceinline__ float cosv(int km);
+    static __device__ __forceinline__ float sinv(int km);
+};
+
+template <>
+__device__ __forceinline__ float OddDft<3>::cosv(int km)
+{
+    return (km % 3 == 0) ? 1.0f : -0.5f;
+}
+template <>
+__device__ __forceinline__ float OddDft<3>::sinv(int km)
+{
+    const int r = km % 3;
+    return r == 0 ? 0.0f : (r == 1 ? 0.86602540378443864676f : -0.86602540378443864676f);
+}
+
+template <>
+__device__ __forceinline__ float OddDft<5>::cosv(int km)
+{
+    const int r = km % 5;
+    return r == 0 ? 1.0f : (r == 1 || r == 4) ? 0.30901699437494742410f : -0.80901699437494742410f;
+}
+template <>
+__device__ __forceinline__ float OddDft<5>::sinv(int km)
+{
+    const int r = km % 5;
+    return r == 0 ? 0.0f
+         : r == 1 ? 0.95105651629515357212f
+         : r == 2 ? 0.58778525229247312917f
+         : r == 3 ? -0.58778525229247312917f
+                  : -0.95105651629515357212f;
+}
+
+template <>
+__device__ __forceinline__ float OddDft<7>::cosv(int km)
+{
+    const int r = km % 7;
+    return r == 0 ? 1.0f
+         : (r == 1 || r == 6) ? 0.62348980185873353053f
+         : (r == 2 || r == 5) ? -0.22252093395631440429f
+                              : -0.90096886790241912624f;
+}
+template <>
+__device__ __forceinline__ float OddDft<7>::sinv(int km)
+{
+    const int r = km % 7;
+    return r == 0 ? 0.0f
+         : r == 1 ? 0.78183148246802980871f
+         : r == 2 ? 0.97492791218182360702f
+         : r == 3 ? 0.43388373911755812048f
+         : r == 4 ? -0.43388373911755812048f
+         : r == 5 ? -0.97492791218182360702f
+                  : -0.78183148246802980871f;
+}
+
+template <int R>
+struct DftOdd {
+    static __device__ __forceinline__ void run(float2* v)
+    {
+        constexpr int H = (R - 1) / 2;
+        float2 a[H], b[H];
+        float2 s = v[0];
+#pragma unroll
+        for (int m = 1; m <= H; ++m) {
+            a[m - 1] = cadd(v[m], v[R - m]);
+            b[m - 1] = csub(v[m], v[R - m]);
+            s = cadd(s, a[m - 1]);
+        }
+        float2 out[R];
+        out[0] = s;
+#pragma unroll
+        for (int k = 1; k <= H; ++k) {
+            float2 re = v[0], im = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int m = 1; m <= H; ++m) {
+                const float c = OddDft<R>::cosv(k * m), sn = OddDft<R>::sinv(k * m);
+                re.x += a[m - 1].x * c;
+                re.y += a[m - 1].y * c;
+                im.x += b[m - 1].x * sn;
+                im.y += b[m - 1].y * sn;
+            }
+            // X_k = re - i*im ; X_{R-k} = re + i*im
+            out[k] = make_float2(re.x + im.y, re.y - im.x);
+            out[R - k] = make_float2(re.x - im.y, re.y + im.x);
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k) v[k] = out[k];
+    }
+};
+
+template <>
+struct Dft<3> : DftOdd<3> {};
+template <>
+struct Dft<5> : DftOdd<5> {};
+template <>
+struct Dft<7> : DftOdd<7> {};
+
+// One out-of-place Stockham radix-R pass: butterfly j reads in[j + r*M/R],
+// applies twiddles exp(-2 pi i k r / (Ns R)) with k = j mod Ns, runs Dft<R>,
+// and writes out[(j/Ns)*Ns*R + k + r*Ns]. One barrier per pass.
+template <int R, int NT>
+__device__ __forceinline__ void stockham_pass(const float2* __restrict__ in, float2* __restrict__ out, int M, int Ns,
+                                              const float2* __restrict__ tw)
+{
+    const int nb = M / R;
+    const int stride = M / (Ns * R);
+#pragma unroll 2
+    for (int j = threadIdx.x; j < nb; j += NT) {
+        float2 v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = in[j + r * nb];
+        const int k = j % Ns;
+        if (Ns > 1) {
+            const float2 w1 = __ldg(&tw[k * stride]);
+            float2 w = w1;
+#pragma unroll
+            for (int r = 1; r < R; ++r) {
+                v[r] = cmul(v[r], w);
+                if (r + 1 < R) w = cmul(w, w1);
+            }
+        }
+        Dft<R>::run(v);
+        const int base = (j - k) * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) out[base + r * Ns] = v[r];
+    }
+    __syncthreads();
+}
+
+// Forward FFT of length M = prod(radix[0..npass)) from buffer a, ping-ponging
+// with buffer b. Returns the buffer holding the (natural-order) result.
+template <int NT>
+__device__ __forceinline__ float2* fft_forward(float2* a, float2* b, int M, int npass, const int* radix,
+                                               const float2* __restrict__ tw)
+{
+    int Ns = 1;
+#pragma unroll 1
+    for (int p = 0; p < npass; ++p) {
+        const int R = radix[p];
+        switch (R) {
+            case 2: stockham_pass<2, NT>(a, b, M, Ns, tw); break;
+            case 3: stockham_pass<3, NT>(a, b, M, Ns, tw); break;
+            case 4: stockham_pass<4, NT>(a, b, M, Ns, tw); break;
+            case 5: stockham_pass<5, NT>(a, b, M, Ns, tw); break;
+            case 7: stockham_pass<7, NT>(a, b, M, Ns, tw); break;
+            default: stockham_pass<8, NT>(a, b, M, Ns, tw); break;
+        }
+        Ns *= R;
+        float2* t = a;
+        a = b;
+        b = t;
+    }
+    return a;
+}
+
+}  // namespace wsb

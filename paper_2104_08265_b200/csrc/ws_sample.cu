@@ -1,0 +1,359 @@
+// Per-depo sampling (K1 front half), depo -> wire-band binning, and the
+// sequential-binomial fluctuation walk (K2).
+//
+// Compiled with --fmad=false: every double expression below keeps the
+// reference's operation order and rounding (no FMA contraction), so the
+// footprints and bin integrals are the reference's, and the fluctuation walk
+// reproduces its integer draws.
+#include "ws_common.cuh"
+
+namespace wsb {
+
+constexpr double kInvSqrt2 = 0.70710678118654752440084436210485;
+
+struct Footprint {
+    int w0, n_w, t0, n_t;
+    bool clipped, empty;
+};
+
+// map_depo_to_grid (core.cpp:25-41) + the clip of sample_patch (rasterize.cpp:68-80)
+__device__ __forceinline__ Footprint footprint(const PlaneDesc& P, const ws_depo& d)
+{
+    const long cw = (long)P.pad_w + (long)floor((d.x - P.origin_x) / P.pitch);
+    const long ct = (long)P.pad_t + (long)floor((d.t - P.origin_t) / P.tick);
+    const long hw = d.sigma_x <= 0.0 ? 0 : (long)ceil(P.n_sigma * d.sigma_x / P.pitch);
+    const long ht = d.sigma_t <= 0.0 ? 0 : (long)ceil(P.n_sigma * d.sigma_t / P.tick);
+    const long wlo = cw - hw, whi = cw + hw, tlo = ct - ht, thi = ct + ht;
+    const long max_w = (long)P.W - 1, max_t = (long)P.N - 1;
+    const long wl = wlo > 0 ? wlo : 0, wh = whi < max_w ? whi : max_w;
+    const long tl = tlo > 0 ? tlo : 0, th = thi < max_t ? thi : max_t;
+    Footprint f;
+    f.clipped = wl != wlo || wh != whi || tl != tlo || th != thi;
+    f.empty = wl > wh || tl > th;
+    f.w0 = (int)wl;
+    f.t0 = (int)tl;
+    f.n_w = f.empty ? 0 : (int)(wh - wl + 1);
+    f.n_t = f.empty ? 0 : (int)(th - tl + 1);
+    return f;
+}
+
+// drift_depo (rasterize.cpp:22-42); returns false if the depo is behind the plane.
+__device__ __forceinline__ bool drift(const EventDesc& ev, ws_depo& d)
+{
+    if (d.x < ev.drift_plane_x) return false;
+    const double dx = d.x - ev.drift_plane_x;
+    const double drift_time = dx / ev.drift_speed;
+    d.t = d.t + drift_time;
+    d.x = ev.drift_plane_x;
+    const double v2 = ev.drift_speed * ev.drift_speed;
+    d.sigma_t = sqrt(d.sigma_t * d.sigma_t + 2.0 * ev.drift_dl * drift_time / v2);
+    d.sigma_x = sqrt(d.sigma_x * d.sigma_x + 2.0 * ev.drift_dt * drift_time);
+    return true;
+}
+
+// gauss_bin_integrals (rasterize.cpp:44-64), one thread, reference order.
+// Returns sum and max of the n values; writes them through `put(i, v)`.
+template <typename Put>
+__device__ __forceinline__ void bin_integrals(double center, double sigma, double lo_edge, double spacing, int n,
+                                              Put&& put, double& sum, double& vmax)
+{
+    sum = 0.0;
+    vmax = 0.0;
+    if (sigma <= 0.0) {
+        long idx = (long)floor((center - lo_edge) / spacing);
+        idx = idx < 0 ? 0 : (idx > n - 1 ? n - 1 : idx);
+        for (int i = 0; i < n; ++i) put(i, i == idx ? 1.0 : 0.0);
+        sum = 1.0;
+        vmax = 1.0;
+        return;
+    }
+    const double inv = kInvSqrt2 / sigma;
+    double prev = erf((lo_edge - center) * inv);
+    for (int i = 0; i < n; ++i) {
+        const double next = erf((lo_edge + (double)(i + 1) * spacing - center) * inv);
+        const double v = 0.5 * (next - prev);
+        prev = next;
+        put(i, v);
+        sum += v;
+        vmax = v > vmax ? v : vmax;
+    }
+}
+
+__device__ __forceinline__ void band_ranges(const PlaneDesc& P, int w0, int n_w, int& a0, int& b0, int& a1, int& b1)
+{
+    // effective rows [w0 - h, w0 + n_w - 1 + h] modulo W as up to two ranges
+    const int W = P.W;
+    const int lo = w0 - P.h, hi = w0 + n_w - 1 + P.h;
+    a1 = 1;
+    b1 = 0;  // empty second range
+    if (hi - lo + 1 >= W) {
+        a0 = 0;
+        b0 = W - 1;
+    } else if (lo < 0) {
+        a0 = lo + W;
+        b0 = W - 1;
+        a1 = 0;
+        b1 = hi;
+    } else if (hi >= W) {
+        a0 = lo;
+        b0 = W - 1;
+        a1 = 0;
+        b1 = hi - W;
+    } else {
+        a0 = lo;
+        b0 = hi;
+    }
+}
+
+// Visit each band the unit's effective rows touch, exactly once.
+template <typename F>
+__device__ __forceinline__ void for_each_band(const PlaneDesc& P, int w0, int n_w, F&& f)
+{
+    int a0, b0, a1, b1;
+    band_ranges(P, w0, n_w, a0, b0, a1, b1);
+    const int B = P.rows_per_band;
+    const int c0 = a0 / B, c1 = b0 / B;
+    for (int c = c0; c <= c1; ++c) f(c);
+    if (a1 <= b1) {
+        const int d0 = a1 / B, d1 = b1 / B;
+        for (int c = d0; c <= d1; ++c)
+            if (c < c0 || c > c1) f(c);
+    }
+}
+
+// One thread per unit: footprint (map_depo_to_grid + clip), bin integrals
+// into the pool, emptiness (sample_patch's total <= 0 test), clipped-charge
+// bookkeeping and, with fluctuation off, the normalised separable profiles
+// and the band counts.
+//
+// Pool layout per unit (32-bit words):
+//   fluctuation on : [wv f64 x n_w][tv f64 x n_t]                 (8-byte aligned)
+//   fluctuation off: [raw f32 x n_w][eff f32 x n_eff][tv f32 x n_t]
+// with raw = q/total * wv (the un-stencilled wire profile), eff = the profile
+// after the cross-wire stencil (absent when wire_weights == {1}), and
+// total = sum_w wv * sum_t tv.
+__global__ void k_sample(const EventDesc ev, UnitRec* __restrict__ recs, uint32_t* __restrict__ pool, uint32_t pool_cap,
+                         uint32_t* __restrict__ pool_ctr, uint32_t* __restrict__ band_count, unsigned* __restrict__ err)
+{
+    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= ev.total_units) return;
+    const int pi = plane_of_unit(ev, u);
+    const PlaneDesc& P = ev.p[pi];
+    ws_depo d = P.depos[u - P.unit_base];
+    UnitRec rec;
+    rec.w0 = -1;
+    rec.t0 = 0;
+    rec.n_w = 0;
+    rec.n_t = 0;
+    rec.pool = 0;
+    rec.plane = pi;
+    rec.a = 0.0;
+    if (ev.drift_enabled && !drift(ev, d)) {
+        atomicOr(err, kErrDomain);
+        recs[u] = rec;
+        return;
+    }
+    if (d.q < 0) atomicOr(err, kErrCharge);
+    const Footprint f = footprint(P, d);
+    if (f.clipped) atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[1]), 1ULL);
+    if (f.empty) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[0]), (unsigned long long)d.q);
+        recs[u] = rec;
+        return;
+    }
+    const int h = P.h;
+    const int n_eff = P.ww_is_one ? 0 : f.n_w + 2 * h;
+    const uint32_t need = ev.fluctuate ? (uint32_t)(2 * (f.n_w + f.n_t) + 1) : (uint32_t)(f.n_w + n_eff + f.n_t);
+    uint32_t off = atomicAdd(pool_ctr, need);
+    if ((uint64_t)off + need > pool_cap) {
+        atomicOr(err, kErrPool);
+        recs[u] = rec;
+        return;
+    }
+    const double wire_edge = P.origin_x + ((double)f.w0 - (double)P.pad_w) * P.pitch;
+    const double tick_edge = P.origin_t + ((double)f.t0 - (double)P.pad_t) * P.tick;
+    double sw, mw, st, mt;
+    if (ev.fluctuate) {
+        off += off & 1u;  // 8-byte alignment
+        double* wv = reinterpret_cast<double*>(pool + off);
+        double* tv = wv + f.n_w;
+        bin_integrals(d.x, d.sigma_x, wire_edge, P.pitch, f.n_w, [&](int i, double v) { wv[i] = v; }, sw, mw);
+        bin_integrals(d.t, d.sigma_t, tick_edge, P.tick, f.n_t, [&](int i, double v) { tv[i] = v; }, st, mt);
+    } else {
+        float* raw = reinterpret_cast<float*>(pool + off);
+        float* tv = raw + f.n_w + n_eff;
+        bin_integrals(d.x, d.sigma_x, wire_edge, P.pitch, f.n_w, [&](int i, double v) { raw[i] = (float)v; }, sw, mw);
+        bin_integrals(d.t, d.sigma_t, tick_edge, P.tick, f.n_t, [&](int i, double v) { tv[i] = (float)v; }, st, mt);
+    }
+    // sum_w sum_t wv*tv > 0  <=>  max(wv)*max(tv) > 0 (all terms >= 0, products monotone)
+    if (!(mw * mt > 0.0)) {
+        // numerically empty (rasterize.cpp:111-116) -> clipped charge (pipeline.cpp:339-340)
+        atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[0]), (unsigned long long)d.q);
+        recs[u] = rec;
+        return;
+    }
+    if (!ev.fluctuate) {
+        const double a = (double)d.q / (sw * st);
+        float* raw = reinterpret_cast<float*>(pool + off);
+        for (int i = 0; i < f.n_w; ++i) raw[i] = (float)((double)raw[i] * a);
+        if (n_eff) {
+            float* eff = raw + f.n_w;
+            for (int j = 0; j < n_eff; ++j) {
+                double e = 0.0;
+                for (int dw = -h; dw <= h; ++dw) {
+                    const int i = j - h - dw;
+                    if (i >= 0 && i < f.n_w) e += P.ww[dw + h] * (double)raw[i];
+                }
+                eff[j] = (float)e;
+            }
+        }
+        rec.a = a;
+    }
+    rec.w0 = f.w0;
+    rec.t0 = f.t0;
+    rec.n_w = f.n_w;
+    rec.n_t = f.n_t;
+    rec.pool = off;
+    recs[u] = rec;
+    if (!ev.fluctuate && ev.mode == 0)
+        for_each_band(P, f.w0, f.n_w, [&](int c) { atomicAdd(&band_count[P.band_base + c], 1u); });
+}
+
+// Exclusive scan of band counts (single block); resets the fill cursors.
+__global__ void k_scan_bands(const uint32_t* __restrict__ count, uint32_t* __restrict__ off, uint32_t* __restrict__ fill,
+                             uint32_t n)
+{
+    __shared__ uint32_t warp_sums[32];
+    __shared__ uint32_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (uint32_t base = 0; base < n; base += blockDim.x) {
+        const uint32_t i = base + threadIdx.x;
+        const uint32_t v = i < n ? count[i] : 0u;
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) warp_sums[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            uint32_t s = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0u;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+                if (lane >= o) s += y;
+            }
+            warp_sums[lane] = s;
+        }
+        __syncthreads();
+        const uint32_t excl = carry + (wid ? warp_sums[wid - 1] : 0u) + x - v;
+        if (i < n) {
+            off[i] = excl;
+            fill[i] = 0;
+        }
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry = excl + v;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) off[n] = carry;
+}
+
+__global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ recs, const uint32_t* __restrict__ off,
+                             uint32_t* __restrict__ fill, uint32_t* __restrict__ list)
+{
+    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= ev.total_units) return;
+    const int4 r = *reinterpret_cast<const int4*>(&recs[u]);
+    if (r.x < 0) return;
+    const PlaneDesc& P = ev.p[recs[u].plane];
+    for_each_band(P, r.x, r.z, [&](int c) {
+        const uint32_t b = P.band_base + c;
+        list[off[b] + atomicAdd(&fill[b], 1u)] = u;
+    });
+}
+
+// Fluctuation walk, one thread per unit: sample_patch's exact probabilities
+// (rasterize.cpp:101-118) then fluctuate_sequential (rasterize.cpp:124-149)
+// with the reference binomial (rng.cpp:146-193) or the Gaussian approximation
+// (rasterize.cpp:159-170); counts scattered with float atomics (exact while
+// a cell holds < 2^24 electrons, so the grid is order independent).
+__global__ void k_fluctuate(const EventDesc ev, const UnitRec* __restrict__ recs, const uint32_t* __restrict__ pool,
+                            const uint32_t* __restrict__ order)
+{
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ev.total_units) return;
+    const uint32_t u = order ? order[i] : i;
+    const UnitRec rec = recs[u];
+    if (rec.w0 < 0) return;
+    const PlaneDesc& P = ev.p[rec.plane];
+    const ws_depo d = P.depos[u - P.unit_base];
+    const double* wv = reinterpret_cast<const double*>(pool + rec.pool);
+    const double* tv = wv + rec.n_w;
+    const int n_w = rec.n_w, n_t = rec.n_t;
+    double total = 0.0;
+    for (int w = 0; w < n_w; ++w) {
+        const double pw = wv[w];
+        for (int t = 0; t < n_t; ++t) total += pw * tv[t];
+    }
+    const double norm = 1.0 / total;
+    Rng src;
+    src.init(ev.rng_mode, ev.seed, (uint64_t)d.id);
+    float* grid = P.charge_out;
+    const int N = P.N;
+    int64_t remaining = d.q;
+    double p_rem = 1.0;
+    const int last = n_w * n_t - 1;
+    for (int b = 0; b < last; ++b) {
+        if (remaining == 0) break;
+        const int w = b / n_t, t = b - w * n_t;
+        const double pi = (wv[w] * tv[t]) * norm;
+        double p = 1.0;
+        if (p_rem > 0.0) {
+            p = pi / p_rem;
+            p = p < 0.0 ? 0.0 : (p > 1.0 ? 1.0 : p);
+        }
+        const int64_t k = ev.approx ? binomial_approx(remaining, p, src) : binomial(remaining, p, src);
+        if (k) atomicAdd(&grid[(size_t)(rec.w0 + w) * N + rec.t0 + t], (float)k);
+        remaining -= k;
+        p_rem -= pi;
+    }
+    if (remaining)
+        atomicAdd(&grid[(size_t)(rec.w0 + n_w - 1) * N + rec.t0 + n_t - 1], (float)remaining);
+}
+
+}  // namespace wsb
+
+extern "C" cudaError_t wsb_launch_sample(const wsb::EventDesc& ev, wsb::UnitRec* recs, uint32_t* pool, uint32_t pool_cap,
+                                         uint32_t* pool_ctr, uint32_t* band_count, unsigned* err, cudaStream_t s)
+{
+    if (ev.total_units == 0) return cudaSuccess;
+    const uint32_t threads = 128;
+    const uint32_t blocks = (ev.total_units + threads - 1) / threads;
+    wsb::k_sample<<<blocks, threads, 0, s>>>(ev, recs, pool, pool_cap, pool_ctr, band_count, err);
+    return cudaGetLastError();
+}
+
+extern "C" cudaError_t wsb_launch_scan(const uint32_t* count, uint32_t* off, uint32_t* fill, uint32_t n, cudaStream_t s)
+{
+    wsb::k_scan_bands<<<1, 1024, 0, s>>>(count, off, fill, n);
+    return cudaGetLastError();
+}
+
+extern "C" cudaError_t wsb_launch_fill(const wsb::EventDesc& ev, const wsb::UnitRec* recs, const uint32_t* off,
+                                       uint32_t* fill, uint32_t* list, cudaStream_t s)
+{
+    if (ev.total_units == 0) return cudaSuccess;
+    wsb::k_fill_bands<<<(ev.total_units + 255) / 256, 256, 0, s>>>(ev, recs, off, fill, list);
+    return cudaGetLastError();
+}
+
+extern "C" cudaError_t wsb_launch_fluctuate(const wsb::EventDesc& ev, const wsb::UnitRec* recs, const uint32_t* pool,
+                                            const uint32_t* order, cudaStream_t s)
+{
+    if (ev.total_units == 0) return cudaSuccess;
+    wsb::k_fluctuate<<<(ev.total_units + 127) / 128, 128, 0, s>>>(ev, recs, pool, order);
+    return cudaGetLastError();
+}

@@ -1,0 +1,174 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle (wsoracle.c,
+itself pinned bit-for-bit to the unmodified reference in test_oracle.py).
+
+Tolerances (BASELINE.json north_star): per-channel relative L2 <= 1e-5 on the
+frame, total charge conserved to 1e-6 relative (fluctuation off, fp32);
+fluctuation on: the integer charge grid is identical, the frame within 1e-5.
+"""
+import numpy as np
+import pytest
+
+from paper_2104_08265_b200 import GridSpec, Plane, ResponseParams, SimConfig, RngConfig, DriftParams, WsError
+from paper_2104_08265_b200 import gen_depos, simulate_event
+from paper_2104_08265_b200.workloads import line_tracks
+from oracle.oracle import Drift
+
+from .helpers import oracle_grid, oracle_response, relL2_per_channel
+
+pytestmark = pytest.mark.gpu
+
+TOL_FRAME = 1e-5
+TOL_CHARGE = 1e-6
+
+SMALL = GridSpec(n_wires=96, n_ticks=900, pad_wires=20, pad_ticks=100, pitch=5.0, tick=0.5)
+
+
+def _oracle_frame(oracle, grid, resp, s):
+    return oracle.convolve(oracle_grid(grid), oracle_response(resp), s)
+
+
+@pytest.mark.parametrize("kind", ["collection", "induction"])
+@pytest.mark.parametrize("ww", [(1.0,), (0.1, 1.0, 0.1), (-0.05, 0.2, 1.0, 0.2, -0.05)])
+def test_fluct_off_small(ctx, oracle, kind, ww):
+    resp = ResponseParams(plane_kind=kind, wire_weights=ww)
+    depos = line_tracks(600, SMALL, seed=3)
+    cfg = SimConfig(grid=SMALL, response=resp, fluctuate=False)
+    plane = Plane(ctx, SMALL, resp)
+    res = plane.simulate(depos, cfg, want_charge=True)
+    s_ref, clipped = oracle.charge_fluct_off(oracle_grid(SMALL), depos)
+    m_ref = _oracle_frame(oracle, SMALL, resp, s_ref)
+    assert relL2_per_channel(res.charge, s_ref) < 1e-6
+    assert abs(res.charge.astype(np.float64).sum() - s_ref.sum()) <= TOL_CHARGE * s_ref.sum()
+    assert res.timing["clipped_charge"] == clipped
+    assert relL2_per_channel(res.frame, m_ref) < TOL_FRAME
+
+
+def test_c1_fluct_off(ctx, oracle):
+    """configs[0]: 480 x 6000 (padded 680 x 6200, a folded transform), 10k line-track depos."""
+    grid = GridSpec(n_wires=480, n_ticks=6000)
+    for resp in (ResponseParams(plane_kind="collection", shaper_peaking=0.0), ResponseParams()):
+        depos = line_tracks(10_000, grid, seed=1)
+        plane = Plane(ctx, grid, resp)
+        assert plane.info["folded"] == 1
+        res = plane.simulate(depos, SimConfig(grid=grid, response=resp, fluctuate=False), want_charge=True)
+        s_ref, clipped = oracle.charge_fluct_off(oracle_grid(grid), depos)
+        m_ref = _oracle_frame(oracle, grid, resp, s_ref)
+        q_tot = depos["q"].sum() - clipped
+        assert abs(res.charge.astype(np.float64).sum() - q_tot) <= TOL_CHARGE * q_tot
+        assert relL2_per_channel(res.frame, m_ref) < TOL_FRAME
+
+
+@pytest.mark.parametrize("rng_mode", [0, 1])
+def test_c1_fluct_on_exact_charge(ctx, oracle, rng_mode):
+    """Fluctuation on: the integer charge grid equals the reference's exactly
+    (substream = the reference's own xoshiro stream; philox = the shared stream)."""
+    grid = GridSpec(n_wires=480, n_ticks=6000)
+    resp = ResponseParams()
+    og = oracle_grid(grid)
+    depos = gen_depos(10_000, 7, grid)
+    cfg = SimConfig(grid=grid, response=resp, fluctuate=True,
+                    rng=RngConfig(mode="philox" if rng_mode else "substream", seed=12345))
+    res = Plane(ctx, grid, resp).simulate(depos, cfg, want_charge=True)
+    s_ref, clipped = oracle.charge_fluct_on(og, depos, rng_mode=rng_mode, seed=12345)
+    assert np.array_equal(res.charge.astype(np.int64), s_ref)
+    if rng_mode == 0:
+        assert s_ref.sum() == 55_135_105  # survey anchor
+    m_ref = oracle.convolve(og, oracle_response(resp), s_ref.astype(np.float64))
+    assert relL2_per_channel(res.frame, m_ref) < TOL_FRAME
+
+
+def test_fluct_approx_philox(ctx, oracle):
+    depos = line_tracks(800, SMALL, seed=5)
+    resp = ResponseParams()
+    cfg = SimConfig(grid=SMALL, response=resp, fluctuate=True, approx=True, rng=RngConfig(mode="philox", seed=99))
+    res = Plane(ctx, SMALL, resp).simulate(depos, cfg, want_charge=True)
+    s_ref, _ = oracle.charge_fluct_on(oracle_grid(SMALL), depos, rng_mode=1, approx=True, seed=99)
+    # Gaussian-approx draws go through log/cos/sin; CUDA and glibc may differ in
+    # the last ulp, which can move a rounded draw by one electron.
+    diff = np.abs(res.charge.astype(np.int64) - s_ref)
+    assert diff.sum() <= 0.001 * s_ref.sum()
+    assert res.charge.sum() == s_ref.sum()
+
+
+def test_convolve_only(ctx, oracle):
+    grid, resp = SMALL, ResponseParams(plane_kind="induction", wire_weights=(0.2, 1.0, 0.2))
+    rng = np.random.default_rng(0)
+    s = np.zeros((grid.padded_wires(), grid.padded_ticks()), dtype=np.float32)
+    s[30:60, 200:700] = rng.integers(0, 50, size=(30, 500))
+    plane = Plane(ctx, grid, resp)
+    import torch
+    sd = torch.from_numpy(s).cuda()
+    md = torch.empty_like(sd)
+    torch.cuda.synchronize()
+    plane.convolve_device(sd, md)
+    plane.ctx.synchronize()
+    m_ref = _oracle_frame(oracle, grid, resp, s.astype(np.float64))
+    assert relL2_per_channel(md.cpu().numpy(), m_ref) < TOL_FRAME
+
+
+def test_edge_cases(ctx, oracle):
+    grid = GridSpec(n_wires=40, n_ticks=300, pad_wires=10, pad_ticks=100)
+    resp = ResponseParams(wire_weights=(0.3, 1.0, 0.3))
+    plane = Plane(ctx, grid, resp)
+    cfg = SimConfig(grid=grid, response=resp, fluctuate=False)
+    # empty depo set -> all-zero frame
+    res = plane.simulate(np.zeros(0, dtype=gen_depos(1, 1, grid).dtype), cfg, want_charge=True)
+    assert not res.frame.any() and not res.charge.any()
+    # depos at/outside the edges, zero widths, zero charge
+    d = gen_depos(6, 1, grid)
+    d["x"] = [-1e4, 0.0, 199.999, 1.0, 120.0, 60.0]
+    d["t"] = [10.0, 0.0, 149.99, -49.9, 1e5, 75.0]
+    d["sigma_x"][3] = 0.0
+    d["sigma_t"][4] = 0.0
+    d["q"][5] = 0
+    res = plane.simulate(d, cfg, want_charge=True)
+    s_ref, clipped = oracle.charge_fluct_off(oracle_grid(grid), d)
+    assert res.timing["clipped_charge"] == clipped
+    assert relL2_per_channel(res.charge, s_ref) < 1e-6
+    m_ref = _oracle_frame(oracle, grid, resp, s_ref)
+    assert relL2_per_channel(res.frame, m_ref) < TOL_FRAME
+    for cfgf in (SimConfig(grid=grid, response=resp, fluctuate=True),):
+        res = plane.simulate(d, cfgf, want_charge=True)
+        s_on, _ = oracle.charge_fluct_on(oracle_grid(grid), d, rng_mode=0, seed=12345)
+        assert np.array_equal(res.charge.astype(np.int64), s_on)
+
+
+def test_drift(ctx, oracle):
+    grid = SMALL
+    resp = ResponseParams()
+    d = line_tracks(300, grid, seed=9)
+    dp = DriftParams(response_plane_x=0.0, drift_speed=1.6, diffusion_long=0.0068, diffusion_tran=0.0088, enabled=True)
+    cfg = SimConfig(grid=grid, response=resp, fluctuate=False, drift=dp)
+    res = Plane(ctx, grid, resp).simulate(d, cfg, want_charge=True)
+    s_ref, _ = oracle.charge_fluct_off(oracle_grid(grid), d, drift=Drift(0.0, 1.6, 0.0068, 0.0088))
+    assert relL2_per_channel(res.charge, s_ref) < 1e-6
+    # a depo behind the plane is a domain error (rasterize.cpp:25-28)
+    dp2 = DriftParams(response_plane_x=1e4, enabled=True)
+    with pytest.raises(WsError) as e:
+        Plane(ctx, grid, resp).simulate(d, SimConfig(grid=grid, response=resp, fluctuate=False, drift=dp2))
+    assert e.value.code == 3
+
+
+def test_validation_errors(ctx):
+    grid = SMALL
+    with pytest.raises(WsError) as e:
+        Plane(ctx, grid, ResponseParams(wire_weights=(1.0, 1.0)))
+    assert e.value.code == 1 and "odd" in str(e.value)
+    with pytest.raises(WsError) as e:  # kernel support beyond the tick padding (spectral.cpp:147-153)
+        Plane(ctx, GridSpec(n_wires=10, n_ticks=300, pad_wires=5, pad_ticks=20), ResponseParams())
+    assert e.value.code == 1 and "padding" in str(e.value)
+    with pytest.raises(WsError):
+        Plane(ctx, GridSpec(n_wires=0), ResponseParams())
+
+
+def test_event_matches_planes(ctx):
+    grids = [GridSpec(n_wires=120, n_ticks=800, pad_wires=20, pad_ticks=100),
+             GridSpec(n_wires=200, n_ticks=800, pad_wires=20, pad_ticks=100)]
+    resps = [ResponseParams(plane_kind="induction"), ResponseParams()]
+    planes = [Plane(ctx, g, r) for g, r in zip(grids, resps)]
+    depos = [line_tracks(500, g, seed=11 + i) for i, g in enumerate(grids)]
+    cfg = SimConfig(fluctuate=False)
+    frames, _ = simulate_event(ctx, planes, depos, cfg)
+    for p, d, f in zip(planes, depos, frames):
+        single = p.simulate(d, cfg).frame
+        np.testing.assert_array_equal(single, f)  # fixed-point scatter: bitwise reproducible
