@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""Benchmark of the Wire-Cell signal-simulation hot path (raster + scatter + FFT-conv).
+
+Metric (BASELINE.json): depositions/s (and events/s) for raster + scatter +
+FFT-convolution on a MicroBooNE-scale event (configs[1]): 100k depositions on
+straight 3D tracks projected onto U/V (induction, 2400 wires) and W
+(collection, 3456 wires) planes x 9600 ticks, pad 100/100, pitch 3 mm, tick
+0.5 us, fluctuation off, field + electronics response. One step = one event.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs under torchrun, one rank per GPU, weak scaling: every rank
+simulates its own events (independent event shards, no data-path collective);
+value = all ranks' depositions / max-over-ranks device time.
+
+Timing: CUDA events on the library's stream around exactly K steps, barrier +
+synchronize on both sides, max over ranks. Inputs rotate over 10 distinct
+pre-generated events (144 MB of depos > 126 MB L2). `e2e` repeats the
+measurement through the host-buffer API (ws_simulate_event): pinned depos
+H2D and the three frames D2H inside the timed region.
+
+--impl reference times the reference's own CPU implementation (the
+unmodified library compiled into oracle/_ref) on the host cores, one plane of
+the event per step (rotating U, V, W), response kernels built once outside
+the timed region; events/s = 1 / (3 x mean plane time).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N_DEPOS = 100_000
+N_EVENTS_ROTATE = 10
+WORKLOAD = "microboone_event: 100k depos, U/V/W 2400/2400/3456 wires x 9600 ticks, pad 100/100, fluct off"
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """SM clocks and throttle reasons sampled through NVML every ~2 ms while the
+    timed region runs (nvidia-smi's 100 ms floor would miss short regions)."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self.stop = threading.Event()
+        self.nvml = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self._sample()
+            self.thread = threading.Thread(target=self._run, daemon=True)
+            self.thread.start()
+        except Exception:  # no NVML: report unsampled
+            self.nvml = None
+        return self
+
+    def _sample(self):
+        p = self.nvml
+        sm = p.nvmlDeviceGetClockInfo(self.h, p.NVML_CLOCK_SM)
+        try:
+            r = p.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:
+            r = p.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+        self.samples.append((sm, r))
+
+    def _run(self):
+        while not self.stop.is_set():
+            try:
+                self._sample()
+            except Exception:
+                break
+            time.sleep(0.002)
+
+    def __exit__(self, *a):
+        self.stop.set()
+        if self.nvml:
+            self.thread.join(timeout=1)
+            try:
+                self._sample()
+            except Exception:
+                pass
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [s for s, _ in self.samples]
+        reasons = sorted({n for _, r in self.samples for n, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max_sm, "reasons": reasons,
+                "samples": len(self.samples), "source": "nvml"}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def make_events(rank: int):
+    from paper_2104_08265_b200.workloads import microboone_event
+    return [microboone_event(N_DEPOS, seed=1000 * rank + e + 1) for e in range(N_EVENTS_ROTATE)]
+
+
+def cpu_reference_plane_times(events, planes_idx, workers, max_steps=None, warmup=0):
+    """Time the unmodified reference (oracle/_ref) fluctuation-off path, one plane per step."""
+    from oracle.oracle import Reference, build_ref, make_grid, make_response, ref_available
+    from paper_2104_08265_b200.workloads import microboone_grids
+    if not ref_available():
+        build_ref()
+    ref = Reference()
+    grids, resps = microboone_grids()
+    out = []
+    for step, pi in enumerate(planes_idx):
+        g, r = grids[pi], resps[pi]
+        og = make_grid(g.n_wires, g.n_ticks, g.pad_wires, g.pad_ticks, g.pitch, g.tick)
+        orr = make_response(r.plane_kind, r.field_sigma_t, r.shaper_peaking, r.shaper_order, r.gain)
+        depos = events[step % len(events)][pi]
+        t = ref.time_fluct_off(og, orr, depos, workers=workers)
+        out.append(dict(plane=pi, sample_s=t["sample_s"], scatter_s=t["scatter_s"], convolve_s=t["convolve_s"],
+                        build_response_s=t["build_response_s"]))
+    return out
+
+
+def run_reference_arm(args, world, rank):
+    if rank != 0:
+        return
+    from paper_2104_08265_b200.workloads import microboone_event
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    ev = [microboone_event(N_DEPOS, seed=1)]
+    seq = [(i % 3) for i in range(args.warmup + args.steps)]
+    t = cpu_reference_plane_times(ev, seq, cores)
+    timed = t[args.warmup:]
+    plane_s = [x["sample_s"] + x["scatter_s"] + x["convolve_s"] for x in timed]
+    mean_plane = sum(plane_s) / len(plane_s)
+    ev_s = 3 * mean_plane
+    value = N_DEPOS / ev_s
+    line = {
+        "impl": "reference", "metric": "depositions_per_sec", "value": value, "unit": "depos/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_plane * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic line tracks",
+        "config": {"workload": WORKLOAD, "events_per_sec": 1.0 / ev_s, "step": "one plane (U,V,W rotating)",
+                   "workers": cores},
+        "cpu_baseline": {"value": value, "unit": "depos/s", "cores": cores, "kind": "reference",
+                         "sample": "one plane per step rotating U/V/W of a 100k-depo event; build_response cached"},
+        "e2e": {"value": value, "unit": "depos/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world, rank, local = dist_setup()
+
+    if args.impl == "reference":
+        run_reference_arm(args, world, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2104_08265_b200 import Context, Plane, SimConfig, simulate_event, simulate_event_device
+    from paper_2104_08265_b200._lib import TimingC
+    from paper_2104_08265_b200.workloads import microboone_grids
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ctx = Context(local)
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    grids, resps = microboone_grids()
+    planes = [Plane(ctx, g, r) for g, r in zip(grids, resps)]
+    cfg = SimConfig(fluctuate=False)
+    events = make_events(rank)
+    dev_events = [[torch.from_numpy(d.view(np.uint8)).cuda() for d in ev] for ev in events]
+    n_dep = [[len(d) for d in ev] for ev in events]
+    frames = [torch.empty(p.shape, dtype=torch.float32, device="cuda") for p in planes]
+    cells = sum(p.shape[0] * p.shape[1] for p in planes)
+    torch.cuda.synchronize()
+
+    def step(i, timing=None):
+        e = i % N_EVENTS_ROTATE
+        simulate_event_device(ctx, planes, dev_events[e], n_dep[e], cfg, frames, timing=timing)
+
+    # warmup (also sizes the workspace)
+    for i in range(args.warmup):
+        step(i)
+    ctx.synchronize()
+
+    # per-stage device times (one instrumented pass, outside the timed region)
+    stage = TimingC()
+    step(0, timing=stage)
+    ctx.synchronize()
+
+    launches0 = ctx.launch_count
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        start.record(stream)
+        for i in range(args.steps):
+            step(i)
+        end.record(stream)
+        ctx.synchronize()
+        torch.cuda.synchronize()
+    barrier()
+    gpu_launches = ctx.launch_count - launches0
+    ms = start.elapsed_time(end)
+    ms = max_over_ranks(ms)
+    ms_per_step = ms / args.steps
+    value = world * N_DEPOS * args.steps / (ms * 1e-3)
+
+    # dominant kernel (k_conv) roofline: SURVEY.md §8(d) K3 algorithmic traffic
+    # 8 B/cell (read S + write M) x cells of the event, over its measured time.
+    conv_ms = max_over_ranks(float(stage.convolve_ms))
+    alg_bytes = 8.0 * cells
+    peak, peak_kind = peaks()
+    achieved = alg_bytes / (conv_ms * 1e-3) / 1e9
+    prof = ROOT / "profiles" / "traffic_k_conv.json"
+    traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch") if prof.exists() else None
+
+    # end-to-end through the host-buffer API (pinned host depos in, frames out)
+    e2e = None
+    if not args.no_e2e:
+        host_dep = [[d for d in ev] for ev in events[:2]]
+        pinned_frames = [torch.empty(p.shape, dtype=torch.float32).pin_memory() for p in planes]
+        fr_np = [f.numpy() for f in pinned_frames]
+        pinned_dep = []
+        for ev in host_dep:
+            row = []
+            for d in ev:
+                t = torch.empty(d.nbytes, dtype=torch.uint8).pin_memory()
+                t.numpy()[:] = d.view(np.uint8)
+                row.append(t.numpy().view(d.dtype))
+            pinned_dep.append(row)
+        for i in range(2):
+            simulate_event(ctx, planes, pinned_dep[i % 2], cfg, frames=fr_np)
+        k_e2e = max(3, min(args.steps, 10))
+        barrier()
+        t0 = time.perf_counter()
+        for i in range(k_e2e):
+            simulate_event(ctx, planes, pinned_dep[i % 2], cfg, frames=fr_np)
+        t1 = time.perf_counter()
+        barrier()
+        e2e_s = max_over_ranks(t1 - t0)
+        e2e = {"value": world * N_DEPOS * k_e2e / e2e_s, "unit": "depos/s",
+               "h2d_bytes_per_step": int(sum(d.nbytes for d in host_dep[0])),
+               "d2h_bytes_per_step": int(sum(f.numel() * 4 for f in pinned_frames)),
+               "steps": k_e2e, "ms_per_step": 1e3 * e2e_s / k_e2e}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = len(os.sched_getaffinity(0))
+        t = cpu_reference_plane_times(events, [0], cores)[0]
+        from paper_2104_08265_b200.workloads import microboone_grids as mg
+        g0 = mg()[0][0]
+        u_cells = g0.padded_wires() * g0.padded_ticks()
+        plane_s = t["sample_s"] + t["scatter_s"] + t["convolve_s"]
+        ev_s = plane_s * cells / u_cells
+        cpu = {"value": N_DEPOS / ev_s, "unit": "depos/s", "cores": cores, "kind": "reference",
+               "sample": f"U plane of one event (100k depos, {g0.padded_wires()}x{g0.padded_ticks()}) through the "
+                         f"unmodified reference at {cores} threads, build_response excluded "
+                         f"({t['build_response_s']:.1f} s); scaled to the event by cell count "
+                         f"(W plane's Bluestein cost not included, i.e. flattering the CPU)",
+               "plane_s": plane_s}
+
+    if rank == 0:
+        line = {
+            "metric": "depositions_per_sec", "value": value, "unit": "depos/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (straight 3D line tracks, fixed seeds)",
+            "config": {"workload": WORKLOAD, "events_per_sec": world * 1e3 / ms_per_step, "depos_per_event": N_DEPOS,
+                       "cells_per_event": cells, "l2": "inputs rotate over 10 distinct events (144 MB > 126 MB L2)",
+                       "parallelism": f"event-sharded x{world}",
+                       "stage_ms": {k: round(getattr(stage, k), 4) for k in
+                                    ("prepare_ms", "bin_ms", "convolve_ms", "total_ms")}},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "k_conv",
+                         "algorithmic_bytes": alg_bytes, "peak_kind": peak_kind},
+            "clocks": clocks.summary(),
+            "gpu_launches": gpu_launches,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -296,8 +296,15 @@ PlaneDesc plane_desc(const ws_plane* p)
     d.M = p->M;
     d.lo_lag = (int)p->lo_lag;
     d.hi_lag = (int)(p->lo_lag + p->n_lags - 1);
-    d.npass = (int)p->radix.size();
-    for (size_t i = 0; i < p->radix.size(); ++i) d.radix[i] = p->radix[i];
+    d.fft.npass = (int)p->radix.size();
+    int ns = 1;
+    for (size_t i = 0; i < p->radix.size(); ++i) {
+        d.fft.radix[i] = p->radix[i];
+        d.fft.ns[i] = ns;
+        d.fft.magic[i] = ns > 1 ? (uint32_t)((0x100000000ULL + ns - 1) / ns) : 0u;
+        d.fft.stride[i] = p->M / (ns * p->radix[i]);
+        ns *= p->radix[i];
+    }
     d.ww = p->d_ww;
     d.H = p->d_H;
     d.tw = p->d_tw;

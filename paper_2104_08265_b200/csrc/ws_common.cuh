@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include "wiresim_gpu.h"
+#include "ws_fft.cuh"
 
 namespace wsb {
 
@@ -45,8 +46,7 @@ struct PlaneDesc {
     int32_t folded;            // circular wrap folded from a length-Np linear transform
     int32_t Np, M;             // real FFT length, complex half length
     int32_t lo_lag, hi_lag;    // combined kernel lags
-    int32_t npass;
-    int32_t radix[kMaxPasses];
+    FftPlanDev fft;            // radix passes of the length-M complex transform
     const double* ww;          // 2h+1 wire weights
     const float2* H;           // M+1 response spectrum bins, pre-scaled by 1/M
     const float2* tw;          // exp(-2 pi i m / M), m < M

@@ -24,7 +24,6 @@
 // S never touches HBM in mode 0: the only DRAM traffic is the frame write
 // (4 B/cell) plus the depo records.
 #include "ws_common.cuh"
-#include "ws_fft.cuh"
 
 namespace wsb {
 
@@ -71,7 +70,7 @@ __device__ __forceinline__ void accumulate_row(const PlaneDesc& P, int w, bool r
         const float* tv = reinterpret_cast<const float*>(pool + off) + n_w + (P.ww_is_one ? 0 : n_w + 2 * h);
         float c = 0.0f;
         for (; j < n_rows; j += W) c += __ldg(&prof[j]);  // a wrap can land twice on a tiny grid
-        c *= kFix;
+        c *= (float)__ldg(&recs[u].a) * kFix;              // q / total, 2^24 fixed point
 #pragma unroll 4
         for (int t = 0; t < n_t; ++t) {
             const long long v = __float2ll_rn(c * __ldg(&tv[t]));
@@ -160,7 +159,7 @@ k_conv(const EventDesc ev, const UnitRec* __restrict__ recs, const uint32_t* __r
         __syncthreads();
         if (!want_frame) continue;
 
-        float2* z = fft_forward<kConvThreads>(bufA, bufB, M, P.npass, P.radix, P.tw);
+        float2* z = fft_forward<kConvThreads>(bufA, bufB, M, P.fft, P.tw);
 
         // untangle -> multiply by H -> re-tangle (conjugated for the inverse)
         for (int k = tid; k <= M / 2; k += kConvThreads) {
@@ -199,7 +198,7 @@ k_conv(const EventDesc ev, const UnitRec* __restrict__ recs, const uint32_t* __r
         __syncthreads();
 
         float2* other = (z == bufA) ? bufB : bufA;
-        const float2* y2 = fft_forward<kConvThreads>(z, other, M, P.npass, P.radix, P.tw);
+        const float2* y2 = fft_forward<kConvThreads>(z, other, M, P.fft, P.tw);
 
         // y[2n] = Re res[n], y[2n+1] = -Im res[n]  (1/M folded into H)
         float* frow = P.frame + (size_t)w * N;

@@ -7,6 +7,7 @@
 // exactly the footprint of the row's int64 accumulator, which they alias).
 #pragma once
 
+#include <cstdint>
 #include <cuda_runtime.h>
 
 namespace wsb {
@@ -178,16 +179,16 @@ struct Dft<7> : DftOdd<7> {};
 // and writes out[(j/Ns)*Ns*R + k + r*Ns]. One barrier per pass.
 template <int R, int NT>
 __device__ __forceinline__ void stockham_pass(const float2* __restrict__ in, float2* __restrict__ out, int M, int Ns,
-                                              const float2* __restrict__ tw)
+                                              uint32_t ns_magic, int stride, const float2* __restrict__ tw)
 {
     const int nb = M / R;
-    const int stride = M / (Ns * R);
 #pragma unroll 2
     for (int j = threadIdx.x; j < nb; j += NT) {
         float2 v[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) v[r] = in[j + r * nb];
-        const int k = j % Ns;
+        // k = j mod Ns via a multiply-high (exact for j, Ns < 2^16)
+        const int k = Ns > 1 ? j - Ns * (int)__umulhi((uint32_t)j, ns_magic) : 0;
         if (Ns > 1) {
             const float2 w1 = __ldg(&tw[k * stride]);
             float2 w = w1;
@@ -205,25 +206,35 @@ __device__ __forceinline__ void stockham_pass(const float2* __restrict__ in, flo
     __syncthreads();
 }
 
-// Forward FFT of length M = prod(radix[0..npass)) from buffer a, ping-ponging
-// with buffer b. Returns the buffer holding the (natural-order) result.
+// Per-pass plan: radix, Ns = product of earlier radices, magic = ceil(2^32/Ns),
+// twiddle stride = M / (Ns * R). Built on the host (ws_api.cu).
+struct FftPlanDev {
+    int npass;
+    int radix[12];
+    int ns[12];
+    uint32_t magic[12];
+    int stride[12];
+};
+
+// Forward FFT of length M from buffer a, ping-ponging with buffer b. Returns
+// the buffer holding the (natural-order) result.
 template <int NT>
-__device__ __forceinline__ float2* fft_forward(float2* a, float2* b, int M, int npass, const int* radix,
+__device__ __forceinline__ float2* fft_forward(float2* a, float2* b, int M, const FftPlanDev& plan,
                                                const float2* __restrict__ tw)
 {
-    int Ns = 1;
 #pragma unroll 1
-    for (int p = 0; p < npass; ++p) {
-        const int R = radix[p];
-        switch (R) {
-            case 2: stockham_pass<2, NT>(a, b, M, Ns, tw); break;
-            case 3: stockham_pass<3, NT>(a, b, M, Ns, tw); break;
-            case 4: stockham_pass<4, NT>(a, b, M, Ns, tw); break;
-            case 5: stockham_pass<5, NT>(a, b, M, Ns, tw); break;
-            case 7: stockham_pass<7, NT>(a, b, M, Ns, tw); break;
-            default: stockham_pass<8, NT>(a, b, M, Ns, tw); break;
+    for (int p = 0; p < plan.npass; ++p) {
+        const int Ns = plan.ns[p];
+        const uint32_t mg = plan.magic[p];
+        const int st = plan.stride[p];
+        switch (plan.radix[p]) {
+            case 2: stockham_pass<2, NT>(a, b, M, Ns, mg, st, tw); break;
+            case 3: stockham_pass<3, NT>(a, b, M, Ns, mg, st, tw); break;
+            case 4: stockham_pass<4, NT>(a, b, M, Ns, mg, st, tw); break;
+            case 5: stockham_pass<5, NT>(a, b, M, Ns, mg, st, tw); break;
+            case 7: stockham_pass<7, NT>(a, b, M, Ns, mg, st, tw); break;
+            default: stockham_pass<8, NT>(a, b, M, Ns, mg, st, tw); break;
         }
-        Ns *= R;
         float2* t = a;
         a = b;
         b = t;

@@ -129,8 +129,8 @@ __device__ __forceinline__ void for_each_band(const PlaneDesc& P, int w0, int n_
 // Pool layout per unit (32-bit words):
 //   fluctuation on : [wv f64 x n_w][tv f64 x n_t]                 (8-byte aligned)
 //   fluctuation off: [raw f32 x n_w][eff f32 x n_eff][tv f32 x n_t]
-// with raw = q/total * wv (the un-stencilled wire profile), eff = the profile
-// after the cross-wire stencil (absent when wire_weights == {1}), and
+// with raw = wv (the un-stencilled wire profile), eff = the profile after the
+// cross-wire stencil (absent when wire_weights == {1}); rec.a = q / total with
 // total = sum_w wv * sum_t tv.
 __global__ void k_sample(const EventDesc ev, UnitRec* __restrict__ recs, uint32_t* __restrict__ pool, uint32_t pool_cap,
                          uint32_t* __restrict__ pool_ctr, uint32_t* __restrict__ band_count, unsigned* __restrict__ err)
@@ -193,9 +193,10 @@ __global__ void k_sample(const EventDesc ev, UnitRec* __restrict__ recs, uint32_
         return;
     }
     if (!ev.fluctuate) {
+        // S = q * p = a * wv[w] * tv[t] with a = q / total; a is applied by
+        // the consumer (k_conv), so the profiles are stored unscaled
         const double a = (double)d.q / (sw * st);
         float* raw = reinterpret_cast<float*>(pool + off);
-        for (int i = 0; i < f.n_w; ++i) raw[i] = (float)((double)raw[i] * a);
         if (n_eff) {
             float* eff = raw + f.n_w;
             for (int j = 0; j < n_eff; ++j) {

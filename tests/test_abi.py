@@ -1,0 +1,62 @@
+"""C-ABI boundary checks that need no GPU: the in-tree library loads, exports
+every entry point include/*.h declares, and refuses to compute without a
+device (no CPU fallback)."""
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2104_08265_b200 import _lib
+from paper_2104_08265_b200.api import GridSpec, gen_depos
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def declared_functions():
+    names = set()
+    for h in (ROOT / "include").glob("*.h"):
+        text = re.sub(r"/\*.*?\*/", "", h.read_text(), flags=re.S)
+        for m in re.finditer(r"^\s*(?:const\s+)?[A-Za-z_][\w\s\*]*?\b(ws_\w+)\s*\(", text, flags=re.M):
+            names.add(m.group(1))
+    return names
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for must in ("ws_ctx_create", "ws_plane_create", "ws_simulate_plane", "ws_simulate_event", "ws_convolve_device",
+                 "ws_rasterize_device", "ws_last_error"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+    assert set(_lib.SIGNATURES) <= declared_functions()
+    assert lib.ws_abi_version() == 1
+
+
+def test_struct_layouts_match_reference():
+    import ctypes as C
+    assert _lib.DEPO_DTYPE.itemsize == 48  # wiresim::Depo, core.hpp:63-70
+    assert C.sizeof(_lib.GridSpecC) == 64
+    assert C.sizeof(_lib.SimOptionsC) == 24 + 40
+
+
+def test_no_cpu_fallback_without_device():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    from paper_2104_08265_b200 import Context, WsError
+    with pytest.raises(WsError) as e:
+        Context(0)
+    assert e.value.code == _lib.WS_ECUDA
+
+
+def test_host_generator_matches_reference_gen_depos(ref):
+    g = GridSpec(n_wires=480, n_ticks=6000)
+    from oracle.oracle import make_grid
+    ours = gen_depos(2000, 7, g)
+    theirs = ref.gen_depos(2000, 7, make_grid(480, 6000))
+    assert ours.tobytes() == theirs.tobytes()
