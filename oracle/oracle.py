@@ -268,6 +268,11 @@ class Reference:
                                          C.c_double, C.c_double, C.c_int, C.c_void_p, C.c_void_p, C.c_int]
         L.wsr_time_fluct_off.argtypes = [G, R, C.c_void_p, C.c_uint64, C.c_double, C.c_int, C.c_void_p,
                                          C.c_void_p]
+        L.wsr_plane_create.restype = C.c_void_p
+        L.wsr_plane_create.argtypes = [G, R, C.POINTER(C.c_double)]
+        L.wsr_plane_destroy.argtypes = [C.c_void_p]
+        L.wsr_plane_time_fluct_off.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_double, C.c_int, C.c_void_p,
+                                               C.c_void_p]
 
     def _check(self, rc):
         if rc:
@@ -390,6 +395,14 @@ class Reference:
                                                 _p(noisy), _p(a), workers))
         return noisy, a
 
+    def plane(self, g, r):
+        """Cached response kernel for repeated timing (RefPlane)."""
+        b = C.c_double()
+        h = self.lib.wsr_plane_create(C.byref(g), C.byref(r), C.byref(b))
+        if not h:
+            raise OracleError(self.lib.wsr_last_error().decode())
+        return RefPlane(self, h, padded(g), b.value)
+
     def time_fluct_off(self, g, r, depos, n_sigma=3.0, workers=1, want_m=False):
         d = np.ascontiguousarray(depos, dtype=DEPO_DTYPE)
         W, T = padded(g)
@@ -398,3 +411,22 @@ class Reference:
         self._check(self.lib.wsr_time_fluct_off(C.byref(g), C.byref(r), _p(d), len(d), n_sigma, workers, _p(m),
                                                 _p(times)))
         return dict(sample_s=times[0], scatter_s=times[1], convolve_s=times[2], build_response_s=times[3], m=m)
+
+
+class RefPlane:
+    def __init__(self, ref, handle, shape, build_s):
+        self.ref, self.handle, self.shape, self.build_s = ref, handle, shape, build_s
+
+    def time_fluct_off(self, depos, n_sigma=3.0, workers=1, want_m=False):
+        d = np.ascontiguousarray(depos, dtype=DEPO_DTYPE)
+        m = np.zeros(self.shape, dtype=np.float64) if want_m else None
+        times = np.zeros(3, dtype=np.float64)
+        self.ref._check(self.ref.lib.wsr_plane_time_fluct_off(self.handle, _p(d), len(d), n_sigma, workers, _p(m),
+                                                              _p(times)))
+        return dict(sample_s=times[0], scatter_s=times[1], convolve_s=times[2], m=m)
+
+    def __del__(self):
+        try:
+            self.ref.lib.wsr_plane_destroy(self.handle)
+        except Exception:
+            pass

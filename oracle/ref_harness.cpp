@@ -446,18 +446,41 @@ int wsr_noise_digitize(const wsr_grid* g, const double* m, int noise_mode, doubl
 //   sample  : sample_patch per depo, parallel_for over depos (as rasterize_range, pipeline.cpp:328-331)
 //   scatter : fp64 q*p accumulation, wire-banded ownership (as scatter_banded, scatter.cpp:42-59)
 //   convolve: fft_2d fwd (workers) * R * fft_2d inv (workers), real part (spectral.cpp:155-173)
-// The response kernel is built once per plane outside the timed stages
-// (per-geometry, cacheable; timed separately into times[3]).
-// times = {sample_s, scatter_s, convolve_s, build_response_s}
-int wsr_time_fluct_off(const wsr_grid* g, const wsr_response* r, const Depo* d, std::uint64_t n, double n_sigma,
-                       int workers, double* m_out, double* times)
+// The response kernel is built once per plane (wsr_plane_create, timed into
+// build_s) and reused: it is per-geometry and cacheable.
+struct WsrPlane {
+    GridSpec spec;
+    ResponseKernel kernel;
+    double build_s = 0.0;
+};
+
+void* wsr_plane_create(const wsr_grid* g, const wsr_response* r, double* build_s)
+{
+    WsrPlane* p = nullptr;
+    const int rc = guarded([&] {
+        p = new WsrPlane();
+        p->spec = to_spec(g);
+        const double t0 = now_s();
+        p->kernel = build_response(p->spec, to_resp(r));
+        p->build_s = now_s() - t0;
+    });
+    if (rc) {
+        delete p;
+        return nullptr;
+    }
+    if (build_s) *build_s = p->build_s;
+    return p;
+}
+
+void wsr_plane_destroy(void* p) { delete static_cast<WsrPlane*>(p); }
+
+// times = {sample_s, scatter_s, convolve_s}
+int wsr_plane_time_fluct_off(void* handle, const Depo* d, std::uint64_t n, double n_sigma, int workers, double* m_out,
+                             double* times)
 {
     return guarded([&] {
-        const GridSpec spec = to_spec(g);
-        const double t_r0 = now_s();
-        const ResponseKernel k = build_response(spec, to_resp(r));
-        times[3] = now_s() - t_r0;
-
+        const WsrPlane& P = *static_cast<WsrPlane*>(handle);
+        const GridSpec& spec = P.spec;
         const std::vector<Depo> depos = to_depos(d, n);
         std::vector<SampledPatch> patches(n);
         const double t0 = now_s();
@@ -483,7 +506,7 @@ int wsr_time_fluct_off(const wsr_grid* g, const wsr_response* r, const Depo* d, 
         });
         const double t2 = now_s();
         grid = fft_2d(grid, FftDirection::forward, workers);
-        for (std::size_t i = 0; i < grid.data.size(); ++i) grid.data[i] *= k.values.data[i];
+        for (std::size_t i = 0; i < grid.data.size(); ++i) grid.data[i] *= P.kernel.values.data[i];
         grid = fft_2d(grid, FftDirection::inverse, workers);
         if (m_out)
             for (std::size_t i = 0; i < grid.data.size(); ++i) m_out[i] = grid.data[i].real();
@@ -492,6 +515,17 @@ int wsr_time_fluct_off(const wsr_grid* g, const wsr_response* r, const Depo* d, 
         times[1] = t2 - t1;
         times[2] = t3 - t2;
     });
+}
+
+// One-shot variant (builds the response, timed separately into times[3]).
+int wsr_time_fluct_off(const wsr_grid* g, const wsr_response* r, const Depo* d, std::uint64_t n, double n_sigma,
+                       int workers, double* m_out, double* times)
+{
+    void* p = wsr_plane_create(g, r, &times[3]);
+    if (!p) return 1;
+    const int rc = wsr_plane_time_fluct_off(p, d, n, n_sigma, workers, m_out, times);
+    wsr_plane_destroy(p);
+    return rc;
 }
 
 }  // extern "C"
