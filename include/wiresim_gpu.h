@@ -173,6 +173,15 @@ int ws_simulate_event_device(ws_ctx* ctx, uint32_t n_planes, ws_plane* const* pl
 int ws_simulate_event(ws_ctx* ctx, uint32_t n_planes, ws_plane* const* planes, const ws_depo* const* depos,
                       const uint64_t* n_depos, const ws_sim_options* opt, float* const* frames, ws_timing* timing);
 
+/* A batch of events through the host-buffer path, pipelined: event e is
+ * simulated while the frames of event e-1 stream back to the host on a
+ * second stream (PCIe D2H of the fp32 frames dominates end-to-end time).
+ * depos / n_depos / frames are [n_events * n_planes], event-major. timing
+ * (nullable) describes the first event. Frames should be pinned. */
+int ws_simulate_events(ws_ctx* ctx, uint32_t n_events, uint32_t n_planes, ws_plane* const* planes,
+                       const ws_depo* const* depos, const uint64_t* n_depos, const ws_sim_options* opt,
+                       float* const* frames, ws_timing* timing);
+
 /* Pinned host memory for the host-buffer entry points (cudaMallocHost). */
 int ws_host_alloc(uint64_t bytes, void** out);
 int ws_host_free(void* p);

@@ -18,4 +18,5 @@ from .api import (  # noqa: F401
     run_simulation,
     simulate_event,
     simulate_event_device,
+    simulate_events,
 )

@@ -92,7 +92,9 @@ SIGNATURES = {
     "ws_simulate_event_device": (C.c_int, [_P, C.c_uint32, _P, _P, _P, C.POINTER(SimOptionsC), _P,
                                            C.POINTER(TimingC)]),
     "ws_simulate_event": (C.c_int, [_P, C.c_uint32, _P, _P, _P, C.POINTER(SimOptionsC), _P, C.POINTER(TimingC)]),
-    "ws_gen_depos_uniform": (C.c_int, [C.c_uint64, C.c_uint64, C.POINTER(GridSpecC), _P, _P]),
+    "ws_simulate_events": (C.c_int, [_P, C.c_uint32, C.c_uint32, _P, _P, _P, C.POINTER(SimOptionsC), _P,
+                                     C.POINTER(TimingC)]),
+    "ws_gen_depos_uniform":(C.c_int, [C.c_uint64, C.c_uint64, C.POINTER(GridSpecC), _P, _P]),
     "ws_host_alloc": (C.c_int, [C.c_uint64, C.POINTER(_P)]),
     "ws_host_free": (C.c_int, [_P]),
 }

@@ -230,6 +230,27 @@ def simulate_event(ctx: Context, planes: Sequence[Plane], depos: Sequence, confi
     return frames, t.as_dict()
 
 
+def simulate_events(ctx: Context, planes: Sequence[Plane], events: Sequence[Sequence], config: SimConfig,
+                    frames: Sequence[Sequence[np.ndarray]] | None = None):
+    """A batch of events (each a per-plane list of depo arrays) through the
+    pipelined host-buffer path (ws_simulate_events). Returns frames[e][p]."""
+    n_ev, n_pl = len(events), len(planes)
+    ds = [as_depos(d) for ev in events for d in ev]
+    if frames is None:
+        frames = [[np.empty(p.shape, dtype=np.float32) for p in planes] for _ in range(n_ev)]
+    flat = [f for ev in frames for f in ev]
+    PArr = C.c_void_p * n_pl
+    parr = PArr(*[p.handle.value for p in planes])
+    DArr = C.c_void_p * (n_ev * n_pl)
+    darr = DArr(*[d.ctypes.data for d in ds])
+    narr = (C.c_uint64 * (n_ev * n_pl))(*[len(d) for d in ds])
+    farr = DArr(*[f.ctypes.data for f in flat])
+    t = _lib.TimingC()
+    opt = config.options()
+    check(ctx.lib.ws_simulate_events(ctx.handle, n_ev, n_pl, parr, darr, narr, C.byref(opt), farr, C.byref(t)))
+    return frames, t.as_dict()
+
+
 def simulate_event_device(ctx: Context, planes: Sequence[Plane], depos_dev: Sequence, n_depos: Sequence[int],
                           config: SimConfig, frames_dev: Sequence, timing=None):
     n = len(planes)

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <functional>
 #include <vector>
 
 #include "ws_common.cuh"
@@ -117,6 +118,9 @@ struct ws_ctx {
     std::vector<cudaEvent_t> event_pool;
     size_t pool_hint = 0;
     int sm_count = 0;
+    cudaStream_t copy_stream = nullptr;          // D2H of the pipelined batch path
+    cudaEvent_t slot_computed[2] = {nullptr, nullptr};
+    cudaEvent_t slot_copied[2] = {nullptr, nullptr};
 };
 
 struct ws_plane {
@@ -127,6 +131,7 @@ struct ws_plane {
     long lo_lag = 0, n_lags = 0, support_ticks = 0, support_wires = 0;
     std::vector<double> kernel;  // combined time-domain kernel
     std::vector<int> radix;
+    wsb::FftPlanDev plan{};
     double* d_ww = nullptr;
     float2* d_H = nullptr;
     float2* d_tw = nullptr;
@@ -254,16 +259,30 @@ bool smooth7(long n)
     return n == 1;
 }
 
+// Pass plan for the length-m complex transform: the factorisation into
+// in-register radices with the fewest shared-memory passes, then the smallest
+// largest radix (register pressure), searched exhaustively (m is 7-smooth).
 std::vector<int> plan_radices(int m)
 {
-    std::vector<int> r;
-    while (m % 8 == 0) { r.push_back(8); m /= 8; }
-    while (m % 4 == 0) { r.push_back(4); m /= 4; }
-    while (m % 2 == 0) { r.push_back(2); m /= 2; }
-    while (m % 7 == 0) { r.push_back(7); m /= 7; }
-    while (m % 5 == 0) { r.push_back(5); m /= 5; }
-    while (m % 3 == 0) { r.push_back(3); m /= 3; }
-    return r;
+    static const int kRadices[] = {25, 24, 20, 16, 14, 10, 8, 7, 5, 4, 3, 2};
+    std::vector<int> best, cur;
+    std::function<void(int)> dfs = [&](int rem) {
+        if (rem == 1) {
+            const int mx = cur.empty() ? 0 : *std::max_element(cur.begin(), cur.end());
+            const int bmx = best.empty() ? 1 << 30 : *std::max_element(best.begin(), best.end());
+            if (best.empty() || cur.size() < best.size() || (cur.size() == best.size() && mx < bmx)) best = cur;
+            return;
+        }
+        if (!best.empty() && cur.size() + 1 > best.size()) return;
+        for (int r : kRadices)
+            if (rem % r == 0 && (cur.empty() || r <= cur.back())) {  // non-increasing: one order per multiset
+                cur.push_back(r);
+                dfs(rem / r);
+                cur.pop_back();
+            }
+    };
+    dfs(m);
+    return best;
 }
 
 int validate_grid(const ws_grid_spec* g)
@@ -296,15 +315,7 @@ PlaneDesc plane_desc(const ws_plane* p)
     d.M = p->M;
     d.lo_lag = (int)p->lo_lag;
     d.hi_lag = (int)(p->lo_lag + p->n_lags - 1);
-    d.fft.npass = (int)p->radix.size();
-    int ns = 1;
-    for (size_t i = 0; i < p->radix.size(); ++i) {
-        d.fft.radix[i] = p->radix[i];
-        d.fft.ns[i] = ns;
-        d.fft.magic[i] = ns > 1 ? (uint32_t)((0x100000000ULL + ns - 1) / ns) : 0u;
-        d.fft.stride[i] = p->M / (ns * p->radix[i]);
-        ns *= p->radix[i];
-    }
+    d.fft = p->plan;
     d.ww = p->d_ww;
     d.H = p->d_H;
     d.tw = p->d_tw;
@@ -548,6 +559,14 @@ int ws_ctx_destroy(ws_ctx* c)
         for (cudaEvent_t e : pc.ev) cudaEventDestroy(e);
     for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
     if (c->host_slots) cudaFreeHost(c->host_slots);
+    if (c->copy_stream) {
+        cudaStreamSynchronize(c->copy_stream);
+        cudaStreamDestroy(c->copy_stream);
+    }
+    for (int s = 0; s < 2; ++s) {
+        if (c->slot_computed[s]) cudaEventDestroy(c->slot_computed[s]);
+        if (c->slot_copied[s]) cudaEventDestroy(c->slot_copied[s]);
+    }
     if (c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
     return WS_OK;
@@ -629,7 +648,30 @@ int ws_plane_create(ws_ctx* ctx, const ws_grid_spec* grid, const ws_response* re
         cs[m] = std::cos(a);
         sn[m] = std::sin(a);
     }
-    std::vector<float2> H(M + 1), tw(M), rtw(M / 2 + 1);
+    // pass plan + per-pass twiddle tables W_{Ns R}^{k r}, layout [r-1][k]
+    std::vector<float2> tw;
+    {
+        wsb::FftPlanDev& pl = p->plan;
+        pl = wsb::FftPlanDev{};
+        pl.npass = (int)p->radix.size();
+        int ns = 1;
+        for (int i = 0; i < pl.npass; ++i) {
+            const int R = p->radix[i];
+            pl.radix[i] = R;
+            pl.ns[i] = ns;
+            pl.magic[i] = ns > 1 ? (uint32_t)((0x100000000ULL + ns - 1) / ns) : 0u;
+            pl.tw_off[i] = (int)tw.size();
+            const long step = 2L * (M / (ns * R));  // index step on the Np grid
+            for (int r = 1; r < R && ns > 1; ++r)
+                for (int k = 0; k < ns; ++k) {
+                    const long idx = (step * k * r) % Np;
+                    tw.push_back(make_float2((float)cs[idx], (float)sn[idx]));
+                }
+            ns *= R;
+        }
+        if (tw.empty()) tw.push_back(make_float2(1.f, 0.f));
+    }
+    std::vector<float2> H(M + 1), rtw(M / 2 + 1);
     for (int k = 0; k <= M; ++k) {
         double re = 0.0, im = 0.0;
         for (long i = 0; i < p->n_lags; ++i) {
@@ -641,16 +683,15 @@ int ws_plane_create(ws_ctx* ctx, const ws_grid_spec* grid, const ws_response* re
         }
         H[k] = make_float2((float)(re / M), (float)(im / M));
     }
-    for (int m = 0; m < M; ++m) tw[m] = make_float2((float)cs[2 * m], (float)sn[2 * m]);
     for (int k = 0; k <= M / 2; ++k) rtw[k] = make_float2((float)cs[k], (float)sn[k]);
     std::vector<double> ww(response->wire_weights, response->wire_weights + response->n_wire_weights);
     cudaError_t e = cudaSuccess;
     e = e ? e : cudaMalloc(&p->d_H, sizeof(float2) * (M + 1));
-    e = e ? e : cudaMalloc(&p->d_tw, sizeof(float2) * M);
+    e = e ? e : cudaMalloc(&p->d_tw, sizeof(float2) * tw.size());
     e = e ? e : cudaMalloc(&p->d_rtw, sizeof(float2) * (M / 2 + 1));
     e = e ? e : cudaMalloc(&p->d_ww, sizeof(double) * ww.size());
     e = e ? e : cudaMemcpy(p->d_H, H.data(), sizeof(float2) * (M + 1), cudaMemcpyHostToDevice);
-    e = e ? e : cudaMemcpy(p->d_tw, tw.data(), sizeof(float2) * M, cudaMemcpyHostToDevice);
+    e = e ? e : cudaMemcpy(p->d_tw, tw.data(), sizeof(float2) * tw.size(), cudaMemcpyHostToDevice);
     e = e ? e : cudaMemcpy(p->d_rtw, rtw.data(), sizeof(float2) * (M / 2 + 1), cudaMemcpyHostToDevice);
     e = e ? e : cudaMemcpy(p->d_ww, ww.data(), sizeof(double) * ww.size(), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
@@ -818,6 +859,75 @@ int ws_simulate_event(ws_ctx* ctx, uint32_t n_planes, ws_plane* const* planes, c
     }
     WS_CUDA(cudaStreamSynchronize(ctx->stream));
     return WS_OK;
+}
+
+int ws_simulate_events(ws_ctx* ctx, uint32_t n_events, uint32_t n_planes, ws_plane* const* planes,
+                       const ws_depo* const* depos, const uint64_t* n_depos, const ws_sim_options* opt,
+                       float* const* frames, ws_timing* timing)
+{
+    if (int rc = check_plane_set(ctx, n_planes, planes)) return rc;
+    if (int rc = check_opts(opt)) return rc;
+    if (n_events == 0 || n_planes == 0) return WS_OK;
+    if (!depos || !n_depos || !frames) return set_err(WS_EINVAL, "null argument");
+    WS_CUDA(cudaSetDevice(ctx->device));
+    if (int rc = finish_pending(ctx)) return rc;
+    if (!ctx->copy_stream) WS_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    for (int s = 0; s < 2; ++s) {
+        if (!ctx->slot_computed[s]) WS_CUDA(cudaEventCreateWithFlags(&ctx->slot_computed[s], cudaEventDisableTiming));
+        if (!ctx->slot_copied[s]) WS_CUDA(cudaEventCreateWithFlags(&ctx->slot_copied[s], cudaEventDisableTiming));
+    }
+    size_t cells = 0, max_units = 0;
+    for (uint32_t i = 0; i < n_planes; ++i) cells += (size_t)planes[i]->W * planes[i]->N;
+    for (uint32_t e = 0; e < n_events; ++e) {
+        size_t u = 0;
+        for (uint32_t i = 0; i < n_planes; ++i) u += n_depos[(size_t)e * n_planes + i];
+        max_units = std::max(max_units, u);
+    }
+    WS_CUDA(ctx->depos.reserve(2 * max_units + 1));
+    WS_CUDA(ctx->frames.reserve(2 * cells));
+    std::vector<const ws_depo*> dd(n_planes);
+    std::vector<float*> ff(n_planes);
+    // two slots: event e computes into slot e&1 on the compute stream while the
+    // copy stream drains slot (e-1)&1 to the host (H2D is tiny, D2H dominates)
+    for (uint32_t e = 0; e < n_events; ++e) {
+        const int slot = (int)(e & 1u);
+        if (e >= 2) WS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->slot_copied[slot], 0));
+        size_t uo = (size_t)slot * max_units, co = (size_t)slot * cells;
+        for (uint32_t i = 0; i < n_planes; ++i) {
+            const size_t k = (size_t)e * n_planes + i;
+            dd[i] = ctx->depos.p + uo;
+            ff[i] = ctx->frames.p + co;
+            if (n_depos[k])
+                WS_CUDA(cudaMemcpyAsync(ctx->depos.p + uo, depos[k], sizeof(ws_depo) * n_depos[k],
+                                        cudaMemcpyHostToDevice, ctx->stream));
+            uo += n_depos[k];
+            co += (size_t)planes[i]->W * planes[i]->N;
+        }
+        if (int rc = ws_simulate_event_device(ctx, n_planes, planes, dd.data(), n_depos + (size_t)e * n_planes, opt,
+                                              ff.data(), e == 0 ? timing : nullptr))
+            return rc;
+        WS_CUDA(cudaEventRecord(ctx->slot_computed[slot], ctx->stream));
+        WS_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->slot_computed[slot], 0));
+        for (uint32_t i = 0; i < n_planes; ++i) {
+            float* dst = frames[(size_t)e * n_planes + i];
+            const size_t nc = (size_t)planes[i]->W * planes[i]->N;
+            if (dst)
+                WS_CUDA(cudaMemcpyAsync(dst, ff[i], sizeof(float) * nc, cudaMemcpyDeviceToHost, ctx->copy_stream));
+        }
+        WS_CUDA(cudaEventRecord(ctx->slot_copied[slot], ctx->copy_stream));
+    }
+    WS_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+    const int rc = finish_pending(ctx);
+    if (rc == WS_ERANGE) {
+        // workspace grew on overflow: redo the batch event by event (synchronous path retries)
+        for (uint32_t e = 0; e < n_events; ++e)
+            if (int r2 = ws_simulate_event(ctx, n_planes, planes, depos + (size_t)e * n_planes,
+                                           n_depos + (size_t)e * n_planes, opt, frames + (size_t)e * n_planes,
+                                           e == 0 ? timing : nullptr))
+                return r2;
+        return WS_OK;
+    }
+    return rc;
 }
 
 int ws_simulate_plane(ws_plane* p, const ws_depo* depos, uint64_t n, const ws_sim_options* opt, float* frame,

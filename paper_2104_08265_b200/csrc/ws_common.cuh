@@ -17,7 +17,7 @@ namespace wsb {
 constexpr int kMaxPlanes = 8;
 constexpr int kMaxPasses = 12;
 constexpr int kMaxWireWeights = 33;  // 2h+1 <= 33 taps of cross-wire coupling
-constexpr int kConvThreads = 512;
+constexpr int kConvThreads = 256;
 constexpr int kMaxFftHalf = 12288;   // M = N'/2 <= 12288 (N' <= 24576 ticks)
 constexpr double kFixScale = 4294967296.0;          // 2^32: fixed-point electrons
 constexpr double kFixInv = 1.0 / 4294967296.0;

@@ -230,11 +230,25 @@ extern "C" cudaError_t wsb_launch_conv(const wsb::EventDesc& ev, const wsb::Unit
                                        const uint32_t* band_off, const uint32_t* band_list, int flags,
                                        size_t smem_bytes, cudaStream_t stream)
 {
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(wsb::k_conv, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    // once per device: shared-memory opt-in and the composite-radix twiddles
+    static unsigned long long ready = 0;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (!(ready & (1ull << dev))) {
+        e = cudaFuncSetAttribute(wsb::k_conv, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        float2 host[wsb::kCompositeTwiddles] = {};
+        for (int R : {10, 14, 16, 20, 24, 25, 28, 32, 35, 40, 49}) {
+            const int off = wsb::comp_off(R);
+            for (int m = 0; m < R; ++m) {
+                const double a = -6.283185307179586476925286766559 * (double)m / (double)R;
+                host[off + m] = make_float2((float)cos(a), (float)sin(a));
+            }
+        }
+        e = cudaMemcpyToSymbol(wsb::c_wr, host, sizeof(host));
+        if (e != cudaSuccess) return e;
+        ready |= 1ull << dev;
     }
     if (ev.total_bands == 0) return cudaSuccess;
     wsb::k_conv<<<ev.total_bands, wsb::kConvThreads, smem_bytes, stream>>>(ev, recs, pool, band_off, band_list,

@@ -1,10 +1,12 @@
 // Shared-memory mixed-radix Stockham FFT (complex fp32) for one tick row.
 //
 // Replaces the reference's recursive double FFT (fft.cpp:116-161) on the hot
-// path. The transform length M is 7-smooth (radix 2,3,4,5,7,8 passes), planned
-// on the host (ws_api.cu: plan_radices). One CTA transforms one row in place:
-// passes ping-pong between two M-element buffers (16*M bytes of shared memory,
-// exactly the footprint of the row's int64 accumulator, which they alias).
+// path. The transform length M is 7-smooth and planned on the host
+// (ws_api.cu: plan_passes) into few passes of large radices (2..40, composite
+// radices run as two nested small DFTs in registers), so a row needs ~3
+// shared-memory round trips per transform instead of log2(M). Passes
+// ping-pong between two M-element buffers (16*M bytes of shared memory, the
+// footprint of the row's fixed-point accumulator, which they alias).
 #pragma once
 
 #include <cstdint>
@@ -19,6 +21,18 @@ __device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y
 __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
 // multiply by -i
 __device__ __forceinline__ float2 cmul_mi(float2 a) { return make_float2(a.y, -a.x); }
+
+// Twiddles W_R^m = exp(-2 pi i m / R) of the composite in-register DFTs, filled
+// by the host (ws_api.cu). After full unrolling every index is a compile-time
+// constant, so the values become constant-bank operands of the FMAs.
+constexpr int kCompositeTwiddles = 512;
+static __constant__ float2 c_wr[kCompositeTwiddles];
+// offset of W_R^0 in c_wr for composite R (host and device share this map)
+__host__ __device__ constexpr int comp_off(int R)
+{
+    return R == 10 ? 0 : R == 14 ? 10 : R == 16 ? 24 : R == 20 ? 40 : R == 24 ? 60 : R == 25 ? 84 : R == 28 ? 109
+         : R == 32 ? 137 : R == 35 ? 169 : R == 40 ? 204 : R == 49 ? 244 : -1;
+}
 
 // Forward DFT of size R in registers: X_k = sum_n x_n exp(-2 pi i n k / R).
 template <int R>
@@ -52,7 +66,6 @@ struct Dft<8> {
     static __device__ __forceinline__ void run(float2* v)
     {
         constexpr float r = 0.70710678118654752440f;
-        // radix-2 over pairs (n, n+4), then twiddle, then two radix-4
         float2 a[4], b[4];
 #pragma unroll
         for (int n = 0; n < 4; ++n) {
@@ -174,15 +187,84 @@ struct Dft<5> : DftOdd<5> {};
 template <>
 struct Dft<7> : DftOdd<7> {};
 
+// Composite R = A*B in registers (Cooley-Tukey, n = n1 + A n2, k = k2 + B k1):
+// DFT_B over n2 for every n1, twiddle by W_R^{n1 k2}, DFT_A over n1. Works in
+// place: X[k2 + B k1] ends in slot k1 + A k2, exposed through pos().
+template <int A, int B>
+struct DftComp {
+    static __host__ __device__ constexpr int pos(int r) { return (r / B) + A * (r % B); }
+    static __device__ __forceinline__ void run(float2* v)
+    {
+        constexpr int R = A * B;
+        constexpr int off = comp_off(R);
+#pragma unroll
+        for (int n1 = 0; n1 < A; ++n1) {
+            float2 t[B];
+#pragma unroll
+            for (int n2 = 0; n2 < B; ++n2) t[n2] = v[n1 + A * n2];
+            Dft<B>::run(t);
+#pragma unroll
+            for (int k2 = 0; k2 < B; ++k2)
+                v[n1 + A * k2] = (n1 * k2 == 0) ? t[k2] : cmul(t[k2], c_wr[off + (n1 * k2) % R]);
+        }
+#pragma unroll
+        for (int k2 = 0; k2 < B; ++k2) {
+            float2 z[A];
+#pragma unroll
+            for (int n1 = 0; n1 < A; ++n1) z[n1] = v[n1 + A * k2];
+            Dft<A>::run(z);
+#pragma unroll
+            for (int k1 = 0; k1 < A; ++k1) v[k1 + A * k2] = z[k1];
+        }
+    }
+};
+
+// slot of output X[r] after Dft<R>::run (identity unless composite)
+template <int R>
+struct DftPos {
+    static __host__ __device__ constexpr int pos(int r) { return r; }
+};
+
+template <> struct DftPos<10> : DftComp<2, 5> {};
+template <> struct DftPos<14> : DftComp<2, 7> {};
+template <> struct DftPos<16> : DftComp<4, 4> {};
+template <> struct DftPos<20> : DftComp<4, 5> {};
+template <> struct DftPos<24> : DftComp<8, 3> {};
+template <> struct DftPos<25> : DftComp<5, 5> {};
+template <> struct DftPos<28> : DftComp<4, 7> {};
+template <> struct DftPos<32> : DftComp<8, 4> {};
+
+template <> struct Dft<10> : DftComp<2, 5> {};
+template <> struct Dft<14> : DftComp<2, 7> {};
+template <> struct Dft<16> : DftComp<4, 4> {};
+template <> struct Dft<20> : DftComp<4, 5> {};
+template <> struct Dft<24> : DftComp<8, 3> {};
+template <> struct Dft<25> : DftComp<5, 5> {};
+template <> struct Dft<28> : DftComp<4, 7> {};
+template <> struct Dft<32> : DftComp<8, 4> {};
+template <> struct Dft<35> : DftComp<5, 7> {};
+template <> struct Dft<40> : DftComp<8, 5> {};
+
+// Per-pass plan (host-built, ws_api.cu): radix, Ns = product of the earlier
+// radices, magic = ceil(2^32 / Ns) for j mod Ns, and the offset of the pass's
+// twiddle table W_{Ns R}^{k r} laid out [r-1][k] (k < Ns) in `tw`.
+struct FftPlanDev {
+    int npass;
+    int radix[12];
+    int ns[12];
+    uint32_t magic[12];
+    int tw_off[12];
+};
+
 // One out-of-place Stockham radix-R pass: butterfly j reads in[j + r*M/R],
-// applies twiddles exp(-2 pi i k r / (Ns R)) with k = j mod Ns, runs Dft<R>,
-// and writes out[(j/Ns)*Ns*R + k + r*Ns]. One barrier per pass.
+// applies W_{Ns R}^{k r} with k = j mod Ns, runs Dft<R>, and writes
+// out[(j/Ns)*Ns*R + k + r*Ns]. One barrier per pass.
 template <int R, int NT>
 __device__ __forceinline__ void stockham_pass(const float2* __restrict__ in, float2* __restrict__ out, int M, int Ns,
-                                              uint32_t ns_magic, int stride, const float2* __restrict__ tw)
+                                              uint32_t ns_magic, const float2* __restrict__ tw)
 {
     const int nb = M / R;
-#pragma unroll 2
+#pragma unroll 1
     for (int j = threadIdx.x; j < nb; j += NT) {
         float2 v[R];
 #pragma unroll
@@ -190,31 +272,16 @@ __device__ __forceinline__ void stockham_pass(const float2* __restrict__ in, flo
         // k = j mod Ns via a multiply-high (exact for j, Ns < 2^16)
         const int k = Ns > 1 ? j - Ns * (int)__umulhi((uint32_t)j, ns_magic) : 0;
         if (Ns > 1) {
-            const float2 w1 = __ldg(&tw[k * stride]);
-            float2 w = w1;
 #pragma unroll
-            for (int r = 1; r < R; ++r) {
-                v[r] = cmul(v[r], w);
-                if (r + 1 < R) w = cmul(w, w1);
-            }
+            for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(&tw[(r - 1) * Ns + k]));
         }
         Dft<R>::run(v);
         const int base = (j - k) * R + k;
 #pragma unroll
-        for (int r = 0; r < R; ++r) out[base + r * Ns] = v[r];
+        for (int r = 0; r < R; ++r) out[base + r * Ns] = v[DftPos<R>::pos(r)];
     }
     __syncthreads();
 }
-
-// Per-pass plan: radix, Ns = product of earlier radices, magic = ceil(2^32/Ns),
-// twiddle stride = M / (Ns * R). Built on the host (ws_api.cu).
-struct FftPlanDev {
-    int npass;
-    int radix[12];
-    int ns[12];
-    uint32_t magic[12];
-    int stride[12];
-};
 
 // Forward FFT of length M from buffer a, ping-ponging with buffer b. Returns
 // the buffer holding the (natural-order) result.
@@ -226,18 +293,24 @@ __device__ __forceinline__ float2* fft_forward(float2* a, float2* b, int M, cons
     for (int p = 0; p < plan.npass; ++p) {
         const int Ns = plan.ns[p];
         const uint32_t mg = plan.magic[p];
-        const int st = plan.stride[p];
+        const float2* t = tw + plan.tw_off[p];
         switch (plan.radix[p]) {
-            case 2: stockham_pass<2, NT>(a, b, M, Ns, mg, st, tw); break;
-            case 3: stockham_pass<3, NT>(a, b, M, Ns, mg, st, tw); break;
-            case 4: stockham_pass<4, NT>(a, b, M, Ns, mg, st, tw); break;
-            case 5: stockham_pass<5, NT>(a, b, M, Ns, mg, st, tw); break;
-            case 7: stockham_pass<7, NT>(a, b, M, Ns, mg, st, tw); break;
-            default: stockham_pass<8, NT>(a, b, M, Ns, mg, st, tw); break;
+            case 2: stockham_pass<2, NT>(a, b, M, Ns, mg, t); break;
+            case 3: stockham_pass<3, NT>(a, b, M, Ns, mg, t); break;
+            case 4: stockham_pass<4, NT>(a, b, M, Ns, mg, t); break;
+            case 5: stockham_pass<5, NT>(a, b, M, Ns, mg, t); break;
+            case 7: stockham_pass<7, NT>(a, b, M, Ns, mg, t); break;
+            case 8: stockham_pass<8, NT>(a, b, M, Ns, mg, t); break;
+            case 10: stockham_pass<10, NT>(a, b, M, Ns, mg, t); break;
+            case 14: stockham_pass<14, NT>(a, b, M, Ns, mg, t); break;
+            case 16: stockham_pass<16, NT>(a, b, M, Ns, mg, t); break;
+            case 20: stockham_pass<20, NT>(a, b, M, Ns, mg, t); break;
+            case 24: stockham_pass<24, NT>(a, b, M, Ns, mg, t); break;
+            default: stockham_pass<25, NT>(a, b, M, Ns, mg, t); break;
         }
-        float2* t = a;
+        float2* tmp = a;
         a = b;
-        b = t;
+        b = tmp;
     }
     return a;
 }

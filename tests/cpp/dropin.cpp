@@ -1,0 +1,49 @@
+// C++ drop-in check: the reference-shaped C++ interface (include/wiresim_b200.hpp)
+// over the C ABI. Simulates one plane and writes the frame (float32, padded,
+// row-major) to argv[1]; exit code 0 on success. Built and run by
+// tests/test_gpu_parity.py::test_cpp_dropin.
+#include <cstdio>
+#include <vector>
+
+#include "wiresim_b200.hpp"
+
+int main(int argc, char** argv)
+{
+    if (argc < 2) return 2;
+    wiresim_b200::SimConfig cfg;
+    cfg.grid.n_wires = 64;
+    cfg.grid.n_ticks = 800;
+    cfg.grid.pad_wires = 20;
+    cfg.response.plane_kind = wiresim_b200::PlaneKind::induction;
+    cfg.response.wire_weights = {0.1, 1.0, 0.1};
+    cfg.fluctuate = false;
+    std::vector<wiresim_b200::Depo> depos(std::vector<wiresim_b200::Depo>::size_type(300));
+    for (std::size_t i = 0; i < depos.size(); ++i) {
+        depos[i].id = (int64_t)i;
+        depos[i].t = 20.0 + 0.9 * (double)i;
+        depos[i].x = 30.0 + 0.8 * (double)i;
+        depos[i].q = 1000 + (int64_t)(i * 37 % 9000);
+        depos[i].sigma_t = 0.5 + 0.003 * (double)i;
+        depos[i].sigma_x = 2.5 + 0.01 * (double)i;
+    }
+    try {
+        const wiresim_b200::SimResult r = wiresim_b200::run_simulation(cfg, depos);
+        FILE* f = std::fopen(argv[1], "wb");
+        if (!f) return 3;
+        std::fwrite(r.frame.data.data(), sizeof(float), r.frame.data.size(), f);
+        std::fclose(f);
+        std::printf("frame %zux%zu clipped %lld\n", r.frame.rows, r.frame.cols, (long long)r.clipped_charge);
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "error: %s\n", e.what());
+        return 1;
+    }
+    // the reference's exception categories cross back as the same C++ types
+    try {
+        wiresim_b200::SimConfig bad = cfg;
+        bad.response.wire_weights = {1.0, 1.0};
+        wiresim_b200::run_simulation(bad, depos);
+        return 4;
+    } catch (const std::invalid_argument&) {
+    }
+    return 0;
+}

@@ -54,6 +54,15 @@ def test_no_cpu_fallback_without_device():
     assert e.value.code == _lib.WS_ECUDA
 
 
+def test_cpp_header_compiles_and_links(tmp_path):
+    """include/wiresim_b200.hpp (the reference-shaped C++ interface) builds
+    against the C ABI and links with libwsgpu.so."""
+    import subprocess
+    lib = _lib.load()  # noqa: F841  (ensures the .so exists)
+    subprocess.run(["g++", "-std=c++17", "-O1", f"-I{ROOT / 'include'}", str(ROOT / "tests/cpp/dropin.cpp"),
+                    f"-L{ROOT / 'paper_2104_08265_b200'}", "-lwsgpu", "-o", str(tmp_path / "dropin")], check=True)
+
+
 def test_host_generator_matches_reference_gen_depos(ref):
     g = GridSpec(n_wires=480, n_ticks=6000)
     from oracle.oracle import make_grid

@@ -161,6 +161,28 @@ def test_validation_errors(ctx):
         Plane(ctx, GridSpec(n_wires=0), ResponseParams())
 
 
+def test_cpp_dropin(ctx, tmp_path):
+    """The C++ mirror header drives the same library: identical frame, and a bad
+    config raises the reference's exception type (tests/cpp/dropin.cpp)."""
+    import subprocess
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    exe = tmp_path / "dropin"
+    subprocess.run(["g++", "-std=c++17", "-O2", f"-I{root / 'include'}", str(root / "tests/cpp/dropin.cpp"),
+                    f"-L{root / 'paper_2104_08265_b200'}", "-lwsgpu",
+                    f"-Wl,-rpath,{root / 'paper_2104_08265_b200'}", "-o", str(exe)], check=True)
+    out = tmp_path / "frame.bin"
+    subprocess.run([str(exe), str(out)], check=True)
+    grid = GridSpec(n_wires=64, n_ticks=800, pad_wires=20, pad_ticks=100)
+    resp = ResponseParams(plane_kind="induction", wire_weights=(0.1, 1.0, 0.1))
+    i = np.arange(300)
+    d = np.zeros(300, dtype=gen_depos(1, 1, grid).dtype)
+    d["id"], d["t"], d["x"] = i, 20.0 + 0.9 * i, 30.0 + 0.8 * i
+    d["q"], d["sigma_t"], d["sigma_x"] = 1000 + (i * 37 % 9000), 0.5 + 0.003 * i, 2.5 + 0.01 * i
+    ours = Plane(ctx, grid, resp).simulate(d, SimConfig(grid=grid, response=resp, fluctuate=False)).frame
+    np.testing.assert_array_equal(np.fromfile(out, dtype=np.float32).reshape(ours.shape), ours)
+
+
 def test_event_matches_planes(ctx):
     grids = [GridSpec(n_wires=120, n_ticks=800, pad_wires=20, pad_ticks=100),
              GridSpec(n_wires=200, n_ticks=800, pad_wires=20, pad_ticks=100)]
