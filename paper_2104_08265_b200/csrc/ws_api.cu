@@ -431,7 +431,14 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
         c->launches += bands ? 1 : 0;
     }
     if (want_frame || (ev.mode == 0 && charges && !need_raw)) {
-        WS_CUDA(wsb_launch_conv(ev, c->recs.p, c->pool.p, c->band_off.p, c->band_list.p, want_frame ? 1 : 0, smem, s));
+        // WS_PROFILE_CONV_FLAGS: profiling-only switches of k_conv (4: skip the
+        // transforms, 8: skip the scatter) to split its time; never set in use
+        static const int prof_flags = [] {
+            const char* e = getenv("WS_PROFILE_CONV_FLAGS");
+            return e ? (atoi(e) & 12) : 0;
+        }();
+        WS_CUDA(wsb_launch_conv(ev, c->recs.p, c->pool.p, c->band_off.p, c->band_list.p,
+                                (want_frame ? 1 : 0) | prof_flags, smem, s));
         c->launches += bands ? 1 : 0;
     }
     WS_CUDA(cudaEventRecord(pc.ev[4], s));

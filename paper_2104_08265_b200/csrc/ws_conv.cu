@@ -128,7 +128,8 @@ k_conv(const EventDesc ev, const UnitRec* __restrict__ recs, const uint32_t* __r
                     }
                     __syncthreads();
                 }
-                accumulate_row(P, w, raw, acc_lo, acc_hi, recs, pool, band_list, c0, min(hi, c0 + kChunk));
+                if (!(flags & 8))  // profiling switch: skip the scatter
+                    accumulate_row(P, w, raw, acc_lo, acc_hi, recs, pool, band_list, c0, min(hi, c0 + kChunk));
             }
             __syncthreads();
             // fixed point -> fp32 in place (xs[t] overlays acc_lo[t], same thread)
@@ -158,6 +159,11 @@ k_conv(const EventDesc ev, const UnitRec* __restrict__ recs, const uint32_t* __r
         }
         __syncthreads();
         if (!want_frame) continue;
+        if (flags & 4) {  // profiling switch: skip the transforms, store S
+            for (int t = tid; t < N; t += kConvThreads) P.frame[(size_t)w * N + t] = xs[t];
+            __syncthreads();
+            continue;
+        }
 
         float2* z = fft_forward<kConvThreads>(bufA, bufB, M, P.fft, P.tw);
 
