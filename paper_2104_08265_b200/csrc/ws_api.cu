@@ -26,12 +26,12 @@ extern "C" cudaError_t wsb_launch_sample(const EventDesc& ev, UnitRec* recs, uin
 extern "C" cudaError_t wsb_launch_scan(const uint32_t* count, uint32_t* off, uint32_t* fill, uint32_t n,
                                        cudaStream_t s);
 extern "C" cudaError_t wsb_launch_fill(const EventDesc& ev, const UnitRec* recs, const uint32_t* off, uint32_t* fill,
-                                       uint32_t* list, cudaStream_t s);
+                                       UnitRec* list, cudaStream_t s);
 extern "C" cudaError_t wsb_launch_fluctuate(const EventDesc& ev, const UnitRec* recs, const uint32_t* pool,
                                             const uint32_t* order, cudaStream_t s);
 extern "C" cudaError_t wsb_launch_conv(const EventDesc& ev, const UnitRec* recs, const uint32_t* pool,
-                                       const uint32_t* band_off, const uint32_t* band_list, int flags,
-                                       size_t smem_bytes, cudaStream_t stream);
+                                       const uint32_t* band_off, const UnitRec* band_list, int flags,
+                                       size_t smem_bytes, int threads, cudaStream_t stream);
 
 namespace {
 
@@ -108,7 +108,8 @@ struct ws_ctx {
     uint64_t launches = 0;
     DevBuf<UnitRec> recs;
     DevBuf<uint32_t> pool;
-    DevBuf<uint32_t> band_count, band_off, band_fill, band_list;
+    DevBuf<uint32_t> band_count, band_off, band_fill;
+    DevBuf<UnitRec> band_list;  // CSR lists of full unit records (copied by k_fill_bands)
     DevBuf<ScratchHeader> header;
     DevBuf<ws_depo> depos;
     DevBuf<float> frames, charges;
@@ -118,6 +119,7 @@ struct ws_ctx {
     std::vector<cudaEvent_t> event_pool;
     size_t pool_hint = 0;
     int sm_count = 0;
+    int conv_threads = 256;                      // k_conv variant: 256 (radix <= 25) or 512 (radix <= 8)
     cudaStream_t copy_stream = nullptr;          // D2H of the pipelined batch path
     cudaEvent_t slot_computed[2] = {nullptr, nullptr};
     cudaEvent_t slot_copied[2] = {nullptr, nullptr};
@@ -135,7 +137,6 @@ struct ws_plane {
     double* d_ww = nullptr;
     float2* d_H = nullptr;
     float2* d_tw = nullptr;
-    float2* d_rtw = nullptr;
     int ww_is_one = 0;
     int rows_per_band = 4;
     int n_bands = 0;
@@ -262,9 +263,11 @@ bool smooth7(long n)
 // Pass plan for the length-m complex transform: the factorisation into
 // in-register radices with the fewest shared-memory passes, then the smallest
 // largest radix (register pressure), searched exhaustively (m is 7-smooth).
-std::vector<int> plan_radices(int m)
+std::vector<int> plan_radices(int m, int max_radix)
 {
-    static const int kRadices[] = {25, 24, 20, 16, 14, 10, 8, 7, 5, 4, 3, 2};
+    std::vector<int> kRadices;
+    for (int r : {25, 24, 20, 16, 14, 10, 8, 7, 5, 4, 3, 2})
+        if (r <= max_radix) kRadices.push_back(r);
     std::vector<int> best, cur;
     std::function<void(int)> dfs = [&](int rem) {
         if (rem == 1) {
@@ -319,7 +322,6 @@ PlaneDesc plane_desc(const ws_plane* p)
     d.ww = p->d_ww;
     d.H = p->d_H;
     d.tw = p->d_tw;
-    d.rtw = p->d_rtw;
     d.rows_per_band = p->rows_per_band;
     d.n_bands = p->n_bands;
     return d;
@@ -427,7 +429,7 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
     WS_CUDA(cudaEventRecord(pc.ev[3], s));
     if (ev.mode == 0 && charges && need_raw) {
         // the charge grid is the un-stencilled S: one extra accumulate-only pass
-        WS_CUDA(wsb_launch_conv(ev, c->recs.p, c->pool.p, c->band_off.p, c->band_list.p, 2, smem, s));
+        WS_CUDA(wsb_launch_conv(ev, c->recs.p, c->pool.p, c->band_off.p, c->band_list.p, 2, smem, c->conv_threads, s));
         c->launches += bands ? 1 : 0;
     }
     if (want_frame || (ev.mode == 0 && charges && !need_raw)) {
@@ -435,10 +437,10 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
         // transforms, 8: skip the scatter) to split its time; never set in use
         static const int prof_flags = [] {
             const char* e = getenv("WS_PROFILE_CONV_FLAGS");
-            return e ? (atoi(e) & 12) : 0;
+            return e ? (atoi(e) & 60) : 0;
         }();
         WS_CUDA(wsb_launch_conv(ev, c->recs.p, c->pool.p, c->band_off.p, c->band_list.p,
-                                (want_frame ? 1 : 0) | prof_flags, smem, s));
+                                (want_frame ? 1 : 0) | prof_flags, smem, c->conv_threads, s));
         c->launches += bands ? 1 : 0;
     }
     WS_CUDA(cudaEventRecord(pc.ev[4], s));
@@ -528,6 +530,7 @@ int ws_ctx_create(int device, void* stream, ws_ctx** out)
     ws_ctx* c = new ws_ctx();
     c->device = device;
     c->sm_count = prop.multiProcessorCount;
+    if (const char* e = getenv("WS_CONV_THREADS")) c->conv_threads = atoi(e) == 512 ? 512 : 256;
     if (stream) {
         c->stream = (cudaStream_t)stream;
     } else {
@@ -642,7 +645,7 @@ int ws_plane_create(ws_ctx* ctx, const ws_grid_spec* grid, const ws_response* re
         return set_err(WS_EINVAL, "padded_ticks %d needs a %d-point transform; at most %d supported", p->N, p->Np,
                        2 * wsb::kMaxFftHalf);
     }
-    p->radix = plan_radices(p->M);
+    p->radix = plan_radices(p->M, ctx->conv_threads == 512 ? 8 : 25);
     if ((int)p->radix.size() > wsb::kMaxPasses) {
         delete p;
         return set_err(WS_EINVAL, "transform plan too deep");
@@ -655,8 +658,9 @@ int ws_plane_create(ws_ctx* ctx, const ws_grid_spec* grid, const ws_response* re
         cs[m] = std::cos(a);
         sn[m] = std::sin(a);
     }
-    // pass plan + per-pass twiddle tables W_{Ns R}^{k r}, layout [r-1][k]
-    std::vector<float2> tw;
+    // pass plan (twiddle W_{Ns R}^{k r} = W_M^{k r step}) and the split
+    // twiddle tables [W_M^j | W_M^{64 i} | W_Np^j | W_Np^{64 i}], 64 + 192 each
+    std::vector<float2> tw(wsb::kTwiddleTable);
     {
         wsb::FftPlanDev& pl = p->plan;
         pl = wsb::FftPlanDev{};
@@ -667,18 +671,16 @@ int ws_plane_create(ws_ctx* ctx, const ws_grid_spec* grid, const ws_response* re
             pl.radix[i] = R;
             pl.ns[i] = ns;
             pl.magic[i] = ns > 1 ? (uint32_t)((0x100000000ULL + ns - 1) / ns) : 0u;
-            pl.tw_off[i] = (int)tw.size();
-            const long step = 2L * (M / (ns * R));  // index step on the Np grid
-            for (int r = 1; r < R && ns > 1; ++r)
-                for (int k = 0; k < ns; ++k) {
-                    const long idx = (step * k * r) % Np;
-                    tw.push_back(make_float2((float)cs[idx], (float)sn[idx]));
-                }
+            pl.step[i] = M / (ns * R);
             ns *= R;
         }
-        if (tw.empty()) tw.push_back(make_float2(1.f, 0.f));
+        auto put = [&](int at, long idx) { tw[at] = make_float2((float)cs[idx % Np], (float)sn[idx % Np]); };
+        for (int j = 0; j < 64; ++j) put(j, 2L * j);                 // W_M^j   (W_M = W_Np^2)
+        for (int i = 0; i < 192; ++i) put(64 + i, 2L * 64 * i);      // W_M^{64 i}
+        for (int j = 0; j < 64; ++j) put(256 + j, j);                // W_Np^j
+        for (int i = 0; i < 192; ++i) put(320 + i, 64L * i);         // W_Np^{64 i}
     }
-    std::vector<float2> H(M + 1), rtw(M / 2 + 1);
+    std::vector<float2> H(M + 1);
     for (int k = 0; k <= M; ++k) {
         double re = 0.0, im = 0.0;
         for (long i = 0; i < p->n_lags; ++i) {
@@ -690,23 +692,21 @@ int ws_plane_create(ws_ctx* ctx, const ws_grid_spec* grid, const ws_response* re
         }
         H[k] = make_float2((float)(re / M), (float)(im / M));
     }
-    for (int k = 0; k <= M / 2; ++k) rtw[k] = make_float2((float)cs[k], (float)sn[k]);
     std::vector<double> ww(response->wire_weights, response->wire_weights + response->n_wire_weights);
     cudaError_t e = cudaSuccess;
     e = e ? e : cudaMalloc(&p->d_H, sizeof(float2) * (M + 1));
     e = e ? e : cudaMalloc(&p->d_tw, sizeof(float2) * tw.size());
-    e = e ? e : cudaMalloc(&p->d_rtw, sizeof(float2) * (M / 2 + 1));
     e = e ? e : cudaMalloc(&p->d_ww, sizeof(double) * ww.size());
     e = e ? e : cudaMemcpy(p->d_H, H.data(), sizeof(float2) * (M + 1), cudaMemcpyHostToDevice);
     e = e ? e : cudaMemcpy(p->d_tw, tw.data(), sizeof(float2) * tw.size(), cudaMemcpyHostToDevice);
-    e = e ? e : cudaMemcpy(p->d_rtw, rtw.data(), sizeof(float2) * (M / 2 + 1), cudaMemcpyHostToDevice);
     e = e ? e : cudaMemcpy(p->d_ww, ww.data(), sizeof(double) * ww.size(), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
         ws_plane_destroy(p);
         return set_err(WS_ECUDA, "plane upload: %s", cudaGetErrorString(e));
     }
     p->n_bands = (p->W + p->rows_per_band - 1) / p->rows_per_band;
-    p->smem = (size_t)8 * (size_t)std::max(p->N, p->Np);
+    // row workspace (8 B/tick, 16-aligned) + the split twiddle tables
+    p->smem = (((size_t)8 * (size_t)std::max(p->N, p->Np) + 15) & ~(size_t)15) + sizeof(float2) * wsb::kTwiddleTable;
     if (p->smem > 227 * 1024) {
         ws_plane_destroy(p);
         return set_err(WS_EINVAL, "padded_ticks too large for the shared-memory row transform");
@@ -721,7 +721,6 @@ int ws_plane_destroy(ws_plane* p)
     if (p->ctx) cudaSetDevice(p->ctx->device);
     if (p->d_H) cudaFree(p->d_H);
     if (p->d_tw) cudaFree(p->d_tw);
-    if (p->d_rtw) cudaFree(p->d_rtw);
     if (p->d_ww) cudaFree(p->d_ww);
     delete p;
     return WS_OK;

@@ -18,6 +18,7 @@ constexpr int kMaxPlanes = 8;
 constexpr int kMaxPasses = 12;
 constexpr int kMaxWireWeights = 33;  // 2h+1 <= 33 taps of cross-wire coupling
 constexpr int kConvThreads = 256;
+constexpr int kTwiddleTable = 512;   // [W_M^j | W_M^{64i} | W_Np^j | W_Np^{64i}], 64 + 192 + 64 + 192
 constexpr int kMaxFftHalf = 12288;   // M = N'/2 <= 12288 (N' <= 24576 ticks)
 constexpr double kFixScale = 4294967296.0;          // 2^32: fixed-point electrons
 constexpr double kFixInv = 1.0 / 4294967296.0;
@@ -49,8 +50,7 @@ struct PlaneDesc {
     FftPlanDev fft;            // radix passes of the length-M complex transform
     const double* ww;          // 2h+1 wire weights
     const float2* H;           // M+1 response spectrum bins, pre-scaled by 1/M
-    const float2* tw;          // exp(-2 pi i m / M), m < M
-    const float2* rtw;         // exp(-2 pi i k / Np), k <= M/2
+    const float2* tw;          // split twiddle tables (kTwiddleTable entries, see ws_api.cu)
     // per call
     const ws_depo* depos;
     uint32_t n_units;

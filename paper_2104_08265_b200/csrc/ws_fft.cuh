@@ -246,14 +246,22 @@ template <> struct Dft<35> : DftComp<5, 7> {};
 template <> struct Dft<40> : DftComp<8, 5> {};
 
 // Per-pass plan (host-built, ws_api.cu): radix, Ns = product of the earlier
-// radices, magic = ceil(2^32 / Ns) for j mod Ns, and the offset of the pass's
-// twiddle table W_{Ns R}^{k r} laid out [r-1][k] (k < Ns) in `tw`.
+// radices, magic = ceil(2^32 / Ns) for j mod Ns, and the twiddle step
+// M / (Ns R): the pass twiddle W_{Ns R}^{k r} is W_M^{k r step}.
 struct FftPlanDev {
     int npass;
     int radix[12];
     int ns[12];
     uint32_t magic[12];
-    int tw_off[12];
+    int step[12];
+};
+
+// W_M^m from two 64-way shared-memory tables: lo[j] = W_M^j, hi[i] = W_M^{64 i}
+// (2.5 KB for M <= 12288 instead of an M-entry table that thrashes L1).
+struct TwiddleSplit {
+    const float2* lo;
+    const float2* hi;
+    __device__ __forceinline__ float2 operator()(int m) const { return cmul(hi[m >> 6], lo[m & 63]); }
 };
 
 // One out-of-place Stockham radix-R pass: butterfly j reads in[j + r*M/R],
@@ -261,7 +269,7 @@ struct FftPlanDev {
 // out[(j/Ns)*Ns*R + k + r*Ns]. One barrier per pass.
 template <int R, int NT>
 __device__ __forceinline__ void stockham_pass(const float2* __restrict__ in, float2* __restrict__ out, int M, int Ns,
-                                              uint32_t ns_magic, const float2* __restrict__ tw)
+                                              uint32_t ns_magic, int step, const TwiddleSplit& tw)
 {
     const int nb = M / R;
 #pragma unroll 1
@@ -272,8 +280,10 @@ __device__ __forceinline__ void stockham_pass(const float2* __restrict__ in, flo
         // k = j mod Ns via a multiply-high (exact for j, Ns < 2^16)
         const int k = Ns > 1 ? j - Ns * (int)__umulhi((uint32_t)j, ns_magic) : 0;
         if (Ns > 1) {
+            const int dm = k * step;  // m = k r step < M for r < R
+            int m = dm;
 #pragma unroll
-            for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(&tw[(r - 1) * Ns + k]));
+            for (int r = 1; r < R; ++r, m += dm) v[r] = cmul(v[r], tw(m));
         }
         Dft<R>::run(v);
         const int base = (j - k) * R + k;
@@ -285,28 +295,36 @@ __device__ __forceinline__ void stockham_pass(const float2* __restrict__ in, flo
 
 // Forward FFT of length M from buffer a, ping-ponging with buffer b. Returns
 // the buffer holding the (natural-order) result.
-template <int NT>
+// Only radices <= MAXR are instantiated (the host planner respects the same
+// bound), so a 512-thread build keeps its 64-register budget.
+template <int NT, int MAXR>
 __device__ __forceinline__ float2* fft_forward(float2* a, float2* b, int M, const FftPlanDev& plan,
-                                               const float2* __restrict__ tw)
+                                               const TwiddleSplit& t)
 {
 #pragma unroll 1
     for (int p = 0; p < plan.npass; ++p) {
         const int Ns = plan.ns[p];
-        const uint32_t mg = plan.magic[p];
-        const float2* t = tw + plan.tw_off[p];
+        const uint32_t mg = plan.magic[p] ;
+        const int st = plan.step[p];
         switch (plan.radix[p]) {
-            case 2: stockham_pass<2, NT>(a, b, M, Ns, mg, t); break;
-            case 3: stockham_pass<3, NT>(a, b, M, Ns, mg, t); break;
-            case 4: stockham_pass<4, NT>(a, b, M, Ns, mg, t); break;
-            case 5: stockham_pass<5, NT>(a, b, M, Ns, mg, t); break;
-            case 7: stockham_pass<7, NT>(a, b, M, Ns, mg, t); break;
-            case 8: stockham_pass<8, NT>(a, b, M, Ns, mg, t); break;
-            case 10: stockham_pass<10, NT>(a, b, M, Ns, mg, t); break;
-            case 14: stockham_pass<14, NT>(a, b, M, Ns, mg, t); break;
-            case 16: stockham_pass<16, NT>(a, b, M, Ns, mg, t); break;
-            case 20: stockham_pass<20, NT>(a, b, M, Ns, mg, t); break;
-            case 24: stockham_pass<24, NT>(a, b, M, Ns, mg, t); break;
-            default: stockham_pass<25, NT>(a, b, M, Ns, mg, t); break;
+            case 2: stockham_pass<2, NT>(a, b, M, Ns, mg, st, t); break;
+            case 3: stockham_pass<3, NT>(a, b, M, Ns, mg, st, t); break;
+            case 4: stockham_pass<4, NT>(a, b, M, Ns, mg, st, t); break;
+            case 5: stockham_pass<5, NT>(a, b, M, Ns, mg, st, t); break;
+            case 7: stockham_pass<7, NT>(a, b, M, Ns, mg, st, t); break;
+            case 8: stockham_pass<8, NT>(a, b, M, Ns, mg, st, t); break;
+            default:
+                if constexpr (MAXR >= 25) {
+                    switch (plan.radix[p]) {
+                        case 10: stockham_pass<10, NT>(a, b, M, Ns, mg, st, t); break;
+                        case 14: stockham_pass<14, NT>(a, b, M, Ns, mg, st, t); break;
+                        case 16: stockham_pass<16, NT>(a, b, M, Ns, mg, st, t); break;
+                        case 20: stockham_pass<20, NT>(a, b, M, Ns, mg, st, t); break;
+                        case 24: stockham_pass<24, NT>(a, b, M, Ns, mg, st, t); break;
+                        default: stockham_pass<25, NT>(a, b, M, Ns, mg, st, t); break;
+                    }
+                }
+                break;
         }
         float2* tmp = a;
         a = b;

@@ -263,16 +263,16 @@ __global__ void k_scan_bands(const uint32_t* __restrict__ count, uint32_t* __res
 }
 
 __global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ recs, const uint32_t* __restrict__ off,
-                             uint32_t* __restrict__ fill, uint32_t* __restrict__ list)
+                             uint32_t* __restrict__ fill, UnitRec* __restrict__ list)
 {
     const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
     if (u >= ev.total_units) return;
-    const int4 r = *reinterpret_cast<const int4*>(&recs[u]);
-    if (r.x < 0) return;
-    const PlaneDesc& P = ev.p[recs[u].plane];
-    for_each_band(P, r.x, r.z, [&](int c) {
+    const UnitRec rec = recs[u];
+    if (rec.w0 < 0) return;
+    const PlaneDesc& P = ev.p[rec.plane];
+    for_each_band(P, rec.w0, rec.n_w, [&](int c) {
         const uint32_t b = P.band_base + c;
-        list[off[b] + atomicAdd(&fill[b], 1u)] = u;
+        list[off[b] + atomicAdd(&fill[b], 1u)] = rec;  // full record: k_conv streams the list
     });
 }
 
@@ -344,7 +344,7 @@ extern "C" cudaError_t wsb_launch_scan(const uint32_t* count, uint32_t* off, uin
 }
 
 extern "C" cudaError_t wsb_launch_fill(const wsb::EventDesc& ev, const wsb::UnitRec* recs, const uint32_t* off,
-                                       uint32_t* fill, uint32_t* list, cudaStream_t s)
+                                       uint32_t* fill, wsb::UnitRec* list, cudaStream_t s)
 {
     if (ev.total_units == 0) return cudaSuccess;
     wsb::k_fill_bands<<<(ev.total_units + 255) / 256, 256, 0, s>>>(ev, recs, off, fill, list);
