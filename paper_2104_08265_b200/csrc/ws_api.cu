@@ -29,9 +29,10 @@ extern "C" cudaError_t wsb_launch_fill(const EventDesc& ev, const UnitRec* recs,
                                        UnitRec* list, cudaStream_t s);
 extern "C" cudaError_t wsb_launch_fluctuate(const EventDesc& ev, const UnitRec* recs, const uint32_t* pool,
                                             const uint32_t* order, cudaStream_t s);
-extern "C" cudaError_t wsb_launch_conv(const EventDesc& ev, const UnitRec* recs, const uint32_t* pool,
-                                       const uint32_t* band_off, const UnitRec* band_list, int flags,
-                                       size_t smem_bytes, int threads, cudaStream_t stream);
+extern "C" size_t wsb_conv_smem(int N, int Np, int M);
+extern "C" cudaError_t wsb_launch_conv(const EventDesc& ev, const uint32_t* pool, const uint32_t* band_off,
+                                       const UnitRec* band_list, int flags, size_t smem_bytes, int variant,
+                                       cudaStream_t stream);
 
 namespace {
 
@@ -119,7 +120,7 @@ struct ws_ctx {
     std::vector<cudaEvent_t> event_pool;
     size_t pool_hint = 0;
     int sm_count = 0;
-    int conv_threads = 256;                      // k_conv variant: 256 (radix <= 25) or 512 (radix <= 8)
+    int conv_variant = 25;                       // k_conv: 25 (3 CTAs/SM, radix <= 25) or 8 (4 CTAs/SM, radix <= 8)
     cudaStream_t copy_stream = nullptr;          // D2H of the pipelined batch path
     cudaEvent_t slot_computed[2] = {nullptr, nullptr};
     cudaEvent_t slot_copied[2] = {nullptr, nullptr};
@@ -137,6 +138,7 @@ struct ws_plane {
     double* d_ww = nullptr;
     float2* d_H = nullptr;
     float2* d_tw = nullptr;
+    uint16_t* d_rev = nullptr;
     int ww_is_one = 0;
     int rows_per_band = 4;
     int n_bands = 0;
@@ -263,11 +265,15 @@ bool smooth7(long n)
 // Pass plan for the length-m complex transform: the factorisation into
 // in-register radices with the fewest shared-memory passes, then the smallest
 // largest radix (register pressure), searched exhaustively (m is 7-smooth).
-std::vector<int> plan_radices(int m, int max_radix)
+// Radix sets instantiated by the two k_conv variants (ws_conv.cu). The DIF
+// pass order puts odd radices last: the final DIF pass (and the first DIT
+// pass) has unit stride, where an odd radix keeps the shared-memory accesses
+// free of bank conflicts.
+const std::vector<int> kRadix25 = {25, 24, 20, 16, 14, 10, 8, 7, 5, 4, 3, 2};
+const std::vector<int> kRadix8 = {8, 7, 5, 4, 3, 2};
+
+std::vector<int> plan_radices(int m, const std::vector<int>& kRadices)
 {
-    std::vector<int> kRadices;
-    for (int r : {25, 24, 20, 16, 14, 10, 8, 7, 5, 4, 3, 2})
-        if (r <= max_radix) kRadices.push_back(r);
     std::vector<int> best, cur;
     std::function<void(int)> dfs = [&](int rem) {
         if (rem == 1) {
@@ -285,6 +291,7 @@ std::vector<int> plan_radices(int m, int max_radix)
             }
     };
     dfs(m);
+    std::stable_sort(best.begin(), best.end(), [](int a, int b) { return (a & 1) < (b & 1); });  // odd last
     return best;
 }
 
@@ -322,6 +329,7 @@ PlaneDesc plane_desc(const ws_plane* p)
     d.ww = p->d_ww;
     d.H = p->d_H;
     d.tw = p->d_tw;
+    d.rev = p->d_rev;
     d.rows_per_band = p->rows_per_band;
     d.n_bands = p->n_bands;
     return d;
@@ -427,20 +435,28 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
         c->launches += 1 + (units ? 1 : 0);
     }
     WS_CUDA(cudaEventRecord(pc.ev[3], s));
+    // WS_PROFILE_CONV_FLAGS: profiling-only switches of the ping-pong k_conv
+    // (4: skip the transforms, 8: skip the scatter) to split its time
+    static const int prof_flags = [] {
+        const char* e = getenv("WS_PROFILE_CONV_FLAGS");
+        return e ? (atoi(e) & 60) : 0;
+    }();
+    // WS_PROFILE_SMEM_PAD: profiling-only extra shared memory per CTA (occupancy sensitivity)
+    static const size_t smem_pad = [] {
+        const char* e = getenv("WS_PROFILE_SMEM_PAD");
+        return e ? (size_t)atol(e) : (size_t)0;
+    }();
+    auto launch_conv = [&](int flags) -> cudaError_t {
+        return wsb_launch_conv(ev, c->pool.p, c->band_off.p, c->band_list.p, flags | prof_flags, smem + smem_pad,
+                               c->conv_variant, s);
+    };
     if (ev.mode == 0 && charges && need_raw) {
         // the charge grid is the un-stencilled S: one extra accumulate-only pass
-        WS_CUDA(wsb_launch_conv(ev, c->recs.p, c->pool.p, c->band_off.p, c->band_list.p, 2, smem, c->conv_threads, s));
+        WS_CUDA(launch_conv(2));
         c->launches += bands ? 1 : 0;
     }
     if (want_frame || (ev.mode == 0 && charges && !need_raw)) {
-        // WS_PROFILE_CONV_FLAGS: profiling-only switches of k_conv (4: skip the
-        // transforms, 8: skip the scatter) to split its time; never set in use
-        static const int prof_flags = [] {
-            const char* e = getenv("WS_PROFILE_CONV_FLAGS");
-            return e ? (atoi(e) & 60) : 0;
-        }();
-        WS_CUDA(wsb_launch_conv(ev, c->recs.p, c->pool.p, c->band_off.p, c->band_list.p,
-                                (want_frame ? 1 : 0) | prof_flags, smem, c->conv_threads, s));
+        WS_CUDA(launch_conv(want_frame ? 1 : 0));
         c->launches += bands ? 1 : 0;
     }
     WS_CUDA(cudaEventRecord(pc.ev[4], s));
@@ -530,7 +546,7 @@ int ws_ctx_create(int device, void* stream, ws_ctx** out)
     ws_ctx* c = new ws_ctx();
     c->device = device;
     c->sm_count = prop.multiProcessorCount;
-    if (const char* e = getenv("WS_CONV_THREADS")) c->conv_threads = atoi(e) == 512 ? 512 : 256;
+    if (const char* e = getenv("WS_CONV_VARIANT")) c->conv_variant = atoi(e) == 8 ? 8 : 25;
     if (stream) {
         c->stream = (cudaStream_t)stream;
     } else {
@@ -645,7 +661,11 @@ int ws_plane_create(ws_ctx* ctx, const ws_grid_spec* grid, const ws_response* re
         return set_err(WS_EINVAL, "padded_ticks %d needs a %d-point transform; at most %d supported", p->N, p->Np,
                        2 * wsb::kMaxFftHalf);
     }
-    p->radix = plan_radices(p->M, ctx->conv_threads == 512 ? 8 : 25);
+    p->radix = plan_radices(p->M, ctx->conv_variant == 8 ? kRadix8 : kRadix25);
+    if (p->radix.empty()) {
+        delete p;
+        return set_err(WS_EINVAL, "no radix plan for a %d-point transform", p->M);
+    }
     if ((int)p->radix.size() > wsb::kMaxPasses) {
         delete p;
         return set_err(WS_EINVAL, "transform plan too deep");
@@ -658,21 +678,42 @@ int ws_plane_create(ws_ctx* ctx, const ws_grid_spec* grid, const ws_response* re
         cs[m] = std::cos(a);
         sn[m] = std::sin(a);
     }
-    // pass plan (twiddle W_{Ns R}^{k r} = W_M^{k r step}) and the split
-    // twiddle tables [W_M^j | W_M^{64 i} | W_Np^j | W_Np^{64 i}], 64 + 192 each
+    // DIF / DIT pass plan (ws_fft.cuh), the digit-reversal map of the DIF
+    // output, and the split twiddle tables [W_M^j | W_M^{64 i} | W_Np^j | W_Np^{64 i}]
     std::vector<float2> tw(wsb::kTwiddleTable);
+    std::vector<uint16_t> rev(M);
     {
         wsb::FftPlanDev& pl = p->plan;
         pl = wsb::FftPlanDev{};
-        pl.npass = (int)p->radix.size();
-        int ns = 1;
-        for (int i = 0; i < pl.npass; ++i) {
+        const int P = (int)p->radix.size();
+        pl.npass = P;
+        auto magic = [](int d) { return d > 1 ? (uint32_t)((0x100000000ULL + d - 1) / d) : 0u; };
+        int L = M;
+        for (int i = 0; i < P; ++i) {  // DIF pass i: length L, stride S = L / R
             const int R = p->radix[i];
             pl.radix[i] = R;
-            pl.ns[i] = ns;
-            pl.magic[i] = ns > 1 ? (uint32_t)((0x100000000ULL + ns - 1) / ns) : 0u;
-            pl.step[i] = M / (ns * R);
-            ns *= R;
+            pl.dif_s[i] = L / R;
+            pl.dif_mg[i] = magic(L / R);
+            pl.dif_step[i] = M / L;
+            L /= R;
+        }
+        int lam = 1;
+        for (int i = 0; i < P; ++i) {  // DIT pass i runs radix[P-1-i]
+            const int R = p->radix[P - 1 - i];
+            pl.dit_lam[i] = lam;
+            pl.dit_mg[i] = magic(lam);
+            pl.dit_step[i] = M / (lam * R);
+            lam *= R;
+        }
+        for (int k = 0; k < M; ++k) {  // pos(k) = sum_p q_p M / (R_0..R_p), k = sum_p q_p R_0..R_{p-1}
+            long pos = 0, div = 1, len = M;
+            for (int i = 0; i < P; ++i) {
+                const int R = p->radix[i];
+                len /= R;
+                pos += ((k / div) % R) * len;
+                div *= R;
+            }
+            rev[k] = (uint16_t)pos;
         }
         auto put = [&](int at, long idx) { tw[at] = make_float2((float)cs[idx % Np], (float)sn[idx % Np]); };
         for (int j = 0; j < 64; ++j) put(j, 2L * j);                 // W_M^j   (W_M = W_Np^2)
@@ -700,13 +741,14 @@ int ws_plane_create(ws_ctx* ctx, const ws_grid_spec* grid, const ws_response* re
     e = e ? e : cudaMemcpy(p->d_H, H.data(), sizeof(float2) * (M + 1), cudaMemcpyHostToDevice);
     e = e ? e : cudaMemcpy(p->d_tw, tw.data(), sizeof(float2) * tw.size(), cudaMemcpyHostToDevice);
     e = e ? e : cudaMemcpy(p->d_ww, ww.data(), sizeof(double) * ww.size(), cudaMemcpyHostToDevice);
+    e = e ? e : cudaMalloc(&p->d_rev, sizeof(uint16_t) * M);
+    e = e ? e : cudaMemcpy(p->d_rev, rev.data(), sizeof(uint16_t) * M, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
         ws_plane_destroy(p);
         return set_err(WS_ECUDA, "plane upload: %s", cudaGetErrorString(e));
     }
     p->n_bands = (p->W + p->rows_per_band - 1) / p->rows_per_band;
-    // row workspace (8 B/tick, 16-aligned) + the split twiddle tables
-    p->smem = (((size_t)8 * (size_t)std::max(p->N, p->Np) + 15) & ~(size_t)15) + sizeof(float2) * wsb::kTwiddleTable;
+    p->smem = wsb_conv_smem(p->N, p->Np, p->M);
     if (p->smem > 227 * 1024) {
         ws_plane_destroy(p);
         return set_err(WS_EINVAL, "padded_ticks too large for the shared-memory row transform");
@@ -721,6 +763,7 @@ int ws_plane_destroy(ws_plane* p)
     if (p->ctx) cudaSetDevice(p->ctx->device);
     if (p->d_H) cudaFree(p->d_H);
     if (p->d_tw) cudaFree(p->d_tw);
+    if (p->d_rev) cudaFree(p->d_rev);
     if (p->d_ww) cudaFree(p->d_ww);
     delete p;
     return WS_OK;

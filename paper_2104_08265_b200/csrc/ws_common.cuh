@@ -31,7 +31,8 @@ struct __align__(16) UnitRec {
     int32_t n_t;   // ticks
     uint32_t pool; // offset (in doubles) of [wv(n_w) | tv(n_t)] in the pool
     int32_t plane;
-    double a;      // fluct off: q / total; fluct on: unused
+    float a;       // fluct off: q / total; fluct on: unused
+    float tmax;    // fluct off: max over the tick profile (bounds a row's fixed-point scale)
 };
 
 // Device view of one plane for one launch.
@@ -51,6 +52,7 @@ struct PlaneDesc {
     const double* ww;          // 2h+1 wire weights
     const float2* H;           // M+1 response spectrum bins, pre-scaled by 1/M
     const float2* tw;          // split twiddle tables (kTwiddleTable entries, see ws_api.cu)
+    const uint16_t* rev;       // rev[k] = slot of spectrum bin k after the DIF transform
     // per call
     const ws_depo* depos;
     uint32_t n_units;

@@ -1,25 +1,34 @@
-// Fused accumulate + FFT convolution kernel (K3, with K1's scatter fused in).
+// Fused scatter + FFT convolution kernel (k_conv: K1's scatter fused into K3).
 //
 // One CTA owns a band of `rows_per_band` consecutive wire rows of one plane and
-// walks them one row at a time, entirely in shared memory:
+// walks them one row at a time, entirely in one row of shared memory
+// (4 B/tick), so several rows are in flight per SM:
 //
 //   1. source the charge row S[w, 0:N)
 //        mode 0 (fluctuation off): scatter-add every depo patch that covers
 //               the row from the band's depo list (the reference's
 //               sample_patch -> scatter_add, rasterize.cpp:66-120 +
-//               scatter.cpp:27-36), accumulating q*p in int64 fixed point
-//               (2^-32 e-) so the sum is exact and order independent; the
-//               cross-wire stencil (spectral.cpp:124-135) is applied to the
-//               separable wire profile, S'[w] = sum_dw ww[dw] S[w-dw];
+//               scatter.cpp:27-36), with the cross-wire stencil applied to
+//               the separable wire profile, S'[w] = sum_dw ww[dw] S[w-dw]
+//               (spectral.cpp:124-135). Accumulation is int32 fixed point at a
+//               per-row power-of-two scale chosen from a rigorous bound (each
+//               covering depo adds ceil(|c| max(tv)) to the 64-tick segments it
+//               touches; the largest segment bound maps to 2^30), so no sum can
+//               overflow for any depo count, one native shared-memory atomic
+//               (ATOMS.ADD) per bin suffices, and the row is bitwise
+//               reproducible for any schedule;
 //        mode 1: load S rows from a charge grid (fluctuation on / convolve
 //               only), same stencil;
 //   2. real FFT of length Np along ticks as a complex FFT of length M = Np/2
-//      (row samples paired (2n, 2n+1), so every channel's roundoff is relative
-//      to its own norm — never FFT across wires);
+//      (sample pairs (2n, 2n+1), so each channel's roundoff is relative to its
+//      own norm — never FFT across wires), in place, DIF
+//      (natural in, digit-reversed out);
 //   3. untangle to the half spectrum, multiply by the response spectrum H
-//      (ResponseKernel values, spectral.cpp:137 / convolve :160), re-tangle;
-//   4. inverse FFT (forward FFT of the conjugate), fold the circular wrap when
-//      Np > N, write the frame row (convolve :172-173).
+//      (ResponseKernel values, spectral.cpp:137 / convolve :160), re-tangle,
+//      all in digit-reversed positions;
+//   4. inverse as a forward DIT of the conjugate (digit-reversed in, natural
+//      out), fold of the circular wrap when Np > N, frame row store
+//      (convolve :172-173).
 //
 // S never touches HBM in mode 0: the only DRAM traffic is the frame write
 // (4 B/cell) plus the depo records.
@@ -27,11 +36,7 @@
 
 namespace wsb {
 
-constexpr int kLoBits = 20;              // fixed point split: v = hi * 2^20 + lo
-constexpr uint32_t kLoMask = (1u << kLoBits) - 1;
-constexpr int kChunk = 4095;             // band entries per pass: lo holds 4096 * 2^20 < 2^32
-constexpr float kFix = 16777216.0f;      // 2^24 fixed-point electrons
-constexpr float kFixInvF = 1.0f / 16777216.0f;
+constexpr int kSegShift = 6;  // 64-tick bound segments
 
 __device__ __forceinline__ int band_plane(const EventDesc& ev, uint32_t gb)
 {
@@ -42,113 +47,143 @@ __device__ __forceinline__ int band_plane(const EventDesc& ev, uint32_t gb)
     return p;
 }
 
-// Scatter-add every band entry that covers row w into the row accumulator,
-// one thread per (entry, row): v = c * tv[t] in 2^-24 e- fixed point, split
-// into a signed hi word (v >> 20) and an unsigned lo word (v & 0xFFFFF), both
-// added with native shared-memory int32 atomics (ATOMS.ADD). Integer sums are
-// order independent, so the row is bitwise reproducible for any schedule.
-// raw: accumulate the un-stencilled S (charge-grid output) instead of S'.
-// Split v (an integer-valued fp32, the 2^-24 e- fixed-point bin value) into
-// hi = floor(v / 2^20) and lo = v - hi 2^20 in [0, 2^20) with fp32 ops only
-// (magic-number conversions, exact while |hi| < 2^22, i.e. a bin below
-// ~2.6e5 e-; larger bins take the 64-bit conversion).
-__device__ __forceinline__ void split_fixed(float v, int& hi, uint32_t& lo)
-{
-    const float hf = floorf(v * (1.0f / 1048576.0f));
-    if (fabsf(hf) < 4194304.0f) {
-        const float lf = fmaf(-hf, 1048576.0f, v);                      // exact, in [0, 2^20)
-        hi = __float_as_int(hf + 12582912.0f) - 0x4B400000;             // 1.5 * 2^23 magic
-        lo = (uint32_t)__float_as_int(lf + 8388608.0f) & 0x7FFFFFu;     // 2^23 magic
-    } else {
-        const long long x = __float2ll_rn(v);
-        hi = (int)(x >> kLoBits);
-        lo = (uint32_t)x & kLoMask;
-    }
-}
+// One covering (entry, row) pair.
+struct Cover {
+    float c;       // a * (stencilled) wire weight of this row
+    int t0, n_t;
+    uint32_t tvo;  // pool offset of the tick profile
+};
 
-// Band list entries are full unit records (copied by k_fill), so the scan
-// streams them coalesced instead of chasing an index into the record table.
-template <int NT>
-__device__ __forceinline__ void accumulate_row(const PlaneDesc& P, int w, bool raw, uint32_t* acc_lo, int* acc_hi,
-                                               const uint32_t* __restrict__ pool, const UnitRec* __restrict__ list,
-                                               uint32_t lo, uint32_t hi, int dbg)
+// Does band entry i cover row w? raw: the un-stencilled S (charge output).
+__device__ __forceinline__ bool cover_of(const PlaneDesc& P, int w, bool raw, const UnitRec* __restrict__ list,
+                                         const uint32_t* __restrict__ pool, uint32_t i, Cover& cv, float& tmax)
 {
-    const int W = P.W;
+    const int4 r = __ldg(reinterpret_cast<const int4*>(&list[i]));
+    const int w0 = r.x, n_w = r.z;
     const int h = P.h;
     const bool stencil = !raw && !P.ww_is_one;
+    const int lo_row = stencil ? w0 - h : w0;
+    const int n_rows = stencil ? n_w + 2 * h : n_w;
+    int j = (w - lo_row) % P.W;
+    if (j < 0) j += P.W;
+    if (j >= n_rows) return false;
+    const uint32_t off = __ldg(&list[i].pool);
+    const float2 at = __ldg(reinterpret_cast<const float2*>(&list[i].a));  // a, tmax
+    const float* prof = reinterpret_cast<const float*>(pool + off) + (stencil ? n_w : 0);
+    float c = 0.0f;
+    for (; j < n_rows; j += P.W) c += __ldg(&prof[j]);  // a wrap can land twice on a tiny grid
+    cv.c = c * at.x;
+    cv.t0 = r.y;
+    cv.n_t = r.w;
+    cv.tvo = off + n_w + (P.ww_is_one ? 0 : n_w + 2 * h);
+    tmax = at.y;
+    return true;
+}
+
+constexpr int kKeep = 4;  // covering entries per thread carried from the bound pass
+
+template <int NT>
+__device__ __forceinline__ void scatter_row(const PlaneDesc& P, int w, bool raw, int* acc, unsigned* segb, int* s_red,
+                                            int nseg, const uint32_t* __restrict__ pool,
+                                            const UnitRec* __restrict__ list, uint32_t lo, uint32_t hi, float& inv)
+{
+    const int tid = threadIdx.x;
+    // pass 1: bounds per 64-tick segment (electrons, rounded up); the first
+    // kKeep covers of this thread stay in registers for pass 2
+    Cover keep[kKeep];
+    int keep_at[kKeep];
+    int nkeep = 0;
+    int kdone = 0x7fffffff;  // iterations <= kdone are fully classified
 #pragma unroll 1
-    for (uint32_t i = lo + threadIdx.x; i < hi; i += NT) {
-        const int4 r = __ldg(reinterpret_cast<const int4*>(&list[i]));
-        const int w0 = r.x, t0 = r.y, n_w = r.z, n_t = r.w;
-        const int lo_row = stencil ? w0 - h : w0;
-        const int n_rows = stencil ? n_w + 2 * h : n_w;
-        int j = (w - lo_row) % W;
-        if (j < 0) j += W;
-        if (j >= n_rows) continue;
-        const uint32_t off = __ldg(&list[i].pool);
-        const float* prof = reinterpret_cast<const float*>(pool + off) + (stencil ? n_w : 0);
-        const float* tv = reinterpret_cast<const float*>(pool + off) + n_w + (P.ww_is_one ? 0 : n_w + 2 * h);
-        float c = 0.0f;
-        for (; j < n_rows; j += W) c += __ldg(&prof[j]);  // a wrap can land twice on a tiny grid
-        c *= (float)__ldg(&list[i].a) * kFix;              // q / total, 2^24 fixed point
-        // profile loads in batches of 8 so their latencies overlap
+    for (uint32_t i = lo + tid, k = 0; i < hi; i += NT, ++k) {
+        Cover cv;
+        float tm;
+        if (!cover_of(P, w, raw, list, pool, i, cv, tm)) continue;
+        const unsigned b = (unsigned)fminf(ceilf(fabsf(cv.c) * tm) + 1.0f, 4.0e9f);
+        const int s0 = cv.t0 >> kSegShift, s1 = (cv.t0 + cv.n_t - 1) >> kSegShift;
+        for (int s = s0; s <= s1; ++s) atomicAdd(&segb[s], b);
+        if (nkeep < kKeep) {
+            keep[nkeep] = cv;
+            keep_at[nkeep] = (int)k;
+            if (++nkeep == kKeep) kdone = (int)k;
+        }
+    }
+    __syncthreads();
+    // scale: the largest segment bound maps below 2^30
+    unsigned mx = 0u;
+    for (int i = tid; i < nseg; i += NT) mx = max(mx, segb[i]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((tid & 31) == 0) s_red[tid >> 5] = (int)mx;
+    __syncthreads();
+    mx = 0u;
+#pragma unroll
+    for (int q = 0; q < NT / 32; ++q) mx = max(mx, (unsigned)s_red[q]);
+    const int sh = 30 - (32 - __clz(mx));  // mx < 2^(32-clz)  =>  mx 2^sh < 2^30
+    const float scale = ldexpf(1.0f, sh);
+    inv = ldexpf(1.0f, -sh);
+    // pass 2: scatter, one int32 shared atomic per bin
+    int kk = 0;
 #pragma unroll 1
-        for (int tb = 0; tb < n_t; tb += 8) {
+    for (uint32_t i = lo + tid, k = 0; i < hi; i += NT, ++k) {
+        Cover cv;
+        float tm;
+        if ((int)k <= kdone) {  // classified in pass 1: a kept cover or not covering
+            if (kk >= nkeep || keep_at[kk] != (int)k) continue;
+            cv = keep[kk++];
+        } else if (!cover_of(P, w, raw, list, pool, i, cv, tm)) {
+            continue;
+        }
+        const float cs = cv.c * scale;
+        const float* tv = reinterpret_cast<const float*>(pool + cv.tvo);
+#pragma unroll 1
+        for (int tb = 0; tb < cv.n_t; tb += 8) {
             float tvv[8];
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
-                tvv[k] = tb + k < n_t ? ((dbg & 32) ? 0.25f : __ldg(&tv[tb + k])) : 0.0f;
+            for (int q = 0; q < 8; ++q) tvv[q] = tb + q < cv.n_t ? __ldg(&tv[tb + q]) : 0.0f;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                if (tb + k < n_t) {
-                    int vh;
-                    uint32_t vl;
-                    split_fixed(rintf(c * tvv[k]), vh, vl);
-                    if (dbg & 16) {  // profiling only: racy plain adds, to price the atomics
-                        acc_lo[t0 + tb + k] += vl;
-                        acc_hi[t0 + tb + k] += vh;
-                    } else {
-                        atomicAdd(&acc_lo[t0 + tb + k], vl);
-                        atomicAdd(&acc_hi[t0 + tb + k], vh);
-                    }
-                }
-            }
+            for (int q = 0; q < 8; ++q)
+                if (tb + q < cv.n_t) atomicAdd(&acc[cv.t0 + tb + q], __float2int_rn(cs * tvv[q]));
         }
     }
 }
 
-// NT = 256: 16 warps/SM, <= 128 registers, passes of radix <= 25 (3 passes at
-// M = 4900); NT = 512: 32 warps/SM, <= 64 registers, radix <= 8 (more passes).
-template <int NT, int MAXR>
-__global__ void __launch_bounds__(NT, 2)
-k_conv(const EventDesc ev, const UnitRec* __restrict__ recs, const uint32_t* __restrict__ pool,
-       const uint32_t* __restrict__ band_off, const UnitRec* __restrict__ band_list, int flags)
+template <int NT, int MAXR, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
+k_conv(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* __restrict__ band_off,
+       const UnitRec* __restrict__ band_list, int flags)
 {
     // flags bit 0: produce the frame; bit 1: raw-charge pass (no wire stencil)
-    const bool want_frame = flags & 1;
     extern __shared__ __align__(16) unsigned char smem[];
+    const bool want_frame = flags & 1;
+    const bool raw = flags & 2;
     const uint32_t gb = blockIdx.x;
-    const int pi = band_plane(ev, gb);
-    const PlaneDesc& P = ev.p[pi];
+    const PlaneDesc& P = ev.p[band_plane(ev, gb)];
     const int band = (int)(gb - P.band_base);
     const int W = P.W, N = P.N, Np = P.Np, M = P.M;
     const int r0 = band * P.rows_per_band;
     const int r1 = min(r0 + P.rows_per_band, W);
     const int tid = threadIdx.x;
-    // row workspace (8 * max(N, Np) bytes): the fixed-point accumulator
-    // acc_lo[N] | acc_hi[N], aliased by the float row xs[Np] (xs[t] sits on
-    // acc_lo[t]) and by the two FFT buffers bufA[M] | bufB[M].
-    uint32_t* acc_lo = reinterpret_cast<uint32_t*>(smem);
-    int* acc_hi = reinterpret_cast<int*>(smem) + N;
-    float2* bufA = reinterpret_cast<float2*>(smem);
-    float2* bufB = bufA + M;
+    const int nseg = (N + 63) >> kSegShift;
+    // layout: row (4*Np bytes: int32 accumulator / float row / complex
+    // half-length spectrum, all in place) | segment bounds | twiddles |
+    // digit-reversal table | reduce scratch
+    int* acc = reinterpret_cast<int*>(smem);
     float* xs = reinterpret_cast<float*>(smem);
-    const bool raw = flags & 2;
-    // split twiddle tables after the workspace (read before the first barrier use)
-    float2* s_tw = reinterpret_cast<float2*>(smem + (((size_t)8 * (size_t)max(N, Np) + 15) & ~(size_t)15));
+    float2* buf = reinterpret_cast<float2*>(smem);
+    size_t off = ((size_t)4 * Np + 15) & ~(size_t)15;
+    unsigned* segb = reinterpret_cast<unsigned*>(smem + off);
+    off += ((size_t)4 * nseg + 15) & ~(size_t)15;
+    float2* s_tw = reinterpret_cast<float2*>(smem + off);
+    off += sizeof(float2) * kTwiddleTable;
+    uint16_t* s_rev = reinterpret_cast<uint16_t*>(smem + off);
+    off += ((size_t)2 * M + 15) & ~(size_t)15;
+    int* s_red = reinterpret_cast<int*>(smem + off);
     for (int i = tid; i < kTwiddleTable; i += NT) s_tw[i] = __ldg(&P.tw[i]);
+    for (int i = tid; i < M; i += NT) s_rev[i] = __ldg(&P.rev[i]);
     const TwiddleSplit tw_m{s_tw, s_tw + 64};         // W_M
     const TwiddleSplit tw_np{s_tw + 256, s_tw + 320};  // W_Np
+    const uint32_t lo = ev.mode == 0 ? band_off[gb] : 0u, hi = ev.mode == 0 ? band_off[gb + 1] : 0u;
 
 #pragma unroll 1
     for (int w = r0; w < r1; ++w) {
@@ -157,43 +192,19 @@ k_conv(const EventDesc ev, const UnitRec* __restrict__ recs, const uint32_t* __r
         if (ev.mode == 0) {
             {
                 int4* z4 = reinterpret_cast<int4*>(smem);
-                const int n4 = (2 * N + 3) / 4;
-                for (int i = tid; i < n4; i += NT) z4[i] = make_int4(0, 0, 0, 0);
+                for (int i = tid; i < (Np + 3) / 4; i += NT) z4[i] = make_int4(0, 0, 0, 0);
+                for (int i = tid; i < nseg; i += NT) segb[i] = 0u;
             }
             __syncthreads();
-            const uint32_t lo = band_off[gb], hi = band_off[gb + 1];
-#pragma unroll 1
-            for (uint32_t c0 = lo; c0 < hi; c0 += kChunk) {
-                if (c0 != lo) {
-                    // carry lo into hi so the next chunk cannot overflow the lo words
-                    __syncthreads();
-                    for (int t = tid; t < N; t += NT) {
-                        acc_hi[t] += (int)(acc_lo[t] >> kLoBits);
-                        acc_lo[t] &= kLoMask;
-                    }
-                    __syncthreads();
-                }
-                if (!(flags & 8))  // profiling switch: skip the scatter
-                    accumulate_row<NT>(P, w, raw, acc_lo, acc_hi, pool, band_list, c0, min(hi, c0 + kChunk),
-                                   flags & 48);
-            }
+            float inv;
+            scatter_row<NT>(P, w, raw, acc, segb, s_red, nseg, pool, band_list, lo, hi, inv);
             __syncthreads();
-            // fixed point -> fp32 in place (xs[t] overlays acc_lo[t], same thread):
-            // normalise lo < 2^20, then one rounding of hi 2^20 + lo (FFMA)
-            for (int t = tid; t < N; t += NT) {
-                const uint32_t l = acc_lo[t];
-                const int hh = acc_hi[t] + (int)(l >> kLoBits);
-                const float lf = __int_as_float(0x4B000000 | (l & kLoMask)) - 8388608.0f;
-                const float x = fmaf(__int2float_rn(hh), 1048576.0f, lf) * kFixInvF;
+            for (int t = tid; t < N; t += NT) {  // int -> float in place (same index, same thread)
+                const float x = (float)acc[t] * inv;
                 xs[t] = x;
                 if (crow) __stcs(&crow[t], x);
             }
-            if (Np > N) {
-                __syncthreads();  // acc_hi (overlaid by xs[N..Np)) fully read
-                for (int t = N + tid; t < Np; t += NT) xs[t] = 0.0f;
-            }
         } else {
-            // charge grid source with the cross-wire stencil
             for (int t = tid; t < Np; t += NT) {
                 float s = 0.0f;
                 if (t < N) {
@@ -208,29 +219,25 @@ k_conv(const EventDesc ev, const UnitRec* __restrict__ recs, const uint32_t* __r
         }
         __syncthreads();
         if (!want_frame) continue;
-        if (flags & 4) {  // profiling switch: skip the transforms, store S
-            for (int t = tid; t < N; t += NT) P.frame[(size_t)w * N + t] = xs[t];
-            __syncthreads();
-            continue;
-        }
 
-        float2* z = fft_forward<NT, MAXR>(bufA, bufB, M, P.fft, tw_m);
+        fft_dif<NT, MAXR>(buf, M, P.fft, tw_m);
 
-        // untangle -> multiply by H -> re-tangle (conjugated for the inverse)
+        // untangle -> multiply by H -> re-tangle (conjugated for the inverse);
+        // spectrum bin k lives at s_rev[k]
 #pragma unroll 2
         for (int k = tid; k <= M / 2; k += NT) {
             if (k == 0) {
-                const float2 z0 = z[0];
+                const int p0 = s_rev[0];
+                const float2 z0 = buf[p0];
                 const float x0 = z0.x + z0.y, xm = z0.x - z0.y;  // X[0], X[M]
-                const float2 h0 = __ldg(&P.H[0]), hm = __ldg(&P.H[M]);
-                const float2 y0 = cscale(h0, x0), ym = cscale(hm, xm);
+                const float2 y0 = cscale(__ldg(&P.H[0]), x0), ym = cscale(__ldg(&P.H[M]), xm);
                 const float2 ye = cscale(cadd(y0, ym), 0.5f);
                 const float2 yo = cscale(csub(y0, ym), 0.5f);
-                // Z' = ye + i*yo ; store conj(Z')
-                z[0] = make_float2(ye.x - yo.y, -(ye.y + yo.x));
+                buf[p0] = make_float2(ye.x - yo.y, -(ye.y + yo.x));  // conj(ye + i yo)
             } else {
                 const int kk = M - k;
-                const float2 a = z[k], b = z[kk];
+                const int pk = s_rev[k], pkk = s_rev[kk];
+                const float2 a = buf[pk], b = buf[pkk];
                 const float2 wk = tw_np(k);                   // exp(-2 pi i k / Np)
                 const float2 wkk = make_float2(-wk.x, wk.y);  // exp(-2 pi i (M-k) / Np) = -conj(wk)
                 // X[k] = E + W^k O with E = (a + conj b)/2, O = (a - conj b)/(2i)
@@ -247,34 +254,32 @@ k_conv(const EventDesc ev, const UnitRec* __restrict__ recs, const uint32_t* __r
                 const float2 yo1 = cmul(cscale(csub(yk, cconj(ykk)), 0.5f), cconj(wk));
                 const float2 ye2 = cscale(cadd(ykk, cconj(yk)), 0.5f);
                 const float2 yo2 = cmul(cscale(csub(ykk, cconj(yk)), 0.5f), cconj(wkk));
-                z[k] = make_float2(ye1.x - yo1.y, -(ye1.y + yo1.x));
-                if (kk != k) z[kk] = make_float2(ye2.x - yo2.y, -(ye2.y + yo2.x));
+                buf[pk] = make_float2(ye1.x - yo1.y, -(ye1.y + yo1.x));
+                if (kk != k) buf[pkk] = make_float2(ye2.x - yo2.y, -(ye2.y + yo2.x));
             }
         }
         __syncthreads();
 
-        float2* other = (z == bufA) ? bufB : bufA;
-        const float2* y2 = fft_forward<NT, MAXR>(z, other, M, P.fft, tw_m);
+        fft_dit<NT, MAXR>(buf, M, P.fft, tw_m);
 
         // y[2n] = Re res[n], y[2n+1] = -Im res[n]  (1/M folded into H)
         float* frow = P.frame + (size_t)w * N;
-        const float* yr = reinterpret_cast<const float*>(y2);
-        const int hi_wrap = P.hi_lag;           // t < hi_wrap: + y[t + N]
-        const int lo_wrap = N + P.lo_lag;       // t >= lo_wrap: + y[t - N + Np]
+        const int hi_wrap = P.hi_lag;      // t < hi_wrap: + y[t + N]
+        const int lo_wrap = N + P.lo_lag;  // t >= lo_wrap: + y[t - N + Np]
 #pragma unroll 4
         for (int t = tid; t < N; t += NT) {
-            float y = (t & 1) ? -yr[t] : yr[t];
+            float y = (t & 1) ? -xs[t] : xs[t];
             if (P.folded) {
                 if (t < hi_wrap) {
                     const int tt = t + N;
-                    y += (tt & 1) ? -yr[tt] : yr[tt];
+                    y += (tt & 1) ? -xs[tt] : xs[tt];
                 }
                 if (t >= lo_wrap) {
                     const int tt = t - N + Np;
-                    y += (tt & 1) ? -yr[tt] : yr[tt];
+                    y += (tt & 1) ? -xs[tt] : xs[tt];
                 }
             }
-            __stcs(&frow[t], y);  // streaming store: the frame must not evict the band data from L2
+            __stcs(&frow[t], y);  // streaming store: keep the band data in L2
         }
         __syncthreads();
     }
@@ -282,10 +287,18 @@ k_conv(const EventDesc ev, const UnitRec* __restrict__ recs, const uint32_t* __r
 
 }  // namespace wsb
 
-// launch helper used by ws_api.cu
-extern "C" cudaError_t wsb_launch_conv(const wsb::EventDesc& ev, const wsb::UnitRec* recs, const uint32_t* pool,
-                                       const uint32_t* band_off, const wsb::UnitRec* band_list, int flags,
-                                       size_t smem_bytes, int threads, cudaStream_t stream)
+extern "C" size_t wsb_conv_smem(int N, int Np, int M)
+{
+    const int nseg = (N + 63) >> wsb::kSegShift;
+    return (((size_t)4 * Np + 15) & ~(size_t)15) + (((size_t)4 * nseg + 15) & ~(size_t)15) +
+           sizeof(float2) * wsb::kTwiddleTable + (((size_t)2 * M + 15) & ~(size_t)15) + 4 * 32;
+}
+
+// Variants: 256 threads x 3 CTAs/SM (85 registers, radices up to 25) or
+// 256 threads x 4 CTAs/SM (64 registers, radices up to 8).
+extern "C" cudaError_t wsb_launch_conv(const wsb::EventDesc& ev, const uint32_t* pool, const uint32_t* band_off,
+                                       const wsb::UnitRec* band_list, int flags, size_t smem_bytes, int variant,
+                                       cudaStream_t stream)
 {
     // once per device: shared-memory opt-in and the composite-radix twiddles
     static unsigned long long ready = 0;
@@ -293,16 +306,16 @@ extern "C" cudaError_t wsb_launch_conv(const wsb::EventDesc& ev, const wsb::Unit
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     if (!(ready & (1ull << dev))) {
-        e = cudaFuncSetAttribute(wsb::k_conv<256, 25>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        e = cudaFuncSetAttribute(wsb::k_conv<256, 25, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(wsb::k_conv<512, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        e = cudaFuncSetAttribute(wsb::k_conv<256, 8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e != cudaSuccess) return e;
         float2 host[wsb::kCompositeTwiddles] = {};
         for (int R : {10, 14, 16, 20, 24, 25, 28, 32, 35, 40, 49}) {
-            const int off = wsb::comp_off(R);
+            const int o = wsb::comp_off(R);
             for (int m = 0; m < R; ++m) {
                 const double a = -6.283185307179586476925286766559 * (double)m / (double)R;
-                host[off + m] = make_float2((float)cos(a), (float)sin(a));
+                host[o + m] = make_float2((float)cos(a), (float)sin(a));
             }
         }
         e = cudaMemcpyToSymbol(wsb::c_wr, host, sizeof(host));
@@ -310,9 +323,9 @@ extern "C" cudaError_t wsb_launch_conv(const wsb::EventDesc& ev, const wsb::Unit
         ready |= 1ull << dev;
     }
     if (ev.total_bands == 0) return cudaSuccess;
-    if (threads == 512)
-        wsb::k_conv<512, 8><<<ev.total_bands, 512, smem_bytes, stream>>>(ev, recs, pool, band_off, band_list, flags);
+    if (variant == 8)
+        wsb::k_conv<256, 8, 4><<<ev.total_bands, 256, smem_bytes, stream>>>(ev, pool, band_off, band_list, flags);
     else
-        wsb::k_conv<256, 25><<<ev.total_bands, 256, smem_bytes, stream>>>(ev, recs, pool, band_off, band_list, flags);
+        wsb::k_conv<256, 25, 3><<<ev.total_bands, 256, smem_bytes, stream>>>(ev, pool, band_off, band_list, flags);
     return cudaGetLastError();
 }

@@ -245,92 +245,138 @@ template <> struct Dft<32> : DftComp<8, 4> {};
 template <> struct Dft<35> : DftComp<5, 7> {};
 template <> struct Dft<40> : DftComp<8, 5> {};
 
-// Per-pass plan (host-built, ws_api.cu): radix, Ns = product of the earlier
-// radices, magic = ceil(2^32 / Ns) for j mod Ns, and the twiddle step
-// M / (Ns R): the pass twiddle W_{Ns R}^{k r} is W_M^{k r step}.
+// ---------------------------------------------------------------------------
+// In-place mixed-radix DIF / DIT pair for convolution (no digit reversal pass).
+//
+// DIF (Sande-Tukey) with radices R_0..R_{P-1}: pass p has sub-transforms of
+// length L_p = M / (R_0..R_{p-1}) and stride S_p = L_p / R_p; butterfly
+// (block b, offset j < S_p) reads x[b L_p + j + r S_p], runs DFT_R, multiplies
+// output q by W_{L_p}^{j q}, writes back to the same slots. The result X[k]
+// lands at pos(k) = sum_p q_p M / (R_0..R_p) for k = sum_p q_p R_0..R_{p-1}.
+// DIT (Cooley-Tukey) with the radices reversed consumes exactly that order and
+// returns natural order: butterfly (b, j < Lam_p) pre-multiplies x_r by
+// W_{Lam_p R}^{j r}, runs DFT_R, writes back. Each butterfly touches only its
+// own slots, so a pass needs a single barrier and one row of shared memory.
 struct FftPlanDev {
     int npass;
-    int radix[12];
-    int ns[12];
-    uint32_t magic[12];
-    int step[12];
+    int radix[12];        // DIF order; DIT runs radix[npass-1-p] at pass p
+    int dif_s[12];        // S_p
+    uint32_t dif_mg[12];  // ceil(2^32 / S_p)
+    int dif_step[12];     // M / L_p: W_{L_p}^{jq} = W_M^{jq step}
+    int dit_lam[12];      // Lam_p
+    uint32_t dit_mg[12];  // ceil(2^32 / Lam_p)
+    int dit_step[12];     // M / (Lam_p R)
 };
 
-// W_M^m from two 64-way shared-memory tables: lo[j] = W_M^j, hi[i] = W_M^{64 i}
-// (2.5 KB for M <= 12288 instead of an M-entry table that thrashes L1).
+// W_M^m from two 64-way shared-memory tables: lo[j] = W_M^j, hi[i] = W_M^{64 i}.
 struct TwiddleSplit {
     const float2* lo;
     const float2* hi;
     __device__ __forceinline__ float2 operator()(int m) const { return cmul(hi[m >> 6], lo[m & 63]); }
 };
 
-// One out-of-place Stockham radix-R pass: butterfly j reads in[j + r*M/R],
-// applies W_{Ns R}^{k r} with k = j mod Ns, runs Dft<R>, and writes
-// out[(j/Ns)*Ns*R + k + r*Ns]. One barrier per pass.
+__device__ __forceinline__ int fast_div(int a, int d, uint32_t mg) { return d > 1 ? (int)__umulhi((uint32_t)a, mg) : a; }
+
 template <int R, int NT>
-__device__ __forceinline__ void stockham_pass(const float2* __restrict__ in, float2* __restrict__ out, int M, int Ns,
-                                              uint32_t ns_magic, int step, const TwiddleSplit& tw)
+__device__ __forceinline__ void dif_pass(float2* __restrict__ x, int M, int S, uint32_t mg, int step,
+                                         const TwiddleSplit& tw)
 {
-    const int nb = M / R;
+    const int L = S * R;
 #pragma unroll 1
-    for (int j = threadIdx.x; j < nb; j += NT) {
+    for (int g = threadIdx.x; g < M / R; g += NT) {
+        const int b = fast_div(g, S, mg);
+        const int j = g - b * S;
+        float2* p = x + b * L + j;
         float2 v[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[r] = in[j + r * nb];
-        // k = j mod Ns via a multiply-high (exact for j, Ns < 2^16)
-        const int k = Ns > 1 ? j - Ns * (int)__umulhi((uint32_t)j, ns_magic) : 0;
-        if (Ns > 1) {
-            const int dm = k * step;  // m = k r step < M for r < R
+        for (int r = 0; r < R; ++r) v[r] = p[r * S];
+        Dft<R>::run(v);
+        if (j) {
+            const int dm = j * step;
+            int m = dm;
+#pragma unroll
+            for (int q = 1; q < R; ++q, m += dm) v[DftPos<R>::pos(q)] = cmul(v[DftPos<R>::pos(q)], tw(m));
+        }
+#pragma unroll
+        for (int q = 0; q < R; ++q) p[q * S] = v[DftPos<R>::pos(q)];
+    }
+}
+
+template <int R, int NT>
+__device__ __forceinline__ void dit_pass(float2* __restrict__ x, int M, int Lam, uint32_t mg, int step,
+                                         const TwiddleSplit& tw)
+{
+    const int L = Lam * R;
+#pragma unroll 1
+    for (int g = threadIdx.x; g < M / R; g += NT) {
+        const int b = fast_div(g, Lam, mg);
+        const int j = g - b * Lam;
+        float2* p = x + b * L + j;
+        float2 v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = p[r * Lam];
+        if (j) {
+            const int dm = j * step;
             int m = dm;
 #pragma unroll
             for (int r = 1; r < R; ++r, m += dm) v[r] = cmul(v[r], tw(m));
         }
         Dft<R>::run(v);
-        const int base = (j - k) * R + k;
 #pragma unroll
-        for (int r = 0; r < R; ++r) out[base + r * Ns] = v[DftPos<R>::pos(r)];
+        for (int q = 0; q < R; ++q) p[q * Lam] = v[DftPos<R>::pos(q)];
     }
-    __syncthreads();
 }
 
-// Forward FFT of length M from buffer a, ping-ponging with buffer b. Returns
-// the buffer holding the (natural-order) result.
-// Only radices <= MAXR are instantiated (the host planner respects the same
-// bound), so a 512-thread build keeps its 64-register budget.
+#define WSB_RADIX_SWITCH(R_, CALL)                     \
+    switch (R_) {                                      \
+        case 2: CALL(2); break;                        \
+        case 3: CALL(3); break;                        \
+        case 4: CALL(4); break;                        \
+        case 5: CALL(5); break;                        \
+        case 7: CALL(7); break;                        \
+        case 8: CALL(8); break;                        \
+        default:                                       \
+            if constexpr (MAXR >= 25) {                \
+                switch (R_) {                          \
+                    case 10: CALL(10); break;          \
+                    case 14: CALL(14); break;          \
+                    case 16: CALL(16); break;          \
+                    case 20: CALL(20); break;          \
+                    case 24: CALL(24); break;          \
+                    default: CALL(25); break;          \
+                }                                      \
+            }                                          \
+            break;                                     \
+    }
+
+// forward DFT, natural order in, digit-reversed (pos) order out
 template <int NT, int MAXR>
-__device__ __forceinline__ float2* fft_forward(float2* a, float2* b, int M, const FftPlanDev& plan,
-                                               const TwiddleSplit& t)
+__device__ __forceinline__ void fft_dif(float2* x, int M, const FftPlanDev& pl, const TwiddleSplit& tw)
 {
 #pragma unroll 1
-    for (int p = 0; p < plan.npass; ++p) {
-        const int Ns = plan.ns[p];
-        const uint32_t mg = plan.magic[p] ;
-        const int st = plan.step[p];
-        switch (plan.radix[p]) {
-            case 2: stockham_pass<2, NT>(a, b, M, Ns, mg, st, t); break;
-            case 3: stockham_pass<3, NT>(a, b, M, Ns, mg, st, t); break;
-            case 4: stockham_pass<4, NT>(a, b, M, Ns, mg, st, t); break;
-            case 5: stockham_pass<5, NT>(a, b, M, Ns, mg, st, t); break;
-            case 7: stockham_pass<7, NT>(a, b, M, Ns, mg, st, t); break;
-            case 8: stockham_pass<8, NT>(a, b, M, Ns, mg, st, t); break;
-            default:
-                if constexpr (MAXR >= 25) {
-                    switch (plan.radix[p]) {
-                        case 10: stockham_pass<10, NT>(a, b, M, Ns, mg, st, t); break;
-                        case 14: stockham_pass<14, NT>(a, b, M, Ns, mg, st, t); break;
-                        case 16: stockham_pass<16, NT>(a, b, M, Ns, mg, st, t); break;
-                        case 20: stockham_pass<20, NT>(a, b, M, Ns, mg, st, t); break;
-                        case 24: stockham_pass<24, NT>(a, b, M, Ns, mg, st, t); break;
-                        default: stockham_pass<25, NT>(a, b, M, Ns, mg, st, t); break;
-                    }
-                }
-                break;
-        }
-        float2* tmp = a;
-        a = b;
-        b = tmp;
+    for (int p = 0; p < pl.npass; ++p) {
+        const int S = pl.dif_s[p], st = pl.dif_step[p];
+        const uint32_t mg = pl.dif_mg[p];
+#define WSB_DIF(R) dif_pass<R, NT>(x, M, S, mg, st, tw)
+        WSB_RADIX_SWITCH(pl.radix[p], WSB_DIF)
+#undef WSB_DIF
+        __syncthreads();
     }
-    return a;
+}
+
+// forward DFT, digit-reversed (pos) order in, natural order out
+template <int NT, int MAXR>
+__device__ __forceinline__ void fft_dit(float2* x, int M, const FftPlanDev& pl, const TwiddleSplit& tw)
+{
+#pragma unroll 1
+    for (int p = 0; p < pl.npass; ++p) {
+        const int lam = pl.dit_lam[p], st = pl.dit_step[p];
+        const uint32_t mg = pl.dit_mg[p];
+#define WSB_DIT(R) dit_pass<R, NT>(x, M, lam, mg, st, tw)
+        WSB_RADIX_SWITCH(pl.radix[pl.npass - 1 - p], WSB_DIT)
+#undef WSB_DIT
+        __syncthreads();
+    }
 }
 
 }  // namespace wsb

@@ -147,7 +147,8 @@ __global__ void k_sample(const EventDesc ev, UnitRec* __restrict__ recs, uint32_
     rec.n_t = 0;
     rec.pool = 0;
     rec.plane = pi;
-    rec.a = 0.0;
+    rec.a = 0.0f;
+    rec.tmax = 0.0f;
     if (ev.drift_enabled && !drift(ev, d)) {
         atomicOr(err, kErrDomain);
         recs[u] = rec;
@@ -208,7 +209,8 @@ __global__ void k_sample(const EventDesc ev, UnitRec* __restrict__ recs, uint32_
                 eff[j] = (float)e;
             }
         }
-        rec.a = a;
+        rec.a = (float)a;
+        rec.tmax = (float)mt;
     }
     rec.w0 = f.w0;
     rec.t0 = f.t0;
