@@ -135,6 +135,16 @@ int ws_ctx_create(int device, void* stream, ws_ctx** out);
 int ws_ctx_destroy(ws_ctx* ctx);
 int ws_ctx_synchronize(ws_ctx* ctx);
 void* ws_ctx_stream(ws_ctx* ctx);
+/* Convolution path for fluctuation-off frames. AUTO routes every band of
+ * wire rows to the cheaper of the two kernels from its depo load (sparse
+ * bands: time-domain accumulation of per-depo response profiles; dense
+ * bands: per-row FFT); FFT and DIRECT force one kernel (testing, tuning).
+ * Both compute the reference's circular convolution (spectral.cpp:141-175). */
+enum { WS_CONV_AUTO = 0, WS_CONV_FFT = 1, WS_CONV_DIRECT = 2 };
+int ws_ctx_set_conv_path(ws_ctx* ctx, int path);
+/* AUTO routing threshold: a band takes the time-domain kernel while the sum
+ * of its depos' response-profile lengths is <= kappa x transform length. */
+int ws_ctx_set_direct_kappa(ws_ctx* ctx, double kappa);
 /* Number of CUDA kernels this context has launched so far. */
 uint64_t ws_ctx_launch_count(const ws_ctx* ctx);
 

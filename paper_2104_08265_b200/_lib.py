@@ -81,6 +81,8 @@ SIGNATURES = {
     "ws_ctx_synchronize": (C.c_int, [_P]),
     "ws_ctx_stream": (_P, [_P]),
     "ws_ctx_launch_count": (C.c_uint64, [_P]),
+    "ws_ctx_set_conv_path": (C.c_int, [_P, C.c_int]),
+    "ws_ctx_set_direct_kappa": (C.c_int, [_P, C.c_double]),
     "ws_plane_create": (C.c_int, [_P, C.POINTER(GridSpecC), C.POINTER(ResponseC), C.c_double, C.POINTER(_P)]),
     "ws_plane_destroy": (C.c_int, [_P]),
     "ws_plane_get_info": (C.c_int, [_P, C.POINTER(PlaneInfoC)]),

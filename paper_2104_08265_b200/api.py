@@ -124,6 +124,17 @@ class Context:
     def launch_count(self) -> int:
         return int(self.lib.ws_ctx_launch_count(self.handle))
 
+    CONV_PATHS = {"auto": 0, "fft": 1, "direct": 2}
+
+    def set_conv_path(self, path: str):
+        """Fluctuation-off convolution kernel: "auto" (per band of wire rows,
+        the cheaper of time-domain accumulation and row FFT), "fft", "direct"."""
+        check(self.lib.ws_ctx_set_conv_path(self.handle, self.CONV_PATHS[path]))
+
+    def set_direct_kappa(self, kappa: float):
+        """"auto" routing threshold (time-domain work per band <= kappa x transform length)."""
+        check(self.lib.ws_ctx_set_direct_kappa(self.handle, float(kappa)))
+
     def close(self):
         if self.handle:
             self.lib.ws_ctx_destroy(self.handle)

@@ -22,17 +22,24 @@ using wsb::PlaneDesc;
 using wsb::UnitRec;
 
 extern "C" cudaError_t wsb_launch_sample(const EventDesc& ev, UnitRec* recs, uint32_t* pool, uint32_t pool_cap,
-                                         uint32_t* pool_ctr, uint32_t* band_count, unsigned* err, cudaStream_t s);
-extern "C" cudaError_t wsb_launch_scan(const uint32_t* count, uint32_t* off, uint32_t* fill, uint32_t n,
-                                       cudaStream_t s);
+                                         uint32_t* pool_ctr, uint32_t* band_count, uint32_t* band_cost, unsigned* err,
+                                         cudaStream_t s);
+extern "C" cudaError_t wsb_launch_scan(const EventDesc& ev, const uint32_t* count, const uint32_t* cost, uint32_t* off,
+                                       uint32_t* fill, uint32_t n, uint32_t* maps, uint32_t* map_count, cudaStream_t s);
 extern "C" cudaError_t wsb_launch_fill(const EventDesc& ev, const UnitRec* recs, const uint32_t* off, uint32_t* fill,
                                        UnitRec* list, cudaStream_t s);
+extern "C" cudaError_t wsb_launch_gprof(const EventDesc& ev, const UnitRec* recs, uint32_t* pool, cudaStream_t s);
+extern "C" size_t wsb_direct_smem(int N, int cap);
+extern "C" int wsb_direct_cap(int N);
+extern "C" cudaError_t wsb_launch_direct(const EventDesc& ev, const uint32_t* pool, const uint32_t* band_off,
+                                         const UnitRec* band_list, const uint32_t* map, const uint32_t* map_count,
+                                         size_t smem_bytes, cudaStream_t stream);
 extern "C" cudaError_t wsb_launch_fluctuate(const EventDesc& ev, const UnitRec* recs, const uint32_t* pool,
                                             const uint32_t* order, cudaStream_t s);
 extern "C" size_t wsb_conv_smem(int N, int Np, int M);
 extern "C" cudaError_t wsb_launch_conv(const EventDesc& ev, const uint32_t* pool, const uint32_t* band_off,
-                                       const UnitRec* band_list, int flags, size_t smem_bytes, int variant,
-                                       cudaStream_t stream);
+                                       const UnitRec* band_list, const uint32_t* map, const uint32_t* map_count,
+                                       int flags, size_t smem_bytes, int variant, cudaStream_t stream);
 
 namespace {
 
@@ -109,7 +116,8 @@ struct ws_ctx {
     uint64_t launches = 0;
     DevBuf<UnitRec> recs;
     DevBuf<uint32_t> pool;
-    DevBuf<uint32_t> band_count, band_off, band_fill;
+    DevBuf<uint32_t> band_count, band_off, band_fill, band_cost;
+    DevBuf<uint32_t> band_maps;  // [direct bands | fft bands | counts(2)] from k_scan_bands
     DevBuf<UnitRec> band_list;  // CSR lists of full unit records (copied by k_fill_bands)
     DevBuf<ScratchHeader> header;
     DevBuf<ws_depo> depos;
@@ -121,6 +129,8 @@ struct ws_ctx {
     size_t pool_hint = 0;
     int sm_count = 0;
     int conv_variant = 25;                       // k_conv: 25 (3 CTAs/SM, radix <= 25) or 8 (4 CTAs/SM, radix <= 8)
+    int conv_path = WS_CONV_AUTO;                // ws_ctx_set_conv_path
+    double direct_kappa = 48.0;                  // AUTO: direct if sum of profile lengths <= kappa x Np per band
     cudaStream_t copy_stream = nullptr;          // D2H of the pipelined batch path
     cudaEvent_t slot_computed[2] = {nullptr, nullptr};
     cudaEvent_t slot_copied[2] = {nullptr, nullptr};
@@ -137,6 +147,10 @@ struct ws_plane {
     wsb::FftPlanDev plan{};
     double* d_ww = nullptr;
     float2* d_H = nullptr;
+    float* d_kern = nullptr;  // combined kernel taps (fp32) for the direct path
+    int direct_ok = 0;
+    int direct_cap = 0;  // staged entries per band in k_direct
+    size_t direct_smem = 0;
     float2* d_tw = nullptr;
     uint16_t* d_rev = nullptr;
     int ww_is_one = 0;
@@ -331,6 +345,11 @@ PlaneDesc plane_desc(const ws_plane* p)
     d.tw = p->d_tw;
     d.rev = p->d_rev;
     d.rows_per_band = p->rows_per_band;
+    d.n_lags = (int)p->n_lags;
+    d.kern = p->d_kern ? p->d_kern + wsb::kKernPad : nullptr;
+    d.direct_ok = 0;  // decided per call (run_group)
+    d.direct_thr = 0;
+    d.direct_cap = (uint32_t)p->direct_cap;
     d.n_bands = p->n_bands;
     return d;
 }
@@ -368,9 +387,9 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
     const bool from_grid = charge_in != nullptr;
     ev.mode = (from_grid || ev.fluctuate) ? 1 : 0;
     uint32_t units = 0, bands = 0;
-    int need_raw = 0;
-    size_t smem = 0;
-    bool want_frame = false;
+    size_t smem = 0, smem_direct = 0;
+    bool want_frame = false, any_direct = false;
+    int max_lags = 0;
     for (uint32_t i = 0; i < n; ++i) {
         ws_plane* p = planes[i];
         PlaneDesc d = plane_desc(p);
@@ -382,10 +401,18 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
         d.charge_out = charges ? charges[i] : nullptr;
         d.charge_in = from_grid ? charge_in[i] : (ev.fluctuate ? charges[i] : nullptr);
         d.stats = nullptr;
+        // time-domain path: fluctuation-off accumulation into a frame
+        if (ev.mode == 0 && d.frame && p->direct_ok && c->conv_path != WS_CONV_FFT) {
+            d.direct_ok = 1;
+            const double thr = c->conv_path == WS_CONV_DIRECT ? 4.0e9 : c->direct_kappa * (double)p->Np;
+            d.direct_thr = (uint32_t)std::min(thr, 4.0e9);
+            any_direct = true;
+            smem_direct = std::max(smem_direct, p->direct_smem);
+            max_lags = std::max(max_lags, (int)p->n_lags);
+        }
         ev.p[i] = d;
         units += d.n_units;
         bands += (uint32_t)p->n_bands;
-        need_raw = need_raw || !p->ww_is_one;
         smem = std::max(smem, p->smem);
         want_frame = want_frame || d.frame != nullptr;
     }
@@ -393,12 +420,14 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
     ev.total_bands = bands;
 
     // workspace
-    const size_t pool_need = std::max<size_t>(c->pool_hint, (size_t)units * 96 + 4096);
+    const size_t pool_need = std::max<size_t>(c->pool_hint, (size_t)units * (96 + (any_direct ? max_lags + 36 : 0)) + 4096);
     WS_CUDA(c->recs.reserve(units));
     WS_CUDA(c->pool.reserve(pool_need));
     WS_CUDA(c->band_count.reserve(bands + 1));
     WS_CUDA(c->band_off.reserve(bands + 1));
     WS_CUDA(c->band_fill.reserve(bands + 1));
+    WS_CUDA(c->band_cost.reserve(bands + 1));
+    WS_CUDA(c->band_maps.reserve(2 * (size_t)bands + 2));
     int max_h = 0;
     for (uint32_t i = 0; i < n; ++i) max_h = std::max(max_h, planes[i]->h);
     WS_CUDA(c->band_list.reserve(c->pool.cap + (size_t)units * (2 * max_h + 2) + 16));
@@ -414,13 +443,16 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
 
     WS_CUDA(cudaEventRecord(pc.ev[0], s));
     WS_CUDA(cudaMemsetAsync(hdr, 0, sizeof(ScratchHeader), s));
-    if (ev.mode == 0) WS_CUDA(cudaMemsetAsync(c->band_count.p, 0, sizeof(uint32_t) * (bands + 1), s));
+    if (ev.mode == 0) {
+        WS_CUDA(cudaMemsetAsync(c->band_count.p, 0, sizeof(uint32_t) * (bands + 1), s));
+        WS_CUDA(cudaMemsetAsync(c->band_cost.p, 0, sizeof(uint32_t) * (bands + 1), s));
+    }
     if (ev.fluctuate && !from_grid)
         for (uint32_t i = 0; i < n; ++i)
             WS_CUDA(cudaMemsetAsync(ev.p[i].charge_out, 0, sizeof(float) * (size_t)ev.p[i].W * ev.p[i].N, s));
     if (!from_grid) {
         WS_CUDA(wsb_launch_sample(ev, c->recs.p, c->pool.p, (uint32_t)std::min<size_t>(c->pool.cap, 0xffffffffu),
-                                  &hdr->pool_ctr, c->band_count.p, &hdr->err, s));
+                                  &hdr->pool_ctr, c->band_count.p, c->band_cost.p, &hdr->err, s));
         c->launches += units ? 1 : 0;
     }
     WS_CUDA(cudaEventRecord(pc.ev[1], s));
@@ -429,35 +461,39 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
         c->launches += units ? 1 : 0;
     }
     WS_CUDA(cudaEventRecord(pc.ev[2], s));
+    uint32_t* maps = c->band_maps.p;
+    uint32_t* map_count = maps + 2 * (size_t)bands;
     if (ev.mode == 0) {
-        WS_CUDA(wsb_launch_scan(c->band_count.p, c->band_off.p, c->band_fill.p, bands, s));
+        WS_CUDA(wsb_launch_scan(ev, c->band_count.p, c->band_cost.p, c->band_off.p, c->band_fill.p, bands, maps,
+                                map_count, s));
         WS_CUDA(wsb_launch_fill(ev, c->recs.p, c->band_off.p, c->band_fill.p, c->band_list.p, s));
         c->launches += 1 + (units ? 1 : 0);
+        if (any_direct) {
+            WS_CUDA(wsb_launch_gprof(ev, c->recs.p, c->pool.p, s));
+            c->launches += units ? 1 : 0;
+        }
     }
     WS_CUDA(cudaEventRecord(pc.ev[3], s));
-    // WS_PROFILE_CONV_FLAGS: profiling-only switches of the ping-pong k_conv
-    // (4: skip the transforms, 8: skip the scatter) to split its time
-    static const int prof_flags = [] {
-        const char* e = getenv("WS_PROFILE_CONV_FLAGS");
-        return e ? (atoi(e) & 60) : 0;
-    }();
-    // WS_PROFILE_SMEM_PAD: profiling-only extra shared memory per CTA (occupancy sensitivity)
-    static const size_t smem_pad = [] {
-        const char* e = getenv("WS_PROFILE_SMEM_PAD");
-        return e ? (size_t)atol(e) : (size_t)0;
-    }();
-    auto launch_conv = [&](int flags) -> cudaError_t {
-        return wsb_launch_conv(ev, c->pool.p, c->band_off.p, c->band_list.p, flags | prof_flags, smem + smem_pad,
-                               c->conv_variant, s);
-    };
-    if (ev.mode == 0 && charges && need_raw) {
-        // the charge grid is the un-stencilled S: one extra accumulate-only pass
-        WS_CUDA(launch_conv(2));
+    if (ev.mode == 0 && charges) {
+        // the charge grid is the un-stencilled S: an accumulate-only pass of
+        // the row kernel over every band (parity / inspection output)
+        WS_CUDA(wsb_launch_conv(ev, c->pool.p, c->band_off.p, c->band_list.p, nullptr, nullptr, 2, smem,
+                                c->conv_variant, s));
         c->launches += bands ? 1 : 0;
     }
-    if (want_frame || (ev.mode == 0 && charges && !need_raw)) {
-        WS_CUDA(launch_conv(want_frame ? 1 : 0));
-        c->launches += bands ? 1 : 0;
+    if (want_frame) {
+        if (any_direct) {
+            // bands routed by k_scan_bands: sparse ones to the time-domain
+            // kernel, dense ones to the row FFT
+            WS_CUDA(wsb_launch_direct(ev, c->pool.p, c->band_off.p, c->band_list.p, maps, map_count, smem_direct, s));
+            WS_CUDA(wsb_launch_conv(ev, c->pool.p, c->band_off.p, c->band_list.p, maps + bands, map_count + 1, 1, smem,
+                                    c->conv_variant, s));
+            c->launches += bands ? 2 : 0;
+        } else {
+            WS_CUDA(wsb_launch_conv(ev, c->pool.p, c->band_off.p, c->band_list.p, nullptr, nullptr, 1, smem,
+                                    c->conv_variant, s));
+            c->launches += bands ? 1 : 0;
+        }
     }
     WS_CUDA(cudaEventRecord(pc.ev[4], s));
     // per-call copy of the header into a pinned slot, read at synchronize
@@ -547,6 +583,7 @@ int ws_ctx_create(int device, void* stream, ws_ctx** out)
     c->device = device;
     c->sm_count = prop.multiProcessorCount;
     if (const char* e = getenv("WS_CONV_VARIANT")) c->conv_variant = atoi(e) == 8 ? 8 : 25;
+    if (const char* e = getenv("WS_DIRECT_KAPPA")) c->direct_kappa = atof(e);
     if (stream) {
         c->stream = (cudaStream_t)stream;
     } else {
@@ -576,6 +613,8 @@ int ws_ctx_destroy(ws_ctx* c)
     c->band_count.release();
     c->band_off.release();
     c->band_fill.release();
+    c->band_cost.release();
+    c->band_maps.release();
     c->band_list.release();
     c->header.release();
     c->depos.release();
@@ -606,6 +645,23 @@ int ws_ctx_synchronize(ws_ctx* c)
 }
 
 void* ws_ctx_stream(ws_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int ws_ctx_set_conv_path(ws_ctx* c, int path)
+{
+    if (!c) return set_err(WS_EINVAL, "null context");
+    if (path != WS_CONV_AUTO && path != WS_CONV_FFT && path != WS_CONV_DIRECT)
+        return set_err(WS_EINVAL, "unknown convolution path %d", path);
+    c->conv_path = path;
+    return WS_OK;
+}
+
+int ws_ctx_set_direct_kappa(ws_ctx* c, double kappa)
+{
+    if (!c) return set_err(WS_EINVAL, "null context");
+    if (!(kappa >= 0.0)) return set_err(WS_EINVAL, "direct-path threshold must be >= 0");
+    c->direct_kappa = kappa;
+    return WS_OK;
+}
 uint64_t ws_ctx_launch_count(const ws_ctx* c) { return c ? c->launches : 0; }
 
 int ws_plane_create(ws_ctx* ctx, const ws_grid_spec* grid, const ws_response* response, double n_sigma, ws_plane** out)
@@ -749,6 +805,21 @@ int ws_plane_create(ws_ctx* ctx, const ws_grid_spec* grid, const ws_response* re
     }
     p->n_bands = (p->W + p->rows_per_band - 1) / p->rows_per_band;
     p->smem = wsb_conv_smem(p->N, p->Np, p->M);
+    // time-domain path: kernel taps on the device; eligible while a band's
+    // fixed-point rows fit in shared memory and the kernel is not huge
+    p->direct_cap = wsb_direct_cap(p->N);
+    p->direct_smem = wsb_direct_smem(p->N, p->direct_cap);
+    if (p->direct_cap >= 64 && p->n_lags <= 4096) {
+        std::vector<float> kf(p->kernel.size() + 2 * wsb::kKernPad, 0.0f);
+        std::copy(p->kernel.begin(), p->kernel.end(), kf.begin() + wsb::kKernPad);
+        e = cudaMalloc(&p->d_kern, sizeof(float) * kf.size());
+        e = e ? e : cudaMemcpy(p->d_kern, kf.data(), sizeof(float) * kf.size(), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            ws_plane_destroy(p);
+            return set_err(WS_ECUDA, "plane upload: %s", cudaGetErrorString(e));
+        }
+        p->direct_ok = 1;
+    }
     if (p->smem > 227 * 1024) {
         ws_plane_destroy(p);
         return set_err(WS_EINVAL, "padded_ticks too large for the shared-memory row transform");
@@ -762,6 +833,7 @@ int ws_plane_destroy(ws_plane* p)
     if (!p) return WS_OK;
     if (p->ctx) cudaSetDevice(p->ctx->device);
     if (p->d_H) cudaFree(p->d_H);
+    if (p->d_kern) cudaFree(p->d_kern);
     if (p->d_tw) cudaFree(p->d_tw);
     if (p->d_rev) cudaFree(p->d_rev);
     if (p->d_ww) cudaFree(p->d_ww);

@@ -20,6 +20,7 @@ constexpr int kMaxWireWeights = 33;  // 2h+1 <= 33 taps of cross-wire coupling
 constexpr int kConvThreads = 256;
 constexpr int kTwiddleTable = 512;   // [W_M^j | W_M^{64i} | W_Np^j | W_Np^{64i}], 64 + 192 + 64 + 192
 constexpr int kMaxFftHalf = 12288;   // M = N'/2 <= 12288 (N' <= 24576 ticks)
+constexpr int kKernPad = 192;        // zero taps either side of PlaneDesc::kern (k_gprof window)
 constexpr double kFixScale = 4294967296.0;          // 2^32: fixed-point electrons
 constexpr double kFixInv = 1.0 / 4294967296.0;
 
@@ -53,6 +54,12 @@ struct PlaneDesc {
     const float2* H;           // M+1 response spectrum bins, pre-scaled by 1/M
     const float2* tw;          // split twiddle tables (kTwiddleTable entries, see ws_api.cu)
     const uint16_t* rev;       // rev[k] = slot of spectrum bin k after the DIF transform
+    // time-domain path (ws_direct.cu): per-depo response profiles g = tv (*) kernel
+    int32_t direct_ok;         // plane eligible for the direct path (pool holds g)
+    int32_t n_lags;            // combined kernel length
+    const float* kern;         // n_lags combined-kernel taps (lag lo_lag first), kKernPad zeros either side
+    uint32_t direct_thr;       // band -> direct path if sum of profile lengths <= thr
+    uint32_t direct_cap;       // k_direct stages at most this many entries at a time
     // per call
     const ws_depo* depos;
     uint32_t n_units;
@@ -82,6 +89,52 @@ struct EventDesc {
 
 // Error / overflow flags shared by kernels (device scalar words).
 enum : unsigned { kErrPool = 1u, kErrDomain = 2u, kErrCharge = 4u, kErrRange = 8u };
+
+__device__ __forceinline__ int band_plane(const EventDesc& ev, uint32_t gb)
+{
+    int p = 0;
+#pragma unroll 1
+    for (int i = 1; i < ev.n_planes; ++i)
+        if (gb >= ev.p[i].band_base) p = i;
+    return p;
+}
+
+// Pool layout of a fluctuation-off unit (32-bit words, see k_sample):
+//   [raw f32 x n_w][eff f32 x n_eff][tv f32 x n_t][pad to 16 B][g f32 x L][gmax f32]
+// the last two only when the plane is direct_ok; L = n_t + n_lags - 1.
+__device__ __forceinline__ int unit_n_eff(const PlaneDesc& P, int n_w) { return P.ww_is_one ? 0 : n_w + 2 * P.h; }
+__device__ __forceinline__ uint32_t unit_tv_off(const PlaneDesc& P, const UnitRec& r)
+{
+    return r.pool + (uint32_t)(r.n_w + unit_n_eff(P, r.n_w));
+}
+// g starts on a 16-byte boundary after tv (k_gprof stores float4s)
+__device__ __forceinline__ uint32_t unit_g_off(const PlaneDesc& P, const UnitRec& r)
+{
+    return (unit_tv_off(P, r) + (uint32_t)r.n_t + 3u) & ~3u;
+}
+
+// Coefficient of unit `r` on wire row w of the (stencilled unless raw) charge:
+// a * profile[j], j = (w - first row) mod W, summed over every wrap that lands
+// on the row (a tiny grid can be narrower than the stencilled footprint).
+// Returns false when the unit does not cover the row.
+__device__ __forceinline__ bool row_coef(const PlaneDesc& P, int w, bool raw, const UnitRec& r,
+                                         const uint32_t* __restrict__ pool, float& c)
+{
+    const int h = P.h;
+    const bool stencil = !raw && !P.ww_is_one;
+    const int lo_row = stencil ? r.w0 - h : r.w0;
+    const int n_rows = stencil ? r.n_w + 2 * h : r.n_w;
+    int j = w - lo_row;  // lo_row in [-h, W), w in [0, W)
+    if (j < 0) j += P.W;
+    else if (j >= P.W) j -= P.W;
+    if (j >= P.W) j %= P.W;  // grids narrower than the stencil
+    if (j >= n_rows) return false;
+    const float* prof = reinterpret_cast<const float*>(pool + r.pool) + (stencil ? r.n_w : 0);
+    float s = 0.0f;
+    for (; j < n_rows; j += P.W) s += __ldg(&prof[j]);
+    c = s * r.a;
+    return true;
+}
 
 __device__ __forceinline__ int plane_of_unit(const EventDesc& ev, uint32_t u)
 {

@@ -129,11 +129,14 @@ __device__ __forceinline__ void for_each_band(const PlaneDesc& P, int w0, int n_
 // Pool layout per unit (32-bit words):
 //   fluctuation on : [wv f64 x n_w][tv f64 x n_t]                 (8-byte aligned)
 //   fluctuation off: [raw f32 x n_w][eff f32 x n_eff][tv f32 x n_t]
+//                    (+ [g f32 x L][max|g|] on direct-path planes, filled by
+//                    k_fill_bands; L = n_t + n_lags - 1)
 // with raw = wv (the un-stencilled wire profile), eff = the profile after the
 // cross-wire stencil (absent when wire_weights == {1}); rec.a = q / total with
 // total = sum_w wv * sum_t tv.
 __global__ void k_sample(const EventDesc ev, UnitRec* __restrict__ recs, uint32_t* __restrict__ pool, uint32_t pool_cap,
-                         uint32_t* __restrict__ pool_ctr, uint32_t* __restrict__ band_count, unsigned* __restrict__ err)
+                         uint32_t* __restrict__ pool_ctr, uint32_t* __restrict__ band_count,
+                         uint32_t* __restrict__ band_cost, unsigned* __restrict__ err)
 {
     const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
     if (u >= ev.total_units) return;
@@ -164,7 +167,11 @@ __global__ void k_sample(const EventDesc ev, UnitRec* __restrict__ recs, uint32_
     }
     const int h = P.h;
     const int n_eff = P.ww_is_one ? 0 : f.n_w + 2 * h;
-    const uint32_t need = ev.fluctuate ? (uint32_t)(2 * (f.n_w + f.n_t) + 1) : (uint32_t)(f.n_w + n_eff + f.n_t);
+    // fluctuation off on a direct-path plane: room for g = tv (*) kernel and max|g| (k_fill_bands)
+    const bool with_g = !ev.fluctuate && ev.mode == 0 && P.direct_ok;
+    const uint32_t L = (uint32_t)(f.n_t + P.n_lags - 1);
+    const uint32_t need = ev.fluctuate ? (uint32_t)(2 * (f.n_w + f.n_t) + 1)
+                                       : (uint32_t)(f.n_w + n_eff + f.n_t) + (with_g ? L + 4 : 0u);
     uint32_t off = atomicAdd(pool_ctr, need);
     if ((uint64_t)off + need > pool_cap) {
         atomicOr(err, kErrPool);
@@ -219,49 +226,74 @@ __global__ void k_sample(const EventDesc ev, UnitRec* __restrict__ recs, uint32_
     rec.pool = off;
     recs[u] = rec;
     if (!ev.fluctuate && ev.mode == 0)
-        for_each_band(P, f.w0, f.n_w, [&](int c) { atomicAdd(&band_count[P.band_base + c], 1u); });
+        for_each_band(P, f.w0, f.n_w, [&](int c) {
+            atomicAdd(&band_count[P.band_base + c], 1u);
+            if (with_g) atomicAdd(&band_cost[P.band_base + c], L);  // direct-path work estimate
+        });
 }
 
 // Exclusive scan of band counts (single block); resets the fill cursors.
-__global__ void k_scan_bands(const uint32_t* __restrict__ count, uint32_t* __restrict__ off, uint32_t* __restrict__ fill,
-                             uint32_t n)
+// Also partitions the bands between the two convolution kernels: a band goes
+// to k_direct when its time-domain work (sum of profile lengths, k_sample)
+// is at most the plane's threshold, else to the row-FFT k_conv. maps[0, n) lists direct bands, maps[n, 2n) FFT
+// bands, each in ascending band order (neighbouring bands share depos, so
+// co-resident CTAs reuse their profiles in L2); map_count = {#direct, #fft}.
+// Counts and direct flags are scanned together, packed in 64 bits.
+__global__ void k_scan_bands(const EventDesc ev, const uint32_t* __restrict__ count, const uint32_t* __restrict__ cost,
+                             uint32_t* __restrict__ off, uint32_t* __restrict__ fill, uint32_t n,
+                             uint32_t* __restrict__ maps, uint32_t* __restrict__ map_count)
 {
-    __shared__ uint32_t warp_sums[32];
-    __shared__ uint32_t carry;
-    if (threadIdx.x == 0) carry = 0;
+    constexpr int kFlagShift = 40;
+    __shared__ unsigned long long warp_sums[32];
+    __shared__ unsigned long long carry;
+    if (threadIdx.x == 0) carry = 0ull;
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (uint32_t base = 0; base < n; base += blockDim.x) {
         const uint32_t i = base + threadIdx.x;
-        const uint32_t v = i < n ? count[i] : 0u;
-        uint32_t x = v;
+        unsigned long long v = 0ull;
+        bool direct = false;
+        if (i < n) {
+            const PlaneDesc& P = ev.p[band_plane(ev, i)];
+            direct = P.direct_ok && cost[i] <= P.direct_thr;
+            v = (unsigned long long)count[i] | ((unsigned long long)direct << kFlagShift);
+        }
+        unsigned long long x = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
             if (lane >= o) x += y;
         }
         if (lane == 31) warp_sums[wid] = x;
         __syncthreads();
         if (wid == 0) {
-            uint32_t s = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0u;
+            unsigned long long t = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0ull;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
-                if (lane >= o) s += y;
+                const unsigned long long y = __shfl_up_sync(0xffffffffu, t, o);
+                if (lane >= o) t += y;
             }
-            warp_sums[lane] = s;
+            warp_sums[lane] = t;
         }
         __syncthreads();
-        const uint32_t excl = carry + (wid ? warp_sums[wid - 1] : 0u) + x - v;
+        const unsigned long long excl = carry + (wid ? warp_sums[wid - 1] : 0ull) + x - v;
         if (i < n) {
-            off[i] = excl;
+            off[i] = (uint32_t)(excl & ((1ull << kFlagShift) - 1));
             fill[i] = 0;
+            const uint32_t nd = (uint32_t)(excl >> kFlagShift);  // direct bands before i
+            if (direct) maps[nd] = i;
+            else maps[n + (i - nd)] = i;
         }
         __syncthreads();
         if (threadIdx.x == blockDim.x - 1) carry = excl + v;
         __syncthreads();
     }
-    if (threadIdx.x == 0) off[n] = carry;
+    if (threadIdx.x == 0) {
+        off[n] = (uint32_t)(carry & ((1ull << kFlagShift) - 1));
+        const uint32_t nd = (uint32_t)(carry >> kFlagShift);
+        map_count[0] = nd;
+        map_count[1] = n - nd;
+    }
 }
 
 __global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ recs, const uint32_t* __restrict__ off,
@@ -274,8 +306,90 @@ __global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ rec
     const PlaneDesc& P = ev.p[rec.plane];
     for_each_band(P, rec.w0, rec.n_w, [&](int c) {
         const uint32_t b = P.band_base + c;
-        list[off[b] + atomicAdd(&fill[b], 1u)] = rec;  // full record: k_conv streams the list
+        list[off[b] + atomicAdd(&fill[b], 1u)] = rec;  // full record: the conv kernels stream the list
     });
+}
+
+// Response profiles of the units on direct-path planes: for each unit
+// g[j] = sum_k tv[k] kernel[j - k], j < L = n_t + n_lags - 1 (the tick profile
+// convolved with the combined time kernel, shared by all wire rows of the
+// depo), and max|g| after it. Grid (unit groups, plane): the block stages
+// its plane's kernel, zero-padded by kKernPad taps on both sides, in shared
+// memory; one warp per unit, lane l computes 4 consecutive taps per 128-tap
+// chunk with a sliding register window over the kernel, the tick profile in
+// lane registers broadcast by shuffles, one 16-byte store per lane.
+constexpr int kGprofWarps = 8;
+
+__global__ void __launch_bounds__(32 * kGprofWarps)
+k_gprof(const EventDesc ev, const UnitRec* __restrict__ recs, uint32_t* __restrict__ pool)
+{
+    extern __shared__ float s_h[];
+    const PlaneDesc& P = ev.p[blockIdx.y];
+    if (!P.direct_ok) return;
+    const uint32_t u0 = blockIdx.x * kGprofWarps;
+    if (u0 >= P.n_units) return;
+    const int nl = P.n_lags;
+    // kernel tap i (i >= -kKernPad) lives at s_h[(x & 3) * q4 + (x >> 2)], x = i + kKernPad:
+    // the 4-tap lane stride of the window reads then hits 32 distinct banks
+    const int nh = nl + 2 * kKernPad;
+    const int q4 = (nh + 3) >> 2;
+    for (int x = threadIdx.x; x < nh; x += blockDim.x) s_h[(x & 3) * q4 + (x >> 2)] = __ldg(&P.kern[x - kKernPad]);
+    __syncthreads();
+    auto h = [&](int i) {
+        const int x = i + kKernPad;
+        return s_h[(x & 3) * q4 + (x >> 2)];
+    };
+    const int lane = threadIdx.x & 31;
+    const uint32_t ul = u0 + (threadIdx.x >> 5);
+    if (ul >= P.n_units) return;
+    const UnitRec rec = recs[P.unit_base + ul];
+    if (rec.w0 < 0) return;
+    const float* tv = reinterpret_cast<const float*>(pool + unit_tv_off(P, rec));
+    float* g = reinterpret_cast<float*>(pool + unit_g_off(P, rec));
+    const int nt = rec.n_t, L = nt + nl - 1;
+    float gm = 0.0f;
+    if (nt <= 32) {
+        const float tvl = lane < nt ? tv[lane] : 0.0f;
+        for (int base = 0; base < L; base += 128) {
+            const int j0 = base + 4 * lane;
+            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+            // window w_m = h[j0 + m - k]; j0 + 3 < L + 128 <= nl + kKernPad and j0 - nt >= -kKernPad
+            float w0 = h(j0), w1 = h(j0 + 1), w2 = h(j0 + 2), w3 = h(j0 + 3);
+#pragma unroll 4
+            for (int k = 0; k < nt; ++k) {
+                const float t = __shfl_sync(0xffffffffu, tvl, k);
+                const float wn = h(j0 - k - 1);
+                s0 = __fmaf_rn(t, w0, s0);
+                s1 = __fmaf_rn(t, w1, s1);
+                s2 = __fmaf_rn(t, w2, s2);
+                s3 = __fmaf_rn(t, w3, s3);
+                w3 = w2;
+                w2 = w1;
+                w1 = w0;
+                w0 = wn;
+            }
+            if (j0 + 3 < L) {
+                *reinterpret_cast<float4*>(g + j0) = make_float4(s0, s1, s2, s3);
+            } else {
+                if (j0 < L) g[j0] = s0;
+                if (j0 + 1 < L) g[j0 + 1] = s1;
+                if (j0 + 2 < L) g[j0 + 2] = s2;
+            }
+            gm = fmaxf(gm, fmaxf(fmaxf(fabsf(s0), fabsf(s1)), fmaxf(fabsf(s2), fabsf(s3))));
+        }
+    } else {
+        // wide tick profiles (sigma_t > ~2.5 ticks): plain per-tap sums
+        for (int j = lane; j < L; j += 32) {
+            const int k0 = j - nl + 1 > 0 ? j - nl + 1 : 0, k1 = j < nt - 1 ? j : nt - 1;
+            float sum = 0.0f;
+            for (int k = k0; k <= k1; ++k) sum = __fmaf_rn(tv[k], h(j - k), sum);
+            g[j] = sum;
+            gm = fmaxf(gm, fabsf(sum));
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, o));
+    if (lane == 0) g[L] = gm;
 }
 
 // Fluctuation walk, one thread per unit: sample_patch's exact probabilities
@@ -330,18 +444,21 @@ __global__ void k_fluctuate(const EventDesc ev, const UnitRec* __restrict__ recs
 }  // namespace wsb
 
 extern "C" cudaError_t wsb_launch_sample(const wsb::EventDesc& ev, wsb::UnitRec* recs, uint32_t* pool, uint32_t pool_cap,
-                                         uint32_t* pool_ctr, uint32_t* band_count, unsigned* err, cudaStream_t s)
+                                         uint32_t* pool_ctr, uint32_t* band_count, uint32_t* band_cost, unsigned* err,
+                                         cudaStream_t s)
 {
     if (ev.total_units == 0) return cudaSuccess;
     const uint32_t threads = 128;
     const uint32_t blocks = (ev.total_units + threads - 1) / threads;
-    wsb::k_sample<<<blocks, threads, 0, s>>>(ev, recs, pool, pool_cap, pool_ctr, band_count, err);
+    wsb::k_sample<<<blocks, threads, 0, s>>>(ev, recs, pool, pool_cap, pool_ctr, band_count, band_cost, err);
     return cudaGetLastError();
 }
 
-extern "C" cudaError_t wsb_launch_scan(const uint32_t* count, uint32_t* off, uint32_t* fill, uint32_t n, cudaStream_t s)
+extern "C" cudaError_t wsb_launch_scan(const wsb::EventDesc& ev, const uint32_t* count, const uint32_t* cost,
+                                       uint32_t* off, uint32_t* fill, uint32_t n, uint32_t* maps, uint32_t* map_count,
+                                       cudaStream_t s)
 {
-    wsb::k_scan_bands<<<1, 1024, 0, s>>>(count, off, fill, n);
+    wsb::k_scan_bands<<<1, 1024, 0, s>>>(ev, count, cost, off, fill, n, maps, map_count);
     return cudaGetLastError();
 }
 
@@ -350,6 +467,32 @@ extern "C" cudaError_t wsb_launch_fill(const wsb::EventDesc& ev, const wsb::Unit
 {
     if (ev.total_units == 0) return cudaSuccess;
     wsb::k_fill_bands<<<(ev.total_units + 255) / 256, 256, 0, s>>>(ev, recs, off, fill, list);
+    return cudaGetLastError();
+}
+
+extern "C" cudaError_t wsb_launch_gprof(const wsb::EventDesc& ev, const wsb::UnitRec* recs, uint32_t* pool,
+                                        cudaStream_t s)
+{
+    uint32_t max_units = 0;
+    int max_lags = 0;
+    for (int i = 0; i < ev.n_planes; ++i)
+        if (ev.p[i].direct_ok) {
+            max_units = max_units > ev.p[i].n_units ? max_units : ev.p[i].n_units;
+            max_lags = max_lags > ev.p[i].n_lags ? max_lags : ev.p[i].n_lags;
+        }
+    if (max_units == 0) return cudaSuccess;
+    const size_t smem = sizeof(float) * (size_t)(max_lags + 2 * wsb::kKernPad + 4);
+    static unsigned long long ready = 0;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (!(ready & (1ull << dev))) {
+        e = cudaFuncSetAttribute(wsb::k_gprof, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        if (e != cudaSuccess) return e;
+        ready |= 1ull << dev;
+    }
+    const dim3 grid((max_units + wsb::kGprofWarps - 1) / wsb::kGprofWarps, (unsigned)ev.n_planes);
+    wsb::k_gprof<<<grid, 32 * wsb::kGprofWarps, smem, s>>>(ev, recs, pool);
     return cudaGetLastError();
 }
 

@@ -1,0 +1,141 @@
+"""GPU parity of the two convolution kernels (time-domain k_direct and row-FFT
+k_conv) and of the per-band routing between them, against the CPU oracle
+(wsoracle.c's direct circular convolution, pinned to the reference in
+test_oracle.py) and against each other.
+
+Tolerances as in test_gpu_parity.py (BASELINE.json north_star): per-channel
+relative L2 <= 1e-5 on the frame."""
+import numpy as np
+import pytest
+
+from paper_2104_08265_b200 import Context, GridSpec, Plane, ResponseParams, SimConfig, simulate_event
+from paper_2104_08265_b200.workloads import line_tracks, microboone_event, microboone_grids
+
+from .helpers import oracle_grid, oracle_response, relL2_per_channel
+
+pytestmark = pytest.mark.gpu
+
+TOL_FRAME = 1e-5
+SMALL = GridSpec(n_wires=96, n_ticks=900, pad_wires=20, pad_ticks=100, pitch=5.0, tick=0.5)
+
+
+@pytest.fixture(scope="module")
+def pctx():
+    c = Context(0)
+    yield c
+    c.close()
+
+
+def _frame(ctx, path, grid, resp, depos, kappa=None):
+    ctx.set_conv_path(path)
+    if kappa is not None:
+        ctx.set_direct_kappa(kappa)
+    try:
+        return Plane(ctx, grid, resp).simulate(depos, SimConfig(grid=grid, response=resp, fluctuate=False)).frame
+    finally:
+        ctx.set_conv_path("auto")
+        ctx.set_direct_kappa(48.0)
+
+
+@pytest.mark.parametrize("path", ["direct", "fft", "auto"])
+@pytest.mark.parametrize("kind", ["collection", "induction"])
+@pytest.mark.parametrize("ww", [(1.0,), (0.1, 1.0, 0.1), (-0.05, 0.2, 1.0, 0.2, -0.05)])
+def test_paths_vs_oracle_small(pctx, oracle, path, kind, ww):
+    resp = ResponseParams(plane_kind=kind, wire_weights=ww)
+    depos = line_tracks(600, SMALL, seed=3)
+    m = _frame(pctx, path, SMALL, resp, depos)
+    s_ref, _ = oracle.charge_fluct_off(oracle_grid(SMALL), depos)
+    m_ref = oracle.convolve(oracle_grid(SMALL), oracle_response(resp), s_ref)
+    assert relL2_per_channel(m, m_ref) < TOL_FRAME
+
+
+@pytest.mark.parametrize("shaper", [0.0, 1.0, 2.0])
+def test_direct_c1_folded_and_long_kernels(pctx, oracle, shaper):
+    """configs[0] geometry (padded ticks 6200, not 7-smooth: the FFT path folds
+    a longer transform; the direct path is circular by construction), with
+    kernels from 114 to >300 taps (several 128-tap chunks per profile)."""
+    grid = GridSpec(n_wires=480, n_ticks=6000, pad_wires=100, pad_ticks=400)
+    resp = ResponseParams(plane_kind="collection", shaper_peaking=shaper)
+    depos = line_tracks(10_000, grid, seed=1)
+    m = _frame(pctx, "direct", grid, resp, depos)
+    s_ref, _ = oracle.charge_fluct_off(oracle_grid(grid), depos)
+    m_ref = oracle.convolve(oracle_grid(grid), oracle_response(resp), s_ref)
+    assert relL2_per_channel(m, m_ref) < TOL_FRAME
+
+
+def test_direct_wrap_both_edges(pctx, oracle):
+    """Depos hugging tick 0 and the last tick: the response wraps circularly
+    (the reference's convolve is circular, spectral.cpp:141-175)."""
+    grid = GridSpec(n_wires=30, n_ticks=200, pad_wires=5, pad_ticks=100)
+    resp = ResponseParams(plane_kind="induction", wire_weights=(0.2, 1.0, 0.2))
+    d = line_tracks(40, grid, seed=2)
+    d["t"][:20] = -49.5   # tick ~1 of the padded grid
+    d["t"][20:] = 149.6   # last padded ticks
+    d["x"][:5] = -20.0    # wire wrap across the padded edge
+    m = _frame(pctx, "direct", grid, resp, d)
+    s_ref, _ = oracle.charge_fluct_off(oracle_grid(grid), d)
+    m_ref = oracle.convolve(oracle_grid(grid), oracle_response(resp), s_ref)
+    assert relL2_per_channel(m, m_ref) < TOL_FRAME
+
+
+def test_auto_mixed_routing_bitwise(pctx):
+    """A threshold that splits the bands between both kernels: each band's
+    rows are bitwise those of the kernel it was routed to."""
+    grid = GridSpec(n_wires=400, n_ticks=2000, pad_wires=20, pad_ticks=100)
+    resp = ResponseParams(plane_kind="induction", wire_weights=(0.1, 1.0, 0.1))
+    rng = np.random.default_rng(4)
+    d = line_tracks(20_000, grid, seed=4)
+    d["x"][:15_000] = rng.uniform(0, 300.0, 15_000)  # dense wires 0..60, sparse elsewhere
+    m_fft = _frame(pctx, "fft", grid, resp, d)
+    m_dir = _frame(pctx, "direct", grid, resp, d)
+    m_mix = _frame(pctx, "auto", grid, resp, d, kappa=40.0)
+    from_fft = np.all(m_mix == m_fft, axis=1)
+    from_dir = np.all(m_mix == m_dir, axis=1)
+    assert np.all(from_fft | from_dir)
+    assert from_fft.sum() > 8 and (from_dir & ~from_fft).sum() > 8  # both kernels really ran
+    assert relL2_per_channel(m_dir, m_fft) < TOL_FRAME
+
+
+def test_direct_deterministic(pctx):
+    grid = SMALL
+    resp = ResponseParams(plane_kind="induction", wire_weights=(0.1, 1.0, 0.1))
+    d = line_tracks(3000, grid, seed=8)
+    a = _frame(pctx, "direct", grid, resp, d)
+    b = _frame(pctx, "direct", grid, resp, d)
+    np.testing.assert_array_equal(a, b)
+
+
+def test_microboone_u_plane_full_size(pctx, oracle):
+    """configs[1] at full size (the bench workload): the U plane of a 100k-depo
+    event (2600 x 9800 padded) against the oracle, both kernels; and the whole
+    event through the batched API equals the single planes."""
+    grids, resps = microboone_grids()
+    ev = microboone_event(100_000, seed=1)
+    s_ref, _ = oracle.charge_fluct_off(oracle_grid(grids[0]), ev[0])
+    m_ref = oracle.convolve(oracle_grid(grids[0]), oracle_response(resps[0]), s_ref)
+    for path in ("direct", "fft"):
+        m = _frame(pctx, path, grids[0], resps[0], ev[0])
+        assert relL2_per_channel(m, m_ref) < TOL_FRAME, path
+    planes = [Plane(pctx, g, r) for g, r in zip(grids, resps)]
+    frames, _ = simulate_event(pctx, planes, ev, SimConfig(fluctuate=False))
+    for p, d, f in zip(planes, ev, frames):
+        np.testing.assert_array_equal(p.simulate(d, SimConfig(fluctuate=False)).frame, f)
+
+
+def test_direct_band_beyond_staging(pctx, oracle):
+    """A band with more depos than k_direct stages at once (chunked
+    accumulation) still matches the oracle."""
+    grid = GridSpec(n_wires=16, n_ticks=900, pad_wires=10, pad_ticks=100, pitch=5.0, tick=0.5)
+    # unipolar response: 12k stacked bipolar responses cancel to ~1e-3 of
+    # their absolute sum, which any fp32 method resolves only to ~1e-6
+    resp = ResponseParams(plane_kind="collection", wire_weights=(0.1, 1.0, 0.1))
+    d = line_tracks(12_000, grid, seed=12)
+    # every depo centred on wire 18 of the padded grid; sigma_x keeps the
+    # footprint's edge wires well-conditioned (a 10-sigma tail bin is fp64
+    # erf rounding noise, where CUDA's and glibc's erf legitimately differ)
+    d["x"] = 40.0 + (d["x"] % 3.0)
+    d["sigma_x"] = 2.5
+    m = _frame(pctx, "direct", grid, resp, d)
+    s_ref, _ = oracle.charge_fluct_off(oracle_grid(grid), d)
+    m_ref = oracle.convolve(oracle_grid(grid), oracle_response(resp), s_ref)
+    assert relL2_per_channel(m, m_ref) < TOL_FRAME
