@@ -22,24 +22,22 @@ using wsb::PlaneDesc;
 using wsb::UnitRec;
 
 extern "C" cudaError_t wsb_launch_sample(const EventDesc& ev, UnitRec* recs, uint32_t* pool, uint32_t pool_cap,
-                                         uint32_t* pool_ctr, uint32_t* band_count, uint32_t* band_cost, unsigned* err,
-                                         cudaStream_t s);
-extern "C" cudaError_t wsb_launch_scan(const EventDesc& ev, const uint32_t* count, const uint32_t* cost, uint32_t* off,
-                                       uint32_t* fill, uint32_t n, uint32_t* maps, uint32_t* map_count, cudaStream_t s);
+                                         uint32_t* pool_ctr, uint32_t* band_count, unsigned* err, cudaStream_t s);
+extern "C" cudaError_t wsb_launch_scan(const uint32_t* count, uint32_t* off, uint32_t* fill, uint32_t n, cudaStream_t s);
 extern "C" cudaError_t wsb_launch_fill(const EventDesc& ev, const UnitRec* recs, const uint32_t* off, uint32_t* fill,
-                                       UnitRec* list, cudaStream_t s);
+                                       UnitRec* list, wsb::TEnt* tlist, const uint32_t* pool, unsigned* err,
+                                       cudaStream_t s);
 extern "C" cudaError_t wsb_launch_gprof(const EventDesc& ev, const UnitRec* recs, uint32_t* pool, cudaStream_t s);
-extern "C" size_t wsb_direct_smem(int N, int cap);
-extern "C" int wsb_direct_cap(int N);
+extern "C" size_t wsb_direct_smem(int cap);
+extern "C" int wsb_direct_cap();
 extern "C" cudaError_t wsb_launch_direct(const EventDesc& ev, const uint32_t* pool, const uint32_t* band_off,
-                                         const UnitRec* band_list, const uint32_t* map, const uint32_t* map_count,
-                                         size_t smem_bytes, cudaStream_t stream);
+                                         const wsb::TEnt* tlist, size_t smem_bytes, cudaStream_t stream);
 extern "C" cudaError_t wsb_launch_fluctuate(const EventDesc& ev, const UnitRec* recs, const uint32_t* pool,
                                             const uint32_t* order, cudaStream_t s);
 extern "C" size_t wsb_conv_smem(int N, int Np, int M);
 extern "C" cudaError_t wsb_launch_conv(const EventDesc& ev, const uint32_t* pool, const uint32_t* band_off,
-                                       const UnitRec* band_list, const uint32_t* map, const uint32_t* map_count,
-                                       int flags, size_t smem_bytes, int variant, cudaStream_t stream);
+                                       const UnitRec* band_list, int flags, size_t smem_bytes, int variant,
+                                       cudaStream_t stream);
 
 namespace {
 
@@ -116,9 +114,11 @@ struct ws_ctx {
     uint64_t launches = 0;
     DevBuf<UnitRec> recs;
     DevBuf<uint32_t> pool;
-    DevBuf<uint32_t> band_count, band_off, band_fill, band_cost;
-    DevBuf<uint32_t> band_maps;  // [direct bands | fft bands | counts(2)] from k_scan_bands
-    DevBuf<UnitRec> band_list;  // CSR lists of full unit records (copied by k_fill_bands)
+    DevBuf<uint32_t> band_count, band_off, band_fill;  // per bin (FFT bands / direct tiles)
+    DevBuf<UnitRec> band_list;  // CSR lists of full unit records per FFT band (k_fill_bands)
+    DevBuf<wsb::TEnt> tile_list;  // CSR lists of direct-path tile entries (k_fill_bands)
+    size_t list_hint = 0;       // grown after a kErrRange
+    uint32_t last_list_cap = 0;
     DevBuf<ScratchHeader> header;
     DevBuf<ws_depo> depos;
     DevBuf<float> frames, charges;
@@ -130,7 +130,7 @@ struct ws_ctx {
     int sm_count = 0;
     int conv_variant = 25;                       // k_conv: 25 (3 CTAs/SM, radix <= 25) or 8 (4 CTAs/SM, radix <= 8)
     int conv_path = WS_CONV_AUTO;                // ws_ctx_set_conv_path
-    double direct_kappa = 48.0;                  // AUTO: direct if sum of profile lengths <= kappa x Np per band
+    double direct_kappa = 16.0;                  // AUTO: direct if est. depo-row-taps <= kappa x cells (per plane)
     cudaStream_t copy_stream = nullptr;          // D2H of the pipelined batch path
     cudaEvent_t slot_computed[2] = {nullptr, nullptr};
     cudaEvent_t slot_copied[2] = {nullptr, nullptr};
@@ -148,9 +148,8 @@ struct ws_plane {
     double* d_ww = nullptr;
     float2* d_H = nullptr;
     float* d_kern = nullptr;  // combined kernel taps (fp32) for the direct path
-    int direct_ok = 0;
-    int direct_cap = 0;  // staged entries per band in k_direct
-    size_t direct_smem = 0;
+    int direct_ok = 0;   // eligible for the time-domain path
+    int n_windows = 0;   // direct: tick windows per 16-row band
     float2* d_tw = nullptr;
     uint16_t* d_rev = nullptr;
     int ww_is_one = 0;
@@ -347,9 +346,9 @@ PlaneDesc plane_desc(const ws_plane* p)
     d.rows_per_band = p->rows_per_band;
     d.n_lags = (int)p->n_lags;
     d.kern = p->d_kern ? p->d_kern + wsb::kKernPad : nullptr;
-    d.direct_ok = 0;  // decided per call (run_group)
-    d.direct_thr = 0;
-    d.direct_cap = (uint32_t)p->direct_cap;
+    d.direct = 0;  // decided per call (run_group)
+    d.n_windows = p->n_windows;
+    d.direct_cap = (uint32_t)wsb_direct_cap();
     d.n_bands = p->n_bands;
     return d;
 }
@@ -387,8 +386,8 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
     const bool from_grid = charge_in != nullptr;
     ev.mode = (from_grid || ev.fluctuate) ? 1 : 0;
     uint32_t units = 0, bands = 0;
-    size_t smem = 0, smem_direct = 0;
-    bool want_frame = false, any_direct = false;
+    size_t smem = 0;
+    bool want_frame = false, any_direct = false, any_fft = false;
     int max_lags = 0;
     for (uint32_t i = 0; i < n; ++i) {
         ws_plane* p = planes[i];
@@ -401,18 +400,23 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
         d.charge_out = charges ? charges[i] : nullptr;
         d.charge_in = from_grid ? charge_in[i] : (ev.fluctuate ? charges[i] : nullptr);
         d.stats = nullptr;
-        // time-domain path: fluctuation-off accumulation into a frame
-        if (ev.mode == 0 && d.frame && p->direct_ok && c->conv_path != WS_CONV_FFT) {
-            d.direct_ok = 1;
-            const double thr = c->conv_path == WS_CONV_DIRECT ? 4.0e9 : c->direct_kappa * (double)p->Np;
-            d.direct_thr = (uint32_t)std::min(thr, 4.0e9);
-            any_direct = true;
-            smem_direct = std::max(smem_direct, p->direct_smem);
-            max_lags = std::max(max_lags, (int)p->n_lags);
+        // time-domain path for fluctuation-off frames (not with a charge
+        // grid request: that pass bins by FFT bands). AUTO estimates the
+        // work as depos x ~12 wire rows x profile taps against the plane's
+        // cells (ws_ctx_set_direct_kappa).
+        if (ev.mode == 0 && d.frame && !d.charge_out && p->direct_ok && c->conv_path != WS_CONV_FFT) {
+            const double work = (double)d.n_units * 12.0 * (double)(p->n_lags + 16);
+            if (c->conv_path == WS_CONV_DIRECT || work <= c->direct_kappa * (double)p->W * (double)p->Np) {
+                d.direct = 1;
+                d.n_bands = ((p->W + wsb::kTileRows - 1) / wsb::kTileRows) * p->n_windows;
+                any_direct = true;
+                max_lags = std::max(max_lags, (int)p->n_lags);
+            }
         }
+        any_fft = any_fft || !d.direct;
         ev.p[i] = d;
         units += d.n_units;
-        bands += (uint32_t)p->n_bands;
+        bands += (uint32_t)d.n_bands;
         smem = std::max(smem, p->smem);
         want_frame = want_frame || d.frame != nullptr;
     }
@@ -426,11 +430,16 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
     WS_CUDA(c->band_count.reserve(bands + 1));
     WS_CUDA(c->band_off.reserve(bands + 1));
     WS_CUDA(c->band_fill.reserve(bands + 1));
-    WS_CUDA(c->band_cost.reserve(bands + 1));
-    WS_CUDA(c->band_maps.reserve(2 * (size_t)bands + 2));
     int max_h = 0;
     for (uint32_t i = 0; i < n; ++i) max_h = std::max(max_h, planes[i]->h);
-    WS_CUDA(c->band_list.reserve(c->pool.cap + (size_t)units * (2 * max_h + 2) + 16));
+    // bin lists: ~4.5 entries per unit for 4-row FFT bands, ~2 per unit for
+    // 16 x 2048 tiles at typical widths; overflow is detected on the device
+    const size_t list_cap = std::min<size_t>(std::max<size_t>(c->list_hint, (size_t)units * (8 + max_h) + 4096),
+                                             0xffffffffu);
+    ev.list_cap = (uint32_t)list_cap;
+    c->last_list_cap = (uint32_t)list_cap;
+    if (any_fft) WS_CUDA(c->band_list.reserve(list_cap));
+    if (any_direct) WS_CUDA(c->tile_list.reserve(list_cap));
     WS_CUDA(c->header.reserve(1));
     ScratchHeader* hdr = c->header.p;
     for (uint32_t i = 0; i < n; ++i) ev.p[i].stats = &hdr->stats[2 * i];
@@ -443,16 +452,14 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
 
     WS_CUDA(cudaEventRecord(pc.ev[0], s));
     WS_CUDA(cudaMemsetAsync(hdr, 0, sizeof(ScratchHeader), s));
-    if (ev.mode == 0) {
-        WS_CUDA(cudaMemsetAsync(c->band_count.p, 0, sizeof(uint32_t) * (bands + 1), s));
-        WS_CUDA(cudaMemsetAsync(c->band_cost.p, 0, sizeof(uint32_t) * (bands + 1), s));
-    }
+    if (ev.mode == 0) WS_CUDA(cudaMemsetAsync(c->band_count.p, 0, sizeof(uint32_t) * (bands + 1), s));
+
     if (ev.fluctuate && !from_grid)
         for (uint32_t i = 0; i < n; ++i)
             WS_CUDA(cudaMemsetAsync(ev.p[i].charge_out, 0, sizeof(float) * (size_t)ev.p[i].W * ev.p[i].N, s));
     if (!from_grid) {
         WS_CUDA(wsb_launch_sample(ev, c->recs.p, c->pool.p, (uint32_t)std::min<size_t>(c->pool.cap, 0xffffffffu),
-                                  &hdr->pool_ctr, c->band_count.p, c->band_cost.p, &hdr->err, s));
+                                  &hdr->pool_ctr, c->band_count.p, &hdr->err, s));
         c->launches += units ? 1 : 0;
     }
     WS_CUDA(cudaEventRecord(pc.ev[1], s));
@@ -461,37 +468,32 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
         c->launches += units ? 1 : 0;
     }
     WS_CUDA(cudaEventRecord(pc.ev[2], s));
-    uint32_t* maps = c->band_maps.p;
-    uint32_t* map_count = maps + 2 * (size_t)bands;
     if (ev.mode == 0) {
-        WS_CUDA(wsb_launch_scan(ev, c->band_count.p, c->band_cost.p, c->band_off.p, c->band_fill.p, bands, maps,
-                                map_count, s));
-        WS_CUDA(wsb_launch_fill(ev, c->recs.p, c->band_off.p, c->band_fill.p, c->band_list.p, s));
-        c->launches += 1 + (units ? 1 : 0);
-        if (any_direct) {
+        if (any_direct) {  // profiles first: the tile entries' bounds need max|g|
             WS_CUDA(wsb_launch_gprof(ev, c->recs.p, c->pool.p, s));
             c->launches += units ? 1 : 0;
         }
+        WS_CUDA(wsb_launch_scan(c->band_count.p, c->band_off.p, c->band_fill.p, bands, s));
+        WS_CUDA(wsb_launch_fill(ev, c->recs.p, c->band_off.p, c->band_fill.p, c->band_list.p, c->tile_list.p,
+                                c->pool.p, &hdr->err, s));
+        c->launches += 1 + (units ? 1 : 0);
     }
     WS_CUDA(cudaEventRecord(pc.ev[3], s));
     if (ev.mode == 0 && charges) {
         // the charge grid is the un-stencilled S: an accumulate-only pass of
         // the row kernel over every band (parity / inspection output)
-        WS_CUDA(wsb_launch_conv(ev, c->pool.p, c->band_off.p, c->band_list.p, nullptr, nullptr, 2, smem,
-                                c->conv_variant, s));
+        WS_CUDA(wsb_launch_conv(ev, c->pool.p, c->band_off.p, c->band_list.p, 2, smem, c->conv_variant, s));
         c->launches += bands ? 1 : 0;
     }
     if (want_frame) {
+        // each kernel skips the other's planes
         if (any_direct) {
-            // bands routed by k_scan_bands: sparse ones to the time-domain
-            // kernel, dense ones to the row FFT
-            WS_CUDA(wsb_launch_direct(ev, c->pool.p, c->band_off.p, c->band_list.p, maps, map_count, smem_direct, s));
-            WS_CUDA(wsb_launch_conv(ev, c->pool.p, c->band_off.p, c->band_list.p, maps + bands, map_count + 1, 1, smem,
-                                    c->conv_variant, s));
-            c->launches += bands ? 2 : 0;
-        } else {
-            WS_CUDA(wsb_launch_conv(ev, c->pool.p, c->band_off.p, c->band_list.p, nullptr, nullptr, 1, smem,
-                                    c->conv_variant, s));
+            WS_CUDA(wsb_launch_direct(ev, c->pool.p, c->band_off.p, c->tile_list.p, wsb_direct_smem(wsb_direct_cap()),
+                                      s));
+            c->launches += bands ? 1 : 0;
+        }
+        if (any_fft) {
+            WS_CUDA(wsb_launch_conv(ev, c->pool.p, c->band_off.p, c->band_list.p, 1, smem, c->conv_variant, s));
             c->launches += bands ? 1 : 0;
         }
     }
@@ -522,6 +524,10 @@ int finish_pending(ws_ctx* c)
                 c->pool_hint = std::max<size_t>(c->pool.cap * 2, (size_t)h.pool_ctr + 4096);
                 rc = set_err(WS_ERANGE, "workspace: patch pool overflow (%u doubles needed); grown, re-run the call",
                              h.pool_ctr);
+            } else if (h.err & wsb::kErrRange) {
+                c->list_hint = std::max<size_t>(c->list_hint, 2 * (size_t)c->last_list_cap);
+                rc = set_err(WS_ERANGE, "workspace: bin lists overflow (capacity %u entries); grown, re-run the call",
+                             c->last_list_cap);
             }
         }
         if (pc.timing) {
@@ -613,9 +619,9 @@ int ws_ctx_destroy(ws_ctx* c)
     c->band_count.release();
     c->band_off.release();
     c->band_fill.release();
-    c->band_cost.release();
-    c->band_maps.release();
+
     c->band_list.release();
+    c->tile_list.release();
     c->header.release();
     c->depos.release();
     c->frames.release();
@@ -807,9 +813,8 @@ int ws_plane_create(ws_ctx* ctx, const ws_grid_spec* grid, const ws_response* re
     p->smem = wsb_conv_smem(p->N, p->Np, p->M);
     // time-domain path: kernel taps on the device; eligible while a band's
     // fixed-point rows fit in shared memory and the kernel is not huge
-    p->direct_cap = wsb_direct_cap(p->N);
-    p->direct_smem = wsb_direct_smem(p->N, p->direct_cap);
-    if (p->direct_cap >= 64 && p->n_lags <= 4096) {
+    p->n_windows = (p->N + wsb::kTileTicks - 1) / wsb::kTileTicks;
+    if (p->n_windows <= 32 && p->n_lags <= 4096 && p->N < 65536) {
         std::vector<float> kf(p->kernel.size() + 2 * wsb::kKernPad, 0.0f);
         std::copy(p->kernel.begin(), p->kernel.end(), kf.begin() + wsb::kKernPad);
         e = cudaMalloc(&p->d_kern, sizeof(float) * kf.size());

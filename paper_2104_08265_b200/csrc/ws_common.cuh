@@ -21,6 +21,10 @@ constexpr int kConvThreads = 256;
 constexpr int kTwiddleTable = 512;   // [W_M^j | W_M^{64i} | W_Np^j | W_Np^{64i}], 64 + 192 + 64 + 192
 constexpr int kMaxFftHalf = 12288;   // M = N'/2 <= 12288 (N' <= 24576 ticks)
 constexpr int kKernPad = 192;        // zero taps either side of PlaneDesc::kern (k_gprof window)
+constexpr int kTileRows = 16;        // direct path tile: kTileRows wire rows x kTileTicks ticks
+constexpr int kTileTicks = 2048;
+constexpr int kSegShiftD = 6;        // direct path fixed-point bounds per 64-tick segment
+constexpr int kSegs = kTileTicks >> kSegShiftD;
 constexpr double kFixScale = 4294967296.0;          // 2^32: fixed-point electrons
 constexpr double kFixInv = 1.0 / 4294967296.0;
 
@@ -34,6 +38,15 @@ struct __align__(16) UnitRec {
     int32_t plane;
     float a;       // fluct off: q / total; fluct on: unused
     float tmax;    // fluct off: max over the tick profile (bounds a row's fixed-point scale)
+};
+
+// One entry of a direct-path tile list (k_fill_bands -> k_direct), 80 bytes.
+struct __align__(16) TEnt {
+    uint32_t tsL;   // first output tick ts (circular, < N) | profile length L << 16
+    uint32_t goff;  // pool offset of g (16-byte aligned)
+    uint32_t rows;  // covered tile rows [lo, hi): lo | hi << 8
+    float gmax;     // max |g|
+    float c[kTileRows];  // a * eff[w] per tile row (0: not covered)
 };
 
 // Device view of one plane for one launch.
@@ -55,18 +68,18 @@ struct PlaneDesc {
     const float2* tw;          // split twiddle tables (kTwiddleTable entries, see ws_api.cu)
     const uint16_t* rev;       // rev[k] = slot of spectrum bin k after the DIF transform
     // time-domain path (ws_direct.cu): per-depo response profiles g = tv (*) kernel
-    int32_t direct_ok;         // plane eligible for the direct path (pool holds g)
+    int32_t direct;            // this call: direct path (tiles, pool holds g) instead of the row FFT (bands)
     int32_t n_lags;            // combined kernel length
     const float* kern;         // n_lags combined-kernel taps (lag lo_lag first), kKernPad zeros either side
-    uint32_t direct_thr;       // band -> direct path if sum of profile lengths <= thr
-    uint32_t direct_cap;       // k_direct stages at most this many entries at a time
+    int32_t n_windows;         // direct: tick windows of kTileTicks per row band
+    uint32_t direct_cap;       // direct: k_direct stages at most this many entries at a time
     // per call
     const ws_depo* depos;
     uint32_t n_units;
     uint32_t unit_base;        // first unit index of this plane
-    uint32_t band_base;        // first band index of this plane
-    int32_t rows_per_band;
-    int32_t n_bands;
+    uint32_t band_base;        // first bin of this plane (FFT: bands of rows_per_band rows; direct: tiles)
+    int32_t rows_per_band;     // FFT bands
+    int32_t n_bands;           // bins of this plane in this call
     float* frame;              // out: M (nullable when only the charge grid is wanted)
     float* charge_out;         // out: S (nullable)
     const float* charge_in;    // in: S (mode "grid")
@@ -84,6 +97,7 @@ struct EventDesc {
     double drift_plane_x, drift_speed, drift_dl, drift_dt;
     uint32_t total_units;
     uint32_t total_bands;
+    uint32_t list_cap;         // capacity (entries) of the bin lists; more -> kErrRange, convolution skipped
     PlaneDesc p[kMaxPlanes];
 };
 
@@ -101,7 +115,7 @@ __device__ __forceinline__ int band_plane(const EventDesc& ev, uint32_t gb)
 
 // Pool layout of a fluctuation-off unit (32-bit words, see k_sample):
 //   [raw f32 x n_w][eff f32 x n_eff][tv f32 x n_t][pad to 16 B][g f32 x L][gmax f32]
-// the last two only when the plane is direct_ok; L = n_t + n_lags - 1.
+// the last two only on direct-path planes; L = n_t + n_lags - 1.
 __device__ __forceinline__ int unit_n_eff(const PlaneDesc& P, int n_w) { return P.ww_is_one ? 0 : n_w + 2 * P.h; }
 __device__ __forceinline__ uint32_t unit_tv_off(const PlaneDesc& P, const UnitRec& r)
 {
@@ -134,6 +148,79 @@ __device__ __forceinline__ bool row_coef(const PlaneDesc& P, int w, bool raw, co
     for (; j < n_rows; j += P.W) s += __ldg(&prof[j]);
     c = s * r.a;
     return true;
+}
+
+// Effective rows [w0 - h, w0 + n_w - 1 + h] of a unit modulo W as up to two ranges.
+__device__ __forceinline__ void row_ranges(const PlaneDesc& P, int w0, int n_w, int& a0, int& b0, int& a1, int& b1)
+{
+    const int W = P.W;
+    const int lo = w0 - P.h, hi = w0 + n_w - 1 + P.h;
+    a1 = 1;
+    b1 = 0;  // empty second range
+    if (hi - lo + 1 >= W) {
+        a0 = 0;
+        b0 = W - 1;
+    } else if (lo < 0) {
+        a0 = lo + W;
+        b0 = W - 1;
+        a1 = 0;
+        b1 = hi;
+    } else if (hi >= W) {
+        a0 = lo;
+        b0 = W - 1;
+        a1 = 0;
+        b1 = hi - W;
+    } else {
+        a0 = lo;
+        b0 = hi;
+    }
+}
+
+// Visit each group of B rows the unit's effective rows touch, exactly once.
+template <typename F>
+__device__ __forceinline__ void for_each_row_group(const PlaneDesc& P, int w0, int n_w, int B, F&& f)
+{
+    int a0, b0, a1, b1;
+    row_ranges(P, w0, n_w, a0, b0, a1, b1);
+    const int c0 = a0 / B, c1 = b0 / B;
+    for (int c = c0; c <= c1; ++c) f(c);
+    if (a1 <= b1) {
+        const int d0 = a1 / B, d1 = b1 / B;
+        for (int c = d0; c <= d1; ++c)
+            if (c < c0 || c > c1) f(c);
+    }
+}
+
+// Tick windows (kTileTicks each) touched by the circular output span
+// [ts, ts + L) mod N, as a bit mask (N <= 32 windows on direct planes).
+__device__ __forceinline__ uint32_t span_windows(int ts, int L, int N, int n_windows)
+{
+    if (L >= N) return n_windows >= 32 ? 0xffffffffu : ((1u << n_windows) - 1u);
+    auto range = [](int a, int b) {  // windows a..b
+        const uint32_t hi = b >= 31 ? 0xffffffffu : ((2u << b) - 1u);
+        return hi & ~((1u << a) - 1u);
+    };
+    const int e = ts + L - 1;
+    if (e < N) return range(ts / kTileTicks, e / kTileTicks);
+    return range(ts / kTileTicks, (N - 1) / kTileTicks) | range(0, (e - N) / kTileTicks);
+}
+
+// Visit each bin of the unit exactly once: FFT planes bin by bands of
+// rows_per_band rows; direct planes by (16-row band, tick window) tiles,
+// tile index = band * n_windows + window.
+template <typename F>
+__device__ __forceinline__ void for_each_bin(const PlaneDesc& P, int w0, int n_w, int t0, int n_t, F&& f)
+{
+    if (!P.direct) {
+        for_each_row_group(P, w0, n_w, P.rows_per_band, f);
+        return;
+    }
+    int ts = t0 + P.lo_lag;
+    if (ts < 0) ts += P.N;
+    const uint32_t wm = span_windows(ts, n_t + P.n_lags - 1, P.N, P.n_windows);
+    for_each_row_group(P, w0, n_w, kTileRows, [&](int rb) {
+        for (uint32_t m = wm; m; m &= m - 1) f(rb * P.n_windows + (__ffs(m) - 1));
+    });
 }
 
 __device__ __forceinline__ int plane_of_unit(const EventDesc& ev, uint32_t u)

@@ -142,17 +142,16 @@ __device__ __forceinline__ void scatter_row(const PlaneDesc& P, int w, bool raw,
 template <int NT, int MAXR, int MINB>
 __global__ void __launch_bounds__(NT, MINB)
 k_conv(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* __restrict__ band_off,
-       const UnitRec* __restrict__ band_list, const uint32_t* __restrict__ map, const uint32_t* __restrict__ map_count,
-       int flags)
+       const UnitRec* __restrict__ band_list, int flags)
 {
     // flags bit 0: produce the frame; bit 1: raw-charge pass (no wire stencil)
     extern __shared__ __align__(16) unsigned char smem[];
     const bool want_frame = flags & 1;
     const bool raw = flags & 2;
-    // map (nullable): the bands k_scan_bands routed to this kernel
-    if (map && blockIdx.x >= __ldg(map_count)) return;
-    const uint32_t gb = map ? __ldg(&map[blockIdx.x]) : blockIdx.x;
+    const uint32_t gb = blockIdx.x;
     const PlaneDesc& P = ev.p[band_plane(ev, gb)];
+    if (P.direct) return;  // tiles of a time-domain plane (k_direct)
+    if (ev.mode == 0 && __ldg(&band_off[ev.total_bands]) > ev.list_cap) return;  // lists overflowed (kErrRange)
     const int band = (int)(gb - P.band_base);
     const int W = P.W, N = P.N, Np = P.Np, M = P.M;
     const int r0 = band * P.rows_per_band;
@@ -290,8 +289,8 @@ extern "C" size_t wsb_conv_smem(int N, int Np, int M)
 // Variants: 256 threads x 3 CTAs/SM (85 registers, radices up to 25) or
 // 256 threads x 4 CTAs/SM (64 registers, radices up to 8).
 extern "C" cudaError_t wsb_launch_conv(const wsb::EventDesc& ev, const uint32_t* pool, const uint32_t* band_off,
-                                       const wsb::UnitRec* band_list, const uint32_t* map, const uint32_t* map_count,
-                                       int flags, size_t smem_bytes, int variant, cudaStream_t stream)
+                                       const wsb::UnitRec* band_list, int flags, size_t smem_bytes, int variant,
+                                       cudaStream_t stream)
 {
     // once per device: shared-memory opt-in and the composite-radix twiddles
     static unsigned long long ready = 0;
@@ -317,8 +316,8 @@ extern "C" cudaError_t wsb_launch_conv(const wsb::EventDesc& ev, const uint32_t*
     }
     if (ev.total_bands == 0) return cudaSuccess;
     if (variant == 8)
-        wsb::k_conv<256, 8, 4><<<ev.total_bands, 256, smem_bytes, stream>>>(ev, pool, band_off, band_list, map, map_count, flags);
+        wsb::k_conv<256, 8, 4><<<ev.total_bands, 256, smem_bytes, stream>>>(ev, pool, band_off, band_list, flags);
     else
-        wsb::k_conv<256, 25, 3><<<ev.total_bands, 256, smem_bytes, stream>>>(ev, pool, band_off, band_list, map, map_count, flags);
+        wsb::k_conv<256, 25, 3><<<ev.total_bands, 256, smem_bytes, stream>>>(ev, pool, band_off, band_list, flags);
     return cudaGetLastError();
 }

@@ -79,48 +79,6 @@ __device__ __forceinline__ void bin_integrals(double center, double sigma, doubl
     }
 }
 
-__device__ __forceinline__ void band_ranges(const PlaneDesc& P, int w0, int n_w, int& a0, int& b0, int& a1, int& b1)
-{
-    // effective rows [w0 - h, w0 + n_w - 1 + h] modulo W as up to two ranges
-    const int W = P.W;
-    const int lo = w0 - P.h, hi = w0 + n_w - 1 + P.h;
-    a1 = 1;
-    b1 = 0;  // empty second range
-    if (hi - lo + 1 >= W) {
-        a0 = 0;
-        b0 = W - 1;
-    } else if (lo < 0) {
-        a0 = lo + W;
-        b0 = W - 1;
-        a1 = 0;
-        b1 = hi;
-    } else if (hi >= W) {
-        a0 = lo;
-        b0 = W - 1;
-        a1 = 0;
-        b1 = hi - W;
-    } else {
-        a0 = lo;
-        b0 = hi;
-    }
-}
-
-// Visit each band the unit's effective rows touch, exactly once.
-template <typename F>
-__device__ __forceinline__ void for_each_band(const PlaneDesc& P, int w0, int n_w, F&& f)
-{
-    int a0, b0, a1, b1;
-    band_ranges(P, w0, n_w, a0, b0, a1, b1);
-    const int B = P.rows_per_band;
-    const int c0 = a0 / B, c1 = b0 / B;
-    for (int c = c0; c <= c1; ++c) f(c);
-    if (a1 <= b1) {
-        const int d0 = a1 / B, d1 = b1 / B;
-        for (int c = d0; c <= d1; ++c)
-            if (c < c0 || c > c1) f(c);
-    }
-}
-
 // One thread per unit: footprint (map_depo_to_grid + clip), bin integrals
 // into the pool, emptiness (sample_patch's total <= 0 test), clipped-charge
 // bookkeeping and, with fluctuation off, the normalised separable profiles
@@ -136,7 +94,7 @@ __device__ __forceinline__ void for_each_band(const PlaneDesc& P, int w0, int n_
 // total = sum_w wv * sum_t tv.
 __global__ void k_sample(const EventDesc ev, UnitRec* __restrict__ recs, uint32_t* __restrict__ pool, uint32_t pool_cap,
                          uint32_t* __restrict__ pool_ctr, uint32_t* __restrict__ band_count,
-                         uint32_t* __restrict__ band_cost, unsigned* __restrict__ err)
+                         unsigned* __restrict__ err)
 {
     const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
     if (u >= ev.total_units) return;
@@ -168,7 +126,7 @@ __global__ void k_sample(const EventDesc ev, UnitRec* __restrict__ recs, uint32_
     const int h = P.h;
     const int n_eff = P.ww_is_one ? 0 : f.n_w + 2 * h;
     // fluctuation off on a direct-path plane: room for g = tv (*) kernel and max|g| (k_fill_bands)
-    const bool with_g = !ev.fluctuate && ev.mode == 0 && P.direct_ok;
+    const bool with_g = !ev.fluctuate && ev.mode == 0 && P.direct;
     const uint32_t L = (uint32_t)(f.n_t + P.n_lags - 1);
     const uint32_t need = ev.fluctuate ? (uint32_t)(2 * (f.n_w + f.n_t) + 1)
                                        : (uint32_t)(f.n_w + n_eff + f.n_t) + (with_g ? L + 4 : 0u);
@@ -226,87 +184,100 @@ __global__ void k_sample(const EventDesc ev, UnitRec* __restrict__ recs, uint32_
     rec.pool = off;
     recs[u] = rec;
     if (!ev.fluctuate && ev.mode == 0)
-        for_each_band(P, f.w0, f.n_w, [&](int c) {
-            atomicAdd(&band_count[P.band_base + c], 1u);
-            if (with_g) atomicAdd(&band_cost[P.band_base + c], L);  // direct-path work estimate
-        });
+        for_each_bin(P, f.w0, f.n_w, f.t0, f.n_t, [&](int c) { atomicAdd(&band_count[P.band_base + c], 1u); });
 }
 
-// Exclusive scan of band counts (single block); resets the fill cursors.
-// Also partitions the bands between the two convolution kernels: a band goes
-// to k_direct when its time-domain work (sum of profile lengths, k_sample)
-// is at most the plane's threshold, else to the row-FFT k_conv. maps[0, n) lists direct bands, maps[n, 2n) FFT
-// bands, each in ascending band order (neighbouring bands share depos, so
-// co-resident CTAs reuse their profiles in L2); map_count = {#direct, #fft}.
-// Counts and direct flags are scanned together, packed in 64 bits.
-__global__ void k_scan_bands(const EventDesc ev, const uint32_t* __restrict__ count, const uint32_t* __restrict__ cost,
-                             uint32_t* __restrict__ off, uint32_t* __restrict__ fill, uint32_t n,
-                             uint32_t* __restrict__ maps, uint32_t* __restrict__ map_count)
+// Exclusive scan of bin counts (single block); resets the fill cursors.
+__global__ void k_scan_bands(const uint32_t* __restrict__ count, uint32_t* __restrict__ off, uint32_t* __restrict__ fill,
+                             uint32_t n)
 {
-    constexpr int kFlagShift = 40;
-    __shared__ unsigned long long warp_sums[32];
-    __shared__ unsigned long long carry;
-    if (threadIdx.x == 0) carry = 0ull;
+    __shared__ uint32_t warp_sums[32];
+    __shared__ uint32_t carry;
+    if (threadIdx.x == 0) carry = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (uint32_t base = 0; base < n; base += blockDim.x) {
         const uint32_t i = base + threadIdx.x;
-        unsigned long long v = 0ull;
-        bool direct = false;
-        if (i < n) {
-            const PlaneDesc& P = ev.p[band_plane(ev, i)];
-            direct = P.direct_ok && cost[i] <= P.direct_thr;
-            v = (unsigned long long)count[i] | ((unsigned long long)direct << kFlagShift);
-        }
-        unsigned long long x = v;
+        const uint32_t v = i < n ? count[i] : 0u;
+        uint32_t x = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
             if (lane >= o) x += y;
         }
         if (lane == 31) warp_sums[wid] = x;
         __syncthreads();
         if (wid == 0) {
-            unsigned long long t = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0ull;
+            uint32_t t = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0u;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const unsigned long long y = __shfl_up_sync(0xffffffffu, t, o);
+                const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
                 if (lane >= o) t += y;
             }
             warp_sums[lane] = t;
         }
         __syncthreads();
-        const unsigned long long excl = carry + (wid ? warp_sums[wid - 1] : 0ull) + x - v;
+        const uint32_t excl = carry + (wid ? warp_sums[wid - 1] : 0u) + x - v;
         if (i < n) {
-            off[i] = (uint32_t)(excl & ((1ull << kFlagShift) - 1));
+            off[i] = excl;
             fill[i] = 0;
-            const uint32_t nd = (uint32_t)(excl >> kFlagShift);  // direct bands before i
-            if (direct) maps[nd] = i;
-            else maps[n + (i - nd)] = i;
         }
         __syncthreads();
         if (threadIdx.x == blockDim.x - 1) carry = excl + v;
         __syncthreads();
     }
-    if (threadIdx.x == 0) {
-        off[n] = (uint32_t)(carry & ((1ull << kFlagShift) - 1));
-        const uint32_t nd = (uint32_t)(carry >> kFlagShift);
-        map_count[0] = nd;
-        map_count[1] = n - nd;
-    }
+    if (threadIdx.x == 0) off[n] = carry;
 }
 
+// Thread per unit: append the unit to the list of every bin it touches.
+// FFT planes list the unit record per band; direct planes list, per tile,
+// the entry k_direct consumes: tick span, profile offset, max|g| (k_gprof
+// has written g) and the coefficient a eff[w] of each tile row. Lists larger
+// than ev.list_cap (the scan's total) flag kErrRange and write nothing.
 __global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ recs, const uint32_t* __restrict__ off,
-                             uint32_t* __restrict__ fill, UnitRec* __restrict__ list)
+                             uint32_t* __restrict__ fill, UnitRec* __restrict__ list, TEnt* __restrict__ tlist,
+                             const uint32_t* __restrict__ pool, unsigned* __restrict__ err)
 {
     const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
     if (u >= ev.total_units) return;
+    if (off[ev.total_bands] > ev.list_cap) {
+        if (u == 0) atomicOr(err, kErrRange);
+        return;
+    }
     const UnitRec rec = recs[u];
     if (rec.w0 < 0) return;
     const PlaneDesc& P = ev.p[rec.plane];
-    for_each_band(P, rec.w0, rec.n_w, [&](int c) {
+    if (!P.direct) {
+        for_each_bin(P, rec.w0, rec.n_w, rec.t0, rec.n_t, [&](int c) {
+            const uint32_t b = P.band_base + c;
+            list[off[b] + atomicAdd(&fill[b], 1u)] = rec;  // full record: k_conv streams the list
+        });
+        return;
+    }
+    const int L = rec.n_t + P.n_lags - 1;
+    int ts = rec.t0 + P.lo_lag;
+    if (ts < 0) ts += P.N;
+    const uint32_t goff = unit_g_off(P, rec);
+    const float gmax = __uint_as_float(pool[goff + L]);
+    for_each_bin(P, rec.w0, rec.n_w, rec.t0, rec.n_t, [&](int c) {
         const uint32_t b = P.band_base + c;
-        list[off[b] + atomicAdd(&fill[b], 1u)] = rec;  // full record: the conv kernels stream the list
+        const int r0 = (c / P.n_windows) * kTileRows, nr = min(kTileRows, P.W - r0);
+        TEnt d;
+        d.tsL = (uint32_t)ts | ((uint32_t)L << 16);
+        d.goff = goff;
+        d.gmax = gmax;
+        int rlo = kTileRows, rhi = 0;
+#pragma unroll
+        for (int r = 0; r < kTileRows; ++r) {
+            float cr = 0.0f;
+            if (r < nr && row_coef(P, r0 + r, false, rec, pool, cr) && cr != 0.0f) {
+                rlo = min(rlo, r);
+                rhi = r + 1;
+            }
+            d.c[r] = cr;
+        }
+        d.rows = (uint32_t)rlo | ((uint32_t)max(rhi, rlo) << 8);
+        tlist[off[b] + atomicAdd(&fill[b], 1u)] = d;
     });
 }
 
@@ -323,22 +294,16 @@ constexpr int kGprofWarps = 8;
 __global__ void __launch_bounds__(32 * kGprofWarps)
 k_gprof(const EventDesc ev, const UnitRec* __restrict__ recs, uint32_t* __restrict__ pool)
 {
-    extern __shared__ float s_h[];
+    extern __shared__ __align__(16) float s_h[];
     const PlaneDesc& P = ev.p[blockIdx.y];
-    if (!P.direct_ok) return;
+    if (!P.direct) return;
     const uint32_t u0 = blockIdx.x * kGprofWarps;
     if (u0 >= P.n_units) return;
     const int nl = P.n_lags;
-    // kernel tap i (i >= -kKernPad) lives at s_h[(x & 3) * q4 + (x >> 2)], x = i + kKernPad:
-    // the 4-tap lane stride of the window reads then hits 32 distinct banks
     const int nh = nl + 2 * kKernPad;
-    const int q4 = (nh + 3) >> 2;
-    for (int x = threadIdx.x; x < nh; x += blockDim.x) s_h[(x & 3) * q4 + (x >> 2)] = __ldg(&P.kern[x - kKernPad]);
+    for (int x = threadIdx.x; x < nh; x += blockDim.x) s_h[x] = __ldg(&P.kern[x - kKernPad]);
     __syncthreads();
-    auto h = [&](int i) {
-        const int x = i + kKernPad;
-        return s_h[(x & 3) * q4 + (x >> 2)];
-    };
+    const float* h = s_h + kKernPad;  // h[i], -kKernPad <= i < nl + kKernPad
     const int lane = threadIdx.x & 31;
     const uint32_t ul = u0 + (threadIdx.x >> 5);
     if (ul >= P.n_units) return;
@@ -349,40 +314,42 @@ k_gprof(const EventDesc ev, const UnitRec* __restrict__ recs, uint32_t* __restri
     const int nt = rec.n_t, L = nt + nl - 1;
     float gm = 0.0f;
     if (nt <= 32) {
+        // lane l: taps j0..j0+3, j0 = base + 4 l. Step k needs h[j0 + m - k],
+        // m < 4; four steps at a time use the 8 taps h[j0 - 4kb - 4 .. j0 - 4kb + 3]
+        // = one new 16-byte load (conflict-free: lanes read consecutive
+        // 16-byte words) + the previous one. Steps past n_t multiply tv = 0.
         const float tvl = lane < nt ? tv[lane] : 0.0f;
         for (int base = 0; base < L; base += 128) {
             const int j0 = base + 4 * lane;
-            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-            // window w_m = h[j0 + m - k]; j0 + 3 < L + 128 <= nl + kKernPad and j0 - nt >= -kKernPad
-            float w0 = h(j0), w1 = h(j0 + 1), w2 = h(j0 + 2), w3 = h(j0 + 3);
-#pragma unroll 4
-            for (int k = 0; k < nt; ++k) {
-                const float t = __shfl_sync(0xffffffffu, tvl, k);
-                const float wn = h(j0 - k - 1);
-                s0 = __fmaf_rn(t, w0, s0);
-                s1 = __fmaf_rn(t, w1, s1);
-                s2 = __fmaf_rn(t, w2, s2);
-                s3 = __fmaf_rn(t, w3, s3);
-                w3 = w2;
-                w2 = w1;
-                w1 = w0;
-                w0 = wn;
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+            float4 hc = *reinterpret_cast<const float4*>(h + j0);
+#pragma unroll 1
+            for (int kb = 0; kb < nt; kb += 4) {
+                const float4 hn = *reinterpret_cast<const float4*>(h + j0 - kb - 4);
+                const float w[8] = {hn.x, hn.y, hn.z, hn.w, hc.x, hc.y, hc.z, hc.w};  // h[j0 - kb - 4 + i]
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const float t = __shfl_sync(0xffffffffu, tvl, kb + kk);  // 0 past n_t (and lane >= 32 wraps to lanes with 0)
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) acc[m] = __fmaf_rn(t, w[4 + m - kk], acc[m]);
+                }
+                hc = hn;
             }
             if (j0 + 3 < L) {
-                *reinterpret_cast<float4*>(g + j0) = make_float4(s0, s1, s2, s3);
+                *reinterpret_cast<float4*>(g + j0) = make_float4(acc[0], acc[1], acc[2], acc[3]);
             } else {
-                if (j0 < L) g[j0] = s0;
-                if (j0 + 1 < L) g[j0 + 1] = s1;
-                if (j0 + 2 < L) g[j0 + 2] = s2;
+                if (j0 < L) g[j0] = acc[0];
+                if (j0 + 1 < L) g[j0 + 1] = acc[1];
+                if (j0 + 2 < L) g[j0 + 2] = acc[2];
             }
-            gm = fmaxf(gm, fmaxf(fmaxf(fabsf(s0), fabsf(s1)), fmaxf(fabsf(s2), fabsf(s3))));
+            gm = fmaxf(gm, fmaxf(fmaxf(fabsf(acc[0]), fabsf(acc[1])), fmaxf(fabsf(acc[2]), fabsf(acc[3]))));
         }
     } else {
         // wide tick profiles (sigma_t > ~2.5 ticks): plain per-tap sums
         for (int j = lane; j < L; j += 32) {
             const int k0 = j - nl + 1 > 0 ? j - nl + 1 : 0, k1 = j < nt - 1 ? j : nt - 1;
             float sum = 0.0f;
-            for (int k = k0; k <= k1; ++k) sum = __fmaf_rn(tv[k], h(j - k), sum);
+            for (int k = k0; k <= k1; ++k) sum = __fmaf_rn(tv[k], h[j - k], sum);
             g[j] = sum;
             gm = fmaxf(gm, fabsf(sum));
         }
@@ -444,29 +411,27 @@ __global__ void k_fluctuate(const EventDesc ev, const UnitRec* __restrict__ recs
 }  // namespace wsb
 
 extern "C" cudaError_t wsb_launch_sample(const wsb::EventDesc& ev, wsb::UnitRec* recs, uint32_t* pool, uint32_t pool_cap,
-                                         uint32_t* pool_ctr, uint32_t* band_count, uint32_t* band_cost, unsigned* err,
-                                         cudaStream_t s)
+                                         uint32_t* pool_ctr, uint32_t* band_count, unsigned* err, cudaStream_t s)
 {
     if (ev.total_units == 0) return cudaSuccess;
     const uint32_t threads = 128;
     const uint32_t blocks = (ev.total_units + threads - 1) / threads;
-    wsb::k_sample<<<blocks, threads, 0, s>>>(ev, recs, pool, pool_cap, pool_ctr, band_count, band_cost, err);
+    wsb::k_sample<<<blocks, threads, 0, s>>>(ev, recs, pool, pool_cap, pool_ctr, band_count, err);
     return cudaGetLastError();
 }
 
-extern "C" cudaError_t wsb_launch_scan(const wsb::EventDesc& ev, const uint32_t* count, const uint32_t* cost,
-                                       uint32_t* off, uint32_t* fill, uint32_t n, uint32_t* maps, uint32_t* map_count,
-                                       cudaStream_t s)
+extern "C" cudaError_t wsb_launch_scan(const uint32_t* count, uint32_t* off, uint32_t* fill, uint32_t n, cudaStream_t s)
 {
-    wsb::k_scan_bands<<<1, 1024, 0, s>>>(ev, count, cost, off, fill, n, maps, map_count);
+    wsb::k_scan_bands<<<1, 1024, 0, s>>>(count, off, fill, n);
     return cudaGetLastError();
 }
 
 extern "C" cudaError_t wsb_launch_fill(const wsb::EventDesc& ev, const wsb::UnitRec* recs, const uint32_t* off,
-                                       uint32_t* fill, wsb::UnitRec* list, cudaStream_t s)
+                                       uint32_t* fill, wsb::UnitRec* list, wsb::TEnt* tlist, const uint32_t* pool,
+                                       unsigned* err, cudaStream_t s)
 {
     if (ev.total_units == 0) return cudaSuccess;
-    wsb::k_fill_bands<<<(ev.total_units + 255) / 256, 256, 0, s>>>(ev, recs, off, fill, list);
+    wsb::k_fill_bands<<<(ev.total_units + 255) / 256, 256, 0, s>>>(ev, recs, off, fill, list, tlist, pool, err);
     return cudaGetLastError();
 }
 
@@ -476,7 +441,7 @@ extern "C" cudaError_t wsb_launch_gprof(const wsb::EventDesc& ev, const wsb::Uni
     uint32_t max_units = 0;
     int max_lags = 0;
     for (int i = 0; i < ev.n_planes; ++i)
-        if (ev.p[i].direct_ok) {
+        if (ev.p[i].direct) {
             max_units = max_units > ev.p[i].n_units ? max_units : ev.p[i].n_units;
             max_lags = max_lags > ev.p[i].n_lags ? max_lags : ev.p[i].n_lags;
         }

@@ -34,7 +34,7 @@ def _frame(ctx, path, grid, resp, depos, kappa=None):
         return Plane(ctx, grid, resp).simulate(depos, SimConfig(grid=grid, response=resp, fluctuate=False)).frame
     finally:
         ctx.set_conv_path("auto")
-        ctx.set_direct_kappa(48.0)
+        ctx.set_direct_kappa(16.0)
 
 
 @pytest.mark.parametrize("path", ["direct", "fft", "auto"])
@@ -78,22 +78,31 @@ def test_direct_wrap_both_edges(pctx, oracle):
     assert relL2_per_channel(m, m_ref) < TOL_FRAME
 
 
-def test_auto_mixed_routing_bitwise(pctx):
-    """A threshold that splits the bands between both kernels: each band's
-    rows are bitwise those of the kernel it was routed to."""
+def test_auto_routes_per_plane_bitwise(pctx):
+    """AUTO routes each plane of a call by its depo load: a sparse plane and a
+    dense plane in one event take different kernels, and each frame is
+    bitwise the frame of the kernel it was routed to."""
     grid = GridSpec(n_wires=400, n_ticks=2000, pad_wires=20, pad_ticks=100)
     resp = ResponseParams(plane_kind="induction", wire_weights=(0.1, 1.0, 0.1))
-    rng = np.random.default_rng(4)
-    d = line_tracks(20_000, grid, seed=4)
-    d["x"][:15_000] = rng.uniform(0, 300.0, 15_000)  # dense wires 0..60, sparse elsewhere
-    m_fft = _frame(pctx, "fft", grid, resp, d)
-    m_dir = _frame(pctx, "direct", grid, resp, d)
-    m_mix = _frame(pctx, "auto", grid, resp, d, kappa=40.0)
-    from_fft = np.all(m_mix == m_fft, axis=1)
-    from_dir = np.all(m_mix == m_dir, axis=1)
-    assert np.all(from_fft | from_dir)
-    assert from_fft.sum() > 8 and (from_dir & ~from_fft).sum() > 8  # both kernels really ran
-    assert relL2_per_channel(m_dir, m_fft) < TOL_FRAME
+    sparse = line_tracks(2_000, grid, seed=4)
+    dense = line_tracks(60_000, grid, seed=5)
+    planes = [Plane(pctx, grid, resp), Plane(pctx, grid, resp)]
+    cfg = SimConfig(fluctuate=False)
+    forced = {}
+    for path in ("fft", "direct"):
+        pctx.set_conv_path(path)
+        forced[path] = [p.simulate(d, cfg).frame for p, d in zip(planes, (sparse, dense))]
+    pctx.set_conv_path("auto")
+    # work estimate per plane = depos x 12 x (n_lags + 16); cells = W x Np
+    pctx.set_direct_kappa(10.0)
+    try:
+        frames, _ = simulate_event(pctx, planes, [sparse, dense], cfg)
+    finally:
+        pctx.set_direct_kappa(16.0)
+    np.testing.assert_array_equal(frames[0], forced["direct"][0])
+    np.testing.assert_array_equal(frames[1], forced["fft"][1])
+    for i in range(2):
+        assert relL2_per_channel(forced["direct"][i], forced["fft"][i]) < TOL_FRAME
 
 
 def test_direct_deterministic(pctx):

@@ -179,7 +179,9 @@ def test_cpp_dropin(ctx, tmp_path):
     d = np.zeros(300, dtype=gen_depos(1, 1, grid).dtype)
     d["id"], d["t"], d["x"] = i, 20.0 + 0.9 * i, 30.0 + 0.8 * i
     d["q"], d["sigma_t"], d["sigma_x"] = 1000 + (i * 37 % 9000), 0.5 + 0.003 * i, 2.5 + 0.01 * i
-    ours = Plane(ctx, grid, resp).simulate(d, SimConfig(grid=grid, response=resp, fluctuate=False)).frame
+    # run_simulation in the C++ mirror also returns the charge grid (same kernels as want_charge here)
+    ours = Plane(ctx, grid, resp).simulate(d, SimConfig(grid=grid, response=resp, fluctuate=False),
+                                           want_charge=True).frame
     np.testing.assert_array_equal(np.fromfile(out, dtype=np.float32).reshape(ours.shape), ours)
 
 
