@@ -114,17 +114,18 @@ __device__ __forceinline__ int band_plane(const EventDesc& ev, uint32_t gb)
 }
 
 // Pool layout of a fluctuation-off unit (32-bit words, see k_sample):
-//   [raw f32 x n_w][eff f32 x n_eff][tv f32 x n_t][pad to 16 B][g f32 x L][gmax f32]
-// the last two only on direct-path planes; L = n_t + n_lags - 1.
+//   [raw f32 x n_w][eff f32 x n_eff][tv f32 x n_t][pad][gmax f32][g f32 x L, 0-filled to 32k]
+// the last two only on direct-path planes (g 16-byte aligned); L = n_t + n_lags - 1.
 __device__ __forceinline__ int unit_n_eff(const PlaneDesc& P, int n_w) { return P.ww_is_one ? 0 : n_w + 2 * P.h; }
 __device__ __forceinline__ uint32_t unit_tv_off(const PlaneDesc& P, const UnitRec& r)
 {
     return r.pool + (uint32_t)(r.n_w + unit_n_eff(P, r.n_w));
 }
-// g starts on a 16-byte boundary after tv (k_gprof stores float4s)
+// g starts on a 16-byte boundary after tv and one word for max|g| (g[-1]);
+// k_gprof stores float4s and zero-fills g up to a multiple of 32 taps
 __device__ __forceinline__ uint32_t unit_g_off(const PlaneDesc& P, const UnitRec& r)
 {
-    return (unit_tv_off(P, r) + (uint32_t)r.n_t + 3u) & ~3u;
+    return (unit_tv_off(P, r) + (uint32_t)r.n_t + 4u) & ~3u;
 }
 
 // Coefficient of unit `r` on wire row w of the (stencilled unless raw) charge:

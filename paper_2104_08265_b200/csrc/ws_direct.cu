@@ -30,8 +30,8 @@ namespace wsb {
 
 constexpr int kQ = 5;                          // profile taps per lane in registers: L <= 160 fast path
 constexpr int kSlot = 32 * kQ;                 // ring slot (floats)
-constexpr int kMargin = kSlot;                 // discard margin at the left of every row
-constexpr int kRowStride = kMargin + kTileTicks;  // ints per tile row
+constexpr int kMargin = kSlot;                 // discard margins either side of every row
+constexpr int kRowStride = kMargin + kTileTicks + kMargin;  // ints per tile row
 constexpr int kRing = 3;                       // profile fetches in flight per warp
 constexpr int kDirectThreads = 512;
 
@@ -54,25 +54,45 @@ __device__ __forceinline__ void red_shared_off(uint32_t saddr, int v)
     asm volatile("red.shared.add.s32 [%0+%2], %1;" ::"r"(saddr), "r"(v), "n"(OFF) : "memory");
 }
 
-// Scatter one profile chunk (gv: kQ taps per lane, a: the lanes' byte
-// addresses in row 0) into tile rows r..kTileRows-1 that lie in [rlo, rhi):
-// one FFMA rounding + one IADD + one RED per tap, row offsets as immediates.
-template <int r>
-__device__ __forceinline__ void scatter_rows(const float* __restrict__ c, int rlo, int rhi, bool q4, const uint32_t* a,
+// One tile row r of one profile (gv: taps lane + 32 q, q < NQ; a0: the
+// lane's byte address of tap 0 in row 0): one FFMA rounding + one IADD + one
+// RED per tap, with the row and tap offsets as instruction immediates.
+template <int r, int NQ>
+__device__ __forceinline__ void scatter_row(float cs, uint32_t a0, const float* gv)
+{
+    constexpr int off = r * 4 * kRowStride;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        if constexpr (NQ > 0) {
+            switch (q) {  // compile-time after unrolling: immediates need constants
+                case 0: red_shared_off<off + 0>(a0, fix_rn(cs, gv[0])); break;
+                case 1: red_shared_off<off + 128>(a0, fix_rn(cs, gv[1])); break;
+                case 2: red_shared_off<off + 256>(a0, fix_rn(cs, gv[2])); break;
+                case 3: red_shared_off<off + 384>(a0, fix_rn(cs, gv[3])); break;
+                default: red_shared_off<off + 512>(a0, fix_rn(cs, gv[4])); break;
+            }
+        }
+    }
+}
+
+// Rows [rlo, rhi) of the tile: a jump into an unrolled run of rows (one
+// compare per row), so rows outside the depo's footprint cost nothing.
+template <int NQ>
+__device__ __forceinline__ void scatter_rows(const float* __restrict__ c, int rlo, int rhi, uint32_t a0,
                                              const float* gv)
 {
-    if constexpr (r < kTileRows) {
-        if (r >= rlo && r < rhi) {  // warp-uniform
-            constexpr int off = r * 4 * kRowStride;
-            const float cs = c[r];
-            red_shared_off<off>(a[0], fix_rn(cs, gv[0]));
-            red_shared_off<off>(a[1], fix_rn(cs, gv[1]));
-            red_shared_off<off>(a[2], fix_rn(cs, gv[2]));
-            red_shared_off<off>(a[3], fix_rn(cs, gv[3]));
-            if (q4) red_shared_off<off>(a[4], fix_rn(cs, gv[4]));
-        }
-        scatter_rows<r + 1>(c, rlo, rhi, q4, a, gv);
+    static_assert(kTileRows == 16, "unrolled for 16 rows");
+#define WSB_ROW(R_)                                                \
+    case R_:                                                       \
+        if (R_ >= rhi) break;                                      \
+        scatter_row<R_, NQ>(c[R_], a0, gv);                        \
+        [[fallthrough]];
+    switch (rlo) {
+        WSB_ROW(0) WSB_ROW(1) WSB_ROW(2) WSB_ROW(3) WSB_ROW(4) WSB_ROW(5) WSB_ROW(6) WSB_ROW(7)
+        WSB_ROW(8) WSB_ROW(9) WSB_ROW(10) WSB_ROW(11) WSB_ROW(12) WSB_ROW(13) WSB_ROW(14) WSB_ROW(15)
+        default: break;
     }
+#undef WSB_ROW
 }
 
 __device__ __forceinline__ void cp_async16(uint32_t saddr, const void* gptr)
@@ -118,9 +138,12 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
     __shared__ float s_scale[R], s_inv[R];
     __shared__ int s_ovf;
 
+    const uint32_t sacc = (uint32_t)__cvta_generic_to_shared(acc);
     {
-        int4* z = reinterpret_cast<int4*>(acc);
-        for (int i = tid; i < R * kRowStride / 4; i += NT) z[i] = make_int4(0, 0, 0, 0);
+        constexpr int kZ = R * kRowStride / 4;  // 16-byte words of the rows
+#pragma unroll 4
+        for (int i = tid; i < kZ; i += NT)
+            asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(sacc + 16u * (uint32_t)i), "r"(0) : "memory");
         for (int i = tid; i < R * kSegs; i += NT) segb[i] = 0u;
         if (tid < R) s_tmax[tid] = 0u;
         if (tid == 0) s_ovf = 0;
@@ -212,7 +235,6 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
     // tick ts + j of every covered row (consecutive lanes -> consecutive
     // banks); ticks outside the window go to the lane's margin slot. Each
     // warp streams its entries' profiles through a D-deep cp.async ring.
-    const uint32_t sacc = (uint32_t)__cvta_generic_to_shared(acc);
     constexpr uint32_t row_bytes = 4u * kRowStride;
     float* my_ring = ring + (size_t)warp * D * kSlot;
     const uint32_t s_ring = (uint32_t)__cvta_generic_to_shared(my_ring);
@@ -221,22 +243,22 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
         const uint32_t tsL = d.tsL, rows = d.rows;
         const int ts = (int)(tsL & 0xffffu), L = (int)(tsL >> 16);
         const int rlo = (int)(rows & 0xffu), rhi = (int)(rows >> 8);
-        if (L <= kSlot) {
-            uint32_t a[kQ];
-#pragma unroll
-            for (int q = 0; q < kQ; ++q) {
-                const int j = lane + 32 * q;
-                int t = ts + j;
-                if (L > N) t %= N;
-                else if (t >= N) t -= N;
-                const int loc = t - ws;
-                const bool ok = j < L && (unsigned)loc < (unsigned)wlen;
-                a[q] = sacc + 4u * (uint32_t)(ok ? kMargin + loc : j);
+        if (L <= kSlot && ts + L <= N) {
+            // fast path (no circular wrap): tap j of the profile lands on
+            // window tick ts - ws + j; taps outside the window land in the
+            // row margins, taps past L add 0 (g is 0-filled to 32 k taps)
+            const uint32_t a0 = sacc + 4u * (uint32_t)(kMargin + ts - ws + lane);
+            static_assert(kQ == 5, "scatter_rows handles up to 5 taps per lane");
+            switch ((L + 31) >> 5) {  // 32-tap groups in g's 0-filled length (warp-uniform)
+                case 5: scatter_rows<5>(d.c, rlo, rhi, a0, gv); break;
+                case 4: scatter_rows<4>(d.c, rlo, rhi, a0, gv); break;
+                case 3: scatter_rows<3>(d.c, rlo, rhi, a0, gv); break;
+                case 2: scatter_rows<2>(d.c, rlo, rhi, a0, gv); break;
+                default: scatter_rows<1>(d.c, rlo, rhi, a0, gv); break;
             }
-            static_assert(kQ == 5, "scatter_rows handles 5 taps per lane");
-            scatter_rows<0>(d.c, rlo, rhi, L > 32 * (kQ - 1), a, gv);
         } else {
-            // long profiles: 32-tap steps from global memory
+            // long profiles / spans wrapping past the row end: 32-tap steps
+            // from global memory, general wrap
             const float* g = reinterpret_cast<const float*>(pool + d.goff);
 #pragma unroll 1
             for (int base = 0; base < L; base += 32) {
@@ -264,7 +286,7 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
         auto fetch = [&](int e, int s) {
             if (e < cnt) {
                 const TEnt& d = ent[e];
-                const int n4 = min(((int)(d.tsL >> 16) + 3) >> 2, kSlot / 4);
+                const int n4 = min((((int)(d.tsL >> 16) + 31) & ~31) >> 2, kSlot / 4);
                 const float* src = reinterpret_cast<const float*>(pool + d.goff);
                 const uint32_t dst = s_ring + 4u * (uint32_t)(s * kSlot);
                 if (lane < n4) cp_async16(dst + 16u * lane, src + 4 * lane);
@@ -281,7 +303,7 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
             __syncwarp();
             float gv[kQ];
 #pragma unroll
-            for (int q = 0; q < kQ; ++q) gv[q] = my_ring[s * kSlot + lane + 32 * q];  // past L: discarded lanes
+            for (int q = 0; q < kQ; ++q) gv[q] = my_ring[s * kSlot + lane + 32 * q];  // past ceil32(L): unused
             __syncwarp();
             fetch(e + NW * D, s);
             s = s + 1 == D ? 0 : s + 1;
@@ -291,20 +313,24 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
     }
     __syncthreads();
 
-    // frame rows of the window (convolve's real part, spectral.cpp:172-173), streaming stores
-    for (int r = 0; r < nr; ++r) {
-        const float inv = s_inv[r];
-        const int* row = acc + r * kRowStride + kMargin;
-        float* frow = P.frame + (size_t)(r0 + r) * N + ws;
-        if ((N & 3) == 0) {
-            const int4* a4 = reinterpret_cast<const int4*>(row);
-            float4* f4 = reinterpret_cast<float4*>(frow);
-            for (int i = tid; i < (wlen >> 2); i += NT) {
-                const int4 v = a4[i];
-                __stcs(&f4[i], make_float4((float)v.x * inv, (float)v.y * inv, (float)v.z * inv, (float)v.w * inv));
-            }
-        } else {
-            for (int t = tid; t < wlen; t += NT) __stcs(&frow[t], (float)row[t] * inv);
+    // frame rows of the window (convolve's real part, spectral.cpp:172-173),
+    // streaming stores; one flattened (row, 16-byte word) loop
+    if ((N & 3) == 0 && wlen == kTileTicks) {
+        constexpr int kW = kTileTicks / 4;
+        for (int i = tid; i < nr * kW; i += NT) {
+            const int r = i / kW, c4 = i - r * kW;
+            int4 v;
+            asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                         : "r"(sacc + 4u * (uint32_t)(r * kRowStride + kMargin + 4 * c4)));
+            const float inv = s_inv[r];
+            __stcs(reinterpret_cast<float4*>(P.frame + (size_t)(r0 + r) * N + ws) + c4,
+                   make_float4((float)v.x * inv, (float)v.y * inv, (float)v.z * inv, (float)v.w * inv));
+        }
+    } else {
+        for (int i = tid; i < nr * wlen; i += NT) {
+            const int r = i / wlen, t = i - r * wlen;
+            __stcs(P.frame + (size_t)(r0 + r) * N + ws + t, (float)acc[r * kRowStride + kMargin + t] * s_inv[r]);
         }
     }
 }

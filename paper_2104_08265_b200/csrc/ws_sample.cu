@@ -129,7 +129,7 @@ __global__ void k_sample(const EventDesc ev, UnitRec* __restrict__ recs, uint32_
     const bool with_g = !ev.fluctuate && ev.mode == 0 && P.direct;
     const uint32_t L = (uint32_t)(f.n_t + P.n_lags - 1);
     const uint32_t need = ev.fluctuate ? (uint32_t)(2 * (f.n_w + f.n_t) + 1)
-                                       : (uint32_t)(f.n_w + n_eff + f.n_t) + (with_g ? L + 4 : 0u);
+                                       : (uint32_t)(f.n_w + n_eff + f.n_t) + (with_g ? ((L + 31u) & ~31u) + 4u : 0u);
     uint32_t off = atomicAdd(pool_ctr, need);
     if ((uint64_t)off + need > pool_cap) {
         atomicOr(err, kErrPool);
@@ -258,7 +258,7 @@ __global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ rec
     int ts = rec.t0 + P.lo_lag;
     if (ts < 0) ts += P.N;
     const uint32_t goff = unit_g_off(P, rec);
-    const float gmax = __uint_as_float(pool[goff + L]);
+    const float gmax = __uint_as_float(pool[goff - 1]);
     for_each_bin(P, rec.w0, rec.n_w, rec.t0, rec.n_t, [&](int c) {
         const uint32_t b = P.band_base + c;
         const int r0 = (c / P.n_windows) * kTileRows, nr = min(kTileRows, P.W - r0);
@@ -335,13 +335,9 @@ k_gprof(const EventDesc ev, const UnitRec* __restrict__ recs, uint32_t* __restri
                 }
                 hc = hn;
             }
-            if (j0 + 3 < L) {
-                *reinterpret_cast<float4*>(g + j0) = make_float4(acc[0], acc[1], acc[2], acc[3]);
-            } else {
-                if (j0 < L) g[j0] = acc[0];
-                if (j0 + 1 < L) g[j0 + 1] = acc[1];
-                if (j0 + 2 < L) g[j0 + 2] = acc[2];
-            }
+            // taps past L come out 0 (kernel zero padding): the store fills
+            // g up to the next multiple of 32 taps (the k_direct ring copies)
+            if (j0 < ((L + 31) & ~31)) *reinterpret_cast<float4*>(g + j0) = make_float4(acc[0], acc[1], acc[2], acc[3]);
             gm = fmaxf(gm, fmaxf(fmaxf(fabsf(acc[0]), fabsf(acc[1])), fmaxf(fabsf(acc[2]), fabsf(acc[3]))));
         }
     } else {
@@ -353,10 +349,11 @@ k_gprof(const EventDesc ev, const UnitRec* __restrict__ recs, uint32_t* __restri
             g[j] = sum;
             gm = fmaxf(gm, fabsf(sum));
         }
+        for (int j = L + lane; j < ((L + 31) & ~31); j += 32) g[j] = 0.0f;
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, o));
-    if (lane == 0) g[L] = gm;
+    if (lane == 0) g[-1] = gm;
 }
 
 // Fluctuation walk, one thread per unit: sample_patch's exact probabilities
