@@ -28,6 +28,7 @@ SOURCES = {
     "ws_sample.cu": ["--fmad=false"],
     "ws_conv.cu": [],
     "ws_direct.cu": [],
+    "ws_gprof.cu": [],
     "ws_api.cu": [],
     "ws_host.cu": ["--fmad=false"],
 }

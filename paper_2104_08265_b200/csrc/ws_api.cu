@@ -132,6 +132,8 @@ struct ws_ctx {
     int conv_path = WS_CONV_AUTO;                // ws_ctx_set_conv_path
     double direct_kappa = 16.0;                  // AUTO: direct if est. depo-row-taps <= kappa x cells (per plane)
     cudaStream_t copy_stream = nullptr;          // D2H of the pipelined batch path
+    cudaStream_t aux_stream = nullptr;           // k_gprof, concurrent with binning
+    cudaEvent_t aux_fork = nullptr, aux_join = nullptr;
     cudaEvent_t slot_computed[2] = {nullptr, nullptr};
     cudaEvent_t slot_copied[2] = {nullptr, nullptr};
 };
@@ -148,6 +150,7 @@ struct ws_plane {
     double* d_ww = nullptr;
     float2* d_H = nullptr;
     float* d_kern = nullptr;  // combined kernel taps (fp32) for the direct path
+    float kern_absmax = 0.0f;
     int direct_ok = 0;   // eligible for the time-domain path
     int n_windows = 0;   // direct: tick windows per 16-row band
     float2* d_tw = nullptr;
@@ -346,6 +349,7 @@ PlaneDesc plane_desc(const ws_plane* p)
     d.rows_per_band = p->rows_per_band;
     d.n_lags = (int)p->n_lags;
     d.kern = p->d_kern ? p->d_kern + wsb::kKernPad : nullptr;
+    d.kern_absmax = p->kern_absmax;
     d.direct = 0;  // decided per call (run_group)
     d.n_windows = p->n_windows;
     d.direct_cap = (uint32_t)wsb_direct_cap();
@@ -469,8 +473,18 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
     }
     WS_CUDA(cudaEventRecord(pc.ev[2], s));
     if (ev.mode == 0) {
-        if (any_direct) {  // profiles first: the tile entries' bounds need max|g|
-            WS_CUDA(wsb_launch_gprof(ev, c->recs.p, c->pool.p, s));
+        if (any_direct) {
+            // response profiles on the auxiliary stream, concurrent with the
+            // binning (k_direct is the first consumer)
+            if (!c->aux_stream) {
+                WS_CUDA(cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
+                WS_CUDA(cudaEventCreateWithFlags(&c->aux_fork, cudaEventDisableTiming));
+                WS_CUDA(cudaEventCreateWithFlags(&c->aux_join, cudaEventDisableTiming));
+            }
+            WS_CUDA(cudaEventRecord(c->aux_fork, s));
+            WS_CUDA(cudaStreamWaitEvent(c->aux_stream, c->aux_fork, 0));
+            WS_CUDA(wsb_launch_gprof(ev, c->recs.p, c->pool.p, c->aux_stream));
+            WS_CUDA(cudaEventRecord(c->aux_join, c->aux_stream));
             c->launches += units ? 1 : 0;
         }
         WS_CUDA(wsb_launch_scan(c->band_count.p, c->band_off.p, c->band_fill.p, bands, s));
@@ -488,6 +502,7 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
     if (want_frame) {
         // each kernel skips the other's planes
         if (any_direct) {
+            WS_CUDA(cudaStreamWaitEvent(s, c->aux_join, 0));
             WS_CUDA(wsb_launch_direct(ev, c->pool.p, c->band_off.p, c->tile_list.p, wsb_direct_smem(wsb_direct_cap()),
                                       s));
             c->launches += bands ? 1 : 0;
@@ -634,6 +649,12 @@ int ws_ctx_destroy(ws_ctx* c)
         cudaStreamSynchronize(c->copy_stream);
         cudaStreamDestroy(c->copy_stream);
     }
+    if (c->aux_stream) {
+        cudaStreamSynchronize(c->aux_stream);
+        cudaStreamDestroy(c->aux_stream);
+    }
+    if (c->aux_fork) cudaEventDestroy(c->aux_fork);
+    if (c->aux_join) cudaEventDestroy(c->aux_join);
     for (int s = 0; s < 2; ++s) {
         if (c->slot_computed[s]) cudaEventDestroy(c->slot_computed[s]);
         if (c->slot_copied[s]) cudaEventDestroy(c->slot_copied[s]);
@@ -815,6 +836,9 @@ int ws_plane_create(ws_ctx* ctx, const ws_grid_spec* grid, const ws_response* re
     // fixed-point rows fit in shared memory and the kernel is not huge
     p->n_windows = (p->N + wsb::kTileTicks - 1) / wsb::kTileTicks;
     if (p->n_windows <= 32 && p->n_lags <= 4096 && p->N < 65536) {
+        double km = 0.0;
+        for (double v : p->kernel) km = std::max(km, std::fabs(v));
+        p->kern_absmax = std::nextafter((float)km, INFINITY) * (1.0f + 1e-6f);  // fp32 taps x tv sums stay below
         std::vector<float> kf(p->kernel.size() + 2 * wsb::kKernPad, 0.0f);
         std::copy(p->kernel.begin(), p->kernel.end(), kf.begin() + wsb::kKernPad);
         e = cudaMalloc(&p->d_kern, sizeof(float) * kf.size());

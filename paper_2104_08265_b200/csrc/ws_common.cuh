@@ -37,7 +37,7 @@ struct __align__(16) UnitRec {
     uint32_t pool; // offset (in doubles) of [wv(n_w) | tv(n_t)] in the pool
     int32_t plane;
     float a;       // fluct off: q / total; fluct on: unused
-    float tmax;    // fluct off: max over the tick profile (bounds a row's fixed-point scale)
+    float tsum;    // fluct off: sum of the tick profile, rounded up (>= its max; bounds fixed-point scales)
 };
 
 // One entry of a direct-path tile list (k_fill_bands -> k_direct), 80 bytes.
@@ -45,7 +45,7 @@ struct __align__(16) TEnt {
     uint32_t tsL;   // first output tick ts (circular, < N) | profile length L << 16
     uint32_t goff;  // pool offset of g (16-byte aligned)
     uint32_t rows;  // covered tile rows [lo, hi): lo | hi << 8
-    float gmax;     // max |g|
+    float gbound;   // >= max|g| (sum of the tick profile x max|kernel|)
     float c[kTileRows];  // a * eff[w] per tile row (0: not covered)
 };
 
@@ -71,6 +71,7 @@ struct PlaneDesc {
     int32_t direct;            // this call: direct path (tiles, pool holds g) instead of the row FFT (bands)
     int32_t n_lags;            // combined kernel length
     const float* kern;         // n_lags combined-kernel taps (lag lo_lag first), kKernPad zeros either side
+    float kern_absmax;         // max |kernel tap| (rounded up)
     int32_t n_windows;         // direct: tick windows of kTileTicks per row band
     uint32_t direct_cap;       // direct: k_direct stages at most this many entries at a time
     // per call

@@ -59,7 +59,7 @@ __device__ __forceinline__ bool cover_of(const PlaneDesc& P, int w, bool raw, co
     if (j < 0) j += P.W;
     if (j >= n_rows) return false;
     const uint32_t off = __ldg(&list[i].pool);
-    const float2 at = __ldg(reinterpret_cast<const float2*>(&list[i].a));  // a, tmax
+    const float2 at = __ldg(reinterpret_cast<const float2*>(&list[i].a));  // a, tsum (>= max of the tick profile)
     const float* prof = reinterpret_cast<const float*>(pool + off) + (stencil ? n_w : 0);
     float c = 0.0f;
     for (; j < n_rows; j += P.W) c += __ldg(&prof[j]);  // a wrap can land twice on a tiny grid

@@ -179,7 +179,7 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
             for (int i = tid; i < cnt * R; i += NT) {
                 const TEnt& d = ent[i >> 4];
                 const int r = i & (R - 1);
-                const float t = fabsf(d.c[r]) * d.gmax;
+                const float t = __fmul_ru(fabsf(d.c[r]), d.gbound);  // >= every |a eff g| of the row
                 if (!(t > 0.0f)) continue;
                 const float tu = ceilf(ldexpf(t, -ue));
                 if (tu >= 4294967296.0f) {

@@ -1,0 +1,202 @@
+// Per-depo response profiles for the time-domain path on the tensor cores.
+//
+// Every unit (depo on a direct-path plane) needs g[j] = sum_k tv[k] h[j - k],
+// j < L = n_t + n_lags - 1: its tick profile tv (n_t <= 32 bins,
+// sample_patch's bin integrals, rasterize.cpp:91-92) convolved with the
+// plane's combined time kernel h (build_response's time-domain kernel,
+// spectral.cpp:98-113). For 16 units at a time this is a dense GEMM
+//   G[16 x N] = TV[16 x K] . T[K x N],  T[k][j] = h[j - k]  (Toeplitz, K <= 32),
+// run as mma.sync m16n8k8 TF32 with the 3-pass split (a_hi b_hi + a_hi b_lo +
+// a_lo b_hi, fp32 accumulate: ~fp32 accuracy). The Toeplitz operand is never
+// materialised: B fragments read the kernel's hi/lo TF32 parts from shared
+// memory at offset j - k. g is zero-filled up to a multiple of 32 taps (the
+// kernel is zero-padded) and max|g| goes to g[-1]. Units with n_t > 32 (very
+// wide depos) take a per-warp SIMT loop.
+#include "ws_common.cuh"
+
+#include <algorithm>
+
+namespace wsb {
+
+constexpr int kGpWarps = 4;
+constexpr int kGpPre = 32;  // kernel taps staged before index 0 (j - k >= -31)
+
+__device__ __forceinline__ uint32_t tf32_rna(float x)
+{
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return r;
+}
+
+__device__ __forceinline__ void mma_tf32(float* c, const uint32_t* a, uint32_t b0, uint32_t b1)
+{
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+        "{%0, %1, %2, %3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__global__ void __launch_bounds__(32 * kGpWarps)
+k_gprof(const EventDesc ev, const UnitRec* __restrict__ recs, uint32_t* __restrict__ pool)
+{
+    const PlaneDesc& P = ev.p[blockIdx.y];
+    if (!P.direct || P.n_units == 0) return;
+    const int nl = P.n_lags;
+    const int ntap = (nl + 31 + 31) & ~31;  // >= ceil32(L) for every n_t <= 32
+    // kernel tap i, -kGpPre <= i < ntap, split into TF32 hi + lo parts
+    extern __shared__ uint32_t s_hk[];
+    uint32_t* hh = s_hk;
+    uint32_t* hl = s_hk + (ntap + kGpPre);
+    for (int x = threadIdx.x; x < ntap + kGpPre; x += blockDim.x) {
+        const float v = __ldg(&P.kern[x - kGpPre]);  // zero-padded by kKernPad >= 192 taps
+        const uint32_t hi = tf32_rna(v);
+        hh[x] = hi;
+        hl[x] = tf32_rna(v - __uint_as_float(hi));
+    }
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gq = lane >> 2, tq = lane & 3;  // mma fragment coordinates
+    const int n_groups = (int)((P.n_units + 15) / 16);
+    for (int grp = blockIdx.x * kGpWarps + warp; grp < n_groups; grp += gridDim.x * kGpWarps) {
+        // this thread's two units: rows gq and gq + 8 of the group
+        const float* tv[2];
+        float* gp[2];
+        int nt[2], lp[2];
+        bool mine[2], wide[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t ul = (uint32_t)grp * 16 + gq + 8 * h;
+            mine[h] = false;
+            wide[h] = false;
+            nt[h] = 0;
+            lp[h] = 0;
+            tv[h] = nullptr;
+            gp[h] = nullptr;
+            if (ul < P.n_units) {
+                const UnitRec rec = recs[P.unit_base + ul];
+                if (rec.w0 >= 0) {
+                    tv[h] = reinterpret_cast<const float*>(pool + unit_tv_off(P, rec));
+                    gp[h] = reinterpret_cast<float*>(pool + unit_g_off(P, rec));
+                    wide[h] = rec.n_t > 32;
+                    mine[h] = !wide[h];
+                    nt[h] = mine[h] ? rec.n_t : 0;
+                    lp[h] = (rec.n_t + nl - 1 + 31) & ~31;
+                }
+            }
+        }
+        // k steps (8 taps of tv each) and n tiles (8 output taps) the group needs
+        int ks_n = (max(nt[0], nt[1]) + 7) >> 3;
+        int nt_n = max(mine[0] ? lp[0] : 0, mine[1] ? lp[1] : 0) >> 3;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            ks_n = max(ks_n, __shfl_xor_sync(0xffffffffu, ks_n, o));
+            nt_n = max(nt_n, __shfl_xor_sync(0xffffffffu, nt_n, o));
+        }
+        // A fragments (row-major 16 x 8 per k step): a0 (gq, tq), a1 (gq+8, tq),
+        // a2 (gq, tq+4), a3 (gq+8, tq+4); hi and lo TF32 parts
+        uint32_t ah[4][4], al[4][4];
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int h = e & 1, k = 8 * ks + tq + 4 * (e >> 1);
+                const float v = (ks < ks_n && k < nt[h]) ? tv[h][k] : 0.0f;
+                ah[ks][e] = tf32_rna(v);
+                al[ks][e] = tf32_rna(v - __uint_as_float(ah[ks][e]));
+            }
+        }
+        float gmax[2] = {0.0f, 0.0f};
+#pragma unroll 1
+        for (int n = 0; n < nt_n; ++n) {
+            // three independent accumulation chains (hi.hi, hi.lo, lo.hi)
+            float c[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f}, c2[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+                if (ks >= ks_n) break;
+                // B (col-major 8 x 8): b0 (k = tq, j = gq), b1 (k = tq + 4, j = gq); T[k][j] = h[j - k]
+                const int x = 8 * n + gq - 8 * ks - tq + kGpPre;
+                const uint32_t bh0 = hh[x], bh1 = hh[x - 4], bl0 = hl[x], bl1 = hl[x - 4];
+                mma_tf32(c, ah[ks], bh0, bh1);
+                mma_tf32(c1, ah[ks], bl0, bl1);
+                mma_tf32(c2, al[ks], bh0, bh1);
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) c[e] += c1[e] + c2[e];
+            // C (16 x 8): c0, c1 -> row gq, taps 8n + 2tq, +1; c2, c3 -> row gq + 8
+            const int j = 8 * n + 2 * tq;
+            if (mine[0] && j < lp[0]) *reinterpret_cast<float2*>(gp[0] + j) = make_float2(c[0], c[1]);
+            if (mine[1] && j < lp[1]) *reinterpret_cast<float2*>(gp[1] + j) = make_float2(c[2], c[3]);
+            gmax[0] = fmaxf(gmax[0], fmaxf(fabsf(c[0]), fabsf(c[1])));
+            gmax[1] = fmaxf(gmax[1], fmaxf(fabsf(c[2]), fabsf(c[3])));
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            gmax[h] = fmaxf(gmax[h], __shfl_xor_sync(0xffffffffu, gmax[h], 1));
+            gmax[h] = fmaxf(gmax[h], __shfl_xor_sync(0xffffffffu, gmax[h], 2));
+            if (mine[h] && tq == 0) gp[h][-1] = gmax[h];
+        }
+        // wide tick profiles (n_t > 32): the whole warp, one unit at a time
+        if (!__any_sync(0xffffffffu, wide[0] || wide[1])) continue;
+#pragma unroll 1
+        for (int src = 0; src < 32; src += 4) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const bool w = __shfl_sync(0xffffffffu, wide[h], src);
+                if (!w) continue;  // lane 4 gq (tq == 0) speaks for rows gq, gq + 8
+                const float* tvw = reinterpret_cast<const float*>(
+                    __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(tv[h]), src));
+                float* gw = reinterpret_cast<float*>(
+                    __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(gp[h]), src));
+                const int lpw = __shfl_sync(0xffffffffu, lp[h], src);
+                const UnitRec rec = recs[P.unit_base + (uint32_t)grp * 16 + (src >> 2) + 8 * h];
+                const int ntr = rec.n_t, L = ntr + nl - 1;
+                float gm = 0.0f;
+                for (int jj = lane; jj < lpw; jj += 32) {
+                    const int k0 = jj - nl + 1 > 0 ? jj - nl + 1 : 0, k1 = jj < ntr - 1 ? jj : ntr - 1;
+                    float sum = 0.0f;
+                    for (int k = k0; k <= k1; ++k) sum = __fmaf_rn(tvw[k], __ldg(&P.kern[jj - k]), sum);
+                    gw[jj] = jj < L ? sum : 0.0f;
+                    gm = fmaxf(gm, fabsf(sum));
+                }
+#pragma unroll
+                for (int o = 16; o; o >>= 1) gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, o));
+                if (lane == 0) gw[-1] = gm;
+            }
+        }
+    }
+}
+
+}  // namespace wsb
+
+extern "C" cudaError_t wsb_launch_gprof(const wsb::EventDesc& ev, const wsb::UnitRec* recs, uint32_t* pool,
+                                        cudaStream_t s)
+{
+    uint32_t max_units = 0;
+    int max_lags = 0;
+    for (int i = 0; i < ev.n_planes; ++i)
+        if (ev.p[i].direct) {
+            max_units = max_units > ev.p[i].n_units ? max_units : ev.p[i].n_units;
+            max_lags = max_lags > ev.p[i].n_lags ? max_lags : ev.p[i].n_lags;
+        }
+    if (max_units == 0) return cudaSuccess;
+    const int ntap = (max_lags + 62) & ~31;
+    const size_t smem = 2 * sizeof(uint32_t) * (size_t)(ntap + wsb::kGpPre);
+    static unsigned long long ready = 0;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (!(ready & (1ull << dev))) {
+        e = cudaFuncSetAttribute(wsb::k_gprof, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        if (e != cudaSuccess) return e;
+        ready |= 1ull << dev;
+    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned groups = (max_units + 15) / 16;
+    const unsigned blocks = std::min<unsigned>((groups + wsb::kGpWarps - 1) / wsb::kGpWarps, (unsigned)sms * 8);
+    const dim3 grid(blocks, (unsigned)ev.n_planes);
+    wsb::k_gprof<<<grid, 32 * wsb::kGpWarps, smem, s>>>(ev, recs, pool);
+    return cudaGetLastError();
+}

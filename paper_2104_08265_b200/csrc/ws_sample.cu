@@ -109,7 +109,7 @@ __global__ void k_sample(const EventDesc ev, UnitRec* __restrict__ recs, uint32_
     rec.pool = 0;
     rec.plane = pi;
     rec.a = 0.0f;
-    rec.tmax = 0.0f;
+    rec.tsum = 0.0f;
     if (ev.drift_enabled && !drift(ev, d)) {
         atomicOr(err, kErrDomain);
         recs[u] = rec;
@@ -175,7 +175,7 @@ __global__ void k_sample(const EventDesc ev, UnitRec* __restrict__ recs, uint32_
             }
         }
         rec.a = (float)a;
-        rec.tmax = (float)mt;
+        rec.tsum = __double2float_ru(st);
     }
     rec.w0 = f.w0;
     rec.t0 = f.t0;
@@ -231,8 +231,9 @@ __global__ void k_scan_bands(const uint32_t* __restrict__ count, uint32_t* __res
 
 // Thread per unit: append the unit to the list of every bin it touches.
 // FFT planes list the unit record per band; direct planes list, per tile,
-// the entry k_direct consumes: tick span, profile offset, max|g| (k_gprof
-// has written g) and the coefficient a eff[w] of each tile row. Lists larger
+// the entry k_direct consumes: tick span, profile offset and the
+// coefficient a eff[w] of each tile row (independent of k_gprof, which may
+// run concurrently on the auxiliary stream). Lists larger
 // than ev.list_cap (the scan's total) flag kErrRange and write nothing.
 __global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ recs, const uint32_t* __restrict__ off,
                              uint32_t* __restrict__ fill, UnitRec* __restrict__ list, TEnt* __restrict__ tlist,
@@ -258,14 +259,13 @@ __global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ rec
     int ts = rec.t0 + P.lo_lag;
     if (ts < 0) ts += P.N;
     const uint32_t goff = unit_g_off(P, rec);
-    const float gmax = __uint_as_float(pool[goff - 1]);
     for_each_bin(P, rec.w0, rec.n_w, rec.t0, rec.n_t, [&](int c) {
         const uint32_t b = P.band_base + c;
         const int r0 = (c / P.n_windows) * kTileRows, nr = min(kTileRows, P.W - r0);
         TEnt d;
         d.tsL = (uint32_t)ts | ((uint32_t)L << 16);
         d.goff = goff;
-        d.gmax = gmax;
+        d.gbound = __fmul_ru(rec.tsum, P.kern_absmax);
         int rlo = kTileRows, rhi = 0;
 #pragma unroll
         for (int r = 0; r < kTileRows; ++r) {
@@ -279,81 +279,6 @@ __global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ rec
         d.rows = (uint32_t)rlo | ((uint32_t)max(rhi, rlo) << 8);
         tlist[off[b] + atomicAdd(&fill[b], 1u)] = d;
     });
-}
-
-// Response profiles of the units on direct-path planes: for each unit
-// g[j] = sum_k tv[k] kernel[j - k], j < L = n_t + n_lags - 1 (the tick profile
-// convolved with the combined time kernel, shared by all wire rows of the
-// depo), and max|g| after it. Grid (unit groups, plane): the block stages
-// its plane's kernel, zero-padded by kKernPad taps on both sides, in shared
-// memory; one warp per unit, lane l computes 4 consecutive taps per 128-tap
-// chunk with a sliding register window over the kernel, the tick profile in
-// lane registers broadcast by shuffles, one 16-byte store per lane.
-constexpr int kGprofWarps = 8;
-
-__global__ void __launch_bounds__(32 * kGprofWarps)
-k_gprof(const EventDesc ev, const UnitRec* __restrict__ recs, uint32_t* __restrict__ pool)
-{
-    extern __shared__ __align__(16) float s_h[];
-    const PlaneDesc& P = ev.p[blockIdx.y];
-    if (!P.direct) return;
-    const uint32_t u0 = blockIdx.x * kGprofWarps;
-    if (u0 >= P.n_units) return;
-    const int nl = P.n_lags;
-    const int nh = nl + 2 * kKernPad;
-    for (int x = threadIdx.x; x < nh; x += blockDim.x) s_h[x] = __ldg(&P.kern[x - kKernPad]);
-    __syncthreads();
-    const float* h = s_h + kKernPad;  // h[i], -kKernPad <= i < nl + kKernPad
-    const int lane = threadIdx.x & 31;
-    const uint32_t ul = u0 + (threadIdx.x >> 5);
-    if (ul >= P.n_units) return;
-    const UnitRec rec = recs[P.unit_base + ul];
-    if (rec.w0 < 0) return;
-    const float* tv = reinterpret_cast<const float*>(pool + unit_tv_off(P, rec));
-    float* g = reinterpret_cast<float*>(pool + unit_g_off(P, rec));
-    const int nt = rec.n_t, L = nt + nl - 1;
-    float gm = 0.0f;
-    if (nt <= 32) {
-        // lane l: taps j0..j0+3, j0 = base + 4 l. Step k needs h[j0 + m - k],
-        // m < 4; four steps at a time use the 8 taps h[j0 - 4kb - 4 .. j0 - 4kb + 3]
-        // = one new 16-byte load (conflict-free: lanes read consecutive
-        // 16-byte words) + the previous one. Steps past n_t multiply tv = 0.
-        const float tvl = lane < nt ? tv[lane] : 0.0f;
-        for (int base = 0; base < L; base += 128) {
-            const int j0 = base + 4 * lane;
-            float acc[4] = {0.f, 0.f, 0.f, 0.f};
-            float4 hc = *reinterpret_cast<const float4*>(h + j0);
-#pragma unroll 1
-            for (int kb = 0; kb < nt; kb += 4) {
-                const float4 hn = *reinterpret_cast<const float4*>(h + j0 - kb - 4);
-                const float w[8] = {hn.x, hn.y, hn.z, hn.w, hc.x, hc.y, hc.z, hc.w};  // h[j0 - kb - 4 + i]
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {
-                    const float t = __shfl_sync(0xffffffffu, tvl, kb + kk);  // 0 past n_t (and lane >= 32 wraps to lanes with 0)
-#pragma unroll
-                    for (int m = 0; m < 4; ++m) acc[m] = __fmaf_rn(t, w[4 + m - kk], acc[m]);
-                }
-                hc = hn;
-            }
-            // taps past L come out 0 (kernel zero padding): the store fills
-            // g up to the next multiple of 32 taps (the k_direct ring copies)
-            if (j0 < ((L + 31) & ~31)) *reinterpret_cast<float4*>(g + j0) = make_float4(acc[0], acc[1], acc[2], acc[3]);
-            gm = fmaxf(gm, fmaxf(fmaxf(fabsf(acc[0]), fabsf(acc[1])), fmaxf(fabsf(acc[2]), fabsf(acc[3]))));
-        }
-    } else {
-        // wide tick profiles (sigma_t > ~2.5 ticks): plain per-tap sums
-        for (int j = lane; j < L; j += 32) {
-            const int k0 = j - nl + 1 > 0 ? j - nl + 1 : 0, k1 = j < nt - 1 ? j : nt - 1;
-            float sum = 0.0f;
-            for (int k = k0; k <= k1; ++k) sum = __fmaf_rn(tv[k], h[j - k], sum);
-            g[j] = sum;
-            gm = fmaxf(gm, fabsf(sum));
-        }
-        for (int j = L + lane; j < ((L + 31) & ~31); j += 32) g[j] = 0.0f;
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, o));
-    if (lane == 0) g[-1] = gm;
 }
 
 // Fluctuation walk, one thread per unit: sample_patch's exact probabilities
@@ -429,32 +354,6 @@ extern "C" cudaError_t wsb_launch_fill(const wsb::EventDesc& ev, const wsb::Unit
 {
     if (ev.total_units == 0) return cudaSuccess;
     wsb::k_fill_bands<<<(ev.total_units + 255) / 256, 256, 0, s>>>(ev, recs, off, fill, list, tlist, pool, err);
-    return cudaGetLastError();
-}
-
-extern "C" cudaError_t wsb_launch_gprof(const wsb::EventDesc& ev, const wsb::UnitRec* recs, uint32_t* pool,
-                                        cudaStream_t s)
-{
-    uint32_t max_units = 0;
-    int max_lags = 0;
-    for (int i = 0; i < ev.n_planes; ++i)
-        if (ev.p[i].direct) {
-            max_units = max_units > ev.p[i].n_units ? max_units : ev.p[i].n_units;
-            max_lags = max_lags > ev.p[i].n_lags ? max_lags : ev.p[i].n_lags;
-        }
-    if (max_units == 0) return cudaSuccess;
-    const size_t smem = sizeof(float) * (size_t)(max_lags + 2 * wsb::kKernPad + 4);
-    static unsigned long long ready = 0;
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    if (!(ready & (1ull << dev))) {
-        e = cudaFuncSetAttribute(wsb::k_gprof, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-        if (e != cudaSuccess) return e;
-        ready |= 1ull << dev;
-    }
-    const dim3 grid((max_units + wsb::kGprofWarps - 1) / wsb::kGprofWarps, (unsigned)ev.n_planes);
-    wsb::k_gprof<<<grid, 32 * wsb::kGprofWarps, smem, s>>>(ev, recs, pool);
     return cudaGetLastError();
 }
 
