@@ -258,13 +258,17 @@ def main():
     ms_per_step = ms / args.steps
     value = world * N_DEPOS * args.steps / (ms * 1e-3)
 
-    # dominant kernel (k_conv) roofline: SURVEY.md §8(d) K3 algorithmic traffic
-    # 8 B/cell (read S + write M) x cells of the event, over its measured time.
+    # dominant kernel roofline: the convolution stage (k_direct on
+    # time-domain planes, k_conv on row-FFT planes), timed live by the stage
+    # events around it. Algorithmic traffic = SURVEY.md §8(d) K3's floor,
+    # 8 B/cell (read S + write M), x the event's cells.
     conv_ms = max_over_ranks(float(stage.convolve_ms))
+    n_direct = int(stage.direct_planes)
+    conv_kernel = "k_direct" if n_direct == len(planes) else ("k_conv" if n_direct == 0 else "k_direct+k_conv")
     alg_bytes = 8.0 * cells
     peak, peak_kind = peaks()
     achieved = alg_bytes / (conv_ms * 1e-3) / 1e9
-    prof = ROOT / "profiles" / "traffic_k_conv.json"
+    prof = ROOT / "profiles" / f"traffic_{conv_kernel.split('+')[0]}.json"
     traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch") if prof.exists() else None
 
     # end-to-end through the host-buffer API (pinned host depos in, frames out)
@@ -322,10 +326,11 @@ def main():
                        "cells_per_event": cells, "l2": "inputs rotate over 10 distinct events (144 MB > 126 MB L2)",
                        "parallelism": f"event-sharded x{world}",
                        "stage_ms": {k: round(getattr(stage, k), 4) for k in
-                                    ("prepare_ms", "bin_ms", "convolve_ms", "total_ms")}},
+                                    ("prepare_ms", "bin_ms", "convolve_ms", "total_ms")},
+                       "conv_path": f"{n_direct}/{len(planes)} planes time-domain (k_direct), rest row-FFT (k_conv)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": "k_conv",
-                         "algorithmic_bytes": alg_bytes, "peak_kind": peak_kind},
+                         "frac": achieved / peak, "traffic": traffic, "kernel": conv_kernel,
+                         "kernel_ms": conv_ms, "algorithmic_bytes": alg_bytes, "peak_kind": peak_kind},
             "clocks": clocks.summary(),
             "gpu_launches": gpu_launches,
             "e2e": e2e,

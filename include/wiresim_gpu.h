@@ -108,7 +108,7 @@ typedef struct ws_timing {
     float bin_ms;        /* depo -> wire-band binning */
     float convolve_ms;   /* fused accumulate + FFT convolution */
     float total_ms;      /* device time of the whole call */
-    int32_t reserved;
+    int32_t direct_planes; /* planes convolved by the time-domain kernel (the rest: row FFT) */
     int64_t clipped_patches; /* TimingReport::clipped_patch_count */
     int64_t clipped_charge;  /* SimResult::clipped_charge */
 } ws_timing;

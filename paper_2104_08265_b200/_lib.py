@@ -58,11 +58,11 @@ class SimOptionsC(C.Structure):
 
 class TimingC(C.Structure):
     _fields_ = [("prepare_ms", C.c_float), ("fluctuate_ms", C.c_float), ("bin_ms", C.c_float),
-                ("convolve_ms", C.c_float), ("total_ms", C.c_float), ("reserved", C.c_int32),
+                ("convolve_ms", C.c_float), ("total_ms", C.c_float), ("direct_planes", C.c_int32),
                 ("clipped_patches", C.c_int64), ("clipped_charge", C.c_int64)]
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+        return {k: getattr(self, k) for k, _ in self._fields_}
 
 
 class PlaneInfoC(C.Structure):

@@ -103,6 +103,7 @@ struct PendingCall {
     ws_timing* timing;
     int slot;
     int n_planes;
+    int direct_planes;
     cudaEvent_t ev[6];
     int fluctuate;
 };
@@ -451,6 +452,7 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
     PendingCall pc{};
     pc.timing = timing;
     pc.n_planes = (int)n;
+    for (uint32_t i = 0; i < n; ++i) pc.direct_planes += ev.p[i].direct;
     pc.fluctuate = ev.fluctuate;
     for (int k = 0; k < 6; ++k) pc.ev[k] = take_event(c);
 
@@ -560,6 +562,7 @@ int finish_pending(ws_ctx* c)
             t.total_ms = ms;
             t.clipped_charge = 0;
             t.clipped_patches = 0;
+            t.direct_planes = pc.direct_planes;
             for (int i = 0; i < pc.n_planes; ++i) {
                 t.clipped_charge += h.stats[2 * i];
                 t.clipped_patches += h.stats[2 * i + 1];

@@ -51,7 +51,7 @@ def full(tag, rep, kernel):
             "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "smsp__pcsamp_warps_issue_stalled_long_scoreboard",
             "smsp__pcsamp_warps_issue_stalled_barrier", "smsp__pcsamp_warps_issue_stalled_short_scoreboard",
             "launch__grid_size", "launch__block_size", "launch__shared_mem_per_block_dynamic",
-            "sm__cycles_elapsed.avg"]
+            "sm__cycles_elapsed.avg", "smsp__issue_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread"]
     out = [f"# {tag}: ncu --set full capture of `{kernel}`", "", f"source: `{Path(rep).name}`", "",
            "| metric | value | unit |", "|---|---|---|"]
     traffic = None
@@ -75,13 +75,16 @@ def full(tag, rep, kernel):
 
 
 if __name__ == "__main__":
-    tag, lcsv, rep = sys.argv[1:4]
-    kernel = sys.argv[4] if len(sys.argv) > 4 else "k_conv"
+    # python tools/summarize_profiles.py <tag> <launches.csv> <rep>:<kernel>[,<kernel>...] [...]
+    tag, lcsv = sys.argv[1:3]
     PROF.mkdir(exist_ok=True)
     tot, cnt = launches(tag, lcsv)
-    traffic = full(tag, rep, kernel)
-    (PROF / f"traffic_{kernel}.json").write_text(json.dumps(
-        {"kernel": kernel, "dram_bytes_per_launch": traffic, "source": f"{tag} ncu --set full",
-         "note": "one launch = one MicroBooNE event (3 planes)"}, indent=1) + "\n")
     print((PROF / f"{tag}_launches.md").read_text())
-    print((PROF / f"{tag}_{kernel}_ncu.md").read_text())
+    for spec in sys.argv[3:]:
+        rep, kernels = spec.split(":")
+        for kernel in kernels.split(","):
+            traffic = full(tag, rep, kernel)
+            (PROF / f"traffic_{kernel}.json").write_text(json.dumps(
+                {"kernel": kernel, "dram_bytes_per_launch": traffic, "source": f"{tag} ncu --set full",
+                 "note": "one launch = one MicroBooNE event (3 planes)"}, indent=1) + "\n")
+            print((PROF / f"{tag}_{kernel}_ncu.md").read_text())
