@@ -32,8 +32,8 @@ constexpr int kQ = 5;                          // profile taps per lane in regis
 constexpr int kSlot = 32 * kQ;                 // ring slot (floats)
 constexpr int kMargin = kSlot;                 // discard margins either side of every row
 constexpr int kRowStride = kMargin + kTileTicks + kMargin;  // ints per tile row
-constexpr int kRing = 3;                       // profile fetches in flight per warp
-constexpr int kDirectThreads = 512;
+constexpr int kRing = 2;                       // profile fetches in flight per warp
+constexpr int kDirectThreads = 1024;
 
 // x -> round-to-nearest int for |x| < 2^22 in one FFMA: the magic 1.5 * 2^23
 // pins the exponent, so the mantissa bits hold the rounded value.
