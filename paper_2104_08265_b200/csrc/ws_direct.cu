@@ -54,45 +54,24 @@ __device__ __forceinline__ void red_shared_off(uint32_t saddr, int v)
     asm volatile("red.shared.add.s32 [%0+%2], %1;" ::"r"(saddr), "r"(v), "n"(OFF) : "memory");
 }
 
-// One tile row r of one profile (gv: taps lane + 32 q, q < NQ; a0: the
-// lane's byte address of tap 0 in row 0): one FFMA rounding + one IADD + one
-// RED per tap, with the row and tap offsets as instruction immediates.
-template <int r, int NQ>
-__device__ __forceinline__ void scatter_row(float cs, uint32_t a0, const float* gv)
-{
-    constexpr int off = r * 4 * kRowStride;
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-        if constexpr (NQ > 0) {
-            switch (q) {  // compile-time after unrolling: immediates need constants
-                case 0: red_shared_off<off + 0>(a0, fix_rn(cs, gv[0])); break;
-                case 1: red_shared_off<off + 128>(a0, fix_rn(cs, gv[1])); break;
-                case 2: red_shared_off<off + 256>(a0, fix_rn(cs, gv[2])); break;
-                case 3: red_shared_off<off + 384>(a0, fix_rn(cs, gv[3])); break;
-                default: red_shared_off<off + 512>(a0, fix_rn(cs, gv[4])); break;
-            }
-        }
-    }
-}
-
-// Rows [rlo, rhi) of the tile: a jump into an unrolled run of rows (one
-// compare per row), so rows outside the depo's footprint cost nothing.
+// Rows [rlo, rhi) of one profile (gv: taps lane + 32 q, q < NQ; a0: the
+// lane's byte address of tap 0 in row 0): per row one LDS of the
+// coefficient, one address add, then per tap one FFMA rounding + one IADD +
+// one RED with the tap offset as an instruction immediate.
 template <int NQ>
 __device__ __forceinline__ void scatter_rows(const float* __restrict__ c, int rlo, int rhi, uint32_t a0,
                                              const float* gv)
 {
-    static_assert(kTileRows == 16, "unrolled for 16 rows");
-#define WSB_ROW(R_)                                                \
-    case R_:                                                       \
-        if (R_ >= rhi) break;                                      \
-        scatter_row<R_, NQ>(c[R_], a0, gv);                        \
-        [[fallthrough]];
-    switch (rlo) {
-        WSB_ROW(0) WSB_ROW(1) WSB_ROW(2) WSB_ROW(3) WSB_ROW(4) WSB_ROW(5) WSB_ROW(6) WSB_ROW(7)
-        WSB_ROW(8) WSB_ROW(9) WSB_ROW(10) WSB_ROW(11) WSB_ROW(12) WSB_ROW(13) WSB_ROW(14) WSB_ROW(15)
-        default: break;
+    uint32_t ar = a0 + (uint32_t)rlo * (4u * kRowStride);
+#pragma unroll 1
+    for (int r = rlo; r < rhi; ++r, ar += 4u * kRowStride) {
+        const float cs = c[r];
+        red_shared_off<0>(ar, fix_rn(cs, gv[0]));
+        if constexpr (NQ > 1) red_shared_off<128>(ar, fix_rn(cs, gv[1]));
+        if constexpr (NQ > 2) red_shared_off<256>(ar, fix_rn(cs, gv[2]));
+        if constexpr (NQ > 3) red_shared_off<384>(ar, fix_rn(cs, gv[3]));
+        if constexpr (NQ > 4) red_shared_off<512>(ar, fix_rn(cs, gv[4]));
     }
-#undef WSB_ROW
 }
 
 __device__ __forceinline__ void cp_async16(uint32_t saddr, const void* gptr)
@@ -315,10 +294,12 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
 
     // frame rows of the window (convolve's real part, spectral.cpp:172-173),
     // streaming stores; one flattened (row, 16-byte word) loop
-    if ((N & 3) == 0 && wlen == kTileTicks) {
+    if ((N & 3) == 0) {  // ws is a multiple of 4 as well: whole 16-byte words
         constexpr int kW = kTileTicks / 4;
+        const int wlen4 = wlen >> 2;
         for (int i = tid; i < nr * kW; i += NT) {
-            const int r = i / kW, c4 = i - r * kW;
+            const int r = i / kW, c4 = i - r * kW;  // kW a power of two: shifts
+            if (c4 >= wlen4) continue;
             int4 v;
             asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
                          : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
@@ -328,10 +309,9 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
                    make_float4((float)v.x * inv, (float)v.y * inv, (float)v.z * inv, (float)v.w * inv));
         }
     } else {
-        for (int i = tid; i < nr * wlen; i += NT) {
-            const int r = i / wlen, t = i - r * wlen;
-            __stcs(P.frame + (size_t)(r0 + r) * N + ws + t, (float)acc[r * kRowStride + kMargin + t] * s_inv[r]);
-        }
+        for (int r = 0; r < nr; ++r)
+            for (int t = tid; t < wlen; t += NT)
+                __stcs(P.frame + (size_t)(r0 + r) * N + ws + t, (float)acc[r * kRowStride + kMargin + t] * s_inv[r]);
     }
 }
 
