@@ -146,8 +146,9 @@ __device__ __forceinline__ bool row_coef(const PlaneDesc& P, int w, bool raw, co
     if (j >= P.W) j %= P.W;  // grids narrower than the stencil
     if (j >= n_rows) return false;
     const float* prof = reinterpret_cast<const float*>(pool + r.pool) + (stencil ? r.n_w : 0);
-    float s = 0.0f;
-    for (; j < n_rows; j += P.W) s += __ldg(&prof[j]);
+    float s = __ldg(&prof[j]);  // one load in the common case: rows' loads can all be in flight
+    if (n_rows > P.W)
+        for (j += P.W; j < n_rows; j += P.W) s += __ldg(&prof[j]);
     c = s * r.a;
     return true;
 }

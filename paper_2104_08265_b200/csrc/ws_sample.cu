@@ -259,6 +259,13 @@ __global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ rec
     int ts = rec.t0 + P.lo_lag;
     if (ts < 0) ts += P.N;
     const uint32_t goff = unit_g_off(P, rec);
+    // the unit's (stencilled) wire rows; units whose rows do not wrap around
+    // the padded grid read their profile with branch-free predicated loads
+    const bool stencil = !P.ww_is_one;
+    const int lo_row = stencil ? rec.w0 - P.h : rec.w0;
+    const int n_rows = stencil ? rec.n_w + 2 * P.h : rec.n_w;
+    const bool simple = lo_row >= 0 && lo_row + n_rows <= P.W;
+    const float* prof = reinterpret_cast<const float*>(pool + rec.pool) + (stencil ? rec.n_w : 0);
     for_each_bin(P, rec.w0, rec.n_w, rec.t0, rec.n_t, [&](int c) {
         const uint32_t b = P.band_base + c;
         const int r0 = (c / P.n_windows) * kTileRows, nr = min(kTileRows, P.W - r0);
@@ -267,14 +274,30 @@ __global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ rec
         d.goff = goff;
         d.gbound = __fmul_ru(rec.tsum, P.kern_absmax);
         int rlo = kTileRows, rhi = 0;
+        if (simple) {
 #pragma unroll
-        for (int r = 0; r < kTileRows; ++r) {
-            float cr = 0.0f;
-            if (r < nr && row_coef(P, r0 + r, false, rec, pool, cr) && cr != 0.0f) {
-                rlo = min(rlo, r);
-                rhi = r + 1;
+            for (int r = 0; r < kTileRows; ++r) {
+                const int j = r0 + r - lo_row;
+                const bool in = r < nr && j >= 0 && j < n_rows;
+                const float v = in ? __ldg(&prof[in ? j : 0]) : 0.0f;
+                d.c[r] = v * rec.a;  // row_coef's product
             }
-            d.c[r] = cr;
+#pragma unroll
+            for (int r = 0; r < kTileRows; ++r)
+                if (d.c[r] != 0.0f) {
+                    rlo = min(rlo, r);
+                    rhi = r + 1;
+                }
+        } else {
+#pragma unroll
+            for (int r = 0; r < kTileRows; ++r) {
+                float cr = 0.0f;
+                if (r < nr && row_coef(P, r0 + r, false, rec, pool, cr) && cr != 0.0f) {
+                    rlo = min(rlo, r);
+                    rhi = r + 1;
+                }
+                d.c[r] = cr;
+            }
         }
         d.rows = (uint32_t)rlo | ((uint32_t)max(rhi, rlo) << 8);
         tlist[off[b] + atomicAdd(&fill[b], 1u)] = d;
