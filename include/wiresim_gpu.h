@@ -20,7 +20,7 @@
  *                          pre-noise frame                               include/wiresim/pipeline.hpp:104
  *                          (pipeline.cpp:345-419)
  *   ws_simulate_event      N independent planes (one plane per run)
- *   ws_noise_digitize      add_noise + digitize                          include/wiresim/spectral.hpp:61-65
+ *   ws_noise_digitize_device add_noise (white) + digitize              include/wiresim/spectral.hpp:61-65
  *
  * Data layout (identical to the reference's):
  *   ws_depo     == wiresim::Depo       (core.hpp:63-70), 48 B AoS
@@ -101,6 +101,18 @@ typedef struct ws_sim_options {
     uint64_t seed;       /* SimConfig::rng.seed */
     ws_drift drift;      /* SimConfig::drift */
 } ws_sim_options;
+
+/* NoiseModel (spectral.hpp:51-55), white mode: per-wire normals of sigma
+ * (output units); rng_mode WS_RNG_SUBSTREAM is the reference's own per-wire
+ * stream substream(seed ^ salt, wire) (sequential per wire), WS_RNG_PHILOX the
+ * counter-based stream keyed by (seed ^ salt, wire) (parallel per tick pair). */
+enum { WS_NOISE_OFF = 0, WS_NOISE_WHITE = 1 };
+typedef struct ws_noise_model {
+    int32_t mode;
+    int32_t rng_mode;
+    double sigma;
+    uint64_t seed;
+} ws_noise_model;
 
 typedef struct ws_timing {
     float prepare_ms;    /* sample: footprints + erf integrals (+ drift) */
@@ -191,6 +203,13 @@ int ws_simulate_event(ws_ctx* ctx, uint32_t n_planes, ws_plane* const* planes, c
 int ws_simulate_events(ws_ctx* ctx, uint32_t n_events, uint32_t n_planes, ws_plane* const* planes,
                        const ws_depo* const* depos, const uint64_t* n_depos, const ws_sim_options* opt,
                        float* const* frames, ws_timing* timing);
+
+/* add_noise + digitize of a plane's frame (device pointers, asynchronous):
+ * the frame gets the noise in place (float32); adc (nullable) receives
+ * clamp(round(v * scale + offset), 0, 2^bits - 1) of the noisy fp64 sample
+ * (spectral.cpp:177-196, 228-238). noise may be NULL (digitize only). */
+int ws_noise_digitize_device(ws_plane* plane, float* frame, const ws_noise_model* noise, double scale, double offset,
+                             int32_t bits, int32_t* adc);
 
 /* Pinned host memory for the host-buffer entry points (cudaMallocHost). */
 int ws_host_alloc(uint64_t bytes, void** out);

@@ -117,6 +117,7 @@ class Oracle:
                                       C.POINTER(C.c_long)]
         L.wso_convolve_direct.argtypes = [C.POINTER(Grid), C.POINTER(Response), C.c_void_p, C.c_void_p]
         L.wso_add_white_noise.argtypes = [C.POINTER(Grid), C.c_double, C.c_uint64, C.c_void_p]
+        L.wso_add_white_noise_rng.argtypes = [C.POINTER(Grid), C.c_double, C.c_uint64, C.c_int, C.c_void_p]
         L.wso_digitize.argtypes = [C.c_void_p, C.c_size_t, C.c_double, C.c_double, C.c_int, C.c_void_p]
         L.wso_philox4x32_10.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
 
@@ -210,9 +211,9 @@ class Oracle:
         self._check(self.lib.wso_convolve_direct(C.byref(g), C.byref(r), _p(s), _p(m)))
         return m
 
-    def add_white_noise(self, g, m, sigma, seed):
+    def add_white_noise(self, g, m, sigma, seed, rng_mode=0):
         out = np.ascontiguousarray(m, dtype=np.float64).copy()
-        self._check(self.lib.wso_add_white_noise(C.byref(g), sigma, seed, _p(out)))
+        self._check(self.lib.wso_add_white_noise_rng(C.byref(g), sigma, seed, rng_mode, _p(out)))
         return out
 
     def digitize(self, m, scale=1.0, offset=2048.0, bits=12):

@@ -554,14 +554,25 @@ int wso_convolve_direct(const wso_grid* g, const wso_response* r, const double* 
 
 /* add_noise white mode (spectral.cpp:188-196): per-wire substream of
  * (seed ^ kWhiteNoiseSalt, wire), row[t] += sigma * normal(). */
+int wso_add_white_noise_rng(const wso_grid* g, double sigma, uint64_t seed, int rng_mode, double* m);
+
 int wso_add_white_noise(const wso_grid* g, double sigma, uint64_t seed, double* m)
+{
+    return wso_add_white_noise_rng(g, sigma, seed, 0, m);
+}
+
+/* add_noise white mode with the per-wire stream of rng_mode: 0 the
+ * reference's substream(seed ^ salt, w) (spectral.cpp:188-195), 1 the shared
+ * Philox stream keyed by (seed ^ salt, w) (no reference equivalent: the GPU's
+ * parallel mode, restated here as its checker) */
+int wso_add_white_noise_rng(const wso_grid* g, double sigma, uint64_t seed, int rng_mode, double* m)
 {
     if (sigma < 0.0) return fail("add_noise: sigma must be >= 0");
     if (sigma == 0.0) return 0;
     const size_t W = padded_w(g), T = padded_t(g);
     for (size_t w = 0; w < W; ++w) {
         wso_src src;
-        wso_src_init(&src, 0, seed ^ 0x77686974656e6f69ULL, (uint64_t)w);
+        wso_src_init(&src, rng_mode, seed ^ 0x77686974656e6f69ULL, (uint64_t)w);
         double* row = m + w * T;
         for (size_t t = 0; t < T; ++t) row[t] += sigma * wso_src_normal(&src);
     }

@@ -87,6 +87,7 @@ int wso_response_td(const wso_grid* g, const wso_response* r, double* combined, 
                     size_t* n_lags, long* support_ticks, long* support_wires);
 int wso_convolve_direct(const wso_grid* g, const wso_response* r, const double* s, double* m);
 
+int wso_add_white_noise_rng(const wso_grid* g, double sigma, uint64_t seed, int rng_mode, double* m);
 int wso_add_white_noise(const wso_grid* g, double sigma, uint64_t seed, double* m);
 int wso_digitize(const double* m, size_t n, double scale, double offset, int bits, int32_t* adc);
 

@@ -56,6 +56,10 @@ class SimOptionsC(C.Structure):
                 ("seed", C.c_uint64), ("drift", DriftC)]
 
 
+class NoiseModelC(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("rng_mode", C.c_int32), ("sigma", C.c_double), ("seed", C.c_uint64)]
+
+
 class TimingC(C.Structure):
     _fields_ = [("prepare_ms", C.c_float), ("fluctuate_ms", C.c_float), ("bin_ms", C.c_float),
                 ("convolve_ms", C.c_float), ("total_ms", C.c_float), ("direct_planes", C.c_int32),
@@ -97,6 +101,7 @@ SIGNATURES = {
     "ws_simulate_events": (C.c_int, [_P, C.c_uint32, C.c_uint32, _P, _P, _P, C.POINTER(SimOptionsC), _P,
                                      C.POINTER(TimingC)]),
     "ws_gen_depos_uniform":(C.c_int, [C.c_uint64, C.c_uint64, C.POINTER(GridSpecC), _P, _P]),
+    "ws_noise_digitize_device": (C.c_int, [_P, _P, C.POINTER(NoiseModelC), C.c_double, C.c_double, C.c_int32, _P]),
     "ws_host_alloc": (C.c_int, [C.c_uint64, C.POINTER(_P)]),
     "ws_host_free": (C.c_int, [_P]),
 }

@@ -193,6 +193,14 @@ class Plane:
     def convolve_device(self, charge_dev, frame_dev):
         check(self.lib.ws_convolve_device(self.handle, _ptr(charge_dev), _ptr(frame_dev)))
 
+    def noise_digitize_device(self, frame_dev, sigma=0.0, seed=0, rng="substream", adc_dev=None, scale=1.0,
+                              offset=2048.0, bits=12):
+        """add_noise (white, spectral.cpp:177-196) in place on a device frame, then
+        digitize (spectral.cpp:228-238) into adc_dev (int32, nullable)."""
+        m = _lib.NoiseModelC(1 if sigma else 0, 1 if rng == "philox" else 0, float(sigma), int(seed))
+        check(self.lib.ws_noise_digitize_device(self.handle, _ptr(frame_dev), C.byref(m), scale, offset, bits,
+                                                _ptr(adc_dev)))
+
     def close(self):
         if self.handle:
             self.lib.ws_plane_destroy(self.handle)

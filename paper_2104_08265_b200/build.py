@@ -29,6 +29,7 @@ SOURCES = {
     "ws_conv.cu": [],
     "ws_direct.cu": [],
     "ws_gprof.cu": [],
+    "ws_noise.cu": ["--fmad=false"],
     "ws_api.cu": [],
     "ws_host.cu": ["--fmad=false"],
 }

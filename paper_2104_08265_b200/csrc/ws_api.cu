@@ -28,6 +28,8 @@ extern "C" cudaError_t wsb_launch_fill(const EventDesc& ev, const UnitRec* recs,
                                        UnitRec* list, wsb::TEnt* tlist, const uint32_t* pool, unsigned* err,
                                        cudaStream_t s);
 extern "C" cudaError_t wsb_launch_gprof(const EventDesc& ev, const UnitRec* recs, uint32_t* pool, cudaStream_t s);
+extern "C" cudaError_t wsb_launch_noise(float* frame, int32_t* adc, int W, int N, int noise, int rng_mode, double sigma,
+                                        uint64_t seed, double scale, double offset, double max_code, cudaStream_t s);
 extern "C" size_t wsb_direct_smem(int cap);
 extern "C" int wsb_direct_cap();
 extern "C" cudaError_t wsb_launch_direct(const EventDesc& ev, const uint32_t* pool, const uint32_t* band_off,
@@ -1081,6 +1083,28 @@ int ws_simulate_events(ws_ctx* ctx, uint32_t n_events, uint32_t n_planes, ws_pla
         return WS_OK;
     }
     return rc;
+}
+
+int ws_noise_digitize_device(ws_plane* p, float* frame, const ws_noise_model* noise, double scale, double offset,
+                             int32_t bits, int32_t* adc)
+{
+    if (!p || !frame) return set_err(WS_EINVAL, "null argument");
+    const int white = noise && noise->mode == WS_NOISE_WHITE;
+    if (noise && noise->mode != WS_NOISE_OFF && !white)
+        return set_err(WS_EINVAL, "add_noise: only the white noise mode is implemented on the GPU");
+    if (noise && noise->sigma < 0.0) return set_err(WS_EINVAL, "add_noise: sigma must be >= 0");
+    if (noise && noise->rng_mode != WS_RNG_SUBSTREAM && noise->rng_mode != WS_RNG_PHILOX)
+        return set_err(WS_EINVAL, "add_noise: unknown rng mode %d", noise->rng_mode);
+    if (adc && (bits < 1 || bits > 16)) return set_err(WS_EINVAL, "digitize: bits must be in [1,16]");
+    const int do_noise = white && noise->sigma != 0.0;  // sigma 0: the reference returns the input
+    if (!do_noise && !adc) return WS_OK;
+    ws_ctx* c = p->ctx;
+    WS_CUDA(cudaSetDevice(c->device));
+    WS_CUDA(wsb_launch_noise(frame, adc, p->W, p->N, do_noise, do_noise ? noise->rng_mode : WS_RNG_PHILOX,
+                             do_noise ? noise->sigma : 0.0, do_noise ? noise->seed : 0, scale, offset,
+                             (double)((1 << (adc ? bits : 1)) - 1), c->stream));
+    c->launches += 1;
+    return WS_OK;
 }
 
 int ws_simulate_plane(ws_plane* p, const ws_depo* depos, uint64_t n, const ws_sim_options* opt, float* frame,
