@@ -192,7 +192,7 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
         __syncthreads();
         if (tid == 0) s_ovf = 0;
     }
-    // per-row scale 2^sh: every single term below 2^21 (one-FFMA rounding,
+    // per-row scale 2^sh: every single term below 2^22 (one-FFMA rounding,
     // fix_rn) and the largest segment bound below 2^29, so partial sums
     // (bound + rounding of <= 2^28 terms) stay inside int32
     if (warp < R) {
@@ -203,7 +203,7 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
             const int bits = 32 - __clz(mx) + ue;  // bound < 2^bits
             int sh = 29 - bits;
             const float tm = __uint_as_float(s_tmax[warp]);
-            if (tm > 0.0f) sh = min(sh, 20 - ilogbf(tm));  // tm < 2^(e+1): tm 2^sh < 2^21
+            if (tm > 0.0f) sh = min(sh, 21 - ilogbf(tm));  // tm < 2^(e+1): tm 2^sh < 2^22 (fix_rn range)
             s_scale[warp] = ldexpf(1.0f, sh);
             s_inv[warp] = ldexpf(1.0f, -sh);
         }
