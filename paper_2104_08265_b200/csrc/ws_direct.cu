@@ -35,12 +35,21 @@ constexpr int kRowStride = kMargin + kTileTicks + kMargin;  // ints per tile row
 constexpr int kRing = 2;                       // profile fetches in flight per warp
 constexpr int kDirectThreads = 1024;
 
-// x -> round-to-nearest int for |x| < 2^22 in one FFMA: the magic 1.5 * 2^23
-// pins the exponent, so the mantissa bits hold the rounded value.
+// Fixed-point term round(c g). WS_DIRECT_MAGIC: one FFMA with the magic
+// 1.5 * 2^23 (the mantissa bits hold the rounded value; needs |c g| < 2^22)
+// + one IADD; default: FMUL + F2I.RNI (any |c g| < 2^31, so the scale is set
+// by the segment sums alone: ~16x finer quanta, on the quarter-rate
+// conversion pipe, which runs beside the ALU and shared-memory pipes).
+#ifdef WS_DIRECT_MAGIC
+constexpr bool kTermBudget = true;
 __device__ __forceinline__ int fix_rn(float c, float g)
 {
     return __float_as_int(__fmaf_rn(c, g, 12582912.0f)) - 0x4B400000;
 }
+#else
+constexpr bool kTermBudget = false;
+__device__ __forceinline__ int fix_rn(float c, float g) { return __float2int_rn(c * g); }
+#endif
 
 __device__ __forceinline__ void red_shared(uint32_t saddr, int v)
 {
@@ -192,8 +201,8 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
         __syncthreads();
         if (tid == 0) s_ovf = 0;
     }
-    // per-row scale 2^sh: every single term below 2^22 (one-FFMA rounding,
-    // fix_rn) and the largest segment bound below 2^29, so partial sums
+    // per-row scale 2^sh: the largest segment bound below 2^29 (and, with the
+    // one-FFMA rounding, every single term below 2^22), so partial sums
     // (bound + rounding of <= 2^28 terms) stay inside int32
     if (warp < R) {
         unsigned mx = segb[warp * kSegs + lane];
@@ -203,7 +212,7 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
             const int bits = 32 - __clz(mx) + ue;  // bound < 2^bits
             int sh = 29 - bits;
             const float tm = __uint_as_float(s_tmax[warp]);
-            if (tm > 0.0f) sh = min(sh, 21 - ilogbf(tm));  // tm < 2^(e+1): tm 2^sh < 2^22 (fix_rn range)
+            if (kTermBudget && tm > 0.0f) sh = min(sh, 21 - ilogbf(tm));  // tm < 2^(e+1): tm 2^sh < 2^22 (fix_rn range)
             s_scale[warp] = ldexpf(1.0f, sh);
             s_inv[warp] = ldexpf(1.0f, -sh);
         }
