@@ -148,3 +148,19 @@ def test_direct_band_beyond_staging(pctx, oracle):
     s_ref, _ = oracle.charge_fluct_off(oracle_grid(grid), d)
     m_ref = oracle.convolve(oracle_grid(grid), oracle_response(resp), s_ref)
     assert relL2_per_channel(m, m_ref) < TOL_FRAME
+
+
+def test_dense_event_routes_to_row_fft(pctx):
+    """configs[4]-style dense event (1M depos on the MicroBooNE U plane): AUTO
+    picks the row FFT (its cost is per cell, the time-domain cost per depo),
+    and the two kernels agree within the tolerance."""
+    grids, resps = microboone_grids()
+    d = microboone_event(1_000_000, seed=3)[0]
+    plane = Plane(pctx, grids[0], resps[0])
+    res = plane.simulate(d, SimConfig(fluctuate=False))
+    assert res.timing["direct_planes"] == 0  # AUTO -> row FFT
+    m_dir = _frame(pctx, "direct", grids[0], resps[0], d)
+    assert relL2_per_channel(m_dir, res.frame) < TOL_FRAME
+    # and the 100k-depo event stays on the time-domain kernel
+    res2 = plane.simulate(microboone_event(100_000, seed=1)[0], SimConfig(fluctuate=False))
+    assert res2.timing["direct_planes"] == 1
