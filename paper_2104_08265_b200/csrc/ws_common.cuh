@@ -21,7 +21,7 @@ constexpr int kConvThreads = 256;
 constexpr int kTwiddleTable = 512;   // [W_M^j | W_M^{64i} | W_Np^j | W_Np^{64i}], 64 + 192 + 64 + 192
 constexpr int kMaxFftHalf = 12288;   // M = N'/2 <= 12288 (N' <= 24576 ticks)
 constexpr int kKernPad = 192;        // zero taps either side of PlaneDesc::kern (k_gprof window)
-constexpr int kTileRows = 16;        // direct path tile: kTileRows wire rows x kTileTicks ticks
+constexpr int kTileRows = 8;        // direct path tile: kTileRows wire rows x kTileTicks ticks
 constexpr int kTileTicks = 2048;
 constexpr int kSegShiftD = 6;        // direct path fixed-point bounds per 64-tick segment
 constexpr int kSegs = kTileTicks >> kSegShiftD;

@@ -33,7 +33,7 @@ constexpr int kSlot = 32 * kQ;                 // ring slot (floats)
 constexpr int kMargin = kSlot;                 // discard margins either side of every row
 constexpr int kRowStride = kMargin + kTileTicks + kMargin;  // ints per tile row
 constexpr int kRing = 2;                       // profile fetches in flight per warp
-constexpr int kDirectThreads = 1024;
+constexpr int kDirectThreads = 512;  // two CTAs per SM
 
 // Fixed-point term round(c g). WS_DIRECT_MAGIC: one FFMA with the magic
 // 1.5 * 2^23 (the mantissa bits hold the rounded value; needs |c g| < 2^22)
@@ -95,14 +95,15 @@ __device__ __forceinline__ void cp_wait()
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(NT, 2)
 k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* __restrict__ band_off,
          const TEnt* __restrict__ tlist)
 {
     constexpr int R = kTileRows;
     constexpr int NW = NT / 32;
     constexpr int D = kRing;
-    static_assert(NW >= R && kSegs == 32 && R == 16, "one warp per row computes the scales");
+    static_assert(NW >= R && kSegs == 32 && (R & (R - 1)) == 0, "one warp per row computes the scales");
+    constexpr int kRShift = R == 16 ? 4 : R == 8 ? 3 : R == 4 ? 2 : 1;
     const uint32_t gb = blockIdx.x;
     const PlaneDesc& P = ev.p[band_plane(ev, gb)];
     if (!P.direct || __ldg(&band_off[ev.total_bands]) > ev.list_cap) return;
@@ -165,7 +166,7 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
             if (n > cap || (c0 == 0 && ue == 0)) stage(c0, cnt);
 #pragma unroll 1
             for (int i = tid; i < cnt * R; i += NT) {
-                const TEnt& d = ent[i >> 4];
+                const TEnt& d = ent[i >> kRShift];
                 const int r = i & (R - 1);
                 const float t = __fmul_ru(fabsf(d.c[r]), d.gbound);  // >= every |a eff g| of the row
                 if (!(t > 0.0f)) continue;
@@ -268,7 +269,7 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
         const int cnt = min(cap, n - c0);
         if (n > cap) stage(c0, cnt);
         // coefficients -> fixed-point units of their row
-        for (int i = tid; i < cnt * R; i += NT) ent[i >> 4].c[i & (R - 1)] *= s_scale[i & (R - 1)];
+        for (int i = tid; i < cnt * R; i += NT) ent[i >> kRShift].c[i & (R - 1)] *= s_scale[i & (R - 1)];
         __syncthreads();
         // profile fetch of local entry e into ring slot s (one commit group)
         auto fetch = [&](int e, int s) {
@@ -336,7 +337,7 @@ extern "C" size_t wsb_direct_smem(int cap)
 
 extern "C" int wsb_direct_cap()
 {
-    const size_t limit = 225 * 1024;
+    const size_t limit = 112 * 1024;  // two CTAs per SM (228 KB, 1 KB reserved per CTA, static smem)
     return (int)((limit - wsb_direct_smem(0)) / sizeof(wsb::TEnt));
 }
 
@@ -350,6 +351,8 @@ extern "C" cudaError_t wsb_launch_direct(const wsb::EventDesc& ev, const uint32_
     if (e != cudaSuccess) return e;
     if (!(ready & (1ull << dev))) {
         e = cudaFuncSetAttribute(wsb::k_direct<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(wsb::k_direct<NT>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e != cudaSuccess) return e;
         ready |= 1ull << dev;
     }
