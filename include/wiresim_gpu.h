@@ -117,7 +117,7 @@ typedef struct ws_noise_model {
 typedef struct ws_timing {
     float prepare_ms;    /* sample: footprints + erf integrals (+ drift) */
     float fluctuate_ms;  /* fluctuation walk + integer scatter (0 when off) */
-    float bin_ms;        /* depo -> wire-band binning */
+    float bin_ms;        /* depo -> band / tile binning (+ the response profiles on a second stream) */
     float convolve_ms;   /* fused accumulate + FFT convolution */
     float total_ms;      /* device time of the whole call */
     int32_t direct_planes; /* planes convolved by the time-domain kernel (the rest: row FFT) */

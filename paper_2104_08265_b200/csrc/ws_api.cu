@@ -481,7 +481,11 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
             // response profiles on the auxiliary stream, concurrent with the
             // binning (k_direct is the first consumer)
             if (!c->aux_stream) {
-                WS_CUDA(cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
+                // lowest priority: the binning's blocks (main stream) go first
+                // whenever both kernels have blocks waiting
+                int lo_prio = 0, hi_prio = 0;
+                WS_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+                WS_CUDA(cudaStreamCreateWithPriority(&c->aux_stream, cudaStreamNonBlocking, lo_prio));
                 WS_CUDA(cudaEventCreateWithFlags(&c->aux_fork, cudaEventDisableTiming));
                 WS_CUDA(cudaEventCreateWithFlags(&c->aux_join, cudaEventDisableTiming));
             }
@@ -495,6 +499,7 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
         WS_CUDA(wsb_launch_fill(ev, c->recs.p, c->band_off.p, c->band_fill.p, c->band_list.p, c->tile_list.p,
                                 c->pool.p, &hdr->err, s));
         c->launches += 1 + (units ? 1 : 0);
+        if (any_direct) WS_CUDA(cudaStreamWaitEvent(s, c->aux_join, 0));  // profiles ready (bin stage ends)
     }
     WS_CUDA(cudaEventRecord(pc.ev[3], s));
     if (ev.mode == 0 && charges) {
@@ -506,7 +511,6 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
     if (want_frame) {
         // each kernel skips the other's planes
         if (any_direct) {
-            WS_CUDA(cudaStreamWaitEvent(s, c->aux_join, 0));
             WS_CUDA(wsb_launch_direct(ev, c->pool.p, c->band_off.p, c->tile_list.p, wsb_direct_smem(wsb_direct_cap()),
                                       s));
             c->launches += bands ? 1 : 0;
@@ -613,7 +617,11 @@ int ws_ctx_create(int device, void* stream, ws_ctx** out)
     if (stream) {
         c->stream = (cudaStream_t)stream;
     } else {
-        cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+        // highest priority: within a call, its blocks win over the auxiliary
+        // stream's (k_gprof) whenever both have blocks waiting
+        int lo_prio = 0, hi_prio = 0;
+        cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+        cudaError_t e = cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, hi_prio);
         if (e != cudaSuccess) {
             delete c;
             return set_err(WS_ECUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
