@@ -102,16 +102,21 @@ typedef struct ws_sim_options {
     ws_drift drift;      /* SimConfig::drift */
 } ws_sim_options;
 
-/* NoiseModel (spectral.hpp:51-55), white mode: per-wire normals of sigma
- * (output units); rng_mode WS_RNG_SUBSTREAM is the reference's own per-wire
- * stream substream(seed ^ salt, wire) (sequential per wire), WS_RNG_PHILOX the
- * counter-based stream keyed by (seed ^ salt, wire) (parallel per tick pair). */
-enum { WS_NOISE_OFF = 0, WS_NOISE_WHITE = 1 };
+/* NoiseModel (spectral.hpp:51-55). White: per-wire normals of sigma (output
+ * units). Spectrum: per wire, IFFT of amplitude_spectrum[k] with uniform
+ * random phases, Hermitian-completed (host array of padded-ticks doubles;
+ * needs an even 7-smooth padded tick count). rng_mode WS_RNG_SUBSTREAM is the
+ * reference's own per-wire stream substream(seed ^ salt, wire) (sequential
+ * per wire), WS_RNG_PHILOX the counter-based stream keyed by (seed ^ salt,
+ * wire) (parallel). */
+enum { WS_NOISE_OFF = 0, WS_NOISE_WHITE = 1, WS_NOISE_SPECTRUM = 2 };
 typedef struct ws_noise_model {
     int32_t mode;
     int32_t rng_mode;
     double sigma;
     uint64_t seed;
+    const double* amplitude_spectrum; /* spectrum mode: host pointer, n_amplitude == padded ticks */
+    uint64_t n_amplitude;
 } ws_noise_model;
 
 typedef struct ws_timing {

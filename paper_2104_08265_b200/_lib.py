@@ -57,7 +57,8 @@ class SimOptionsC(C.Structure):
 
 
 class NoiseModelC(C.Structure):
-    _fields_ = [("mode", C.c_int32), ("rng_mode", C.c_int32), ("sigma", C.c_double), ("seed", C.c_uint64)]
+    _fields_ = [("mode", C.c_int32), ("rng_mode", C.c_int32), ("sigma", C.c_double), ("seed", C.c_uint64),
+                ("amplitude_spectrum", C.c_void_p), ("n_amplitude", C.c_uint64)]
 
 
 class TimingC(C.Structure):

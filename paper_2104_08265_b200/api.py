@@ -194,10 +194,16 @@ class Plane:
         check(self.lib.ws_convolve_device(self.handle, _ptr(charge_dev), _ptr(frame_dev)))
 
     def noise_digitize_device(self, frame_dev, sigma=0.0, seed=0, rng="substream", adc_dev=None, scale=1.0,
-                              offset=2048.0, bits=12):
-        """add_noise (white, spectral.cpp:177-196) in place on a device frame, then
+                              offset=2048.0, bits=12, spectrum=None):
+        """add_noise (white with sigma, or spectrum mode with an amplitude
+        spectrum; spectral.cpp:177-226) in place on a device frame, then
         digitize (spectral.cpp:228-238) into adc_dev (int32, nullable)."""
-        m = _lib.NoiseModelC(1 if sigma else 0, 1 if rng == "philox" else 0, float(sigma), int(seed))
+        amp = None
+        if spectrum is not None:
+            amp = np.ascontiguousarray(spectrum, dtype=np.float64)
+            m = _lib.NoiseModelC(2, 1 if rng == "philox" else 0, 0.0, int(seed), amp.ctypes.data, amp.size)
+        else:
+            m = _lib.NoiseModelC(1 if sigma else 0, 1 if rng == "philox" else 0, float(sigma), int(seed), None, 0)
         check(self.lib.ws_noise_digitize_device(self.handle, _ptr(frame_dev), C.byref(m), scale, offset, bits,
                                                 _ptr(adc_dev)))
 

@@ -30,6 +30,9 @@ extern "C" cudaError_t wsb_launch_fill(const EventDesc& ev, const UnitRec* recs,
 extern "C" cudaError_t wsb_launch_gprof(const EventDesc& ev, const UnitRec* recs, uint32_t* pool, cudaStream_t s);
 extern "C" cudaError_t wsb_launch_noise(float* frame, int32_t* adc, int W, int N, int noise, int rng_mode, double sigma,
                                         uint64_t seed, double scale, double offset, double max_code, cudaStream_t s);
+extern "C" cudaError_t wsb_launch_noise_spectrum(const wsb::PlaneDesc& P, const double* amp, uint64_t seed, int rng_mode,
+                                                 float* frame, int32_t* adc, double scale, double offset,
+                                                 double max_code, int variant, cudaStream_t stream);
 extern "C" size_t wsb_direct_smem(int cap);
 extern "C" int wsb_direct_cap();
 extern "C" cudaError_t wsb_launch_direct(const EventDesc& ev, const uint32_t* pool, const uint32_t* band_off,
@@ -125,6 +128,7 @@ struct ws_ctx {
     DevBuf<ScratchHeader> header;
     DevBuf<ws_depo> depos;
     DevBuf<float> frames, charges;
+    DevBuf<double> noise_amp;  // spectrum-mode amplitudes of the last ws_noise_digitize_device
     ScratchHeader* host_slots = nullptr;  // pinned, kStatSlots
     int next_slot = 0;
     std::vector<PendingCall> pending;
@@ -654,6 +658,7 @@ int ws_ctx_destroy(ws_ctx* c)
     c->depos.release();
     c->frames.release();
     c->charges.release();
+    c->noise_amp.release();
     for (PendingCall& pc : c->pending)
         for (cudaEvent_t e : pc.ev) cudaEventDestroy(e);
     for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
@@ -1098,8 +1103,31 @@ int ws_noise_digitize_device(ws_plane* p, float* frame, const ws_noise_model* no
 {
     if (!p || !frame) return set_err(WS_EINVAL, "null argument");
     const int white = noise && noise->mode == WS_NOISE_WHITE;
-    if (noise && noise->mode != WS_NOISE_OFF && !white)
-        return set_err(WS_EINVAL, "add_noise: only the white noise mode is implemented on the GPU");
+    const int spectrum = noise && noise->mode == WS_NOISE_SPECTRUM;
+    if (noise && noise->mode != WS_NOISE_OFF && !white && !spectrum)
+        return set_err(WS_EINVAL, "add_noise: unknown noise mode %d", noise->mode);
+    if (spectrum) {
+        if (noise->rng_mode != WS_RNG_SUBSTREAM && noise->rng_mode != WS_RNG_PHILOX)
+            return set_err(WS_EINVAL, "add_noise: unknown rng mode %d", noise->rng_mode);
+        if (!noise->amplitude_spectrum || noise->n_amplitude != (uint64_t)p->N)
+            return set_err(WS_EINVAL,
+                           "add_noise: amplitude_spectrum length %llu does not match the padded tick count %d",
+                           (unsigned long long)noise->n_amplitude, p->N);
+        if (adc && (bits < 1 || bits > 16)) return set_err(WS_EINVAL, "digitize: bits must be in [1,16]");
+        if (p->folded)
+            return set_err(WS_EINVAL, "add_noise: spectrum mode needs an even 7-smooth padded tick count (got %d)",
+                           p->N);
+        ws_ctx* c = p->ctx;
+        WS_CUDA(cudaSetDevice(c->device));
+        WS_CUDA(c->noise_amp.reserve((size_t)p->N));
+        WS_CUDA(cudaMemcpyAsync(c->noise_amp.p, noise->amplitude_spectrum, sizeof(double) * p->N,
+                                cudaMemcpyHostToDevice, c->stream));
+        const PlaneDesc d = plane_desc(p);
+        WS_CUDA(wsb_launch_noise_spectrum(d, c->noise_amp.p, noise->seed, noise->rng_mode, frame, adc, scale, offset,
+                                          (double)((1 << (adc ? bits : 1)) - 1), c->conv_variant, c->stream));
+        c->launches += 1;
+        return WS_OK;
+    }
     if (noise && noise->sigma < 0.0) return set_err(WS_EINVAL, "add_noise: sigma must be >= 0");
     if (noise && noise->rng_mode != WS_RNG_SUBSTREAM && noise->rng_mode != WS_RNG_PHILOX)
         return set_err(WS_EINVAL, "add_noise: unknown rng mode %d", noise->rng_mode);

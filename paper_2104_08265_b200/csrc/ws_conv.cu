@@ -277,6 +277,95 @@ k_conv(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* __
     }
 }
 
+// Spectrum-mode electronics noise (the reference's add_noise, NoiseMode::
+// spectrum, spectral.cpp:198-225): one CTA per wire row synthesises the
+// waveform IFFT_N(X) with X[k] = amp[k] e^{2 pi i u_k} Hermitian-completed
+// (X[0], X[N/2] real: amp cos(2 pi u)), u_k the row's k-th uniform of the
+// reference's stream substream(seed ^ kSpectrumNoiseSalt, w) (drawn by one
+// thread: the stream is sequential) or of the Philox stream (one draw per
+// thread), and adds it to the frame row (optionally digitizing). The
+// half-length real inverse transform is k_conv's second half: re-tangle of
+// the half spectrum into the digit-reversed layout, DIT of the conjugate.
+// Needs an even, 7-smooth padded tick count (Np == N).
+template <int NT, int MAXR>
+__global__ void __launch_bounds__(NT)
+k_noise_spectrum(const PlaneDesc P, const double* __restrict__ amp, uint64_t seed, int rng_mode, float* frame,
+                 int32_t* adc, double scale, double offset, double max_code)
+{
+    constexpr uint64_t kSpectrumNoiseSalt = 0x737065636e6f6973ULL;  // spectral.cpp:22
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int w = blockIdx.x, tid = threadIdx.x;
+    const int N = P.N, M = P.M;
+    float2* buf = reinterpret_cast<float2*>(smem);
+    float* xs = reinterpret_cast<float*>(smem);
+    size_t off = ((size_t)8 * M + 15) & ~(size_t)15;
+    float2* s_tw = reinterpret_cast<float2*>(smem + off);
+    off += sizeof(float2) * kTwiddleTable;
+    uint16_t* s_rev = reinterpret_cast<uint16_t*>(smem + off);
+    off += ((size_t)2 * M + 15) & ~(size_t)15;
+    double* s_u = reinterpret_cast<double*>(smem + off);  // M + 1 uniforms
+    for (int i = tid; i < kTwiddleTable; i += NT) s_tw[i] = __ldg(&P.tw[i]);
+    for (int i = tid; i < M; i += NT) s_rev[i] = __ldg(&P.rev[i]);
+    const TwiddleSplit tw_m{s_tw, s_tw + 64};
+    const TwiddleSplit tw_np{s_tw + 256, s_tw + 320};
+    if (rng_mode == WS_RNG_SUBSTREAM) {
+        if (tid == 0) {
+            Rng src;
+            src.init(WS_RNG_SUBSTREAM, seed ^ kSpectrumNoiseSalt, (uint64_t)w);
+            for (int k = 0; k <= M; ++k) s_u[k] = src.uniform();
+        }
+    } else {
+        for (int k = tid; k <= M; k += NT) {
+            Rng src;
+            src.init(WS_RNG_PHILOX, seed ^ kSpectrumNoiseSalt, (uint64_t)w);
+            src.draw = (uint32_t)k;
+            s_u[k] = src.uniform();
+        }
+    }
+    __syncthreads();
+    // Y[k] = X[k] / M (k_conv's spectrum scaling: the DIT below then yields IFFT_N(X), 1/N included)
+    const double kTwoPiD = 6.283185307179586476925286766559;
+    auto Y = [&](int k) {
+        const double a = amp[k] / (double)M;
+        if (k == 0 || k == M) return make_float2((float)(a * cos(kTwoPiD * s_u[k])), 0.0f);
+        double sn, cs;
+        sincos(kTwoPiD * s_u[k], &sn, &cs);
+        return make_float2((float)(a * cs), (float)(a * sn));
+    };
+    for (int k = tid; k <= M / 2; k += NT) {
+        if (k == 0) {
+            const float2 y0 = Y(0), ym = Y(M);
+            const float2 ye = cscale(cadd(y0, ym), 0.5f);
+            const float2 yo = cscale(csub(y0, ym), 0.5f);
+            buf[s_rev[0]] = make_float2(ye.x - yo.y, -(ye.y + yo.x));  // conj(ye + i yo)
+        } else {
+            const int kk = M - k;
+            const float2 wk = tw_np(k);
+            const float2 wkk = make_float2(-wk.x, wk.y);
+            const float2 yk = Y(k), ykk = Y(kk);
+            const float2 ye1 = cscale(cadd(yk, cconj(ykk)), 0.5f);
+            const float2 yo1 = cmul(cscale(csub(yk, cconj(ykk)), 0.5f), cconj(wk));
+            const float2 ye2 = cscale(cadd(ykk, cconj(yk)), 0.5f);
+            const float2 yo2 = cmul(cscale(csub(ykk, cconj(yk)), 0.5f), cconj(wkk));
+            buf[s_rev[k]] = make_float2(ye1.x - yo1.y, -(ye1.y + yo1.x));
+            if (kk != k) buf[s_rev[kk]] = make_float2(ye2.x - yo2.y, -(ye2.y + yo2.x));
+        }
+    }
+    __syncthreads();
+    fft_dit<NT, MAXR>(buf, M, P.fft, tw_m);
+    // y[2n] = Re res[n], y[2n+1] = -Im res[n]; add to the row (fp64), digitize
+    const size_t base = (size_t)w * N;
+    for (int t = tid; t < N; t += NT) {
+        const float y = (t & 1) ? -xs[t] : xs[t];
+        const double v = __dadd_rn((double)frame[base + t], (double)y);
+        frame[base + t] = (float)v;
+        if (adc) {
+            const double c = round(__dadd_rn(__dmul_rn(v, scale), offset));
+            adc[base + t] = (int32_t)(c < 0.0 ? 0.0 : (c > max_code ? max_code : c));
+        }
+    }
+}
+
 }  // namespace wsb
 
 extern "C" size_t wsb_conv_smem(int N, int Np, int M)
@@ -288,36 +377,68 @@ extern "C" size_t wsb_conv_smem(int N, int Np, int M)
 
 // Variants: 256 threads x 3 CTAs/SM (85 registers, radices up to 25) or
 // 256 threads x 4 CTAs/SM (64 registers, radices up to 8).
-extern "C" cudaError_t wsb_launch_conv(const wsb::EventDesc& ev, const uint32_t* pool, const uint32_t* band_off,
-                                       const wsb::UnitRec* band_list, int flags, size_t smem_bytes, int variant,
-                                       cudaStream_t stream)
+// Once per device: the composite-radix twiddles in constant memory (every
+// kernel that runs the row FFT needs them) and the shared-memory opt-ins.
+static cudaError_t conv_device_setup()
 {
-    // once per device: shared-memory opt-in and the composite-radix twiddles
     static unsigned long long ready = 0;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
-    if (!(ready & (1ull << dev))) {
-        e = cudaFuncSetAttribute(wsb::k_conv<256, 25, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(wsb::k_conv<256, 8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e != cudaSuccess) return e;
-        float2 host[wsb::kCompositeTwiddles] = {};
-        for (int R : {10, 14, 16, 20, 24, 25, 28, 32, 35, 40, 49}) {
-            const int o = wsb::comp_off(R);
-            for (int m = 0; m < R; ++m) {
-                const double a = -6.283185307179586476925286766559 * (double)m / (double)R;
-                host[o + m] = make_float2((float)cos(a), (float)sin(a));
-            }
+    if (ready & (1ull << dev)) return cudaSuccess;
+    e = cudaFuncSetAttribute(wsb::k_conv<256, 25, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(wsb::k_conv<256, 8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(wsb::k_noise_spectrum<256, 25>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(wsb::k_noise_spectrum<256, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    float2 host[wsb::kCompositeTwiddles] = {};
+    for (int R : {10, 14, 16, 20, 24, 25, 28, 32, 35, 40, 49}) {
+        const int o = wsb::comp_off(R);
+        for (int m = 0; m < R; ++m) {
+            const double a = -6.283185307179586476925286766559 * (double)m / (double)R;
+            host[o + m] = make_float2((float)cos(a), (float)sin(a));
         }
-        e = cudaMemcpyToSymbol(wsb::c_wr, host, sizeof(host));
-        if (e != cudaSuccess) return e;
-        ready |= 1ull << dev;
     }
+    e = cudaMemcpyToSymbol(wsb::c_wr, host, sizeof(host));
+    if (e != cudaSuccess) return e;
+    ready |= 1ull << dev;
+    return cudaSuccess;
+}
+
+extern "C" cudaError_t wsb_launch_conv(const wsb::EventDesc& ev, const uint32_t* pool, const uint32_t* band_off,
+                                       const wsb::UnitRec* band_list, int flags, size_t smem_bytes, int variant,
+                                       cudaStream_t stream)
+{
+    cudaError_t e = conv_device_setup();
+    if (e != cudaSuccess) return e;
     if (ev.total_bands == 0) return cudaSuccess;
     if (variant == 8)
         wsb::k_conv<256, 8, 4><<<ev.total_bands, 256, smem_bytes, stream>>>(ev, pool, band_off, band_list, flags);
     else
         wsb::k_conv<256, 25, 3><<<ev.total_bands, 256, smem_bytes, stream>>>(ev, pool, band_off, band_list, flags);
+    return cudaGetLastError();
+}
+
+extern "C" size_t wsb_noise_spectrum_smem(int M)
+{
+    return (((size_t)8 * M + 15) & ~(size_t)15) + sizeof(float2) * wsb::kTwiddleTable + (((size_t)2 * M + 15) & ~(size_t)15) +
+           sizeof(double) * ((size_t)M + 1);
+}
+
+extern "C" cudaError_t wsb_launch_noise_spectrum(const wsb::PlaneDesc& P, const double* amp, uint64_t seed, int rng_mode,
+                                                 float* frame, int32_t* adc, double scale, double offset,
+                                                 double max_code, int variant, cudaStream_t stream)
+{
+    const size_t smem = wsb_noise_spectrum_smem(P.M);
+    cudaError_t e = conv_device_setup();  // composite-radix twiddles (the DIT below uses them)
+    if (e != cudaSuccess) return e;
+    if (variant == 8)
+        wsb::k_noise_spectrum<256, 8><<<P.W, 256, smem, stream>>>(P, amp, seed, rng_mode, frame, adc, scale, offset, max_code);
+    else
+        wsb::k_noise_spectrum<256, 25><<<P.W, 256, smem, stream>>>(P, amp, seed, rng_mode, frame, adc, scale, offset,
+                                                                   max_code);
     return cudaGetLastError();
 }
