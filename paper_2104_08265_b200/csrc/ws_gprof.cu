@@ -195,7 +195,8 @@ extern "C" cudaError_t wsb_launch_gprof(const wsb::EventDesc& ev, const wsb::Uni
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const unsigned groups = (max_units + 15) / 16;
-    const unsigned blocks = std::min<unsigned>((groups + wsb::kGpWarps - 1) / wsb::kGpWarps, (unsigned)sms * 8);
+    const unsigned blocks = (groups + wsb::kGpWarps - 1) / wsb::kGpWarps;  // one group per warp
+    (void)sms;
     const dim3 grid(blocks, (unsigned)ev.n_planes);
     wsb::k_gprof<<<grid, 32 * wsb::kGpWarps, smem, s>>>(ev, recs, pool);
     return cudaGetLastError();
