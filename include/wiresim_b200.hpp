@@ -17,6 +17,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstring>
 #include <stdexcept>
 #include <string>
 #include <type_traits>
@@ -191,6 +192,21 @@ SimResult run_simulation(const SimConfig& config, const std::vector<D>& depos, i
     Context ctx(device);
     Plane plane(ctx, config.grid, config.response, config.n_sigma);
     return plane.simulate(config, depos);
+}
+
+// load_depos (pipeline.cpp:226-262): the native CSV reader, same validation and
+// std::runtime_error messages. Depo must be layout-compatible with ws_depo.
+template <class D = ws_depo>
+std::vector<D> load_depos(const std::string& path)
+{
+    static_assert(sizeof(D) == sizeof(ws_depo), "Depo layout must match ws_depo");
+    ws_depo* p = nullptr;
+    std::uint64_t n = 0;
+    check(ws_load_depos_csv(path.c_str(), 0, &p, &n));
+    std::vector<D> out(n);
+    if (n) std::memcpy(static_cast<void*>(out.data()), p, n * sizeof(ws_depo));
+    ws_free_depos(p, 0);
+    return out;
 }
 
 }  // namespace wiresim_b200

@@ -226,6 +226,18 @@ int ws_host_free(void* p);
  * q_max, sigma_t_min, sigma_t_max, sigma_x_min, sigma_x_max} or NULL. */
 int ws_gen_depos_uniform(uint64_t n, uint64_t seed, const ws_grid_spec* grid, const double* ranges6, ws_depo* out);
 
+/* Depo CSV ingestion: load_depos (pipeline.cpp:226-262), same header, row
+ * format ("id,t_us,x_mm,q,sigma_t_us,sigma_x_mm", %ld,%lf,%lf,%ld,%lf,%lf) and
+ * the same validation (bad header, malformed row, id != row index, negative
+ * charge or width; blank lines skipped), each a WS_ERUNTIME with the
+ * reference's message. *out is pinned (cudaMallocHost) when pinned != 0, so it
+ * can feed ws_simulate_* directly; release it with ws_free_depos(p, pinned). */
+int ws_load_depos_csv(const char* path, int pinned, ws_depo** out, uint64_t* n);
+int ws_free_depos(ws_depo* p, int pinned);
+/* The CSV writer of gen_depos (pipeline.cpp:270-293): %.17g fields, so a
+ * save -> load round trip is exact. Ids must equal the row index. */
+int ws_save_depos_csv(const char* path, const ws_depo* depos, uint64_t n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -262,6 +262,8 @@ class Reference:
         L.wsr_fluct_philox_charge.argtypes = [G, C.c_void_p, C.c_uint64, C.c_double, C.c_uint64, C.c_int,
                                               C.c_void_p, C.POINTER(C.c_int64)]
         L.wsr_gen_depos.argtypes = [C.c_uint64, C.c_uint64, G, C.c_void_p]
+        L.wsr_gen_depos_csv.argtypes = [C.c_uint64, C.c_uint64, G, C.c_char_p]
+        L.wsr_load_depos.argtypes = [C.c_char_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
         L.wsr_draws.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p]
         L.wsr_binomials.argtypes = [C.c_int64, C.c_double, C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p]
         L.wsr_philox4x32_10.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
@@ -283,6 +285,15 @@ class Reference:
         out = np.zeros(n, dtype=DEPO_DTYPE)
         self._check(self.lib.wsr_gen_depos(n, seed, C.byref(g), _p(out)))
         return out
+
+    def gen_depos_csv(self, n, seed, g, path):
+        self._check(self.lib.wsr_gen_depos_csv(n, seed, C.byref(g), str(path).encode()))
+
+    def load_depos(self, path, cap=1 << 20):
+        out = np.zeros(cap, dtype=DEPO_DTYPE)
+        n = C.c_uint64()
+        self._check(self.lib.wsr_load_depos(str(path).encode(), _p(out), cap, C.byref(n)))
+        return out[:n.value].copy()
 
     def draws(self, mode, kind, seed, stream_id, count):
         out = np.zeros(count, dtype=np.float64)

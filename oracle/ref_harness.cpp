@@ -409,6 +409,12 @@ int wsr_gen_depos(std::uint64_t n, std::uint64_t seed, const wsr_grid* g, Depo* 
     });
 }
 
+// gen_depos (pipeline.cpp:264-294) to a CSV file, unmodified (golden input files).
+int wsr_gen_depos_csv(std::uint64_t n, std::uint64_t seed, const wsr_grid* g, const char* path)
+{
+    return guarded([&] { gen_depos(n, seed, to_spec(g), DepoGenRanges{}, path); });
+}
+
 int wsr_load_depos(const char* path, Depo* out, std::uint64_t cap, std::uint64_t* n_out)
 {
     return guarded([&] {

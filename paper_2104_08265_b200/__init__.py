@@ -15,7 +15,9 @@ from .api import (  # noqa: F401
     SimConfig,
     SimResult,
     gen_depos,
+    load_depos,
     run_simulation,
+    save_depos,
     simulate_event,
     simulate_event_device,
     simulate_events,

@@ -105,6 +105,9 @@ SIGNATURES = {
     "ws_noise_digitize_device": (C.c_int, [_P, _P, C.POINTER(NoiseModelC), C.c_double, C.c_double, C.c_int32, _P]),
     "ws_host_alloc": (C.c_int, [C.c_uint64, C.POINTER(_P)]),
     "ws_host_free": (C.c_int, [_P]),
+    "ws_load_depos_csv": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(_P), C.POINTER(C.c_uint64)]),
+    "ws_free_depos": (C.c_int, [_P, C.c_int]),
+    "ws_save_depos_csv": (C.c_int, [C.c_char_p, _P, C.c_uint64]),
 }
 
 _lib = None

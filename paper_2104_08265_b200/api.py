@@ -307,3 +307,26 @@ def gen_depos(n: int, seed: int, grid: GridSpec, ranges: Sequence[float] | None 
     r = None if ranges is None else np.ascontiguousarray(ranges, dtype=np.float64)
     check(lib.ws_gen_depos_uniform(n, seed, C.byref(g), r.ctypes.data if r is not None else None, out.ctypes.data))
     return out
+
+
+def load_depos(path) -> np.ndarray:
+    """load_depos (pipeline.cpp:226-262) through the native CSV reader: same
+    format and validation; a bad file raises WsError (WS_ERUNTIME)."""
+    lib = _lib.load()
+    ptr = C.c_void_p()
+    n = C.c_uint64()
+    check(lib.ws_load_depos_csv(str(path).encode(), 0, C.byref(ptr), C.byref(n)))
+    try:
+        out = np.empty(n.value, dtype=DEPO_DTYPE)
+        if n.value:
+            C.memmove(out.ctypes.data, ptr.value, n.value * DEPO_DTYPE.itemsize)
+        return out
+    finally:
+        lib.ws_free_depos(ptr, 0)
+
+
+def save_depos(path, depos) -> None:
+    """gen_depos's CSV writer (pipeline.cpp:270-293), %.17g fields."""
+    lib = _lib.load()
+    d = np.ascontiguousarray(depos, dtype=DEPO_DTYPE)
+    check(lib.ws_save_depos_csv(str(path).encode(), d.ctypes.data if len(d) else None, len(d)))

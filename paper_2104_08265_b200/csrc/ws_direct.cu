@@ -227,6 +227,7 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
     constexpr uint32_t row_bytes = 4u * kRowStride;
     float* my_ring = ring + (size_t)warp * D * kSlot;
     const uint32_t s_ring = (uint32_t)__cvta_generic_to_shared(my_ring);
+    const uint32_t s_lane = s_ring + 4u * (uint32_t)lane;
 
     auto scatter = [&](const TEnt& d, const float* gv) {  // d: staged, coefficients pre-scaled
         const uint32_t tsL = d.tsL, rows = d.rows;
@@ -292,7 +293,8 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
             __syncwarp();
             float gv[kQ];
 #pragma unroll
-            for (int q = 0; q < kQ; ++q) gv[q] = my_ring[s * kSlot + lane + 32 * q];  // past ceil32(L): unused
+            for (int q = 0; q < kQ; ++q)  // past ceil32(L): unused
+                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(gv[q]) : "r"(s_lane + 4u * (uint32_t)(s * kSlot + 32 * q)));
             __syncwarp();
             fetch(e + NW * D, s);
             s = s + 1 == D ? 0 : s + 1;

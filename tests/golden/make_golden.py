@@ -31,9 +31,55 @@ def edge_depos():
     return d
 
 
+CSV_CASES = {
+    "ok_blank_lines": "id,t_us,x_mm,q,sigma_t_us,sigma_x_mm\n0,1.5,2.5,100,0.5,3\n\n1,+2,  3.25,7,1e-1,0\n",
+    "no_trailing_newline": "id,t_us,x_mm,q,sigma_t_us,sigma_x_mm\n0,1,2,3,4,5",
+    "header_only": "id,t_us,x_mm,q,sigma_t_us,sigma_x_mm\n",
+    "empty": "",
+    "bad_header": "id,t,x,q,st,sx\n0,1,2,3,4,5\n",
+    "crlf": "id,t_us,x_mm,q,sigma_t_us,sigma_x_mm\r\n0,1,2,3,4,5\r\n",
+    "crlf_row": "id,t_us,x_mm,q,sigma_t_us,sigma_x_mm\n0,1,2,3,4,5\r\n",
+    "trailing_field": "id,t_us,x_mm,q,sigma_t_us,sigma_x_mm\n0,1,2,3,4,5,6\n",
+    "short_row": "id,t_us,x_mm,q,sigma_t_us,sigma_x_mm\n0,1,2,3,4\n",
+    "text_field": "id,t_us,x_mm,q,sigma_t_us,sigma_x_mm\n0,1,abc,3,4,5\n",
+    "float_charge": "id,t_us,x_mm,q,sigma_t_us,sigma_x_mm\n0,1,2,3.5,4,5\n",
+    "id_gap": "id,t_us,x_mm,q,sigma_t_us,sigma_x_mm\n0,1,2,3,4,5\n2,1,2,3,4,5\n",
+    "negative_charge": "id,t_us,x_mm,q,sigma_t_us,sigma_x_mm\n0,1,2,-3,4,5\n",
+    "negative_width": "id,t_us,x_mm,q,sigma_t_us,sigma_x_mm\n0,1,2,3,4,-5\n",
+    "zero_width": "id,t_us,x_mm,q,sigma_t_us,sigma_x_mm\n0,-1e3,-2.5e-7,0,0,0\n",
+}
+
+
+def csv_fixtures(ref):
+    """Depo CSV ingestion (load_depos, pipeline.cpp:226-262) and writer
+    (gen_depos, pipeline.cpp:264-294): a reference-written file plus the
+    reference loader's verdict on edge-case files (path replaced by <path>)."""
+    import tempfile
+    g = make_grid(48, 300, 12, 100, 5.0, 0.5)
+    ref.gen_depos_csv(64, 11, g, HERE / "depos_ref.csv")
+    cases = {}
+    with tempfile.TemporaryDirectory() as td:
+        for name, text in CSV_CASES.items():
+            path = Path(td) / f"{name}.csv"
+            path.write_bytes(text.encode())
+            try:
+                d = ref.load_depos(path)
+                cases[name] = {"text": text, "ok": True,
+                               "depos": [[int(r["id"]), float(r["t"]), float(r["x"]), int(r["q"]),
+                                          float(r["sigma_t"]), float(r["sigma_x"])] for r in d]}
+            except Exception as e:  # OracleError carries the reference's what()
+                cases[name] = {"text": text, "ok": False, "error": str(e).replace(str(path), "<path>")}
+    (HERE / "golden_csv.json").write_text(json.dumps(
+        {"gen": {"n": 64, "seed": 11, "grid": [48, 300, 12, 100, 5.0, 0.5]}, "cases": cases}, indent=1))
+    print("wrote", HERE / "depos_ref.csv", HERE / "golden_csv.json")
+
+
 def main():
     build_ref()
     ref = Reference()
+    csv_fixtures(ref)
+    if "--csv-only" in sys.argv:
+        return
     gold = {}
 
     # Philox4x32-10 KATs (Random123; SURVEY.md §8(c))
