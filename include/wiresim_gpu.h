@@ -226,6 +226,38 @@ int ws_host_free(void* p);
  * q_max, sigma_t_min, sigma_t_max, sigma_x_min, sigma_x_max} or NULL. */
 int ws_gen_depos_uniform(uint64_t n, uint64_t seed, const ws_grid_spec* grid, const double* ranges6, ws_depo* out);
 
+/* ---- signal processing (sigproc.hpp, the paper's Listing 1) ------------
+ * A batch of constant-length signals, one row per signal (SignalBatch,
+ * sigproc.hpp:17-29): data is rows x cols complex128, interleaved (re, im),
+ * row-major; pad_rows guard rows precede the out_rows of interest. */
+typedef struct ws_signal_batch {
+    const double* data;
+    uint64_t rows, cols, pad_rows, out_rows;
+} ws_signal_batch;
+
+/* sigproc_chain (sigproc.cpp:104-118): out[r] = Re(IDFT_row(data[r] * filter))
+ * for r in [pad_rows, pad_rows + out_rows) -> block (out_rows x cols, fp64),
+ * and medians[r] = row_median(block[r]) (nullable). The inverse DFT is the
+ * reference's (1/n scaled, fft.cpp:96-100) along each row; all rows are
+ * transformed so *max_rel_imag (nullable; max |imag| / max |real| over the
+ * batch, i.e. idft_rows_to_real with workers = 1) is the reference's
+ * diagnostic, printed to stderr as it does when > 1e-6. filter: filter_len
+ * complex128 values (== cols, else WS_EINVAL like apply_filter). Validation
+ * follows SignalBatch::validate. Rows up to ws_sigproc_max_cols() samples
+ * whose length factors into primes <= 13.
+ * _device: device pointers, asynchronous unless max_rel_imag is non-null. */
+int ws_sigproc_chain_device(ws_ctx* ctx, const ws_signal_batch* batch, const double* filter, uint64_t filter_len,
+                            double* block, double* medians, double* max_rel_imag);
+/* Host buffers (pinned recommended); filter_complex = 0 takes a real filter
+ * (apply_filter's double overload, sigproc.cpp:26-30). Rows are streamed in
+ * chunks so the H2D, the chain and the D2H overlap. */
+int ws_sigproc_chain(ws_ctx* ctx, const ws_signal_batch* batch, const double* filter, uint64_t filter_len,
+                     int filter_complex, double* block, double* medians, double* max_rel_imag);
+/* row_median (sigproc.cpp:80-93) of each row of a real rows x cols matrix
+ * (device pointers, asynchronous). */
+int ws_row_medians_device(ws_ctx* ctx, const double* m, uint64_t rows, uint64_t cols, double* medians);
+uint64_t ws_sigproc_max_cols(void);
+
 /* Depo CSV ingestion: load_depos (pipeline.cpp:226-262), same header, row
  * format ("id,t_us,x_mm,q,sigma_t_us,sigma_x_mm", %ld,%lf,%lf,%ld,%lf,%lf) and
  * the same validation (bad header, malformed row, id != row index, negative

@@ -120,6 +120,10 @@ class Oracle:
         L.wso_add_white_noise_rng.argtypes = [C.POINTER(Grid), C.c_double, C.c_uint64, C.c_int, C.c_void_p]
         L.wso_digitize.argtypes = [C.c_void_p, C.c_size_t, C.c_double, C.c_double, C.c_int, C.c_void_p]
         L.wso_philox4x32_10.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.wso_sigproc_chain.argtypes = [C.c_void_p, C.c_size_t, C.c_size_t, C.c_size_t, C.c_size_t, C.c_void_p,
+                                        C.c_void_p, C.c_void_p, C.POINTER(C.c_double)]
+        L.wso_row_median.restype = C.c_double
+        L.wso_row_median.argtypes = [C.c_void_p, C.c_size_t]
 
     def _check(self, rc):
         if rc:
@@ -211,6 +215,22 @@ class Oracle:
         self._check(self.lib.wso_convolve_direct(C.byref(g), C.byref(r), _p(s), _p(m)))
         return m
 
+    def sigproc_chain(self, data, filt, pad_rows, out_rows, medians=True):
+        """sigproc_chain restated (sigproc.cpp:104-118): (block, medians, max_rel_imag)."""
+        data = np.ascontiguousarray(data, dtype=np.complex128)
+        filt = np.ascontiguousarray(np.broadcast_to(filt, (data.shape[1],)), dtype=np.complex128)
+        rows, cols = data.shape
+        block = np.zeros((out_rows, cols))
+        med = np.zeros(out_rows) if medians else None
+        mri = C.c_double()
+        self._check(self.lib.wso_sigproc_chain(_p(data), rows, cols, pad_rows, out_rows, _p(filt), _p(block),
+                                               _p(med) if medians else None, C.byref(mri)))
+        return block, med, mri.value
+
+    def row_median(self, v):
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        return self.lib.wso_row_median(_p(v), v.size)
+
     def add_white_noise(self, g, m, sigma, seed, rng_mode=0):
         out = np.ascontiguousarray(m, dtype=np.float64).copy()
         self._check(self.lib.wso_add_white_noise_rng(C.byref(g), sigma, seed, rng_mode, _p(out)))
@@ -264,6 +284,11 @@ class Reference:
         L.wsr_gen_depos.argtypes = [C.c_uint64, C.c_uint64, G, C.c_void_p]
         L.wsr_gen_depos_csv.argtypes = [C.c_uint64, C.c_uint64, G, C.c_char_p]
         L.wsr_load_depos.argtypes = [C.c_char_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
+        L.wsr_sigproc_chain.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p,
+                                        C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_double),
+                                        C.POINTER(C.c_double)]
+        L.wsr_row_median.restype = C.c_double
+        L.wsr_row_median.argtypes = [C.c_void_p, C.c_uint64, C.c_int]
         L.wsr_draws.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p]
         L.wsr_binomials.argtypes = [C.c_int64, C.c_double, C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p]
         L.wsr_philox4x32_10.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
@@ -285,6 +310,22 @@ class Reference:
         out = np.zeros(n, dtype=DEPO_DTYPE)
         self._check(self.lib.wsr_gen_depos(n, seed, C.byref(g), _p(out)))
         return out
+
+    def sigproc_chain(self, data, filt, pad_rows, out_rows, workers=1):
+        """sigproc_chain (sigproc.cpp:104-118): (block, medians, max_rel_imag, seconds)."""
+        data = np.ascontiguousarray(data, dtype=np.complex128)
+        filt = np.ascontiguousarray(np.broadcast_to(filt, (data.shape[1],)), dtype=np.complex128)
+        rows, cols = data.shape
+        block = np.zeros((out_rows, cols))
+        med = np.zeros(out_rows)
+        mri, sec = C.c_double(), C.c_double()
+        self._check(self.lib.wsr_sigproc_chain(_p(data), rows, cols, pad_rows, out_rows, _p(filt), workers,
+                                               _p(block), _p(med), C.byref(mri), C.byref(sec)))
+        return block, med, mri.value, sec.value
+
+    def row_median(self, v, by_sort=False):
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        return self.lib.wsr_row_median(_p(v), v.size, int(by_sort))
 
     def gen_depos_csv(self, n, seed, g, path):
         self._check(self.lib.wsr_gen_depos_csv(n, seed, C.byref(g), str(path).encode()))

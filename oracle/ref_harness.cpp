@@ -534,4 +534,34 @@ int wsr_time_fluct_off(const wsr_grid* g, const wsr_response* r, const Depo* d, 
     return rc;
 }
 
+// sigproc_chain (sigproc.cpp:104-118), unmodified; data/filter are interleaved
+// complex. seconds (nullable) = wall time of the chain call alone.
+int wsr_sigproc_chain(const double* data, std::uint64_t rows, std::uint64_t cols, std::uint64_t pad_rows,
+                      std::uint64_t out_rows, const double* filter, int workers, double* block, double* medians,
+                      double* max_rel_imag, double* seconds)
+{
+    return guarded([&] {
+        SignalBatch batch;
+        batch.data = Matrix<cdouble>(rows, cols);
+        std::memcpy(static_cast<void*>(batch.data.data.data()), data, sizeof(double) * 2 * rows * cols);
+        batch.pad_rows = pad_rows;
+        batch.out_rows = out_rows;
+        std::vector<cdouble> f(cols);
+        std::memcpy(static_cast<void*>(f.data()), filter, sizeof(double) * 2 * cols);
+        const auto t0 = std::chrono::steady_clock::now();
+        const ChainResult r = sigproc_chain(batch, f, workers);
+        const auto t1 = std::chrono::steady_clock::now();
+        if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+        if (block) std::copy(r.block.data.begin(), r.block.data.end(), block);
+        if (medians) std::copy(r.medians.begin(), r.medians.end(), medians);
+        if (max_rel_imag) *max_rel_imag = r.max_rel_imag;
+    });
+}
+
+double wsr_row_median(const double* v, std::uint64_t n, int by_sort)
+{
+    const std::span<const double> s(v, n);
+    return by_sort ? row_median_by_sort(s) : row_median(s);
+}
+
 }  // extern "C"

@@ -601,3 +601,132 @@ uint64_t wso_fnv1a64(const void* data, size_t nbytes)
     }
     return h;
 }
+
+/* ------------------------------------------------------------------------
+ * Signal processing (sigproc.cpp:12-118): filter -> inverse DFT along rows ->
+ * block cut -> per-row medians.
+ *
+ * The DFT is a plain recursive mixed-radix decimation in time (smallest prime
+ * factor first, O(n * sum of prime factors)); it is not the reference's
+ * FftPlan but computes the same unscaled forward transform
+ * X[k] = sum_j x[j] exp(-2 pi i jk / n) (fft.cpp:50), and the inverse by the
+ * reference's conjugation identity with the 1/n factor applied as a multiply
+ * (fft.cpp:96-100).
+ */
+
+/* out = DFT_n of x[0], x[stride], ...; scratch holds n complex values. The
+ * children ping-pong between out and scratch. tw[j] = exp(-2 pi i j / N) of
+ * the root length N (a multiple of n). */
+static void dft_forward_rec(const double* x, size_t stride, size_t n, double* out, double* scratch,
+                            const double* tw, size_t N)
+{
+    if (n == 1) {
+        out[0] = x[0];
+        out[1] = x[1];
+        return;
+    }
+    size_t p = 2;
+    while (p * p <= n && n % p) ++p;
+    if (n % p) p = n;
+    const size_t m = n / p, step = N / n;
+    for (size_t q = 0; q < p; ++q) dft_forward_rec(x + 2 * q * stride, stride * p, m, scratch + 2 * q * m, out, tw, N);
+    for (size_t k = 0; k < n; ++k) {
+        double re = 0.0, im = 0.0;
+        const size_t kk = k % m;
+        for (size_t q = 0; q < p; ++q) {
+            const size_t j = ((q * k) % n) * step;
+            const double c = tw[2 * j], s = tw[2 * j + 1];
+            const double a = scratch[2 * (q * m + kk)], b = scratch[2 * (q * m + kk) + 1];
+            re += a * c - b * s;
+            im += a * s + b * c;
+        }
+        out[2 * k] = re;
+        out[2 * k + 1] = im;
+    }
+}
+
+/* forward unscaled DFT of n complex (interleaved) values, out-of-place;
+ * tw from dft_twiddles(n) */
+static int dft_forward(const double* x, size_t n, double* out, const double* tw)
+{
+    double* work = (double*)malloc(sizeof(double) * 2 * n);
+    if (!work) return fail("sigproc: out of memory");
+    dft_forward_rec(x, 1, n, out, work, tw, n);
+    free(work);
+    return 0;
+}
+
+static double* dft_twiddles(size_t n)
+{
+    double* tw = (double*)malloc(sizeof(double) * 2 * n);
+    if (!tw) return NULL;
+    for (size_t j = 0; j < n; ++j) {
+        const double ang = -2.0 * M_PI * (double)j / (double)n; /* fft.cpp:50 */
+        tw[2 * j] = cos(ang);
+        tw[2 * j + 1] = sin(ang);
+    }
+    return tw;
+}
+
+static int cmp_double(const void* a, const void* b)
+{
+    const double x = *(const double*)a, y = *(const double*)b;
+    return (x > y) - (x < y);
+}
+
+/* row_median_by_sort (sigproc.cpp:95-102): must equal row_median exactly */
+double wso_row_median(const double* v, size_t n)
+{
+    double* w = (double*)malloc(sizeof(double) * (n ? n : 1));
+    memcpy(w, v, sizeof(double) * n);
+    qsort(w, n, sizeof(double), cmp_double);
+    const double r = (n % 2) ? w[n / 2] : (w[n / 2 - 1] + w[n / 2]) / 2.0;
+    free(w);
+    return r;
+}
+
+int wso_sigproc_chain(const double* data, size_t rows, size_t cols, size_t pad_rows, size_t out_rows,
+                      const double* filter, double* block, double* medians, double* max_rel_imag)
+{
+    /* SignalBatch::validate (sigproc.hpp:24-28) */
+    if (cols < 1) return fail("SignalBatch: need at least one column");
+    if (pad_rows + out_rows > rows) return fail("SignalBatch: pad_rows + out_rows exceeds the row count");
+    double* line = (double*)malloc(sizeof(double) * 2 * cols);
+    double* spec = (double*)malloc(sizeof(double) * 2 * cols);
+    double* tw = dft_twiddles(cols);
+    if (!line || !spec || !tw) {
+        free(line);
+        free(spec);
+        free(tw);
+        return fail("sigproc: out of memory");
+    }
+    const double inv = 1.0 / (double)cols;
+    double peak = 0.0, residue = 0.0;
+    int rc = 0;
+    for (size_t r = 0; r < rows && !rc; ++r) {
+        const double* src = data + 2 * r * cols;
+        for (size_t c = 0; c < cols; ++c) {
+            /* apply_filter (sigproc.cpp:12-24), then conj for the inverse (fft.cpp:97) */
+            const double a = src[2 * c], b = src[2 * c + 1], fc = filter[2 * c], fd = filter[2 * c + 1];
+            line[2 * c] = a * fc - b * fd;
+            line[2 * c + 1] = -(a * fd + b * fc);
+        }
+        rc = dft_forward(line, cols, spec, tw);
+        if (rc) break;
+        const int in_block = r >= pad_rows && r < pad_rows + out_rows;
+        for (size_t c = 0; c < cols; ++c) {
+            const double re = spec[2 * c] * inv, im = -spec[2 * c + 1] * inv;
+            if (fabs(re) > peak) peak = fabs(re);
+            if (fabs(im) > residue) residue = fabs(im);
+            if (in_block) block[(r - pad_rows) * cols + c] = re;
+        }
+    }
+    free(line);
+    free(spec);
+    free(tw);
+    if (rc) return rc;
+    if (medians)
+        for (size_t r = 0; r < out_rows; ++r) medians[r] = wso_row_median(block + r * cols, cols);
+    if (max_rel_imag) *max_rel_imag = peak > 0.0 ? residue / peak : residue;
+    return 0;
+}

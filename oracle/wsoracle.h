@@ -93,6 +93,13 @@ int wso_digitize(const double* m, size_t n, double scale, double offset, int bit
 
 uint64_t wso_fnv1a64(const void* data, size_t nbytes);
 
+/* sigproc (sigproc.cpp:12-118). data: rows x cols complex (interleaved re,im),
+ * filter: cols complex. block: out_rows x cols, medians: out_rows (nullable).
+ * max_rel_imag = max |imag| / max |real| over all rows (workers = 1). */
+double wso_row_median(const double* v, size_t n);
+int wso_sigproc_chain(const double* data, size_t rows, size_t cols, size_t pad_rows, size_t out_rows,
+                      const double* filter, double* block, double* medians, double* max_rel_imag);
+
 #ifdef __cplusplus
 }
 #endif

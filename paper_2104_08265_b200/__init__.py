@@ -17,6 +17,11 @@ from .api import (  # noqa: F401
     gen_depos,
     load_depos,
     run_simulation,
+    row_medians_device,
+    sigproc_chain,
+    sigproc_chain_device,
+    sigproc_max_cols,
+    ChainResult,
     save_depos,
     simulate_event,
     simulate_event_device,

@@ -61,6 +61,11 @@ class NoiseModelC(C.Structure):
                 ("amplitude_spectrum", C.c_void_p), ("n_amplitude", C.c_uint64)]
 
 
+class SignalBatchC(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("rows", C.c_uint64), ("cols", C.c_uint64), ("pad_rows", C.c_uint64),
+                ("out_rows", C.c_uint64)]
+
+
 class TimingC(C.Structure):
     _fields_ = [("prepare_ms", C.c_float), ("fluctuate_ms", C.c_float), ("bin_ms", C.c_float),
                 ("convolve_ms", C.c_float), ("total_ms", C.c_float), ("direct_planes", C.c_int32),
@@ -105,6 +110,12 @@ SIGNATURES = {
     "ws_noise_digitize_device": (C.c_int, [_P, _P, C.POINTER(NoiseModelC), C.c_double, C.c_double, C.c_int32, _P]),
     "ws_host_alloc": (C.c_int, [C.c_uint64, C.POINTER(_P)]),
     "ws_host_free": (C.c_int, [_P]),
+    "ws_sigproc_chain_device": (C.c_int, [_P, C.POINTER(SignalBatchC), _P, C.c_uint64, _P, _P,
+                                          C.POINTER(C.c_double)]),
+    "ws_sigproc_chain": (C.c_int, [_P, C.POINTER(SignalBatchC), _P, C.c_uint64, C.c_int, _P, _P,
+                                   C.POINTER(C.c_double)]),
+    "ws_row_medians_device": (C.c_int, [_P, _P, C.c_uint64, C.c_uint64, _P]),
+    "ws_sigproc_max_cols": (C.c_uint64, []),
     "ws_load_depos_csv": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(_P), C.POINTER(C.c_uint64)]),
     "ws_free_depos": (C.c_int, [_P, C.c_int]),
     "ws_save_depos_csv": (C.c_int, [C.c_char_p, _P, C.c_uint64]),

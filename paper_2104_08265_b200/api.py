@@ -330,3 +330,58 @@ def save_depos(path, depos) -> None:
     lib = _lib.load()
     d = np.ascontiguousarray(depos, dtype=DEPO_DTYPE)
     check(lib.ws_save_depos_csv(str(path).encode(), d.ctypes.data if len(d) else None, len(d)))
+
+
+# ---- signal processing (sigproc.hpp; the paper's Listing 1) ----------------
+
+@dataclass
+class ChainResult:
+    """ChainResult (sigproc.hpp:53-57)."""
+    block: np.ndarray
+    medians: np.ndarray
+    max_rel_imag: float
+
+
+def sigproc_chain(data, filt, pad_rows: int = 0, out_rows: int | None = None, ctx: Context | None = None,
+                  want_medians: bool = True) -> ChainResult:
+    """sigproc_chain (sigproc.cpp:104-118) on the GPU through host buffers:
+    filter -> inverse DFT along rows (real part) -> rows [pad_rows, pad_rows +
+    out_rows) -> per-row medians. data: (rows, cols) complex128; filt: cols
+    real or complex values."""
+    ctx = ctx or Context()
+    data = np.ascontiguousarray(data, dtype=np.complex128)
+    if data.ndim != 2:
+        raise WsError(_lib.WS_EINVAL, "SignalBatch: data must be 2-D")
+    rows, cols = data.shape
+    out_rows = rows - pad_rows if out_rows is None else out_rows
+    f = np.asarray(filt)
+    is_complex = np.iscomplexobj(f)
+    f = np.ascontiguousarray(f, dtype=np.complex128 if is_complex else np.float64).reshape(-1)
+    block = np.empty((max(out_rows, 0), cols), dtype=np.float64)
+    med = np.empty(max(out_rows, 0), dtype=np.float64) if want_medians else None
+    mri = C.c_double()
+    b = _lib.SignalBatchC(data.ctypes.data, rows, cols, pad_rows, out_rows)
+    check(ctx.lib.ws_sigproc_chain(ctx.handle, C.byref(b), f.ctypes.data, f.size, int(is_complex),
+                                   block.ctypes.data, med.ctypes.data if med is not None else None, C.byref(mri)))
+    return ChainResult(block, med, mri.value)
+
+
+def sigproc_chain_device(ctx: Context, data_dev, rows: int, cols: int, filter_dev, block_dev, medians_dev=None,
+                         pad_rows: int = 0, out_rows: int | None = None, residue: bool = False):
+    """Device-pointer form (asynchronous unless residue=True, which returns
+    max_rel_imag). data_dev: rows x cols complex128; filter_dev: cols complex128."""
+    out_rows = rows - pad_rows if out_rows is None else out_rows
+    b = _lib.SignalBatchC(_ptr(data_dev).value, rows, cols, pad_rows, out_rows)
+    mri = C.c_double()
+    check(ctx.lib.ws_sigproc_chain_device(ctx.handle, C.byref(b), _ptr(filter_dev), cols, _ptr(block_dev),
+                                          _ptr(medians_dev), C.byref(mri) if residue else None))
+    return mri.value if residue else None
+
+
+def row_medians_device(ctx: Context, m_dev, rows: int, cols: int, medians_dev):
+    """row_median (sigproc.cpp:80-93) of every row of a real rows x cols device matrix."""
+    check(ctx.lib.ws_row_medians_device(ctx.handle, _ptr(m_dev), rows, cols, _ptr(medians_dev)))
+
+
+def sigproc_max_cols() -> int:
+    return int(_lib.load().ws_sigproc_max_cols())

@@ -30,6 +30,7 @@ SOURCES = {
     "ws_direct.cu": [],
     "ws_gprof.cu": [],
     "ws_noise.cu": ["--fmad=false"],
+    "ws_sigproc.cu": [],
     "ws_api.cu": [],
     "ws_host.cu": ["--fmad=false"],
 }

@@ -39,6 +39,9 @@ extern "C" cudaError_t wsb_launch_direct(const EventDesc& ev, const uint32_t* po
                                          const wsb::TEnt* tlist, size_t smem_bytes, cudaStream_t stream);
 extern "C" cudaError_t wsb_launch_fluctuate(const EventDesc& ev, const UnitRec* recs, const uint32_t* pool,
                                             const uint32_t* order, cudaStream_t s);
+extern "C" size_t wsb_sigproc_smem(int n);
+extern "C" int wsb_sigproc_max_n();
+extern "C" cudaError_t wsb_launch_sigproc(const wsb::SigprocDesc& d, cudaStream_t s);
 extern "C" size_t wsb_conv_smem(int N, int Np, int M);
 extern "C" cudaError_t wsb_launch_conv(const EventDesc& ev, const uint32_t* pool, const uint32_t* band_off,
                                        const UnitRec* band_list, int flags, size_t smem_bytes, int variant,
@@ -143,6 +146,15 @@ struct ws_ctx {
     cudaEvent_t aux_fork = nullptr, aux_join = nullptr;
     cudaEvent_t slot_computed[2] = {nullptr, nullptr};
     cudaEvent_t slot_copied[2] = {nullptr, nullptr};
+    // sigproc chain: plan of the last row length + staging of the host path
+    uint64_t sp_n = 0;
+    std::vector<int8_t> sp_radix;
+    DevBuf<double2> sp_tw, sp_data, sp_filter;
+    DevBuf<int> sp_perm;
+    DevBuf<double> sp_block, sp_med;
+    DevBuf<unsigned long long> sp_stats;
+    cudaStream_t h2d_stream = nullptr;
+    cudaEvent_t sp_loaded[2] = {nullptr, nullptr}, sp_done[2] = {nullptr, nullptr}, sp_copied[2] = {nullptr, nullptr};
 };
 
 struct ws_plane {
@@ -677,6 +689,20 @@ int ws_ctx_destroy(ws_ctx* c)
         if (c->slot_computed[s]) cudaEventDestroy(c->slot_computed[s]);
         if (c->slot_copied[s]) cudaEventDestroy(c->slot_copied[s]);
     }
+    c->sp_tw.release();
+    c->sp_data.release();
+    c->sp_filter.release();
+    c->sp_perm.release();
+    c->sp_block.release();
+    c->sp_med.release();
+    c->sp_stats.release();
+    if (c->h2d_stream) {
+        cudaStreamSynchronize(c->h2d_stream);
+        cudaStreamDestroy(c->h2d_stream);
+    }
+    for (int s = 0; s < 2; ++s)
+        for (cudaEvent_t e : {c->sp_loaded[s], c->sp_done[s], c->sp_copied[s]})
+            if (e) cudaEventDestroy(e);
     if (c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
     return WS_OK;
@@ -1168,6 +1194,233 @@ int ws_simulate_plane(ws_plane* p, const ws_depo* depos, uint64_t n, const ws_si
     if (frame) WS_CUDA(cudaMemcpyAsync(frame, c->frames.p, sizeof(float) * cells, cudaMemcpyDeviceToHost, c->stream));
     if (charge) WS_CUDA(cudaMemcpyAsync(charge, c->charges.p, sizeof(float) * cells, cudaMemcpyDeviceToHost, c->stream));
     WS_CUDA(cudaStreamSynchronize(c->stream));
+    return WS_OK;
+}
+
+// ---- signal processing (ws_sigproc.cu) -------------------------------------
+
+namespace {
+
+// plan for row length n: radices (8s, then 4 / 2, then odd primes <= 13),
+// output permutation of the in-place DIF passes, split twiddle table
+int sigproc_plan(ws_ctx* c, uint64_t n)
+{
+    if (c->sp_n == n && n) return WS_OK;
+    std::vector<int8_t> radix;
+    uint64_t m = n;
+    int twos = 0;
+    while (m % 2 == 0) {
+        m /= 2;
+        ++twos;
+    }
+    for (; twos >= 3; twos -= 3) radix.push_back(8);
+    if (twos == 2) radix.push_back(4);
+    if (twos == 1) radix.push_back(2);
+    for (int p : {3, 5, 7, 11, 13})
+        while (m % p == 0) {
+            m /= p;
+            radix.push_back((int8_t)p);
+        }
+    if (m != 1)
+        return set_err(WS_EINVAL, "sigproc: row length %llu has a prime factor > 13 (not supported on the GPU path)",
+                       (unsigned long long)n);
+    if ((int)radix.size() > wsb::kSpMaxRadices) return set_err(WS_EINVAL, "sigproc: too many radix passes");
+    std::vector<int> perm(n);
+    for (uint64_t k = 0; k < n; ++k) {
+        uint64_t kk = k, S = n, pos = 0;
+        for (int8_t R : radix) {
+            S /= (uint64_t)R;
+            pos += (kk % (uint64_t)R) * S;
+            kk /= (uint64_t)R;
+        }
+        perm[k] = (int)pos;
+    }
+    const size_t n_tw = 64 + (n + 63) / 64;
+    std::vector<double2> tw(n_tw);
+    for (size_t j = 0; j < n_tw; ++j) {
+        const uint64_t k = j < 64 ? j : 64 * (j - 64);
+        const long double a = 6.283185307179586476925286766559L * (long double)(k % n) / (long double)n;
+        tw[j] = make_double2((double)cosl(a), (double)sinl(a));
+    }
+    WS_CUDA(c->sp_perm.reserve(n));
+    WS_CUDA(c->sp_tw.reserve(n_tw));
+    WS_CUDA(cudaMemcpyAsync(c->sp_perm.p, perm.data(), sizeof(int) * n, cudaMemcpyHostToDevice, c->stream));
+    WS_CUDA(cudaMemcpyAsync(c->sp_tw.p, tw.data(), sizeof(double2) * n_tw, cudaMemcpyHostToDevice, c->stream));
+    WS_CUDA(cudaStreamSynchronize(c->stream));  // host vectors go out of scope
+    c->sp_radix = radix;
+    c->sp_n = n;
+    return WS_OK;
+}
+
+int sigproc_validate(const ws_signal_batch* b, uint64_t filter_len)
+{
+    if (!b) return set_err(WS_EINVAL, "null batch");
+    // SignalBatch::validate (sigproc.hpp:24-28), apply_filter (sigproc.cpp:14-17)
+    if (b->cols < 1) return set_err(WS_EINVAL, "SignalBatch: need at least one column");
+    if (b->pad_rows + b->out_rows > b->rows)
+        return set_err(WS_EINVAL, "SignalBatch: pad_rows + out_rows exceeds the row count");
+    if (filter_len != b->cols)
+        return set_err(WS_EINVAL, "apply_filter: filter length %llu does not match %llu columns",
+                       (unsigned long long)filter_len, (unsigned long long)b->cols);
+    if (b->cols > (uint64_t)wsb_sigproc_max_n())
+        return set_err(WS_EINVAL, "sigproc: row length %llu exceeds the GPU path's %d samples",
+                       (unsigned long long)b->cols, wsb_sigproc_max_n());
+    if (b->rows > 0x7fffffffull) return set_err(WS_EINVAL, "sigproc: too many rows");
+    if (b->rows && !b->data) return set_err(WS_EINVAL, "null batch data");
+    return WS_OK;
+}
+
+wsb::SigprocDesc sigproc_desc(ws_ctx* c, const double* data, uint64_t rows, int pad, int out, const double2* filter,
+                              double* block, double* medians)
+{
+    wsb::SigprocDesc d{};
+    d.data = reinterpret_cast<const double2*>(data);
+    d.filter = filter;
+    d.block = block;
+    d.medians = medians;
+    d.stats = c->sp_stats.p;
+    d.tw = c->sp_tw.p;
+    d.perm = c->sp_perm.p;
+    d.n = (int)c->sp_n;
+    d.rows = (int)rows;
+    d.pad = pad;
+    d.out = out;
+    d.mode = 0;
+    d.nf = (int)c->sp_radix.size();
+    d.inv_n = 1.0 / (double)c->sp_n;  // fft.cpp:99
+    for (int i = 0; i < d.nf; ++i) d.radix[i >> 4] |= (unsigned long long)c->sp_radix[i] << (4 * (i & 15));
+    return d;
+}
+
+int sigproc_residue(ws_ctx* c, double* max_rel_imag)
+{
+    unsigned long long st[2];
+    WS_CUDA(cudaMemcpyAsync(st, c->sp_stats.p, sizeof st, cudaMemcpyDeviceToHost, c->stream));
+    WS_CUDA(cudaStreamSynchronize(c->stream));
+    double peak, resid;
+    std::memcpy(&peak, &st[0], sizeof peak);
+    std::memcpy(&resid, &st[1], sizeof resid);
+    *max_rel_imag = peak > 0.0 ? resid / peak : resid;
+    if (*max_rel_imag > 1e-6)  // idft_rows_to_real's report (sigproc.cpp:66-68)
+        std::fprintf(stderr, "idft_rows_to_real: imaginary residue %.3e relative (input not Hermitian?)\n",
+                     *max_rel_imag);
+    return WS_OK;
+}
+
+}  // namespace
+
+uint64_t ws_sigproc_max_cols(void) { return (uint64_t)wsb_sigproc_max_n(); }
+
+int ws_sigproc_chain_device(ws_ctx* c, const ws_signal_batch* b, const double* filter, uint64_t filter_len,
+                            double* block, double* medians, double* max_rel_imag)
+{
+    if (!c) return set_err(WS_EINVAL, "null context");
+    if (int rc = sigproc_validate(b, filter_len)) return rc;
+    if (!filter) return set_err(WS_EINVAL, "null filter");
+    if (b->out_rows && !block) return set_err(WS_EINVAL, "null block");
+    WS_CUDA(cudaSetDevice(c->device));
+    if (int rc = sigproc_plan(c, b->cols)) return rc;
+    WS_CUDA(c->sp_stats.reserve(2));
+    WS_CUDA(cudaMemsetAsync(c->sp_stats.p, 0, 2 * sizeof(unsigned long long), c->stream));
+    const wsb::SigprocDesc d = sigproc_desc(c, b->data, b->rows, (int)b->pad_rows, (int)b->out_rows,
+                                            reinterpret_cast<const double2*>(filter), block, medians);
+    WS_CUDA(wsb_launch_sigproc(d, c->stream));
+    if (b->rows) c->launches += 1;
+    if (max_rel_imag) return sigproc_residue(c, max_rel_imag);
+    return WS_OK;
+}
+
+int ws_sigproc_chain(ws_ctx* c, const ws_signal_batch* b, const double* filter, uint64_t filter_len,
+                     int filter_complex, double* block, double* medians, double* max_rel_imag)
+{
+    if (!c) return set_err(WS_EINVAL, "null context");
+    if (int rc = sigproc_validate(b, filter_len)) return rc;
+    if (!filter) return set_err(WS_EINVAL, "null filter");
+    if (b->out_rows && !block) return set_err(WS_EINVAL, "null block");
+    WS_CUDA(cudaSetDevice(c->device));
+    if (int rc = finish_pending(c)) return rc;
+    const uint64_t n = b->cols;
+    if (int rc = sigproc_plan(c, n)) return rc;
+    // filter -> complex on the device (a real filter gets zero imaginary parts)
+    std::vector<double2> f(n);
+    for (uint64_t i = 0; i < n; ++i)
+        f[i] = filter_complex ? make_double2(filter[2 * i], filter[2 * i + 1]) : make_double2(filter[i], 0.0);
+    WS_CUDA(c->sp_filter.reserve(n));
+    WS_CUDA(cudaMemcpyAsync(c->sp_filter.p, f.data(), sizeof(double2) * n, cudaMemcpyHostToDevice, c->stream));
+    WS_CUDA(c->sp_stats.reserve(2));
+    WS_CUDA(cudaMemsetAsync(c->sp_stats.p, 0, 2 * sizeof(unsigned long long), c->stream));
+    WS_CUDA(c->sp_med.reserve(std::max<uint64_t>(b->out_rows, 1)));
+    // rows stream through two staging slots: H2D (h2d_stream) -> chain (main) -> D2H (copy_stream)
+    if (!c->h2d_stream) WS_CUDA(cudaStreamCreateWithFlags(&c->h2d_stream, cudaStreamNonBlocking));
+    if (!c->copy_stream) WS_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    for (int s = 0; s < 2; ++s)
+        for (cudaEvent_t* e : {&c->sp_loaded[s], &c->sp_done[s], &c->sp_copied[s]})
+            if (!*e) WS_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(b->rows, (8u << 20) / (16 * n)));
+    WS_CUDA(c->sp_data.reserve(2 * chunk * n));
+    WS_CUDA(c->sp_block.reserve(2 * chunk * n));
+    WS_CUDA(cudaEventRecord(c->sp_done[0], c->stream));  // filter / stats / plan uploads precede every chunk
+    WS_CUDA(cudaStreamWaitEvent(c->h2d_stream, c->sp_done[0], 0));
+    const uint64_t pad = b->pad_rows, out = b->out_rows;
+    int k = 0;
+    for (uint64_t r0 = 0; r0 < b->rows; r0 += chunk, ++k) {
+        const int slot = k & 1;
+        const uint64_t nr = std::min(chunk, b->rows - r0);
+        double2* din = c->sp_data.p + (size_t)slot * chunk * n;
+        double* dblk = c->sp_block.p + (size_t)slot * chunk * n;
+        // slot reuse: the chain of chunk k - 2 has read din, its block has left dblk
+        if (k >= 2) {
+            WS_CUDA(cudaStreamWaitEvent(c->h2d_stream, c->sp_done[slot], 0));
+            WS_CUDA(cudaStreamWaitEvent(c->stream, c->sp_copied[slot], 0));
+        }
+        WS_CUDA(cudaMemcpyAsync(din, b->data + 2 * r0 * n, sizeof(double2) * nr * n, cudaMemcpyHostToDevice,
+                                c->h2d_stream));
+        WS_CUDA(cudaEventRecord(c->sp_loaded[slot], c->h2d_stream));
+        WS_CUDA(cudaStreamWaitEvent(c->stream, c->sp_loaded[slot], 0));
+        const uint64_t o0 = std::max(r0, pad), o1 = std::min(r0 + nr, pad + out);  // block rows of this chunk
+        const int n_out = o1 > o0 ? (int)(o1 - o0) : 0;
+        const int pad_in_chunk = n_out ? (int)(o0 - r0) : (int)nr;
+        const wsb::SigprocDesc d =
+            sigproc_desc(c, reinterpret_cast<const double*>(din), nr, pad_in_chunk, n_out, c->sp_filter.p, dblk,
+                         medians && n_out ? c->sp_med.p + (o0 - pad) : nullptr);
+        WS_CUDA(wsb_launch_sigproc(d, c->stream));
+        c->launches += 1;
+        WS_CUDA(cudaEventRecord(c->sp_done[slot], c->stream));
+        if (n_out) {
+            WS_CUDA(cudaStreamWaitEvent(c->copy_stream, c->sp_done[slot], 0));
+            WS_CUDA(cudaMemcpyAsync(block + (o0 - pad) * n, dblk, sizeof(double) * (size_t)n_out * n,
+                                    cudaMemcpyDeviceToHost, c->copy_stream));
+        }
+        WS_CUDA(cudaEventRecord(c->sp_copied[slot], c->copy_stream));
+    }
+    if (medians && out) {
+        WS_CUDA(cudaMemcpyAsync(medians, c->sp_med.p, sizeof(double) * out, cudaMemcpyDeviceToHost, c->stream));
+    }
+    WS_CUDA(cudaStreamSynchronize(c->copy_stream));
+    WS_CUDA(cudaStreamSynchronize(c->stream));
+    if (max_rel_imag) return sigproc_residue(c, max_rel_imag);
+    return WS_OK;
+}
+
+int ws_row_medians_device(ws_ctx* c, const double* m, uint64_t rows, uint64_t cols, double* medians)
+{
+    if (!c) return set_err(WS_EINVAL, "null context");
+    if (cols < 1) return set_err(WS_EINVAL, "row_median: empty input");
+    if (cols > (uint64_t)wsb_sigproc_max_n())
+        return set_err(WS_EINVAL, "row_median: row length %llu exceeds the GPU path's %d samples",
+                       (unsigned long long)cols, wsb_sigproc_max_n());
+    if (rows > 0x7fffffffull) return set_err(WS_EINVAL, "row_median: too many rows");
+    if (rows && (!m || !medians)) return set_err(WS_EINVAL, "null argument");
+    WS_CUDA(cudaSetDevice(c->device));
+    wsb::SigprocDesc d{};
+    d.data = reinterpret_cast<const double2*>(m);
+    d.medians = medians;
+    d.n = (int)cols;
+    d.rows = (int)rows;
+    d.out = (int)rows;
+    d.mode = 1;
+    WS_CUDA(wsb_launch_sigproc(d, c->stream));
+    if (rows) c->launches += 1;
     return WS_OK;
 }
 

@@ -412,4 +412,19 @@ __device__ __forceinline__ int64_t binomial_approx(int64_t n, double p, Rng& src
     return (int64_t)k;
 }
 
+// sigproc chain (ws_sigproc.cu): one launch over a batch of signal rows
+constexpr int kSpMaxRadices = 32;
+struct SigprocDesc {
+    const double2* data;        // mode 0: rows x n complex; mode 1: rows x n real
+    const double2* filter;      // n complex (mode 0)
+    double* block;              // out x n (nullable)
+    double* medians;            // out (nullable)
+    unsigned long long* stats;  // [max |re|, max |im|] as bit patterns (mode 0)
+    const double2* tw;          // w(k) = tw[k & 63] * tw[64 + (k >> 6)], w(k) = exp(+2 pi i k / n)
+    const int* perm;            // natural output index -> position after the DIF passes
+    int n, rows, pad, out, mode, nf;
+    double inv_n;
+    unsigned long long radix[2];  // pass f's radix = (radix[f >> 4] >> (4 * (f & 15))) & 15
+};
+
 }  // namespace wsb

@@ -1,0 +1,436 @@
+// Signal processing chain of the paper's Listing 1 (sigproc.cpp:104-118):
+// per-row filter multiply -> inverse DFT along the row (real part kept) ->
+// block cut [pad_rows, pad_rows + out_rows) -> per-row median.
+//
+// One CTA per signal row, the whole row resident in shared memory as
+// complex fp64 (16 B x n; 96 KB at the paper's n = 6000, two CTAs per SM):
+//   load     row x filter (coalesced 16-B loads, streaming), natural order
+//   FFT      in-place mixed-radix decimation in frequency (radices 8/4/2 first,
+//            then odd primes <= 13), exp(+2 pi i/n) twiddles from a 64 x n/64
+//            split table in shared memory; no scratch buffer
+//   store    the DIF output is in digit-reversed order: a gather through the
+//            plan's permutation writes the block row coalesced (x 1/n, the
+//            reference's conjugation identity, fft.cpp:96-100) and leaves the
+//            real part in place for the median; max |re| / max |im| feed the
+//            imaginary-residue report (sigproc.cpp:33-69)
+//   median   radix select on the order-preserving 64-bit keys of the row's
+//            values (11-bit digits, 2048-bin shared histogram), with an early
+//            exit once the rank's bin holds a single element; even lengths
+//            average the two central order statistics (sigproc.cpp:80-93)
+// The median does not need the values in natural order, which is what lets
+// the whole chain run in one buffer.
+#include "ws_common.cuh"
+
+namespace wsb {
+
+constexpr int kSpThreads = 256;
+constexpr int kSpBinsLog = 11;
+constexpr int kSpBins = 1 << kSpBinsLog;
+
+// cos / sin (2 pi m / R) for the odd radices, m < R: offsets 3:0 5:3 7:8 11:15 13:26
+__constant__ double2 c_sproot[39];
+
+template <int R>
+__device__ __forceinline__ constexpr int sp_root_off()
+{
+    return R == 3 ? 0 : R == 5 ? 3 : R == 7 ? 8 : R == 11 ? 15 : 26;
+}
+
+__device__ __forceinline__ double2 c_add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 c_sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 c_mul(double2 a, double2 b)
+{
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 c_muli(double2 a) { return make_double2(-a.y, a.x); }  // a * (+i)
+
+// y_q = sum_r x_r exp(+2 pi i q r / R), in place
+template <int R>
+__device__ __forceinline__ void sp_dft(double2* x)
+{
+    if constexpr (R == 2) {
+        const double2 t = x[0];
+        x[0] = c_add(t, x[1]);
+        x[1] = c_sub(t, x[1]);
+    } else if constexpr (R == 4) {
+        const double2 t0 = c_add(x[0], x[2]), t1 = c_sub(x[0], x[2]);
+        const double2 t2 = c_add(x[1], x[3]), t3 = c_muli(c_sub(x[1], x[3]));
+        x[0] = c_add(t0, t2);
+        x[2] = c_sub(t0, t2);
+        x[1] = c_add(t1, t3);
+        x[3] = c_sub(t1, t3);
+    } else if constexpr (R == 8) {
+        double2 e[4] = {x[0], x[2], x[4], x[6]}, o[4] = {x[1], x[3], x[5], x[7]};
+        sp_dft<4>(e);
+        sp_dft<4>(o);
+        constexpr double h = 0.70710678118654752440084436210485;
+        o[1] = make_double2(h * (o[1].x - o[1].y), h * (o[1].x + o[1].y));
+        o[2] = c_muli(o[2]);
+        o[3] = make_double2(-h * (o[3].x + o[3].y), h * (o[3].x - o[3].y));
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            x[q] = c_add(e[q], o[q]);
+            x[q + 4] = c_sub(e[q], o[q]);
+        }
+    } else {
+        constexpr int H = (R - 1) / 2;
+        double2 s[H + 1], d[H + 1];
+        double2 y0 = x[0];
+#pragma unroll
+        for (int r = 1; r <= H; ++r) {
+            s[r] = c_add(x[r], x[R - r]);
+            d[r] = c_sub(x[r], x[R - r]);
+            y0 = c_add(y0, s[r]);
+        }
+        const double2 x0 = x[0];
+#pragma unroll
+        for (int q = 1; q <= H; ++q) {
+            double2 a = x0, b = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int r = 1; r <= H; ++r) {
+                const double2 w = c_sproot[sp_root_off<R>() + (q * r) % R];
+                a.x = fma(s[r].x, w.x, a.x);
+                a.y = fma(s[r].y, w.x, a.y);
+                b.x = fma(d[r].x, w.y, b.x);
+                b.y = fma(d[r].y, w.y, b.y);
+            }
+            x[q] = make_double2(a.x - b.y, a.y + b.x);
+            x[R - q] = make_double2(a.x + b.y, a.y - b.x);
+        }
+        x[0] = y0;
+    }
+}
+
+__device__ __forceinline__ double2 sp_filter_mul(double2 v, double2 f)
+{
+    // std::complex operator*= (apply_filter, sigproc.cpp:20), no contraction
+    return make_double2(__dsub_rn(__dmul_rn(v.x, f.x), __dmul_rn(v.y, f.y)),
+                        __dadd_rn(__dmul_rn(v.x, f.y), __dmul_rn(v.y, f.x)));
+}
+
+// One decimation-in-frequency pass over sub-transforms of length L:
+// butterflies of radix R at stride S = L / R, then the exp(+2 pi i q j / L)
+// twiddles (w^q by recurrence from one split-table lookup), in place. The
+// first pass (L = n) applies the filter to its inputs.
+template <int R, bool kFilter>
+__device__ __forceinline__ void sp_pass(double2* buf, const double2* tw, const double2* __restrict__ filter, int n,
+                                        int L)
+{
+    const int S = L / R, step = n / L, nb = n / R;
+    const uint32_t magic = 0xffffffffu / (uint32_t)S + 1u;  // b / S for b, S < 2^15
+    for (int b = threadIdx.x; b < nb; b += kSpThreads) {
+        const int blk = S == 1 ? b : (int)__umulhi((uint32_t)b, magic), j = b - blk * S;
+        double2* p = buf + blk * L + j;
+        double2 x[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) x[r] = p[r * S];
+        if constexpr (kFilter) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) x[r] = sp_filter_mul(x[r], __ldg(filter + j + r * S));
+        }
+        sp_dft<R>(x);
+        if (j) {
+            const int k = j * step;
+            const double2 w1 = c_mul(tw[k & 63], tw[64 + (k >> 6)]);
+            double2 w = w1;
+            x[1] = c_mul(x[1], w1);
+#pragma unroll
+            for (int q = 2; q < R; ++q) {
+                w = c_mul(w, w1);
+                x[q] = c_mul(x[q], w);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) p[r * S] = x[r];
+    }
+}
+
+template <bool kFilter>
+__device__ __forceinline__ void sp_pass_any(int R, double2* buf, const double2* tw, const double2* filter, int n, int L)
+{
+    switch (R) {
+        case 2: sp_pass<2, kFilter>(buf, tw, filter, n, L); break;
+        case 3: sp_pass<3, kFilter>(buf, tw, filter, n, L); break;
+        case 4: sp_pass<4, kFilter>(buf, tw, filter, n, L); break;
+        case 5: sp_pass<5, kFilter>(buf, tw, filter, n, L); break;
+        case 7: sp_pass<7, kFilter>(buf, tw, filter, n, L); break;
+        case 8: sp_pass<8, kFilter>(buf, tw, filter, n, L); break;
+        case 11: sp_pass<11, kFilter>(buf, tw, filter, n, L); break;
+        default: sp_pass<13, kFilter>(buf, tw, filter, n, L); break;
+    }
+}
+
+__device__ __forceinline__ unsigned long long sp_key(double v)
+{
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__device__ __forceinline__ double sp_key_value(unsigned long long k)
+{
+    return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
+}
+
+struct SpSelect {
+    uint32_t hist[kSpBins];
+    uint32_t warp_sum[kSpThreads / 32];
+    uint32_t bin, cum, cnt, cnt_less;
+    unsigned long long key, max_less;
+    unsigned long long red[2 * (kSpThreads / 32)];
+    unsigned long long bar;  // mbarrier of the row's bulk copy
+};
+
+// key of the rank-k (0-based) element of buf[0..n).x
+__device__ unsigned long long sp_select(const double2* buf, int n, uint32_t k, SpSelect& s)
+{
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    unsigned long long prefix = 0, hmask = 0;
+    int shift = 64;
+    while (shift > 0) {
+        const int w = shift < kSpBinsLog ? shift : kSpBinsLog;
+        shift -= w;
+        const uint32_t mask = (1u << w) - 1;
+        for (int i = tid; i < kSpBins; i += kSpThreads) s.hist[i] = 0;
+        __syncthreads();
+        for (int i = tid; i < n; i += kSpThreads) {
+            const unsigned long long key = sp_key(buf[i].x);
+            if ((key & hmask) == prefix) atomicAdd(&s.hist[(uint32_t)(key >> shift) & mask], 1u);
+        }
+        __syncthreads();
+        constexpr int kPer = kSpBins / kSpThreads;
+        uint32_t loc[kPer], sum = 0;
+#pragma unroll
+        for (int e = 0; e < kPer; ++e) {
+            loc[e] = s.hist[tid * kPer + e];
+            sum += loc[e];
+        }
+        uint32_t incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        if (lane == 31) s.warp_sum[warp] = incl;
+        __syncthreads();
+        uint32_t base = incl - sum;
+        for (int v = 0; v < warp; ++v) base += s.warp_sum[v];
+        if (k >= base && k < base + sum) {
+#pragma unroll
+            for (int e = 0; e < kPer; ++e) {
+                if (k < base + loc[e]) {
+                    s.bin = tid * kPer + e;
+                    s.cum = base;
+                    s.cnt = loc[e];
+                    break;
+                }
+                base += loc[e];
+            }
+        }
+        __syncthreads();
+        const uint32_t bin = s.bin, cnt = s.cnt;
+        k -= s.cum;
+        prefix |= (unsigned long long)bin << shift;
+        hmask |= (unsigned long long)mask << shift;
+        if (cnt == 1 && shift > 0) {  // the rank's bin holds one element: find it
+            for (int i = tid; i < n; i += kSpThreads) {
+                const unsigned long long key = sp_key(buf[i].x);
+                if ((key & hmask) == prefix) s.key = key;
+            }
+            __syncthreads();
+            const unsigned long long key = s.key;
+            __syncthreads();
+            return key;
+        }
+    }
+    return prefix;
+}
+
+// row_median (sigproc.cpp:80-93) of buf[0..n).x
+__device__ double sp_median(const double2* buf, int n, SpSelect& s)
+{
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned long long upper = sp_select(buf, n, (uint32_t)(n / 2), s);
+    if (n & 1) return sp_key_value(upper);
+    // the rank n/2 - 1 element: upper again unless exactly n/2 elements are below it
+    uint32_t cnt = 0;
+    unsigned long long mx = 0;
+    for (int i = tid; i < n; i += kSpThreads) {
+        const unsigned long long key = sp_key(buf[i].x);
+        if (key < upper) {
+            ++cnt;
+            mx = key > mx ? key : mx;
+        }
+    }
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long v = __shfl_xor_sync(0xffffffffu, mx, o);
+        mx = v > mx ? v : mx;
+    }
+    if (lane == 0) {
+        s.red[warp] = cnt;
+        s.red[kSpThreads / 32 + warp] = mx;
+    }
+    __syncthreads();
+    uint32_t below = 0;
+    unsigned long long max_below = 0;
+    for (int v = 0; v < kSpThreads / 32; ++v) {
+        below += (uint32_t)s.red[v];
+        max_below = s.red[kSpThreads / 32 + v] > max_below ? s.red[kSpThreads / 32 + v] : max_below;
+    }
+    __syncthreads();
+    const unsigned long long lower = below == (uint32_t)(n / 2) ? max_below : upper;
+    return (sp_key_value(lower) + sp_key_value(upper)) / 2.0;
+}
+
+__global__ void __launch_bounds__(kSpThreads, 2) k_sigproc(const SigprocDesc d)
+{
+    extern __shared__ __align__(16) unsigned char sp_smem[];
+    const int n = d.n;
+    double2* buf = reinterpret_cast<double2*>(sp_smem);
+    double2* tw = buf + n;
+    SpSelect& sel = *reinterpret_cast<SpSelect*>(tw + 64 + ((n + 63) >> 6));
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int row = blockIdx.x;
+    const int out_row = row - d.pad;
+    const bool in_block = out_row >= 0 && out_row < d.out;
+
+    if (d.mode == 1) {  // row medians of a real matrix
+        const double* src = reinterpret_cast<const double*>(d.data) + (size_t)row * n;
+        for (int c = tid; c < n; c += kSpThreads) buf[c].x = __ldcs(src + c);
+        __syncthreads();
+        const double med = sp_median(buf, n, sel);
+        if (tid == 0) d.medians[row] = med;
+        return;
+    }
+
+    // the row: one bulk async copy into shared memory (completion on an
+    // mbarrier) while the threads stage the twiddle table
+    const double2* src = d.data + (size_t)row * n;
+    const uint32_t s_buf = (uint32_t)__cvta_generic_to_shared(buf);
+    const uint32_t s_bar = (uint32_t)__cvta_generic_to_shared(&sel.bar);
+    const bool bulk = ((reinterpret_cast<uintptr_t>(d.data) & 15) == 0);
+    if (bulk && tid == 0) {
+        asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(s_bar));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();  // the barrier is initialised before anyone waits on it
+    if (bulk) {
+        if (tid == 0) {
+            const uint32_t bytes = (uint32_t)n * 16u;
+            asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(s_bar), "r"(bytes) : "memory");
+            constexpr uint32_t kChunk = 32768;
+            for (uint32_t off = 0; off < bytes; off += kChunk) {
+                const uint32_t sz = bytes - off < kChunk ? bytes - off : kChunk;
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        s_buf + off),
+                    "l"(reinterpret_cast<const char*>(src) + off), "r"(sz), "r"(s_bar)
+                    : "memory");
+            }
+        }
+    } else {
+        for (int c = tid; c < n; c += kSpThreads) buf[c] = __ldcs(src + c);
+    }
+    const int n_tw = 64 + ((n + 63) >> 6);
+    for (int i = tid; i < n_tw; i += kSpThreads) tw[i] = __ldg(d.tw + i);
+    if (bulk) {
+        uint32_t done = 0;
+        while (!done)
+            asm volatile(
+                "{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                : "=r"(done)
+                : "r"(s_bar)
+                : "memory");
+    }
+    __syncthreads();
+    if (bulk && tid == 0) asm volatile("mbarrier.inval.shared.b64 [%0];" ::"r"(s_bar) : "memory");
+
+    if (d.nf == 0) {  // n == 1
+        if (tid == 0) buf[0] = sp_filter_mul(buf[0], d.filter[0]);
+        __syncthreads();
+    }
+    int L = n;
+    for (int f = 0; f < d.nf; ++f) {
+        const int R = (int)((d.radix[f >> 4] >> (4 * (f & 15))) & 15);
+        if (f == 0)
+            sp_pass_any<true>(R, buf, tw, d.filter, n, L);
+        else
+            sp_pass_any<false>(R, buf, tw, d.filter, n, L);
+        L /= R;
+        __syncthreads();
+    }
+
+    // natural-order gather: block row, residue statistics, real part kept in place
+    double peak = 0.0, resid = 0.0;
+    double* dst = in_block && d.block ? d.block + (size_t)out_row * n : nullptr;
+    for (int i = tid; i < n; i += kSpThreads) {
+        const int p = __ldg(d.perm + i);
+        const double2 v = buf[p];
+        const double re = v.x * d.inv_n, im = v.y * d.inv_n;
+        peak = fmax(peak, fabs(re));
+        resid = fmax(resid, fabs(im));
+        if (dst) __stcs(dst + i, re);
+        buf[p].x = re;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        peak = fmax(peak, __shfl_xor_sync(0xffffffffu, peak, o));
+        resid = fmax(resid, __shfl_xor_sync(0xffffffffu, resid, o));
+    }
+    if (lane == 0) {  // non-negative doubles order as their bit patterns
+        atomicMax(d.stats, (unsigned long long)__double_as_longlong(peak));
+        atomicMax(d.stats + 1, (unsigned long long)__double_as_longlong(resid));
+    }
+    (void)warp;
+    if (!in_block || !d.medians) return;
+    __syncthreads();
+    const double med = sp_median(buf, n, sel);
+    if (tid == 0) d.medians[out_row] = med;
+}
+
+}  // namespace wsb
+
+extern "C" size_t wsb_sigproc_smem(int n)
+{
+    return sizeof(double2) * (size_t)(n + 64 + ((n + 63) >> 6)) + sizeof(wsb::SpSelect);
+}
+
+extern "C" int wsb_sigproc_max_n()
+{
+    // largest row that fits one CTA's shared memory (227 KB opt-in)
+    int n = 0;
+    while (wsb_sigproc_smem(n + 64) <= 227 * 1024) n += 64;
+    return n;
+}
+
+extern "C" cudaError_t wsb_sigproc_setup()
+{
+    static unsigned long long ready = 0;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (ready & (1ull << dev)) return cudaSuccess;
+    double2 roots[39];
+    const int rs[5] = {3, 5, 7, 11, 13}, off[5] = {0, 3, 8, 15, 26};
+    for (int i = 0; i < 5; ++i)
+        for (int m = 0; m < rs[i]; ++m) {
+            const long double a = 6.283185307179586476925286766559L * m / rs[i];
+            roots[off[i] + m] = make_double2((double)cosl(a), (double)sinl(a));
+        }
+    e = cudaMemcpyToSymbol(wsb::c_sproot, roots, sizeof roots);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(wsb::k_sigproc, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    ready |= 1ull << dev;
+    return cudaSuccess;
+}
+
+extern "C" cudaError_t wsb_launch_sigproc(const wsb::SigprocDesc& d, cudaStream_t s)
+{
+    cudaError_t e = wsb_sigproc_setup();
+    if (e != cudaSuccess) return e;
+    if (d.rows == 0) return cudaSuccess;
+    wsb::k_sigproc<<<d.rows, wsb::kSpThreads, wsb_sigproc_smem(d.n), s>>>(d);
+    return cudaGetLastError();
+}

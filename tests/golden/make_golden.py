@@ -74,11 +74,41 @@ def csv_fixtures(ref):
     print("wrote", HERE / "depos_ref.csv", HERE / "golden_csv.json")
 
 
+def sigproc_fixtures(ref):
+    """sigproc_chain (sigproc.cpp:104-118) and row_median (sigproc.cpp:80-102)
+    known answers from the unmodified reference -> tests/golden/sigproc.npz."""
+    rng = np.random.default_rng(2104)
+    out = {}
+    cases = [("c600", 16, 600, 3, 10, True), ("c735", 9, 735, 0, 9, True), ("c1", 4, 1, 1, 2, True),
+             ("c64_real_filter", 6, 64, 2, 4, False)]
+    for name, rows, cols, pad, nout, cfilt in cases:
+        data = rng.normal(size=(rows, cols)) + 1j * rng.normal(size=(rows, cols))
+        filt = (rng.normal(size=cols) + 1j * rng.normal(size=cols)) if cfilt else rng.normal(size=cols) + 0j
+        block, med, mri, _ = ref.sigproc_chain(data, filt, pad, nout)
+        out.update({f"{name}_data": data, f"{name}_filter": filt, f"{name}_block": block, f"{name}_medians": med,
+                    f"{name}_meta": np.array([pad, nout, mri])})
+    # Hermitian rows: forward DFT of real signals, identity filter (SPEC sigproc AC9)
+    sig = rng.normal(size=(12, 6000))
+    spec = np.fft.fft(sig, axis=1)
+    block, med, mri, _ = ref.sigproc_chain(spec, np.ones(6000), 2, 8)
+    out.update({"herm_signal": sig, "herm_block": block, "herm_medians": med, "herm_meta": np.array([2, 8, mri])})
+    # row_median on ties, signed zeros, odd / even lengths
+    med_rows = [np.array([3.0, 1.0, 2.0]), np.array([1.0, 2.0, 3.0, 4.0]), np.array([0.0, -0.0, 0.0, -0.0]),
+                np.array([5.0] * 7), np.array([2.0, 2.0, 1.0, 1.0, 3.0, 3.0]), rng.normal(size=10000),
+                rng.integers(-3, 4, size=1001).astype(np.float64), np.array([-1e300, 1e-300, -0.0, 7.0, 1e300])]
+    for i, v in enumerate(med_rows):
+        out[f"median{i}_in"] = v
+        out[f"median{i}_out"] = np.array([ref.row_median(v), ref.row_median(v, by_sort=True)])
+    np.savez_compressed(HERE / "sigproc.npz", **out)
+    print("wrote", HERE / "sigproc.npz")
+
+
 def main():
     build_ref()
     ref = Reference()
     csv_fixtures(ref)
-    if "--csv-only" in sys.argv:
+    sigproc_fixtures(ref)
+    if "--aux-only" in sys.argv:
         return
     gold = {}
 
