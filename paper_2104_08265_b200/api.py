@@ -343,7 +343,8 @@ class ChainResult:
 
 
 def sigproc_chain(data, filt, pad_rows: int = 0, out_rows: int | None = None, ctx: Context | None = None,
-                  want_medians: bool = True) -> ChainResult:
+                  want_medians: bool = True, block_out: np.ndarray | None = None,
+                  medians_out: np.ndarray | None = None) -> ChainResult:
     """sigproc_chain (sigproc.cpp:104-118) on the GPU through host buffers:
     filter -> inverse DFT along rows (real part) -> rows [pad_rows, pad_rows +
     out_rows) -> per-row medians. data: (rows, cols) complex128; filt: cols
@@ -357,8 +358,12 @@ def sigproc_chain(data, filt, pad_rows: int = 0, out_rows: int | None = None, ct
     f = np.asarray(filt)
     is_complex = np.iscomplexobj(f)
     f = np.ascontiguousarray(f, dtype=np.complex128 if is_complex else np.float64).reshape(-1)
-    block = np.empty((max(out_rows, 0), cols), dtype=np.float64)
-    med = np.empty(max(out_rows, 0), dtype=np.float64) if want_medians else None
+    block = np.empty((max(out_rows, 0), cols), dtype=np.float64) if block_out is None else block_out
+    if block.shape != (max(out_rows, 0), cols) or block.dtype != np.float64 or not block.flags.c_contiguous:
+        raise WsError(_lib.WS_EINVAL, "block_out must be a C-contiguous float64 (out_rows, cols) array")
+    med = None
+    if want_medians:
+        med = np.empty(max(out_rows, 0), dtype=np.float64) if medians_out is None else medians_out
     mri = C.c_double()
     b = _lib.SignalBatchC(data.ctypes.data, rows, cols, pad_rows, out_rows)
     check(ctx.lib.ws_sigproc_chain(ctx.handle, C.byref(b), f.ctypes.data, f.size, int(is_complex),

@@ -1235,13 +1235,18 @@ int sigproc_plan(ws_ctx* c, uint64_t n)
         }
         perm[k] = (int)pos;
     }
-    const size_t n_tw = 64 + (n + 63) / 64;
-    std::vector<double2> tw(n_tw);
-    for (size_t j = 0; j < n_tw; ++j) {
-        const uint64_t k = j < 64 ? j : 64 * (j - 64);
-        const long double a = 6.283185307179586476925286766559L * (long double)(k % n) / (long double)n;
-        tw[j] = make_double2((double)cosl(a), (double)sinl(a));
+    std::vector<double2> tw;  // per pass: exp(+2 pi i j / L), j < L / R
+    uint64_t L = n;
+    for (int8_t R : radix) {
+        const uint64_t S = L / (uint64_t)R;
+        for (uint64_t j = 0; j < S; ++j) {
+            const long double a = 6.283185307179586476925286766559L * (long double)j / (long double)L;
+            tw.push_back(make_double2((double)cosl(a), (double)sinl(a)));
+        }
+        L = S;
     }
+    if (tw.empty()) tw.push_back(make_double2(1.0, 0.0));
+    const size_t n_tw = tw.size();
     WS_CUDA(c->sp_perm.reserve(n));
     WS_CUDA(c->sp_tw.reserve(n_tw));
     WS_CUDA(cudaMemcpyAsync(c->sp_perm.p, perm.data(), sizeof(int) * n, cudaMemcpyHostToDevice, c->stream));

@@ -420,7 +420,7 @@ struct SigprocDesc {
     double* block;              // out x n (nullable)
     double* medians;            // out (nullable)
     unsigned long long* stats;  // [max |re|, max |im|] as bit patterns (mode 0)
-    const double2* tw;          // w(k) = tw[k & 63] * tw[64 + (k >> 6)], w(k) = exp(+2 pi i k / n)
+    const double2* tw;          // per-pass tables: pass f (sub-length L_f) holds exp(+2 pi i j / L_f), j < L_f / R_f
     const int* perm;            // natural output index -> position after the DIF passes
     int n, rows, pad, out, mode, nf;
     double inv_n;

@@ -6,17 +6,20 @@
 // complex fp64 (16 B x n; 96 KB at the paper's n = 6000, two CTAs per SM):
 //   load     row x filter (coalesced 16-B loads, streaming), natural order
 //   FFT      in-place mixed-radix decimation in frequency (radices 8/4/2 first,
-//            then odd primes <= 13), exp(+2 pi i/n) twiddles from a 64 x n/64
-//            split table in shared memory; no scratch buffer
+//            then odd primes <= 13; the filter is applied in the first pass),
+//            exp(+2 pi i/L) twiddles from per-pass tables (coalesced L1
+//            loads); no scratch buffer
 //   store    the DIF output is in digit-reversed order: a gather through the
 //            plan's permutation writes the block row coalesced (x 1/n, the
 //            reference's conjugation identity, fft.cpp:96-100) and leaves the
 //            real part in place for the median; max |re| / max |im| feed the
 //            imaginary-residue report (sigproc.cpp:33-69)
 //   median   radix select on the order-preserving 64-bit keys of the row's
-//            values (11-bit digits, 2048-bin shared histogram), with an early
-//            exit once the rank's bin holds a single element; even lengths
-//            average the two central order statistics (sigproc.cpp:80-93)
+//            values: a 2048-bin histogram over the row's [min, max] locates
+//            the central rank(s); their bins' elements are ranked by counting
+//            (exact radix select on the 64-bit keys as the fallback); even
+//            lengths average the two central order statistics
+//            (sigproc.cpp:80-93)
 // The median does not need the values in natural order, which is what lets
 // the whole chain run in one buffer.
 #include "ws_common.cuh"
@@ -110,13 +113,14 @@ __device__ __forceinline__ double2 sp_filter_mul(double2 v, double2 f)
 
 // One decimation-in-frequency pass over sub-transforms of length L:
 // butterflies of radix R at stride S = L / R, then the exp(+2 pi i q j / L)
-// twiddles (w^q by recurrence from one split-table lookup), in place. The
+// twiddles (w^q by recurrence from the pass's table tw[j] = exp(+2 pi i j / L),
+// coalesced through L1), in place. The
 // first pass (L = n) applies the filter to its inputs.
 template <int R, bool kFilter>
 __device__ __forceinline__ void sp_pass(double2* buf, const double2* tw, const double2* __restrict__ filter, int n,
                                         int L)
 {
-    const int S = L / R, step = n / L, nb = n / R;
+    const int S = L / R, nb = n / R;
     const uint32_t magic = 0xffffffffu / (uint32_t)S + 1u;  // b / S for b, S < 2^15
     for (int b = threadIdx.x; b < nb; b += kSpThreads) {
         const int blk = S == 1 ? b : (int)__umulhi((uint32_t)b, magic), j = b - blk * S;
@@ -130,8 +134,7 @@ __device__ __forceinline__ void sp_pass(double2* buf, const double2* tw, const d
         }
         sp_dft<R>(x);
         if (j) {
-            const int k = j * step;
-            const double2 w1 = c_mul(tw[k & 63], tw[64 + (k >> 6)]);
+            const double2 w1 = __ldg(tw + j);  // exp(+2 pi i j / L)
             double2 w = w1;
             x[1] = c_mul(x[1], w1);
 #pragma unroll
@@ -145,6 +148,13 @@ __device__ __forceinline__ void sp_pass(double2* buf, const double2* tw, const d
     }
 }
 
+// the wide odd radices out of line: their register demand stays out of the hot passes
+template <int R>
+__device__ __noinline__ void sp_pass_wide(double2* buf, const double2* tw, int n, int L)
+{
+    sp_pass<R, false>(buf, tw, nullptr, n, L);
+}
+
 template <bool kFilter>
 __device__ __forceinline__ void sp_pass_any(int R, double2* buf, const double2* tw, const double2* filter, int n, int L)
 {
@@ -155,8 +165,8 @@ __device__ __forceinline__ void sp_pass_any(int R, double2* buf, const double2* 
         case 5: sp_pass<5, kFilter>(buf, tw, filter, n, L); break;
         case 7: sp_pass<7, kFilter>(buf, tw, filter, n, L); break;
         case 8: sp_pass<8, kFilter>(buf, tw, filter, n, L); break;
-        case 11: sp_pass<11, kFilter>(buf, tw, filter, n, L); break;
-        default: sp_pass<13, kFilter>(buf, tw, filter, n, L); break;
+        case 11: sp_pass_wide<11>(buf, tw, n, L); break;  // filtered beforehand
+        default: sp_pass_wide<13>(buf, tw, n, L); break;
     }
 }
 
@@ -171,12 +181,18 @@ __device__ __forceinline__ double sp_key_value(unsigned long long k)
     return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
 }
 
+constexpr int kSpCand = 512;  // candidates finished by rank counting
+
 struct SpSelect {
     uint32_t hist[kSpBins];
     uint32_t warp_sum[kSpThreads / 32];
     uint32_t bin, cum, cnt, cnt_less;
     unsigned long long key, max_less;
     unsigned long long red[2 * (kSpThreads / 32)];
+    double wmin[kSpThreads / 32], wmax[kSpThreads / 32];
+    uint32_t bin_lo, cum_lo, bin_hi, cum_hi, n_cand;
+    unsigned long long rank_key[2];
+    unsigned long long cand[kSpCand];
     unsigned long long bar;  // mbarrier of the row's bulk copy
 };
 
@@ -246,7 +262,7 @@ __device__ unsigned long long sp_select(const double2* buf, int n, uint32_t k, S
 }
 
 // row_median (sigproc.cpp:80-93) of buf[0..n).x
-__device__ double sp_median(const double2* buf, int n, SpSelect& s)
+__device__ __noinline__ double sp_median(const double2* buf, int n, SpSelect& s)
 {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned long long upper = sp_select(buf, n, (uint32_t)(n / 2), s);
@@ -283,13 +299,111 @@ __device__ double sp_median(const double2* buf, int n, SpSelect& s)
     return (sp_key_value(lower) + sp_key_value(upper)) / 2.0;
 }
 
+// row_median via a value-range histogram: bins of (v - lo) * 2048 / (hi - lo)
+// are monotone in v, so the rank(s) n/2 (and n/2 - 1) fall in known bins; the
+// elements of those bins (usually a handful) are compacted and ranked by
+// counting. More than kSpCand candidates (heavy ties, extreme ranges) take the
+// exact radix select instead. lo / hi: the row's min / max, known to all threads.
+__device__ __noinline__ double sp_median_fast(const double2* buf, int n, double lo, double hi, SpSelect& s)
+{
+    if (!(hi > lo)) return lo;  // constant row (or no usable range)
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const double scale = (double)kSpBins / (hi - lo);
+    if (!(scale > 0.0) || isinf(scale)) return sp_median(buf, n, s);
+    auto bin_of = [&](double v) {
+        const int b = (int)((v - lo) * scale);
+        return b < kSpBins - 1 ? b : kSpBins - 1;
+    };
+    for (int i = tid; i < kSpBins; i += kSpThreads) s.hist[i] = 0;
+    if (tid == 0) s.n_cand = 0;
+    __syncthreads();
+    for (int i = tid; i < n; i += kSpThreads) atomicAdd(&s.hist[bin_of(buf[i].x)], 1u);
+    __syncthreads();
+    constexpr int kPer = kSpBins / kSpThreads;
+    uint32_t loc[kPer], sum = 0;
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {
+        loc[e] = s.hist[tid * kPer + e];
+        sum += loc[e];
+    }
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) s.warp_sum[warp] = incl;
+    __syncthreads();
+    uint32_t base = incl - sum;
+    for (int v = 0; v < warp; ++v) base += s.warp_sum[v];
+    const uint32_t k_hi = (uint32_t)(n / 2), k_lo = (n & 1) ? k_hi : k_hi - 1;
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {
+        if (k_lo >= base && k_lo < base + loc[e]) {
+            s.bin_lo = tid * kPer + e;
+            s.cum_lo = base;
+        }
+        if (k_hi >= base && k_hi < base + loc[e]) {
+            s.bin_hi = tid * kPer + e;
+            s.cum_hi = base + loc[e];  // through bin_hi
+        }
+        base += loc[e];
+    }
+    __syncthreads();
+    const int b_lo = (int)s.bin_lo, b_hi = (int)s.bin_hi;
+    const uint32_t c0 = s.cum_lo, n_c = s.cum_hi - c0;
+    if (n_c > (uint32_t)kSpCand) return sp_median(buf, n, s);
+    for (int i = tid; i < n; i += kSpThreads) {
+        const double v = buf[i].x;
+        const int b = bin_of(v);
+        if (b >= b_lo && b <= b_hi) s.cand[atomicAdd(&s.n_cand, 1u)] = sp_key(v);
+    }
+    __syncthreads();
+    for (int t = tid; t < (int)n_c; t += kSpThreads) {
+        const unsigned long long key = s.cand[t];
+        uint32_t less = 0, eq = 0;
+        for (uint32_t j = 0; j < n_c; ++j) {
+            const unsigned long long o = s.cand[j];
+            less += o < key;
+            eq += o == key;
+        }
+        const uint32_t r_lo = k_lo - c0, r_hi = k_hi - c0;
+        if (r_lo >= less && r_lo < less + eq) s.rank_key[0] = key;
+        if (r_hi >= less && r_hi < less + eq) s.rank_key[1] = key;
+    }
+    __syncthreads();
+    const double a = sp_key_value(s.rank_key[0]), b = sp_key_value(s.rank_key[1]);
+    __syncthreads();
+    return (n & 1) ? b : (a + b) / 2.0;
+}
+
+// CTA-wide min / max, result in every thread
+__device__ __forceinline__ void sp_minmax(double& lo, double& hi, SpSelect& s)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (lane == 0) {
+        s.wmin[warp] = lo;
+        s.wmax[warp] = hi;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int v = 0; v < kSpThreads / 32; ++v) {
+        lo = fmin(lo, s.wmin[v]);
+        hi = fmax(hi, s.wmax[v]);
+    }
+}
+
 __global__ void __launch_bounds__(kSpThreads, 2) k_sigproc(const SigprocDesc d)
 {
     extern __shared__ __align__(16) unsigned char sp_smem[];
     const int n = d.n;
     double2* buf = reinterpret_cast<double2*>(sp_smem);
-    double2* tw = buf + n;
-    SpSelect& sel = *reinterpret_cast<SpSelect*>(tw + 64 + ((n + 63) >> 6));
+    SpSelect& sel = *reinterpret_cast<SpSelect*>(buf + n);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int row = blockIdx.x;
     const int out_row = row - d.pad;
@@ -297,9 +411,15 @@ __global__ void __launch_bounds__(kSpThreads, 2) k_sigproc(const SigprocDesc d)
 
     if (d.mode == 1) {  // row medians of a real matrix
         const double* src = reinterpret_cast<const double*>(d.data) + (size_t)row * n;
-        for (int c = tid; c < n; c += kSpThreads) buf[c].x = __ldcs(src + c);
-        __syncthreads();
-        const double med = sp_median(buf, n, sel);
+        double lo = INFINITY, hi = -INFINITY;
+        for (int c = tid; c < n; c += kSpThreads) {
+            const double v = __ldcs(src + c);
+            buf[c].x = v;
+            lo = fmin(lo, v);
+            hi = fmax(hi, v);
+        }
+        sp_minmax(lo, hi, sel);  // includes the barrier after the stores
+        const double med = sp_median_fast(buf, n, lo, hi, sel);
         if (tid == 0) d.medians[row] = med;
         return;
     }
@@ -332,8 +452,6 @@ __global__ void __launch_bounds__(kSpThreads, 2) k_sigproc(const SigprocDesc d)
     } else {
         for (int c = tid; c < n; c += kSpThreads) buf[c] = __ldcs(src + c);
     }
-    const int n_tw = 64 + ((n + 63) >> 6);
-    for (int i = tid; i < n_tw; i += kSpThreads) tw[i] = __ldg(d.tw + i);
     if (bulk) {
         uint32_t done = 0;
         while (!done)
@@ -346,11 +464,13 @@ __global__ void __launch_bounds__(kSpThreads, 2) k_sigproc(const SigprocDesc d)
     __syncthreads();
     if (bulk && tid == 0) asm volatile("mbarrier.inval.shared.b64 [%0];" ::"r"(s_bar) : "memory");
 
-    if (d.nf == 0) {  // n == 1
-        if (tid == 0) buf[0] = sp_filter_mul(buf[0], d.filter[0]);
+    const int r0 = (int)(d.radix[0] & 15);
+    if (d.nf == 0 || r0 > 8) {  // no pass (n == 1) or a first radix too wide to fuse the filter into
+        for (int c = tid; c < n; c += kSpThreads) buf[c] = sp_filter_mul(buf[c], __ldg(d.filter + c));
         __syncthreads();
     }
     int L = n;
+    const double2* tw = d.tw;  // per-pass twiddle tables, back to back
     for (int f = 0; f < d.nf; ++f) {
         const int R = (int)((d.radix[f >> 4] >> (4 * (f & 15))) & 15);
         if (f == 0)
@@ -358,11 +478,12 @@ __global__ void __launch_bounds__(kSpThreads, 2) k_sigproc(const SigprocDesc d)
         else
             sp_pass_any<false>(R, buf, tw, d.filter, n, L);
         L /= R;
+        tw += L;  // this pass's table had S = L_new entries
         __syncthreads();
     }
 
     // natural-order gather: block row, residue statistics, real part kept in place
-    double peak = 0.0, resid = 0.0;
+    double peak = 0.0, resid = 0.0, lo = INFINITY, hi = -INFINITY;
     double* dst = in_block && d.block ? d.block + (size_t)out_row * n : nullptr;
     for (int i = tid; i < n; i += kSpThreads) {
         const int p = __ldg(d.perm + i);
@@ -370,6 +491,8 @@ __global__ void __launch_bounds__(kSpThreads, 2) k_sigproc(const SigprocDesc d)
         const double re = v.x * d.inv_n, im = v.y * d.inv_n;
         peak = fmax(peak, fabs(re));
         resid = fmax(resid, fabs(im));
+        lo = fmin(lo, re);
+        hi = fmax(hi, re);
         if (dst) __stcs(dst + i, re);
         buf[p].x = re;
     }
@@ -384,8 +507,8 @@ __global__ void __launch_bounds__(kSpThreads, 2) k_sigproc(const SigprocDesc d)
     }
     (void)warp;
     if (!in_block || !d.medians) return;
-    __syncthreads();
-    const double med = sp_median(buf, n, sel);
+    sp_minmax(lo, hi, sel);
+    const double med = sp_median_fast(buf, n, lo, hi, sel);
     if (tid == 0) d.medians[out_row] = med;
 }
 
@@ -393,7 +516,7 @@ __global__ void __launch_bounds__(kSpThreads, 2) k_sigproc(const SigprocDesc d)
 
 extern "C" size_t wsb_sigproc_smem(int n)
 {
-    return sizeof(double2) * (size_t)(n + 64 + ((n + 63) >> 6)) + sizeof(wsb::SpSelect);
+    return sizeof(double2) * (size_t)n + sizeof(wsb::SpSelect);
 }
 
 extern "C" int wsb_sigproc_max_n()
