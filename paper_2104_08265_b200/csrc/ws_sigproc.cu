@@ -116,36 +116,63 @@ __device__ __forceinline__ double2 sp_filter_mul(double2 v, double2 f)
 // twiddles (w^q by recurrence from the pass's table tw[j] = exp(+2 pi i j / L),
 // coalesced through L1), in place. The
 // first pass (L = n) applies the filter to its inputs.
+// U butterflies of one pass at once (independent chains for the scheduler)
+template <int R, bool kFilter, int U>
+__device__ __forceinline__ void sp_bfly(double2* buf, const double2* tw, const double2* __restrict__ filter, int L,
+                                        int S, uint32_t magic, int b0)
+{
+    double2 x[U][R];
+    double2* p[U];
+    int j[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int b = b0 + u * kSpThreads;
+        const int blk = S == 1 ? b : (int)__umulhi((uint32_t)b, magic);
+        j[u] = b - blk * S;
+        p[u] = buf + blk * L + j[u];
+#pragma unroll
+        for (int r = 0; r < R; ++r) x[u][r] = p[u][r * S];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        if constexpr (kFilter) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) x[u][r] = sp_filter_mul(x[u][r], __ldg(filter + j[u] + r * S));
+        }
+        sp_dft<R>(x[u]);
+        // exp(+2 pi i q j / L) by recurrence from tw[j] (tw[0] = 1: exact)
+        const double2 w1 = __ldg(tw + j[u]);
+        double2 w = w1;
+        x[u][1] = c_mul(x[u][1], w1);
+#pragma unroll
+        for (int q = 2; q < R; ++q) {
+            w = c_mul(w, w1);
+            x[u][q] = c_mul(x[u][q], w);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int r = 0; r < R; ++r) p[u][r * S] = x[u][r];
+}
+
+// One decimation-in-frequency pass over sub-transforms of length L:
+// butterflies of radix R at stride S = L / R, then the exp(+2 pi i q j / L)
+// twiddles (w^q by recurrence from the pass's table tw[j] = exp(+2 pi i j / L),
+// coalesced through L1), in place. The first pass (L = n) applies the filter
+// to its inputs. Butterflies touch disjoint elements, so two per thread are
+// in flight at once for radices <= 5.
 template <int R, bool kFilter>
 __device__ __forceinline__ void sp_pass(double2* buf, const double2* tw, const double2* __restrict__ filter, int n,
                                         int L)
 {
     const int S = L / R, nb = n / R;
     const uint32_t magic = 0xffffffffu / (uint32_t)S + 1u;  // b / S for b, S < 2^15
-    for (int b = threadIdx.x; b < nb; b += kSpThreads) {
-        const int blk = S == 1 ? b : (int)__umulhi((uint32_t)b, magic), j = b - blk * S;
-        double2* p = buf + blk * L + j;
-        double2 x[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) x[r] = p[r * S];
-        if constexpr (kFilter) {
-#pragma unroll
-            for (int r = 0; r < R; ++r) x[r] = sp_filter_mul(x[r], __ldg(filter + j + r * S));
-        }
-        sp_dft<R>(x);
-        if (j) {
-            const double2 w1 = __ldg(tw + j);  // exp(+2 pi i j / L)
-            double2 w = w1;
-            x[1] = c_mul(x[1], w1);
-#pragma unroll
-            for (int q = 2; q < R; ++q) {
-                w = c_mul(w, w1);
-                x[q] = c_mul(x[q], w);
-            }
-        }
-#pragma unroll
-        for (int r = 0; r < R; ++r) p[r * S] = x[r];
+    int b = threadIdx.x;
+    if constexpr (R <= 5) {
+        for (; b + kSpThreads < nb; b += 2 * kSpThreads) sp_bfly<R, kFilter, 2>(buf, tw, filter, L, S, magic, b);
     }
+    for (; b < nb; b += kSpThreads) sp_bfly<R, kFilter, 1>(buf, tw, filter, L, S, magic, b);
 }
 
 // the wide odd radices out of line: their register demand stays out of the hot passes
@@ -310,9 +337,12 @@ __device__ __noinline__ double sp_median_fast(const double2* buf, int n, double 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const double scale = (double)kSpBins / (hi - lo);
     if (!(scale > 0.0) || isinf(scale)) return sp_median(buf, n, s);
+    // round((v - lo) * scale) through the 2^52 magic constant: one FFMA on the
+    // fp64 pipe instead of an F2I conversion; rounding is monotone, which is
+    // all the binning needs
     auto bin_of = [&](double v) {
-        const int b = (int)((v - lo) * scale);
-        return b < kSpBins - 1 ? b : kSpBins - 1;
+        const uint32_t b = (uint32_t)__double2loint(fma(v - lo, scale, 0x1p52));
+        return (int)(b < (uint32_t)kSpBins - 1 ? b : (uint32_t)kSpBins - 1);
     };
     for (int i = tid; i < kSpBins; i += kSpThreads) s.hist[i] = 0;
     if (tid == 0) s.n_cand = 0;
@@ -472,7 +502,7 @@ __global__ void __launch_bounds__(kSpThreads, 2) k_sigproc(const SigprocDesc d)
     int L = n;
     const double2* tw = d.tw;  // per-pass twiddle tables, back to back
     for (int f = 0; f < d.nf; ++f) {
-        const int R = (int)((d.radix[f >> 4] >> (4 * (f & 15))) & 15);
+        const int R = (int)(((f < 16 ? d.radix[0] : d.radix[1]) >> (4 * (f & 15))) & 15);
         if (f == 0)
             sp_pass_any<true>(R, buf, tw, d.filter, n, L);
         else
