@@ -86,5 +86,6 @@ if __name__ == "__main__":
             traffic = full(tag, rep, kernel)
             (PROF / f"traffic_{kernel}.json").write_text(json.dumps(
                 {"kernel": kernel, "dram_bytes_per_launch": traffic, "source": f"{tag} ncu --set full",
-                 "note": "one launch = one MicroBooNE event (3 planes)"}, indent=1) + "\n")
+                 "note": ("one launch = one 960 x 6000 sigproc batch" if kernel == "k_sigproc"
+                          else "one launch = one MicroBooNE event (3 planes)")}, indent=1) + "\n")
             print((PROF / f"{tag}_{kernel}_ncu.md").read_text())
