@@ -34,8 +34,8 @@ struct __align__(16) UnitRec {
     int32_t t0;    // first tick (padded index)
     int32_t n_w;   // wires
     int32_t n_t;   // ticks
-    uint32_t pool; // offset (in doubles) of [wv(n_w) | tv(n_t)] in the pool
-    int32_t plane;
+    uint32_t pool; // pool offset (32-bit words) of the profiles: fluct off [raw | eff | tv] (f32), on [wv | tv] (f64)
+    uint32_t goff; // direct-path planes: pool offset of g (16-byte aligned; max|g| at g[-1]); else 0
     float a;       // fluct off: q / total; fluct on: unused
     float tsum;    // fluct off: sum of the tick profile, rounded up (>= its max; bounds fixed-point scales)
 };
@@ -122,13 +122,6 @@ __device__ __forceinline__ uint32_t unit_tv_off(const PlaneDesc& P, const UnitRe
 {
     return r.pool + (uint32_t)(r.n_w + unit_n_eff(P, r.n_w));
 }
-// g starts on a 16-byte boundary after tv and one word for max|g| (g[-1]);
-// k_gprof stores float4s and zero-fills g up to a multiple of 32 taps
-__device__ __forceinline__ uint32_t unit_g_off(const PlaneDesc& P, const UnitRec& r)
-{
-    return (unit_tv_off(P, r) + (uint32_t)r.n_t + 4u) & ~3u;
-}
-
 // Coefficient of unit `r` on wire row w of the (stencilled unless raw) charge:
 // a * profile[j], j = (w - first row) mod W, summed over every wrap that lands
 // on the row (a tiny grid can be narrower than the stencilled footprint).

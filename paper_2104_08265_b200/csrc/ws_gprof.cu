@@ -78,7 +78,7 @@ k_gprof(const EventDesc ev, const UnitRec* __restrict__ recs, uint32_t* __restri
                 const UnitRec rec = recs[P.unit_base + ul];
                 if (rec.w0 >= 0) {
                     tv[h] = reinterpret_cast<const float*>(pool + unit_tv_off(P, rec));
-                    gp[h] = reinterpret_cast<float*>(pool + unit_g_off(P, rec));
+                    gp[h] = reinterpret_cast<float*>(pool + rec.goff);
                     wide[h] = rec.n_t > 32;
                     mine[h] = !wide[h];
                     nt[h] = mine[h] ? rec.n_t : 0;

@@ -79,6 +79,63 @@ __device__ __forceinline__ void bin_integrals(double center, double sigma, doubl
     }
 }
 
+// Fluctuation-off bin integrals in fp32 (the north star's fp32 mode): one
+// erfcf per edge, differences formed on the side of the centre where they
+// do not cancel (the tails keep their relative accuracy). Used when both
+// widths are at least a quarter bin, so every edge argument is within
+// |x| < 5 and nothing underflows; narrower depos take the fp64 path.
+template <typename Put>
+__device__ __forceinline__ void bin_integrals_f32(double center, double sigma, double lo_edge, double spacing, int n,
+                                                  Put&& put, double& sum, double& vmax)
+{
+    const double inv = kInvSqrt2 / sigma;
+    const float x0 = (float)((lo_edge - center) * inv), dx = (float)(spacing * inv);
+    float xp = x0, cp = erfcf(fabsf(x0));
+    float s = 0.0f, m = 0.0f, fi = 1.0f;  // float counter: no I2F on the XU pipe
+    for (int i = 0; i < n; ++i, fi += 1.0f) {
+        const float xn = fmaf(fi, dx, x0);
+        const float cn = erfcf(fabsf(xn));
+        // erf(xn) - erf(xp) with erf(x) = sign(x) (1 - erfc|x|)
+        const float diff = xp >= 0.0f ? cp - cn : (xn <= 0.0f ? cn - cp : 2.0f - cn - cp);
+        const float v = 0.5f * diff;
+        put(i, v);
+        s += v;
+        m = fmaxf(m, v);
+        xp = xn;
+        cp = cn;
+    }
+    sum = s;
+    vmax = m;
+}
+
+// fp64 bin integrals out of line (fluctuation on, and narrow depos with it
+// off): their register demand stays out of the common fp32 path.
+// out = {sum_w, max_w, sum_t, max_t}
+template <bool kInline>
+__device__ __forceinline__ void sample_f64_body(const ws_depo* d, double wire_edge, double pitch, int n_w, double tick_edge,
+                                        double tick, int n_t, double* wv64, double* tv64, float* wv32, float* tv32,
+                                        double* out)
+{
+    double sw, mw, st, mt;
+    if (wv64) {
+        bin_integrals(d->x, d->sigma_x, wire_edge, pitch, n_w, [&](int i, double v) { wv64[i] = v; }, sw, mw);
+        bin_integrals(d->t, d->sigma_t, tick_edge, tick, n_t, [&](int i, double v) { tv64[i] = v; }, st, mt);
+    } else {
+        bin_integrals(d->x, d->sigma_x, wire_edge, pitch, n_w, [&](int i, double v) { wv32[i] = (float)v; }, sw, mw);
+        bin_integrals(d->t, d->sigma_t, tick_edge, tick, n_t, [&](int i, double v) { tv32[i] = (float)v; }, st, mt);
+    }
+    out[0] = sw;
+    out[1] = mw;
+    out[2] = st;
+    out[3] = mt;
+}
+
+__device__ __noinline__ void sample_f64_ool(const ws_depo* d, double wire_edge, double pitch, int n_w, double tick_edge,
+                                            double tick, int n_t, float* wv32, float* tv32, double* out)
+{
+    sample_f64_body<false>(d, wire_edge, pitch, n_w, tick_edge, tick, n_t, nullptr, nullptr, wv32, tv32, out);
+}
+
 // One thread per unit: footprint (map_depo_to_grid + clip), bin integrals
 // into the pool, emptiness (sample_patch's total <= 0 test), clipped-charge
 // bookkeeping and, with fluctuation off, the normalised separable profiles
@@ -92,7 +149,10 @@ __device__ __forceinline__ void bin_integrals(double center, double sigma, doubl
 // with raw = wv (the un-stencilled wire profile), eff = the profile after the
 // cross-wire stencil (absent when wire_weights == {1}); rec.a = q / total with
 // total = sum_w wv * sum_t tv.
-__global__ void k_sample(const EventDesc ev, UnitRec* __restrict__ recs, uint32_t* __restrict__ pool, uint32_t pool_cap,
+// kFluct = false (the fluctuation-off hot path): fp32 profiles, 64 registers
+// for occupancy, the rare fp64 fallback out of line; kFluct = true: fp64.
+template <bool kFluct>
+__global__ void __launch_bounds__(128, kFluct ? 1 : 8) k_sample(const EventDesc ev, UnitRec* __restrict__ recs, uint32_t* __restrict__ pool, uint32_t pool_cap,
                          uint32_t* __restrict__ pool_ctr, uint32_t* __restrict__ band_count,
                          unsigned* __restrict__ err)
 {
@@ -107,7 +167,7 @@ __global__ void k_sample(const EventDesc ev, UnitRec* __restrict__ recs, uint32_
     rec.n_w = 0;
     rec.n_t = 0;
     rec.pool = 0;
-    rec.plane = pi;
+    rec.goff = 0;
     rec.a = 0.0f;
     rec.tsum = 0.0f;
     if (ev.drift_enabled && !drift(ev, d)) {
@@ -126,9 +186,9 @@ __global__ void k_sample(const EventDesc ev, UnitRec* __restrict__ recs, uint32_
     const int h = P.h;
     const int n_eff = P.ww_is_one ? 0 : f.n_w + 2 * h;
     // fluctuation off on a direct-path plane: room for g = tv (*) kernel and max|g| (k_fill_bands)
-    const bool with_g = !ev.fluctuate && ev.mode == 0 && P.direct;
+    const bool with_g = !kFluct && ev.mode == 0 && P.direct;
     const uint32_t L = (uint32_t)(f.n_t + P.n_lags - 1);
-    const uint32_t need = ev.fluctuate ? (uint32_t)(2 * (f.n_w + f.n_t) + 1)
+    const uint32_t need = kFluct ? (uint32_t)(2 * (f.n_w + f.n_t) + 1)
                                        : (uint32_t)(f.n_w + n_eff + f.n_t) + (with_g ? ((L + 31u) & ~31u) + 4u : 0u);
     uint32_t off = atomicAdd(pool_ctr, need);
     if ((uint64_t)off + need > pool_cap) {
@@ -139,17 +199,29 @@ __global__ void k_sample(const EventDesc ev, UnitRec* __restrict__ recs, uint32_
     const double wire_edge = P.origin_x + ((double)f.w0 - (double)P.pad_w) * P.pitch;
     const double tick_edge = P.origin_t + ((double)f.t0 - (double)P.pad_t) * P.tick;
     double sw, mw, st, mt;
-    if (ev.fluctuate) {
+    if constexpr (kFluct) {
+        double o4[4];
         off += off & 1u;  // 8-byte alignment
         double* wv = reinterpret_cast<double*>(pool + off);
-        double* tv = wv + f.n_w;
-        bin_integrals(d.x, d.sigma_x, wire_edge, P.pitch, f.n_w, [&](int i, double v) { wv[i] = v; }, sw, mw);
-        bin_integrals(d.t, d.sigma_t, tick_edge, P.tick, f.n_t, [&](int i, double v) { tv[i] = v; }, st, mt);
+        sample_f64_body<true>(&d, wire_edge, P.pitch, f.n_w, tick_edge, P.tick, f.n_t, wv, wv + f.n_w, nullptr, nullptr,
+                              o4);
+        sw = o4[0];
+        mw = o4[1];
+        st = o4[2];
+        mt = o4[3];
+    } else if (!(d.sigma_x * 4.0 >= P.pitch && d.sigma_t * 4.0 >= P.tick)) {
+        double o4[4];
+        float* raw = reinterpret_cast<float*>(pool + off);
+        sample_f64_ool(&d, wire_edge, P.pitch, f.n_w, tick_edge, P.tick, f.n_t, raw, raw + f.n_w + n_eff, o4);
+        sw = o4[0];
+        mw = o4[1];
+        st = o4[2];
+        mt = o4[3];
     } else {
         float* raw = reinterpret_cast<float*>(pool + off);
         float* tv = raw + f.n_w + n_eff;
-        bin_integrals(d.x, d.sigma_x, wire_edge, P.pitch, f.n_w, [&](int i, double v) { raw[i] = (float)v; }, sw, mw);
-        bin_integrals(d.t, d.sigma_t, tick_edge, P.tick, f.n_t, [&](int i, double v) { tv[i] = (float)v; }, st, mt);
+        bin_integrals_f32(d.x, d.sigma_x, wire_edge, P.pitch, f.n_w, [&](int i, float v) { raw[i] = v; }, sw, mw);
+        bin_integrals_f32(d.t, d.sigma_t, tick_edge, P.tick, f.n_t, [&](int i, float v) { tv[i] = v; }, st, mt);
     }
     // sum_w sum_t wv*tv > 0  <=>  max(wv)*max(tv) > 0 (all terms >= 0, products monotone)
     if (!(mw * mt > 0.0)) {
@@ -158,7 +230,7 @@ __global__ void k_sample(const EventDesc ev, UnitRec* __restrict__ recs, uint32_
         recs[u] = rec;
         return;
     }
-    if (!ev.fluctuate) {
+    if constexpr (!kFluct) {
         // S = q * p = a * wv[w] * tv[t] with a = q / total; a is applied by
         // the consumer (k_conv), so the profiles are stored unscaled
         const double a = (double)d.q / (sw * st);
@@ -166,12 +238,12 @@ __global__ void k_sample(const EventDesc ev, UnitRec* __restrict__ recs, uint32_
         if (n_eff) {
             float* eff = raw + f.n_w;
             for (int j = 0; j < n_eff; ++j) {
-                double e = 0.0;
+                float e = 0.0f;
                 for (int dw = -h; dw <= h; ++dw) {
                     const int i = j - h - dw;
-                    if (i >= 0 && i < f.n_w) e += P.ww[dw + h] * (double)raw[i];
+                    if (i >= 0 && i < f.n_w) e = fmaf((float)P.ww[dw + h], raw[i], e);
                 }
-                eff[j] = (float)e;
+                eff[j] = e;
             }
         }
         rec.a = (float)a;
@@ -183,7 +255,149 @@ __global__ void k_sample(const EventDesc ev, UnitRec* __restrict__ recs, uint32_
     rec.n_t = f.n_t;
     rec.pool = off;
     recs[u] = rec;
-    if (!ev.fluctuate && ev.mode == 0)
+    if (!kFluct && ev.mode == 0)
+        for_each_bin(P, f.w0, f.n_w, f.t0, f.n_t, [&](int c) { atomicAdd(&band_count[P.band_base + c], 1u); });
+}
+
+// Fluctuation-off sampling (the hot path), one thread per unit as k_sample,
+// but the profiles [raw][eff][tv] are written through shared memory: every
+// lane stages its unit's words, then the warp copies unit after unit with
+// coalesced stores (per-lane scattered 4-byte stores were the limiter:
+// 8.4M L2 sectors for 50 MB). Units with more than kStageWords profile words
+// (or the fp64 fallback for sub-quarter-bin widths) write directly.
+constexpr int kSampleThreads = 128;
+constexpr int kStageWarp = 32 * 52;  // staged profile words per warp
+
+__global__ void __launch_bounds__(kSampleThreads, 8)
+k_sample_off(const EventDesc ev, UnitRec* __restrict__ recs, uint32_t* __restrict__ pool, uint32_t pool_cap,
+             uint32_t* __restrict__ pool_ctr, uint32_t* __restrict__ band_count, unsigned* __restrict__ err)
+{
+    extern __shared__ float s_stage[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool in_range = u < ev.total_units;
+    const int pi = in_range ? plane_of_unit(ev, u) : 0;
+    const PlaneDesc& P = ev.p[pi];
+    ws_depo d{};
+    if (in_range) d = P.depos[u - P.unit_base];
+    UnitRec rec;
+    rec.w0 = -1;
+    rec.t0 = 0;
+    rec.n_w = 0;
+    rec.n_t = 0;
+    rec.pool = 0;
+    rec.goff = 0;
+    rec.a = 0.0f;
+    rec.tsum = 0.0f;
+    bool live = in_range;
+    if (live && ev.drift_enabled && !drift(ev, d)) {
+        atomicOr(err, kErrDomain);
+        live = false;
+    }
+    Footprint f{};
+    if (live) {
+        if (d.q < 0) atomicOr(err, kErrCharge);
+        f = footprint(P, d);
+        if (f.clipped) atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[1]), 1ULL);
+        if (f.empty) {
+            atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[0]), (unsigned long long)d.q);
+            live = false;
+        }
+    }
+    const int h = P.h;
+    const int n_eff = live && !P.ww_is_one ? f.n_w + 2 * h : 0;
+    // warp-contiguous allocation, one atomic per warp: the 32 units' profiles
+    // back to back [base, base + W), then their g regions (direct planes:
+    // 4 header words, g[-1] = max|g|, then ceil32(L) taps)
+    const uint32_t words = live ? (uint32_t)(f.n_w + n_eff + f.n_t) : 0u;
+    const uint32_t gneed = (live && ev.mode == 0 && P.direct) ? (((uint32_t)(f.n_t + P.n_lags - 1) + 31u) & ~31u) + 4u
+                                                               : 0u;
+    uint32_t wex = words, gex = gneed;  // inclusive scans -> exclusive below
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t a = __shfl_up_sync(0xffffffffu, wex, o), b = __shfl_up_sync(0xffffffffu, gex, o);
+        if (lane >= o) {
+            wex += a;
+            gex += b;
+        }
+    }
+    const uint32_t w_tot = __shfl_sync(0xffffffffu, wex, 31), g_tot = __shfl_sync(0xffffffffu, gex, 31);
+    wex -= words;
+    gex -= gneed;
+    const uint32_t w_pad = (w_tot + 3u) & ~3u;
+    uint32_t base = 0;
+    if (lane == 0 && w_tot + g_tot) base = atomicAdd(pool_ctr, w_pad + g_tot + 4u);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    const uint32_t gbase = (base + w_pad + 3u) & ~3u;  // 16-byte aligned
+    if ((uint64_t)base + w_pad + g_tot + 4u > pool_cap && (w_tot + g_tot)) {
+        if (live) atomicOr(err, kErrPool);
+        live = false;
+    }
+    const uint32_t off = base + wex;
+    const bool fast = live && d.sigma_x * 4.0 >= P.pitch && d.sigma_t * 4.0 >= P.tick;
+    // the staged prefix of the warp's profile words (compact, same order as the pool)
+    const bool staged = live && wex + words <= (uint32_t)kStageWarp;  // a prefix of the lanes
+    float* stage = s_stage + warp * kStageWarp;
+    double sw = 0.0, mw = 0.0, st = 0.0, mt = 0.0;
+    float* raw = reinterpret_cast<float*>(pool + off);
+    if (live) {
+        rec.goff = gneed ? gbase + gex + 4u : 0u;
+        const double wire_edge = P.origin_x + ((double)f.w0 - (double)P.pad_w) * P.pitch;
+        const double tick_edge = P.origin_t + ((double)f.t0 - (double)P.pad_t) * P.tick;
+        float* dst = staged ? stage + wex : raw;
+        if (fast) {
+            float* tv = dst + f.n_w + n_eff;
+            bin_integrals_f32(d.x, d.sigma_x, wire_edge, P.pitch, f.n_w, [&](int i, float v) { dst[i] = v; }, sw,
+                              mw);
+            bin_integrals_f32(d.t, d.sigma_t, tick_edge, P.tick, f.n_t, [&](int i, float v) { tv[i] = v; }, st, mt);
+        } else {
+            double o4[4];
+            sample_f64_ool(&d, wire_edge, P.pitch, f.n_w, tick_edge, P.tick, f.n_t, dst, dst + f.n_w + n_eff, o4);
+            sw = o4[0];
+            mw = o4[1];
+            st = o4[2];
+            mt = o4[3];
+        }
+        if (n_eff) {
+            float* eff = dst + f.n_w;
+            for (int j = 0; j < n_eff; ++j) {
+                float e = 0.0f;
+                for (int dw = -h; dw <= h; ++dw) {
+                    const int i = j - h - dw;
+                    if (i >= 0 && i < f.n_w) e = fmaf((float)P.ww[dw + h], dst[i], e);
+                }
+                eff[j] = e;
+            }
+        }
+    }
+    // coalesced write-out of the staged prefix [base, base + n_staged)
+    __syncwarp();
+    uint32_t n_staged = staged ? wex + words : 0u;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) n_staged = max(n_staged, __shfl_xor_sync(0xffffffffu, n_staged, o));
+    float* pw = reinterpret_cast<float*>(pool) + base;
+    for (uint32_t k = lane; k < n_staged; k += 32) pw[k] = stage[k];
+    if (!live) {
+        if (in_range) recs[u] = rec;
+        return;
+    }
+    // sum_w sum_t wv*tv > 0  <=>  max(wv)*max(tv) > 0
+    if (!(mw * mt > 0.0)) {
+        // numerically empty (rasterize.cpp:111-116) -> clipped charge (pipeline.cpp:339-340)
+        atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[0]), (unsigned long long)d.q);
+        recs[u] = rec;
+        return;
+    }
+    // S = q * p = a * wv[w] * tv[t] with a = q / total (applied by the consumers)
+    rec.a = (float)((double)d.q / (sw * st));
+    rec.tsum = __double2float_ru(st);
+    rec.w0 = f.w0;
+    rec.t0 = f.t0;
+    rec.n_w = f.n_w;
+    rec.n_t = f.n_t;
+    rec.pool = off;
+    recs[u] = rec;
+    if (ev.mode == 0)
         for_each_bin(P, f.w0, f.n_w, f.t0, f.n_t, [&](int c) { atomicAdd(&band_count[P.band_base + c], 1u); });
 }
 
@@ -247,7 +461,7 @@ __global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ rec
     }
     const UnitRec rec = recs[u];
     if (rec.w0 < 0) return;
-    const PlaneDesc& P = ev.p[rec.plane];
+    const PlaneDesc& P = ev.p[plane_of_unit(ev, u)];
     if (!P.direct) {
         for_each_bin(P, rec.w0, rec.n_w, rec.t0, rec.n_t, [&](int c) {
             const uint32_t b = P.band_base + c;
@@ -258,7 +472,7 @@ __global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ rec
     const int L = rec.n_t + P.n_lags - 1;
     int ts = rec.t0 + P.lo_lag;
     if (ts < 0) ts += P.N;
-    const uint32_t goff = unit_g_off(P, rec);
+    const uint32_t goff = rec.goff;
     // the unit's (stencilled) wire rows; units whose rows do not wrap around
     // the padded grid read their profile with branch-free predicated loads
     const bool stencil = !P.ww_is_one;
@@ -317,7 +531,7 @@ __global__ void k_fluctuate(const EventDesc ev, const UnitRec* __restrict__ recs
     const uint32_t u = order ? order[i] : i;
     const UnitRec rec = recs[u];
     if (rec.w0 < 0) return;
-    const PlaneDesc& P = ev.p[rec.plane];
+    const PlaneDesc& P = ev.p[plane_of_unit(ev, u)];
     const ws_depo d = P.depos[u - P.unit_base];
     const double* wv = reinterpret_cast<const double*>(pool + rec.pool);
     const double* tv = wv + rec.n_w;
@@ -361,7 +575,13 @@ extern "C" cudaError_t wsb_launch_sample(const wsb::EventDesc& ev, wsb::UnitRec*
     if (ev.total_units == 0) return cudaSuccess;
     const uint32_t threads = 128;
     const uint32_t blocks = (ev.total_units + threads - 1) / threads;
-    wsb::k_sample<<<blocks, threads, 0, s>>>(ev, recs, pool, pool_cap, pool_ctr, band_count, err);
+    if (ev.fluctuate) {
+        wsb::k_sample<true><<<blocks, threads, 0, s>>>(ev, recs, pool, pool_cap, pool_ctr, band_count, err);
+    } else {
+        constexpr size_t smem = sizeof(float) * (wsb::kSampleThreads / 32) * wsb::kStageWarp;
+        wsb::k_sample_off<<<(ev.total_units + wsb::kSampleThreads - 1) / wsb::kSampleThreads, wsb::kSampleThreads,
+                            smem, s>>>(ev, recs, pool, pool_cap, pool_ctr, band_count, err);
+    }
     return cudaGetLastError();
 }
 
