@@ -16,9 +16,9 @@
 // depos (tick span, profile offset, max|g|, per-row coefficients). The CTA
 // stages the list, bounds every row (per 64-tick segment sum of |terms|,
 // largest term; one thread per entry x row) to fix a per-row power-of-two
-// scale, then one warp per entry streams the depo's profile through a
-// cp.async ring and adds round(c_w g_j) to every covered row with native
-// shared atomics (one FFMA rounding + one RED per tap). The
+// scale, then one warp per entry loads the depo's profile into registers
+// (the next entry's load in flight behind the current one's atomics) and adds
+// round(c_w g_j) to every covered row with native shared atomics. The
 // integer sums are exact, so the frame is bitwise reproducible for any
 // schedule. Lanes whose tick falls outside the window write to a row margin
 // that is discarded. Work ~ depos x rows x L instead of cells x log(ticks).
@@ -29,10 +29,9 @@
 namespace wsb {
 
 constexpr int kQ = 5;                          // profile taps per lane in registers: L <= 160 fast path
-constexpr int kSlot = 32 * kQ;                 // ring slot (floats)
+constexpr int kSlot = 32 * kQ;                 // taps of the register fast path
 constexpr int kMargin = kSlot;                 // discard margins either side of every row
 constexpr int kRowStride = kMargin + kTileTicks + kMargin;  // ints per tile row
-constexpr int kRing = 2;                       // profile fetches in flight per warp
 constexpr int kDirectThreads = 512;  // two CTAs per SM
 
 // Fixed-point term round(c g). WS_DIRECT_MAGIC: one FFMA with the magic
@@ -101,7 +100,6 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
 {
     constexpr int R = kTileRows;
     constexpr int NW = NT / 32;
-    constexpr int D = kRing;
     static_assert(NW >= R && kSegs == 32 && (R & (R - 1)) == 0, "one warp per row computes the scales");
     constexpr int kRShift = R == 16 ? 4 : R == 8 ? 3 : R == 4 ? 2 : 1;
     const uint32_t gb = blockIdx.x;
@@ -116,13 +114,11 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
     // layout: fixed-point rows [R][kRowStride] (the first kMargin ints of a
-    // row are the discard margin) | segment bounds [R][kSegs] | profile ring
-    // [NW][D][kSlot] | staged entries [cap]
+    // row are the discard margin) | segment bounds [R][kSegs] | staged entries [cap]
     extern __shared__ __align__(16) unsigned char smem[];
     int* acc = reinterpret_cast<int*>(smem);
     unsigned* segb = reinterpret_cast<unsigned*>(acc + R * kRowStride);
-    float* ring = reinterpret_cast<float*>(segb + R * kSegs);
-    TEnt* ent = reinterpret_cast<TEnt*>(ring + NW * D * kSlot);
+    TEnt* ent = reinterpret_cast<TEnt*>(segb + R * kSegs);
     __shared__ unsigned s_tmax[R];  // max single term per row (float bits)
     __shared__ float s_scale[R], s_inv[R];
     __shared__ int s_ovf;
@@ -223,11 +219,8 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
     // accumulate, one warp per entry: lane j adds round(c_w g[j] scale_w) to
     // tick ts + j of every covered row (consecutive lanes -> consecutive
     // banks); ticks outside the window go to the lane's margin slot. Each
-    // warp streams its entries' profiles through a D-deep cp.async ring.
+    // warp holds its entry's profile in registers, the next one in flight.
     constexpr uint32_t row_bytes = 4u * kRowStride;
-    float* my_ring = ring + (size_t)warp * D * kSlot;
-    const uint32_t s_ring = (uint32_t)__cvta_generic_to_shared(my_ring);
-    const uint32_t s_lane = s_ring + 4u * (uint32_t)lane;
 
     auto scatter = [&](const TEnt& d, const float* gv) {  // d: staged, coefficients pre-scaled
         const uint32_t tsL = d.tsL, rows = d.rows;
@@ -272,35 +265,29 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
         // coefficients -> fixed-point units of their row
         for (int i = tid; i < cnt * R; i += NT) ent[i >> kRShift].c[i & (R - 1)] *= s_scale[i & (R - 1)];
         __syncthreads();
-        // profile fetch of local entry e into ring slot s (one commit group)
-        auto fetch = [&](int e, int s) {
+        // profile of local entry e -> registers (tap lane + 32 q; g is 0-filled
+        // to a multiple of 32 taps, nothing past it is read); one entry ahead
+        auto load_g = [&](int e, float* gv) {
+            int lc = 0;
+            const float* src = nullptr;
             if (e < cnt) {
                 const TEnt& d = ent[e];
-                const int n4 = min((((int)(d.tsL >> 16) + 31) & ~31) >> 2, kSlot / 4);
-                const float* src = reinterpret_cast<const float*>(pool + d.goff);
-                const uint32_t dst = s_ring + 4u * (uint32_t)(s * kSlot);
-                if (lane < n4) cp_async16(dst + 16u * lane, src + 4 * lane);
-                if (lane + 32 < n4) cp_async16(dst + 16u * (lane + 32), src + 4 * (lane + 32));
+                lc = (int)(((d.tsL >> 16) + 31u) & ~31u);
+                src = reinterpret_cast<const float*>(pool + d.goff) + lane;
             }
-            cp_commit();
-        };
 #pragma unroll
-        for (int k = 0; k < D; ++k) fetch(warp + NW * k, k);
-        int s = 0;
+            for (int q = 0; q < kQ; ++q) gv[q] = 32 * q < lc ? __ldg(src + 32 * q) : 0.0f;
+        };
+        float gn[kQ];
+        load_g(warp, gn);
 #pragma unroll 1
         for (int e = warp; e < cnt; e += NW) {
-            cp_wait<D - 1>();
-            __syncwarp();
             float gv[kQ];
 #pragma unroll
-            for (int q = 0; q < kQ; ++q)  // past ceil32(L): unused
-                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(gv[q]) : "r"(s_lane + 4u * (uint32_t)(s * kSlot + 32 * q)));
-            __syncwarp();
-            fetch(e + NW * D, s);
-            s = s + 1 == D ? 0 : s + 1;
+            for (int q = 0; q < kQ; ++q) gv[q] = gn[q];
+            load_g(e + NW, gn);
             scatter(ent[e], gv);
         }
-        cp_wait<0>();
     }
     __syncthreads();
 
@@ -334,7 +321,7 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
 extern "C" size_t wsb_direct_smem(int cap)
 {
     return sizeof(int) * wsb::kTileRows * wsb::kRowStride + sizeof(unsigned) * wsb::kTileRows * wsb::kSegs +
-           sizeof(float) * (wsb::kDirectThreads / 32) * wsb::kRing * wsb::kSlot + sizeof(wsb::TEnt) * (size_t)cap;
+           sizeof(wsb::TEnt) * (size_t)cap;
 }
 
 extern "C" int wsb_direct_cap()
