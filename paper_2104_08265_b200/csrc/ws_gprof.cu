@@ -59,7 +59,34 @@ k_gprof(const EventDesc ev, const UnitRec* __restrict__ recs, uint32_t* __restri
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gq = lane >> 2, tq = lane & 3;  // mma fragment coordinates
     const int n_groups = (int)((P.n_units + 15) / 16);
-    for (int grp = blockIdx.x * kGpWarps + warp; grp < n_groups; grp += gridDim.x * kGpWarps) {
+    const int stride = gridDim.x * kGpWarps;
+    // the fields of this thread's two records (rows gq, gq + 8), the next
+    // group's prefetched while the current one computes
+    struct Rec {
+        int w0, n_w, n_t;
+        uint32_t pool, goff;
+    };
+    auto load_rec = [&](int grp, Rec* out) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t ul = (uint32_t)grp * 16 + gq + 8 * h;
+            out[h].w0 = -1;
+            if (grp < n_groups && ul < P.n_units) {
+                const int4 a = __ldg(reinterpret_cast<const int4*>(recs + P.unit_base + ul));
+                const int4 b = __ldg(reinterpret_cast<const int4*>(recs + P.unit_base + ul) + 1);
+                out[h].w0 = a.x;
+                out[h].n_w = a.z;
+                out[h].n_t = a.w;
+                out[h].pool = (uint32_t)b.x;
+                out[h].goff = (uint32_t)b.y;
+            }
+        }
+    };
+    Rec nxt[2];
+    load_rec(blockIdx.x * kGpWarps + warp, nxt);
+    for (int grp = blockIdx.x * kGpWarps + warp; grp < n_groups; grp += stride) {
+        Rec cur[2] = {nxt[0], nxt[1]};
+        load_rec(grp + stride, nxt);
         // this thread's two units: rows gq and gq + 8 of the group
         const float* tv[2];
         float* gp[2];
@@ -67,23 +94,20 @@ k_gprof(const EventDesc ev, const UnitRec* __restrict__ recs, uint32_t* __restri
         bool mine[2], wide[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            const uint32_t ul = (uint32_t)grp * 16 + gq + 8 * h;
             mine[h] = false;
             wide[h] = false;
             nt[h] = 0;
             lp[h] = 0;
             tv[h] = nullptr;
             gp[h] = nullptr;
-            if (ul < P.n_units) {
-                const UnitRec rec = recs[P.unit_base + ul];
-                if (rec.w0 >= 0) {
-                    tv[h] = reinterpret_cast<const float*>(pool + unit_tv_off(P, rec));
-                    gp[h] = reinterpret_cast<float*>(pool + rec.goff);
-                    wide[h] = rec.n_t > 32;
-                    mine[h] = !wide[h];
-                    nt[h] = mine[h] ? rec.n_t : 0;
-                    lp[h] = (rec.n_t + nl - 1 + 31) & ~31;
-                }
+            if (cur[h].w0 >= 0) {
+                const uint32_t tvo = cur[h].pool + (uint32_t)(cur[h].n_w + unit_n_eff(P, cur[h].n_w));
+                tv[h] = reinterpret_cast<const float*>(pool + tvo);
+                gp[h] = reinterpret_cast<float*>(pool + cur[h].goff);
+                wide[h] = cur[h].n_t > 32;
+                mine[h] = !wide[h];
+                nt[h] = mine[h] ? cur[h].n_t : 0;
+                lp[h] = (cur[h].n_t + nl - 1 + 31) & ~31;
             }
         }
         // k steps (8 taps of tv each) and n tiles (8 output taps) the group needs
@@ -195,8 +219,8 @@ extern "C" cudaError_t wsb_launch_gprof(const wsb::EventDesc& ev, const wsb::Uni
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const unsigned groups = (max_units + 15) / 16;
-    const unsigned blocks = (groups + wsb::kGpWarps - 1) / wsb::kGpWarps;  // one group per warp
-    (void)sms;
+    // persistent warps (a few groups each, the next group's records in flight)
+    const unsigned blocks = std::min((groups + wsb::kGpWarps - 1) / wsb::kGpWarps, (unsigned)sms * 6u);
     const dim3 grid(blocks, (unsigned)ev.n_planes);
     wsb::k_gprof<<<grid, 32 * wsb::kGpWarps, smem, s>>>(ev, recs, pool);
     return cudaGetLastError();
