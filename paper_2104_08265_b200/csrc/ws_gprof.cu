@@ -20,6 +20,7 @@ namespace wsb {
 
 constexpr int kGpWarps = 4;
 constexpr int kGpPre = 32;  // kernel taps staged before index 0 (j - k >= -31)
+constexpr int kGpPost = 16; // taps past the last tile (the paired tile loop's spare tile)
 
 __device__ __forceinline__ uint32_t tf32_rna(float x)
 {
@@ -37,6 +38,66 @@ __device__ __forceinline__ void mma_tf32(float* c, const uint32_t* a, uint32_t b
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+// The n tiles (8 output taps each) of one 16-unit group with KS k steps. B
+// fragments depend on n - ks only, so a window of the last KS fragments
+// slides along n (one new fragment = 4 shared loads per tile); the three
+// TF32 passes accumulate into one chain per tile.
+template <int KS>
+__device__ __forceinline__ void gp_tiles(const uint32_t* hh, const uint32_t* hl, const uint32_t (*ah)[4],
+                                         const uint32_t (*al)[4], int nt_n, int gq, int tq, const bool* mine,
+                                         const int* lp, float* const* gp, float* gmax)
+{
+    // fragment for m = n - ks: b0 (k = tq, j = gq) = h[8 m + gq - tq], b1 = h[8 m + gq - tq - 4]
+    uint32_t bh0[KS], bh1[KS], bl0[KS], bl1[KS];
+    const int x0 = gq - tq + kGpPre;
+#pragma unroll
+    for (int i = 0; i + 1 < KS; ++i) {  // the window as of n = -1: slot i holds m = -1 - i (zero-padded taps)
+        const int x = x0 - 8 * (i + 1);
+        bh0[i] = hh[x];
+        bh1[i] = hh[x - 4];
+        bl0[i] = hl[x];
+        bl1[i] = hl[x - 4];
+    }
+    // two tiles per iteration (independent MMA chains); an odd count computes
+    // one spare tile past the end (padded taps, stores predicated off)
+#pragma unroll 1
+    for (int n = 0; n < nt_n; n += 2) {
+        float c[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+#pragma unroll
+            for (int i = KS - 1; i > 0; --i) {
+                bh0[i] = bh0[i - 1];
+                bh1[i] = bh1[i - 1];
+                bl0[i] = bl0[i - 1];
+                bl1[i] = bl1[i - 1];
+            }
+            const int x = x0 + 8 * (n + t);
+            bh0[0] = hh[x];
+            bh1[0] = hh[x - 4];
+            bl0[0] = hl[x];
+            bl1[0] = hl[x - 4];
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) {
+                mma_tf32(c[t], ah[ks], bh0[ks], bh1[ks]);
+                mma_tf32(c[t], ah[ks], bl0[ks], bl1[ks]);
+                mma_tf32(c[t], al[ks], bh0[ks], bh1[ks]);
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            // C (16 x 8): c0, c1 -> row gq, taps 8n + 2tq, +1; c2, c3 -> row gq + 8
+            const int j = 8 * (n + t) + 2 * tq;
+            if (mine[0] && j < lp[0]) *reinterpret_cast<float2*>(gp[0] + j) = make_float2(c[t][0], c[t][1]);
+            if (mine[1] && j < lp[1]) *reinterpret_cast<float2*>(gp[1] + j) = make_float2(c[t][2], c[t][3]);
+            if (n + t < nt_n) {
+                gmax[0] = fmaxf(gmax[0], fmaxf(fabsf(c[t][0]), fabsf(c[t][1])));
+                gmax[1] = fmaxf(gmax[1], fmaxf(fabsf(c[t][2]), fabsf(c[t][3])));
+            }
+        }
+    }
+}
+
 __global__ void __launch_bounds__(32 * kGpWarps)
 k_gprof(const EventDesc ev, const UnitRec* __restrict__ recs, uint32_t* __restrict__ pool)
 {
@@ -47,8 +108,8 @@ k_gprof(const EventDesc ev, const UnitRec* __restrict__ recs, uint32_t* __restri
     // kernel tap i, -kGpPre <= i < ntap, split into TF32 hi + lo parts
     extern __shared__ uint32_t s_hk[];
     uint32_t* hh = s_hk;
-    uint32_t* hl = s_hk + (ntap + kGpPre);
-    for (int x = threadIdx.x; x < ntap + kGpPre; x += blockDim.x) {
+    uint32_t* hl = s_hk + (ntap + kGpPre + kGpPost);
+    for (int x = threadIdx.x; x < ntap + kGpPre + kGpPost; x += blockDim.x) {
         const float v = __ldg(&P.kern[x - kGpPre]);  // zero-padded by kKernPad >= 192 taps
         const uint32_t hi = tf32_rna(v);
         hh[x] = hi;
@@ -132,28 +193,11 @@ k_gprof(const EventDesc ev, const UnitRec* __restrict__ recs, uint32_t* __restri
             }
         }
         float gmax[2] = {0.0f, 0.0f};
-#pragma unroll 1
-        for (int n = 0; n < nt_n; ++n) {
-            // three independent accumulation chains (hi.hi, hi.lo, lo.hi)
-            float c[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f}, c2[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-            for (int ks = 0; ks < 4; ++ks) {
-                if (ks >= ks_n) break;
-                // B (col-major 8 x 8): b0 (k = tq, j = gq), b1 (k = tq + 4, j = gq); T[k][j] = h[j - k]
-                const int x = 8 * n + gq - 8 * ks - tq + kGpPre;
-                const uint32_t bh0 = hh[x], bh1 = hh[x - 4], bl0 = hl[x], bl1 = hl[x - 4];
-                mma_tf32(c, ah[ks], bh0, bh1);
-                mma_tf32(c1, ah[ks], bl0, bl1);
-                mma_tf32(c2, al[ks], bh0, bh1);
-            }
-#pragma unroll
-            for (int e = 0; e < 4; ++e) c[e] += c1[e] + c2[e];
-            // C (16 x 8): c0, c1 -> row gq, taps 8n + 2tq, +1; c2, c3 -> row gq + 8
-            const int j = 8 * n + 2 * tq;
-            if (mine[0] && j < lp[0]) *reinterpret_cast<float2*>(gp[0] + j) = make_float2(c[0], c[1]);
-            if (mine[1] && j < lp[1]) *reinterpret_cast<float2*>(gp[1] + j) = make_float2(c[2], c[3]);
-            gmax[0] = fmaxf(gmax[0], fmaxf(fabsf(c[0]), fabsf(c[1])));
-            gmax[1] = fmaxf(gmax[1], fmaxf(fabsf(c[2]), fabsf(c[3])));
+        switch (ks_n) {
+            case 1: gp_tiles<1>(hh, hl, ah, al, nt_n, gq, tq, mine, lp, gp, gmax); break;
+            case 2: gp_tiles<2>(hh, hl, ah, al, nt_n, gq, tq, mine, lp, gp, gmax); break;
+            case 3: gp_tiles<3>(hh, hl, ah, al, nt_n, gq, tq, mine, lp, gp, gmax); break;
+            default: gp_tiles<4>(hh, hl, ah, al, nt_n, gq, tq, mine, lp, gp, gmax); break;
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -206,7 +250,7 @@ extern "C" cudaError_t wsb_launch_gprof(const wsb::EventDesc& ev, const wsb::Uni
         }
     if (max_units == 0) return cudaSuccess;
     const int ntap = (max_lags + 62) & ~31;
-    const size_t smem = 2 * sizeof(uint32_t) * (size_t)(ntap + wsb::kGpPre);
+    const size_t smem = 2 * sizeof(uint32_t) * (size_t)(ntap + wsb::kGpPre + wsb::kGpPost);
     static unsigned long long ready = 0;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
