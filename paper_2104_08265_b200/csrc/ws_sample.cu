@@ -9,6 +9,8 @@
 
 namespace wsb {
 
+__device__ __forceinline__ int lane_id() { return (int)(threadIdx.x & 31); }
+
 constexpr double kInvSqrt2 = 0.70710678118654752440084436210485;
 
 struct Footprint {
@@ -454,20 +456,22 @@ __global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ rec
                              const uint32_t* __restrict__ pool, unsigned* __restrict__ err)
 {
     const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
-    if (u >= ev.total_units) return;
-    if (off[ev.total_bands] > ev.list_cap) {
+    if (off[ev.total_bands] > ev.list_cap) {  // grid-uniform
         if (u == 0) atomicOr(err, kErrRange);
         return;
     }
-    const UnitRec rec = recs[u];
-    if (rec.w0 < 0) return;
-    const PlaneDesc& P = ev.p[plane_of_unit(ev, u)];
-    if (!P.direct) {
+    // no early exits below: the warp-collective tile-slot allocation needs every lane
+    bool live = u < ev.total_units;
+    UnitRec rec{};
+    if (live) rec = recs[u];
+    live = live && rec.w0 >= 0;
+    const PlaneDesc& P = ev.p[plane_of_unit(ev, live ? u : 0)];
+    if (live && !P.direct) {
         for_each_bin(P, rec.w0, rec.n_w, rec.t0, rec.n_t, [&](int c) {
             const uint32_t b = P.band_base + c;
             list[off[b] + atomicAdd(&fill[b], 1u)] = rec;  // full record: k_conv streams the list
         });
-        return;
+        live = false;
     }
     const int L = rec.n_t + P.n_lags - 1;
     int ts = rec.t0 + P.lo_lag;
@@ -480,8 +484,8 @@ __global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ rec
     const int n_rows = stencil ? rec.n_w + 2 * P.h : rec.n_w;
     const bool simple = lo_row >= 0 && lo_row + n_rows <= P.W;
     const float* prof = reinterpret_cast<const float*>(pool + rec.pool) + (stencil ? rec.n_w : 0);
-    for_each_bin(P, rec.w0, rec.n_w, rec.t0, rec.n_t, [&](int c) {
-        const uint32_t b = P.band_base + c;
+    // the entry for tile (row group c / n_windows, window c % n_windows)
+    auto make_entry = [&](int c) {
         const int r0 = (c / P.n_windows) * kTileRows, nr = min(kTileRows, P.W - r0);
         TEnt d;
         d.tsL = (uint32_t)ts | ((uint32_t)L << 16);
@@ -514,7 +518,53 @@ __global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ rec
             }
         }
         d.rows = (uint32_t)rlo | ((uint32_t)max(rhi, rlo) << 8);
-        tlist[off[b] + atomicAdd(&fill[b], 1u)] = d;
+        return d;
+    };
+    // common case (rows not wrapping, <= 4 row groups x <= 2 windows): all the
+    // slot atomics issued back to back before any entry is written, instead of
+    // one dependent global round trip per entry
+    const uint32_t wm = span_windows(ts, L, P.N, P.n_windows);
+    const int g0 = lo_row / kTileRows, g1 = (lo_row + n_rows - 1) / kTileRows;
+    const bool fast = live && simple && __popc(wm) <= 2 && g1 - g0 < 4;
+    const unsigned act = __ballot_sync(0xffffffffu, fast);
+    if (fast) {
+        {
+            const int w0 = __ffs(wm) - 1, w1 = __popc(wm) > 1 ? 31 - __clz(wm) : -1;
+            // consecutive depos (one track) mostly share tiles: one atomic per
+            // distinct tile of the warp, ranks by match mask
+            uint32_t slot[8];
+            const unsigned lt = (1u << lane_id()) - 1u;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int g = g0 + (k >> 1), w = (k & 1) ? w1 : w0;
+                const bool valid = g <= g1 && w >= 0;
+                const unsigned vm = __ballot_sync(act, valid);
+                slot[k] = 0u;
+                if (valid) {
+                    const uint32_t b = P.band_base + g * P.n_windows + w;
+                    const unsigned peers = __match_any_sync(vm, b);
+                    const int leader = __ffs(peers) - 1;
+                    uint32_t base = 0;
+                    if (lane_id() == leader) base = atomicAdd(&fill[b], (unsigned)__popc(peers));
+                    base = __shfl_sync(peers, base, leader);
+                    slot[k] = base + __popc(peers & lt);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int g = g0 + (k >> 1), w = (k & 1) ? w1 : w0;
+                if (g <= g1 && w >= 0) {
+                    const int c = g * P.n_windows + w;
+                    tlist[off[P.band_base + c] + slot[k]] = make_entry(c);
+                }
+            }
+            return;
+        }
+    }
+    if (!live) return;
+    for_each_bin(P, rec.w0, rec.n_w, rec.t0, rec.n_t, [&](int c) {
+        const uint32_t b = P.band_base + c;
+        tlist[off[b] + atomicAdd(&fill[b], 1u)] = make_entry(c);
     });
 }
 
