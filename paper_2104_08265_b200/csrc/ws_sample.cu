@@ -404,27 +404,37 @@ k_sample_off(const EventDesc ev, UnitRec* __restrict__ recs, uint32_t* __restric
 }
 
 // Exclusive scan of bin counts (single block); resets the fill cursors.
-__global__ void k_scan_bands(const uint32_t* __restrict__ count, uint32_t* __restrict__ off, uint32_t* __restrict__ fill,
-                             uint32_t n)
+__global__ void __launch_bounds__(1024) k_scan_bands(const uint32_t* __restrict__ count, uint32_t* __restrict__ off,
+                                                    uint32_t* __restrict__ fill, uint32_t n)
 {
+    // one pass: each thread scans kPer consecutive counts in registers, the
+    // block scans the 1024 partial sums (two warp-shuffle levels), carry
+    // across passes only for n > 1024 * kPer
+    constexpr int kPer = 8;
     __shared__ uint32_t warp_sums[32];
     __shared__ uint32_t carry;
     if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (uint32_t base = 0; base < n; base += blockDim.x) {
-        const uint32_t i = base + threadIdx.x;
-        const uint32_t v = i < n ? count[i] : 0u;
-        uint32_t x = v;
+#pragma unroll 1
+    for (uint32_t base = 0; base < n; base += 1024u * kPer) {
+        const uint32_t i0 = base + threadIdx.x * kPer;
+        uint32_t v[kPer], sum = 0;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            v[k] = i0 + k < n ? __ldg(count + i0 + k) : 0u;
+            sum += v[k];
+        }
+        uint32_t x = sum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
             if (lane >= o) x += y;
         }
+        __syncthreads();  // carry / warp_sums of the previous pass consumed
         if (lane == 31) warp_sums[wid] = x;
         __syncthreads();
         if (wid == 0) {
-            uint32_t t = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0u;
+            uint32_t t = warp_sums[lane];
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
@@ -433,15 +443,18 @@ __global__ void k_scan_bands(const uint32_t* __restrict__ count, uint32_t* __res
             warp_sums[lane] = t;
         }
         __syncthreads();
-        const uint32_t excl = carry + (wid ? warp_sums[wid - 1] : 0u) + x - v;
-        if (i < n) {
-            off[i] = excl;
-            fill[i] = 0;
-        }
+        uint32_t run = carry + (wid ? warp_sums[wid - 1] : 0u) + x - sum;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k)
+            if (i0 + k < n) {
+                off[i0 + k] = run;
+                fill[i0 + k] = 0;
+                run += v[k];
+            }
         __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) carry = excl + v;
-        __syncthreads();
+        if (threadIdx.x == 1023) carry = run;
     }
+    __syncthreads();
     if (threadIdx.x == 0) off[n] = carry;
 }
 
