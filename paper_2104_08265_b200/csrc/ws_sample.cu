@@ -630,6 +630,154 @@ __global__ void k_fluctuate(const EventDesc ev, const UnitRec* __restrict__ recs
         atomicAdd(&grid[(size_t)(rec.w0 + n_w - 1) * N + rec.t0 + n_t - 1], (float)remaining);
 }
 
+// Exact fluctuation (fluctuate_sequential with the reference binomial), the
+// same per-depo operation sequence as k_fluctuate, scheduled for SIMT: the
+// nested loop (bins x CDF-walk steps) diverges per bin (the warp pays the
+// longest walk of every bin), so each lane runs a state machine instead -
+// lanes walk their current draw one step per iteration and only when a
+// quarter of the warp's live lanes have finished their draws does the warp
+// set up the next draws (RNG, pmf seed) together. The integer grid is
+// unchanged (same draws, same order per depo; float atomics exact < 2^24).
+__global__ void __launch_bounds__(128) k_fluctuate_exact(const EventDesc ev, const UnitRec* __restrict__ recs,
+                                                          const uint32_t* __restrict__ pool)
+{
+    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    bool done = u >= ev.total_units;
+    UnitRec rec{};
+    if (!done) rec = recs[u];
+    done = done || rec.w0 < 0;
+    const PlaneDesc& P = ev.p[plane_of_unit(ev, done ? 0 : u)];
+    ws_depo d{};
+    if (!done) d = P.depos[u - P.unit_base];
+    const double* wv = reinterpret_cast<const double*>(pool + rec.pool);
+    const double* tv = wv + rec.n_w;
+    const int n_t = rec.n_t;
+    double norm = 0.0;
+    if (!done) {
+        double total = 0.0;
+        for (int w = 0; w < rec.n_w; ++w) {
+            const double pw = wv[w];
+            for (int t = 0; t < n_t; ++t) total += pw * tv[t];
+        }
+        norm = 1.0 / total;
+    }
+    Rng src;
+    src.init(ev.rng_mode, ev.seed, (uint64_t)d.id);
+    float* grid = P.charge_out;
+    const int N = P.N;
+    const int last = rec.n_w * n_t - 1;
+    int64_t remaining = d.q;
+    double p_rem = 1.0, pi = 0.0;
+    int b = 0;
+    // the draw in progress (invert_binomial_cdf's loop state)
+    bool walking = false, flip = false;
+    int64_t n = 0;
+    double odds = 0.0, pmf = 0.0, cdf = 0.0, uu = 0.0, kd = 0.0, nd = 0.0, nk = 0.0, k1 = 0.0;
+
+    auto cell = [&](int bin) {
+        const int w = bin / n_t, t = bin - w * n_t;
+        return &grid[(size_t)(rec.w0 + w) * N + rec.t0 + t];
+    };
+    auto commit = [&](int64_t k) {  // bin b drew k electrons
+        if (k) atomicAdd(cell(b), (float)k);
+        remaining -= k;
+        p_rem -= pi;
+        ++b;
+    };
+    // draws until one needs a CDF walk (or the depo is finished)
+    auto setup = [&]() {
+        while (!done && !walking) {
+            if (remaining == 0 || b >= last) {
+                if (remaining) atomicAdd(cell(last), (float)remaining);  // the last bin takes the rest
+                done = true;
+                break;
+            }
+            const int w = b / n_t, t = b - w * n_t;
+            pi = (wv[w] * tv[t]) * norm;
+            double p = 1.0;
+            if (p_rem > 0.0) {
+                p = pi / p_rem;
+                p = p < 0.0 ? 0.0 : (p > 1.0 ? 1.0 : p);
+            }
+            // binomial (rng.cpp:174-193)
+            n = remaining;
+            if (p == 0.0) {
+                commit(0);
+                continue;
+            }
+            if (p == 1.0) {
+                commit(n);
+                continue;
+            }
+            const double mean = __dmul_rn((double)n, p);
+            const double var = __dmul_rn(mean, __dsub_rn(1.0, p));
+            const double q1 = __dsub_rn(1.0, p);
+            const double mn = (q1 < p) ? q1 : p;
+            if (__dmul_rn((double)n, mn) > 1e6) {
+                const double k = round(__dadd_rn(mean, __dmul_rn(sqrt(var), src.normal())));
+                commit(k < 0.0 ? 0 : (k > (double)n ? n : (int64_t)k));
+                continue;
+            }
+            uu = src.uniform();
+            flip = p > 0.5;
+            const double pp = flip ? q1 : p;
+            // invert_binomial_cdf (rng.cpp:146-170): the pmf seed
+            odds = __ddiv_rn(pp, __dsub_rn(1.0, pp));
+            int64_t k = 0;
+            const double log_pmf0 = __dmul_rn((double)n, log1p(-pp));
+            if (log_pmf0 > -700.0) {
+                pmf = exp_ref(log_pmf0);
+            } else {
+                const double m2 = __dmul_rn((double)n, pp);
+                const double sd = sqrt(__dmul_rn(m2, __dsub_rn(1.0, pp)));
+                const int64_t k0 = (int64_t)__dsub_rn(m2, __dmul_rn(30.0, sd));
+                k = k0 > 0 ? k0 : 0;
+                const double nn = (double)n, kk = (double)k;
+                double e = __dsub_rn(lgamma(__dadd_rn(nn, 1.0)), lgamma(__dadd_rn(kk, 1.0)));
+                e = __dsub_rn(e, lgamma(__dadd_rn(__dsub_rn(nn, kk), 1.0)));
+                e = __dadd_rn(e, __dmul_rn(kk, log(pp)));
+                e = __dadd_rn(e, __dmul_rn(__dsub_rn(nn, kk), log1p(-pp)));
+                pmf = exp_ref(e);
+            }
+            cdf = pmf;
+            if (cdf <= uu && k < n) {
+                walking = true;
+                kd = (double)k;
+                nd = (double)n;
+                nk = (double)(n - k);  // exact integers below 2^53: the reference's casts
+                k1 = (double)(k + 1);
+            } else {
+                commit(flip ? n - k : k);
+            }
+        }
+    };
+
+#pragma unroll 1
+    for (;;) {
+        setup();
+        const unsigned alive = __ballot_sync(0xffffffffu, !done);
+        if (!alive) break;
+        const int quorum = max(1, __popc(alive) >> 2);
+#pragma unroll 1
+        for (;;) {
+            if (walking) {
+                pmf = __dmul_rn(pmf, __ddiv_rn(__dmul_rn(odds, nk), k1));
+                kd += 1.0;
+                cdf = __dadd_rn(cdf, pmf);
+                nk -= 1.0;
+                k1 += 1.0;
+                if (!(cdf <= uu && kd < nd)) {
+                    walking = false;
+                    const int64_t k = (int64_t)kd;
+                    commit(flip ? n - k : k);
+                }
+            }
+            const unsigned wk = __ballot_sync(0xffffffffu, walking);
+            if (wk == 0 || __popc(alive & ~wk) >= quorum) break;
+        }
+    }
+}
+
 }  // namespace wsb
 
 extern "C" cudaError_t wsb_launch_sample(const wsb::EventDesc& ev, wsb::UnitRec* recs, uint32_t* pool, uint32_t pool_cap,
@@ -667,6 +815,9 @@ extern "C" cudaError_t wsb_launch_fluctuate(const wsb::EventDesc& ev, const wsb:
                                             const uint32_t* order, cudaStream_t s)
 {
     if (ev.total_units == 0) return cudaSuccess;
-    wsb::k_fluctuate<<<(ev.total_units + 127) / 128, 128, 0, s>>>(ev, recs, pool, order);
+    if (ev.approx)
+        wsb::k_fluctuate<<<(ev.total_units + 127) / 128, 128, 0, s>>>(ev, recs, pool, order);
+    else
+        wsb::k_fluctuate_exact<<<(ev.total_units + 127) / 128, 128, 0, s>>>(ev, recs, pool);
     return cudaGetLastError();
 }
