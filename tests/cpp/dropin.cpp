@@ -3,6 +3,7 @@
 // row-major) to argv[1]; exit code 0 on success. Built and run by
 // tests/test_gpu_parity.py::test_cpp_dropin.
 #include <cstdio>
+#include <string>
 #include <vector>
 
 #include "wiresim_b200.hpp"
@@ -36,6 +37,26 @@ int main(int argc, char** argv)
     } catch (const std::exception& e) {
         std::fprintf(stderr, "error: %s\n", e.what());
         return 1;
+    }
+    // depo CSV ingestion (load_depos, pipeline.cpp:226-262) through the C++ mirror
+    {
+        const std::string csv = std::string(argv[1]) + ".csv";
+        if (ws_save_depos_csv(csv.c_str(), reinterpret_cast<const ws_depo*>(depos.data()), depos.size()) != WS_OK)
+            return 5;
+        const std::vector<wiresim_b200::Depo> back = wiresim_b200::load_depos<wiresim_b200::Depo>(csv);
+        if (back.size() != depos.size()) return 6;
+        for (std::size_t i = 0; i < back.size(); ++i)
+            if (back[i].t != depos[i].t || back[i].x != depos[i].x || back[i].q != depos[i].q ||
+                back[i].sigma_t != depos[i].sigma_t || back[i].sigma_x != depos[i].sigma_x)
+                return 7;
+        FILE* f = std::fopen(csv.c_str(), "w");
+        std::fputs("id,t,x\n", f);
+        std::fclose(f);
+        try {
+            wiresim_b200::load_depos<wiresim_b200::Depo>(csv);
+            return 8;
+        } catch (const std::runtime_error&) {
+        }
     }
     // the reference's exception categories cross back as the same C++ types
     try {
