@@ -29,6 +29,7 @@ SOURCES = {
     "ws_conv.cu": [],
     "ws_direct.cu": [],
     "ws_gprof.cu": [],
+    "ws_gprof_umma.cu": [],
     "ws_noise.cu": ["--fmad=false"],
     "ws_sigproc.cu": [],
     "ws_api.cu": [],

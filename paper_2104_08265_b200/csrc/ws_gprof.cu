@@ -15,6 +15,7 @@
 #include "ws_common.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace wsb {
 
@@ -238,9 +239,23 @@ k_gprof(const EventDesc ev, const UnitRec* __restrict__ recs, uint32_t* __restri
 
 }  // namespace wsb
 
+extern "C" int wsb_gprof_umma_n(const wsb::EventDesc& ev);
+extern "C" cudaError_t wsb_launch_gprof_umma(const wsb::EventDesc& ev, const wsb::UnitRec* recs, uint32_t* pool,
+                                             int N, cudaStream_t s);
+
 extern "C" cudaError_t wsb_launch_gprof(const wsb::EventDesc& ev, const wsb::UnitRec* recs, uint32_t* pool,
                                         cudaStream_t s)
 {
+    // tcgen05 path (ws_gprof_umma.cu) unless a kernel is too long for it or
+    // WS_GPROF_MMASYNC=1 selects the warp-level mma.sync kernel below
+    static const bool mmasync = [] {
+        const char* v = getenv("WS_GPROF_MMASYNC");
+        return v && v[0] == '1';
+    }();
+    if (!mmasync) {
+        const int N = wsb_gprof_umma_n(ev);
+        if (N > 0) return wsb_launch_gprof_umma(ev, recs, pool, N, s);
+    }
     uint32_t max_units = 0;
     int max_lags = 0;
     for (int i = 0; i < ev.n_planes; ++i)

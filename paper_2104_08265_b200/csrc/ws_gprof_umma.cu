@@ -1,0 +1,277 @@
+// Per-depo response profiles on the 5th-generation tensor cores (tcgen05).
+//
+// g_u = tv_u (*) h for 128 units u at a time is one GEMM
+//   G[128 x N] = TV[128 x 32] . T[32 x N],  T[k][j] = h[j - k]   (Toeplitz)
+// (N = ceil32(n_lags + 31) output taps, n_t <= 32 tick taps), issued by one
+// thread as tcgen05.mma kind::tf32 with the fp32 accumulator in TMEM. TF32
+// operands in the 3-pass split (hi.hi + hi.lo + lo.hi, all into the same
+// accumulator: ~fp32 accuracy), 12 MMAs of 128 x N x 8 per tile. Operands are
+// staged in shared memory in the canonical K-major no-swizzle layout (core
+// matrices of 8 rows x 16 bytes); the Toeplitz T is rebuilt per CTA from the
+// plane's zero-padded kernel. The epilogue reads the accumulator back with
+// tcgen05.ld (warp w owns TMEM lanes 32w..32w+31 = units) and writes each
+// unit's ceil32(L) taps. This replaces the warp-level mma.sync kernel
+// (k_gprof), whose TF32 rate on sm_100 was its limiter. Units with n_t > 32
+// compute their profile with a scalar loop in the epilogue.
+#include "ws_common.cuh"
+
+#include <algorithm>
+
+namespace wsb {
+
+constexpr int kUmM = 128;  // units per tile (UMMA M)
+constexpr int kUmK = 32;   // tick-profile taps (UMMA K = 4 steps of 8)
+constexpr int kUmThreads = 128;
+
+__device__ __forceinline__ uint32_t um_tf32(float x)
+{
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return r;
+}
+
+// byte offset of element (row r, k) in a K-major SWIZZLE_NONE operand of R rows:
+// core matrix (k / 4, r / 8) of 8 rows x 16 bytes, K-chunks R/8 core matrices apart
+__device__ __forceinline__ uint32_t um_off(int r, int kc, int R) { return ((kc * (R >> 3) + (r >> 3)) << 7) + ((r & 7) << 4); }
+
+// shared-memory matrix descriptor (sm100): start, leading (K) and stride (M/N)
+// byte offsets >> 4, version 1, no swizzle
+__device__ __forceinline__ uint64_t um_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo)
+{
+    return (uint64_t)((saddr >> 4) & 0x3fffu) | ((uint64_t)((lbo >> 4) & 0x3fffu) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3fffu) << 32) | (1ull << 46);
+}
+
+__device__ __forceinline__ void um_mma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accum)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accum), "r"(0u), "r"(0u), "r"(0u), "r"(0u));
+}
+
+__global__ void __launch_bounds__(kUmThreads) k_gprof_umma(const EventDesc ev, const UnitRec* __restrict__ recs,
+                                                           uint32_t* __restrict__ pool, int N)
+{
+    const PlaneDesc& P = ev.p[blockIdx.y];
+    if (!P.direct || P.n_units == 0) return;
+    const int nl = P.n_lags;
+    const int tid = threadIdx.x, warp = tid >> 5;
+
+    // layout: A hi | A lo (128 x 32 each) | B hi | B lo (N x 32 each), 128-byte aligned
+    extern __shared__ __align__(128) unsigned char um_smem[];
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(um_smem);
+    const uint32_t a_hi = sbase, a_lo = a_hi + kUmM * kUmK * 4;
+    const uint32_t b_hi = a_lo + kUmM * kUmK * 4, b_lo = b_hi + (uint32_t)N * kUmK * 4;
+    __shared__ uint32_t s_tmem;
+    __shared__ __align__(8) unsigned long long s_bar;
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar);
+
+    // TMEM accumulator (N fp32 columns x 128 lanes) and the completion barrier
+    if (warp == 0) {
+        const uint32_t cols = N <= 32 ? 32u : N <= 64 ? 64u : N <= 128 ? 128u : 256u;
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(&s_tmem)),
+                     "r"(cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(bar));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+
+    // B = the plane's Toeplitz kernel, hi and lo TF32 parts: row n, taps k..k+3
+    for (int i = tid; i < N * (kUmK / 4); i += kUmThreads) {
+        const int n = i % N, kc = i / N;
+        uint32_t hi[4], lo[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float v = __ldg(&P.kern[n - (4 * kc + q)]);  // zero-padded both sides
+            hi[q] = um_tf32(v);
+            lo[q] = um_tf32(v - __uint_as_float(hi[q]));
+        }
+        const uint32_t o = um_off(n, kc, N);
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(b_hi + o), "r"(hi[0]), "r"(hi[1]), "r"(hi[2]),
+                     "r"(hi[3]));
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(b_lo + o), "r"(lo[0]), "r"(lo[1]), "r"(lo[2]),
+                     "r"(lo[3]));
+    }
+    // TMEM address to all threads
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = s_tmem;
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kUmM >> 4) << 24);
+    const uint32_t lbo_a = (kUmM / 8) * 128, lbo_b = (uint32_t)(N / 8) * 128;
+    const uint32_t trow = tmem + ((uint32_t)(32 * warp) << 16);
+    const int n_tiles = (int)((P.n_units + kUmM - 1) / kUmM);
+
+    // persistent over this plane's tiles; B (and the TMEM allocation) stay
+    // this thread's unit of a tile (row tid): record and tick profile (0 past
+    // n_t; wide units 0); the next tile's are loaded while this one's
+    // accumulator drains
+    auto fetch = [&](int tile, UnitRec& rec, float* vals) {
+        const uint32_t ul = (uint32_t)tile * kUmM + (uint32_t)tid;
+        rec = UnitRec{};
+        rec.w0 = -1;
+        if (tile < n_tiles && ul < P.n_units) rec = recs[P.unit_base + ul];
+        const bool ok = rec.w0 >= 0 && rec.n_t <= kUmK;
+        const float* t = reinterpret_cast<const float*>(pool + rec.pool + (uint32_t)(rec.n_w + unit_n_eff(P, rec.n_w)));
+#pragma unroll
+        for (int k = 0; k < kUmK; ++k) vals[k] = ok && k < rec.n_t ? __ldg(t + k) : 0.0f;
+    };
+    UnitRec rec_n;
+    float vals_n[kUmK];
+    fetch(blockIdx.x, rec_n, vals_n);
+#pragma unroll 1
+    for (int tile = blockIdx.x, it = 0; tile < n_tiles; tile += gridDim.x, ++it) {
+        const UnitRec rec = rec_n;
+        float vals[kUmK];
+#pragma unroll
+        for (int k = 0; k < kUmK; ++k) vals[k] = vals_n[k];
+        const bool live = rec.w0 >= 0;
+        const float* tv =
+            reinterpret_cast<const float*>(pool + rec.pool + (uint32_t)(rec.n_w + unit_n_eff(P, rec.n_w)));
+        const int nt = live && rec.n_t <= kUmK ? rec.n_t : 0;
+#pragma unroll
+        for (int kc = 0; kc < kUmK / 4; ++kc) {
+            uint32_t hi[4], lo[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float v = vals[4 * kc + q];
+                hi[q] = um_tf32(v);
+                lo[q] = um_tf32(v - __uint_as_float(hi[q]));
+            }
+            const uint32_t o = um_off(tid, kc, kUmM);
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a_hi + o), "r"(hi[0]), "r"(hi[1]),
+                         "r"(hi[2]), "r"(hi[3]));
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a_lo + o), "r"(lo[0]), "r"(lo[1]),
+                         "r"(lo[2]), "r"(lo[3]));
+        }
+        // operands visible to the tensor core (async proxy); the previous
+        // tile's TMEM reads are complete (fence before the barrier)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (tid == 0) {
+            // 3 passes x 4 K steps (8 taps = two 16-byte K chunks per step)
+            const uint32_t as[3] = {a_hi, a_hi, a_lo}, bs[3] = {b_hi, b_lo, b_hi};
+#pragma unroll
+            for (int pass = 0; pass < 3; ++pass)
+#pragma unroll
+                for (int s = 0; s < kUmK / 8; ++s)
+                    um_mma(tmem, um_desc(as[pass] + 2u * s * lbo_a, lbo_a, 128),
+                           um_desc(bs[pass] + 2u * s * lbo_b, lbo_b, 128), idesc, (pass | s) ? 1u : 0u);
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                         : "memory");
+        }
+        fetch(tile + gridDim.x, rec_n, vals_n);  // in flight while the MMAs run
+        {
+            uint32_t done = 0;
+            const uint32_t parity = (uint32_t)(it & 1);
+            while (!done)
+                asm volatile(
+                    "{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                    : "=r"(done)
+                    : "r"(bar), "r"(parity)
+                    : "memory");
+        }
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+
+        // epilogue: accumulator rows -> g (ceil32(L) taps per unit). TMEM gives
+        // lane = unit row; a per-warp shared transpose turns each 16-column
+        // chunk into 8-row x 64-byte float4 stores (full sectors)
+        const int lp = live ? (rec.n_t + nl - 1 + 31) & ~31 : 0;
+        float* g = reinterpret_cast<float*>(pool + rec.goff);
+        const int lane = tid & 31;
+        float* stg = reinterpret_cast<float*>(um_smem + kUmM * kUmK * 4) + warp * (32 * 20);  // A lo area (free now)
+        float* rg[4];
+        int rlp[4];
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr) {
+            const int row = 8 * rr + (lane >> 2);
+            rg[rr] = reinterpret_cast<float*>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(g), row));
+            rlp[rr] = __shfl_sync(0xffffffffu, nt > 0 ? lp : 0, row);
+        }
+        const int cq = 4 * (lane & 3);
+        for (int c0 = 0; c0 < N; c0 += 16) {
+            uint32_t v[16];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+                "%13, %14, %15}, [%16];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                  "=r"(v[15])
+                : "r"(trow + (uint32_t)c0));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                reinterpret_cast<uint4*>(stg + lane * 20)[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            __syncwarp();
+#pragma unroll
+            for (int rr = 0; rr < 4; ++rr) {
+                const int row = 8 * rr + (lane >> 2);
+                const float4 x = *reinterpret_cast<const float4*>(stg + row * 20 + cq);
+                if (c0 + cq < rlp[rr]) *reinterpret_cast<float4*>(rg[rr] + c0 + cq) = x;
+            }
+            __syncwarp();
+        }
+        if (live && rec.n_t > kUmK) {  // wide tick profile: scalar
+            const int L = rec.n_t + nl - 1;
+            for (int j = 0; j < lp; ++j) {
+                const int k0 = j - nl + 1 > 0 ? j - nl + 1 : 0, k1 = j < rec.n_t - 1 ? j : rec.n_t - 1;
+                float sum = 0.0f;
+                for (int k = k0; k <= k1; ++k) sum = __fmaf_rn(__ldg(tv + k), __ldg(&P.kern[j - k]), sum);
+                g[j] = j < L ? sum : 0.0f;
+            }
+        }
+        __syncthreads();  // the transpose staging (A lo area) is free for the next tile's operands
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t cols = N <= 32 ? 32u : N <= 64 ? 64u : N <= 128 ? 128u : 256u;
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(cols));
+    }
+}
+
+}  // namespace wsb
+
+// N (output taps per unit) of the UMMA path for the event, or 0 when a plane's
+// kernel is too long for it (then k_gprof runs)
+extern "C" int wsb_gprof_umma_n(const wsb::EventDesc& ev)
+{
+    int max_lags = 0;
+    for (int i = 0; i < ev.n_planes; ++i)
+        if (ev.p[i].direct) max_lags = max_lags > ev.p[i].n_lags ? max_lags : ev.p[i].n_lags;
+    const int N = (max_lags + 31 + 31) & ~31;
+    return N <= 256 ? N : 0;
+}
+
+extern "C" cudaError_t wsb_launch_gprof_umma(const wsb::EventDesc& ev, const wsb::UnitRec* recs, uint32_t* pool,
+                                             int N, cudaStream_t s)
+{
+    uint32_t max_units = 0;
+    for (int i = 0; i < ev.n_planes; ++i)
+        if (ev.p[i].direct) max_units = max_units > ev.p[i].n_units ? max_units : ev.p[i].n_units;
+    if (max_units == 0) return cudaSuccess;
+    const size_t smem = (size_t)2 * wsb::kUmK * 4 * (wsb::kUmM + (size_t)N);
+    static unsigned long long ready = 0;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (!(ready & (1ull << dev))) {
+        e = cudaFuncSetAttribute(wsb::k_gprof_umma, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+        if (e != cudaSuccess) return e;
+        ready |= 1ull << dev;
+    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned tiles = (max_units + wsb::kUmM - 1) / wsb::kUmM;
+    // persistent: two CTAs per SM over the planes (B staged once per CTA)
+    const unsigned per_plane = std::max(1u, (unsigned)(2 * sms) / (unsigned)ev.n_planes);
+    const dim3 grid(std::min(tiles, per_plane), (unsigned)ev.n_planes);
+    wsb::k_gprof_umma<<<grid, wsb::kUmThreads, smem, s>>>(ev, recs, pool, N);
+    return cudaGetLastError();
+}
