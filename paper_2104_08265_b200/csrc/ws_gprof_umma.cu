@@ -21,7 +21,7 @@ namespace wsb {
 
 constexpr int kUmM = 128;  // units per tile (UMMA M)
 constexpr int kUmK = 32;   // tick-profile taps (UMMA K = 4 steps of 8)
-constexpr int kUmThreads = 128;
+constexpr int kUmThreads = 256;  // two warps per TMEM lane quadrant
 
 __device__ __forceinline__ uint32_t um_tf32(float x)
 {
@@ -103,46 +103,50 @@ __global__ void __launch_bounds__(kUmThreads) k_gprof_umma(const EventDesc ev, c
     const uint32_t tmem = s_tmem;
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kUmM >> 4) << 24);
     const uint32_t lbo_a = (kUmM / 8) * 128, lbo_b = (uint32_t)(N / 8) * 128;
-    const uint32_t trow = tmem + ((uint32_t)(32 * warp) << 16);
+    // thread -> unit row (tid & 127) and half (tid >> 7): K taps 16 h..16 h+15
+    // when staging, output columns [h N/2, (h+1) N/2) in the epilogue
+    const int row = tid & (kUmM - 1), half = tid >> 7;
+    const uint32_t trow = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
     const int n_tiles = (int)((P.n_units + kUmM - 1) / kUmM);
 
     // persistent over this plane's tiles; B (and the TMEM allocation) stay
     // this thread's unit of a tile (row tid): record and tick profile (0 past
     // n_t; wide units 0); the next tile's are loaded while this one's
     // accumulator drains
+    constexpr int kH = kUmK / 2;
     auto fetch = [&](int tile, UnitRec& rec, float* vals) {
-        const uint32_t ul = (uint32_t)tile * kUmM + (uint32_t)tid;
+        const uint32_t ul = (uint32_t)tile * kUmM + (uint32_t)row;
         rec = UnitRec{};
         rec.w0 = -1;
         if (tile < n_tiles && ul < P.n_units) rec = recs[P.unit_base + ul];
         const bool ok = rec.w0 >= 0 && rec.n_t <= kUmK;
         const float* t = reinterpret_cast<const float*>(pool + rec.pool + (uint32_t)(rec.n_w + unit_n_eff(P, rec.n_w)));
 #pragma unroll
-        for (int k = 0; k < kUmK; ++k) vals[k] = ok && k < rec.n_t ? __ldg(t + k) : 0.0f;
+        for (int k = 0; k < kH; ++k) vals[k] = ok && kH * half + k < rec.n_t ? __ldg(t + kH * half + k) : 0.0f;
     };
     UnitRec rec_n;
-    float vals_n[kUmK];
+    float vals_n[kH];
     fetch(blockIdx.x, rec_n, vals_n);
 #pragma unroll 1
     for (int tile = blockIdx.x, it = 0; tile < n_tiles; tile += gridDim.x, ++it) {
         const UnitRec rec = rec_n;
-        float vals[kUmK];
+        float vals[kH];
 #pragma unroll
-        for (int k = 0; k < kUmK; ++k) vals[k] = vals_n[k];
+        for (int k = 0; k < kH; ++k) vals[k] = vals_n[k];
         const bool live = rec.w0 >= 0;
         const float* tv =
             reinterpret_cast<const float*>(pool + rec.pool + (uint32_t)(rec.n_w + unit_n_eff(P, rec.n_w)));
         const int nt = live && rec.n_t <= kUmK ? rec.n_t : 0;
 #pragma unroll
-        for (int kc = 0; kc < kUmK / 4; ++kc) {
+        for (int kq = 0; kq < kH / 4; ++kq) {
             uint32_t hi[4], lo[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                const float v = vals[4 * kc + q];
+                const float v = vals[4 * kq + q];
                 hi[q] = um_tf32(v);
                 lo[q] = um_tf32(v - __uint_as_float(hi[q]));
             }
-            const uint32_t o = um_off(tid, kc, kUmM);
+            const uint32_t o = um_off(row, (kH / 4) * half + kq, kUmM);
             asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a_hi + o), "r"(hi[0]), "r"(hi[1]),
                          "r"(hi[2]), "r"(hi[3]));
             asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a_lo + o), "r"(lo[0]), "r"(lo[1]),
@@ -185,17 +189,17 @@ __global__ void __launch_bounds__(kUmThreads) k_gprof_umma(const EventDesc ev, c
         const int lp = live ? (rec.n_t + nl - 1 + 31) & ~31 : 0;
         float* g = reinterpret_cast<float*>(pool + rec.goff);
         const int lane = tid & 31;
-        float* stg = reinterpret_cast<float*>(um_smem + kUmM * kUmK * 4) + warp * (32 * 20);  // A lo area (free now)
+        float* stg = reinterpret_cast<float*>(um_smem) + warp * (32 * 20);  // A area (free now)
         float* rg[4];
         int rlp[4];
 #pragma unroll
         for (int rr = 0; rr < 4; ++rr) {
-            const int row = 8 * rr + (lane >> 2);
-            rg[rr] = reinterpret_cast<float*>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(g), row));
-            rlp[rr] = __shfl_sync(0xffffffffu, nt > 0 ? lp : 0, row);
+            const int src = 8 * rr + (lane >> 2);
+            rg[rr] = reinterpret_cast<float*>(__shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(g), src));
+            rlp[rr] = __shfl_sync(0xffffffffu, nt > 0 ? lp : 0, src);
         }
         const int cq = 4 * (lane & 3);
-        for (int c0 = 0; c0 < N; c0 += 16) {
+        for (int c0 = half * (N / 2); c0 < (half + 1) * (N / 2); c0 += 16) {
             uint32_t v[16];
             asm volatile(
                 "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
@@ -211,13 +215,13 @@ __global__ void __launch_bounds__(kUmThreads) k_gprof_umma(const EventDesc ev, c
             __syncwarp();
 #pragma unroll
             for (int rr = 0; rr < 4; ++rr) {
-                const int row = 8 * rr + (lane >> 2);
-                const float4 x = *reinterpret_cast<const float4*>(stg + row * 20 + cq);
+                const int r8 = 8 * rr + (lane >> 2);
+                const float4 x = *reinterpret_cast<const float4*>(stg + r8 * 20 + cq);
                 if (c0 + cq < rlp[rr]) *reinterpret_cast<float4*>(rg[rr] + c0 + cq) = x;
             }
             __syncwarp();
         }
-        if (live && rec.n_t > kUmK) {  // wide tick profile: scalar
+        if (half == 0 && live && rec.n_t > kUmK) {  // wide tick profile: scalar
             const int L = rec.n_t + nl - 1;
             for (int j = 0; j < lp; ++j) {
                 const int k0 = j - nl + 1 > 0 ? j - nl + 1 : 0, k1 = j < rec.n_t - 1 ? j : rec.n_t - 1;
