@@ -674,26 +674,32 @@ __global__ void __launch_bounds__(128) k_fluctuate_exact(const EventDesc ev, con
     int64_t n = 0;
     double odds = 0.0, pmf = 0.0, cdf = 0.0, uu = 0.0, kd = 0.0, nd = 0.0, nk = 0.0, k1 = 0.0;
 
-    auto cell = [&](int bin) {
-        const int w = bin / n_t, t = bin - w * n_t;
-        return &grid[(size_t)(rec.w0 + w) * N + rec.t0 + t];
-    };
+    // bin b = (bw, bt), tracked incrementally (no integer division per draw)
+    int bw = 0, bt = 0;
+    float* cellp = grid + (size_t)rec.w0 * N + rec.t0;  // &grid[w0 + bw][t0 + bt]
     auto commit = [&](int64_t k) {  // bin b drew k electrons
-        if (k) atomicAdd(cell(b), (float)k);
+        if (k) atomicAdd(cellp, (float)k);
         remaining -= k;
         p_rem -= pi;
         ++b;
+        if (++bt == n_t) {
+            bt = 0;
+            ++bw;
+            cellp += N - (n_t - 1);
+        } else {
+            ++cellp;
+        }
     };
     // draws until one needs a CDF walk (or the depo is finished)
     auto setup = [&]() {
         while (!done && !walking) {
             if (remaining == 0 || b >= last) {
-                if (remaining) atomicAdd(cell(last), (float)remaining);  // the last bin takes the rest
+                if (remaining)  // the last bin takes the rest
+                    atomicAdd(&grid[(size_t)(rec.w0 + rec.n_w - 1) * N + rec.t0 + n_t - 1], (float)remaining);
                 done = true;
                 break;
             }
-            const int w = b / n_t, t = b - w * n_t;
-            pi = (wv[w] * tv[t]) * norm;
+            pi = (wv[bw] * tv[bt]) * norm;
             double p = 1.0;
             if (p_rem > 0.0) {
                 p = pi / p_rem;
@@ -757,7 +763,7 @@ __global__ void __launch_bounds__(128) k_fluctuate_exact(const EventDesc ev, con
         setup();
         const unsigned alive = __ballot_sync(0xffffffffu, !done);
         if (!alive) break;
-        const int quorum = max(1, __popc(alive) >> 2);
+        const int quorum = max(1, __popc(alive) >> 1);  // half the live lanes idle: set up together
 #pragma unroll 1
         for (;;) {
             if (walking) {
