@@ -1213,7 +1213,8 @@ int sigproc_plan(ws_ctx* c, uint64_t n)
         m /= 2;
         ++twos;
     }
-    for (; twos >= 3; twos -= 3) radix.push_back(8);
+    for (; twos >= 4; twos -= 4) radix.push_back(16);
+    if (twos == 3) radix.push_back(8);
     if (twos == 2) radix.push_back(4);
     if (twos == 1) radix.push_back(2);
     for (int p : {3, 5, 7, 11, 13})
@@ -1293,7 +1294,8 @@ wsb::SigprocDesc sigproc_desc(ws_ctx* c, const double* data, uint64_t rows, int 
     d.mode = 0;
     d.nf = (int)c->sp_radix.size();
     d.inv_n = 1.0 / (double)c->sp_n;  // fft.cpp:99
-    for (int i = 0; i < d.nf; ++i) d.radix[i >> 4] |= (unsigned long long)c->sp_radix[i] << (4 * (i & 15));
+    for (int i = 0; i < d.nf; ++i)  // 4 bits per pass, radix 16 encoded as 1
+        d.radix[i >> 4] |= (unsigned long long)(c->sp_radix[i] == 16 ? 1 : c->sp_radix[i]) << (4 * (i & 15));
     return d;
 }
 

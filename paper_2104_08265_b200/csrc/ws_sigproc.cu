@@ -75,6 +75,31 @@ __device__ __forceinline__ void sp_dft(double2* x)
             x[q] = c_add(e[q], o[q]);
             x[q + 4] = c_sub(e[q], o[q]);
         }
+    } else if constexpr (R == 16) {
+        // 16 = 4 x 4: X[k1 + 4 k2] = sum_n2 W16^(n2 k1) W4^(n2 k2) sum_n1 x[4 n1 + n2] W4^(n1 k1)
+        double2 a[4][4];
+#pragma unroll
+        for (int n2 = 0; n2 < 4; ++n2) {
+            double2 t[4] = {x[n2], x[4 + n2], x[8 + n2], x[12 + n2]};
+            sp_dft<4>(t);
+#pragma unroll
+            for (int k1 = 0; k1 < 4; ++k1) a[n2][k1] = t[k1];
+        }
+        constexpr double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173, h = 0.70710678118654752440;
+        // twiddles W16^m = exp(+2 pi i m / 16), m = n2 k1
+        const double2 w[10] = {{1.0, 0.0}, {c1, s1}, {h, h}, {s1, c1}, {0.0, 1.0},
+                               {-s1, c1}, {-h, h}, {-c1, s1}, {-1.0, 0.0}, {-c1, -s1}};
+#pragma unroll
+        for (int n2 = 1; n2 < 4; ++n2)
+#pragma unroll
+            for (int k1 = 1; k1 < 4; ++k1) a[n2][k1] = c_mul(a[n2][k1], w[n2 * k1]);
+#pragma unroll
+        for (int k1 = 0; k1 < 4; ++k1) {
+            double2 t[4] = {a[0][k1], a[1][k1], a[2][k1], a[3][k1]};
+            sp_dft<4>(t);
+#pragma unroll
+            for (int k2 = 0; k2 < 4; ++k2) x[k1 + 4 * k2] = t[k2];
+        }
     } else {
         constexpr int H = (R - 1) / 2;
         double2 s[H + 1], d[H + 1];
@@ -192,6 +217,7 @@ __device__ __forceinline__ void sp_pass_any(int R, double2* buf, const double2* 
         case 5: sp_pass<5, kFilter>(buf, tw, filter, n, L); break;
         case 7: sp_pass<7, kFilter>(buf, tw, filter, n, L); break;
         case 8: sp_pass<8, kFilter>(buf, tw, filter, n, L); break;
+        case 16: sp_pass<16, kFilter>(buf, tw, filter, n, L); break;
         case 11: sp_pass_wide<11>(buf, tw, n, L); break;  // filtered beforehand
         default: sp_pass_wide<13>(buf, tw, n, L); break;
     }
@@ -494,15 +520,16 @@ __global__ void __launch_bounds__(kSpThreads, 2) k_sigproc(const SigprocDesc d)
     __syncthreads();
     if (bulk && tid == 0) asm volatile("mbarrier.inval.shared.b64 [%0];" ::"r"(s_bar) : "memory");
 
-    const int r0 = (int)(d.radix[0] & 15);
-    if (d.nf == 0 || r0 > 8) {  // no pass (n == 1) or a first radix too wide to fuse the filter into
+    const int r0c = (int)(d.radix[0] & 15);
+    if (d.nf == 0 || (r0c > 8)) {  // radix 16 (code 1) fuses the filter too  // no pass (n == 1) or a first radix too wide to fuse the filter into
         for (int c = tid; c < n; c += kSpThreads) buf[c] = sp_filter_mul(buf[c], __ldg(d.filter + c));
         __syncthreads();
     }
     int L = n;
     const double2* tw = d.tw;  // per-pass twiddle tables, back to back
     for (int f = 0; f < d.nf; ++f) {
-        const int R = (int)(((f < 16 ? d.radix[0] : d.radix[1]) >> (4 * (f & 15))) & 15);
+        const int rc = (int)(((f < 16 ? d.radix[0] : d.radix[1]) >> (4 * (f & 15))) & 15);
+        const int R = rc == 1 ? 16 : rc;  // code 1 = radix 16
         if (f == 0)
             sp_pass_any<true>(R, buf, tw, d.filter, n, L);
         else
