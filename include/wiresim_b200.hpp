@@ -16,6 +16,7 @@
 // convolve (spectral.hpp:47), float32, padded wire x tick, row-major.
 #pragma once
 
+#include <complex>
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
@@ -192,6 +193,43 @@ SimResult run_simulation(const SimConfig& config, const std::vector<D>& depos, i
     Context ctx(device);
     Plane plane(ctx, config.grid, config.response, config.n_sigma);
     return plane.simulate(config, depos);
+}
+
+// ---- signal processing (sigproc.hpp, the paper's Listing 1) ---------------
+// SignalBatch (sigproc.hpp:17-29): rows x cols complex spectra (row-major),
+// pad_rows guard rows before the out_rows of interest.
+struct SignalBatch {
+    std::size_t rows = 0, cols = 0;
+    std::vector<std::complex<double>> data;
+    std::size_t pad_rows = 0;
+    std::size_t out_rows = 0;
+};
+
+// ChainResult (sigproc.hpp:53-57): block (out_rows x cols, row-major), one
+// median per block row, the imaginary-residue diagnostic.
+struct ChainResult {
+    std::size_t rows = 0, cols = 0;
+    std::vector<double> block;
+    std::vector<double> medians;
+    double max_rel_imag = 0.0;
+};
+
+// sigproc_chain (sigproc.cpp:104-118) on the GPU: filter -> inverse DFT along
+// rows -> block [pad_rows, pad_rows + out_rows) -> row medians. The reference's
+// invalid_argument cases (filter length, pad + out > rows) throw the same type.
+inline ChainResult sigproc_chain(Context& ctx, const SignalBatch& batch,
+                                 const std::vector<std::complex<double>>& filter)
+{
+    ChainResult r;
+    r.rows = batch.out_rows;
+    r.cols = batch.cols;
+    r.block.resize(batch.out_rows * batch.cols);
+    r.medians.resize(batch.out_rows);
+    ws_signal_batch b{reinterpret_cast<const double*>(batch.data.data()), batch.rows, batch.cols, batch.pad_rows,
+                      batch.out_rows};
+    check(ws_sigproc_chain(ctx.get(), &b, reinterpret_cast<const double*>(filter.data()), filter.size(), 1,
+                           r.block.data(), r.medians.data(), &r.max_rel_imag));
+    return r;
 }
 
 // load_depos (pipeline.cpp:226-262): the native CSV reader, same validation and

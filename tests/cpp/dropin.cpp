@@ -2,6 +2,7 @@
 // over the C ABI. Simulates one plane and writes the frame (float32, padded,
 // row-major) to argv[1]; exit code 0 on success. Built and run by
 // tests/test_gpu_parity.py::test_cpp_dropin.
+#include <complex>
 #include <cstdio>
 #include <string>
 #include <vector>
@@ -56,6 +57,30 @@ int main(int argc, char** argv)
             wiresim_b200::load_depos<wiresim_b200::Depo>(csv);
             return 8;
         } catch (const std::runtime_error&) {
+        }
+    }
+    // sigproc_chain (sigproc.cpp:104-118): a Hermitian row (spectrum of a real
+    // impulse at sample 3) through an identity filter comes back as the impulse
+    {
+        wiresim_b200::Context ctx;
+        wiresim_b200::SignalBatch b;
+        b.rows = 2;
+        b.cols = 12;
+        b.pad_rows = 1;
+        b.out_rows = 1;
+        b.data.resize(b.rows * b.cols);
+        for (std::size_t r = 0; r < b.rows; ++r)
+            for (std::size_t k = 0; k < b.cols; ++k)
+                b.data[r * b.cols + k] = std::polar(1.0, -2.0 * 3.14159265358979323846 * 3.0 * (double)k / 12.0);
+        const std::vector<std::complex<double>> ones(b.cols, 1.0);
+        const wiresim_b200::ChainResult c = wiresim_b200::sigproc_chain(ctx, b, ones);
+        for (std::size_t t = 0; t < b.cols; ++t)
+            if (std::abs(c.block[t] - (t == 3 ? 1.0 : 0.0)) > 1e-12) return 9;
+        if (c.medians.size() != 1 || std::abs(c.medians[0]) > 1e-12) return 10;
+        try {
+            wiresim_b200::sigproc_chain(ctx, b, std::vector<std::complex<double>>(5, 1.0));
+            return 11;
+        } catch (const std::invalid_argument&) {
         }
     }
     // the reference's exception categories cross back as the same C++ types
