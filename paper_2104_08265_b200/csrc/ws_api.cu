@@ -489,7 +489,7 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
     WS_CUDA(cudaEventRecord(pc.ev[1], s));
     if (ev.fluctuate && !from_grid) {
         WS_CUDA(wsb_launch_fluctuate(ev, c->recs.p, c->pool.p, nullptr, s));
-        c->launches += units ? 1 : 0;
+        c->launches += units ? (ev.approx ? 1 : 2) : 0;  // exact: key kernel + walk (the CUB sort between is library code)
     }
     WS_CUDA(cudaEventRecord(pc.ev[2], s));
     if (ev.mode == 0) {

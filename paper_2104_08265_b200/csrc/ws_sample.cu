@@ -7,6 +7,8 @@
 // reproduces its integer draws.
 #include "ws_common.cuh"
 
+#include <cub/device/device_radix_sort.cuh>
+
 namespace wsb {
 
 __device__ __forceinline__ int lane_id() { return (int)(threadIdx.x & 31); }
@@ -638,11 +640,26 @@ __global__ void k_fluctuate(const EventDesc ev, const UnitRec* __restrict__ recs
 // quarter of the warp's live lanes have finished their draws does the warp
 // set up the next draws (RNG, pmf seed) together. The integer grid is
 // unchanged (same draws, same order per depo; float atomics exact < 2^24).
-__global__ void __launch_bounds__(128) k_fluctuate_exact(const EventDesc ev, const UnitRec* __restrict__ recs,
-                                                          const uint32_t* __restrict__ pool)
+// walk-length key of every unit (the walk is ~q steps): warps of similar
+// charge keep their lanes busy together
+__global__ void k_fluct_keys(const EventDesc ev, const UnitRec* __restrict__ recs, uint32_t* __restrict__ keys,
+                             uint32_t* __restrict__ vals)
 {
     const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
-    bool done = u >= ev.total_units;
+    if (u >= ev.total_units) return;
+    const PlaneDesc& P = ev.p[plane_of_unit(ev, u)];
+    const int64_t q = recs[u].w0 >= 0 ? P.depos[u - P.unit_base].q : 0;
+    keys[u] = (uint32_t)(q < 0 ? 0 : (q > 0xffffffffll ? 0xffffffffll : q));
+    vals[u] = u;
+}
+
+__global__ void __launch_bounds__(128) k_fluctuate_exact(const EventDesc ev, const UnitRec* __restrict__ recs,
+                                                          const uint32_t* __restrict__ pool,
+                                                          const uint32_t* __restrict__ order)
+{
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    bool done = i >= ev.total_units;
+    const uint32_t u = done ? 0u : (order ? order[i] : i);
     UnitRec rec{};
     if (!done) rec = recs[u];
     done = done || rec.w0 < 0;
@@ -821,9 +838,28 @@ extern "C" cudaError_t wsb_launch_fluctuate(const wsb::EventDesc& ev, const wsb:
                                             const uint32_t* order, cudaStream_t s)
 {
     if (ev.total_units == 0) return cudaSuccess;
-    if (ev.approx)
+    if (ev.approx) {
         wsb::k_fluctuate<<<(ev.total_units + 127) / 128, 128, 0, s>>>(ev, recs, pool, order);
-    else
-        wsb::k_fluctuate_exact<<<(ev.total_units + 127) / 128, 128, 0, s>>>(ev, recs, pool);
+        return cudaGetLastError();
+    }
+    // exact walk: units in descending charge (CUB radix sort, stream-ordered scratch)
+    const uint32_t n = ev.total_units;
+    uint32_t* buf = nullptr;
+    size_t temp = 0;
+    cudaError_t e = cub::DeviceRadixSort::SortPairsDescending(nullptr, temp, (const uint32_t*)nullptr,
+                                                              (uint32_t*)nullptr, (const uint32_t*)nullptr,
+                                                              (uint32_t*)nullptr, (int)n, 0, 32, s);
+    if (e != cudaSuccess) return e;
+    e = cudaMallocAsync(reinterpret_cast<void**>(&buf), sizeof(uint32_t) * 4 * (size_t)n + temp, s);
+    if (e != cudaSuccess) return e;
+    uint32_t *k_in = buf, *k_out = buf + n, *v_in = buf + 2 * (size_t)n, *v_out = buf + 3 * (size_t)n;
+    wsb::k_fluct_keys<<<(n + 255) / 256, 256, 0, s>>>(ev, recs, k_in, v_in);
+    e = cub::DeviceRadixSort::SortPairsDescending(buf + 4 * (size_t)n, temp, k_in, k_out, v_in, v_out, (int)n, 0, 32,
+                                                  s);
+    if (e == cudaSuccess)
+        wsb::k_fluctuate_exact<<<(n + 127) / 128, 128, 0, s>>>(ev, recs, pool, v_out);
+    const cudaError_t e2 = cudaFreeAsync(buf, s);
+    if (e != cudaSuccess) return e;
+    if (e2 != cudaSuccess) return e2;
     return cudaGetLastError();
 }
