@@ -265,14 +265,14 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
         // coefficients -> fixed-point units of their row
         for (int i = tid; i < cnt * R; i += NT) ent[i >> kRShift].c[i & (R - 1)] *= s_scale[i & (R - 1)];
         __syncthreads();
-        // profile of local entry e -> registers (tap lane + 32 q; g is 0-filled
-        // to a multiple of 32 taps, nothing past it is read); one entry ahead
+        // profile of local entry e -> registers (tap lane + 32 q < L, 0 past
+        // the profile); one entry ahead
         auto load_g = [&](int e, float* gv) {
             int lc = 0;
             const float* src = nullptr;
             if (e < cnt) {
                 const TEnt& d = ent[e];
-                lc = (int)(((d.tsL >> 16) + 31u) & ~31u);
+                lc = (int)(d.tsL >> 16) - lane;  // tap lane + 32 q exists iff 32 q < L - lane
                 src = reinterpret_cast<const float*>(pool + d.goff) + lane;
             }
 #pragma unroll

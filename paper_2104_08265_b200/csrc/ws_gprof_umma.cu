@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(kUmThreads) k_gprof_umma(const EventDesc ev, c
         // epilogue: accumulator rows -> g (ceil32(L) taps per unit). TMEM gives
         // lane = unit row; a per-warp shared transpose turns each 16-column
         // chunk into 8-row x 64-byte float4 stores (full sectors)
-        const int lp = live ? (rec.n_t + nl - 1 + 31) & ~31 : 0;
+        const int lp = live ? (rec.n_t + nl - 1 + 15) & ~15 : 0;  // k_direct reads taps < L only
         float* g = reinterpret_cast<float*>(pool + rec.goff);
         const int lane = tid & 31;
         float* stg = reinterpret_cast<float*>(um_smem) + warp * (32 * 20);  // A area (free now)
