@@ -32,7 +32,7 @@ constexpr int kQ = 5;                          // profile taps per lane in regis
 constexpr int kSlot = 32 * kQ;                 // taps of the register fast path
 constexpr int kMargin = kSlot;                 // discard margins either side of every row
 constexpr int kRowStride = kMargin + kTileTicks + kMargin;  // ints per tile row
-constexpr int kDirectThreads = 512;  // two CTAs per SM
+constexpr int kDirectThreads = 640;  // two CTAs per SM
 
 // Fixed-point term round(c g). WS_DIRECT_MAGIC: one FFMA with the magic
 // 1.5 * 2^23 (the mantissa bits hold the rounded value; needs |c g| < 2^22)
