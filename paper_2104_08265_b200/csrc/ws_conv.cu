@@ -34,6 +34,8 @@
 // (4 B/cell) plus the depo records.
 #include "ws_common.cuh"
 
+#include <atomic>
+
 namespace wsb {
 
 constexpr int kSegShift = 6;  // 64-tick bound segments
@@ -381,7 +383,7 @@ extern "C" size_t wsb_conv_smem(int N, int Np, int M)
 // kernel that runs the row FFT needs them) and the shared-memory opt-ins.
 static cudaError_t conv_device_setup()
 {
-    static unsigned long long ready = 0;
+    static std::atomic<unsigned long long> ready{0};  // per-device attribute setup (idempotent)
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;

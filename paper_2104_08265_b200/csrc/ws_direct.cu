@@ -24,6 +24,8 @@
 // that is discarded. Work ~ depos x rows x L instead of cells x log(ticks).
 #include "ws_common.cuh"
 
+#include <atomic>
+
 #include <algorithm>
 
 namespace wsb {
@@ -334,7 +336,7 @@ extern "C" cudaError_t wsb_launch_direct(const wsb::EventDesc& ev, const uint32_
                                          const wsb::TEnt* tlist, size_t smem_bytes, cudaStream_t stream)
 {
     constexpr int NT = wsb::kDirectThreads;
-    static unsigned long long ready = 0;
+    static std::atomic<unsigned long long> ready{0};  // per-device attribute setup (idempotent)
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;

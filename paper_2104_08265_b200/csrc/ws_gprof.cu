@@ -14,6 +14,8 @@
 // wide depos) take a per-warp SIMT loop.
 #include "ws_common.cuh"
 
+#include <atomic>
+
 #include <algorithm>
 #include <cstdlib>
 
@@ -266,7 +268,7 @@ extern "C" cudaError_t wsb_launch_gprof(const wsb::EventDesc& ev, const wsb::Uni
     if (max_units == 0) return cudaSuccess;
     const int ntap = (max_lags + 62) & ~31;
     const size_t smem = 2 * sizeof(uint32_t) * (size_t)(ntap + wsb::kGpPre + wsb::kGpPost);
-    static unsigned long long ready = 0;
+    static std::atomic<unsigned long long> ready{0};  // per-device attribute setup (idempotent)
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;

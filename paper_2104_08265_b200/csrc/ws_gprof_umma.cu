@@ -15,6 +15,8 @@
 // compute their profile with a scalar loop in the epilogue.
 #include "ws_common.cuh"
 
+#include <atomic>
+
 #include <algorithm>
 
 namespace wsb {
@@ -261,7 +263,7 @@ extern "C" cudaError_t wsb_launch_gprof_umma(const wsb::EventDesc& ev, const wsb
         if (ev.p[i].direct) max_units = max_units > ev.p[i].n_units ? max_units : ev.p[i].n_units;
     if (max_units == 0) return cudaSuccess;
     const size_t smem = (size_t)2 * wsb::kUmK * 4 * (wsb::kUmM + (size_t)N);
-    static unsigned long long ready = 0;
+    static std::atomic<unsigned long long> ready{0};  // per-device attribute setup (idempotent)
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;

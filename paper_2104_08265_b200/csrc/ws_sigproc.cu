@@ -24,6 +24,8 @@
 // the whole chain run in one buffer.
 #include "ws_common.cuh"
 
+#include <atomic>
+
 namespace wsb {
 
 constexpr int kSpThreads = 256;
@@ -586,7 +588,7 @@ extern "C" int wsb_sigproc_max_n()
 
 extern "C" cudaError_t wsb_sigproc_setup()
 {
-    static unsigned long long ready = 0;
+    static std::atomic<unsigned long long> ready{0};  // per-device attribute setup (idempotent)
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
