@@ -244,7 +244,8 @@ typedef struct ws_signal_batch {
  * diagnostic, printed to stderr as it does when > 1e-6. filter: filter_len
  * complex128 values (== cols, else WS_EINVAL like apply_filter). Validation
  * follows SignalBatch::validate. Rows up to ws_sigproc_max_cols() samples
- * whose length factors into primes <= 13.
+ * whose length factors into primes <= 13 take the mixed-radix row FFT; other
+ * lengths (up to ~9.1k samples) a direct O(n^2) inverse DFT per row.
  * _device: device pointers, asynchronous unless max_rel_imag is non-null. */
 int ws_sigproc_chain_device(ws_ctx* ctx, const ws_signal_batch* batch, const double* filter, uint64_t filter_len,
                             double* block, double* medians, double* max_rel_imag);

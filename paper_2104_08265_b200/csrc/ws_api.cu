@@ -41,6 +41,7 @@ extern "C" cudaError_t wsb_launch_fluctuate(const EventDesc& ev, const UnitRec* 
                                             const uint32_t* order, cudaStream_t s);
 extern "C" size_t wsb_sigproc_smem(int n);
 extern "C" int wsb_sigproc_max_n();
+extern "C" int wsb_sigproc_dft_max_n();
 extern "C" cudaError_t wsb_launch_sigproc(const wsb::SigprocDesc& d, cudaStream_t s);
 extern "C" size_t wsb_conv_smem(int N, int Np, int M);
 extern "C" cudaError_t wsb_launch_conv(const EventDesc& ev, const uint32_t* pool, const uint32_t* band_off,
@@ -148,6 +149,7 @@ struct ws_ctx {
     cudaEvent_t slot_copied[2] = {nullptr, nullptr};
     // sigproc chain: plan of the last row length + staging of the host path
     uint64_t sp_n = 0;
+    bool sp_dft = false;  // direct-DFT plan (a prime factor > 13)
     std::vector<int8_t> sp_radix;
     DevBuf<double2> sp_tw, sp_data, sp_filter;
     DevBuf<int> sp_perm;
@@ -1222,9 +1224,25 @@ int sigproc_plan(ws_ctx* c, uint64_t n)
             m /= p;
             radix.push_back((int8_t)p);
         }
-    if (m != 1)
-        return set_err(WS_EINVAL, "sigproc: row length %llu has a prime factor > 13 (not supported on the GPU path)",
-                       (unsigned long long)n);
+    if (m != 1) {
+        // a prime factor > 13: the direct inverse DFT, twiddles exp(+2 pi i m / n), m < n
+        if (n > (uint64_t)wsb_sigproc_dft_max_n())
+            return set_err(WS_EINVAL, "sigproc: row length %llu has a prime factor > 13 and exceeds the direct "
+                           "path's %d samples", (unsigned long long)n, wsb_sigproc_dft_max_n());
+        std::vector<double2> tw(n);
+        for (uint64_t j = 0; j < n; ++j) {
+            const long double a = 6.283185307179586476925286766559L * (long double)j / (long double)n;
+            tw[j] = make_double2((double)cosl(a), (double)sinl(a));
+        }
+        WS_CUDA(c->sp_tw.reserve(n));
+        WS_CUDA(cudaMemcpyAsync(c->sp_tw.p, tw.data(), sizeof(double2) * n, cudaMemcpyHostToDevice, c->stream));
+        WS_CUDA(cudaStreamSynchronize(c->stream));
+        c->sp_radix.clear();
+        c->sp_dft = true;
+        c->sp_n = n;
+        return WS_OK;
+    }
+    c->sp_dft = false;
     if ((int)radix.size() > wsb::kSpMaxRadices) return set_err(WS_EINVAL, "sigproc: too many radix passes");
     std::vector<int> perm(n);
     for (uint64_t k = 0; k < n; ++k) {
@@ -1291,7 +1309,7 @@ wsb::SigprocDesc sigproc_desc(ws_ctx* c, const double* data, uint64_t rows, int 
     d.rows = (int)rows;
     d.pad = pad;
     d.out = out;
-    d.mode = 0;
+    d.mode = c->sp_dft ? 2 : 0;
     d.nf = (int)c->sp_radix.size();
     d.inv_n = 1.0 / (double)c->sp_n;  // fft.cpp:99
     for (int i = 0; i < d.nf; ++i)  // 4 bits per pass, radix 16 encoded as 1

@@ -252,7 +252,7 @@ struct SpSelect {
 };
 
 // key of the rank-k (0-based) element of buf[0..n).x
-__device__ unsigned long long sp_select(const double2* buf, int n, uint32_t k, SpSelect& s)
+__device__ unsigned long long sp_select(const double* v, int st, int n, uint32_t k, SpSelect& s)
 {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     unsigned long long prefix = 0, hmask = 0;
@@ -264,7 +264,7 @@ __device__ unsigned long long sp_select(const double2* buf, int n, uint32_t k, S
         for (int i = tid; i < kSpBins; i += kSpThreads) s.hist[i] = 0;
         __syncthreads();
         for (int i = tid; i < n; i += kSpThreads) {
-            const unsigned long long key = sp_key(buf[i].x);
+            const unsigned long long key = sp_key(v[i * st]);
             if ((key & hmask) == prefix) atomicAdd(&s.hist[(uint32_t)(key >> shift) & mask], 1u);
         }
         __syncthreads();
@@ -304,7 +304,7 @@ __device__ unsigned long long sp_select(const double2* buf, int n, uint32_t k, S
         hmask |= (unsigned long long)mask << shift;
         if (cnt == 1 && shift > 0) {  // the rank's bin holds one element: find it
             for (int i = tid; i < n; i += kSpThreads) {
-                const unsigned long long key = sp_key(buf[i].x);
+                const unsigned long long key = sp_key(v[i * st]);
                 if ((key & hmask) == prefix) s.key = key;
             }
             __syncthreads();
@@ -317,16 +317,16 @@ __device__ unsigned long long sp_select(const double2* buf, int n, uint32_t k, S
 }
 
 // row_median (sigproc.cpp:80-93) of buf[0..n).x
-__device__ __noinline__ double sp_median(const double2* buf, int n, SpSelect& s)
+__device__ __noinline__ double sp_median(const double* v, int st, int n, SpSelect& s)
 {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const unsigned long long upper = sp_select(buf, n, (uint32_t)(n / 2), s);
+    const unsigned long long upper = sp_select(v, st, n, (uint32_t)(n / 2), s);
     if (n & 1) return sp_key_value(upper);
     // the rank n/2 - 1 element: upper again unless exactly n/2 elements are below it
     uint32_t cnt = 0;
     unsigned long long mx = 0;
     for (int i = tid; i < n; i += kSpThreads) {
-        const unsigned long long key = sp_key(buf[i].x);
+        const unsigned long long key = sp_key(v[i * st]);
         if (key < upper) {
             ++cnt;
             mx = key > mx ? key : mx;
@@ -359,12 +359,12 @@ __device__ __noinline__ double sp_median(const double2* buf, int n, SpSelect& s)
 // elements of those bins (usually a handful) are compacted and ranked by
 // counting. More than kSpCand candidates (heavy ties, extreme ranges) take the
 // exact radix select instead. lo / hi: the row's min / max, known to all threads.
-__device__ __noinline__ double sp_median_fast(const double2* buf, int n, double lo, double hi, SpSelect& s)
+__device__ __noinline__ double sp_median_fast(const double* v, int st, int n, double lo, double hi, SpSelect& s)
 {
     if (!(hi > lo)) return lo;  // constant row (or no usable range)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const double scale = (double)kSpBins / (hi - lo);
-    if (!(scale > 0.0) || isinf(scale)) return sp_median(buf, n, s);
+    if (!(scale > 0.0) || isinf(scale)) return sp_median(v, st, n, s);
     // round((v - lo) * scale) through the 2^52 magic constant: one FFMA on the
     // fp64 pipe instead of an F2I conversion; rounding is monotone, which is
     // all the binning needs
@@ -375,7 +375,7 @@ __device__ __noinline__ double sp_median_fast(const double2* buf, int n, double 
     for (int i = tid; i < kSpBins; i += kSpThreads) s.hist[i] = 0;
     if (tid == 0) s.n_cand = 0;
     __syncthreads();
-    for (int i = tid; i < n; i += kSpThreads) atomicAdd(&s.hist[bin_of(buf[i].x)], 1u);
+    for (int i = tid; i < n; i += kSpThreads) atomicAdd(&s.hist[bin_of(v[i * st])], 1u);
     __syncthreads();
     constexpr int kPer = kSpBins / kSpThreads;
     uint32_t loc[kPer], sum = 0;
@@ -410,11 +410,11 @@ __device__ __noinline__ double sp_median_fast(const double2* buf, int n, double 
     __syncthreads();
     const int b_lo = (int)s.bin_lo, b_hi = (int)s.bin_hi;
     const uint32_t c0 = s.cum_lo, n_c = s.cum_hi - c0;
-    if (n_c > (uint32_t)kSpCand) return sp_median(buf, n, s);
+    if (n_c > (uint32_t)kSpCand) return sp_median(v, st, n, s);
     for (int i = tid; i < n; i += kSpThreads) {
-        const double v = buf[i].x;
-        const int b = bin_of(v);
-        if (b >= b_lo && b <= b_hi) s.cand[atomicAdd(&s.n_cand, 1u)] = sp_key(v);
+        const double x = v[i * st];
+        const int b = bin_of(x);
+        if (b >= b_lo && b <= b_hi) s.cand[atomicAdd(&s.n_cand, 1u)] = sp_key(x);
     }
     __syncthreads();
     for (int t = tid; t < (int)n_c; t += kSpThreads) {
@@ -456,6 +456,86 @@ __device__ __forceinline__ void sp_minmax(double& lo, double& hi, SpSelect& s)
     }
 }
 
+// Rows whose length has a prime factor > 13 (the reference takes them through
+// Bluestein, fft.cpp:140-160): the inverse DFT directly, O(n^2) per row in
+// fp64, twiddles exp(+2 pi i j k / n) reseeded from a table (d.tw) every 64
+// k and advanced by complex multiplies in between. Same outputs as the chain: block row,
+// residue statistics, medians. Shared: the filtered row (16 n) + the real
+// parts (8 n) + the selection scratch.
+__global__ void __launch_bounds__(kSpThreads) k_sigproc_dft(const SigprocDesc d)
+{
+    extern __shared__ __align__(16) unsigned char dft_smem[];
+    const int n = d.n, tid = threadIdx.x, lane = tid & 31;
+    double2* X = reinterpret_cast<double2*>(dft_smem);
+    double* re_s = reinterpret_cast<double*>(X + n);
+    SpSelect& sel = *reinterpret_cast<SpSelect*>(dft_smem + (((size_t)n * 24 + 15) & ~(size_t)15));
+    const int row = blockIdx.x, out_row = row - d.pad;
+    const bool in_block = out_row >= 0 && out_row < d.out;
+    const double2* src = d.data + (size_t)row * n;
+    for (int c = tid; c < n; c += kSpThreads) X[c] = sp_filter_mul(__ldcs(src + c), __ldg(d.filter + c));
+    __syncthreads();
+    double peak = 0.0, resid = 0.0, lo = INFINITY, hi = -INFINITY;
+    double* dst = in_block && d.block ? d.block + (size_t)out_row * n : nullptr;
+    constexpr int kJ = 4;  // outputs per thread per sweep: one X[k] load feeds four independent chains
+    for (int j0 = tid; j0 < n; j0 += kJ * kSpThreads) {
+        double ar[kJ], ai[kJ];
+        int m[kJ], jj[kJ];  // m = j k mod n
+#pragma unroll
+        for (int q = 0; q < kJ; ++q) {
+            ar[q] = ai[q] = 0.0;
+            m[q] = 0;
+            jj[q] = min(j0 + q * kSpThreads, n - 1);  // past n: a duplicate, not stored
+        }
+        // twiddle w = exp(+2 pi i j k / n): reseeded from the table every 64
+        // k, advanced by one complex multiply in between (error ~64 ulp)
+        double2 st[kJ];
+#pragma unroll
+        for (int q = 0; q < kJ; ++q) st[q] = __ldg(d.tw + jj[q]);
+        for (int k0 = 0; k0 < n; k0 += 64) {
+            double2 w[kJ];
+#pragma unroll
+            for (int q = 0; q < kJ; ++q) w[q] = __ldg(d.tw + m[q]);
+            const int k1 = min(k0 + 64, n);
+            for (int k = k0; k < k1; ++k) {
+                const double2 x = X[k];
+#pragma unroll
+                for (int q = 0; q < kJ; ++q) {
+                    ar[q] = fma(x.x, w[q].x, fma(-x.y, w[q].y, ar[q]));
+                    ai[q] = fma(x.x, w[q].y, fma(x.y, w[q].x, ai[q]));
+                    w[q] = c_mul(w[q], st[q]);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < kJ; ++q) m[q] = (int)(((long long)m[q] + 64ll * jj[q]) % n);
+        }
+#pragma unroll
+        for (int q = 0; q < kJ; ++q) {
+            const int j = j0 + q * kSpThreads;
+            if (j >= n) break;
+            const double re = ar[q] * d.inv_n, im = ai[q] * d.inv_n;
+            peak = fmax(peak, fabs(re));
+            resid = fmax(resid, fabs(im));
+            lo = fmin(lo, re);
+            hi = fmax(hi, re);
+            re_s[j] = re;
+            if (dst) __stcs(dst + j, re);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        peak = fmax(peak, __shfl_xor_sync(0xffffffffu, peak, o));
+        resid = fmax(resid, __shfl_xor_sync(0xffffffffu, resid, o));
+    }
+    if (lane == 0) {
+        atomicMax(d.stats, (unsigned long long)__double_as_longlong(peak));
+        atomicMax(d.stats + 1, (unsigned long long)__double_as_longlong(resid));
+    }
+    if (!in_block || !d.medians) return;
+    sp_minmax(lo, hi, sel);  // includes the barrier after the re_s stores
+    const double med = sp_median_fast(re_s, 1, n, lo, hi, sel);
+    if (tid == 0) d.medians[out_row] = med;
+}
+
 __global__ void __launch_bounds__(kSpThreads, 2) k_sigproc(const SigprocDesc d)
 {
     extern __shared__ __align__(16) unsigned char sp_smem[];
@@ -477,7 +557,7 @@ __global__ void __launch_bounds__(kSpThreads, 2) k_sigproc(const SigprocDesc d)
             hi = fmax(hi, v);
         }
         sp_minmax(lo, hi, sel);  // includes the barrier after the stores
-        const double med = sp_median_fast(buf, n, lo, hi, sel);
+        const double med = sp_median_fast(reinterpret_cast<const double*>(buf), 2, n, lo, hi, sel);
         if (tid == 0) d.medians[row] = med;
         return;
     }
@@ -567,7 +647,7 @@ __global__ void __launch_bounds__(kSpThreads, 2) k_sigproc(const SigprocDesc d)
     (void)warp;
     if (!in_block || !d.medians) return;
     sp_minmax(lo, hi, sel);
-    const double med = sp_median_fast(buf, n, lo, hi, sel);
+    const double med = sp_median_fast(reinterpret_cast<const double*>(buf), 2, n, lo, hi, sel);
     if (tid == 0) d.medians[out_row] = med;
 }
 
@@ -576,6 +656,12 @@ __global__ void __launch_bounds__(kSpThreads, 2) k_sigproc(const SigprocDesc d)
 extern "C" size_t wsb_sigproc_smem(int n)
 {
     return sizeof(double2) * (size_t)n + sizeof(wsb::SpSelect);
+}
+
+extern "C" int wsb_sigproc_dft_max_n()
+{
+    // the direct-DFT path (lengths with a prime factor > 13)
+    return (int)((227 * 1024 - sizeof(wsb::SpSelect) - 16) / 24);
 }
 
 extern "C" int wsb_sigproc_max_n()
@@ -604,6 +690,8 @@ extern "C" cudaError_t wsb_sigproc_setup()
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(wsb::k_sigproc, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(wsb::k_sigproc_dft, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
     ready |= 1ull << dev;
     return cudaSuccess;
 }
@@ -613,6 +701,11 @@ extern "C" cudaError_t wsb_launch_sigproc(const wsb::SigprocDesc& d, cudaStream_
     cudaError_t e = wsb_sigproc_setup();
     if (e != cudaSuccess) return e;
     if (d.rows == 0) return cudaSuccess;
-    wsb::k_sigproc<<<d.rows, wsb::kSpThreads, wsb_sigproc_smem(d.n), s>>>(d);
+    if (d.mode == 2) {
+        const size_t smem = (((size_t)d.n * 24 + 15) & ~(size_t)15) + sizeof(wsb::SpSelect);
+        wsb::k_sigproc_dft<<<d.rows, wsb::kSpThreads, smem, s>>>(d);
+    } else {
+        wsb::k_sigproc<<<d.rows, wsb::kSpThreads, wsb_sigproc_smem(d.n), s>>>(d);
+    }
     return cudaGetLastError();
 }

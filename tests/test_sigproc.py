@@ -103,7 +103,8 @@ def test_gpu_paper_size_vs_oracle(ctx, oracle):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("n", [2, 7, 8, 12, 13, 60, 64, 343, 1000, 1024, 1144, 4096, 6000, 8192, 9600, 13312])
+@pytest.mark.parametrize("n", [2, 7, 8, 12, 13, 60, 64, 343, 1000, 1024, 1144, 4096, 6000, 8192, 9600, 13312,
+                               17, 97, 2 * 3 * 17, 1009, 6007])  # the last five: direct-DFT path
 def test_gpu_lengths_vs_numpy(ctx, n):
     from paper_2104_08265_b200 import sigproc_chain
     rng = np.random.default_rng(n)
@@ -167,9 +168,9 @@ def test_gpu_device_path_equals_host_path(ctx):
 @pytest.mark.gpu
 def test_gpu_errors(ctx):
     from paper_2104_08265_b200 import WsError, sigproc_chain, sigproc_max_cols
-    d = np.zeros((4, 17), dtype=np.complex128)
-    with pytest.raises(WsError, match="prime factor"):
-        sigproc_chain(d, np.ones(17), 0, 4, ctx=ctx)
+    d = np.zeros((1, 9973), dtype=np.complex128)  # prime, beyond the direct path's shared-memory row
+    with pytest.raises(WsError, match="prime factor > 13 and exceeds"):
+        sigproc_chain(d, np.ones(9973), 0, 1, ctx=ctx)
     d = np.zeros((4, 16), dtype=np.complex128)
     with pytest.raises(WsError, match="filter length 15 does not match 16"):
         sigproc_chain(d, np.ones(15), 0, 4, ctx=ctx)
