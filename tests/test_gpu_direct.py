@@ -164,3 +164,23 @@ def test_dense_event_routes_to_row_fft(pctx):
     # and the 100k-depo event stays on the time-domain kernel
     res2 = plane.simulate(microboone_event(100_000, seed=1)[0], SimConfig(fluctuate=False))
     assert res2.timing["direct_planes"] == 1
+
+
+@pytest.mark.parametrize("kind", ["collection", "induction"])
+def test_direct_wide_and_narrow_depos(pctx, oracle, kind):
+    """Tick profiles wider than 32 bins (sigma_t 3-6 us: the scalar path of the
+    response-profile kernel, profiles longer than a warp's 160 register taps:
+    k_direct's general path) and depos narrower than a quarter bin (the fp64
+    fallback of the fp32 sampler), mixed with ordinary ones, on the forced
+    time-domain path."""
+    resp = ResponseParams(plane_kind=kind, wire_weights=(0.1, 1.0, 0.1) if kind == "induction" else (1.0,))
+    depos = line_tracks(600, SMALL, seed=8)
+    depos["sigma_t"][::7] = np.linspace(3.0, 6.0, len(depos[::7]))
+    depos["sigma_x"][3::11] = 0.2   # < pitch / 4
+    depos["sigma_t"][5::13] = 0.05  # < tick / 4
+    m = _frame(pctx, "direct", SMALL, resp, depos)
+    s_ref, _ = oracle.charge_fluct_off(oracle_grid(SMALL), depos)
+    m_ref = oracle.convolve(oracle_grid(SMALL), oracle_response(resp), s_ref)
+    assert relL2_per_channel(m, m_ref) < TOL_FRAME
+    m_fft = _frame(pctx, "fft", SMALL, resp, depos)
+    assert relL2_per_channel(m_fft, m_ref) < TOL_FRAME
