@@ -466,28 +466,36 @@ __global__ void __launch_bounds__(1024) k_scan_bands(const uint32_t* __restrict_
 // coefficient a eff[w] of each tile row (independent of k_gprof, which may
 // run concurrently on the auxiliary stream). Lists larger
 // than ev.list_cap (the scan's total) flag kErrRange and write nothing.
-__global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ recs, const uint32_t* __restrict__ off,
-                             uint32_t* __restrict__ fill, UnitRec* __restrict__ list, TEnt* __restrict__ tlist,
-                             const uint32_t* __restrict__ pool, unsigned* __restrict__ err)
+// The direct-path tile entries of one unit (every lane of the warp calls it;
+// `live` false for lanes without a unit): a TEnt per (8-row group x window)
+// tile the unit touches, with its row coefficients a eff[w]. Slots come from
+// counter[] (warp-aggregated over the lanes that share a tile); put(b, slot,
+// entry) stores them (CSR offsets in k_fill_bands, fixed-capacity lists in
+// k_sample_off).
+// base: the unit's profile words [raw][eff][tv] (global with kLdg, or the
+// staging copy in shared memory / the unit's own global writes without).
+template <bool kLdg, typename Put>
+__device__ __forceinline__ void emit_tile_entries(const PlaneDesc& P, const UnitRec& rec, bool live,
+                                                  const float* base, uint32_t* __restrict__ counter, Put&& put)
 {
-    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
-    if (off[ev.total_bands] > ev.list_cap) {  // grid-uniform
-        if (u == 0) atomicOr(err, kErrRange);
-        return;
-    }
-    // no early exits below: the warp-collective tile-slot allocation needs every lane
-    bool live = u < ev.total_units;
-    UnitRec rec{};
-    if (live) rec = recs[u];
-    live = live && rec.w0 >= 0;
-    const PlaneDesc& P = ev.p[plane_of_unit(ev, live ? u : 0)];
-    if (live && !P.direct) {
-        for_each_bin(P, rec.w0, rec.n_w, rec.t0, rec.n_t, [&](int c) {
-            const uint32_t b = P.band_base + c;
-            list[off[b] + atomicAdd(&fill[b], 1u)] = rec;  // full record: k_conv streams the list
-        });
-        live = false;
-    }
+    auto ld = [&](const float* a) { return kLdg ? __ldg(a) : *a; };
+    // row_coef (ws_common.cuh) on `base`: a * profile[j], j = (w - first row) mod W, every wrap summed
+    auto coef = [&](int w, float& c) {
+        const bool stencil = !P.ww_is_one;
+        const int lo = stencil ? rec.w0 - P.h : rec.w0;
+        const int nrw = stencil ? rec.n_w + 2 * P.h : rec.n_w;
+        int j = w - lo;
+        if (j < 0) j += P.W;
+        else if (j >= P.W) j -= P.W;
+        if (j >= P.W) j %= P.W;
+        if (j >= nrw) return false;
+        const float* pr = base + (stencil ? rec.n_w : 0);
+        float acc = ld(&pr[j]);
+        if (nrw > P.W)
+            for (j += P.W; j < nrw; j += P.W) acc += ld(&pr[j]);
+        c = acc * rec.a;
+        return true;
+    };
     const int L = rec.n_t + P.n_lags - 1;
     int ts = rec.t0 + P.lo_lag;
     if (ts < 0) ts += P.N;
@@ -498,7 +506,7 @@ __global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ rec
     const int lo_row = stencil ? rec.w0 - P.h : rec.w0;
     const int n_rows = stencil ? rec.n_w + 2 * P.h : rec.n_w;
     const bool simple = lo_row >= 0 && lo_row + n_rows <= P.W;
-    const float* prof = reinterpret_cast<const float*>(pool + rec.pool) + (stencil ? rec.n_w : 0);
+    const float* prof = base + (stencil ? rec.n_w : 0);
     // the entry for tile (row group c / n_windows, window c % n_windows)
     auto make_entry = [&](int c) {
         const int r0 = (c / P.n_windows) * kTileRows, nr = min(kTileRows, P.W - r0);
@@ -512,7 +520,7 @@ __global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ rec
             for (int r = 0; r < kTileRows; ++r) {
                 const int j = r0 + r - lo_row;
                 const bool in = r < nr && j >= 0 && j < n_rows;
-                const float v = in ? __ldg(&prof[in ? j : 0]) : 0.0f;
+                const float v = in ? ld(&prof[in ? j : 0]) : 0.0f;
                 d.c[r] = v * rec.a;  // row_coef's product
             }
 #pragma unroll
@@ -525,7 +533,7 @@ __global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ rec
 #pragma unroll
             for (int r = 0; r < kTileRows; ++r) {
                 float cr = 0.0f;
-                if (r < nr && row_coef(P, r0 + r, false, rec, pool, cr) && cr != 0.0f) {
+                if (r < nr && coef(r0 + r, cr) && cr != 0.0f) {
                     rlo = min(rlo, r);
                     rhi = r + 1;
                 }
@@ -560,7 +568,7 @@ __global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ rec
                     const unsigned peers = __match_any_sync(vm, b);
                     const int leader = __ffs(peers) - 1;
                     uint32_t base = 0;
-                    if (lane_id() == leader) base = atomicAdd(&fill[b], (unsigned)__popc(peers));
+                    if (lane_id() == leader) base = atomicAdd(&counter[b], (unsigned)__popc(peers));
                     base = __shfl_sync(peers, base, leader);
                     slot[k] = base + __popc(peers & lt);
                 }
@@ -570,7 +578,7 @@ __global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ rec
                 const int g = g0 + (k >> 1), w = (k & 1) ? w1 : w0;
                 if (g <= g1 && w >= 0) {
                     const int c = g * P.n_windows + w;
-                    tlist[off[P.band_base + c] + slot[k]] = make_entry(c);
+                    put(P.band_base + c, slot[k], make_entry(c));
                 }
             }
             return;
@@ -579,8 +587,34 @@ __global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ rec
     if (!live) return;
     for_each_bin(P, rec.w0, rec.n_w, rec.t0, rec.n_t, [&](int c) {
         const uint32_t b = P.band_base + c;
-        tlist[off[b] + atomicAdd(&fill[b], 1u)] = make_entry(c);
+        put(b, atomicAdd(&counter[b], 1u), make_entry(c));
     });
+}
+
+__global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ recs, const uint32_t* __restrict__ off,
+                             uint32_t* __restrict__ fill, UnitRec* __restrict__ list, TEnt* __restrict__ tlist,
+                             const uint32_t* __restrict__ pool, unsigned* __restrict__ err)
+{
+    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (off[ev.total_bands] > ev.list_cap) {  // grid-uniform
+        if (u == 0) atomicOr(err, kErrRange);
+        return;
+    }
+    // no early exits below: the warp-collective tile-slot allocation needs every lane
+    bool live = u < ev.total_units;
+    UnitRec rec{};
+    if (live) rec = recs[u];
+    live = live && rec.w0 >= 0;
+    const PlaneDesc& P = ev.p[plane_of_unit(ev, live ? u : 0)];
+    if (live && !P.direct) {
+        for_each_bin(P, rec.w0, rec.n_w, rec.t0, rec.n_t, [&](int c) {
+            const uint32_t b = P.band_base + c;
+            list[off[b] + atomicAdd(&fill[b], 1u)] = rec;  // full record: k_conv streams the list
+        });
+        live = false;
+    }
+    emit_tile_entries<true>(P, rec, live, reinterpret_cast<const float*>(pool + rec.pool), fill,
+                            [&](uint32_t b, uint32_t slot, const TEnt& e) { tlist[off[b] + slot] = e; });
 }
 
 // Fluctuation walk, one thread per unit: sample_patch's exact probabilities
