@@ -10,6 +10,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <functional>
 #include <vector>
@@ -127,6 +128,8 @@ struct ws_ctx {
     DevBuf<uint32_t> band_count, band_off, band_fill;  // per bin (FFT bands / direct tiles)
     DevBuf<UnitRec> band_list;  // CSR lists of full unit records per FFT band (k_fill_bands)
     DevBuf<wsb::TEnt> tile_list;  // CSR lists of direct-path tile entries (k_fill_bands)
+    DevBuf<wsb::TEnt> tile_fixed;  // fixed-capacity tile lists (all-direct events, filled by the sampler)
+    uint32_t tile_cap_hint = 2048;  // entries per tile; doubled after a kErrTileCap
     size_t list_hint = 0;       // grown after a kErrRange
     uint32_t last_list_cap = 0;
     DevBuf<ScratchHeader> header;
@@ -464,7 +467,23 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
     ev.list_cap = (uint32_t)list_cap;
     c->last_list_cap = (uint32_t)list_cap;
     if (any_fft) WS_CUDA(c->band_list.reserve(list_cap));
-    if (any_direct) WS_CUDA(c->tile_list.reserve(list_cap));
+    // all-direct fluctuation-off events: the sampler fills fixed-capacity tile
+    // lists (no count scan, no k_fill_bands); WS_TILE_CSR=1 forces the CSR path
+    static const bool csr_only = [] {
+        const char* v = getenv("WS_TILE_CSR");
+        return v && v[0] == '1';
+    }();
+    const bool use_fixed = any_direct && !any_fft && ev.mode == 0 && !ev.fluctuate && !csr_only && bands > 0;
+    ev.tile_cap = 0;
+    ev.tiles = nullptr;
+    ev.tile_count = c->band_count.p;
+    if (use_fixed) {
+        WS_CUDA(c->tile_fixed.reserve((size_t)bands * c->tile_cap_hint));
+        ev.tile_cap = c->tile_cap_hint;
+        ev.tiles = c->tile_fixed.p;
+    } else if (any_direct) {
+        WS_CUDA(c->tile_list.reserve(list_cap));
+    }
     WS_CUDA(c->header.reserve(1));
     ScratchHeader* hdr = c->header.p;
     for (uint32_t i = 0; i < n; ++i) ev.p[i].stats = &hdr->stats[2 * i];
@@ -513,10 +532,12 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
             WS_CUDA(cudaEventRecord(c->aux_join, c->aux_stream));
             c->launches += units ? 1 : 0;
         }
-        WS_CUDA(wsb_launch_scan(c->band_count.p, c->band_off.p, c->band_fill.p, bands, s));
-        WS_CUDA(wsb_launch_fill(ev, c->recs.p, c->band_off.p, c->band_fill.p, c->band_list.p, c->tile_list.p,
-                                c->pool.p, &hdr->err, s));
-        c->launches += 1 + (units ? 1 : 0);
+        if (!ev.tile_cap) {  // CSR lists: scan the counts, then append
+            WS_CUDA(wsb_launch_scan(c->band_count.p, c->band_off.p, c->band_fill.p, bands, s));
+            WS_CUDA(wsb_launch_fill(ev, c->recs.p, c->band_off.p, c->band_fill.p, c->band_list.p,
+                                    c->tile_list.p, c->pool.p, &hdr->err, s));
+            c->launches += 1 + (units ? 1 : 0);
+        }
         if (any_direct) WS_CUDA(cudaStreamWaitEvent(s, c->aux_join, 0));  // profiles ready (bin stage ends)
     }
     WS_CUDA(cudaEventRecord(pc.ev[3], s));
@@ -565,6 +586,10 @@ int finish_pending(ws_ctx* c)
                 c->pool_hint = std::max<size_t>(c->pool.cap * 2, (size_t)h.pool_ctr + 4096);
                 rc = set_err(WS_ERANGE, "workspace: patch pool overflow (%u doubles needed); grown, re-run the call",
                              h.pool_ctr);
+            } else if (h.err & wsb::kErrTileCap) {
+                rc = set_err(WS_ERANGE, "workspace: tile list overflow (%u entries per tile); grown, re-run the call",
+                             c->tile_cap_hint);
+                c->tile_cap_hint *= 2;
             } else if (h.err & wsb::kErrRange) {
                 c->list_hint = std::max<size_t>(c->list_hint, 2 * (size_t)c->last_list_cap);
                 rc = set_err(WS_ERANGE, "workspace: bin lists overflow (capacity %u entries); grown, re-run the call",
@@ -668,6 +693,7 @@ int ws_ctx_destroy(ws_ctx* c)
 
     c->band_list.release();
     c->tile_list.release();
+    c->tile_fixed.release();
     c->header.release();
     c->depos.release();
     c->frames.release();

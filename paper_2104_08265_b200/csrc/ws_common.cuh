@@ -99,11 +99,17 @@ struct EventDesc {
     uint32_t total_units;
     uint32_t total_bands;
     uint32_t list_cap;         // capacity (entries) of the bin lists; more -> kErrRange, convolution skipped
+    // direct planes with fixed-capacity tile lists (fluctuation off): the
+    // sampler appends each unit's entries to tiles[b * tile_cap + slot],
+    // slot from tile_count[b] (no scan, no k_fill_bands); tile_cap 0 = CSR
+    uint32_t tile_cap;
+    TEnt* tiles;
+    uint32_t* tile_count;
     PlaneDesc p[kMaxPlanes];
 };
 
 // Error / overflow flags shared by kernels (device scalar words).
-enum : unsigned { kErrPool = 1u, kErrDomain = 2u, kErrCharge = 4u, kErrRange = 8u };
+enum : unsigned { kErrPool = 1u, kErrDomain = 2u, kErrCharge = 4u, kErrRange = 8u, kErrTileCap = 16u };
 
 __device__ __forceinline__ int band_plane(const EventDesc& ev, uint32_t gb)
 {

@@ -106,7 +106,9 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
     constexpr int kRShift = R == 16 ? 4 : R == 8 ? 3 : R == 4 ? 2 : 1;
     const uint32_t gb = blockIdx.x;
     const PlaneDesc& P = ev.p[band_plane(ev, gb)];
-    if (!P.direct || __ldg(&band_off[ev.total_bands]) > ev.list_cap) return;
+    if (!P.direct) return;
+    const bool fixed = ev.tile_cap != 0;  // fixed-capacity tile lists filled by the sampler
+    if (!fixed && __ldg(&band_off[ev.total_bands]) > ev.list_cap) return;
     const int tile = (int)(gb - P.band_base);
     const int W = P.W, N = P.N;
     const int rb = tile / P.n_windows, win = tile - rb * P.n_windows;
@@ -136,8 +138,9 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
         if (tid == 0) s_ovf = 0;
     }
 
-    const uint32_t lo = __ldg(&band_off[gb]);
-    const int n = (int)(__ldg(&band_off[gb + 1]) - lo);
+    const uint32_t lo = fixed ? gb * ev.tile_cap : __ldg(&band_off[gb]);
+    const int n = fixed ? (int)min(__ldg(&ev.tile_count[gb]), ev.tile_cap) : (int)(__ldg(&band_off[gb + 1]) - lo);
+    if (fixed) tlist = ev.tiles;
     const uint32_t s_ent = (uint32_t)__cvta_generic_to_shared(ent);
 
     // entries [c0, c0 + cnt) of the tile list -> staging (coalesced async copies)

@@ -263,209 +263,6 @@ __global__ void __launch_bounds__(128, kFluct ? 1 : 8) k_sample(const EventDesc 
         for_each_bin(P, f.w0, f.n_w, f.t0, f.n_t, [&](int c) { atomicAdd(&band_count[P.band_base + c], 1u); });
 }
 
-// Fluctuation-off sampling (the hot path), one thread per unit as k_sample,
-// but the profiles [raw][eff][tv] are written through shared memory: every
-// lane stages its unit's words, then the warp copies unit after unit with
-// coalesced stores (per-lane scattered 4-byte stores were the limiter:
-// 8.4M L2 sectors for 50 MB). Units with more than kStageWords profile words
-// (or the fp64 fallback for sub-quarter-bin widths) write directly.
-constexpr int kSampleThreads = 128;
-constexpr int kStageWarp = 32 * 52;  // staged profile words per warp
-
-__global__ void __launch_bounds__(kSampleThreads, 8)
-k_sample_off(const EventDesc ev, UnitRec* __restrict__ recs, uint32_t* __restrict__ pool, uint32_t pool_cap,
-             uint32_t* __restrict__ pool_ctr, uint32_t* __restrict__ band_count, unsigned* __restrict__ err)
-{
-    extern __shared__ float s_stage[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
-    const bool in_range = u < ev.total_units;
-    const int pi = in_range ? plane_of_unit(ev, u) : 0;
-    const PlaneDesc& P = ev.p[pi];
-    ws_depo d{};
-    if (in_range) d = P.depos[u - P.unit_base];
-    UnitRec rec;
-    rec.w0 = -1;
-    rec.t0 = 0;
-    rec.n_w = 0;
-    rec.n_t = 0;
-    rec.pool = 0;
-    rec.goff = 0;
-    rec.a = 0.0f;
-    rec.tsum = 0.0f;
-    bool live = in_range;
-    if (live && ev.drift_enabled && !drift(ev, d)) {
-        atomicOr(err, kErrDomain);
-        live = false;
-    }
-    Footprint f{};
-    if (live) {
-        if (d.q < 0) atomicOr(err, kErrCharge);
-        f = footprint(P, d);
-        if (f.clipped) atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[1]), 1ULL);
-        if (f.empty) {
-            atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[0]), (unsigned long long)d.q);
-            live = false;
-        }
-    }
-    const int h = P.h;
-    const int n_eff = live && !P.ww_is_one ? f.n_w + 2 * h : 0;
-    // warp-contiguous allocation, one atomic per warp: the 32 units' profiles
-    // back to back [base, base + W), then their g regions (direct planes:
-    // 4 header words, g[-1] = max|g|, then ceil32(L) taps)
-    const uint32_t words = live ? (uint32_t)(f.n_w + n_eff + f.n_t) : 0u;
-    const uint32_t gneed = (live && ev.mode == 0 && P.direct) ? (((uint32_t)(f.n_t + P.n_lags - 1) + 31u) & ~31u) + 4u
-                                                               : 0u;
-    uint32_t wex = words, gex = gneed;  // inclusive scans -> exclusive below
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t a = __shfl_up_sync(0xffffffffu, wex, o), b = __shfl_up_sync(0xffffffffu, gex, o);
-        if (lane >= o) {
-            wex += a;
-            gex += b;
-        }
-    }
-    const uint32_t w_tot = __shfl_sync(0xffffffffu, wex, 31), g_tot = __shfl_sync(0xffffffffu, gex, 31);
-    wex -= words;
-    gex -= gneed;
-    const uint32_t w_pad = (w_tot + 3u) & ~3u;
-    uint32_t base = 0;
-    if (lane == 0 && w_tot + g_tot) base = atomicAdd(pool_ctr, w_pad + g_tot + 4u);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    const uint32_t gbase = (base + w_pad + 3u) & ~3u;  // 16-byte aligned
-    if ((uint64_t)base + w_pad + g_tot + 4u > pool_cap && (w_tot + g_tot)) {
-        if (live) atomicOr(err, kErrPool);
-        live = false;
-    }
-    const uint32_t off = base + wex;
-    const bool fast = live && d.sigma_x * 4.0 >= P.pitch && d.sigma_t * 4.0 >= P.tick;
-    // the staged prefix of the warp's profile words (compact, same order as the pool)
-    const bool staged = live && wex + words <= (uint32_t)kStageWarp;  // a prefix of the lanes
-    float* stage = s_stage + warp * kStageWarp;
-    double sw = 0.0, mw = 0.0, st = 0.0, mt = 0.0;
-    float* raw = reinterpret_cast<float*>(pool + off);
-    if (live) {
-        rec.goff = gneed ? gbase + gex + 4u : 0u;
-        const double wire_edge = P.origin_x + ((double)f.w0 - (double)P.pad_w) * P.pitch;
-        const double tick_edge = P.origin_t + ((double)f.t0 - (double)P.pad_t) * P.tick;
-        float* dst = staged ? stage + wex : raw;
-        if (fast) {
-            float* tv = dst + f.n_w + n_eff;
-            bin_integrals_f32(d.x, d.sigma_x, wire_edge, P.pitch, f.n_w, [&](int i, float v) { dst[i] = v; }, sw,
-                              mw);
-            bin_integrals_f32(d.t, d.sigma_t, tick_edge, P.tick, f.n_t, [&](int i, float v) { tv[i] = v; }, st, mt);
-        } else {
-            double o4[4];
-            sample_f64_ool(&d, wire_edge, P.pitch, f.n_w, tick_edge, P.tick, f.n_t, dst, dst + f.n_w + n_eff, o4);
-            sw = o4[0];
-            mw = o4[1];
-            st = o4[2];
-            mt = o4[3];
-        }
-        if (n_eff) {
-            float* eff = dst + f.n_w;
-            for (int j = 0; j < n_eff; ++j) {
-                float e = 0.0f;
-                for (int dw = -h; dw <= h; ++dw) {
-                    const int i = j - h - dw;
-                    if (i >= 0 && i < f.n_w) e = fmaf((float)P.ww[dw + h], dst[i], e);
-                }
-                eff[j] = e;
-            }
-        }
-    }
-    // coalesced write-out of the staged prefix [base, base + n_staged)
-    __syncwarp();
-    uint32_t n_staged = staged ? wex + words : 0u;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) n_staged = max(n_staged, __shfl_xor_sync(0xffffffffu, n_staged, o));
-    float* pw = reinterpret_cast<float*>(pool) + base;
-    for (uint32_t k = lane; k < n_staged; k += 32) pw[k] = stage[k];
-    if (!live) {
-        if (in_range) recs[u] = rec;
-        return;
-    }
-    // sum_w sum_t wv*tv > 0  <=>  max(wv)*max(tv) > 0
-    if (!(mw * mt > 0.0)) {
-        // numerically empty (rasterize.cpp:111-116) -> clipped charge (pipeline.cpp:339-340)
-        atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[0]), (unsigned long long)d.q);
-        recs[u] = rec;
-        return;
-    }
-    // S = q * p = a * wv[w] * tv[t] with a = q / total (applied by the consumers)
-    rec.a = (float)((double)d.q / (sw * st));
-    rec.tsum = __double2float_ru(st);
-    rec.w0 = f.w0;
-    rec.t0 = f.t0;
-    rec.n_w = f.n_w;
-    rec.n_t = f.n_t;
-    rec.pool = off;
-    recs[u] = rec;
-    if (ev.mode == 0)
-        for_each_bin(P, f.w0, f.n_w, f.t0, f.n_t, [&](int c) { atomicAdd(&band_count[P.band_base + c], 1u); });
-}
-
-// Exclusive scan of bin counts (single block); resets the fill cursors.
-__global__ void __launch_bounds__(1024) k_scan_bands(const uint32_t* __restrict__ count, uint32_t* __restrict__ off,
-                                                    uint32_t* __restrict__ fill, uint32_t n)
-{
-    // one pass: each thread scans kPer consecutive counts in registers, the
-    // block scans the 1024 partial sums (two warp-shuffle levels), carry
-    // across passes only for n > 1024 * kPer
-    constexpr int kPer = 8;
-    __shared__ uint32_t warp_sums[32];
-    __shared__ uint32_t carry;
-    if (threadIdx.x == 0) carry = 0;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll 1
-    for (uint32_t base = 0; base < n; base += 1024u * kPer) {
-        const uint32_t i0 = base + threadIdx.x * kPer;
-        uint32_t v[kPer], sum = 0;
-#pragma unroll
-        for (int k = 0; k < kPer; ++k) {
-            v[k] = i0 + k < n ? __ldg(count + i0 + k) : 0u;
-            sum += v[k];
-        }
-        uint32_t x = sum;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        __syncthreads();  // carry / warp_sums of the previous pass consumed
-        if (lane == 31) warp_sums[wid] = x;
-        __syncthreads();
-        if (wid == 0) {
-            uint32_t t = warp_sums[lane];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
-                if (lane >= o) t += y;
-            }
-            warp_sums[lane] = t;
-        }
-        __syncthreads();
-        uint32_t run = carry + (wid ? warp_sums[wid - 1] : 0u) + x - sum;
-#pragma unroll
-        for (int k = 0; k < kPer; ++k)
-            if (i0 + k < n) {
-                off[i0 + k] = run;
-                fill[i0 + k] = 0;
-                run += v[k];
-            }
-        __syncthreads();
-        if (threadIdx.x == 1023) carry = run;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) off[n] = carry;
-}
-
-// Thread per unit: append the unit to the list of every bin it touches.
-// FFT planes list the unit record per band; direct planes list, per tile,
-// the entry k_direct consumes: tick span, profile offset and the
-// coefficient a eff[w] of each tile row (independent of k_gprof, which may
-// run concurrently on the auxiliary stream). Lists larger
-// than ev.list_cap (the scan's total) flag kErrRange and write nothing.
 // The direct-path tile entries of one unit (every lane of the warp calls it;
 // `live` false for lanes without a unit): a TEnt per (8-row group x window)
 // tile the unit touches, with its row coefficients a eff[w]. Slots come from
@@ -591,6 +388,223 @@ __device__ __forceinline__ void emit_tile_entries(const PlaneDesc& P, const Unit
     });
 }
 
+// Fluctuation-off sampling (the hot path), one thread per unit as k_sample,
+// but the profiles [raw][eff][tv] are written through shared memory: every
+// lane stages its unit's words, then the warp copies unit after unit with
+// coalesced stores (per-lane scattered 4-byte stores were the limiter:
+// 8.4M L2 sectors for 50 MB). Units with more than kStageWords profile words
+// (or the fp64 fallback for sub-quarter-bin widths) write directly.
+constexpr int kSampleThreads = 128;
+constexpr int kStageWarp = 32 * 52;  // staged profile words per warp
+
+__global__ void __launch_bounds__(kSampleThreads, 8)
+k_sample_off(const EventDesc ev, UnitRec* __restrict__ recs, uint32_t* __restrict__ pool, uint32_t pool_cap,
+             uint32_t* __restrict__ pool_ctr, uint32_t* __restrict__ band_count, unsigned* __restrict__ err)
+{
+    extern __shared__ float s_stage[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool in_range = u < ev.total_units;
+    const int pi = in_range ? plane_of_unit(ev, u) : 0;
+    const PlaneDesc& P = ev.p[pi];
+    ws_depo d{};
+    if (in_range) d = P.depos[u - P.unit_base];
+    UnitRec rec;
+    rec.w0 = -1;
+    rec.t0 = 0;
+    rec.n_w = 0;
+    rec.n_t = 0;
+    rec.pool = 0;
+    rec.goff = 0;
+    rec.a = 0.0f;
+    rec.tsum = 0.0f;
+    bool live = in_range;
+    if (live && ev.drift_enabled && !drift(ev, d)) {
+        atomicOr(err, kErrDomain);
+        live = false;
+    }
+    Footprint f{};
+    if (live) {
+        if (d.q < 0) atomicOr(err, kErrCharge);
+        f = footprint(P, d);
+        if (f.clipped) atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[1]), 1ULL);
+        if (f.empty) {
+            atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[0]), (unsigned long long)d.q);
+            live = false;
+        }
+    }
+    const int h = P.h;
+    const int n_eff = live && !P.ww_is_one ? f.n_w + 2 * h : 0;
+    // warp-contiguous allocation, one atomic per warp: the 32 units' profiles
+    // back to back [base, base + W), then their g regions (direct planes:
+    // 4 header words, g[-1] = max|g|, then ceil32(L) taps)
+    const uint32_t words = live ? (uint32_t)(f.n_w + n_eff + f.n_t) : 0u;
+    const uint32_t gneed = (live && ev.mode == 0 && P.direct) ? (((uint32_t)(f.n_t + P.n_lags - 1) + 31u) & ~31u) + 4u
+                                                               : 0u;
+    uint32_t wex = words, gex = gneed;  // inclusive scans -> exclusive below
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t a = __shfl_up_sync(0xffffffffu, wex, o), b = __shfl_up_sync(0xffffffffu, gex, o);
+        if (lane >= o) {
+            wex += a;
+            gex += b;
+        }
+    }
+    const uint32_t w_tot = __shfl_sync(0xffffffffu, wex, 31), g_tot = __shfl_sync(0xffffffffu, gex, 31);
+    wex -= words;
+    gex -= gneed;
+    const uint32_t w_pad = (w_tot + 3u) & ~3u;
+    uint32_t base = 0;
+    if (lane == 0 && w_tot + g_tot) base = atomicAdd(pool_ctr, w_pad + g_tot + 4u);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    const uint32_t gbase = (base + w_pad + 3u) & ~3u;  // 16-byte aligned
+    if ((uint64_t)base + w_pad + g_tot + 4u > pool_cap && (w_tot + g_tot)) {
+        if (live) atomicOr(err, kErrPool);
+        live = false;
+    }
+    const uint32_t off = base + wex;
+    const bool fast = live && d.sigma_x * 4.0 >= P.pitch && d.sigma_t * 4.0 >= P.tick;
+    // the staged prefix of the warp's profile words (compact, same order as the pool)
+    const bool staged = live && wex + words <= (uint32_t)kStageWarp;  // a prefix of the lanes
+    float* stage = s_stage + warp * kStageWarp;
+    double sw = 0.0, mw = 0.0, st = 0.0, mt = 0.0;
+    float* raw = reinterpret_cast<float*>(pool + off);
+    if (live) {
+        rec.goff = gneed ? gbase + gex + 4u : 0u;
+        const double wire_edge = P.origin_x + ((double)f.w0 - (double)P.pad_w) * P.pitch;
+        const double tick_edge = P.origin_t + ((double)f.t0 - (double)P.pad_t) * P.tick;
+        float* dst = staged ? stage + wex : raw;
+        if (fast) {
+            float* tv = dst + f.n_w + n_eff;
+            bin_integrals_f32(d.x, d.sigma_x, wire_edge, P.pitch, f.n_w, [&](int i, float v) { dst[i] = v; }, sw,
+                              mw);
+            bin_integrals_f32(d.t, d.sigma_t, tick_edge, P.tick, f.n_t, [&](int i, float v) { tv[i] = v; }, st, mt);
+        } else {
+            double o4[4];
+            sample_f64_ool(&d, wire_edge, P.pitch, f.n_w, tick_edge, P.tick, f.n_t, dst, dst + f.n_w + n_eff, o4);
+            sw = o4[0];
+            mw = o4[1];
+            st = o4[2];
+            mt = o4[3];
+        }
+        if (n_eff) {
+            float* eff = dst + f.n_w;
+            for (int j = 0; j < n_eff; ++j) {
+                float e = 0.0f;
+                for (int dw = -h; dw <= h; ++dw) {
+                    const int i = j - h - dw;
+                    if (i >= 0 && i < f.n_w) e = fmaf((float)P.ww[dw + h], dst[i], e);
+                }
+                eff[j] = e;
+            }
+        }
+    }
+    // coalesced write-out of the staged prefix [base, base + n_staged)
+    __syncwarp();
+    uint32_t n_staged = staged ? wex + words : 0u;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) n_staged = max(n_staged, __shfl_xor_sync(0xffffffffu, n_staged, o));
+    float* pw = reinterpret_cast<float*>(pool) + base;
+    for (uint32_t k = lane; k < n_staged; k += 32) pw[k] = stage[k];
+    // sum_w sum_t wv*tv > 0  <=>  max(wv)*max(tv) > 0; numerically empty
+    // (rasterize.cpp:111-116) -> clipped charge (pipeline.cpp:339-340)
+    bool emit = live;
+    if (live && !(mw * mt > 0.0)) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[0]), (unsigned long long)d.q);
+        emit = false;
+    }
+    if (emit) {
+        // S = q * p = a * wv[w] * tv[t] with a = q / total (applied by the consumers)
+        rec.a = (float)((double)d.q / (sw * st));
+        rec.tsum = __double2float_ru(st);
+        rec.w0 = f.w0;
+        rec.t0 = f.t0;
+        rec.n_w = f.n_w;
+        rec.n_t = f.n_t;
+        rec.pool = off;
+    } else {
+        rec.goff = 0;
+    }
+    if (in_range) recs[u] = rec;
+    if (ev.mode != 0) return;  // warp-uniform
+    const bool fixed = emit && ev.tile_cap != 0 && P.direct;
+    if (emit && !fixed)  // counts for the CSR lists (k_scan_bands -> k_fill_bands)
+        for_each_bin(P, f.w0, f.n_w, f.t0, f.n_t, [&](int c) { atomicAdd(&band_count[P.band_base + c], 1u); });
+    if (__any_sync(0xffffffffu, fixed)) {
+        // fixed-capacity tile lists: this warp's entries straight away (the
+        // profile from the staging copy, or the lane's own global writes)
+        const float* prof = staged ? stage + wex : raw;
+        const uint32_t cap = ev.tile_cap;
+        emit_tile_entries<false>(P, rec, fixed, prof, ev.tile_count, [&](uint32_t b, uint32_t slot, const TEnt& e) {
+            if (slot < cap)
+                ev.tiles[(size_t)b * cap + slot] = e;
+            else
+                atomicOr(err, kErrTileCap);
+        });
+    }
+}
+
+// Exclusive scan of bin counts (single block); resets the fill cursors.
+__global__ void __launch_bounds__(1024) k_scan_bands(const uint32_t* __restrict__ count, uint32_t* __restrict__ off,
+                                                    uint32_t* __restrict__ fill, uint32_t n)
+{
+    // one pass: each thread scans kPer consecutive counts in registers, the
+    // block scans the 1024 partial sums (two warp-shuffle levels), carry
+    // across passes only for n > 1024 * kPer
+    constexpr int kPer = 8;
+    __shared__ uint32_t warp_sums[32];
+    __shared__ uint32_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll 1
+    for (uint32_t base = 0; base < n; base += 1024u * kPer) {
+        const uint32_t i0 = base + threadIdx.x * kPer;
+        uint32_t v[kPer], sum = 0;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            v[k] = i0 + k < n ? __ldg(count + i0 + k) : 0u;
+            sum += v[k];
+        }
+        uint32_t x = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        __syncthreads();  // carry / warp_sums of the previous pass consumed
+        if (lane == 31) warp_sums[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            uint32_t t = warp_sums[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+                if (lane >= o) t += y;
+            }
+            warp_sums[lane] = t;
+        }
+        __syncthreads();
+        uint32_t run = carry + (wid ? warp_sums[wid - 1] : 0u) + x - sum;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k)
+            if (i0 + k < n) {
+                off[i0 + k] = run;
+                fill[i0 + k] = 0;
+                run += v[k];
+            }
+        __syncthreads();
+        if (threadIdx.x == 1023) carry = run;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) off[n] = carry;
+}
+
+// Thread per unit: append the unit to the list of every bin it touches.
+// FFT planes list the unit record per band; direct planes list, per tile,
+// the entry k_direct consumes: tick span, profile offset and the
+// coefficient a eff[w] of each tile row (independent of k_gprof, which may
+// run concurrently on the auxiliary stream). Lists larger
+// than ev.list_cap (the scan's total) flag kErrRange and write nothing.
 __global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ recs, const uint32_t* __restrict__ off,
                              uint32_t* __restrict__ fill, UnitRec* __restrict__ list, TEnt* __restrict__ tlist,
                              const uint32_t* __restrict__ pool, unsigned* __restrict__ err)
