@@ -514,7 +514,12 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
     }
     WS_CUDA(cudaEventRecord(pc.ev[2], s));
     if (ev.mode == 0) {
-        if (any_direct) {
+        if (any_direct && ev.tile_cap) {
+            // fixed tile lists: the binning happened in the sampler, the
+            // profiles are all that is left before k_direct (same stream)
+            WS_CUDA(wsb_launch_gprof(ev, c->recs.p, c->pool.p, s));
+            c->launches += units ? 1 : 0;
+        } else if (any_direct) {
             // response profiles on the auxiliary stream, concurrent with the
             // binning (k_direct is the first consumer)
             if (!c->aux_stream) {
@@ -538,7 +543,8 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
                                     c->tile_list.p, c->pool.p, &hdr->err, s));
             c->launches += 1 + (units ? 1 : 0);
         }
-        if (any_direct) WS_CUDA(cudaStreamWaitEvent(s, c->aux_join, 0));  // profiles ready (bin stage ends)
+        if (any_direct && !ev.tile_cap)
+            WS_CUDA(cudaStreamWaitEvent(s, c->aux_join, 0));  // profiles ready (bin stage ends)
     }
     WS_CUDA(cudaEventRecord(pc.ev[3], s));
     if (ev.mode == 0 && charges) {
