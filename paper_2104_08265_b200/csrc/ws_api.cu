@@ -393,6 +393,8 @@ int check_opts(const ws_sim_options* o)
 
 // Launch one group of <= kMaxPlanes planes. frames/charges are device
 // pointers (frames[i] may be null when only charge is wanted).
+int finish_pending(ws_ctx* c);
+
 int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* const* depos, const uint64_t* n_depos,
               const ws_sim_options* opt, float* const* frames, float* const* charges, const float* const* charge_in,
               ws_timing* timing)
@@ -484,8 +486,17 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
     } else if (any_direct) {
         WS_CUDA(c->tile_list.reserve(list_cap));
     }
-    WS_CUDA(c->header.reserve(1));
-    ScratchHeader* hdr = c->header.p;
+    // per-call header in a device ring (zeroed when allocated and after each
+    // read-back), copied to the host at synchronize: no per-call memset / D2H
+    if (!c->header.p) {
+        WS_CUDA(c->header.reserve(kStatSlots));
+        WS_CUDA(cudaMemsetAsync(c->header.p, 0, sizeof(ScratchHeader) * kStatSlots, s));
+    }
+    if ((int)c->pending.size() >= kStatSlots)
+        if (int rc = finish_pending(c)) return rc;  // ring full: drain (reads and re-zeroes the slots)
+    const int slot = c->next_slot;
+    c->next_slot = (c->next_slot + 1) % kStatSlots;
+    ScratchHeader* hdr = c->header.p + slot;
     for (uint32_t i = 0; i < n; ++i) ev.p[i].stats = &hdr->stats[2 * i];
 
     PendingCall pc{};
@@ -496,7 +507,6 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
     for (int k = 0; k < 6; ++k) pc.ev[k] = take_event(c);
 
     WS_CUDA(cudaEventRecord(pc.ev[0], s));
-    WS_CUDA(cudaMemsetAsync(hdr, 0, sizeof(ScratchHeader), s));
     if (ev.mode == 0) WS_CUDA(cudaMemsetAsync(c->band_count.p, 0, sizeof(uint32_t) * (bands + 1), s));
 
     if (ev.fluctuate && !from_grid)
@@ -566,14 +576,7 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
         }
     }
     WS_CUDA(cudaEventRecord(pc.ev[4], s));
-    // per-call copy of the header into a pinned slot, read at synchronize
-    if ((int)c->pending.size() >= kStatSlots) {
-        // too many calls in flight: drain
-        WS_CUDA(cudaStreamSynchronize(s));
-    }
-    pc.slot = c->next_slot;
-    c->next_slot = (c->next_slot + 1) % kStatSlots;
-    WS_CUDA(cudaMemcpyAsync(&c->host_slots[pc.slot], hdr, sizeof(ScratchHeader), cudaMemcpyDeviceToHost, s));
+    pc.slot = slot;
     WS_CUDA(cudaEventRecord(pc.ev[5], s));
     c->pending.push_back(pc);
     return WS_OK;
@@ -582,6 +585,12 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
 int finish_pending(ws_ctx* c)
 {
     WS_CUDA(cudaStreamSynchronize(c->stream));
+    if (!c->pending.empty()) {
+        // the ring's headers of the pending calls -> host, then zero them for reuse
+        WS_CUDA(cudaMemcpy(c->host_slots, c->header.p, sizeof(ScratchHeader) * kStatSlots, cudaMemcpyDeviceToHost));
+        for (const PendingCall& pc : c->pending)
+            WS_CUDA(cudaMemsetAsync(c->header.p + pc.slot, 0, sizeof(ScratchHeader), c->stream));
+    }
     int rc = WS_OK;
     for (PendingCall& pc : c->pending) {
         const ScratchHeader& h = c->host_slots[pc.slot];
