@@ -37,7 +37,7 @@ extern "C" cudaError_t wsb_launch_noise_spectrum(const wsb::PlaneDesc& P, const 
 extern "C" size_t wsb_direct_smem(int cap);
 extern "C" int wsb_direct_cap();
 extern "C" cudaError_t wsb_launch_direct(const EventDesc& ev, const uint32_t* pool, const uint32_t* band_off,
-                                         const wsb::TEnt* tlist, size_t smem_bytes, cudaStream_t stream);
+                                         const wsb::TEnt* tlist, size_t smem_bytes, cudaStream_t stream, int pdl);
 extern "C" cudaError_t wsb_launch_fluctuate(const EventDesc& ev, const UnitRec* recs, const uint32_t* pool,
                                             const uint32_t* order, cudaStream_t s);
 extern "C" size_t wsb_sigproc_smem(int n);
@@ -504,9 +504,10 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
     pc.n_planes = (int)n;
     for (uint32_t i = 0; i < n; ++i) pc.direct_planes += ev.p[i].direct;
     pc.fluctuate = ev.fluctuate;
-    for (int k = 0; k < 6; ++k) pc.ev[k] = take_event(c);
+    if (timing)
+        for (int k = 0; k < 6; ++k) pc.ev[k] = take_event(c);
 
-    WS_CUDA(cudaEventRecord(pc.ev[0], s));
+    if (timing) WS_CUDA(cudaEventRecord(pc.ev[0], s));  // stage timing only
     if (ev.mode == 0) WS_CUDA(cudaMemsetAsync(c->band_count.p, 0, sizeof(uint32_t) * (bands + 1), s));
 
     if (ev.fluctuate && !from_grid)
@@ -517,12 +518,12 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
                                   &hdr->pool_ctr, c->band_count.p, &hdr->err, s));
         c->launches += units ? 1 : 0;
     }
-    WS_CUDA(cudaEventRecord(pc.ev[1], s));
+    if (timing) WS_CUDA(cudaEventRecord(pc.ev[1], s));  // stage timing only
     if (ev.fluctuate && !from_grid) {
         WS_CUDA(wsb_launch_fluctuate(ev, c->recs.p, c->pool.p, nullptr, s));
         c->launches += units ? (ev.approx ? 1 : 2) : 0;  // exact: key kernel + walk (the CUB sort between is library code)
     }
-    WS_CUDA(cudaEventRecord(pc.ev[2], s));
+    if (timing) WS_CUDA(cudaEventRecord(pc.ev[2], s));  // stage timing only
     if (ev.mode == 0) {
         if (any_direct && ev.tile_cap) {
             // fixed tile lists: the binning happened in the sampler, the
@@ -556,7 +557,7 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
         if (any_direct && !ev.tile_cap)
             WS_CUDA(cudaStreamWaitEvent(s, c->aux_join, 0));  // profiles ready (bin stage ends)
     }
-    WS_CUDA(cudaEventRecord(pc.ev[3], s));
+    if (timing) WS_CUDA(cudaEventRecord(pc.ev[3], s));  // stage timing only
     if (ev.mode == 0 && charges) {
         // the charge grid is the un-stencilled S: an accumulate-only pass of
         // the row kernel over every band (parity / inspection output)
@@ -566,8 +567,11 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
     if (want_frame) {
         // each kernel skips the other's planes
         if (any_direct) {
+            // programmatic launch after the profiles kernel on the same stream
+            // (fixed tile lists, no charge pass in between)
+            const int pdl = ev.tile_cap != 0 && !(ev.mode == 0 && charges) ? 1 : 0;
             WS_CUDA(wsb_launch_direct(ev, c->pool.p, c->band_off.p, c->tile_list.p, wsb_direct_smem(wsb_direct_cap()),
-                                      s));
+                                      s, pdl));
             c->launches += bands ? 1 : 0;
         }
         if (any_fft) {
@@ -575,9 +579,9 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
             c->launches += bands ? 1 : 0;
         }
     }
-    WS_CUDA(cudaEventRecord(pc.ev[4], s));
+    if (timing) WS_CUDA(cudaEventRecord(pc.ev[4], s));  // stage timing only
     pc.slot = slot;
-    WS_CUDA(cudaEventRecord(pc.ev[5], s));
+    if (timing) WS_CUDA(cudaEventRecord(pc.ev[5], s));  // stage timing only
     c->pending.push_back(pc);
     return WS_OK;
 }
@@ -632,7 +636,8 @@ int finish_pending(ws_ctx* c)
                 t.clipped_patches += h.stats[2 * i + 1];
             }
         }
-        for (int k = 0; k < 6; ++k) c->event_pool.push_back(pc.ev[k]);
+        if (pc.timing)
+            for (int k = 0; k < 6; ++k) c->event_pool.push_back(pc.ev[k]);
     }
     c->pending.clear();
     return rc;

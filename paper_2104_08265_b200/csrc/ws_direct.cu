@@ -221,6 +221,10 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
     }
     __syncthreads();
 
+    // the profiles come from the previous kernel (k_gprof_umma): with a
+    // programmatic launch everything above overlapped its tail
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+
     // accumulate, one warp per entry: lane j adds round(c_w g[j] scale_w) to
     // tick ts + j of every covered row (consecutive lanes -> consecutive
     // banks); ticks outside the window go to the lane's margin slot. Each
@@ -336,7 +340,7 @@ extern "C" int wsb_direct_cap()
 }
 
 extern "C" cudaError_t wsb_launch_direct(const wsb::EventDesc& ev, const uint32_t* pool, const uint32_t* band_off,
-                                         const wsb::TEnt* tlist, size_t smem_bytes, cudaStream_t stream)
+                                         const wsb::TEnt* tlist, size_t smem_bytes, cudaStream_t stream, int pdl)
 {
     constexpr int NT = wsb::kDirectThreads;
     static std::atomic<unsigned long long> ready{0};  // per-device attribute setup (idempotent)
@@ -351,6 +355,22 @@ extern "C" cudaError_t wsb_launch_direct(const wsb::EventDesc& ev, const uint32_
         ready |= 1ull << dev;
     }
     if (ev.total_bands == 0) return cudaSuccess;
-    wsb::k_direct<NT><<<ev.total_bands, NT, smem_bytes, stream>>>(ev, pool, band_off, tlist);
-    return cudaGetLastError();
+    if (!pdl) {
+        wsb::k_direct<NT><<<ev.total_bands, NT, smem_bytes, stream>>>(ev, pool, band_off, tlist);
+        return cudaGetLastError();
+    }
+    // programmatic dependent launch: the tiles' prologue (zeroing, staging,
+    // bounds) runs while the previous kernel drains; griddepcontrol.wait
+    // guards the profile reads
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(ev.total_bands);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem_bytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, wsb::k_direct<NT>, ev, pool, band_off, tlist);
 }

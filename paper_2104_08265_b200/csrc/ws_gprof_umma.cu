@@ -55,6 +55,9 @@ __device__ __forceinline__ void um_mma(uint32_t tmem_d, uint64_t a, uint64_t b, 
 __global__ void __launch_bounds__(kUmThreads) k_gprof_umma(const EventDesc ev, const UnitRec* __restrict__ recs,
                                                            uint32_t* __restrict__ pool, int N)
 {
+    // a programmatically launched successor (k_direct) may start its
+    // profile-independent prologue now; it waits for this grid's completion
+    asm volatile("griddepcontrol.launch_dependents;");
     const PlaneDesc& P = ev.p[blockIdx.y];
     if (!P.direct || P.n_units == 0) return;
     const int nl = P.n_lags;
