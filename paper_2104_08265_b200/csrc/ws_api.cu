@@ -28,7 +28,8 @@ extern "C" cudaError_t wsb_launch_scan(const uint32_t* count, uint32_t* off, uin
 extern "C" cudaError_t wsb_launch_fill(const EventDesc& ev, const UnitRec* recs, const uint32_t* off, uint32_t* fill,
                                        UnitRec* list, wsb::TEnt* tlist, const uint32_t* pool, unsigned* err,
                                        cudaStream_t s);
-extern "C" cudaError_t wsb_launch_gprof(const EventDesc& ev, const UnitRec* recs, uint32_t* pool, cudaStream_t s);
+extern "C" cudaError_t wsb_launch_gprof(const EventDesc& ev, const UnitRec* recs, uint32_t* pool, cudaStream_t s,
+                                        int pdl);
 extern "C" cudaError_t wsb_launch_noise(float* frame, int32_t* adc, int W, int N, int noise, int rng_mode, double sigma,
                                         uint64_t seed, double scale, double offset, double max_code, cudaStream_t s);
 extern "C" cudaError_t wsb_launch_noise_spectrum(const wsb::PlaneDesc& P, const double* amp, uint64_t seed, int rng_mode,
@@ -528,7 +529,7 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
         if (any_direct && ev.tile_cap) {
             // fixed tile lists: the binning happened in the sampler, the
             // profiles are all that is left before k_direct (same stream)
-            WS_CUDA(wsb_launch_gprof(ev, c->recs.p, c->pool.p, s));
+            WS_CUDA(wsb_launch_gprof(ev, c->recs.p, c->pool.p, s, timing ? 0 : 1));  // programmatic after the sampler
             c->launches += units ? 1 : 0;
         } else if (any_direct) {
             // response profiles on the auxiliary stream, concurrent with the
@@ -544,7 +545,7 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
             }
             WS_CUDA(cudaEventRecord(c->aux_fork, s));
             WS_CUDA(cudaStreamWaitEvent(c->aux_stream, c->aux_fork, 0));
-            WS_CUDA(wsb_launch_gprof(ev, c->recs.p, c->pool.p, c->aux_stream));
+            WS_CUDA(wsb_launch_gprof(ev, c->recs.p, c->pool.p, c->aux_stream, 0));
             WS_CUDA(cudaEventRecord(c->aux_join, c->aux_stream));
             c->launches += units ? 1 : 0;
         }

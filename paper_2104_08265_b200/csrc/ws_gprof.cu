@@ -243,10 +243,10 @@ k_gprof(const EventDesc ev, const UnitRec* __restrict__ recs, uint32_t* __restri
 
 extern "C" int wsb_gprof_umma_n(const wsb::EventDesc& ev);
 extern "C" cudaError_t wsb_launch_gprof_umma(const wsb::EventDesc& ev, const wsb::UnitRec* recs, uint32_t* pool,
-                                             int N, cudaStream_t s);
+                                             int N, cudaStream_t s, int pdl);
 
 extern "C" cudaError_t wsb_launch_gprof(const wsb::EventDesc& ev, const wsb::UnitRec* recs, uint32_t* pool,
-                                        cudaStream_t s)
+                                        cudaStream_t s, int pdl)
 {
     // tcgen05 path (ws_gprof_umma.cu) unless a kernel is too long for it or
     // WS_GPROF_MMASYNC=1 selects the warp-level mma.sync kernel below
@@ -256,7 +256,7 @@ extern "C" cudaError_t wsb_launch_gprof(const wsb::EventDesc& ev, const wsb::Uni
     }();
     if (!mmasync) {
         const int N = wsb_gprof_umma_n(ev);
-        if (N > 0) return wsb_launch_gprof_umma(ev, recs, pool, N, s);
+        if (N > 0) return wsb_launch_gprof_umma(ev, recs, pool, N, s, pdl);
     }
     uint32_t max_units = 0;
     int max_lags = 0;

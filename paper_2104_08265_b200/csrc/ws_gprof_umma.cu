@@ -55,9 +55,6 @@ __device__ __forceinline__ void um_mma(uint32_t tmem_d, uint64_t a, uint64_t b, 
 __global__ void __launch_bounds__(kUmThreads) k_gprof_umma(const EventDesc ev, const UnitRec* __restrict__ recs,
                                                            uint32_t* __restrict__ pool, int N)
 {
-    // a programmatically launched successor (k_direct) may start its
-    // profile-independent prologue now; it waits for this grid's completion
-    asm volatile("griddepcontrol.launch_dependents;");
     const PlaneDesc& P = ev.p[blockIdx.y];
     if (!P.direct || P.n_units == 0) return;
     const int nl = P.n_lags;
@@ -129,6 +126,14 @@ __global__ void __launch_bounds__(kUmThreads) k_gprof_umma(const EventDesc ev, c
 #pragma unroll
         for (int k = 0; k < kH; ++k) vals[k] = ok && kH * half + k < rec.n_t ? __ldg(t + kH * half + k) : 0.0f;
     };
+    // the records and tick profiles come from the previous kernel (k_sample_off);
+    // with a programmatic launch the TMEM / barrier / Toeplitz setup above
+    // overlapped its tail
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // the sampler has completed: a programmatically launched successor
+    // (k_direct) may now run its profile-independent prologue (it reads the
+    // sampler's tile lists), waiting for this grid before the profiles
+    asm volatile("griddepcontrol.launch_dependents;");
     UnitRec rec_n;
     float vals_n[kH];
     fetch(blockIdx.x, rec_n, vals_n);
@@ -259,7 +264,7 @@ extern "C" int wsb_gprof_umma_n(const wsb::EventDesc& ev)
 }
 
 extern "C" cudaError_t wsb_launch_gprof_umma(const wsb::EventDesc& ev, const wsb::UnitRec* recs, uint32_t* pool,
-                                             int N, cudaStream_t s)
+                                             int N, cudaStream_t s, int pdl)
 {
     uint32_t max_units = 0;
     for (int i = 0; i < ev.n_planes; ++i)
@@ -281,6 +286,20 @@ extern "C" cudaError_t wsb_launch_gprof_umma(const wsb::EventDesc& ev, const wsb
     // persistent: two CTAs per SM over the planes (B staged once per CTA)
     const unsigned per_plane = std::max(1u, (unsigned)(2 * sms) / (unsigned)ev.n_planes);
     const dim3 grid(std::min(tiles, per_plane), (unsigned)ev.n_planes);
-    wsb::k_gprof_umma<<<grid, wsb::kUmThreads, smem, s>>>(ev, recs, pool, N);
+    if (!pdl) {
+        wsb::k_gprof_umma<<<grid, wsb::kUmThreads, smem, s>>>(ev, recs, pool, N);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(wsb::kUmThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, wsb::k_gprof_umma, ev, recs, pool, N);
     return cudaGetLastError();
 }

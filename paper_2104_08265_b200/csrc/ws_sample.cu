@@ -402,6 +402,7 @@ k_sample_off(const EventDesc ev, UnitRec* __restrict__ recs, uint32_t* __restric
              uint32_t* __restrict__ pool_ctr, uint32_t* __restrict__ band_count, unsigned* __restrict__ err)
 {
     extern __shared__ float s_stage[];
+    asm volatile("griddepcontrol.launch_dependents;");  // the profiles kernel may set up meanwhile
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
     const bool in_range = u < ev.total_units;

@@ -184,3 +184,25 @@ def test_direct_wide_and_narrow_depos(pctx, oracle, kind):
     assert relL2_per_channel(m, m_ref) < TOL_FRAME
     m_fft = _frame(pctx, "fft", SMALL, resp, depos)
     assert relL2_per_channel(m_fft, m_ref) < TOL_FRAME
+
+
+def test_untimed_device_event_equals_timed(pctx):
+    """The untimed device path chains its three kernels with programmatic
+    dependent launches (the profile and tile kernels start while their
+    predecessor drains); its frames must equal the timed host path's bitwise,
+    call after call."""
+    import torch
+    from paper_2104_08265_b200 import simulate_event_device
+    grids, resps = microboone_grids()
+    planes = [Plane(pctx, g, r) for g, r in zip(grids, resps)]
+    ev = microboone_event(100_000, seed=21)
+    cfg = SimConfig(fluctuate=False)
+    want = [p.simulate(d, SimConfig(grid=g, response=r, fluctuate=False)).frame
+            for p, d, g, r in zip(planes, ev, grids, resps)]
+    dev = [torch.from_numpy(d.view(np.uint8)).cuda() for d in ev]
+    frames = [torch.empty(p.shape, dtype=torch.float32, device="cuda") for p in planes]
+    for _ in range(3):
+        simulate_event_device(pctx, planes, dev, [len(d) for d in ev], cfg, frames)
+        pctx.synchronize()
+        for f, w in zip(frames, want):
+            assert np.array_equal(f.cpu().numpy(), w)
