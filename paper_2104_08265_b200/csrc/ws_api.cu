@@ -24,7 +24,7 @@ using wsb::UnitRec;
 
 extern "C" cudaError_t wsb_launch_sample(const EventDesc& ev, UnitRec* recs, uint32_t* pool, uint32_t pool_cap,
                                          uint32_t* pool_ctr, uint32_t* band_count, unsigned* err, cudaStream_t s);
-extern "C" cudaError_t wsb_launch_scan(const uint32_t* count, uint32_t* off, uint32_t* fill, uint32_t n, cudaStream_t s);
+extern "C" cudaError_t wsb_launch_scan(uint32_t* count, uint32_t* off, uint32_t* fill, uint32_t n, cudaStream_t s);
 extern "C" cudaError_t wsb_launch_fill(const EventDesc& ev, const UnitRec* recs, const uint32_t* off, uint32_t* fill,
                                        UnitRec* list, wsb::TEnt* tlist, const uint32_t* pool, unsigned* err,
                                        cudaStream_t s);
@@ -458,7 +458,14 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
     const size_t pool_need = std::max<size_t>(c->pool_hint, (size_t)units * (96 + (any_direct ? max_lags + 36 : 0)) + 4096);
     WS_CUDA(c->recs.reserve(units));
     WS_CUDA(c->pool.reserve(pool_need));
-    WS_CUDA(c->band_count.reserve(bands + 1));
+    {
+        // the counts are zeroed by their consumer (k_scan_bands / k_direct)
+        // for the next call; a fresh allocation is zeroed here
+        const size_t cap0 = c->band_count.cap;
+        WS_CUDA(c->band_count.reserve(bands + 1));
+        if (c->band_count.cap != cap0)
+            WS_CUDA(cudaMemsetAsync(c->band_count.p, 0, sizeof(uint32_t) * c->band_count.cap, s));
+    }
     WS_CUDA(c->band_off.reserve(bands + 1));
     WS_CUDA(c->band_fill.reserve(bands + 1));
     int max_h = 0;
@@ -476,7 +483,7 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
         const char* v = getenv("WS_TILE_CSR");
         return v && v[0] == '1';
     }();
-    const bool use_fixed = any_direct && !any_fft && ev.mode == 0 && !ev.fluctuate && !csr_only && bands > 0;
+    const bool use_fixed = any_direct && !any_fft && ev.mode == 0 && !ev.fluctuate && !csr_only && bands > 0 && want_frame;
     ev.tile_cap = 0;
     ev.tiles = nullptr;
     ev.tile_count = c->band_count.p;
@@ -509,7 +516,6 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
         for (int k = 0; k < 6; ++k) pc.ev[k] = take_event(c);
 
     if (timing) WS_CUDA(cudaEventRecord(pc.ev[0], s));  // stage timing only
-    if (ev.mode == 0) WS_CUDA(cudaMemsetAsync(c->band_count.p, 0, sizeof(uint32_t) * (bands + 1), s));
 
     if (ev.fluctuate && !from_grid)
         for (uint32_t i = 0; i < n; ++i)

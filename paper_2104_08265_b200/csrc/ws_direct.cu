@@ -139,7 +139,7 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
     }
 
     const uint32_t lo = fixed ? gb * ev.tile_cap : __ldg(&band_off[gb]);
-    const int n = fixed ? (int)min(__ldg(&ev.tile_count[gb]), ev.tile_cap) : (int)(__ldg(&band_off[gb + 1]) - lo);
+    const int n = fixed ? (int)min(ev.tile_count[gb], ev.tile_cap) : (int)(__ldg(&band_off[gb + 1]) - lo);
     if (fixed) tlist = ev.tiles;
     const uint32_t s_ent = (uint32_t)__cvta_generic_to_shared(ent);
 
@@ -220,6 +220,7 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
         }
     }
     __syncthreads();
+    if (fixed && tid == 0) ev.tile_count[gb] = 0;  // every thread has read it: zero for the next call
 
     // the profiles come from the previous kernel (k_gprof_umma): with a
     // programmatic launch everything above overlapped its tail

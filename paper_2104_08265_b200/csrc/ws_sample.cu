@@ -546,7 +546,7 @@ k_sample_off(const EventDesc ev, UnitRec* __restrict__ recs, uint32_t* __restric
 }
 
 // Exclusive scan of bin counts (single block); resets the fill cursors.
-__global__ void __launch_bounds__(1024) k_scan_bands(const uint32_t* __restrict__ count, uint32_t* __restrict__ off,
+__global__ void __launch_bounds__(1024) k_scan_bands(uint32_t* __restrict__ count, uint32_t* __restrict__ off,
                                                     uint32_t* __restrict__ fill, uint32_t n)
 {
     // one pass: each thread scans kPer consecutive counts in registers, the
@@ -563,7 +563,7 @@ __global__ void __launch_bounds__(1024) k_scan_bands(const uint32_t* __restrict_
         uint32_t v[kPer], sum = 0;
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
-            v[k] = i0 + k < n ? __ldg(count + i0 + k) : 0u;
+            v[k] = i0 + k < n ? count[i0 + k] : 0u;
             sum += v[k];
         }
         uint32_t x = sum;
@@ -591,6 +591,7 @@ __global__ void __launch_bounds__(1024) k_scan_bands(const uint32_t* __restrict_
             if (i0 + k < n) {
                 off[i0 + k] = run;
                 fill[i0 + k] = 0;
+                count[i0 + k] = 0;  // zero for the next call (no memset per call)
                 run += v[k];
             }
         __syncthreads();
@@ -868,7 +869,7 @@ extern "C" cudaError_t wsb_launch_sample(const wsb::EventDesc& ev, wsb::UnitRec*
     return cudaGetLastError();
 }
 
-extern "C" cudaError_t wsb_launch_scan(const uint32_t* count, uint32_t* off, uint32_t* fill, uint32_t n, cudaStream_t s)
+extern "C" cudaError_t wsb_launch_scan(uint32_t* count, uint32_t* off, uint32_t* fill, uint32_t n, cudaStream_t s)
 {
     wsb::k_scan_bands<<<1, 1024, 0, s>>>(count, off, fill, n);
     return cudaGetLastError();
