@@ -23,7 +23,8 @@ using wsb::PlaneDesc;
 using wsb::UnitRec;
 
 extern "C" cudaError_t wsb_launch_sample(const EventDesc& ev, UnitRec* recs, uint32_t* pool, uint32_t pool_cap,
-                                         uint32_t* pool_ctr, uint32_t* band_count, unsigned* err, cudaStream_t s);
+                                         uint32_t* pool_ctr, uint32_t* band_count, unsigned* err, cudaStream_t s,
+                                         int pdl);
 extern "C" cudaError_t wsb_launch_scan(uint32_t* count, uint32_t* off, uint32_t* fill, uint32_t n, cudaStream_t s);
 extern "C" cudaError_t wsb_launch_fill(const EventDesc& ev, const UnitRec* recs, const uint32_t* off, uint32_t* fill,
                                        UnitRec* list, wsb::TEnt* tlist, const uint32_t* pool, unsigned* err,
@@ -522,7 +523,7 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
             WS_CUDA(cudaMemsetAsync(ev.p[i].charge_out, 0, sizeof(float) * (size_t)ev.p[i].W * ev.p[i].N, s));
     if (!from_grid) {
         WS_CUDA(wsb_launch_sample(ev, c->recs.p, c->pool.p, (uint32_t)std::min<size_t>(c->pool.cap, 0xffffffffu),
-                                  &hdr->pool_ctr, c->band_count.p, &hdr->err, s));
+                                  &hdr->pool_ctr, c->band_count.p, &hdr->err, s, timing ? 0 : 1));
         c->launches += units ? 1 : 0;
     }
     if (timing) WS_CUDA(cudaEventRecord(pc.ev[1], s));  // stage timing only

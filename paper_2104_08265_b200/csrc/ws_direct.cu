@@ -106,6 +106,9 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
     constexpr int kRShift = R == 16 ? 4 : R == 8 ? 3 : R == 4 ? 2 : 1;
     const uint32_t gb = blockIdx.x;
     const PlaneDesc& P = ev.p[band_plane(ev, gb)];
+    // the next call's sampler may launch now (it waits for this grid before
+    // touching the pool, the records or the tile lists)
+    asm volatile("griddepcontrol.launch_dependents;");
     if (!P.direct) return;
     const bool fixed = ev.tile_cap != 0;  // fixed-capacity tile lists filled by the sampler
     if (!fixed && __ldg(&band_off[ev.total_bands]) > ev.list_cap) return;

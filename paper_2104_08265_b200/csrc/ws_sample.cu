@@ -464,6 +464,10 @@ k_sample_off(const EventDesc ev, UnitRec* __restrict__ recs, uint32_t* __restric
         live = false;
     }
     const uint32_t off = base + wex;
+    // everything above touched only this call's header slot; the pool, the
+    // records and the tile lists may still be in use by the previous call's
+    // k_direct when this kernel was launched programmatically behind it
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const bool fast = live && d.sigma_x * 4.0 >= P.pitch && d.sigma_t * 4.0 >= P.tick;
     // the staged prefix of the warp's profile words (compact, same order as the pool)
     const bool staged = live && wex + words <= (uint32_t)kStageWarp;  // a prefix of the lanes
@@ -854,7 +858,8 @@ __global__ void __launch_bounds__(128) k_fluctuate_exact(const EventDesc ev, con
 }  // namespace wsb
 
 extern "C" cudaError_t wsb_launch_sample(const wsb::EventDesc& ev, wsb::UnitRec* recs, uint32_t* pool, uint32_t pool_cap,
-                                         uint32_t* pool_ctr, uint32_t* band_count, unsigned* err, cudaStream_t s)
+                                         uint32_t* pool_ctr, uint32_t* band_count, unsigned* err, cudaStream_t s,
+                                         int pdl)
 {
     if (ev.total_units == 0) return cudaSuccess;
     const uint32_t threads = 128;
@@ -863,8 +868,25 @@ extern "C" cudaError_t wsb_launch_sample(const wsb::EventDesc& ev, wsb::UnitRec*
         wsb::k_sample<true><<<blocks, threads, 0, s>>>(ev, recs, pool, pool_cap, pool_ctr, band_count, err);
     } else {
         constexpr size_t smem = sizeof(float) * (wsb::kSampleThreads / 32) * wsb::kStageWarp;
-        wsb::k_sample_off<<<(ev.total_units + wsb::kSampleThreads - 1) / wsb::kSampleThreads, wsb::kSampleThreads,
-                            smem, s>>>(ev, recs, pool, pool_cap, pool_ctr, band_count, err);
+        const unsigned grid = (ev.total_units + wsb::kSampleThreads - 1) / wsb::kSampleThreads;
+        if (!pdl) {
+            wsb::k_sample_off<<<grid, wsb::kSampleThreads, smem, s>>>(ev, recs, pool, pool_cap, pool_ctr, band_count,
+                                                                       err);
+            return cudaGetLastError();
+        }
+        // programmatic launch behind the previous call's k_direct (footprints
+        // and pool allocation overlap its tail; griddepcontrol.wait guards the rest)
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(wsb::kSampleThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, wsb::k_sample_off, ev, recs, pool, pool_cap, pool_ctr, band_count, err);
     }
     return cudaGetLastError();
 }

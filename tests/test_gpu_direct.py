@@ -206,3 +206,16 @@ def test_untimed_device_event_equals_timed(pctx):
         pctx.synchronize()
         for f, w in zip(frames, want):
             assert np.array_equal(f.cpu().numpy(), w)
+    # back to back without synchronisation (each call's sampler launched
+    # programmatically behind the previous call's k_direct): A, B, A
+    ev_b = microboone_event(60_000, seed=22)
+    want_b = [p.simulate(d, SimConfig(grid=g, response=r, fluctuate=False)).frame
+              for p, d, g, r in zip(planes, ev_b, grids, resps)]
+    dev_b = [torch.from_numpy(d.view(np.uint8)).cuda() for d in ev_b]
+    outs = [[torch.empty(p.shape, dtype=torch.float32, device="cuda") for p in planes] for _ in range(3)]
+    for k, (dv, e) in enumerate([(dev, ev), (dev_b, ev_b), (dev, ev)]):
+        simulate_event_device(pctx, planes, dv, [len(d) for d in e], cfg, outs[k])
+    pctx.synchronize()
+    for k, w_all in enumerate([want, want_b, want]):
+        for f, w in zip(outs[k], w_all):
+            assert np.array_equal(f.cpu().numpy(), w)
