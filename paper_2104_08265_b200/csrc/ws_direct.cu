@@ -9,11 +9,12 @@
 // linearity, M[w, t] = sum_d a_d eff_d[w] g_d[t - t0_d - lo_lag] with
 // eff_d the stencilled wire profile and g_d = tv_d (*) k the depo's tick
 // profile convolved with the combined time kernel (L = n_t + n_lags - 1
-// taps, computed once per depo by k_gprof and shared by all its wire rows).
+// taps, computed once per depo by k_gprof_umma and shared by all its wire rows).
 //
-// One CTA owns a tile of kTileRows wire rows x kTileTicks ticks of the frame
-// in shared memory as int32 fixed point. k_fill_bands has listed the tile's
-// depos (tick span, profile offset, max|g|, per-row coefficients). The CTA
+// One CTA (640 threads, two per SM) owns a tile of kTileRows wire rows x
+// kTileTicks ticks of the frame in shared memory as int32 fixed point. The
+// sampler (fixed-capacity lists) or k_fill_bands (CSR lists) has listed the
+// tile's depos (tick span, profile offset, max|g|, per-row coefficients). The CTA
 // stages the list, bounds every row (per 64-tick segment sum of |terms|,
 // largest term; one thread per entry x row) to fix a per-row power-of-two
 // scale, then one warp per entry loads the depo's profile into registers
@@ -22,11 +23,12 @@
 // integer sums are exact, so the frame is bitwise reproducible for any
 // schedule. Lanes whose tick falls outside the window write to a row margin
 // that is discarded. Work ~ depos x rows x L instead of cells x log(ticks).
+// Launched programmatically behind the profiles kernel: everything before the
+// accumulation (zeroing, staging, bounds) overlaps its tail.
 #include "ws_common.cuh"
 
-#include <atomic>
-
 #include <algorithm>
+#include <atomic>
 
 namespace wsb {
 

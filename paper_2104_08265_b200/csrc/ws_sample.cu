@@ -392,8 +392,10 @@ __device__ __forceinline__ void emit_tile_entries(const PlaneDesc& P, const Unit
 // but the profiles [raw][eff][tv] are written through shared memory: every
 // lane stages its unit's words, then the warp copies unit after unit with
 // coalesced stores (per-lane scattered 4-byte stores were the limiter:
-// 8.4M L2 sectors for 50 MB). Units with more than kStageWords profile words
-// (or the fp64 fallback for sub-quarter-bin widths) write directly.
+// 8.4M L2 sectors for 50 MB). Lanes past the warp's staging capacity write
+// directly. On all-direct events the kernel also appends every unit's tile
+// entries to the fixed-capacity per-tile lists (emit_tile_entries), which
+// replaces the count scan and k_fill_bands.
 constexpr int kSampleThreads = 128;
 constexpr int kStageWarp = 32 * 52;  // staged profile words per warp
 
