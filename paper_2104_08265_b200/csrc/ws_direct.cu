@@ -39,19 +39,35 @@ constexpr int kRowStride = kMargin + kTileTicks + kMargin;  // ints per tile row
 constexpr int kDirectThreads = 640;  // two CTAs per SM
 
 // Fixed-point term round(c g). WS_DIRECT_MAGIC: one FFMA with the magic
-// 1.5 * 2^23 (the mantissa bits hold the rounded value; needs |c g| < 2^22)
-// + one IADD; default: FMUL + F2I.RNI (any |c g| < 2^31, so the scale is set
-// by the segment sums alone: ~16x finer quanta, on the quarter-rate
-// conversion pipe, which runs beside the ALU and shared-memory pipes).
-#ifdef WS_DIRECT_MAGIC
+// 1.5 * 2^23 (the mantissa bits hold the rounded value; needs |c g| < 2^22,
+// so single terms cap the row scale) + one IADD; WS_DIRECT_F2I: FMUL +
+// F2I.RNI on the quarter-rate conversion pipe (r1j: 45% busy, 283 us);
+// default: one DFMA (below; 259 us). The last two allow any term the
+// segment sums allow, so the scale is set by those alone.
+#if defined(WS_DIRECT_MAGIC)
 constexpr bool kTermBudget = true;
+using gtap_t = float;
 __device__ __forceinline__ int fix_rn(float c, float g)
 {
     return __float_as_int(__fmaf_rn(c, g, 12582912.0f)) - 0x4B400000;
 }
-#else
+#elif defined(WS_DIRECT_F2I)
 constexpr bool kTermBudget = false;
+using gtap_t = float;
 __device__ __forceinline__ int fix_rn(float c, float g) { return __float2int_rn(c * g); }
+#else
+// default: one DFMA with the magic 1.5 * 2^52: the low word of the sum is
+// round(c g) of the EXACT product (24 x 24 bits fit the 53-bit mantissa) for
+// any |c g| < 2^51. B200's FP64 pipe runs at half the FP32 rate, so a term
+// costs one half-rate DFMA instead of an FMUL plus a quarter-rate F2I; the
+// taps are widened once per entry and the coefficient once per row.
+constexpr bool kTermBudget = false;
+using gtap_t = double;
+__device__ __forceinline__ int fix_rn_d(double c, double g)
+{
+    return __double2loint(__fma_rn(c, g, 6755399441055744.0));
+}
+__device__ __forceinline__ int fix_rn(float c, float g) { return fix_rn_d((double)c, (double)g); }
 #endif
 
 __device__ __forceinline__ void red_shared(uint32_t saddr, int v)
@@ -72,17 +88,24 @@ __device__ __forceinline__ void red_shared_off(uint32_t saddr, int v)
 // one RED with the tap offset as an instruction immediate.
 template <int NQ>
 __device__ __forceinline__ void scatter_rows(const float* __restrict__ c, int rlo, int rhi, uint32_t a0,
-                                             const float* gv)
+                                             const gtap_t* gv)
 {
     uint32_t ar = a0 + (uint32_t)rlo * (4u * kRowStride);
 #pragma unroll 1
     for (int r = rlo; r < rhi; ++r, ar += 4u * kRowStride) {
+#if defined(WS_DIRECT_MAGIC) || defined(WS_DIRECT_F2I)
         const float cs = c[r];
-        red_shared_off<0>(ar, fix_rn(cs, gv[0]));
-        if constexpr (NQ > 1) red_shared_off<128>(ar, fix_rn(cs, gv[1]));
-        if constexpr (NQ > 2) red_shared_off<256>(ar, fix_rn(cs, gv[2]));
-        if constexpr (NQ > 3) red_shared_off<384>(ar, fix_rn(cs, gv[3]));
-        if constexpr (NQ > 4) red_shared_off<512>(ar, fix_rn(cs, gv[4]));
+#define WS_TERM(q) fix_rn(cs, gv[q])
+#else
+        const double cs = (double)c[r];
+#define WS_TERM(q) fix_rn_d(cs, gv[q])
+#endif
+        red_shared_off<0>(ar, WS_TERM(0));
+        if constexpr (NQ > 1) red_shared_off<128>(ar, WS_TERM(1));
+        if constexpr (NQ > 2) red_shared_off<256>(ar, WS_TERM(2));
+        if constexpr (NQ > 3) red_shared_off<384>(ar, WS_TERM(3));
+        if constexpr (NQ > 4) red_shared_off<512>(ar, WS_TERM(4));
+#undef WS_TERM
     }
 }
 
@@ -237,7 +260,7 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
     // warp holds its entry's profile in registers, the next one in flight.
     constexpr uint32_t row_bytes = 4u * kRowStride;
 
-    auto scatter = [&](const TEnt& d, const float* gv) {  // d: staged, coefficients pre-scaled
+    auto scatter = [&](const TEnt& d, const gtap_t* gv) {  // d: staged, coefficients pre-scaled
         const uint32_t tsL = d.tsL, rows = d.rows;
         const int ts = (int)(tsL & 0xffffu), L = (int)(tsL >> 16);
         const int rlo = (int)(rows & 0xffu), rhi = (int)(rows >> 8);
@@ -297,9 +320,9 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
         load_g(warp, gn);
 #pragma unroll 1
         for (int e = warp; e < cnt; e += NW) {
-            float gv[kQ];
+            gtap_t gv[kQ];
 #pragma unroll
-            for (int q = 0; q < kQ; ++q) gv[q] = gn[q];
+            for (int q = 0; q < kQ; ++q) gv[q] = (gtap_t)gn[q];
             load_g(e + NW, gn);
             scatter(ent[e], gv);
         }
