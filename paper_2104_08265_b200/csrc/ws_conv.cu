@@ -81,27 +81,49 @@ __device__ __forceinline__ void scatter_row(const PlaneDesc& P, int w, bool raw,
                                             const UnitRec* __restrict__ list, uint32_t lo, uint32_t hi, float& inv)
 {
     const int tid = threadIdx.x;
-    // pass 1: bounds per 64-tick segment (electrons, rounded up); the first
-    // kKeep covers of this thread stay in registers for pass 2
+    // pass 1: bounds per 64-tick segment in units of 2^ue electrons (rounded
+    // up); the first kKeep covers of this thread stay in registers for pass
+    // 2. The row's total of all cover bounds (>= every segment sum) decides
+    // whether a 32-bit sum could overflow (extreme charges only): then the
+    // pass re-runs with a 2^16 coarser unit.
     Cover keep[kKeep];
     int keep_at[kKeep];
-    int nkeep = 0;
-    int kdone = 0x7fffffff;  // iterations <= kdone are fully classified
+    int nkeep, kdone, ue = 0;
 #pragma unroll 1
-    for (uint32_t i = lo + tid, k = 0; i < hi; i += NT, ++k) {
-        Cover cv;
-        float tm;
-        if (!cover_of(P, w, raw, list, pool, i, cv, tm)) continue;
-        const unsigned b = (unsigned)fminf(ceilf(fabsf(cv.c) * tm) + 1.0f, 4.0e9f);
-        const int s0 = cv.t0 >> kSegShift, s1 = (cv.t0 + cv.n_t - 1) >> kSegShift;
-        for (int s = s0; s <= s1; ++s) atomicAdd(&segb[s], b);
-        if (nkeep < kKeep) {
-            keep[nkeep] = cv;
-            keep_at[nkeep] = (int)k;
-            if (++nkeep == kKeep) kdone = (int)k;
+    for (;;) {
+        nkeep = 0;
+        kdone = 0x7fffffff;  // iterations <= kdone are fully classified
+        double tot = 0.0;
+#pragma unroll 1
+        for (uint32_t i = lo + tid, k = 0; i < hi; i += NT, ++k) {
+            Cover cv;
+            float tm;
+            if (!cover_of(P, w, raw, list, pool, i, cv, tm)) continue;
+            const float bu = ceilf(ldexpf(fabsf(cv.c) * tm, -ue)) + 1.0f;
+            tot += (double)bu;
+            const unsigned b = (unsigned)fminf(bu, 4.0e9f);
+            const int s0 = cv.t0 >> kSegShift, s1 = (cv.t0 + cv.n_t - 1) >> kSegShift;
+            for (int s = s0; s <= s1; ++s) atomicAdd(&segb[s], b);
+            if (nkeep < kKeep) {
+                keep[nkeep] = cv;
+                keep_at[nkeep] = (int)k;
+                if (++nkeep == kKeep) kdone = (int)k;
+            }
         }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        double* s_tot = reinterpret_cast<double*>(s_red);  // NT / 32 <= 16 doubles
+        if ((tid & 31) == 0) s_tot[tid >> 5] = tot;
+        __syncthreads();
+        tot = 0.0;
+#pragma unroll
+        for (int q = 0; q < NT / 32; ++q) tot += s_tot[q];
+        __syncthreads();  // s_red is reused below
+        if (tot < 4294967296.0) break;
+        ue += 16;
+        for (int i = tid; i < nseg; i += NT) segb[i] = 0u;
+        __syncthreads();
     }
-    __syncthreads();
     // scale: the largest segment bound maps below 2^30
     unsigned mx = 0u;
     for (int i = tid; i < nseg; i += NT) mx = max(mx, segb[i]);
@@ -112,7 +134,7 @@ __device__ __forceinline__ void scatter_row(const PlaneDesc& P, int w, bool raw,
     mx = 0u;
 #pragma unroll
     for (int q = 0; q < NT / 32; ++q) mx = max(mx, (unsigned)s_red[q]);
-    const int sh = 30 - (32 - __clz(mx));  // mx < 2^(32-clz)  =>  mx 2^sh < 2^30
+    const int sh = 30 - (32 - __clz(mx) + ue);  // bound < 2^(32-clz+ue)  =>  bound 2^sh < 2^30
     const float scale = ldexpf(1.0f, sh);
     inv = ldexpf(1.0f, -sh);
     // pass 2: scatter, one int32 shared atomic per bin

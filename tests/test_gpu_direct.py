@@ -186,6 +186,25 @@ def test_direct_wide_and_narrow_depos(pctx, oracle, kind):
     assert relL2_per_channel(m_fft, m_ref) < TOL_FRAME
 
 
+@pytest.mark.parametrize("path", ["direct", "fft"])
+def test_extreme_charge_range(pctx, oracle, path):
+    """Charges from 1 to 1e12 electrons on one plane: segment bounds beyond
+    32 bits (k_direct's bound pass re-runs with a coarser unit), per-row
+    fixed-point scales spanning ~40 binary orders, and single terms near
+    the row's 2^29 budget (k_direct rounds each term with one DFMA, exact
+    for |term| < 2^51)."""
+    resp = ResponseParams(plane_kind="induction", wire_weights=(0.1, 1.0, 0.1))
+    depos = line_tracks(600, SMALL, seed=12)
+    rng = np.random.default_rng(12)
+    depos["q"] = np.round(10.0 ** rng.uniform(0.0, 12.0, len(depos))).astype(np.int64)
+    depos["q"][::50] = 10**12
+    m = _frame(pctx, path, SMALL, resp, depos)
+    s_ref, _ = oracle.charge_fluct_off(oracle_grid(SMALL), depos)
+    m_ref = oracle.convolve(oracle_grid(SMALL), oracle_response(resp), s_ref)
+    assert np.isfinite(m).all()
+    assert relL2_per_channel(m, m_ref) < TOL_FRAME
+
+
 def test_untimed_device_event_equals_timed(pctx):
     """The untimed device path chains its three kernels with programmatic
     dependent launches (the profile and tile kernels start while their
