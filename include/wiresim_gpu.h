@@ -21,6 +21,10 @@
  *                          (pipeline.cpp:345-419)
  *   ws_simulate_event      N independent planes (one plane per run)
  *   ws_noise_digitize_device add_noise (white) + digitize              include/wiresim/spectral.hpp:61-65
+ *   ws_run_simulation      run_simulation(SimConfig, vector<Depo>) whole: raster -> scatter ->
+ *                          convolve -> add_noise -> digitize, SimResult::adc
+ *                          (pipeline.cpp:345-427, pipeline.hpp:94-104)
+ *   ws_run_events          the same for a batch of events (pipelined host buffers)
  *
  * Data layout (identical to the reference's):
  *   ws_depo     == wiresim::Depo       (core.hpp:63-70), 48 B AoS
@@ -43,7 +47,7 @@
 extern "C" {
 #endif
 
-#define WS_ABI_VERSION 1
+#define WS_ABI_VERSION 2
 
 typedef enum ws_status {
     WS_OK = 0,
@@ -97,7 +101,8 @@ typedef struct ws_sim_options {
     int32_t fluctuate;   /* 0: S = q * p (fp32, fixed-point accumulated); 1: binomial fluctuation */
     int32_t approx;      /* fluctuation sampler: 0 exact binomial (fluctuate), 1 Gaussian approx (fluctuate_approx) */
     int32_t rng_mode;    /* WS_RNG_* */
-    int32_t reserved;
+    int32_t charge_u32;  /* fluctuation on: charge outputs hold the exact integer counts as uint32 (the
+                            reference's int64 ChargeGrid up to 2^32-1 per cell) instead of float32 */
     uint64_t seed;       /* SimConfig::rng.seed */
     ws_drift drift;      /* SimConfig::drift */
 } ws_sim_options;
@@ -118,6 +123,34 @@ typedef struct ws_noise_model {
     const double* amplitude_spectrum; /* spectrum mode: host pointer, n_amplitude == padded ticks */
     uint64_t n_amplitude;
 } ws_noise_model;
+
+/* AdcConfig (pipeline.hpp:30-34): code = clamp(round(v * scale + offset), 0, 2^bits - 1) */
+typedef struct ws_adc_config {
+    double scale;
+    double offset;
+    int32_t bits; /* 1..16 */
+    int32_t reserved;
+} ws_adc_config;
+
+enum { WS_FRAME_F32 = 0, WS_FRAME_F64 = 1 };
+enum { WS_ADC_I32 = 0, /* SimResult::adc's Matrix<int32_t> */
+       WS_ADC_U16 = 1 }; /* the same codes in 2 bytes (bits <= 16) */
+
+/* The readout stage of run_simulation after the convolution
+ * (pipeline.cpp:420-423): m = add_noise(m, noise, seed), adc = digitize(m,
+ * adc). White noise from the Philox stream and digitize run fused in the
+ * convolution kernels' frame stores; white noise from the reference's
+ * sequential per-wire substream and spectrum noise run as a second kernel
+ * over the fp32 frame. The noise seed is noise.seed (the reference passes
+ * SimConfig::rng.seed). frame_type selects the element type of frame
+ * outputs: WS_FRAME_F64 widens the fp32 result (MeasurementGrid is double;
+ * the values carry fp32 precision). */
+typedef struct ws_readout {
+    ws_noise_model noise; /* mode WS_NOISE_OFF: no noise */
+    ws_adc_config adc;
+    int32_t frame_type;   /* WS_FRAME_F32 | WS_FRAME_F64 */
+    int32_t adc_type;     /* WS_ADC_I32 | WS_ADC_U16 */
+} ws_readout;
 
 typedef struct ws_timing {
     float prepare_ms;    /* sample: footprints + erf integrals (+ drift) */
@@ -183,12 +216,17 @@ int ws_convolve_device(ws_plane* plane, const float* charge, float* frame);
 
 /* raster -> scatter -> convolve for one plane, device pointers, asynchronous.
  * charge (nullable) additionally receives the charge grid. timing (nullable)
- * is filled at the next ws_ctx_synchronize. */
+ * is filled at the next ws_ctx_synchronize, which also reports errors found
+ * on the device: WS_ERANGE for a workspace overflow (the workspace is then
+ * sized from what the device recorded; call again), never a silently
+ * truncated result. */
 int ws_simulate_plane_device(ws_plane* plane, const ws_depo* depos, uint64_t n, const ws_sim_options* opt,
                              float* frame, float* charge, ws_timing* timing);
 
 /* Host-buffer drop-in for run_simulation's hot section: depos and frame in
- * host memory (pinned recommended), synchronous. */
+ * host memory (pinned recommended), synchronous. Workspace overflows are
+ * re-run internally; WS_ERANGE only if they persist (never WS_OK with a
+ * partial result). */
 int ws_simulate_plane(ws_plane* plane, const ws_depo* depos, uint64_t n, const ws_sim_options* opt, float* frame,
                       float* charge, ws_timing* timing);
 
@@ -208,6 +246,33 @@ int ws_simulate_event(ws_ctx* ctx, uint32_t n_planes, ws_plane* const* planes, c
 int ws_simulate_events(ws_ctx* ctx, uint32_t n_events, uint32_t n_planes, ws_plane* const* planes,
                        const ws_depo* const* depos, const uint64_t* n_depos, const ws_sim_options* opt,
                        float* const* frames, ws_timing* timing);
+
+/* run_simulation (pipeline.cpp:345-427) for one plane, host buffers,
+ * synchronous: adc (padded wires x padded ticks, int32 or uint16 per
+ * readout->adc_type) is SimResult::adc; frame (nullable) the noisy frame
+ * before digitization (fp32 or fp64 per readout->frame_type); charge
+ * (nullable) the charge grid S (float32; exact integers with fluctuation).
+ * Workspace overflows are re-run internally (never WS_OK with a partial
+ * result). */
+int ws_run_simulation(ws_plane* plane, const ws_depo* depos, uint64_t n, const ws_sim_options* opt,
+                      const ws_readout* readout, void* adc, void* frame, float* charge, ws_timing* timing);
+/* The same with device pointers, asynchronous: a workspace overflow is
+ * reported as WS_ERANGE by the next ws_ctx_synchronize (sized for the
+ * re-run; call again). */
+int ws_run_simulation_device(ws_plane* plane, const ws_depo* depos, uint64_t n, const ws_sim_options* opt,
+                             const ws_readout* readout, void* adc, void* frame, float* charge, ws_timing* timing);
+/* Several planes of one event (device pointers, asynchronous); arrays of
+ * n_planes, adcs / frames entries nullable. */
+int ws_run_event_device(ws_ctx* ctx, uint32_t n_planes, ws_plane* const* planes, const ws_depo* const* depos,
+                        const uint64_t* n_depos, const ws_sim_options* opt, const ws_readout* readout,
+                        void* const* adcs, void* const* frames, ws_timing* timing);
+/* A batch of events, host buffers, pipelined like ws_simulate_events:
+ * depos / n_depos / adcs / frames are [n_events * n_planes], event-major
+ * (adcs, frames and their entries nullable). With WS_ADC_U16 and no frames
+ * the device-to-host traffic is 2 B per cell. */
+int ws_run_events(ws_ctx* ctx, uint32_t n_events, uint32_t n_planes, ws_plane* const* planes,
+                  const ws_depo* const* depos, const uint64_t* n_depos, const ws_sim_options* opt,
+                  const ws_readout* readout, void* const* adcs, void* const* frames, ws_timing* timing);
 
 /* add_noise + digitize of a plane's frame (device pointers, asynchronous):
  * the frame gets the noise in place (float32); adc (nullable) receives

@@ -253,6 +253,11 @@ def build_ref() -> Path | None:
     if not ref_src.exists():
         return REF_SO if REF_SO.exists() else None
     subprocess.run(["make", "-C", str(HERE), "ref", f"REF={ref_src}", "-j8"], check=True, capture_output=True)
+    # the drop-in check program (reference types -> B200 library and reference), once libwsgpu.so exists
+    if (HERE.parent / "paper_2104_08265_b200" / "libwsgpu.so").exists():
+        r = subprocess.run(["make", "-C", str(HERE), "dropin", f"REF={ref_src}"], capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError("make dropin failed:\n" + r.stdout + r.stderr)
     return REF_SO
 
 

@@ -6,7 +6,11 @@ C++ interface (see api.py) plus the synthetic workloads used by bench.py.
 """
 from ._lib import DEPO_DTYPE, WsError  # noqa: F401
 from .api import (  # noqa: F401
+    AdcConfig,
     Context,
+    NoiseModel,
+    RunResult,
+    run_events,
     DriftParams,
     GridSpec,
     Plane,

@@ -52,13 +52,26 @@ class DriftC(C.Structure):
 
 
 class SimOptionsC(C.Structure):
-    _fields_ = [("fluctuate", C.c_int32), ("approx", C.c_int32), ("rng_mode", C.c_int32), ("reserved", C.c_int32),
+    _fields_ = [("fluctuate", C.c_int32), ("approx", C.c_int32), ("rng_mode", C.c_int32), ("charge_u32", C.c_int32),
                 ("seed", C.c_uint64), ("drift", DriftC)]
 
 
 class NoiseModelC(C.Structure):
     _fields_ = [("mode", C.c_int32), ("rng_mode", C.c_int32), ("sigma", C.c_double), ("seed", C.c_uint64),
                 ("amplitude_spectrum", C.c_void_p), ("n_amplitude", C.c_uint64)]
+
+
+class AdcConfigC(C.Structure):
+    _fields_ = [("scale", C.c_double), ("offset", C.c_double), ("bits", C.c_int32), ("reserved", C.c_int32)]
+
+
+WS_FRAME_F32, WS_FRAME_F64 = 0, 1
+WS_ADC_I32, WS_ADC_U16 = 0, 1
+WS_NOISE_OFF, WS_NOISE_WHITE, WS_NOISE_SPECTRUM = 0, 1, 2
+
+
+class ReadoutC(C.Structure):
+    _fields_ = [("noise", NoiseModelC), ("adc", AdcConfigC), ("frame_type", C.c_int32), ("adc_type", C.c_int32)]
 
 
 class SignalBatchC(C.Structure):
@@ -106,6 +119,14 @@ SIGNATURES = {
     "ws_simulate_event": (C.c_int, [_P, C.c_uint32, _P, _P, _P, C.POINTER(SimOptionsC), _P, C.POINTER(TimingC)]),
     "ws_simulate_events": (C.c_int, [_P, C.c_uint32, C.c_uint32, _P, _P, _P, C.POINTER(SimOptionsC), _P,
                                      C.POINTER(TimingC)]),
+    "ws_run_simulation": (C.c_int, [_P, _P, C.c_uint64, C.POINTER(SimOptionsC), C.POINTER(ReadoutC), _P, _P, _P,
+                                    C.POINTER(TimingC)]),
+    "ws_run_simulation_device": (C.c_int, [_P, _P, C.c_uint64, C.POINTER(SimOptionsC), C.POINTER(ReadoutC), _P, _P,
+                                           _P, C.POINTER(TimingC)]),
+    "ws_run_event_device": (C.c_int, [_P, C.c_uint32, _P, _P, _P, C.POINTER(SimOptionsC), C.POINTER(ReadoutC), _P, _P,
+                                      C.POINTER(TimingC)]),
+    "ws_run_events": (C.c_int, [_P, C.c_uint32, C.c_uint32, _P, _P, _P, C.POINTER(SimOptionsC), C.POINTER(ReadoutC),
+                                _P, _P, C.POINTER(TimingC)]),
     "ws_gen_depos_uniform":(C.c_int, [C.c_uint64, C.c_uint64, C.POINTER(GridSpecC), _P, _P]),
     "ws_noise_digitize_device": (C.c_int, [_P, _P, C.POINTER(NoiseModelC), C.c_double, C.c_double, C.c_int32, _P]),
     "ws_host_alloc": (C.c_int, [C.c_uint64, C.POINTER(_P)]),

@@ -79,20 +79,60 @@ class RngConfig:
 
 
 @dataclass
+class NoiseModel:
+    """NoiseModel (spectral.hpp:51-55). rng: the per-wire stream, "substream"
+    (the reference's, sequential per wire: a second kernel) or "philox"
+    (counter-based: fused into the convolution's frame stores)."""
+    mode: str = "off"  # "off" | "white" | "spectrum"
+    sigma: float = 0.0
+    amplitude_spectrum: Sequence[float] | None = None
+    rng: str = "substream"
+
+
+@dataclass
+class AdcConfig:
+    """AdcConfig (pipeline.hpp:30-34)."""
+    scale: float = 1.0
+    offset: float = 2048.0
+    bits: int = 12
+
+
+@dataclass
 class SimConfig:
     grid: GridSpec = field(default_factory=GridSpec)
     drift: DriftParams = field(default_factory=DriftParams)
     response: ResponseParams = field(default_factory=ResponseParams)
+    noise: NoiseModel = field(default_factory=NoiseModel)
     n_sigma: float = 3.0
     rng: RngConfig = field(default_factory=RngConfig)
+    adc: AdcConfig = field(default_factory=AdcConfig)
     fluctuate: bool = True       # the reference always fluctuates (rasterize.cpp:182-202)
     approx: bool = False         # fluctuate_approx sampler (rasterize.cpp:159-170)
 
-    def options(self) -> _lib.SimOptionsC:
+    def readout(self, adc_type: str = "i32", frame_type: str = "f32"):
+        """(ReadoutC, keep-alive) for the ws_run_* entry points; the noise
+        seed is rng.seed, as run_simulation passes it (pipeline.cpp:421)."""
+        n = self.noise
+        amp = None
+        if n.mode == "spectrum":
+            amp = np.ascontiguousarray(n.amplitude_spectrum, dtype=np.float64)
+        mode = {"off": _lib.WS_NOISE_OFF, "white": _lib.WS_NOISE_WHITE, "spectrum": _lib.WS_NOISE_SPECTRUM}[n.mode]
+        nm = _lib.NoiseModelC(mode, _lib.WS_RNG_PHILOX if n.rng == "philox" else _lib.WS_RNG_SUBSTREAM,
+                              float(n.sigma), int(self.rng.seed), amp.ctypes.data if amp is not None else None,
+                              amp.size if amp is not None else 0)
+        r = _lib.ReadoutC(nm, _lib.AdcConfigC(self.adc.scale, self.adc.offset, self.adc.bits, 0),
+                          _lib.WS_FRAME_F64 if frame_type == "f64" else _lib.WS_FRAME_F32,
+                          _lib.WS_ADC_U16 if adc_type == "u16" else _lib.WS_ADC_I32)
+        return r, amp
+
+    def options(self, charge_u32: bool = False) -> _lib.SimOptionsC:
+        """ws_sim_options; charge_u32: with fluctuation, charge outputs hold
+        the exact uint32 counts instead of float32."""
         d = self.drift
         return _lib.SimOptionsC(
             int(self.fluctuate), int(self.approx),
-            _lib.WS_RNG_PHILOX if self.rng.mode == "philox" else _lib.WS_RNG_SUBSTREAM, 0, self.rng.seed,
+            _lib.WS_RNG_PHILOX if self.rng.mode == "philox" else _lib.WS_RNG_SUBSTREAM, int(charge_u32),
+            self.rng.seed,
             _lib.DriftC(int(d.enabled), 0, d.response_plane_x, d.drift_speed, d.diffusion_long, d.diffusion_tran))
 
 
@@ -179,9 +219,35 @@ class Plane:
                                          charge.ctypes.data if charge is not None else None, C.byref(t)))
         return SimResult(frame=frame, charge=charge, timing=t.as_dict())
 
-    # ---- device entry points (torch tensors; asynchronous on the context stream)
-    def simulate_device(self, depos_dev, n: int, config: SimConfig, frame_dev, charge_dev=None, timing=None):
+    def run(self, depos, config: SimConfig, adc_type: str = "i32", want_frame: bool = False,
+            frame_type: str = "f32", want_charge: bool = False):
+        """run_simulation (pipeline.cpp:345-427) on this plane: adc codes
+        (int32 like SimResult::adc, or uint16), optionally the noisy frame
+        before digitization and the charge grid (host buffers)."""
+        d = as_depos(depos)
+        r, _keep = config.readout(adc_type, frame_type)
+        adc = np.empty(self.shape, dtype=np.uint16 if adc_type == "u16" else np.int32)
+        frame = np.empty(self.shape, dtype=np.float64 if frame_type == "f64" else np.float32) if want_frame else None
+        charge = np.empty(self.shape, dtype=np.float32) if want_charge else None
+        t = _lib.TimingC()
         opt = config.options()
+        check(self.lib.ws_run_simulation(self.handle, d.ctypes.data, len(d), C.byref(opt), C.byref(r),
+                                         adc.ctypes.data, _ptr(frame), _ptr(charge), C.byref(t)))
+        return RunResult(adc=adc, frame=frame, charge=charge, timing=t.as_dict(),
+                         clipped_charge=int(t.clipped_charge))
+
+    def run_device(self, depos_dev, n: int, config: SimConfig, adc_dev, frame_dev=None, charge_dev=None,
+                   adc_type: str = "i32", frame_type: str = "f32", timing=None):
+        r, _keep = config.readout(adc_type, frame_type)
+        opt = config.options()
+        check(self.lib.ws_run_simulation_device(self.handle, _ptr(depos_dev), n, C.byref(opt), C.byref(r),
+                                                _ptr(adc_dev), _ptr(frame_dev), _ptr(charge_dev),
+                                                C.byref(timing) if timing is not None else None))
+
+    # ---- device entry points (torch tensors; asynchronous on the context stream)
+    def simulate_device(self, depos_dev, n: int, config: SimConfig, frame_dev, charge_dev=None, timing=None,
+                        charge_u32: bool = False):
+        opt = config.options(charge_u32)
         check(self.lib.ws_simulate_plane_device(self.handle, _ptr(depos_dev), n, C.byref(opt), _ptr(frame_dev),
                                                 _ptr(charge_dev), C.byref(timing) if timing is not None else None))
 
@@ -238,6 +304,17 @@ class SimResult:
     timing: dict
 
 
+@dataclass
+class RunResult:
+    """SimResult (pipeline.hpp:94-99): adc codes, the charge grid (optional),
+    clipped charge; plus the noisy frame before digitization (optional)."""
+    adc: np.ndarray
+    frame: np.ndarray | None
+    charge: np.ndarray | None
+    timing: dict
+    clipped_charge: int
+
+
 def simulate_event(ctx: Context, planes: Sequence[Plane], depos: Sequence, config: SimConfig,
                    frames: Sequence[np.ndarray] | None = None):
     """Independent planes of one event through one batch of launches (host buffers)."""
@@ -276,6 +353,33 @@ def simulate_events(ctx: Context, planes: Sequence[Plane], events: Sequence[Sequ
     return frames, t.as_dict()
 
 
+def run_events(ctx: Context, planes: Sequence[Plane], events: Sequence[Sequence], config: SimConfig,
+               adc_type: str = "i32", want_frame: bool = False, frame_type: str = "f32", adcs=None, frames=None):
+    """run_simulation over a batch of events (ws_run_events, pipelined host
+    buffers): returns (adcs[e][p], frames[e][p] or None, timing)."""
+    n_ev, n_pl = len(events), len(planes)
+    ds = [as_depos(d) for ev in events for d in ev]
+    adt = np.uint16 if adc_type == "u16" else np.int32
+    if adcs is None:
+        adcs = [[np.empty(p.shape, dtype=adt) for p in planes] for _ in range(n_ev)]
+    if frames is None and want_frame:
+        fdt = np.float64 if frame_type == "f64" else np.float32
+        frames = [[np.empty(p.shape, dtype=fdt) for p in planes] for _ in range(n_ev)]
+    PArr = C.c_void_p * n_pl
+    parr = PArr(*[p.handle.value for p in planes])
+    DArr = C.c_void_p * (n_ev * n_pl)
+    darr = DArr(*[d.ctypes.data for d in ds])
+    narr = (C.c_uint64 * (n_ev * n_pl))(*[len(d) for d in ds])
+    aarr = DArr(*[a.ctypes.data for ev in adcs for a in ev])
+    farr = DArr(*[f.ctypes.data for ev in frames for f in ev]) if frames is not None else None
+    r, _keep = config.readout(adc_type, frame_type)
+    t = _lib.TimingC()
+    opt = config.options()
+    check(ctx.lib.ws_run_events(ctx.handle, n_ev, n_pl, parr, darr, narr, C.byref(opt), C.byref(r), aarr, farr,
+                                C.byref(t)))
+    return adcs, frames, t.as_dict()
+
+
 def simulate_event_device(ctx: Context, planes: Sequence[Plane], depos_dev: Sequence, n_depos: Sequence[int],
                           config: SimConfig, frames_dev: Sequence, timing=None):
     n = len(planes)
@@ -289,12 +393,14 @@ def simulate_event_device(ctx: Context, planes: Sequence[Plane], depos_dev: Sequ
                                            C.byref(timing) if timing is not None else None))
 
 
-def run_simulation(config: SimConfig, depos, device: int = 0, ctx: Context | None = None) -> SimResult:
-    """run_simulation (pipeline.hpp:104) up to the pre-noise frame, on the GPU."""
+def run_simulation(config: SimConfig, depos, device: int = 0, ctx: Context | None = None,
+                   adc_type: str = "i32", want_frame: bool = False) -> RunResult:
+    """run_simulation (pipeline.hpp:104) on the GPU: SimResult's adc,
+    charge grid and clipped charge (+ the noisy frame if asked)."""
     ctx = ctx or Context(device)
     plane = Plane(ctx, config.grid, config.response, config.n_sigma)
     try:
-        return plane.simulate(depos, config, want_charge=True)
+        return plane.run(depos, config, adc_type=adc_type, want_frame=want_frame, want_charge=True)
     finally:
         plane.close()
 

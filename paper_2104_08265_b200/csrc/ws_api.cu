@@ -31,11 +31,12 @@ extern "C" cudaError_t wsb_launch_fill(const EventDesc& ev, const UnitRec* recs,
                                        cudaStream_t s);
 extern "C" cudaError_t wsb_launch_gprof(const EventDesc& ev, const UnitRec* recs, uint32_t* pool, cudaStream_t s,
                                         int pdl);
-extern "C" cudaError_t wsb_launch_noise(float* frame, int32_t* adc, int W, int N, int noise, int rng_mode, double sigma,
-                                        uint64_t seed, double scale, double offset, double max_code, cudaStream_t s);
+extern "C" cudaError_t wsb_launch_noise(const float* in, const wsb::Sink& out, int W, int N, int noise, int rng_mode,
+                                        double sigma, uint64_t seed, cudaStream_t s);
+extern "C" cudaError_t wsb_launch_u32_to_f32(uint32_t* g, size_t n, cudaStream_t s);
 extern "C" cudaError_t wsb_launch_noise_spectrum(const wsb::PlaneDesc& P, const double* amp, uint64_t seed, int rng_mode,
-                                                 float* frame, int32_t* adc, double scale, double offset,
-                                                 double max_code, int variant, cudaStream_t stream);
+                                                 const float* in, const wsb::Sink& out, int variant,
+                                                 cudaStream_t stream);
 extern "C" size_t wsb_direct_smem(int cap);
 extern "C" int wsb_direct_cap();
 extern "C" cudaError_t wsb_launch_direct(const EventDesc& ev, const uint32_t* pool, const uint32_t* band_off,
@@ -103,12 +104,16 @@ struct DevBuf {
 
 }  // namespace
 
-// per-call device scratch header: [pool_ctr, err, pad, pad] u32 + stats i64[2*kMaxPlanes]
+// per-call device scratch header: [pool_ctr, err, list_need, pad] u32 + stats
+// i64[2*kMaxPlanes] + per-plane tile needs (the sizes a re-run needs after an
+// overflow: nothing is ever dropped silently)
 struct ScratchHeader {
     uint32_t pool_ctr;
     uint32_t err;
-    uint32_t pad[2];
+    uint32_t list_need;
+    uint32_t pad;
     long long stats[2 * wsb::kMaxPlanes];
+    uint32_t tile_need[wsb::kMaxPlanes];
 };
 
 struct PendingCall {
@@ -118,7 +123,14 @@ struct PendingCall {
     int direct_planes;
     cudaEvent_t ev[6];
     int fluctuate;
+    int tag;                               // caller's tag (ws_simulate_events: event index), -1 none
+    uint64_t tiles;                        // fixed-list tiles of the call (bands)
+    ws_plane* planes[wsb::kMaxPlanes];     // direct-routed planes (null otherwise)
 };
+
+// budget of the fixed-capacity tile lists (bands x capacity x 80 B); above it
+// the direct path uses exact-size CSR lists
+constexpr size_t kFixedTileBudget = size_t(2) << 30;
 
 struct ws_ctx {
     int device = 0;
@@ -131,12 +143,16 @@ struct ws_ctx {
     DevBuf<UnitRec> band_list;  // CSR lists of full unit records per FFT band (k_fill_bands)
     DevBuf<wsb::TEnt> tile_list;  // CSR lists of direct-path tile entries (k_fill_bands)
     DevBuf<wsb::TEnt> tile_fixed;  // fixed-capacity tile lists (all-direct events, filled by the sampler)
-    uint32_t tile_cap_hint = 2048;  // entries per tile; doubled after a kErrTileCap
-    size_t list_hint = 0;       // grown after a kErrRange
+    uint32_t tile_cap_hint = 2048;  // entries per tile; sized from the real count after a kErrTileCap
+    bool csr_next = false;      // next call: CSR tile lists (a fixed capacity would exceed kFixedTileBudget)
+    int call_tag = -1;          // tag recorded with the next calls (ws_simulate_events: event index)
+    std::vector<int> failed_tags;  // tags of calls that overflowed (re-run by their owner)
+    size_t list_hint = 0;       // exact CSR list size after a kErrRange
     uint32_t last_list_cap = 0;
     DevBuf<ScratchHeader> header;
     DevBuf<ws_depo> depos;
-    DevBuf<float> frames, charges;
+    DevBuf<float> frames, charges, ro_scratch;
+    DevBuf<unsigned char> out_stage;  // ws_run_*: device staging of the readout outputs (ADC / fp64 frames)
     DevBuf<double> noise_amp;  // spectrum-mode amplitudes of the last ws_noise_digitize_device
     ScratchHeader* host_slots = nullptr;  // pinned, kStatSlots
     int next_slot = 0;
@@ -182,6 +198,7 @@ struct ws_plane {
     float2* d_tw = nullptr;
     uint16_t* d_rev = nullptr;
     int ww_is_one = 0;
+    bool route_fft_next = false;  // AUTO: a tile overflowed (dense, e.g. a shower): the row FFT on the re-run
     int rows_per_band = 4;
     int n_bands = 0;
     size_t smem = 0;
@@ -397,12 +414,57 @@ int check_opts(const ws_sim_options* o)
 // pointers (frames[i] may be null when only charge is wanted).
 int finish_pending(ws_ctx* c);
 
+// Readout of a call (run_simulation's add_noise + digitize, pipeline.cpp:420-423)
+struct Readout {
+    const ws_readout* spec;  // noise model, ADC config, output types
+    void* const* adc;        // per plane (nullable entries)
+    double* const* frame64;  // per plane (nullable entries)
+};
+
+// The noise runs fused in the frame-store epilogues unless it needs a
+// sequential per-wire stream (white noise, substream) or its own row IFFT
+// (spectrum mode): those run as a second kernel over the fp32 frame.
+bool readout_fused(const ws_readout* r)
+{
+    return r->noise.mode == WS_NOISE_OFF || (r->noise.mode == WS_NOISE_WHITE && r->noise.rng_mode == WS_RNG_PHILOX) ||
+           (r->noise.mode == WS_NOISE_WHITE && r->noise.sigma == 0.0);
+}
+
 int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* const* depos, const uint64_t* n_depos,
               const ws_sim_options* opt, float* const* frames, float* const* charges, const float* const* charge_in,
-              ws_timing* timing)
+              ws_timing* timing, const Readout* ro = nullptr, bool charge_to_float = false)
 {
     cudaStream_t s = c->stream;
     EventDesc ev{};
+    const bool ro_fused = ro && readout_fused(ro->spec);
+    if (ro_fused) {
+        const ws_readout& r = *ro->spec;
+        ev.ro = 1;
+        ev.ro_noise = r.noise.mode == WS_NOISE_WHITE && r.noise.sigma != 0.0 ? 1 : 0;
+        ev.ro_sigma = r.noise.sigma;
+        ev.ro_seed = r.noise.seed;
+        ev.adc_u16 = r.adc_type == WS_ADC_U16 ? 1 : 0;
+        ev.adc_scale = r.adc.scale;
+        ev.adc_offset = r.adc.offset;
+        ev.adc_max = (double)((1 << r.adc.bits) - 1);
+    }
+    // an unfused readout noise kernel reads an fp32 frame: the caller's, or scratch
+    std::vector<float*> fr32(n, nullptr);
+    if (ro && !ro_fused) {
+        size_t need = 0;
+        for (uint32_t i = 0; i < n; ++i)
+            if (!(frames && frames[i])) need += (size_t)planes[i]->W * planes[i]->N;
+        WS_CUDA(c->ro_scratch.reserve(need));
+        size_t off = 0;
+        for (uint32_t i = 0; i < n; ++i) {
+            if (frames && frames[i]) {
+                fr32[i] = frames[i];
+            } else {
+                fr32[i] = c->ro_scratch.p + off;
+                off += (size_t)planes[i]->W * planes[i]->N;
+            }
+        }
+    }
     ev.n_planes = (int)n;
     ev.fluctuate = opt ? opt->fluctuate : 0;
     ev.approx = opt ? opt->approx : 0;
@@ -428,15 +490,27 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
         d.n_units = depos ? (uint32_t)n_depos[i] : 0u;
         d.unit_base = units;
         d.band_base = bands;
-        d.frame = frames ? frames[i] : nullptr;
-        d.charge_out = charges ? charges[i] : nullptr;
-        d.charge_in = from_grid ? charge_in[i] : (ev.fluctuate ? charges[i] : nullptr);
+        d.frame = (ro && !ro_fused) ? fr32[i] : (frames ? frames[i] : nullptr);
+        if (ro_fused) {
+            d.frame64 = ro->frame64 ? ro->frame64[i] : nullptr;
+            d.adc = ro->adc ? ro->adc[i] : nullptr;
+        }
+        // fluctuation on: the walk's integer grid lives in the charge buffer
+        d.charge_u32 = (ev.fluctuate && !from_grid) ? reinterpret_cast<uint32_t*>(charges[i]) : nullptr;
+        d.charge_out = (charges && !d.charge_u32) ? charges[i] : nullptr;
+        d.charge_in = from_grid ? charge_in[i] : nullptr;
         d.stats = nullptr;
+        const bool has_out = d.frame || d.frame64 || d.adc;
         // time-domain path for fluctuation-off frames (not with a charge
         // grid request: that pass bins by FFT bands). AUTO estimates the
         // work as depos x ~12 wire rows x profile taps against the plane's
         // cells (ws_ctx_set_direct_kappa).
-        if (ev.mode == 0 && d.frame && !d.charge_out && p->direct_ok && c->conv_path != WS_CONV_FFT) {
+        // A plane whose tile list overflowed in the previous call (a local
+        // density far above the plane average, e.g. a shower) takes the row
+        // FFT once under AUTO: its cost does not depend on the depo density.
+        const bool dense = p->route_fft_next && c->conv_path == WS_CONV_AUTO;
+        p->route_fft_next = false;
+        if (ev.mode == 0 && has_out && !d.charge_out && p->direct_ok && c->conv_path != WS_CONV_FFT && !dense) {
             const double work = (double)d.n_units * 12.0 * (double)(p->n_lags + 16);
             if (c->conv_path == WS_CONV_DIRECT || work <= c->direct_kappa * (double)p->W * (double)p->Np) {
                 d.direct = 1;
@@ -450,7 +524,7 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
         units += d.n_units;
         bands += (uint32_t)d.n_bands;
         smem = std::max(smem, p->smem);
-        want_frame = want_frame || d.frame != nullptr;
+        want_frame = want_frame || has_out;
     }
     ev.total_units = units;
     ev.total_bands = bands;
@@ -484,7 +558,10 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
         const char* v = getenv("WS_TILE_CSR");
         return v && v[0] == '1';
     }();
-    const bool use_fixed = any_direct && !any_fft && ev.mode == 0 && !ev.fluctuate && !csr_only && bands > 0 && want_frame;
+    const bool fixed_fits = (size_t)bands * c->tile_cap_hint * sizeof(wsb::TEnt) <= kFixedTileBudget;
+    const bool use_fixed = any_direct && !any_fft && ev.mode == 0 && !ev.fluctuate && !csr_only && bands > 0 &&
+                           want_frame && fixed_fits && !c->csr_next;
+    c->csr_next = false;
     ev.tile_cap = 0;
     ev.tiles = nullptr;
     ev.tile_count = c->band_count.p;
@@ -501,17 +578,34 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
         WS_CUDA(c->header.reserve(kStatSlots));
         WS_CUDA(cudaMemsetAsync(c->header.p, 0, sizeof(ScratchHeader) * kStatSlots, s));
     }
-    if ((int)c->pending.size() >= kStatSlots)
-        if (int rc = finish_pending(c)) return rc;  // ring full: drain (reads and re-zeroes the slots)
+    if ((int)c->pending.size() >= kStatSlots) {
+        // ring full: drain (reads and re-zeroes the slots). Inside a batch
+        // (tagged calls) an overflow of an earlier event is re-run by the
+        // batch at its end; this call still goes ahead.
+        const int rc = finish_pending(c);
+        if (rc && !(rc == WS_ERANGE && c->call_tag >= 0)) return rc;
+    }
     const int slot = c->next_slot;
     c->next_slot = (c->next_slot + 1) % kStatSlots;
     ScratchHeader* hdr = c->header.p + slot;
-    for (uint32_t i = 0; i < n; ++i) ev.p[i].stats = &hdr->stats[2 * i];
+    for (uint32_t i = 0; i < n; ++i) {
+        ev.p[i].stats = &hdr->stats[2 * i];
+        ev.p[i].tile_need = &hdr->tile_need[i];
+    }
+    ev.list_need = &hdr->list_need;
+    ev.err = &hdr->err;
 
     PendingCall pc{};
     pc.timing = timing;
     pc.n_planes = (int)n;
-    for (uint32_t i = 0; i < n; ++i) pc.direct_planes += ev.p[i].direct;
+    pc.tag = c->call_tag;
+    pc.tiles = bands;
+    uint32_t direct_units = 0;  // units on direct planes: the profiles kernel runs iff > 0
+    for (uint32_t i = 0; i < n; ++i) {
+        pc.direct_planes += ev.p[i].direct;
+        pc.planes[i] = ev.p[i].direct ? planes[i] : nullptr;
+        if (ev.p[i].direct) direct_units += ev.p[i].n_units;
+    }
     pc.fluctuate = ev.fluctuate;
     if (timing)
         for (int k = 0; k < 6; ++k) pc.ev[k] = take_event(c);
@@ -520,7 +614,7 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
 
     if (ev.fluctuate && !from_grid)
         for (uint32_t i = 0; i < n; ++i)
-            WS_CUDA(cudaMemsetAsync(ev.p[i].charge_out, 0, sizeof(float) * (size_t)ev.p[i].W * ev.p[i].N, s));
+            WS_CUDA(cudaMemsetAsync(ev.p[i].charge_u32, 0, sizeof(uint32_t) * (size_t)ev.p[i].W * ev.p[i].N, s));
     if (!from_grid) {
         WS_CUDA(wsb_launch_sample(ev, c->recs.p, c->pool.p, (uint32_t)std::min<size_t>(c->pool.cap, 0xffffffffu),
                                   &hdr->pool_ctr, c->band_count.p, &hdr->err, s, timing ? 0 : 1));
@@ -576,8 +670,12 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
         // each kernel skips the other's planes
         if (any_direct) {
             // programmatic launch after the profiles kernel on the same stream
-            // (fixed tile lists, no charge pass in between)
-            const int pdl = ev.tile_cap != 0 && !(ev.mode == 0 && charges) ? 1 : 0;
+            // (fixed tile lists, no charge pass in between). Only when the
+            // profiles kernel was launched in this call: otherwise the
+            // predecessor could be the previous call's k_direct, which
+            // releases its dependents at its start, before it has consumed
+            // (and zeroed) the tile counts this launch reads.
+            const int pdl = ev.tile_cap != 0 && !(ev.mode == 0 && charges) && direct_units > 0 ? 1 : 0;
             WS_CUDA(wsb_launch_direct(ev, c->pool.p, c->band_off.p, c->tile_list.p, wsb_direct_smem(wsb_direct_cap()),
                                       s, pdl));
             c->launches += bands ? 1 : 0;
@@ -587,6 +685,32 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
             c->launches += bands ? 1 : 0;
         }
     }
+    if (ro && !ro_fused) {
+        // readout with a sequential per-wire stream or a spectrum: its own
+        // kernel over the fp32 frame (in place), then digitize
+        const ws_readout& r = *ro->spec;
+        for (uint32_t i = 0; i < n; ++i) {
+            const PlaneDesc& d = ev.p[i];
+            const wsb::Sink sk{frames && frames[i] ? frames[i] : nullptr, ro->frame64 ? ro->frame64[i] : nullptr,
+                               ro->adc ? ro->adc[i] : nullptr, r.adc_type == WS_ADC_U16 ? 1 : 0, r.adc.scale,
+                               r.adc.offset, (double)((1 << r.adc.bits) - 1)};
+            if (r.noise.mode == WS_NOISE_SPECTRUM) {
+                WS_CUDA(c->noise_amp.reserve((size_t)d.N));
+                WS_CUDA(cudaMemcpyAsync(c->noise_amp.p, r.noise.amplitude_spectrum, sizeof(double) * d.N,
+                                        cudaMemcpyHostToDevice, s));
+                WS_CUDA(wsb_launch_noise_spectrum(d, c->noise_amp.p, r.noise.seed, r.noise.rng_mode, d.frame, sk,
+                                                  c->conv_variant, s));
+            } else {
+                WS_CUDA(wsb_launch_noise(d.frame, sk, d.W, d.N, 1, r.noise.rng_mode, r.noise.sigma, r.noise.seed, s));
+            }
+            c->launches += 1;
+        }
+    }
+    if (ev.fluctuate && !from_grid && charge_to_float && !(opt && opt->charge_u32))
+        for (uint32_t i = 0; i < n; ++i) {  // the caller's charge output: integer counts -> float32 in place
+            WS_CUDA(wsb_launch_u32_to_f32(ev.p[i].charge_u32, (size_t)ev.p[i].W * ev.p[i].N, s));
+            c->launches += 1;
+        }
     if (timing) WS_CUDA(cudaEventRecord(pc.ev[4], s));  // stage timing only
     pc.slot = slot;
     if (timing) WS_CUDA(cudaEventRecord(pc.ev[5], s));  // stage timing only
@@ -603,26 +727,63 @@ int finish_pending(ws_ctx* c)
         for (const PendingCall& pc : c->pending)
             WS_CUDA(cudaMemsetAsync(c->header.p + pc.slot, 0, sizeof(ScratchHeader), c->stream));
     }
+    // Every call's status is evaluated (the first error is returned): an
+    // overflow never yields WS_OK. The workspace is sized from the real needs
+    // the device recorded, so a single re-run fits; tagged calls that
+    // overflowed are listed for their owner (ws_simulate_events) to re-run.
     int rc = WS_OK;
     for (PendingCall& pc : c->pending) {
         const ScratchHeader& h = c->host_slots[pc.slot];
-        if (rc == WS_OK) {
-            if (h.err & wsb::kErrDomain) rc = set_err(WS_EDOMAIN, "drift_depo: a depo is behind the response plane");
-            else if (h.err & wsb::kErrCharge) rc = set_err(WS_EINVAL, "fluctuate: charge must be >= 0");
-            else if (h.err & wsb::kErrPool) {
-                c->pool_hint = std::max<size_t>(c->pool.cap * 2, (size_t)h.pool_ctr + 4096);
-                rc = set_err(WS_ERANGE, "workspace: patch pool overflow (%u doubles needed); grown, re-run the call",
-                             h.pool_ctr);
-            } else if (h.err & wsb::kErrTileCap) {
-                rc = set_err(WS_ERANGE, "workspace: tile list overflow (%u entries per tile); grown, re-run the call",
-                             c->tile_cap_hint);
-                c->tile_cap_hint *= 2;
-            } else if (h.err & wsb::kErrRange) {
-                c->list_hint = std::max<size_t>(c->list_hint, 2 * (size_t)c->last_list_cap);
-                rc = set_err(WS_ERANGE, "workspace: bin lists overflow (capacity %u entries); grown, re-run the call",
-                             c->last_list_cap);
+        int prc = WS_OK;
+        char msg[256] = {0};
+        if (h.err & wsb::kErrDomain) {
+            prc = WS_EDOMAIN;
+            snprintf(msg, sizeof msg, "drift_depo: a depo is behind the response plane");
+        } else if (h.err & wsb::kErrCharge) {
+            prc = WS_EINVAL;
+            snprintf(msg, sizeof msg, "fluctuate: charge must be >= 0");
+        } else if (h.err & wsb::kErrCellOvf) {
+            prc = WS_ERUNTIME;  // a cell of the integer charge grid would pass 2^32 - 1 electrons (not retried)
+            snprintf(msg, sizeof msg, "fluctuate: a charge-grid cell exceeds 4294967295 electrons");
+        }
+        if (h.err & wsb::kErrPool) {
+            c->pool_hint = std::max<size_t>(c->pool_hint, (size_t)h.pool_ctr + 4096);
+            if (!prc) {
+                prc = WS_ERANGE;
+                snprintf(msg, sizeof msg, "workspace: patch pool overflow (%u words needed); grown, re-run the call",
+                         h.pool_ctr);
             }
         }
+        if (h.err & wsb::kErrTileCap) {
+            // the real per-tile counts: size the fixed lists from them, or
+            // (beyond the budget) take exact-size CSR lists; under AUTO the
+            // overflowing (dense) planes take the row FFT on the re-run
+            uint32_t need = 0;
+            for (int i = 0; i < pc.n_planes; ++i) {
+                need = std::max(need, h.tile_need[i]);
+                if (h.tile_need[i] && pc.planes[i]) pc.planes[i]->route_fft_next = true;
+            }
+            uint32_t cap = c->tile_cap_hint;
+            while (cap < need && cap < (1u << 30)) cap *= 2;
+            if ((size_t)pc.tiles * cap * sizeof(wsb::TEnt) <= kFixedTileBudget) c->tile_cap_hint = cap;
+            else c->csr_next = true;
+            if (!prc) {
+                prc = WS_ERANGE;
+                snprintf(msg, sizeof msg,
+                         "workspace: tile list overflow (%u entries in one tile, capacity %u); grown, re-run the call",
+                         need, c->tile_cap_hint);
+            }
+        }
+        if (h.err & wsb::kErrRange) {
+            c->list_hint = std::max<size_t>(c->list_hint, (size_t)h.list_need + 4096);
+            if (!prc) {
+                prc = WS_ERANGE;
+                snprintf(msg, sizeof msg, "workspace: bin lists overflow (%u entries, capacity %u); grown, re-run the call",
+                         h.list_need, c->last_list_cap);
+            }
+        }
+        if (prc == WS_ERANGE && pc.tag >= 0) c->failed_tags.push_back(pc.tag);
+        if (prc && rc == WS_OK) rc = set_err(prc, "%s", msg);
         if (pc.timing) {
             ws_timing& t = *pc.timing;
             float ms = 0.f;
@@ -726,6 +887,8 @@ int ws_ctx_destroy(ws_ctx* c)
     c->depos.release();
     c->frames.release();
     c->charges.release();
+    c->ro_scratch.release();
+    c->out_stage.release();
     c->noise_amp.release();
     for (PendingCall& pc : c->pending)
         for (cudaEvent_t e : pc.ev) cudaEventDestroy(e);
@@ -993,6 +1156,226 @@ int ws_plane_get_kernel(const ws_plane* p, double* out, uint64_t cap)
     return WS_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+constexpr int kMaxAttempts = 6;  // host paths: re-runs after a workspace overflow (one normally suffices)
+
+int check_readout(const ws_readout* r, uint32_t n_planes, ws_plane* const* planes)
+{
+    if (!r) return WS_OK;
+    const ws_noise_model& m = r->noise;
+    if (m.mode != WS_NOISE_OFF && m.mode != WS_NOISE_WHITE && m.mode != WS_NOISE_SPECTRUM)
+        return set_err(WS_EINVAL, "add_noise: unknown noise mode %d", m.mode);
+    if (m.mode != WS_NOISE_OFF && m.rng_mode != WS_RNG_SUBSTREAM && m.rng_mode != WS_RNG_PHILOX)
+        return set_err(WS_EINVAL, "add_noise: unknown rng mode %d", m.rng_mode);
+    if (m.sigma < 0.0) return set_err(WS_EINVAL, "add_noise: sigma must be >= 0");
+    if (r->adc.bits < 1 || r->adc.bits > 16) return set_err(WS_EINVAL, "digitize: bits must be in [1,16]");
+    if (r->frame_type != WS_FRAME_F32 && r->frame_type != WS_FRAME_F64)
+        return set_err(WS_EINVAL, "readout: unknown frame type %d", r->frame_type);
+    if (r->adc_type != WS_ADC_I32 && r->adc_type != WS_ADC_U16)
+        return set_err(WS_EINVAL, "readout: unknown adc type %d", r->adc_type);
+    if (m.mode == WS_NOISE_SPECTRUM)
+        for (uint32_t i = 0; i < n_planes; ++i) {
+            if (!m.amplitude_spectrum || m.n_amplitude != (uint64_t)planes[i]->N)
+                return set_err(WS_EINVAL,
+                               "add_noise: amplitude_spectrum length %llu does not match the padded tick count %d",
+                               (unsigned long long)m.n_amplitude, planes[i]->N);
+            if (planes[i]->folded)
+                return set_err(WS_EINVAL,
+                               "add_noise: spectrum mode needs an even 7-smooth padded tick count (got %d)",
+                               planes[i]->N);
+        }
+    return WS_OK;
+}
+
+size_t frame_elem(const ws_readout* r) { return r && r->frame_type == WS_FRAME_F64 ? 8 : 4; }
+size_t adc_elem(const ws_readout* r) { return r && r->adc_type == WS_ADC_U16 ? 2 : 4; }
+
+// One event (any number of planes, in launch groups of kMaxPlanes), device
+// pointers, asynchronous. frames[i]: fp32 (ro == null or an fp32 readout) or
+// fp64 (fp64 readout); adcs[i]: readout codes; charges[i] (nullable array):
+// the caller's charge grids (float32 on return).
+int event_device(ws_ctx* ctx, uint32_t n_planes, ws_plane* const* planes, const ws_depo* const* depos,
+                 const uint64_t* n_depos, const ws_sim_options* opt, const ws_readout* spec, void* const* frames,
+                 void* const* adcs, float* const* charges, ws_timing* timing)
+{
+    std::vector<float*> ch(n_planes, nullptr);
+    bool user_charge = false;
+    if (charges)
+        for (uint32_t i = 0; i < n_planes; ++i) user_charge = user_charge || charges[i];
+    if (opt->fluctuate || user_charge) {
+        // fluctuation: the integer grid of the walk (internal unless the caller wants it)
+        size_t total = 0;
+        for (uint32_t i = 0; i < n_planes; ++i)
+            if (!(charges && charges[i])) total += (size_t)planes[i]->W * planes[i]->N;
+        if (opt->fluctuate) WS_CUDA(ctx->charges.reserve(total));
+        size_t off = 0;
+        for (uint32_t i = 0; i < n_planes; ++i) {
+            if (charges && charges[i]) {
+                ch[i] = charges[i];
+            } else if (opt->fluctuate) {
+                ch[i] = ctx->charges.p + off;
+                off += (size_t)planes[i]->W * planes[i]->N;
+            }
+        }
+    }
+    const bool f64 = spec && spec->frame_type == WS_FRAME_F64;
+    std::vector<float*> fr(n_planes, nullptr);
+    std::vector<double*> fr64(n_planes, nullptr);
+    std::vector<void*> ad(n_planes, nullptr);
+    for (uint32_t i = 0; i < n_planes; ++i) {
+        void* f = frames ? frames[i] : nullptr;
+        if (f64) fr64[i] = static_cast<double*>(f);
+        else fr[i] = static_cast<float*>(f);
+        ad[i] = adcs ? adcs[i] : nullptr;
+    }
+    for (uint32_t g = 0; g < n_planes; g += wsb::kMaxPlanes) {
+        const uint32_t n = std::min<uint32_t>(wsb::kMaxPlanes, n_planes - g);
+        const Readout ro{spec, ad.data() + g, fr64.data() + g};
+        bool any_charge = false;
+        for (uint32_t i = g; i < g + n; ++i) any_charge = any_charge || ch[i];
+        const int rc = run_group(ctx, n, planes + g, depos + g, n_depos + g, opt, fr.data() + g,
+                                 any_charge ? ch.data() + g : nullptr, nullptr, g == 0 ? timing : nullptr,
+                                 spec ? &ro : nullptr, user_charge);
+        if (rc) return rc;
+    }
+    return WS_OK;
+}
+
+// Host buffers: events pipelined over two device slots (event e computes
+// while event e-1's outputs stream back on the copy stream). Calls whose
+// workspace overflowed are re-run (the device recorded the sizes they need),
+// at most kMaxAttempts times; an overflow never returns WS_OK.
+// frames / adcs / charges: [n_events * n_planes] host pointers (arrays and
+// entries nullable).
+int events_host(ws_ctx* ctx, uint32_t n_events, uint32_t n_planes, ws_plane* const* planes,
+                const ws_depo* const* depos, const uint64_t* n_depos, const ws_sim_options* opt,
+                const ws_readout* spec, void* const* frames, void* const* adcs, float* const* charges,
+                ws_timing* timing)
+{
+    if (int rc = check_plane_set(ctx, n_planes, planes)) return rc;
+    if (int rc = check_opts(opt)) return rc;
+    if (int rc = check_readout(spec, n_planes, planes)) return rc;
+    if (n_events == 0 || n_planes == 0) return WS_OK;
+    if (!depos || !n_depos) return set_err(WS_EINVAL, "null argument");
+    WS_CUDA(cudaSetDevice(ctx->device));
+    if (int rc = finish_pending(ctx)) return rc;
+    if (!ctx->copy_stream) WS_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    for (int s = 0; s < 2; ++s) {
+        if (!ctx->slot_computed[s]) WS_CUDA(cudaEventCreateWithFlags(&ctx->slot_computed[s], cudaEventDisableTiming));
+        if (!ctx->slot_copied[s]) WS_CUDA(cudaEventCreateWithFlags(&ctx->slot_copied[s], cudaEventDisableTiming));
+    }
+    const size_t total = (size_t)n_events * n_planes;
+    auto any = [&](void* const* a) {
+        if (a)
+            for (size_t k = 0; k < total; ++k)
+                if (a[k]) return true;
+        return false;
+    };
+    const bool want_f = any(frames), want_a = spec && any(adcs);
+    const bool want_c = charges && any(reinterpret_cast<void* const*>(charges));
+    if (!want_f && !want_a && !want_c) return set_err(WS_EINVAL, "no output requested");
+    // per-slot device layout, per plane: [frame][adc][charge]
+    std::vector<size_t> off_f(n_planes), off_a(n_planes), off_c(n_planes);
+    size_t slot_bytes = 0;
+    for (uint32_t i = 0; i < n_planes; ++i) {
+        const size_t cells = (size_t)planes[i]->W * planes[i]->N;
+        auto put = [&](bool on, size_t el) {
+            const size_t o = slot_bytes;
+            if (on) slot_bytes += (cells * el + 255) & ~(size_t)255;
+            return o;
+        };
+        off_f[i] = put(want_f, frame_elem(spec));
+        off_a[i] = put(want_a, adc_elem(spec));
+        off_c[i] = put(want_c, 4);
+    }
+    size_t max_units = 0;
+    for (uint32_t e = 0; e < n_events; ++e) {
+        size_t u = 0;
+        for (uint32_t i = 0; i < n_planes; ++i) u += n_depos[(size_t)e * n_planes + i];
+        max_units = std::max(max_units, u);
+    }
+    WS_CUDA(ctx->depos.reserve(2 * max_units + 1));
+    WS_CUDA(ctx->out_stage.reserve(2 * slot_bytes));
+    unsigned char* stage = ctx->out_stage.p;
+    std::vector<const ws_depo*> dd(n_planes);
+    std::vector<void*> df(n_planes), da(n_planes);
+    std::vector<float*> dc(n_planes);
+
+    std::vector<uint32_t> todo(n_events);
+    for (uint32_t e = 0; e < n_events; ++e) todo[e] = e;
+    for (int attempt = 0; attempt < kMaxAttempts && !todo.empty(); ++attempt) {
+        ctx->failed_tags.clear();
+        int rc = WS_OK;
+        for (size_t j = 0; j < todo.size() && rc == WS_OK; ++j) {
+            const uint32_t e = todo[j];
+            const int slot = (int)(j & 1u);
+            rc = [&]() -> int {
+                if (j >= 2) WS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->slot_copied[slot], 0));
+                size_t uo = (size_t)slot * max_units;
+                unsigned char* base = stage + (size_t)slot * slot_bytes;
+                for (uint32_t i = 0; i < n_planes; ++i) {
+                    const size_t k = (size_t)e * n_planes + i;
+                    dd[i] = ctx->depos.p + uo;
+                    if (n_depos[k])
+                        WS_CUDA(cudaMemcpyAsync(ctx->depos.p + uo, depos[k], sizeof(ws_depo) * n_depos[k],
+                                                cudaMemcpyHostToDevice, ctx->stream));
+                    uo += n_depos[k];
+                    df[i] = frames && frames[k] ? base + off_f[i] : nullptr;
+                    da[i] = want_a && adcs[k] ? base + off_a[i] : nullptr;
+                    dc[i] = want_c && charges[k] ? reinterpret_cast<float*>(base + off_c[i]) : nullptr;
+                }
+                ctx->call_tag = (int)e;
+                const int r = event_device(ctx, n_planes, planes, dd.data(), n_depos + (size_t)e * n_planes, opt, spec,
+                                           df.data(), da.data(), want_c ? dc.data() : nullptr,
+                                           e == 0 ? timing : nullptr);
+                ctx->call_tag = -1;
+                if (r) return r;
+                WS_CUDA(cudaEventRecord(ctx->slot_computed[slot], ctx->stream));
+                WS_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->slot_computed[slot], 0));
+                for (uint32_t i = 0; i < n_planes; ++i) {
+                    const size_t k = (size_t)e * n_planes + i, cells = (size_t)planes[i]->W * planes[i]->N;
+                    if (df[i])
+                        WS_CUDA(cudaMemcpyAsync(frames[k], df[i], cells * frame_elem(spec), cudaMemcpyDeviceToHost,
+                                                ctx->copy_stream));
+                    if (da[i])
+                        WS_CUDA(cudaMemcpyAsync(adcs[k], da[i], cells * adc_elem(spec), cudaMemcpyDeviceToHost,
+                                                ctx->copy_stream));
+                    if (dc[i])
+                        WS_CUDA(cudaMemcpyAsync(charges[k], dc[i], cells * 4, cudaMemcpyDeviceToHost,
+                                                ctx->copy_stream));
+                }
+                WS_CUDA(cudaEventRecord(ctx->slot_copied[slot], ctx->copy_stream));
+                return WS_OK;
+            }();
+        }
+        // every copy has landed before this returns, whatever happened
+        const cudaError_t ce = cudaStreamSynchronize(ctx->copy_stream);
+        if (rc == WS_OK && ce != cudaSuccess)
+            rc = set_err(WS_ECUDA, "copy stream: %s", cudaGetErrorString(ce));
+        const int frc = finish_pending(ctx);
+        if (rc == WS_OK || rc == WS_ERANGE) rc = frc;
+        if (rc && rc != WS_ERANGE) return rc;
+        std::vector<uint32_t> redo;
+        for (int t : ctx->failed_tags) redo.push_back((uint32_t)t);
+        std::sort(redo.begin(), redo.end());
+        redo.erase(std::unique(redo.begin(), redo.end()), redo.end());
+        if (rc == WS_ERANGE && redo.empty()) return rc;  // an untagged overflow: nothing to re-run
+        todo.swap(redo);
+    }
+    ctx->failed_tags.clear();
+    if (!todo.empty())
+        return set_err(WS_ERANGE, "workspace: %zu event(s) still overflow after %d attempts", todo.size(),
+                       kMaxAttempts);
+    return WS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int ws_simulate_event_device(ws_ctx* ctx, uint32_t n_planes, ws_plane* const* planes, const ws_depo* const* depos,
                              const uint64_t* n_depos, const ws_sim_options* opt, float* const* frames,
                              ws_timing* timing)
@@ -1000,24 +1383,20 @@ int ws_simulate_event_device(ws_ctx* ctx, uint32_t n_planes, ws_plane* const* pl
     if (int rc = check_plane_set(ctx, n_planes, planes)) return rc;
     if (int rc = check_opts(opt)) return rc;
     WS_CUDA(cudaSetDevice(ctx->device));
-    std::vector<float*> charges(n_planes, nullptr);
-    if (opt->fluctuate) {
-        size_t total = 0;
-        for (uint32_t i = 0; i < n_planes; ++i) total += (size_t)planes[i]->W * planes[i]->N;
-        WS_CUDA(ctx->charges.reserve(total));
-        size_t off = 0;
-        for (uint32_t i = 0; i < n_planes; ++i) {
-            charges[i] = ctx->charges.p + off;
-            off += (size_t)planes[i]->W * planes[i]->N;
-        }
-    }
-    for (uint32_t g = 0; g < n_planes; g += wsb::kMaxPlanes) {
-        const uint32_t n = std::min<uint32_t>(wsb::kMaxPlanes, n_planes - g);
-        const int rc = run_group(ctx, n, planes + g, depos + g, n_depos + g, opt, frames + g,
-                                 opt->fluctuate ? charges.data() + g : nullptr, nullptr, g == 0 ? timing : nullptr);
-        if (rc) return rc;
-    }
-    return WS_OK;
+    return event_device(ctx, n_planes, planes, depos, n_depos, opt, nullptr,
+                        reinterpret_cast<void* const*>(frames), nullptr, nullptr, timing);
+}
+
+int ws_run_event_device(ws_ctx* ctx, uint32_t n_planes, ws_plane* const* planes, const ws_depo* const* depos,
+                        const uint64_t* n_depos, const ws_sim_options* opt, const ws_readout* readout,
+                        void* const* adcs, void* const* frames, ws_timing* timing)
+{
+    if (int rc = check_plane_set(ctx, n_planes, planes)) return rc;
+    if (int rc = check_opts(opt)) return rc;
+    if (!readout) return set_err(WS_EINVAL, "null readout");
+    if (int rc = check_readout(readout, n_planes, planes)) return rc;
+    WS_CUDA(cudaSetDevice(ctx->device));
+    return event_device(ctx, n_planes, planes, depos, n_depos, opt, readout, frames, adcs, nullptr, timing);
 }
 
 int ws_simulate_plane_device(ws_plane* p, const ws_depo* depos, uint64_t n, const ws_sim_options* opt, float* frame,
@@ -1025,19 +1404,30 @@ int ws_simulate_plane_device(ws_plane* p, const ws_depo* depos, uint64_t n, cons
 {
     if (!p) return set_err(WS_EINVAL, "null plane");
     if (int rc = check_opts(opt)) return rc;
-    ws_ctx* c = p->ctx;
-    WS_CUDA(cudaSetDevice(c->device));
-    float* ch = charge;
-    if (opt->fluctuate && !ch) {
-        WS_CUDA(c->charges.reserve((size_t)p->W * p->N));
-        ch = c->charges.p;
-    }
+    WS_CUDA(cudaSetDevice(p->ctx->device));
     ws_plane* planes[1] = {p};
     const ws_depo* dp[1] = {depos};
     uint64_t nd[1] = {n};
-    float* fr[1] = {frame};
-    float* chs[1] = {ch};
-    return run_group(c, 1, planes, dp, nd, opt, fr, ch ? chs : nullptr, nullptr, timing);
+    void* fr[1] = {frame};
+    float* ch[1] = {charge};
+    return event_device(p->ctx, 1, planes, dp, nd, opt, nullptr, fr, nullptr, ch, timing);
+}
+
+int ws_run_simulation_device(ws_plane* p, const ws_depo* depos, uint64_t n, const ws_sim_options* opt,
+                             const ws_readout* readout, void* adc, void* frame, float* charge, ws_timing* timing)
+{
+    if (!p) return set_err(WS_EINVAL, "null plane");
+    if (int rc = check_opts(opt)) return rc;
+    if (!readout) return set_err(WS_EINVAL, "null readout");
+    ws_plane* planes[1] = {p};
+    if (int rc = check_readout(readout, 1, planes)) return rc;
+    WS_CUDA(cudaSetDevice(p->ctx->device));
+    const ws_depo* dp[1] = {depos};
+    uint64_t nd[1] = {n};
+    void* fr[1] = {frame};
+    void* ad[1] = {adc};
+    float* ch[1] = {charge};
+    return event_device(p->ctx, 1, planes, dp, nd, opt, readout, fr, ad, ch, timing);
 }
 
 int ws_rasterize_device(ws_plane* p, const ws_depo* depos, uint64_t n, const ws_sim_options* opt, float* charge,
@@ -1050,7 +1440,7 @@ int ws_rasterize_device(ws_plane* p, const ws_depo* depos, uint64_t n, const ws_
     const ws_depo* dp[1] = {depos};
     uint64_t nd[1] = {n};
     float* chs[1] = {charge};
-    return run_group(p->ctx, 1, planes, dp, nd, opt, nullptr, chs, nullptr, timing);
+    return run_group(p->ctx, 1, planes, dp, nd, opt, nullptr, chs, nullptr, timing, nullptr, true);
 }
 
 int ws_convolve_device(ws_plane* p, const float* charge, float* frame)
@@ -1067,117 +1457,26 @@ int ws_convolve_device(ws_plane* p, const float* charge, float* frame)
 int ws_simulate_event(ws_ctx* ctx, uint32_t n_planes, ws_plane* const* planes, const ws_depo* const* depos,
                       const uint64_t* n_depos, const ws_sim_options* opt, float* const* frames, ws_timing* timing)
 {
-    if (int rc = check_plane_set(ctx, n_planes, planes)) return rc;
-    if (int rc = check_opts(opt)) return rc;
-    WS_CUDA(cudaSetDevice(ctx->device));
-    if (int rc = finish_pending(ctx)) return rc;
-    // host validation the reference does at ingestion / drift time
-    size_t units = 0, cells = 0;
-    for (uint32_t i = 0; i < n_planes; ++i) {
-        units += n_depos[i];
-        cells += (size_t)planes[i]->W * planes[i]->N;
-    }
-    WS_CUDA(ctx->depos.reserve(units));
-    WS_CUDA(ctx->frames.reserve(cells));
-    std::vector<const ws_depo*> dd(n_planes);
-    std::vector<float*> ff(n_planes);
-    size_t uo = 0, co = 0;
-    for (uint32_t i = 0; i < n_planes; ++i) {
-        dd[i] = ctx->depos.p + uo;
-        ff[i] = ctx->frames.p + co;
-        if (n_depos[i])
-            WS_CUDA(cudaMemcpyAsync(ctx->depos.p + uo, depos[i], sizeof(ws_depo) * n_depos[i], cudaMemcpyHostToDevice,
-                                    ctx->stream));
-        uo += n_depos[i];
-        co += (size_t)planes[i]->W * planes[i]->N;
-    }
-    for (int attempt = 0; attempt < 3; ++attempt) {
-        if (int rc = ws_simulate_event_device(ctx, n_planes, planes, dd.data(), n_depos, opt, ff.data(), timing))
-            return rc;
-        const int rc = finish_pending(ctx);
-        if (rc == WS_ERANGE) continue;  // pool grown; re-run
-        if (rc) return rc;
-        break;
-    }
-    co = 0;
-    for (uint32_t i = 0; i < n_planes; ++i) {
-        const size_t nc = (size_t)planes[i]->W * planes[i]->N;
-        if (frames && frames[i])
-            WS_CUDA(cudaMemcpyAsync(frames[i], ctx->frames.p + co, sizeof(float) * nc, cudaMemcpyDeviceToHost,
-                                    ctx->stream));
-        co += nc;
-    }
-    WS_CUDA(cudaStreamSynchronize(ctx->stream));
-    return WS_OK;
+    if (!frames) return set_err(WS_EINVAL, "null frames");
+    return events_host(ctx, 1, n_planes, planes, depos, n_depos, opt, nullptr,
+                       reinterpret_cast<void* const*>(frames), nullptr, nullptr, timing);
 }
 
 int ws_simulate_events(ws_ctx* ctx, uint32_t n_events, uint32_t n_planes, ws_plane* const* planes,
                        const ws_depo* const* depos, const uint64_t* n_depos, const ws_sim_options* opt,
                        float* const* frames, ws_timing* timing)
 {
-    if (int rc = check_plane_set(ctx, n_planes, planes)) return rc;
-    if (int rc = check_opts(opt)) return rc;
-    if (n_events == 0 || n_planes == 0) return WS_OK;
-    if (!depos || !n_depos || !frames) return set_err(WS_EINVAL, "null argument");
-    WS_CUDA(cudaSetDevice(ctx->device));
-    if (int rc = finish_pending(ctx)) return rc;
-    if (!ctx->copy_stream) WS_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
-    for (int s = 0; s < 2; ++s) {
-        if (!ctx->slot_computed[s]) WS_CUDA(cudaEventCreateWithFlags(&ctx->slot_computed[s], cudaEventDisableTiming));
-        if (!ctx->slot_copied[s]) WS_CUDA(cudaEventCreateWithFlags(&ctx->slot_copied[s], cudaEventDisableTiming));
-    }
-    size_t cells = 0, max_units = 0;
-    for (uint32_t i = 0; i < n_planes; ++i) cells += (size_t)planes[i]->W * planes[i]->N;
-    for (uint32_t e = 0; e < n_events; ++e) {
-        size_t u = 0;
-        for (uint32_t i = 0; i < n_planes; ++i) u += n_depos[(size_t)e * n_planes + i];
-        max_units = std::max(max_units, u);
-    }
-    WS_CUDA(ctx->depos.reserve(2 * max_units + 1));
-    WS_CUDA(ctx->frames.reserve(2 * cells));
-    std::vector<const ws_depo*> dd(n_planes);
-    std::vector<float*> ff(n_planes);
-    // two slots: event e computes into slot e&1 on the compute stream while the
-    // copy stream drains slot (e-1)&1 to the host (H2D is tiny, D2H dominates)
-    for (uint32_t e = 0; e < n_events; ++e) {
-        const int slot = (int)(e & 1u);
-        if (e >= 2) WS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->slot_copied[slot], 0));
-        size_t uo = (size_t)slot * max_units, co = (size_t)slot * cells;
-        for (uint32_t i = 0; i < n_planes; ++i) {
-            const size_t k = (size_t)e * n_planes + i;
-            dd[i] = ctx->depos.p + uo;
-            ff[i] = ctx->frames.p + co;
-            if (n_depos[k])
-                WS_CUDA(cudaMemcpyAsync(ctx->depos.p + uo, depos[k], sizeof(ws_depo) * n_depos[k],
-                                        cudaMemcpyHostToDevice, ctx->stream));
-            uo += n_depos[k];
-            co += (size_t)planes[i]->W * planes[i]->N;
-        }
-        if (int rc = ws_simulate_event_device(ctx, n_planes, planes, dd.data(), n_depos + (size_t)e * n_planes, opt,
-                                              ff.data(), e == 0 ? timing : nullptr))
-            return rc;
-        WS_CUDA(cudaEventRecord(ctx->slot_computed[slot], ctx->stream));
-        WS_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->slot_computed[slot], 0));
-        for (uint32_t i = 0; i < n_planes; ++i) {
-            float* dst = frames[(size_t)e * n_planes + i];
-            const size_t nc = (size_t)planes[i]->W * planes[i]->N;
-            if (dst)
-                WS_CUDA(cudaMemcpyAsync(dst, ff[i], sizeof(float) * nc, cudaMemcpyDeviceToHost, ctx->copy_stream));
-        }
-        WS_CUDA(cudaEventRecord(ctx->slot_copied[slot], ctx->copy_stream));
-    }
-    WS_CUDA(cudaStreamSynchronize(ctx->copy_stream));
-    const int rc = finish_pending(ctx);
-    if (rc == WS_ERANGE) {
-        // workspace grew on overflow: redo the batch event by event (synchronous path retries)
-        for (uint32_t e = 0; e < n_events; ++e)
-            if (int r2 = ws_simulate_event(ctx, n_planes, planes, depos + (size_t)e * n_planes,
-                                           n_depos + (size_t)e * n_planes, opt, frames + (size_t)e * n_planes,
-                                           e == 0 ? timing : nullptr))
-                return r2;
-        return WS_OK;
-    }
-    return rc;
+    if (n_events && n_planes && !frames) return set_err(WS_EINVAL, "null frames");
+    return events_host(ctx, n_events, n_planes, planes, depos, n_depos, opt, nullptr,
+                       reinterpret_cast<void* const*>(frames), nullptr, nullptr, timing);
+}
+
+int ws_run_events(ws_ctx* ctx, uint32_t n_events, uint32_t n_planes, ws_plane* const* planes,
+                  const ws_depo* const* depos, const uint64_t* n_depos, const ws_sim_options* opt,
+                  const ws_readout* readout, void* const* adcs, void* const* frames, ws_timing* timing)
+{
+    if (!readout) return set_err(WS_EINVAL, "null readout");
+    return events_host(ctx, n_events, n_planes, planes, depos, n_depos, opt, readout, frames, adcs, nullptr, timing);
 }
 
 int ws_noise_digitize_device(ws_plane* p, float* frame, const ws_noise_model* noise, double scale, double offset,
@@ -1188,6 +1487,7 @@ int ws_noise_digitize_device(ws_plane* p, float* frame, const ws_noise_model* no
     const int spectrum = noise && noise->mode == WS_NOISE_SPECTRUM;
     if (noise && noise->mode != WS_NOISE_OFF && !white && !spectrum)
         return set_err(WS_EINVAL, "add_noise: unknown noise mode %d", noise->mode);
+    const wsb::Sink sk{frame, nullptr, adc, 0, scale, offset, (double)((1 << (adc && bits >= 1 && bits <= 16 ? bits : 1)) - 1)};
     if (spectrum) {
         if (noise->rng_mode != WS_RNG_SUBSTREAM && noise->rng_mode != WS_RNG_PHILOX)
             return set_err(WS_EINVAL, "add_noise: unknown rng mode %d", noise->rng_mode);
@@ -1205,8 +1505,8 @@ int ws_noise_digitize_device(ws_plane* p, float* frame, const ws_noise_model* no
         WS_CUDA(cudaMemcpyAsync(c->noise_amp.p, noise->amplitude_spectrum, sizeof(double) * p->N,
                                 cudaMemcpyHostToDevice, c->stream));
         const PlaneDesc d = plane_desc(p);
-        WS_CUDA(wsb_launch_noise_spectrum(d, c->noise_amp.p, noise->seed, noise->rng_mode, frame, adc, scale, offset,
-                                          (double)((1 << (adc ? bits : 1)) - 1), c->conv_variant, c->stream));
+        WS_CUDA(wsb_launch_noise_spectrum(d, c->noise_amp.p, noise->seed, noise->rng_mode, frame, sk, c->conv_variant,
+                                          c->stream));
         c->launches += 1;
         return WS_OK;
     }
@@ -1218,9 +1518,10 @@ int ws_noise_digitize_device(ws_plane* p, float* frame, const ws_noise_model* no
     if (!do_noise && !adc) return WS_OK;
     ws_ctx* c = p->ctx;
     WS_CUDA(cudaSetDevice(c->device));
-    WS_CUDA(wsb_launch_noise(frame, adc, p->W, p->N, do_noise, do_noise ? noise->rng_mode : WS_RNG_PHILOX,
-                             do_noise ? noise->sigma : 0.0, do_noise ? noise->seed : 0, scale, offset,
-                             (double)((1 << (adc ? bits : 1)) - 1), c->stream));
+    wsb::Sink k = sk;
+    if (!do_noise) k.frame = nullptr;  // digitize only: the frame is untouched
+    WS_CUDA(wsb_launch_noise(frame, k, p->W, p->N, do_noise, do_noise ? noise->rng_mode : WS_RNG_PHILOX,
+                             do_noise ? noise->sigma : 0.0, do_noise ? noise->seed : 0, c->stream));
     c->launches += 1;
     return WS_OK;
 }
@@ -1229,29 +1530,29 @@ int ws_simulate_plane(ws_plane* p, const ws_depo* depos, uint64_t n, const ws_si
                       float* charge, ws_timing* timing)
 {
     if (!p) return set_err(WS_EINVAL, "null plane");
-    if (int rc = check_opts(opt)) return rc;
-    ws_ctx* c = p->ctx;
-    WS_CUDA(cudaSetDevice(c->device));
-    if (int rc = finish_pending(c)) return rc;
-    const size_t cells = (size_t)p->W * p->N;
-    WS_CUDA(c->depos.reserve(n));
-    WS_CUDA(c->frames.reserve(cells));
-    if (charge || opt->fluctuate) WS_CUDA(c->charges.reserve(cells));
-    if (n) WS_CUDA(cudaMemcpyAsync(c->depos.p, depos, sizeof(ws_depo) * n, cudaMemcpyHostToDevice, c->stream));
-    for (int attempt = 0; attempt < 3; ++attempt) {
-        if (int rc = ws_simulate_plane_device(p, c->depos.p, n, opt, frame ? c->frames.p : nullptr,
-                                              (charge || opt->fluctuate) ? c->charges.p : nullptr, timing))
-            return rc;
-        const int rc = finish_pending(c);
-        if (rc == WS_ERANGE) continue;
-        if (rc) return rc;
-        break;
-    }
-    if (frame) WS_CUDA(cudaMemcpyAsync(frame, c->frames.p, sizeof(float) * cells, cudaMemcpyDeviceToHost, c->stream));
-    if (charge) WS_CUDA(cudaMemcpyAsync(charge, c->charges.p, sizeof(float) * cells, cudaMemcpyDeviceToHost, c->stream));
-    WS_CUDA(cudaStreamSynchronize(c->stream));
-    return WS_OK;
+    ws_plane* planes[1] = {p};
+    const ws_depo* dp[1] = {depos};
+    uint64_t nd[1] = {n};
+    void* fr[1] = {frame};
+    float* ch[1] = {charge};
+    return events_host(p->ctx, 1, 1, planes, dp, nd, opt, nullptr, fr, nullptr, ch, timing);
 }
+
+int ws_run_simulation(ws_plane* p, const ws_depo* depos, uint64_t n, const ws_sim_options* opt,
+                      const ws_readout* readout, void* adc, void* frame, float* charge, ws_timing* timing)
+{
+    if (!p) return set_err(WS_EINVAL, "null plane");
+    if (!readout) return set_err(WS_EINVAL, "null readout");
+    ws_plane* planes[1] = {p};
+    const ws_depo* dp[1] = {depos};
+    uint64_t nd[1] = {n};
+    void* fr[1] = {frame};
+    void* ad[1] = {adc};
+    float* ch[1] = {charge};
+    return events_host(p->ctx, 1, 1, planes, dp, nd, opt, readout, fr, ad, ch, timing);
+}
+
+}  // extern "C"
 
 // ---- signal processing (ws_sigproc.cu) -------------------------------------
 
@@ -1387,6 +1688,8 @@ int sigproc_residue(ws_ctx* c, double* max_rel_imag)
 }
 
 }  // namespace
+
+extern "C" {
 
 uint64_t ws_sigproc_max_cols(void) { return (uint64_t)wsb_sigproc_max_n(); }
 

@@ -82,9 +82,13 @@ struct PlaneDesc {
     int32_t rows_per_band;     // FFT bands
     int32_t n_bands;           // bins of this plane in this call
     float* frame;              // out: M (nullable when only the charge grid is wanted)
+    double* frame64;           // out: M widened to fp64 (readout, nullable)
+    void* adc;                 // out: digitized codes, int32 or uint16 per EventDesc::adc_u16 (readout, nullable)
     float* charge_out;         // out: S (nullable)
     const float* charge_in;    // in: S (mode "grid")
+    uint32_t* charge_u32;      // fluctuation on: the integer charge grid (exact sums, mode 1 reads it)
     long long* stats;          // [0] clipped_charge, [1] clipped_patches
+    uint32_t* tile_need;       // fixed tile lists: the largest slot + 1 that did not fit (atomicMax, 0 = none)
 };
 
 struct EventDesc {
@@ -105,11 +109,22 @@ struct EventDesc {
     uint32_t tile_cap;
     TEnt* tiles;
     uint32_t* tile_count;
+    uint32_t* list_need;       // CSR lists: the entry total when it exceeded list_cap (k_fill_bands)
+    unsigned* err;             // the call's error flags
+    // readout fused into the frame-store epilogues (add_noise + digitize,
+    // spectral.cpp:177-196, 228-238): ro = 0 -> plain fp32 frame stores
+    int32_t ro;
+    int32_t ro_noise;          // 1: white noise from the Philox stream (seed ^ salt, wire), pair p -> draws 2p, 2p+1
+    int32_t adc_u16;           // adc element type: 0 int32 (Matrix<int32_t>), 1 uint16
+    double ro_sigma;
+    uint64_t ro_seed;
+    double adc_scale, adc_offset, adc_max;
     PlaneDesc p[kMaxPlanes];
 };
 
 // Error / overflow flags shared by kernels (device scalar words).
-enum : unsigned { kErrPool = 1u, kErrDomain = 2u, kErrCharge = 4u, kErrRange = 8u, kErrTileCap = 16u };
+enum : unsigned { kErrPool = 1u, kErrDomain = 2u, kErrCharge = 4u, kErrRange = 8u, kErrTileCap = 16u,
+                  kErrCellOvf = 32u };
 
 __device__ __forceinline__ int band_plane(const EventDesc& ev, uint32_t gb)
 {
@@ -409,6 +424,99 @@ __device__ __forceinline__ int64_t binomial_approx(int64_t n, double p, Rng& src
     if (k < 0.0) return 0;
     if (k > (double)n) return n;
     return (int64_t)k;
+}
+
+// ---------------------------------------------------------------- readout --
+// add_noise (white, spectral.cpp:184-196) + digitize (spectral.cpp:228-238)
+// of frame samples, fused into the store epilogue of the convolution kernels
+// (or run by ws_noise.cu / k_noise_spectrum after them). Noise is added in
+// fp64 to the fp32 sample, as the unfused kernels do, so both give the same
+// bits; the ADC code is round(v * scale + offset) clamped to [0, 2^bits - 1].
+constexpr uint64_t kWhiteNoiseSalt = 0x77686974656e6f69ULL;  // spectral.cpp:21
+
+struct Sink {  // outputs of one plane's samples (any may be null)
+    float* frame;
+    double* frame64;
+    void* adc;
+    int adc_u16;
+    double scale, offset, max_code;
+};
+
+__device__ __forceinline__ int adc_code(double v, double scale, double offset, double max_code)
+{
+    const double c = round(__dadd_rn(__dmul_rn(v, scale), offset));
+    return (int)(c < 0.0 ? 0.0 : (c > max_code ? max_code : c));
+}
+
+__device__ __forceinline__ void sink_put(const Sink& k, size_t i, double v)
+{
+    if (k.frame) k.frame[i] = (float)v;
+    if (k.frame64) k.frame64[i] = v;
+    if (k.adc) {
+        const int c = adc_code(v, k.scale, k.offset, k.max_code);
+        if (k.adc_u16) static_cast<uint16_t*>(k.adc)[i] = (uint16_t)c;
+        else static_cast<int32_t*>(k.adc)[i] = c;
+    }
+}
+
+// White-noise pair p of wire w (Philox): the normals of ticks 2p and 2p+1
+__device__ __forceinline__ void white_pair(uint64_t seed, int w, int p, double& n0, double& n1)
+{
+    Rng src;
+    src.init(WS_RNG_PHILOX, seed ^ kWhiteNoiseSalt, (uint64_t)w);
+    src.draw = 2u * (uint32_t)p;
+    n0 = src.normal();
+    n1 = src.normal();  // the cached spare
+}
+
+// Readout of samples t, t+1 of row w (t even; has1 false past the row end)
+__device__ __forceinline__ void readout_pair(const EventDesc& ev, const PlaneDesc& P, int w, int t, float v0, float v1,
+                                             bool has1)
+{
+    double a = (double)v0, b = (double)v1;
+    if (ev.ro_noise) {
+        double n0, n1;
+        white_pair(ev.ro_seed, w, t >> 1, n0, n1);
+        a = __dadd_rn(a, __dmul_rn(ev.ro_sigma, n0));
+        b = __dadd_rn(b, __dmul_rn(ev.ro_sigma, n1));
+    }
+    const Sink k{P.frame, P.frame64, P.adc, ev.adc_u16, ev.adc_scale, ev.adc_offset, ev.adc_max};
+    const size_t i = (size_t)w * P.N + t;
+    sink_put(k, i, a);
+    if (has1) sink_put(k, i + 1, b);
+}
+
+// Readout of 4 samples t..t+3 of row w (t a multiple of 4, all in the row;
+// the row length a multiple of 4): vector stores
+__device__ __forceinline__ void readout4(const EventDesc& ev, const PlaneDesc& P, int w, int t, const float v[4])
+{
+    double x[4] = {(double)v[0], (double)v[1], (double)v[2], (double)v[3]};
+    if (ev.ro_noise) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            double n0, n1;
+            white_pair(ev.ro_seed, w, (t >> 1) + h, n0, n1);
+            x[2 * h] = __dadd_rn(x[2 * h], __dmul_rn(ev.ro_sigma, n0));
+            x[2 * h + 1] = __dadd_rn(x[2 * h + 1], __dmul_rn(ev.ro_sigma, n1));
+        }
+    }
+    const size_t i = (size_t)w * P.N + t;
+    if (P.frame)
+        __stcs(reinterpret_cast<float4*>(P.frame + i), make_float4((float)x[0], (float)x[1], (float)x[2], (float)x[3]));
+    if (P.frame64) {
+        __stcs(reinterpret_cast<double2*>(P.frame64 + i), make_double2(x[0], x[1]));
+        __stcs(reinterpret_cast<double2*>(P.frame64 + i) + 1, make_double2(x[2], x[3]));
+    }
+    if (P.adc) {
+        int c[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c[j] = adc_code(x[j], ev.adc_scale, ev.adc_offset, ev.adc_max);
+        if (ev.adc_u16)
+            __stcs(reinterpret_cast<uint2*>(static_cast<uint16_t*>(P.adc) + i),
+                   make_uint2((uint32_t)c[0] | ((uint32_t)c[1] << 16), (uint32_t)c[2] | ((uint32_t)c[3] << 16)));
+        else
+            __stcs(reinterpret_cast<int4*>(static_cast<int32_t*>(P.adc) + i), make_int4(c[0], c[1], c[2], c[3]));
+    }
 }
 
 // sigproc chain (ws_sigproc.cu): one launch over a batch of signal rows

@@ -227,14 +227,17 @@ k_conv(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* __
                     for (int dw = -P.h; dw <= P.h; ++dw) {
                         int src = (w - dw) % W;
                         if (src < 0) src += W;
-                        s += (float)P.ww[dw + P.h] * __ldg(&P.charge_in[(size_t)src * N + t]);
+                        // the integer grid of the fluctuation walk, or a float grid (ws_convolve_device)
+                        const float q = P.charge_u32 ? (float)__ldg(&P.charge_u32[(size_t)src * N + t])
+                                                     : __ldg(&P.charge_in[(size_t)src * N + t]);
+                        s += (float)P.ww[dw + P.h] * q;
                     }
                 }
                 xs[t] = s;
             }
         }
         __syncthreads();
-        if (!want_frame) continue;
+        if (!want_frame || !(P.frame || P.frame64 || P.adc)) continue;  // (block-uniform)
 
         fft_dif<NT, MAXR>(buf, M, P.fft, tw_m);
 
@@ -279,11 +282,9 @@ k_conv(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* __
         fft_dit<NT, MAXR>(buf, M, P.fft, tw_m);
 
         // y[2n] = Re res[n], y[2n+1] = -Im res[n]  (1/M folded into H)
-        float* frow = P.frame + (size_t)w * N;
         const int hi_wrap = P.hi_lag;      // t < hi_wrap: + y[t + N]
         const int lo_wrap = N + P.lo_lag;  // t >= lo_wrap: + y[t - N + Np]
-#pragma unroll 4
-        for (int t = tid; t < N; t += NT) {
+        auto sample = [&](int t) {
             float y = (t & 1) ? -xs[t] : xs[t];
             if (P.folded) {
                 if (t < hi_wrap) {
@@ -295,7 +296,18 @@ k_conv(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* __
                     y += (tt & 1) ? -xs[tt] : xs[tt];
                 }
             }
-            __stcs(&frow[t], y);  // streaming store: keep the band data in L2
+            return y;
+        };
+        if (!ev.ro) {
+            float* frow = P.frame + (size_t)w * N;
+#pragma unroll 4
+            for (int t = tid; t < N; t += NT) __stcs(&frow[t], sample(t));  // streaming store: keep the band data in L2
+        } else {
+            // fused readout (noise + digitize, fp64 frame), one tick pair per thread
+            for (int t = 2 * tid; t < N; t += 2 * NT) {
+                const bool has1 = t + 1 < N;
+                readout_pair(ev, P, w, t, sample(t), has1 ? sample(t + 1) : 0.0f, has1);
+            }
         }
         __syncthreads();
     }
@@ -313,8 +325,8 @@ k_conv(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* __
 // Needs an even, 7-smooth padded tick count (Np == N).
 template <int NT, int MAXR>
 __global__ void __launch_bounds__(NT)
-k_noise_spectrum(const PlaneDesc P, const double* __restrict__ amp, uint64_t seed, int rng_mode, float* frame,
-                 int32_t* adc, double scale, double offset, double max_code)
+k_noise_spectrum(const PlaneDesc P, const double* __restrict__ amp, uint64_t seed, int rng_mode, const float* in,
+                 const Sink out)
 {
     constexpr uint64_t kSpectrumNoiseSalt = 0x737065636e6f6973ULL;  // spectral.cpp:22
     extern __shared__ __align__(16) unsigned char smem[];
@@ -381,12 +393,7 @@ k_noise_spectrum(const PlaneDesc P, const double* __restrict__ amp, uint64_t see
     const size_t base = (size_t)w * N;
     for (int t = tid; t < N; t += NT) {
         const float y = (t & 1) ? -xs[t] : xs[t];
-        const double v = __dadd_rn((double)frame[base + t], (double)y);
-        frame[base + t] = (float)v;
-        if (adc) {
-            const double c = round(__dadd_rn(__dmul_rn(v, scale), offset));
-            adc[base + t] = (int32_t)(c < 0.0 ? 0.0 : (c > max_code ? max_code : c));
-        }
+        sink_put(out, base + t, __dadd_rn((double)in[base + t], (double)y));
     }
 }
 
@@ -453,16 +460,15 @@ extern "C" size_t wsb_noise_spectrum_smem(int M)
 }
 
 extern "C" cudaError_t wsb_launch_noise_spectrum(const wsb::PlaneDesc& P, const double* amp, uint64_t seed, int rng_mode,
-                                                 float* frame, int32_t* adc, double scale, double offset,
-                                                 double max_code, int variant, cudaStream_t stream)
+                                                 const float* in, const wsb::Sink& out, int variant,
+                                                 cudaStream_t stream)
 {
     const size_t smem = wsb_noise_spectrum_smem(P.M);
     cudaError_t e = conv_device_setup();  // composite-radix twiddles (the DIT below uses them)
     if (e != cudaSuccess) return e;
     if (variant == 8)
-        wsb::k_noise_spectrum<256, 8><<<P.W, 256, smem, stream>>>(P, amp, seed, rng_mode, frame, adc, scale, offset, max_code);
+        wsb::k_noise_spectrum<256, 8><<<P.W, 256, smem, stream>>>(P, amp, seed, rng_mode, in, out);
     else
-        wsb::k_noise_spectrum<256, 25><<<P.W, 256, smem, stream>>>(P, amp, seed, rng_mode, frame, adc, scale, offset,
-                                                                   max_code);
+        wsb::k_noise_spectrum<256, 25><<<P.W, 256, smem, stream>>>(P, amp, seed, rng_mode, in, out);
     return cudaGetLastError();
 }

@@ -330,8 +330,30 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
     __syncthreads();
 
     // frame rows of the window (convolve's real part, spectral.cpp:172-173),
-    // streaming stores; one flattened (row, 16-byte word) loop
-    if ((N & 3) == 0) {  // ws is a multiple of 4 as well: whole 16-byte words
+    // streaming stores; one flattened (row, 16-byte word) loop. With a
+    // readout (ev.ro) the same words go through noise + digitize instead.
+    if (ev.ro) {
+        if ((N & 3) == 0) {
+            constexpr int kW = kTileTicks / 4;
+            const int wlen4 = wlen >> 2;
+            for (int i = tid; i < nr * kW; i += NT) {
+                const int r = i / kW, c4 = i - r * kW;
+                if (c4 >= wlen4) continue;
+                const int* a = acc + r * kRowStride + kMargin + 4 * c4;
+                const float inv = s_inv[r];
+                const float v[4] = {(float)a[0] * inv, (float)a[1] * inv, (float)a[2] * inv, (float)a[3] * inv};
+                readout4(ev, P, r0 + r, ws + 4 * c4, v);
+            }
+        } else {  // N even or odd: tick pairs (ws is even)
+            for (int r = 0; r < nr; ++r)
+                for (int t = 2 * tid; t < wlen; t += 2 * NT) {
+                    const int* a = acc + r * kRowStride + kMargin;
+                    const bool has1 = t + 1 < wlen;
+                    readout_pair(ev, P, r0 + r, ws + t, (float)a[t] * s_inv[r], has1 ? (float)a[t + 1] * s_inv[r] : 0.0f,
+                                 has1);
+                }
+        }
+    } else if ((N & 3) == 0) {  // ws is a multiple of 4 as well: whole 16-byte words
         constexpr int kW = kTileTicks / 4;
         const int wlen4 = wlen >> 2;
         for (int i = tid; i < nr * kW; i += NT) {

@@ -11,32 +11,24 @@
 //     tick pair p draws uniforms 2p and 2p+1 (one Philox4x32-10 call), so
 //     every pair is independent: one thread per pair.
 // The frame is updated in place (float32); the ADC codes (int32, the
-// reference's Matrix<int32_t>) are computed from the fp64 noisy value.
+// reference's Matrix<int32_t>, or uint16) are computed from the fp64 noisy
+// value. The same readout runs fused in the convolution kernels' epilogues
+// (ws_common.cuh readout_pair / readout4) for the Philox stream.
 #include "ws_common.cuh"
+
+#include <algorithm>
 
 namespace wsb {
 
-constexpr uint64_t kWhiteNoiseSalt = 0x77686974656e6f69ULL;  // spectral.cpp:21
-
 struct NoiseArgs {
-    float* frame;
-    int32_t* adc;     // nullable
+    const float* in;  // the frame samples (fp32)
+    Sink out;         // noisy frame (may alias `in`), fp64 frame, ADC codes
     int W, N;
     int noise;        // 0 off, 1 white
     int rng_mode;
     double sigma;
     uint64_t seed;
-    double scale, offset, max_code;
 };
-
-__device__ __forceinline__ void emit(const NoiseArgs& a, size_t i, double v)
-{
-    if (a.noise) a.frame[i] = (float)v;
-    if (a.adc) {
-        const double c = round(__dadd_rn(__dmul_rn(v, a.scale), a.offset));
-        a.adc[i] = (int32_t)(c < 0.0 ? 0.0 : (c > a.max_code ? a.max_code : c));
-    }
-}
 
 __global__ void k_noise_rows(const NoiseArgs a)
 {
@@ -46,9 +38,9 @@ __global__ void k_noise_rows(const NoiseArgs a)
     src.init(WS_RNG_SUBSTREAM, a.seed ^ kWhiteNoiseSalt, (uint64_t)w);
     const size_t base = (size_t)w * a.N;
     for (int t = 0; t < a.N; ++t) {
-        double v = (double)a.frame[base + t];
+        double v = (double)a.in[base + t];
         if (a.noise) v = __dadd_rn(v, __dmul_rn(a.sigma, src.normal()));
-        emit(a, base + t, v);
+        sink_put(a.out, base + t, v);
     }
 }
 
@@ -67,23 +59,39 @@ __global__ void k_noise_pairs(const NoiseArgs a)
         n0 = src.normal();
         n1 = src.normal();  // the cached spare
     }
-    emit(a, base, a.noise ? __dadd_rn((double)a.frame[base], __dmul_rn(a.sigma, n0)) : (double)a.frame[base]);
-    if (2 * p + 1 < a.N)
-        emit(a, base + 1,
-             a.noise ? __dadd_rn((double)a.frame[base + 1], __dmul_rn(a.sigma, n1)) : (double)a.frame[base + 1]);
+    const bool has1 = 2 * p + 1 < a.N;
+    const double v0 = (double)a.in[base], v1 = has1 ? (double)a.in[base + 1] : 0.0;
+    sink_put(a.out, base, a.noise ? __dadd_rn(v0, __dmul_rn(a.sigma, n0)) : v0);
+    if (has1) sink_put(a.out, base + 1, a.noise ? __dadd_rn(v1, __dmul_rn(a.sigma, n1)) : v1);
+}
+
+// integer charge grid (fluctuation on) -> float32 in place
+__global__ void k_u32_to_f32(uint32_t* __restrict__ g, size_t n)
+{
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        reinterpret_cast<float*>(g)[i] = (float)g[i];
 }
 
 }  // namespace wsb
 
-extern "C" cudaError_t wsb_launch_noise(float* frame, int32_t* adc, int W, int N, int noise, int rng_mode, double sigma,
-                                        uint64_t seed, double scale, double offset, double max_code, cudaStream_t s)
+// add_noise (white) + digitize: `in` -> sink (frame in place when noisy, fp64
+// frame, ADC codes); rng substream walks each wire's sequential stream
+extern "C" cudaError_t wsb_launch_noise(const float* in, const wsb::Sink& out, int W, int N, int noise, int rng_mode,
+                                        double sigma, uint64_t seed, cudaStream_t s)
 {
-    const wsb::NoiseArgs a{frame, adc, W, N, noise, rng_mode, sigma, seed, scale, offset, max_code};
+    const wsb::NoiseArgs a{in, out, W, N, noise, rng_mode, sigma, seed};
     if (noise && rng_mode == WS_RNG_SUBSTREAM) {
         wsb::k_noise_rows<<<(W + 63) / 64, 64, 0, s>>>(a);
     } else {
         const size_t pairs = (size_t)W * ((N + 1) / 2);
         wsb::k_noise_pairs<<<(unsigned)((pairs + 255) / 256), 256, 0, s>>>(a);
     }
+    return cudaGetLastError();
+}
+
+extern "C" cudaError_t wsb_launch_u32_to_f32(uint32_t* g, size_t n, cudaStream_t s)
+{
+    if (!n) return cudaSuccess;
+    wsb::k_u32_to_f32<<<(unsigned)std::min<size_t>((n + 255) / 256, 148 * 16), 256, 0, s>>>(g, n);
     return cudaGetLastError();
 }

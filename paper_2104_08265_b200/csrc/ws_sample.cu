@@ -543,10 +543,14 @@ k_sample_off(const EventDesc ev, UnitRec* __restrict__ recs, uint32_t* __restric
         const float* prof = staged ? stage + wex : raw;
         const uint32_t cap = ev.tile_cap;
         emit_tile_entries<false>(P, rec, fixed, prof, ev.tile_count, [&](uint32_t b, uint32_t slot, const TEnt& e) {
-            if (slot < cap)
+            if (slot < cap) {
                 ev.tiles[(size_t)b * cap + slot] = e;
-            else
+            } else {
+                // never dropped silently: the host sizes the re-run from the
+                // real count (or routes the dense plane to the row FFT)
                 atomicOr(err, kErrTileCap);
+                atomicMax(P.tile_need, slot + 1u);
+            }
         });
     }
 }
@@ -619,7 +623,10 @@ __global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ rec
 {
     const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
     if (off[ev.total_bands] > ev.list_cap) {  // grid-uniform
-        if (u == 0) atomicOr(err, kErrRange);
+        if (u == 0) {
+            atomicOr(err, kErrRange);
+            *ev.list_need = off[ev.total_bands];  // the exact size for the re-run
+        }
         return;
     }
     // no early exits below: the warp-collective tile-slot allocation needs every lane
@@ -639,11 +646,25 @@ __global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ rec
                             [&](uint32_t b, uint32_t slot, const TEnt& e) { tlist[off[b] + slot] = e; });
 }
 
+// Electron counts into the integer charge grid (the reference's ChargeGrid is
+// int64, core.hpp:94-99): u32 atomics, exact and order independent; a cell
+// past 2^32 - 1 electrons (or a single draw past it) flags kErrCellOvf, an
+// error of the call, never a silently wrapped sum.
+__device__ __forceinline__ void add_count(uint32_t* cell, int64_t k, unsigned* err)
+{
+    if (k <= 0) return;
+    if (k > 0xffffffffll) {
+        atomicOr(err, kErrCellOvf);
+        return;
+    }
+    const uint32_t old = atomicAdd(cell, (uint32_t)k);
+    if ((uint32_t)(old + (uint32_t)k) < old) atomicOr(err, kErrCellOvf);
+}
+
 // Fluctuation walk, one thread per unit: sample_patch's exact probabilities
 // (rasterize.cpp:101-118) then fluctuate_sequential (rasterize.cpp:124-149)
 // with the reference binomial (rng.cpp:146-193) or the Gaussian approximation
-// (rasterize.cpp:159-170); counts scattered with float atomics (exact while
-// a cell holds < 2^24 electrons, so the grid is order independent).
+// (rasterize.cpp:159-170); counts scattered with integer atomics (add_count).
 __global__ void k_fluctuate(const EventDesc ev, const UnitRec* __restrict__ recs, const uint32_t* __restrict__ pool,
                             const uint32_t* __restrict__ order)
 {
@@ -665,7 +686,7 @@ __global__ void k_fluctuate(const EventDesc ev, const UnitRec* __restrict__ recs
     const double norm = 1.0 / total;
     Rng src;
     src.init(ev.rng_mode, ev.seed, (uint64_t)d.id);
-    float* grid = P.charge_out;
+    uint32_t* grid = P.charge_u32;
     const int N = P.N;
     int64_t remaining = d.q;
     double p_rem = 1.0;
@@ -680,12 +701,12 @@ __global__ void k_fluctuate(const EventDesc ev, const UnitRec* __restrict__ recs
             p = p < 0.0 ? 0.0 : (p > 1.0 ? 1.0 : p);
         }
         const int64_t k = ev.approx ? binomial_approx(remaining, p, src) : binomial(remaining, p, src);
-        if (k) atomicAdd(&grid[(size_t)(rec.w0 + w) * N + rec.t0 + t], (float)k);
+        add_count(&grid[(size_t)(rec.w0 + w) * N + rec.t0 + t], k, ev.err);
         remaining -= k;
         p_rem -= pi;
     }
     if (remaining)
-        atomicAdd(&grid[(size_t)(rec.w0 + n_w - 1) * N + rec.t0 + n_t - 1], (float)remaining);
+        add_count(&grid[(size_t)(rec.w0 + n_w - 1) * N + rec.t0 + n_t - 1], remaining, ev.err);
 }
 
 // Exact fluctuation (fluctuate_sequential with the reference binomial), the
@@ -695,7 +716,7 @@ __global__ void k_fluctuate(const EventDesc ev, const UnitRec* __restrict__ recs
 // lanes walk their current draw one step per iteration and only when a
 // quarter of the warp's live lanes have finished their draws does the warp
 // set up the next draws (RNG, pmf seed) together. The integer grid is
-// unchanged (same draws, same order per depo; float atomics exact < 2^24).
+// unchanged (same draws, same order per depo; exact integer atomics).
 // walk-length key of every unit (the walk is ~q steps): warps of similar
 // charge keep their lanes busy together
 __global__ void k_fluct_keys(const EventDesc ev, const UnitRec* __restrict__ recs, uint32_t* __restrict__ keys,
@@ -736,7 +757,7 @@ __global__ void __launch_bounds__(128) k_fluctuate_exact(const EventDesc ev, con
     }
     Rng src;
     src.init(ev.rng_mode, ev.seed, (uint64_t)d.id);
-    float* grid = P.charge_out;
+    uint32_t* grid = P.charge_u32;
     const int N = P.N;
     const int last = rec.n_w * n_t - 1;
     int64_t remaining = d.q;
@@ -749,9 +770,9 @@ __global__ void __launch_bounds__(128) k_fluctuate_exact(const EventDesc ev, con
 
     // bin b = (bw, bt), tracked incrementally (no integer division per draw)
     int bw = 0, bt = 0;
-    float* cellp = grid + (size_t)rec.w0 * N + rec.t0;  // &grid[w0 + bw][t0 + bt]
+    uint32_t* cellp = grid + (size_t)rec.w0 * N + rec.t0;  // &grid[w0 + bw][t0 + bt]
     auto commit = [&](int64_t k) {  // bin b drew k electrons
-        if (k) atomicAdd(cellp, (float)k);
+        add_count(cellp, k, ev.err);
         remaining -= k;
         p_rem -= pi;
         ++b;
@@ -768,7 +789,7 @@ __global__ void __launch_bounds__(128) k_fluctuate_exact(const EventDesc ev, con
         while (!done && !walking) {
             if (remaining == 0 || b >= last) {
                 if (remaining)  // the last bin takes the rest
-                    atomicAdd(&grid[(size_t)(rec.w0 + rec.n_w - 1) * N + rec.t0 + n_t - 1], (float)remaining);
+                    add_count(&grid[(size_t)(rec.w0 + rec.n_w - 1) * N + rec.t0 + n_t - 1], remaining, ev.err);
                 done = true;
                 break;
             }

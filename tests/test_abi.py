@@ -34,7 +34,7 @@ def test_library_exports_every_declared_symbol():
     missing = [n for n in declared_functions() if not hasattr(lib, n)]
     assert not missing, missing
     assert set(_lib.SIGNATURES) <= declared_functions()
-    assert lib.ws_abi_version() == 1
+    assert lib.ws_abi_version() == 2
 
 
 def test_struct_layouts_match_reference():

@@ -131,9 +131,12 @@ def test_microboone_u_plane_full_size(pctx, oracle):
         np.testing.assert_array_equal(p.simulate(d, SimConfig(fluctuate=False)).frame, f)
 
 
-def test_direct_band_beyond_staging(pctx, oracle):
+def test_direct_band_beyond_staging(oracle):
     """A band with more depos than k_direct stages at once (chunked
-    accumulation) still matches the oracle."""
+    accumulation) still matches the oracle. A fresh context: the tile list
+    capacity starts at its default, so the ~12k-entry tiles overflow it and
+    the host re-runs with the recorded size (never a truncated tile)."""
+    pctx = Context(0)
     grid = GridSpec(n_wires=16, n_ticks=900, pad_wires=10, pad_ticks=100, pitch=5.0, tick=0.5)
     # unipolar response: 12k stacked bipolar responses cancel to ~1e-3 of
     # their absolute sum, which any fp32 method resolves only to ~1e-6
