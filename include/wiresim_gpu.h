@@ -199,7 +199,10 @@ int ws_ctx_set_direct_kappa(ws_ctx* ctx, double kappa);
 uint64_t ws_ctx_launch_count(const ws_ctx* ctx);
 
 /* Plane: geometry + response precomputed on the device (response spectrum,
- * FFT plan, twiddles). Validation mirrors build_response and convolve. */
+ * FFT plan, twiddles). Validation mirrors build_response and convolve. A
+ * plane is used with its context only; destroying it never touches the
+ * context (either may be destroyed first), but a plane whose context is gone
+ * can only be destroyed. */
 int ws_plane_create(ws_ctx* ctx, const ws_grid_spec* grid, const ws_response* response, double n_sigma,
                     ws_plane** out);
 int ws_plane_destroy(ws_plane* plane);
@@ -280,6 +283,40 @@ int ws_run_events(ws_ctx* ctx, uint32_t n_events, uint32_t n_planes, ws_plane* c
  * (spectral.cpp:177-196, 228-238). noise may be NULL (digitize only). */
 int ws_noise_digitize_device(ws_plane* plane, float* frame, const ws_noise_model* noise, double scale, double offset,
                              int32_t bits, int32_t* adc);
+
+/* ---- several GPUs of one node (ws_multi.cu) -------------------------------
+ * One context per entry of `devices` (a device may be listed twice: two
+ * streams on it) with the same n_planes plane specs on each, and a host
+ * thread per device. Work units are independent (events, or (anode-face,
+ * plane) runs), so nothing is exchanged between GPUs: each thread runs its
+ * shard through the pipelined host-buffer path and its device-to-host copies
+ * land in the caller's disjoint output buffers (the final frame gather).
+ * Sharding is longest-processing-time first by ws_multi_cost. Results are
+ * bitwise independent of the placement (RNG streams keyed by seed and depo
+ * id). SURVEY.md §8(e); BASELINE.json configs[3] (faces) and configs[4]. */
+typedef struct ws_multi ws_multi;
+int ws_multi_create(uint32_t n_devices, const int* devices, uint32_t n_planes, const ws_grid_spec* grids,
+                    const ws_response* responses, double n_sigma, ws_multi** out);
+int ws_multi_destroy(ws_multi* m);
+uint32_t ws_multi_device_count(const ws_multi* m);
+ws_ctx* ws_multi_context(ws_multi* m, uint32_t device_index);
+ws_plane* ws_multi_plane(ws_multi* m, uint32_t device_index, uint32_t plane);
+int ws_multi_set_conv_path(ws_multi* m, int path);
+/* cost model of one plane run: cells + 150 x depos */
+double ws_multi_cost(uint64_t cells, uint64_t n_depos);
+/* Whole events over the devices: depos / n_depos / adcs / frames are
+ * [n_events * n_planes] (as ws_run_events). readout NULL: fp32 frames (as
+ * ws_simulate_events; adcs ignored). event_device (nullable, n_events) gets
+ * each event's device index. timing (nullable): the first event of device 0. */
+int ws_multi_run_events(ws_multi* m, uint32_t n_events, const ws_depo* const* depos, const uint64_t* n_depos,
+                        const ws_sim_options* opt, const ws_readout* readout, void* const* adcs, void* const* frames,
+                        uint32_t* event_device, ws_timing* timing);
+/* Independent plane runs (e.g. 12 faces x 3 planes): unit u uses plane spec
+ * plane_of[u]; arrays are [n_units]. unit_device (nullable) gets each unit's
+ * device index. */
+int ws_multi_run_units(ws_multi* m, uint32_t n_units, const uint32_t* plane_of, const ws_depo* const* depos,
+                       const uint64_t* n_depos, const ws_sim_options* opt, const ws_readout* readout,
+                       void* const* adcs, void* const* frames, uint32_t* unit_device);
 
 /* Pinned host memory for the host-buffer entry points (cudaMallocHost). */
 int ws_host_alloc(uint64_t bytes, void** out);

@@ -8,6 +8,7 @@ from ._lib import DEPO_DTYPE, WsError  # noqa: F401
 from .api import (  # noqa: F401
     AdcConfig,
     Context,
+    Multi,
     NoiseModel,
     RunResult,
     run_events,

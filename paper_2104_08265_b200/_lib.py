@@ -127,6 +127,17 @@ SIGNATURES = {
                                       C.POINTER(TimingC)]),
     "ws_run_events": (C.c_int, [_P, C.c_uint32, C.c_uint32, _P, _P, _P, C.POINTER(SimOptionsC), C.POINTER(ReadoutC),
                                 _P, _P, C.POINTER(TimingC)]),
+    "ws_multi_create": (C.c_int, [C.c_uint32, _P, C.c_uint32, _P, _P, C.c_double, C.POINTER(_P)]),
+    "ws_multi_destroy": (C.c_int, [_P]),
+    "ws_multi_device_count": (C.c_uint32, [_P]),
+    "ws_multi_context": (_P, [_P, C.c_uint32]),
+    "ws_multi_plane": (_P, [_P, C.c_uint32, C.c_uint32]),
+    "ws_multi_set_conv_path": (C.c_int, [_P, C.c_int]),
+    "ws_multi_cost": (C.c_double, [C.c_uint64, C.c_uint64]),
+    "ws_multi_run_events": (C.c_int, [_P, C.c_uint32, _P, _P, C.POINTER(SimOptionsC), C.POINTER(ReadoutC), _P, _P,
+                                      _P, C.POINTER(TimingC)]),
+    "ws_multi_run_units": (C.c_int, [_P, C.c_uint32, _P, _P, _P, C.POINTER(SimOptionsC), C.POINTER(ReadoutC), _P,
+                                     _P, _P]),
     "ws_gen_depos_uniform":(C.c_int, [C.c_uint64, C.c_uint64, C.POINTER(GridSpecC), _P, _P]),
     "ws_noise_digitize_device": (C.c_int, [_P, _P, C.POINTER(NoiseModelC), C.c_double, C.c_double, C.c_int32, _P]),
     "ws_host_alloc": (C.c_int, [C.c_uint64, C.POINTER(_P)]),

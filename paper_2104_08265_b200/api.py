@@ -15,6 +15,7 @@ fallback. Errors raise ``WsError`` carrying the reference exception category
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 from dataclasses import dataclass, field
 from typing import Sequence
 
@@ -152,6 +153,7 @@ class Context:
         check(self.lib.ws_ctx_create(device, C.c_void_p(stream) if stream else None, C.byref(h)))
         self.handle = h
         self.device = device
+        self._planes = weakref.WeakSet()  # closed before the context (a plane lives on its context)
 
     def synchronize(self):
         check(self.lib.ws_ctx_synchronize(self.handle))
@@ -177,6 +179,8 @@ class Context:
 
     def close(self):
         if self.handle:
+            for p in list(self._planes):
+                p.close()
             self.lib.ws_ctx_destroy(self.handle)
             self.handle = None
 
@@ -198,6 +202,7 @@ class Plane:
         h = C.c_void_p()
         check(self.lib.ws_plane_create(ctx.handle, C.byref(g), C.byref(r), n_sigma, C.byref(h)))
         self.handle = h
+        ctx._planes.add(self)
         info = _lib.PlaneInfoC()
         check(self.lib.ws_plane_get_info(h, C.byref(info)))
         self.info = {k: getattr(info, k) for k, _ in info._fields_}
@@ -378,6 +383,80 @@ def run_events(ctx: Context, planes: Sequence[Plane], events: Sequence[Sequence]
     check(ctx.lib.ws_run_events(ctx.handle, n_ev, n_pl, parr, darr, narr, C.byref(opt), C.byref(r), aarr, farr,
                                 C.byref(t)))
     return adcs, frames, t.as_dict()
+
+
+class Multi:
+    """Several GPUs of one node (ws_multi_*): a context per device (a device
+    may repeat), the same plane specs on each, a host thread per device;
+    independent events or (face, plane) units sharded by LPT, outputs
+    gathered into the caller's host buffers. No data crosses devices."""
+
+    def __init__(self, devices: Sequence[int], specs: Sequence[tuple], n_sigma: float = 3.0):
+        self.lib = _lib.load()
+        self.specs = list(specs)
+        g = (_lib.GridSpecC * len(specs))(*[gs.to_c() for gs, _ in specs])
+        rs = [r.to_c() for _, r in specs]
+        self._ww = [w for _, w in rs]
+        r = (_lib.ResponseC * len(specs))(*[rc for rc, _ in rs])
+        devs = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        check(self.lib.ws_multi_create(len(devices), devs, len(specs), g, r, n_sigma, C.byref(h)))
+        self.handle = h
+        self.n_devices = len(devices)
+        self.shapes = [(gs.padded_wires(), gs.padded_ticks()) for gs, _ in specs]
+
+    def set_conv_path(self, path: str):
+        check(self.lib.ws_multi_set_conv_path(self.handle, Context.CONV_PATHS[path]))
+
+    def run_events(self, events: Sequence[Sequence], config: SimConfig, adc_type: str | None = None):
+        """events[e][p] depo arrays. adc_type None: fp32 frames; else ADC codes
+        ("i32" / "u16"). Returns (outputs[e][p], device index per event)."""
+        n_ev, n_pl = len(events), len(self.specs)
+        ds = [as_depos(d) for ev in events for d in ev]
+        if adc_type is None:
+            outs = [[np.empty(sh, dtype=np.float32) for sh in self.shapes] for _ in range(n_ev)]
+        else:
+            dt = np.uint16 if adc_type == "u16" else np.int32
+            outs = [[np.empty(sh, dtype=dt) for sh in self.shapes] for _ in range(n_ev)]
+        A = C.c_void_p * (n_ev * n_pl)
+        darr = A(*[d.ctypes.data for d in ds])
+        narr = (C.c_uint64 * (n_ev * n_pl))(*[len(d) for d in ds])
+        oarr = A(*[o.ctypes.data for ev in outs for o in ev])
+        where = (C.c_uint32 * n_ev)()
+        opt = config.options()
+        if adc_type is None:
+            check(self.lib.ws_multi_run_events(self.handle, n_ev, darr, narr, C.byref(opt), None, None, oarr, where,
+                                               None))
+        else:
+            r, _keep = config.readout(adc_type)
+            check(self.lib.ws_multi_run_events(self.handle, n_ev, darr, narr, C.byref(opt), C.byref(r), oarr, None,
+                                               where, None))
+        return outs, list(where)
+
+    def run_units(self, plane_of: Sequence[int], depos: Sequence, config: SimConfig):
+        """Independent plane runs (unit u on plane spec plane_of[u]), fp32
+        frames. Returns (frames[u], device index per unit)."""
+        n = len(plane_of)
+        ds = [as_depos(d) for d in depos]
+        outs = [np.empty(self.shapes[p], dtype=np.float32) for p in plane_of]
+        A = C.c_void_p * n
+        where = (C.c_uint32 * n)()
+        opt = config.options()
+        check(self.lib.ws_multi_run_units(self.handle, n, (C.c_uint32 * n)(*plane_of), A(*[d.ctypes.data for d in ds]),
+                                          (C.c_uint64 * n)(*[len(d) for d in ds]), C.byref(opt), None, None,
+                                          A(*[o.ctypes.data for o in outs]), where))
+        return outs, list(where)
+
+    def close(self):
+        if self.handle:
+            self.lib.ws_multi_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def simulate_event_device(ctx: Context, planes: Sequence[Plane], depos_dev: Sequence, n_depos: Sequence[int],

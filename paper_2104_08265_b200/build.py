@@ -34,6 +34,7 @@ SOURCES = {
     "ws_sigproc.cu": [],
     "ws_api.cu": [],
     "ws_host.cu": ["--fmad=false"],
+    "ws_multi.cu": [],
 }
 
 

@@ -182,6 +182,7 @@ struct ws_ctx {
 
 struct ws_plane {
     ws_ctx* ctx = nullptr;
+    int device = 0;  // the context's device (destroy must not touch the context: it may be gone)
     ws_grid_spec grid{};
     double n_sigma = 3.0;
     int W = 0, N = 0, Np = 0, M = 0, folded = 0, h = 0;
@@ -924,6 +925,7 @@ int ws_ctx_destroy(ws_ctx* c)
             if (e) cudaEventDestroy(e);
     if (c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
+    (void)cudaGetLastError();  // nothing of this teardown may surface in a later launch check
     return WS_OK;
 }
 
@@ -963,6 +965,7 @@ int ws_plane_create(ws_ctx* ctx, const ws_grid_spec* grid, const ws_response* re
     WS_CUDA(cudaSetDevice(ctx->device));
     ws_plane* p = new ws_plane();
     p->ctx = ctx;
+    p->device = ctx->device;
     p->grid = *grid;
     p->n_sigma = n_sigma;
     p->W = (int)(grid->n_wires + 2 * grid->pad_wires);
@@ -1123,13 +1126,14 @@ int ws_plane_create(ws_ctx* ctx, const ws_grid_spec* grid, const ws_response* re
 int ws_plane_destroy(ws_plane* p)
 {
     if (!p) return WS_OK;
-    if (p->ctx) cudaSetDevice(p->ctx->device);
+    cudaSetDevice(p->device);
     if (p->d_H) cudaFree(p->d_H);
     if (p->d_kern) cudaFree(p->d_kern);
     if (p->d_tw) cudaFree(p->d_tw);
     if (p->d_rev) cudaFree(p->d_rev);
     if (p->d_ww) cudaFree(p->d_ww);
     delete p;
+    (void)cudaGetLastError();  // nothing of this teardown may surface in a later launch check
     return WS_OK;
 }
 

@@ -11,11 +11,15 @@ from __future__ import annotations
 from typing import Sequence
 
 
-def unit_cost(padded_wires: int, padded_ticks: int, n_depos: int, bins_per_depo: float = 160.0) -> float:
-    """Device-time model of one plane: the row transform is linear in cells,
-    the scatter in depo bins (k_conv dominates; the constant weighs a bin as
-    ~0.15 cells of transform work)."""
-    return float(padded_wires) * padded_ticks + 0.15 * bins_per_depo * n_depos
+DEPO_COST = 150.0  # cells-equivalent of one depo on one plane (ws_multi_cost in csrc/ws_multi.cu)
+
+
+def unit_cost(padded_wires: int, padded_ticks: int, n_depos: int) -> float:
+    """Device-time model of one plane run, the same as the C ABI's
+    ws_multi_cost: the time-domain path (k_direct, the default for sparse
+    planes) writes every cell once and adds each depo's response profile
+    (~12 wire rows x ~160 taps) to its rows, so cost = cells + 150 x depos."""
+    return float(padded_wires) * padded_ticks + DEPO_COST * n_depos
 
 
 def shard_units(costs: Sequence[float], world: int) -> list[list[int]]:

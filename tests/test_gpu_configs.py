@@ -133,3 +133,43 @@ def test_fluct_on_philox_with_shaper_microboone_u(oracle):
     assert relL2_per_channel(res.frame, m_ref) < TOL_FRAME
     plane.close()
     ctx.close()
+
+
+def test_multi_device_abi_events_and_units():
+    """ws_multi_* (one host thread per context; here two contexts on the one
+    GPU of the box): events and (face, plane) units sharded by LPT, outputs
+    gathered into the caller's buffers, bitwise equal to one context."""
+    from paper_2104_08265_b200 import Multi
+    grids, resps, _ = microboone_like_small()
+    specs = list(zip(grids, resps))
+    cfg = SimConfig(fluctuate=False)
+    events = [[line_tracks(500 + 300 * (e % 3), g, seed=40 + 3 * e + i) for i, g in enumerate(grids)]
+              for e in range(7)]
+    m = Multi([0, 0], specs)
+    outs, where = m.run_events(events, cfg)
+    assert sorted(set(where)) == [0, 1]
+    ctx = Context(0)
+    planes = [Plane(ctx, g, r) for g, r in specs]
+    for e, ev in enumerate(events):
+        for i, d in enumerate(ev):
+            np.testing.assert_array_equal(outs[e][i], planes[i].simulate(d, cfg).frame)
+    adcs, _ = m.run_events(events[:3], cfg, adc_type="u16")
+    for e in range(3):
+        for i, d in enumerate(events[e]):
+            np.testing.assert_array_equal(adcs[e][i], planes[i].run(d, cfg, adc_type="u16").adc)
+    plane_of = [u % len(specs) for u in range(9)]
+    depos = [line_tracks(200 + 100 * u, grids[p], seed=90 + u) for u, p in enumerate(plane_of)]
+    frames, udev = m.run_units(plane_of, depos, cfg)
+    assert sorted(set(udev)) == [0, 1]
+    for u, p in enumerate(plane_of):
+        np.testing.assert_array_equal(frames[u], planes[p].simulate(depos[u], cfg).frame)
+    m.close()
+    ctx.close()
+
+
+def microboone_like_small():
+    grids = [GridSpec(n_wires=240, n_ticks=1600, pad_wires=20, pad_ticks=100, pitch=3.0),
+             GridSpec(n_wires=240, n_ticks=1600, pad_wires=20, pad_ticks=100, pitch=3.0),
+             GridSpec(n_wires=300, n_ticks=1600, pad_wires=20, pad_ticks=100, pitch=3.0)]
+    resps = [ResponseParams(plane_kind="induction"), ResponseParams(plane_kind="induction"), ResponseParams()]
+    return grids, resps, None

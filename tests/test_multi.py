@@ -76,3 +76,11 @@ def test_two_rank_union_equals_single(tmp_path):
     merged = np.load(out, allow_pickle=True)
     for i in range(len(_small_units())):
         np.testing.assert_array_equal(merged[i], _unit_result(i))
+
+
+def test_cost_model_matches_c_abi():
+    """The Python sharding cost model is the C ABI's (ws_multi_cost, host-only)."""
+    from paper_2104_08265_b200 import _lib
+    lib = _lib.load()
+    for w, t, n in ((2600, 9800, 100_000), (1000, 6200, 0), (680, 6200, 10_000)):
+        assert lib.ws_multi_cost(w * t, n) == unit_cost(w, t, n)
