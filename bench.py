@@ -9,16 +9,23 @@ straight 3D tracks projected onto U/V (induction, 2400 wires) and W
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
   python bench.py --workload sigproc ...   (the paper's Listing 1 chain, §8(f))
+  python bench.py --workload c4 ...        (configs[3]: ProtoDUNE-SP 6-APA event, 36 (face, plane) units)
+  python bench.py --workload c5 ...        (configs[4]: 64-event batches, 1k-1M depos/event sweep)
 
-N > 1 runs under torchrun, one rank per GPU, weak scaling: every rank
-simulates its own events (independent event shards, no data-path collective);
-value = all ranks' depositions / max-over-ranks device time.
+N > 1 runs one rank per GPU (torchrun; `--gpus N` without torchrun's
+environment re-launches itself under torch.distributed.run). event: weak
+scaling, every rank simulates its own events; c4 / c5: strong scaling, the
+36 units / 64 events of a step are sharded over the ranks (LPT / round
+robin). No data-path collective; value = all ranks' depositions / max-over-
+ranks device time.
 
 Timing: CUDA events on the library's stream around exactly K steps, barrier +
 synchronize on both sides, max over ranks. Inputs rotate over 10 distinct
-pre-generated events (144 MB of depos > 126 MB L2). `e2e` repeats the
-measurement through the host-buffer API (ws_simulate_event): pinned depos
-H2D and the three frames D2H inside the timed region.
+pre-generated events (144 MB of depos > 126 MB L2; every step also writes
+347 MB of frames). `e2e` measures the same workload through the
+reference-facing host-buffer call, ws_run_events (run_simulation's output:
+SimResult::adc, digitized codes in uint16): pinned depos H2D and the ADC
+frames D2H inside the timed region, pipelined.
 
 --impl reference times the reference's own CPU implementation (the
 unmodified library compiled into oracle/_ref) on the host cores, one plane of
@@ -124,6 +131,19 @@ def dist_setup():
     return world, rank, local
 
 
+def relaunch_distributed(n: int) -> int:
+    """`--gpus N` without a torchrun environment: run this script under
+    torch.distributed.run with N ranks (one per GPU) and pass its output through."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def make_events(rank: int):
     from paper_2104_08265_b200.workloads import microboone_event
     return [microboone_event(N_DEPOS, seed=1000 * rank + e + 1) for e in range(N_EVENTS_ROTATE)]
@@ -152,6 +172,26 @@ def cpu_reference_plane_times(events, planes_idx, workers):
     return out
 
 
+def cpu_baseline_event(events, cores):
+    """The GPU arm's cpu_baseline: the unmodified reference on ALL three planes
+    of one event at `cores` threads (stage breakdown per plane), plus the U
+    plane at one worker; build_response excluded (cached, reported)."""
+    t_all = cpu_reference_plane_times(events, [0, 1, 2], cores)
+    t_one = cpu_reference_plane_times(events, [0], 1)[0]
+    stages = {k: sum(x[k] for x in t_all) for k in ("sample_s", "scatter_s", "convolve_s")}
+    ev_s = sum(stages.values())
+    return {"value": N_DEPOS / ev_s, "unit": "depos/s", "cores": cores, "kind": "reference",
+            "sample": f"all three planes (U, V, W) of one 100k-depo event through the unmodified reference at "
+                      f"{cores} threads, build_response excluded (cached); stage seconds summed over planes",
+            "event_s": ev_s, "stages_s": stages,
+            "per_plane_s": [round(x["sample_s"] + x["scatter_s"] + x["convolve_s"], 4) for x in t_all],
+            "build_response_s": [round(x["build_response_s"], 2) for x in t_all],
+            "workers_1": {"plane": "U", "plane_s": t_one["sample_s"] + t_one["scatter_s"] + t_one["convolve_s"],
+                          "stages_s": {k: t_one[k] for k in ("sample_s", "scatter_s", "convolve_s")},
+                          "depos_per_s_event_equiv": N_DEPOS / (3 * (t_one["sample_s"] + t_one["scatter_s"] +
+                                                                      t_one["convolve_s"]))}}
+
+
 def run_reference_arm(args, world, rank):
     if rank != 0:
         return
@@ -176,6 +216,13 @@ def run_reference_arm(args, world, rank):
         "e2e": {"value": value, "unit": "depos/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def profile_facts(kernel: str):
+    """Per-launch counters of `kernel` from the committed ncu captures
+    (profiles/traffic_<kernel>.json): DRAM bytes, warp instructions, pipes."""
+    prof = ROOT / "profiles" / f"traffic_{kernel}.json"
+    return json.loads(prof.read_text()) if prof.exists() else {}
 
 
 SP_ROWS, SP_COLS, SP_PAD, SP_OUT = 960, 6000, 80, 800
@@ -305,32 +352,86 @@ def run_sigproc(args, world, rank, local):
         dist.destroy_process_group()
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="event", choices=["event", "sigproc"],
-                    help="event: the headline simulation metric; sigproc: the Listing 1 chain (§8(f))")
-    args = ap.parse_args()
-    args.warmup = max(args.warmup, 3)
-    world, rank, local = dist_setup()
-    if args.workload == "sigproc":
-        run_sigproc(args, world, rank, local)
-        return
+def cpu_reference_units(units, workers):
+    """The unmodified reference's fluctuation-off path on (grid, response,
+    depos) units, one plane run each (response built once per geometry,
+    excluded): seconds per unit (sample + scatter + convolve)."""
+    from oracle.oracle import Reference, build_ref, make_grid, make_response, ref_available
+    if not ref_available():
+        build_ref()
+    ref = Reference()
+    cache, out = {}, []
+    for g, r, d in units:
+        key = (g.n_wires, g.n_ticks, g.pad_wires, g.pad_ticks, g.pitch, r.plane_kind, tuple(r.wire_weights))
+        if key not in cache:
+            og = make_grid(g.n_wires, g.n_ticks, g.pad_wires, g.pad_ticks, g.pitch, g.tick)
+            orr = make_response(r.plane_kind, r.field_sigma_t, r.shaper_peaking, r.shaper_order, r.gain,
+                                tuple(r.wire_weights))
+            cache[key] = ref.plane(og, orr)
+        t = cache[key].time_fluct_off(d, workers=workers)
+        out.append(t["sample_s"] + t["scatter_s"] + t["convolve_s"])
+    return out
 
-    if args.impl == "reference":
-        run_reference_arm(args, world, rank)
-        return
 
+C4_DEPOS = 20_000      # per (face, plane) unit
+C4_ROTATE = 4          # distinct events (4 x 36 units x 20k x 48 B = 138 MB of depos > L2)
+C5_EVENTS = 64
+C5_ROTATE = 8          # distinct events per size (rotating over the 64 of a step)
+C5_SIZES = (1_000, 10_000, 100_000, 1_000_000)
+
+
+def workload_desc(args):
+    if args.workload == "c4":
+        return (f"protodune_event (configs[3]): 12 faces x U/V/W (800/800/480 wires) x 6000 ticks, pad 100/100, "
+                f"pitch 5 mm, {C4_DEPOS} depos per (face, plane) unit (720k per event), fluct off; 36 units "
+                f"LPT-sharded over the ranks")
+    if args.workload == "c5":
+        return (f"batched events (configs[4]): {C5_EVENTS} MicroBooNE-geometry events of {args.depos} depos per "
+                f"step, round-robin over the ranks, fluct off")
+    return WORKLOAD
+
+
+def reference_sample(args, cores):
+    """CPU reference (oracle/_ref) on a bounded sample of the c4 / c5 step, scaled
+    to the step by unit counts; returns (depos/s, description)."""
+    from paper_2104_08265_b200.workloads import microboone_event, microboone_grids, protodune_event, protodune_specs
+    if args.workload == "c4":
+        specs = protodune_specs()
+        plane_of, depos = protodune_event(C4_DEPOS, seed=1)
+        t = cpu_reference_units([(specs[0][0], specs[0][1], depos[0]), (specs[2][0], specs[2][1], depos[2])], cores)
+        step_s = 24 * t[0] + 12 * t[1]  # 12 U + 12 V (same geometry as U) + 12 W units
+        return 36 * C4_DEPOS / step_s, (f"face 0's U and W units timed at {cores} threads ({t[0]:.2f} s, {t[1]:.2f} s), "
+                                        f"scaled by unit count to the 36-unit event; build_response excluded")
+    grids, resps = microboone_grids()
+    ev = microboone_event(args.depos, seed=1)
+    t = cpu_reference_units([(grids[i], resps[i], ev[i]) for i in range(3)], cores)
+    return args.depos / sum(t), (f"one {args.depos}-depo event (3 planes) timed at {cores} threads "
+                                 f"({sum(t):.2f} s); depos/s of the 64-event step equals the per-event rate")
+
+
+def run_sim(args, world, rank, local):
+    """The simulation workloads (event / c4 / c5) on this rank's GPU."""
     import torch
     import torch.distributed as dist
-    from paper_2104_08265_b200 import Context, Plane, SimConfig, simulate_event_device, simulate_events
+    from paper_2104_08265_b200 import AdcConfig, Context, Plane, SimConfig, run_events, simulate_event_device
     from paper_2104_08265_b200._lib import TimingC
-    from paper_2104_08265_b200.workloads import microboone_grids
+    from paper_2104_08265_b200.sharding import shard_units, unit_cost
+    from paper_2104_08265_b200.workloads import microboone_event, microboone_grids, protodune_event, protodune_specs
+
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    if args.impl == "reference":
+        if rank == 0:
+            value, sample = reference_sample(args, cores)
+            print(json.dumps({
+                "impl": "reference", "metric": "depositions_per_sec", "value": value, "unit": "depos/s",
+                "n_gpus": args.gpus, "steps": 1, "warmup": 0, "ms_per_step": None, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic line tracks",
+                "config": {"workload": workload_desc(args), "workers": cores},
+                "cpu_baseline": {"value": value, "unit": "depos/s", "cores": cores, "kind": "reference",
+                                 "sample": sample},
+                "e2e": {"value": value, "unit": "depos/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+                flush=True)
+        return
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -349,27 +450,60 @@ def main():
 
     ctx = Context(local)
     stream = torch.cuda.ExternalStream(ctx.stream)
-    grids, resps = microboone_grids()
-    planes = [Plane(ctx, g, r) for g, r in zip(grids, resps)]
-    cfg = SimConfig(fluctuate=False)
-    events = make_events(rank)
-    dev_events = [[torch.from_numpy(d.view(np.uint8)).cuda() for d in ev] for ev in events]
-    n_dep = [[len(d) for d in ev] for ev in events]
-    frames = [torch.empty(p.shape, dtype=torch.float32, device="cuda") for p in planes]
-    cells = sum(p.shape[0] * p.shape[1] for p in planes)
+    cfg = SimConfig(fluctuate=False, adc=AdcConfig(1.0, 2048.0, 12))
+    # calls[r] = list of (planes, [host depo arrays]) for rotation slot r; one
+    # step runs every call of one slot
+    if args.workload == "event":
+        grids, resps = microboone_grids()
+        planes = [Plane(ctx, g, r) for g, r in zip(grids, resps)]
+        calls = [[(planes, ev)] for ev in make_events(rank)]
+        scaling = "weak"
+        step_depos_all = world * N_DEPOS
+        parallel = f"event-sharded x{world}"
+    elif args.workload == "c5":
+        grids, resps = microboone_grids()
+        planes = [Plane(ctx, g, r) for g, r in zip(grids, resps)]
+        distinct = [microboone_event(args.depos, seed=50 + e) for e in range(C5_ROTATE)]
+        mine = list(range(rank, C5_EVENTS, world))
+        calls = [[(planes, distinct[(e + k) % C5_ROTATE]) for e in mine] for k in range(2)]
+        scaling = "strong"
+        step_depos_all = C5_EVENTS * args.depos
+        parallel = f"{C5_EVENTS} events round-robin over {world} rank(s)"
+    else:
+        specs = protodune_specs()
+        plane_of, _ = protodune_event(1, seed=1)
+        costs = [unit_cost(specs[p][0].padded_wires(), specs[p][0].padded_ticks(), C4_DEPOS) for p in plane_of]
+        mine = shard_units(costs, world)[rank]
+        planes = [Plane(ctx, *specs[plane_of[u]]) for u in mine]
+        calls = []
+        for k in range(C4_ROTATE):
+            _, depos = protodune_event(C4_DEPOS, seed=1 + k)
+            calls.append([(planes, [depos[u] for u in mine])])
+        scaling = "strong"
+        step_depos_all = 36 * C4_DEPOS
+        parallel = f"36 (face, plane) units LPT-sharded over {world} rank(s)"
+    n_rot = len(calls)
+    dev = [[([torch.from_numpy(d.view(np.uint8)).cuda() for d in ds], [len(d) for d in ds]) for _, ds in slot]
+           for slot in calls]
+    frames = {}
+    for slot in calls:
+        for pl, _ in slot:
+            for p in pl:
+                if id(p) not in frames:
+                    frames[id(p)] = torch.empty(p.shape, dtype=torch.float32, device="cuda")
+    step_cells = sum(p.shape[0] * p.shape[1] for pl, _ in calls[0] for p in pl)
     torch.cuda.synchronize()
 
     def step(i, timing=None):
-        e = i % N_EVENTS_ROTATE
-        simulate_event_device(ctx, planes, dev_events[e], n_dep[e], cfg, frames, timing=timing)
+        for j, (pl, _) in enumerate(calls[i % n_rot]):
+            dd, nd = dev[i % n_rot][j]
+            simulate_event_device(ctx, pl, dd, nd, cfg, [frames[id(p)] for p in pl],
+                                  timing=timing if j == 0 else None)
 
-    # warmup (also sizes the workspace)
-    for i in range(args.warmup):
+    for i in range(args.warmup):  # also sizes the workspace
         step(i)
     ctx.synchronize()
-
-    # per-stage device times (one instrumented pass, outside the timed region)
-    stage = TimingC()
+    stage = TimingC()  # per-stage device times of one call (outside the timed region)
     step(0, timing=stage)
     ctx.synchronize()
 
@@ -386,92 +520,148 @@ def main():
         torch.cuda.synchronize()
     barrier()
     gpu_launches = ctx.launch_count - launches0
-    ms = start.elapsed_time(end)
-    ms = max_over_ranks(ms)
+    ms = max_over_ranks(start.elapsed_time(end))
     ms_per_step = ms / args.steps
-    value = world * N_DEPOS * args.steps / (ms * 1e-3)
+    value = step_depos_all * args.steps / (ms * 1e-3)
+    clk = clocks.summary()
 
-    # dominant kernel roofline: the convolution stage (k_direct on
-    # time-domain planes, k_conv on row-FFT planes), timed live by the stage
-    # events around it. Algorithmic traffic = SURVEY.md §8(d) K3's floor,
-    # 8 B/cell (read S + write M), x the event's cells.
+    # dominant kernel roofline: the convolution stage of one call (k_direct on
+    # time-domain planes, k_conv on row-FFT planes), timed by stage events on
+    # the library's stream. Algorithmic traffic = SURVEY.md §8(d) K3's floor,
+    # 8 B/cell (read S + write M), x the call's cells.
+    call_planes = calls[0][0][0][:8]
+    call_cells = sum(p.shape[0] * p.shape[1] for p in call_planes)
     conv_ms = max_over_ranks(float(stage.convolve_ms))
     n_direct = int(stage.direct_planes)
-    conv_kernel = "k_direct" if n_direct == len(planes) else ("k_conv" if n_direct == 0 else "k_direct+k_conv")
-    alg_bytes = 8.0 * cells
+    conv_kernel = "k_direct" if n_direct == len(call_planes) else ("k_conv" if n_direct == 0 else "k_direct+k_conv")
+    alg_bytes = 8.0 * call_cells
     peak, peak_kind = peaks()
     achieved = alg_bytes / (conv_ms * 1e-3) / 1e9
-    prof = ROOT / "profiles" / f"traffic_{conv_kernel.split('+')[0]}.json"
-    traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch") if prof.exists() else None
+    facts = profile_facts(conv_kernel.split("+")[0])
+    binding = None
+    if facts.get("warp_inst_per_launch") and args.workload == "event":
+        # k_direct is bound by instruction issue (shared-memory REDs and their
+        # address / rounding arithmetic), not by HBM: its issue roofline
+        sm_hz = 1e6 * float(clk.get("sm_mhz") or 1965.0)
+        issue_peak = 148 * 4 * sm_hz  # warp instructions / s (4 schedulers per SM, 1 issue / clk)
+        issue_ach = facts["warp_inst_per_launch"] / (conv_ms * 1e-3)
+        binding = {"resource": "instruction issue (warp instr/s)", "achieved": issue_ach, "peak": issue_peak,
+                   "frac": issue_ach / issue_peak, "warp_inst_per_launch": facts["warp_inst_per_launch"],
+                   "source": facts.get("source")}
 
-    # end-to-end through the host-buffer API (pinned host depos in, frames out)
-    e2e = None
+    # end to end through the reference-facing call: ws_run_events (SimResult::adc
+    # as uint16 codes) with pinned host depos in and ADC frames out, pipelined
+    e2e = e2e_f32 = None
     if not args.no_e2e:
-        host_dep = [[d for d in ev] for ev in events[:2]]
-        pinned_frames = [torch.empty(p.shape, dtype=torch.float32).pin_memory() for p in planes]
-        fr_np = [f.numpy() for f in pinned_frames]
-        pinned_dep = []
-        for ev in host_dep:
-            row = []
-            for d in ev:
-                t = torch.empty(d.nbytes, dtype=torch.uint8).pin_memory()
-                t.numpy()[:] = d.view(np.uint8)
-                row.append(t.numpy().view(d.dtype))
-            pinned_dep.append(row)
-        fr_np2 = [torch.empty(p.shape, dtype=torch.float32).pin_memory().numpy() for p in planes]
-        k_e2e = max(3, min(args.steps, 20))
-        batch = [pinned_dep[i % 2] for i in range(k_e2e)]
-        outs = [fr_np if i % 2 == 0 else fr_np2 for i in range(k_e2e)]
-        simulate_events(ctx, planes, batch[:2], cfg, frames=outs[:2])  # warm-up
+        slot_planes = calls[0][0][0]
+        host_events = []
+        for k in range(min(2, n_rot)):
+            for _, ds in calls[k]:
+                row = []
+                for d in ds:
+                    t = torch.empty(d.nbytes, dtype=torch.uint8).pin_memory()
+                    t.numpy()[:] = d.view(np.uint8)
+                    row.append(t.numpy().view(d.dtype))
+                host_events.append(row)
+        per_step = len(calls[0])
+        k_e2e = max(3, min(args.steps, 20)) if args.workload == "event" else max(1, min(args.steps, 3))
+        batch = [host_events[i % len(host_events)] for i in range(k_e2e * per_step)]
+        adc_bufs = [[torch.empty(p.shape, dtype=torch.uint16).pin_memory().numpy() for p in slot_planes]
+                    for _ in range(2)]
+        adcs = [adc_bufs[i % 2] for i in range(len(batch))]
+        run_events(ctx, slot_planes, batch[:2], cfg, adc_type="u16", adcs=adcs[:2])  # warm-up
         barrier()
         t0 = time.perf_counter()
-        simulate_events(ctx, planes, batch, cfg, frames=outs)  # pipelined H2D / compute / D2H
+        run_events(ctx, slot_planes, batch, cfg, adc_type="u16", adcs=adcs)
         t1 = time.perf_counter()
         barrier()
         e2e_s = max_over_ranks(t1 - t0)
-        e2e = {"value": world * N_DEPOS * k_e2e / e2e_s, "unit": "depos/s",
-               "h2d_bytes_per_step": int(sum(d.nbytes for d in host_dep[0])),
-               "d2h_bytes_per_step": int(sum(f.numel() * 4 for f in pinned_frames)),
-               "steps": k_e2e, "ms_per_step": 1e3 * e2e_s / k_e2e}
+        h2d = int(sum(d.nbytes for d in host_events[0]))
+        d2h = int(sum(p.shape[0] * p.shape[1] * 2 for p in slot_planes))
+        e2e = {"value": step_depos_all * k_e2e / e2e_s, "unit": "depos/s",
+               "h2d_bytes_per_step": h2d * per_step, "d2h_bytes_per_step": d2h * per_step,
+               "steps": k_e2e, "ms_per_step": 1e3 * e2e_s / k_e2e,
+               "call": "ws_run_events (run_simulation's SimResult::adc, uint16 codes, digitize fused; pinned host "
+                       "buffers, pipelined H2D / compute / D2H)"}
+        if args.workload == "event":
+            from paper_2104_08265_b200 import simulate_events
+            fr_bufs = [[torch.empty(p.shape, dtype=torch.float32).pin_memory().numpy() for p in slot_planes]
+                       for _ in range(2)]
+            outs = [fr_bufs[i % 2] for i in range(len(batch))]
+            simulate_events(ctx, slot_planes, batch[:2], cfg, frames=outs[:2])
+            barrier()
+            t0 = time.perf_counter()
+            simulate_events(ctx, slot_planes, batch, cfg, frames=outs)
+            t1 = time.perf_counter()
+            barrier()
+            s2 = max_over_ranks(t1 - t0)
+            e2e_f32 = {"value": step_depos_all * k_e2e / s2, "unit": "depos/s", "h2d_bytes_per_step": h2d,
+                       "d2h_bytes_per_step": int(sum(p.shape[0] * p.shape[1] * 4 for p in slot_planes)),
+                       "steps": k_e2e, "ms_per_step": 1e3 * s2 / k_e2e,
+                       "call": "ws_simulate_events (fp32 pre-noise frames M)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cores = len(os.sched_getaffinity(0))
-        t = cpu_reference_plane_times(events, [0], cores)[0]
-        from paper_2104_08265_b200.workloads import microboone_grids as mg
-        g0 = mg()[0][0]
-        u_cells = g0.padded_wires() * g0.padded_ticks()
-        plane_s = t["sample_s"] + t["scatter_s"] + t["convolve_s"]
-        ev_s = plane_s * cells / u_cells
-        cpu = {"value": N_DEPOS / ev_s, "unit": "depos/s", "cores": cores, "kind": "reference",
-               "sample": f"U plane of one event (100k depos, {g0.padded_wires()}x{g0.padded_ticks()}) through the "
-                         f"unmodified reference at {cores} threads, build_response excluded "
-                         f"({t['build_response_s']:.1f} s); scaled to the event by cell count "
-                         f"(W plane's Bluestein cost not included, i.e. flattering the CPU)",
-               "plane_s": plane_s}
+        if args.workload == "event":
+            cpu = cpu_baseline_event([calls[0][0][1]], cores)
+        else:
+            v, sample = reference_sample(args, cores)
+            cpu = {"value": v, "unit": "depos/s", "cores": cores, "kind": "reference", "sample": sample}
 
     if rank == 0:
         line = {
             "metric": "depositions_per_sec", "value": value, "unit": "depos/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic (straight 3D line tracks, fixed seeds)",
-            "config": {"workload": WORKLOAD, "events_per_sec": world * 1e3 / ms_per_step, "depos_per_event": N_DEPOS,
-                       "cells_per_event": cells, "l2": "inputs rotate over 10 distinct events (144 MB > 126 MB L2)",
-                       "parallelism": f"event-sharded x{world}",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": scaling,
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (straight line tracks, fixed seeds)",
+            "config": {"workload": workload_desc(args), "events_per_sec": None if args.workload == "c4" else
+                       (world if args.workload == "event" else C5_EVENTS) * 1e3 / ms_per_step,
+                       "depos_per_step": step_depos_all, "cells_per_call": call_cells,
+                       "l2": "inputs rotate over distinct events (> 126 MB L2); every step writes the frames",
+                       "parallelism": parallel,
                        "stage_ms": {k: round(getattr(stage, k), 4) for k in
                                     ("prepare_ms", "bin_ms", "convolve_ms", "total_ms")},
-                       "conv_path": f"{n_direct}/{len(planes)} planes time-domain (k_direct), rest row-FFT (k_conv)"},
+                       "conv_path": f"{n_direct}/{len(call_planes)} planes of a call time-domain (k_direct), "
+                                    f"rest row-FFT (k_conv)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": conv_kernel,
-                         "kernel_ms": conv_ms, "algorithmic_bytes": alg_bytes, "peak_kind": peak_kind},
-            "clocks": clocks.summary(),
+                         "frac": achieved / peak, "traffic": facts.get("dram_bytes_per_launch"),
+                         "kernel": conv_kernel, "kernel_ms": conv_ms, "algorithmic_bytes": alg_bytes,
+                         "peak_kind": peak_kind, "binding": binding,
+                         "raster_pipes": profile_facts("k_sample_off").get("pipes")},
+            "clocks": clk,
             "gpu_launches": gpu_launches,
             "e2e": e2e,
+            "e2e_frames_f32": e2e_f32,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--workload", default="event", choices=["event", "sigproc", "c4", "c5"],
+                    help="event: the headline metric (configs[1]); c4: configs[3]; c5: configs[4]; "
+                         "sigproc: the Listing 1 chain (§8(f))")
+    ap.add_argument("--depos", type=int, default=100_000, help="c5: depositions per event (1k-1M sweep)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_distributed(args.gpus))
+    world, rank, local = dist_setup()
+    if args.workload == "sigproc":
+        run_sigproc(args, world, rank, local)
+        return
+    if args.impl == "reference" and args.workload == "event":
+        run_reference_arm(args, world, rank)
+        return
+    run_sim(args, world, rank, local)
 
 
 if __name__ == "__main__":

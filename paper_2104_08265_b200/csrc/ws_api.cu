@@ -77,7 +77,7 @@ int set_err(int code, const char* fmt, ...)
 
 constexpr double kTwoPi = 6.283185307179586476925286766559;
 constexpr double kInvSqrt2 = 0.70710678118654752440084436210485;
-constexpr int kStatSlots = 64;
+constexpr int kStatSlots = 256;  // per-call headers in flight before a drain (a 64-event batch fits)
 
 template <typename T>
 struct DevBuf {

@@ -98,3 +98,33 @@ def microboone_event(n: int = 100_000, seed: int = 1, n_tracks: int | None = Non
         d["x"] = np.clip(coord, 0.0, wires * MICROBOONE_PITCH - 1e-6)
         out.append(d)
     return out
+
+
+PROTODUNE_WIRES = (800, 800, 480)   # U, V, W channels per anode face (ProtoDUNE-SP, domain numbers)
+PROTODUNE_KINDS = ("induction", "induction", "collection")
+PROTODUNE_FACES = 12                # 6 APAs x 2 faces
+
+
+def protodune_specs():
+    """(GridSpec, ResponseParams) of the three plane kinds of one anode face
+    (BASELINE.json configs[3]): 800/800/480 wires x 6000 ticks, pad 100/100,
+    pitch 5 mm; induction planes with +-1 wire coupling."""
+    specs = []
+    for wires, kind in zip(PROTODUNE_WIRES, PROTODUNE_KINDS):
+        g = GridSpec(n_wires=wires, n_ticks=6000, pad_wires=100, pad_ticks=100, pitch=5.0, tick=0.5)
+        r = ResponseParams(plane_kind=kind, wire_weights=(0.1, 1.0, 0.1) if kind == "induction" else (1.0,))
+        specs.append((g, r))
+    return specs
+
+
+def protodune_event(n_per_unit: int = 20_000, seed: int = 1):
+    """A 6-APA event as 36 independent (face, plane) units: returns
+    (plane_of[36], depos[36]); unit u = face u // 3, plane kind u % 3; each
+    unit's depos lie on line tracks across its face (n_per_unit each)."""
+    specs = protodune_specs()
+    plane_of, depos = [], []
+    for f in range(PROTODUNE_FACES):
+        for p in range(3):
+            plane_of.append(p)
+            depos.append(line_tracks(n_per_unit, specs[p][0], seed=1000 * seed + 3 * f + p))
+    return plane_of, depos

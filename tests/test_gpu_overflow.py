@@ -57,7 +57,7 @@ def test_shower_plane_fresh_context(reference, path):
     ctx.close()
 
 
-def test_shower_event_and_events_fresh_context(reference):
+def test_shower_event_fresh_context(reference):
     d, m_ref = reference
     ctx = Context(0)
     ctx.set_conv_path("direct")
@@ -65,21 +65,36 @@ def test_shower_event_and_events_fresh_context(reference):
     light = line_tracks(500, GRID, seed=9)
     frames, _ = simulate_event(ctx, planes, [light, d], CFG)
     assert relL2_per_channel(frames[1], m_ref) < 1e-5
-    ctx2 = Context(0)
-    ctx2.set_conv_path("direct")
-    planes2 = [Plane(ctx2, GRID, RESP)]
-    # 70 events (more than the 64-slot header ring: a mid-batch drain), the
-    # shower in the middle and at the end
-    events = [[line_tracks(300, GRID, seed=100 + e)] for e in range(70)]
-    events[33] = [d]
-    events[69] = [d]
-    out, _ = simulate_events(ctx2, planes2, events, CFG)
-    assert relL2_per_channel(out[33][0], m_ref) < 1e-5
-    assert relL2_per_channel(out[69][0], m_ref) < 1e-5
-    for e in (0, 32, 34, 68):
-        np.testing.assert_array_equal(out[e][0], planes2[0].simulate(events[e][0], CFG).frame)
+    np.testing.assert_array_equal(frames[0], planes[0].simulate(light, CFG).frame)
     ctx.close()
-    ctx2.close()
+
+
+SMALL = GridSpec(n_wires=64, n_ticks=1200, pad_wires=10, pad_ticks=100, pitch=5.0, tick=0.5)
+
+
+def test_shower_in_long_batch_fresh_context(oracle):
+    """ws_simulate_events over 300 events (more than the 256-slot header ring:
+    a mid-batch drain), showers in the middle, just before the drain and at
+    the end: each overflowing event is re-run, every frame is right."""
+    rng = np.random.default_rng(3)
+    sh = line_tracks(24_000, SMALL, seed=8)
+    sh["x"] = 150.0 + rng.uniform(0.0, 8.0, size=len(sh))
+    sh["t"] = 200.0 + rng.uniform(0.0, 100.0, size=len(sh))
+    s_ref, _ = oracle.charge_fluct_off(oracle_grid(SMALL), sh)
+    m_ref = oracle.convolve(oracle_grid(SMALL), oracle_response(RESP), s_ref)
+    ctx = Context(0)
+    ctx.set_conv_path("direct")
+    plane = Plane(ctx, SMALL, RESP)
+    cfg = SimConfig(grid=SMALL, response=RESP, fluctuate=False)
+    events = [[line_tracks(100, SMALL, seed=100 + e)] for e in range(300)]
+    for e in (33, 255, 299):
+        events[e] = [sh]
+    out, _ = simulate_events(ctx, [plane], events, cfg)
+    for e in (33, 255, 299):
+        assert relL2_per_channel(out[e][0], m_ref) < 1e-5, e
+    for e in (0, 32, 34, 254, 256, 298):
+        np.testing.assert_array_equal(out[e][0], plane.simulate(events[e][0], cfg).frame)
+    ctx.close()
 
 
 def test_device_path_reports_overflow_then_fits(reference):
