@@ -381,6 +381,10 @@ C5_SIZES = (1_000, 10_000, 100_000, 1_000_000)
 
 
 def workload_desc(args):
+    if args.workload == "c3":
+        return ("microboone_event with fluctuation (configs[2]): 100k depos, U/V/W 2400/2400/3456 wires x 9600 "
+                "ticks, exact binomial walk on the shared Philox stream (seed 12345), field + electronics response "
+                "(shaper 2 us, order 2, gain 14)")
     if args.workload == "c4":
         return (f"protodune_event (configs[3]): 12 faces x U/V/W (800/800/480 wires) x 6000 ticks, pad 100/100, "
                 f"pitch 5 mm, {C4_DEPOS} depos per (face, plane) unit (720k per event), fluct off; 36 units "
@@ -391,10 +395,41 @@ def workload_desc(args):
     return WORKLOAD
 
 
+def c3_reference(cores):
+    """configs[2] on the CPU: the unmodified reference's run_simulation (it
+    always fluctuates; substream mode, the reference's own stream) on the three
+    planes of the event at `cores` threads; the time of build_response (rebuilt
+    inside every run_simulation call, pipeline.cpp:417) is measured apart and
+    subtracted, so the CPU is credited with a cached response."""
+    from oracle.oracle import Reference, build_ref, make_grid, make_response, ref_available
+    from paper_2104_08265_b200.workloads import microboone_event, microboone_grids
+    if not ref_available():
+        build_ref()
+    ref = Reference()
+    grids, resps = microboone_grids()
+    ev = microboone_event(N_DEPOS, seed=1)
+    total, parts = 0.0, []
+    for g, r, d in zip(grids, resps, ev):
+        og = make_grid(g.n_wires, g.n_ticks, g.pad_wires, g.pad_ticks, g.pitch, g.tick)
+        orr = make_response(r.plane_kind, r.field_sigma_t, r.shaper_peaking, r.shaper_order, r.gain)
+        t0 = time.perf_counter()
+        ref.build_response(og, orr, values=True)
+        build_s = time.perf_counter() - t0
+        t = ref.run_simulation(og, orr, d, rng_mode=2, seed=12345, workers=cores)["timing"]
+        plane_s = float(t[0]) + float(t[3]) + max(0.0, float(t[4]) - build_s)  # raster + scatter + (ft - build)
+        parts.append(round(plane_s, 3))
+        total += plane_s
+    return N_DEPOS / total, (f"the three planes of one 100k-depo event through the unmodified reference's "
+                             f"run_simulation (substream fluctuation) at {cores} threads, build_response time "
+                             f"subtracted; per-plane s {parts}")
+
+
 def reference_sample(args, cores):
     """CPU reference (oracle/_ref) on a bounded sample of the c4 / c5 step, scaled
     to the step by unit counts; returns (depos/s, description)."""
     from paper_2104_08265_b200.workloads import microboone_event, microboone_grids, protodune_event, protodune_specs
+    if args.workload == "c3":
+        return c3_reference(cores)
     if args.workload == "c4":
         specs = protodune_specs()
         plane_of, depos = protodune_event(C4_DEPOS, seed=1)
@@ -450,10 +485,12 @@ def run_sim(args, world, rank, local):
 
     ctx = Context(local)
     stream = torch.cuda.ExternalStream(ctx.stream)
-    cfg = SimConfig(fluctuate=False, adc=AdcConfig(1.0, 2048.0, 12))
+    from paper_2104_08265_b200 import RngConfig
+    cfg = SimConfig(fluctuate=args.workload == "c3", rng=RngConfig(mode="philox", seed=12345),
+                    adc=AdcConfig(1.0, 2048.0, 12))
     # calls[r] = list of (planes, [host depo arrays]) for rotation slot r; one
     # step runs every call of one slot
-    if args.workload == "event":
+    if args.workload in ("event", "c3"):
         grids, resps = microboone_grids()
         planes = [Plane(ctx, g, r) for g, r in zip(grids, resps)]
         calls = [[(planes, ev)] for ev in make_events(rank)]
@@ -539,7 +576,7 @@ def run_sim(args, world, rank, local):
     achieved = alg_bytes / (conv_ms * 1e-3) / 1e9
     facts = profile_facts(conv_kernel.split("+")[0])
     binding = None
-    if facts.get("warp_inst_per_launch") and args.workload == "event":
+    if facts.get("warp_inst_per_launch") and args.workload in ("event", "c4", "c5"):
         # k_direct is bound by instruction issue (shared-memory REDs and their
         # address / rounding arithmetic), not by HBM: its issue roofline
         sm_hz = 1e6 * float(clk.get("sm_mhz") or 1965.0)
@@ -564,7 +601,7 @@ def run_sim(args, world, rank, local):
                     row.append(t.numpy().view(d.dtype))
                 host_events.append(row)
         per_step = len(calls[0])
-        k_e2e = max(3, min(args.steps, 20)) if args.workload == "event" else max(1, min(args.steps, 3))
+        k_e2e = max(3, min(args.steps, 20)) if args.workload in ("event", "c3") else max(1, min(args.steps, 3))
         batch = [host_events[i % len(host_events)] for i in range(k_e2e * per_step)]
         adc_bufs = [[torch.empty(p.shape, dtype=torch.uint16).pin_memory().numpy() for p in slot_planes]
                     for _ in range(2)]
@@ -604,6 +641,9 @@ def run_sim(args, world, rank, local):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         if args.workload == "event":
             cpu = cpu_baseline_event([calls[0][0][1]], cores)
+        elif args.workload == "c3":
+            v, sample = c3_reference(cores)
+            cpu = {"value": v, "unit": "depos/s", "cores": cores, "kind": "reference", "sample": sample}
         else:
             v, sample = reference_sample(args, cores)
             cpu = {"value": v, "unit": "depos/s", "cores": cores, "kind": "reference", "sample": sample}
@@ -614,7 +654,7 @@ def run_sim(args, world, rank, local):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (straight line tracks, fixed seeds)",
             "config": {"workload": workload_desc(args), "events_per_sec": None if args.workload == "c4" else
-                       (world if args.workload == "event" else C5_EVENTS) * 1e3 / ms_per_step,
+                       (world if args.workload in ("event", "c3") else C5_EVENTS) * 1e3 / ms_per_step,
                        "depos_per_step": step_depos_all, "cells_per_call": call_cells,
                        "l2": "inputs rotate over distinct events (> 126 MB L2); every step writes the frames",
                        "parallelism": parallel,
@@ -627,6 +667,10 @@ def run_sim(args, world, rank, local):
                          "kernel": conv_kernel, "kernel_ms": conv_ms, "algorithmic_bytes": alg_bytes,
                          "peak_kind": peak_kind, "binding": binding,
                          "raster_pipes": profile_facts("k_sample_off").get("pipes")},
+            "fluctuation": None if args.workload != "c3" else {
+                "kernel": "k_fluctuate_exact", "stage_ms": float(stage.fluctuate_ms),
+                "share_of_event": float(stage.fluctuate_ms) / float(stage.total_ms),
+                "pipes": profile_facts("k_fluctuate_exact").get("pipes")},
             "clocks": clk,
             "gpu_launches": gpu_launches,
             "e2e": e2e,
@@ -646,8 +690,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="event", choices=["event", "sigproc", "c4", "c5"],
-                    help="event: the headline metric (configs[1]); c4: configs[3]; c5: configs[4]; "
+    ap.add_argument("--workload", default="event", choices=["event", "sigproc", "c3", "c4", "c5"],
+                    help="event: the headline metric (configs[1]); c3: configs[2]; c4: configs[3]; c5: configs[4]; "
                          "sigproc: the Listing 1 chain (§8(f))")
     ap.add_argument("--depos", type=int, default=100_000, help="c5: depositions per event (1k-1M sweep)")
     args = ap.parse_args()

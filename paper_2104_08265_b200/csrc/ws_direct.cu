@@ -120,7 +120,9 @@ __device__ __forceinline__ void cp_wait()
     asm volatile("cp.async.wait_group %0;" ::"n"(K) : "memory");
 }
 
-template <int NT>
+// kRO: the fused readout (noise + digitize, fp64 frame) in the frame store;
+// a separate instantiation so the plain fp32 store keeps its registers
+template <int NT, bool kRO>
 __global__ void __launch_bounds__(NT, 2)
 k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* __restrict__ band_off,
          const TEnt* __restrict__ tlist)
@@ -332,7 +334,7 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
     // frame rows of the window (convolve's real part, spectral.cpp:172-173),
     // streaming stores; one flattened (row, 16-byte word) loop. With a
     // readout (ev.ro) the same words go through noise + digitize instead.
-    if (ev.ro) {
+    if constexpr (kRO) {
         if ((N & 3) == 0) {
             constexpr int kW = kTileTicks / 4;
             const int wlen4 = wlen >> 2;
@@ -399,15 +401,18 @@ extern "C" cudaError_t wsb_launch_direct(const wsb::EventDesc& ev, const uint32_
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     if (!(ready & (1ull << dev))) {
-        e = cudaFuncSetAttribute(wsb::k_direct<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(wsb::k_direct<NT>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        if (e != cudaSuccess) return e;
+        for (auto f : {wsb::k_direct<NT, false>, wsb::k_direct<NT, true>}) {
+            e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
+            if (e != cudaSuccess) return e;
+            e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+            if (e != cudaSuccess) return e;
+        }
         ready |= 1ull << dev;
     }
+    const auto KFN = ev.ro ? wsb::k_direct<NT, true> : wsb::k_direct<NT, false>;
     if (ev.total_bands == 0) return cudaSuccess;
     if (!pdl) {
-        wsb::k_direct<NT><<<ev.total_bands, NT, smem_bytes, stream>>>(ev, pool, band_off, tlist);
+        KFN<<<ev.total_bands, NT, smem_bytes, stream>>>(ev, pool, band_off, tlist);
         return cudaGetLastError();
     }
     // programmatic dependent launch: the tiles' prologue (zeroing, staging,
@@ -423,5 +428,5 @@ extern "C" cudaError_t wsb_launch_direct(const wsb::EventDesc& ev, const uint32_
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, wsb::k_direct<NT>, ev, pool, band_off, tlist);
+    return cudaLaunchKernelEx(&cfg, KFN, ev, pool, band_off, tlist);
 }

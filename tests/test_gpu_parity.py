@@ -84,10 +84,13 @@ def test_fluct_approx_philox(ctx, oracle):
     res = Plane(ctx, SMALL, resp).simulate(depos, cfg, want_charge=True)
     s_ref, _ = oracle.charge_fluct_on(oracle_grid(SMALL), depos, rng_mode=1, approx=True, seed=99)
     # Gaussian-approx draws go through log/cos/sin; CUDA and glibc may differ in
-    # the last ulp, which can move a rounded draw by one electron.
+    # the last ulp, which moves a rounded draw only at an exact .5 tie: the
+    # frame meets the north star's 1e-5 and almost every cell is identical
     diff = np.abs(res.charge.astype(np.int64) - s_ref)
-    assert diff.sum() <= 0.001 * s_ref.sum()
     assert res.charge.sum() == s_ref.sum()
+    assert diff.sum() <= 1e-5 * s_ref.sum()
+    m_ref = oracle.convolve(oracle_grid(SMALL), oracle_response(resp), s_ref.astype(np.float64))
+    assert relL2_per_channel(res.frame, m_ref) < 1e-5
 
 
 def test_convolve_only(ctx, oracle):

@@ -69,9 +69,23 @@ def full(tag, rep, kernel):
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
             return v * scale
         traffic = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
+        inst = val("smsp__inst_executed.sum") if "smsp__inst_executed.sum" in d else None
+        # pipe utilisation (FP32 FMA, XU/SFU, FP64, ALU, LSU...): % of peak over active cycles
+        pipes = {}
+        for m in hdr:
+            if m.startswith("sm__pipe_") and m.endswith("cycles_active.avg.pct_of_peak_sustained_active") \
+                    and d.get(m) not in (None, "", "n/a"):
+                pipes[m[len("sm__pipe_"):-len("_cycles_active.avg.pct_of_peak_sustained_active")]] = float(d[m])
+            if m.startswith("sm__inst_executed_pipe_") and m.endswith("avg.pct_of_peak_sustained_active") \
+                    and d.get(m) not in (None, "", "n/a"):
+                pipes["inst_" + m[len("sm__inst_executed_pipe_"):-len(".avg.pct_of_peak_sustained_active")]] = \
+                    float(d[m])
+        if pipes:
+            out += ["", "pipe utilisation (% of peak, active cycles):", "",
+                    "| pipe | % |", "|---|---|"] + [f"| {k} | {v:.1f} |" for k, v in sorted(pipes.items())]
         break
     (PROF / f"{tag}_{kernel}_ncu.md").write_text("\n".join(out) + "\n")
-    return traffic
+    return traffic, inst, pipes
 
 
 if __name__ == "__main__":
@@ -83,9 +97,10 @@ if __name__ == "__main__":
     for spec in sys.argv[3:]:
         rep, kernels = spec.split(":")
         for kernel in kernels.split(","):
-            traffic = full(tag, rep, kernel)
+            traffic, inst, pipes = full(tag, rep, kernel)
             (PROF / f"traffic_{kernel}.json").write_text(json.dumps(
-                {"kernel": kernel, "dram_bytes_per_launch": traffic, "source": f"{tag} ncu --set full",
+                {"kernel": kernel, "dram_bytes_per_launch": traffic, "warp_inst_per_launch": inst, "pipes": pipes,
+                 "source": f"{tag} ncu --set full",
                  "note": ("one launch = one 960 x 6000 sigproc batch" if kernel == "k_sigproc"
                           else "one launch = one MicroBooNE event (3 planes)")}, indent=1) + "\n")
             print((PROF / f"{tag}_{kernel}_ncu.md").read_text())
