@@ -100,7 +100,7 @@ class Simulator {
         o.fluctuate = 1;  // the reference always fluctuates (rasterize.cpp:182-202)
         o.approx = config.rng.mode == wiresim::RngMode::pool ? 1 : 0;
         o.rng_mode = WS_RNG_SUBSTREAM;
-        o.charge_u32 = 1;  // exact integer counts (ChargeGrid is int64)
+        o.charge_type = WS_CHARGE_I64;  // the exact counts straight into ChargeGrid's int64 matrix
         o.seed = config.rng.seed;
         o.drift.enabled = config.drift.enabled ? 1 : 0;
         o.drift.response_plane_x = config.drift.response_plane_x;
@@ -125,11 +125,10 @@ class Simulator {
         const std::size_t W = config.grid.padded_wires(), T = config.grid.padded_ticks();
         wiresim::SimResult res{wiresim::Matrix<std::int32_t>(W, T), wiresim::TimingReport{},
                                wiresim::ChargeGrid(config.grid), 0};
-        m_charge.resize(W * T);  // uint32 counts
         ws_timing t{};
         check(ws_run_simulation(plane, reinterpret_cast<const ws_depo*>(depos.data()), depos.size(), &o, &ro,
-                                res.adc.data.data(), nullptr, reinterpret_cast<float*>(m_charge.data()), &t));
-        for (std::size_t i = 0; i < W * T; ++i) res.charge.counts.data[i] = (std::int64_t)m_charge[i];
+                                res.adc.data.data(), nullptr, reinterpret_cast<float*>(res.charge.counts.data.data()),
+                                &t));
         res.clipped_charge = t.clipped_charge;
         res.timing.rasterization_total_s = 1e-3 * (t.prepare_ms + t.fluctuate_ms);
         res.timing.sampling_2d_s = 1e-3 * t.prepare_ms;
@@ -176,7 +175,6 @@ class Simulator {
 
     ws_ctx* m_ctx = nullptr;
     std::vector<Entry> m_planes;
-    std::vector<std::uint32_t> m_charge;
 };
 
 // Drop-in for wiresim::run_simulation (pipeline.hpp:104): one Simulator per

@@ -97,12 +97,16 @@ typedef struct ws_drift {
 enum { WS_RNG_SUBSTREAM = 0, /* reference xoshiro256** substream(seed, depo.id), rng.cpp:64-76 */
        WS_RNG_PHILOX = 1 };  /* shared Philox4x32-10 stream keyed by (seed, depo.id) */
 
+enum { WS_CHARGE_F32 = 0, WS_CHARGE_U32 = 1, WS_CHARGE_I64 = 2 };
+
 typedef struct ws_sim_options {
     int32_t fluctuate;   /* 0: S = q * p (fp32, fixed-point accumulated); 1: binomial fluctuation */
     int32_t approx;      /* fluctuation sampler: 0 exact binomial (fluctuate), 1 Gaussian approx (fluctuate_approx) */
     int32_t rng_mode;    /* WS_RNG_* */
-    int32_t charge_u32;  /* fluctuation on: charge outputs hold the exact integer counts as uint32 (the
-                            reference's int64 ChargeGrid up to 2^32-1 per cell) instead of float32 */
+    int32_t charge_type; /* charge outputs with fluctuation on: WS_CHARGE_F32 (float32), WS_CHARGE_U32
+                            (exact counts; a cell past 2^32-1 is a WS_ERUNTIME) or WS_CHARGE_I64 (the
+                            reference's int64 ChargeGrid, core.hpp:94-99; 8 B per cell). Fluctuation off:
+                            float32 always. */
     uint64_t seed;       /* SimConfig::rng.seed */
     ws_drift drift;      /* SimConfig::drift */
 } ws_sim_options;
@@ -170,6 +174,8 @@ typedef struct ws_plane_info {
     int32_t n_radix_passes;
     int64_t support_ticks, support_wires; /* ResponseKernel::support_* */
     int64_t lo_lag, n_lags;               /* combined time kernel lags [lo_lag, lo_lag + n_lags) */
+    int32_t impacts_per_pitch;            /* 1 unless made by ws_plane_create_impacts */
+    int32_t n_response_classes;           /* distinct per-impact responses */
 } ws_plane_info;
 
 typedef struct ws_ctx ws_ctx;
@@ -205,6 +211,25 @@ uint64_t ws_ctx_launch_count(const ws_ctx* ctx);
  * can only be destroyed. */
 int ws_plane_create(ws_ctx* ctx, const ws_grid_spec* grid, const ws_response* response, double n_sigma,
                     ws_plane** out);
+/* Impact positions (north star (3); WCT's per-impact field response, which
+ * the reference replaces by one response per plane): each
+ * wire pitch is split into impacts_per_pitch equal sub-bins, impact i of wire
+ * w spanning [origin_x + (w - pad_wires + i / P) pitch, + pitch / P). Depos
+ * are sampled at impact resolution (the Gaussian's integral over every
+ * sub-bin, normalised over the footprint's sub-bins) and responses[i] — its
+ * own time kernel K_i and wire weights ww_i — applies to the charge S_i
+ * binned at impact i:  M[w] = sum_i sum_dw ww_i[dw] (K_i (*) S_i[w - dw]).
+ * Impacts with identical responses form one class, whose sub-bins are summed
+ * to wires before the convolution (one class, e.g. 10 identical responses,
+ * telescopes to the reference's wire binning, core.cpp:25-41 with
+ * spectral.cpp:124-135, and runs every path: both kernels, fluctuation).
+ * Several classes run on the time-domain path: each class's per-depo
+ * profiles are added into the same frame tiles (the sum over impact
+ * positions fused into k_direct's accumulation); fluctuation and charge
+ * outputs need a single class. impacts_per_pitch in [1, 32], at most 8
+ * classes. ws_plane_create is impacts_per_pitch = 1. */
+int ws_plane_create_impacts(ws_ctx* ctx, const ws_grid_spec* grid, const ws_response* responses,
+                            uint32_t impacts_per_pitch, double n_sigma, ws_plane** out);
 int ws_plane_destroy(ws_plane* plane);
 int ws_plane_get_info(const ws_plane* plane, ws_plane_info* info);
 /* Combined time-domain kernel samples (n_lags doubles, lag lo_lag first). */
@@ -254,7 +279,8 @@ int ws_simulate_events(ws_ctx* ctx, uint32_t n_events, uint32_t n_planes, ws_pla
  * synchronous: adc (padded wires x padded ticks, int32 or uint16 per
  * readout->adc_type) is SimResult::adc; frame (nullable) the noisy frame
  * before digitization (fp32 or fp64 per readout->frame_type); charge
- * (nullable) the charge grid S (float32; exact integers with fluctuation).
+ * (nullable) the charge grid S (float32; with fluctuation the exact counts
+ * in opt->charge_type: float32, uint32 or int64).
  * Workspace overflows are re-run internally (never WS_OK with a partial
  * result). */
 int ws_run_simulation(ws_plane* plane, const ws_depo* depos, uint64_t n, const ws_sim_options* opt,

@@ -488,3 +488,53 @@ class RefPlane:
             self.ref.lib.wsr_plane_destroy(self.handle)
         except Exception:
             pass
+
+
+def impact_charge(g, depos, impacts: int, masks, n_sigma: float = 3.0):
+    """CPU restatement (numpy; test infrastructure) of fluctuation-off sampling
+    at impact resolution — the extension ws_plane_create_impacts implements,
+    which the reference does not have. It follows
+    sample_patch (rasterize.cpp:66-120) with map_depo_to_grid's footprint and
+    clip (core.cpp:25-41): the wire axis of the footprint is split into
+    `impacts` sub-bins per wire, each the Gaussian's integral
+    (gauss_bin_integrals, rasterize.cpp:44-64, at spacing pitch / impacts;
+    sigma <= 0: the containing sub-bin), the patch normalised over all
+    sub-bins x ticks. Returns one float64 charge grid per class mask
+    (S_c[w, t] = q sum_{i in c} p[w, i, t]) and the clipped charge."""
+    from math import ceil, erf, floor, sqrt
+    W, T = padded(g)
+    out = [np.zeros((W, T)) for _ in masks]
+    clipped = 0
+
+    def integrals(center, sigma, lo, spacing, n):
+        v = np.zeros(n)
+        if sigma <= 0.0:
+            v[min(max(int(floor((center - lo) / spacing)), 0), n - 1)] = 1.0
+            return v
+        inv = 1.0 / (sqrt(2.0) * sigma)
+        e = [erf((lo + k * spacing - center) * inv) for k in range(n + 1)]
+        return 0.5 * (np.array(e[1:]) - np.array(e[:-1]))
+
+    for d in np.asarray(depos):
+        cw = int(g.pad_wires) + floor((d["x"] - g.origin_x) / g.pitch)
+        ct = int(g.pad_ticks) + floor((d["t"] - g.origin_t) / g.tick)
+        hw = 0 if d["sigma_x"] <= 0 else ceil(n_sigma * d["sigma_x"] / g.pitch)
+        ht = 0 if d["sigma_t"] <= 0 else ceil(n_sigma * d["sigma_t"] / g.tick)
+        w0, w1 = max(cw - hw, 0), min(cw + hw, W - 1)
+        t0, t1 = max(ct - ht, 0), min(ct + ht, T - 1)
+        if w0 > w1 or t0 > t1:
+            clipped += int(d["q"])
+            continue
+        nw, nt = w1 - w0 + 1, t1 - t0 + 1
+        wlo = g.origin_x + (w0 - int(g.pad_wires)) * g.pitch
+        tlo = g.origin_t + (t0 - int(g.pad_ticks)) * g.tick
+        sub = integrals(d["x"], d["sigma_x"], wlo, g.pitch / impacts, nw * impacts).reshape(nw, impacts)
+        tv = integrals(d["t"], d["sigma_t"], tlo, g.tick, nt)
+        total = sub.sum() * tv.sum()
+        if not total > 0.0:
+            clipped += int(d["q"])
+            continue
+        for c, m in enumerate(masks):
+            wv = sub[:, [i for i in range(impacts) if (m >> i) & 1]].sum(axis=1)
+            out[c][w0:w1 + 1, t0:t1 + 1] += float(d["q"]) * np.outer(wv, tv) / total
+    return out, clipped

@@ -18,6 +18,7 @@ LIB_PATH = PKG / "libwsgpu.so"
 WS_OK, WS_EINVAL, WS_ERANGE, WS_EDOMAIN, WS_ERUNTIME, WS_ECUDA, WS_ENOMEM = range(7)
 WS_INDUCTION, WS_COLLECTION = 0, 1
 WS_RNG_SUBSTREAM, WS_RNG_PHILOX = 0, 1
+WS_CHARGE_F32, WS_CHARGE_U32, WS_CHARGE_I64 = 0, 1, 2
 
 # ws_depo == wiresim::Depo (core.hpp:63-70)
 DEPO_DTYPE = np.dtype(
@@ -52,7 +53,7 @@ class DriftC(C.Structure):
 
 
 class SimOptionsC(C.Structure):
-    _fields_ = [("fluctuate", C.c_int32), ("approx", C.c_int32), ("rng_mode", C.c_int32), ("charge_u32", C.c_int32),
+    _fields_ = [("fluctuate", C.c_int32), ("approx", C.c_int32), ("rng_mode", C.c_int32), ("charge_type", C.c_int32),
                 ("seed", C.c_uint64), ("drift", DriftC)]
 
 
@@ -91,7 +92,8 @@ class TimingC(C.Structure):
 class PlaneInfoC(C.Structure):
     _fields_ = [("padded_wires", C.c_uint64), ("padded_ticks", C.c_uint64), ("fft_length", C.c_uint64),
                 ("folded", C.c_int32), ("n_radix_passes", C.c_int32), ("support_ticks", C.c_int64),
-                ("support_wires", C.c_int64), ("lo_lag", C.c_int64), ("n_lags", C.c_int64)]
+                ("support_wires", C.c_int64), ("lo_lag", C.c_int64), ("n_lags", C.c_int64),
+                ("impacts_per_pitch", C.c_int32), ("n_response_classes", C.c_int32)]
 
 
 # exported symbols (name -> (restype, argtypes)); every one is declared in include/*.h
@@ -107,6 +109,7 @@ SIGNATURES = {
     "ws_ctx_set_conv_path": (C.c_int, [_P, C.c_int]),
     "ws_ctx_set_direct_kappa": (C.c_int, [_P, C.c_double]),
     "ws_plane_create": (C.c_int, [_P, C.POINTER(GridSpecC), C.POINTER(ResponseC), C.c_double, C.POINTER(_P)]),
+    "ws_plane_create_impacts": (C.c_int, [_P, C.POINTER(GridSpecC), _P, C.c_uint32, C.c_double, C.POINTER(_P)]),
     "ws_plane_destroy": (C.c_int, [_P]),
     "ws_plane_get_info": (C.c_int, [_P, C.POINTER(PlaneInfoC)]),
     "ws_plane_get_kernel": (C.c_int, [_P, _P, C.c_uint64]),

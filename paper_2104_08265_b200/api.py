@@ -126,13 +126,13 @@ class SimConfig:
                           _lib.WS_ADC_U16 if adc_type == "u16" else _lib.WS_ADC_I32)
         return r, amp
 
-    def options(self, charge_u32: bool = False) -> _lib.SimOptionsC:
-        """ws_sim_options; charge_u32: with fluctuation, charge outputs hold
-        the exact uint32 counts instead of float32."""
+    def options(self, charge_type: str = "f32") -> _lib.SimOptionsC:
+        """ws_sim_options; charge_type: with fluctuation, the charge outputs'
+        type: "f32", "u32" (exact counts) or "i64" (the reference's int64)."""
         d = self.drift
         return _lib.SimOptionsC(
             int(self.fluctuate), int(self.approx),
-            _lib.WS_RNG_PHILOX if self.rng.mode == "philox" else _lib.WS_RNG_SUBSTREAM, int(charge_u32),
+            _lib.WS_RNG_PHILOX if self.rng.mode == "philox" else _lib.WS_RNG_SUBSTREAM, {"f32": 0, "u32": 1, "i64": 2}[charge_type],
             self.rng.seed,
             _lib.DriftC(int(d.enabled), 0, d.response_plane_x, d.drift_speed, d.diffusion_long, d.diffusion_tran))
 
@@ -194,13 +194,28 @@ class Context:
 class Plane:
     """Geometry + response, precomputed on the device (ws_plane)."""
 
-    def __init__(self, ctx: Context, grid: GridSpec, response: ResponseParams, n_sigma: float = 3.0):
+    def __init__(self, ctx: Context, grid: GridSpec, response: ResponseParams | Sequence[ResponseParams],
+                 n_sigma: float = 3.0, impacts_per_pitch: int = 1):
+        """response: one ResponseParams, or (impact positions,
+        ws_plane_create_impacts) impacts_per_pitch of them, impact i at sub-bin
+        i of the pitch; a single response with impacts_per_pitch > 1 is used
+        for every impact (the degenerate case the reference pins)."""
         self.ctx, self.grid, self.response, self.n_sigma = ctx, grid, response, n_sigma
         self.lib = ctx.lib
-        r, self._ww = response.to_c()
         g = grid.to_c()
         h = C.c_void_p()
-        check(self.lib.ws_plane_create(ctx.handle, C.byref(g), C.byref(r), n_sigma, C.byref(h)))
+        if impacts_per_pitch == 1 and isinstance(response, ResponseParams):
+            r, self._ww = response.to_c()
+            check(self.lib.ws_plane_create(ctx.handle, C.byref(g), C.byref(r), n_sigma, C.byref(h)))
+        else:
+            rs = [response] * impacts_per_pitch if isinstance(response, ResponseParams) else list(response)
+            if len(rs) != impacts_per_pitch:
+                raise WsError(_lib.WS_EINVAL, "need one response per impact position")
+            conv = [x.to_c() for x in rs]
+            self._ww = [w for _, w in conv]
+            arr = (_lib.ResponseC * len(rs))(*[c for c, _ in conv])
+            check(self.lib.ws_plane_create_impacts(ctx.handle, C.byref(g), arr, impacts_per_pitch, n_sigma,
+                                                   C.byref(h)))
         self.handle = h
         ctx._planes.add(self)
         info = _lib.PlaneInfoC()
@@ -251,8 +266,8 @@ class Plane:
 
     # ---- device entry points (torch tensors; asynchronous on the context stream)
     def simulate_device(self, depos_dev, n: int, config: SimConfig, frame_dev, charge_dev=None, timing=None,
-                        charge_u32: bool = False):
-        opt = config.options(charge_u32)
+                        charge_type: str = "f32"):
+        opt = config.options(charge_type)
         check(self.lib.ws_simulate_plane_device(self.handle, _ptr(depos_dev), n, C.byref(opt), _ptr(frame_dev),
                                                 _ptr(charge_dev), C.byref(timing) if timing is not None else None))
 

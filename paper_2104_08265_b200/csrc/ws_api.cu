@@ -33,7 +33,8 @@ extern "C" cudaError_t wsb_launch_gprof(const EventDesc& ev, const UnitRec* recs
                                         int pdl);
 extern "C" cudaError_t wsb_launch_noise(const float* in, const wsb::Sink& out, int W, int N, int noise, int rng_mode,
                                         double sigma, uint64_t seed, cudaStream_t s);
-extern "C" cudaError_t wsb_launch_u32_to_f32(uint32_t* g, size_t n, cudaStream_t s);
+extern "C" cudaError_t wsb_launch_counts_out(const unsigned long long* g, void* out, int type, size_t n, unsigned* err,
+                                             cudaStream_t s);
 extern "C" cudaError_t wsb_launch_noise_spectrum(const wsb::PlaneDesc& P, const double* amp, uint64_t seed, int rng_mode,
                                                  const float* in, const wsb::Sink& out, int variant,
                                                  cudaStream_t stream);
@@ -152,6 +153,7 @@ struct ws_ctx {
     DevBuf<ScratchHeader> header;
     DevBuf<ws_depo> depos;
     DevBuf<float> frames, charges, ro_scratch;
+    DevBuf<unsigned long long> counts;  // fluctuation on: the integer charge grids (u64 counts)
     DevBuf<unsigned char> out_stage;  // ws_run_*: device staging of the readout outputs (ADC / fp64 frames)
     DevBuf<double> noise_amp;  // spectrum-mode amplitudes of the last ws_noise_digitize_device
     ScratchHeader* host_slots = nullptr;  // pinned, kStatSlots
@@ -200,6 +202,12 @@ struct ws_plane {
     uint16_t* d_rev = nullptr;
     int ww_is_one = 0;
     bool route_fft_next = false;  // AUTO: a tile overflowed (dense, e.g. a shower): the row FFT on the re-run
+    // impact positions (ws_plane_create_impacts): sub-bins per pitch and the
+    // impacts of this plane's response class; further classes (distinct
+    // responses) are child planes run alongside this one into the same frame
+    int impacts = 1;
+    uint32_t imp_mask = 1u;
+    std::vector<ws_plane*> classes;
     int rows_per_band = 4;
     int n_bands = 0;
     size_t smem = 0;
@@ -395,6 +403,9 @@ PlaneDesc plane_desc(const ws_plane* p)
     d.kern = p->d_kern ? p->d_kern + wsb::kKernPad : nullptr;
     d.kern_absmax = p->kern_absmax;
     d.direct = 0;  // decided per call (run_group)
+    d.impacts = p->impacts;
+    d.imp_mask = p->imp_mask;
+    d.stats_owner = 1;
     d.n_windows = p->n_windows;
     d.direct_cap = (uint32_t)wsb_direct_cap();
     d.n_bands = p->n_bands;
@@ -408,6 +419,8 @@ int check_opts(const ws_sim_options* o)
         return set_err(WS_EINVAL, "options: unknown rng mode %d", o->rng_mode);
     if (o->drift.enabled && !(o->drift.drift_speed > 0.0))
         return set_err(WS_EINVAL, "drift_depo: drift_speed must be > 0");
+    if (o->charge_type != WS_CHARGE_F32 && o->charge_type != WS_CHARGE_U32 && o->charge_type != WS_CHARGE_I64)
+        return set_err(WS_EINVAL, "options: unknown charge type %d", o->charge_type);
     return WS_OK;
 }
 
@@ -431,9 +444,13 @@ bool readout_fused(const ws_readout* r)
            (r->noise.mode == WS_NOISE_WHITE && r->noise.sigma == 0.0);
 }
 
+// charges: per plane (nullable array / entries): fluctuation off, the float32
+// charge grid S (an extra accumulate pass); fluctuation on, the caller's copy
+// of the integer counts in opt->charge_type. counts: fluctuation on, the
+// device count grids of the walk (u64, required).
 int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* const* depos, const uint64_t* n_depos,
               const ws_sim_options* opt, float* const* frames, float* const* charges, const float* const* charge_in,
-              ws_timing* timing, const Readout* ro = nullptr, bool charge_to_float = false)
+              ws_timing* timing, const Readout* ro = nullptr, unsigned long long* const* counts = nullptr)
 {
     cudaStream_t s = c->stream;
     EventDesc ev{};
@@ -484,6 +501,12 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
     size_t smem = 0;
     bool want_frame = false, any_direct = false, any_fft = false;
     int max_lags = 0;
+    // plane descriptors of the launch: one per plane, plus one per further
+    // response class of a plane with impact positions (same depos, tiles and
+    // frame; its own response), right after its plane
+    uint32_t nd = 0;
+    std::vector<uint32_t> desc_of(n);
+    std::vector<ws_plane*> desc_plane;
     for (uint32_t i = 0; i < n; ++i) {
         ws_plane* p = planes[i];
         PlaneDesc d = plane_desc(p);
@@ -496,9 +519,9 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
             d.frame64 = ro->frame64 ? ro->frame64[i] : nullptr;
             d.adc = ro->adc ? ro->adc[i] : nullptr;
         }
-        // fluctuation on: the walk's integer grid lives in the charge buffer
-        d.charge_u32 = (ev.fluctuate && !from_grid) ? reinterpret_cast<uint32_t*>(charges[i]) : nullptr;
-        d.charge_out = (charges && !d.charge_u32) ? charges[i] : nullptr;
+        // fluctuation on: the walk's integer grid
+        d.charge_cnt = (ev.fluctuate && !from_grid) ? counts[i] : nullptr;
+        d.charge_out = (charges && !ev.fluctuate) ? charges[i] : nullptr;
         d.charge_in = from_grid ? charge_in[i] : nullptr;
         d.stats = nullptr;
         const bool has_out = d.frame || d.frame64 || d.adc;
@@ -511,22 +534,56 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
         // FFT once under AUTO: its cost does not depend on the depo density.
         const bool dense = p->route_fft_next && c->conv_path == WS_CONV_AUTO;
         p->route_fft_next = false;
-        if (ev.mode == 0 && has_out && !d.charge_out && p->direct_ok && c->conv_path != WS_CONV_FFT && !dense) {
+        const bool classes = !p->classes.empty();
+        if (classes) {
+            // distinct per-impact responses: the classes' profiles are summed
+            // in k_direct's tiles (the sum over impacts fused into the
+            // time-domain convolution)
+            if (ev.mode != 0 || d.charge_out)
+                return set_err(WS_EINVAL, "impact planes with distinct responses: fluctuation, charge-grid input and "
+                                          "charge output are not supported");
+            if (c->conv_path == WS_CONV_FFT)
+                return set_err(WS_EINVAL, "impact planes with distinct responses run on the time-domain path only");
+        }
+        if (ev.mode == 0 && has_out && !d.charge_out && p->direct_ok && c->conv_path != WS_CONV_FFT &&
+            (!dense || classes)) {
             const double work = (double)d.n_units * 12.0 * (double)(p->n_lags + 16);
-            if (c->conv_path == WS_CONV_DIRECT || work <= c->direct_kappa * (double)p->W * (double)p->Np) {
+            if (classes || c->conv_path == WS_CONV_DIRECT || work <= c->direct_kappa * (double)p->W * (double)p->Np) {
                 d.direct = 1;
                 d.n_bands = ((p->W + wsb::kTileRows - 1) / wsb::kTileRows) * p->n_windows;
                 any_direct = true;
                 max_lags = std::max(max_lags, (int)p->n_lags);
             }
         }
+        if (nd + 1 + p->classes.size() > (size_t)wsb::kMaxPlanes)
+            return set_err(WS_EINVAL, "launch group: more than %d plane descriptors", wsb::kMaxPlanes);
         any_fft = any_fft || !d.direct;
-        ev.p[i] = d;
+        desc_of[i] = nd;
+        desc_plane.push_back(classes ? nullptr : p);  // (dense re-routing only for single-class planes)
+        ev.p[nd++] = d;
         units += d.n_units;
         bands += (uint32_t)d.n_bands;
         smem = std::max(smem, p->smem);
         want_frame = want_frame || has_out;
+        for (ws_plane* cp : p->classes) {
+            PlaneDesc e = plane_desc(cp);
+            e.depos = d.depos;
+            e.n_units = d.n_units;
+            e.unit_base = units;
+            e.band_base = d.band_base;  // the plane's tiles
+            e.n_bands = 0;
+            e.frame = d.frame;
+            e.frame64 = d.frame64;
+            e.adc = d.adc;
+            e.direct = 1;
+            e.stats_owner = 0;
+            max_lags = std::max(max_lags, (int)cp->n_lags);
+            desc_plane.push_back(nullptr);
+            ev.p[nd++] = e;
+            units += e.n_units;
+        }
     }
+    ev.n_planes = (int)nd;
     ev.total_units = units;
     ev.total_bands = bands;
 
@@ -545,7 +602,7 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
     WS_CUDA(c->band_off.reserve(bands + 1));
     WS_CUDA(c->band_fill.reserve(bands + 1));
     int max_h = 0;
-    for (uint32_t i = 0; i < n; ++i) max_h = std::max(max_h, planes[i]->h);
+    for (uint32_t i = 0; i < nd; ++i) max_h = std::max(max_h, ev.p[i].h);
     // bin lists: ~4.5 entries per unit for 4-row FFT bands, ~2 per unit for
     // 16 x 2048 tiles at typical widths; overflow is detected on the device
     const size_t list_cap = std::min<size_t>(std::max<size_t>(c->list_hint, (size_t)units * (8 + max_h) + 4096),
@@ -589,7 +646,7 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
     const int slot = c->next_slot;
     c->next_slot = (c->next_slot + 1) % kStatSlots;
     ScratchHeader* hdr = c->header.p + slot;
-    for (uint32_t i = 0; i < n; ++i) {
+    for (uint32_t i = 0; i < nd; ++i) {
         ev.p[i].stats = &hdr->stats[2 * i];
         ev.p[i].tile_need = &hdr->tile_need[i];
     }
@@ -598,13 +655,13 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
 
     PendingCall pc{};
     pc.timing = timing;
-    pc.n_planes = (int)n;
+    pc.n_planes = (int)nd;
     pc.tag = c->call_tag;
     pc.tiles = bands;
     uint32_t direct_units = 0;  // units on direct planes: the profiles kernel runs iff > 0
-    for (uint32_t i = 0; i < n; ++i) {
-        pc.direct_planes += ev.p[i].direct;
-        pc.planes[i] = ev.p[i].direct ? planes[i] : nullptr;
+    for (uint32_t i = 0; i < nd; ++i) {
+        pc.direct_planes += ev.p[i].direct && ev.p[i].stats_owner;
+        pc.planes[i] = ev.p[i].direct ? desc_plane[i] : nullptr;
         if (ev.p[i].direct) direct_units += ev.p[i].n_units;
     }
     pc.fluctuate = ev.fluctuate;
@@ -614,8 +671,10 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
     if (timing) WS_CUDA(cudaEventRecord(pc.ev[0], s));  // stage timing only
 
     if (ev.fluctuate && !from_grid)
-        for (uint32_t i = 0; i < n; ++i)
-            WS_CUDA(cudaMemsetAsync(ev.p[i].charge_u32, 0, sizeof(uint32_t) * (size_t)ev.p[i].W * ev.p[i].N, s));
+        for (uint32_t i = 0; i < nd; ++i)
+            if (ev.p[i].charge_cnt)
+                WS_CUDA(cudaMemsetAsync(ev.p[i].charge_cnt, 0, sizeof(unsigned long long) * (size_t)ev.p[i].W * ev.p[i].N,
+                                        s));
     if (!from_grid) {
         WS_CUDA(wsb_launch_sample(ev, c->recs.p, c->pool.p, (uint32_t)std::min<size_t>(c->pool.cap, 0xffffffffu),
                                   &hdr->pool_ctr, c->band_count.p, &hdr->err, s, timing ? 0 : 1));
@@ -691,7 +750,7 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
         // kernel over the fp32 frame (in place), then digitize
         const ws_readout& r = *ro->spec;
         for (uint32_t i = 0; i < n; ++i) {
-            const PlaneDesc& d = ev.p[i];
+            const PlaneDesc& d = ev.p[desc_of[i]];
             const wsb::Sink sk{frames && frames[i] ? frames[i] : nullptr, ro->frame64 ? ro->frame64[i] : nullptr,
                                ro->adc ? ro->adc[i] : nullptr, r.adc_type == WS_ADC_U16 ? 1 : 0, r.adc.scale,
                                r.adc.offset, (double)((1 << r.adc.bits) - 1)};
@@ -707,9 +766,11 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
             c->launches += 1;
         }
     }
-    if (ev.fluctuate && !from_grid && charge_to_float && !(opt && opt->charge_u32))
-        for (uint32_t i = 0; i < n; ++i) {  // the caller's charge output: integer counts -> float32 in place
-            WS_CUDA(wsb_launch_u32_to_f32(ev.p[i].charge_u32, (size_t)ev.p[i].W * ev.p[i].N, s));
+    if (ev.fluctuate && !from_grid && charges)
+        for (uint32_t i = 0; i < n; ++i) {  // the caller's charge output: the counts in its type
+            const PlaneDesc& d = ev.p[desc_of[i]];
+            if (!charges[i]) continue;
+            WS_CUDA(wsb_launch_counts_out(d.charge_cnt, charges[i], opt->charge_type, (size_t)d.W * d.N, &hdr->err, s));
             c->launches += 1;
         }
     if (timing) WS_CUDA(cudaEventRecord(pc.ev[4], s));  // stage timing only
@@ -744,8 +805,9 @@ int finish_pending(ws_ctx* c)
             prc = WS_EINVAL;
             snprintf(msg, sizeof msg, "fluctuate: charge must be >= 0");
         } else if (h.err & wsb::kErrCellOvf) {
-            prc = WS_ERUNTIME;  // a cell of the integer charge grid would pass 2^32 - 1 electrons (not retried)
-            snprintf(msg, sizeof msg, "fluctuate: a charge-grid cell exceeds 4294967295 electrons");
+            prc = WS_ERUNTIME;  // (not retried)
+            snprintf(msg, sizeof msg, "charge output: a cell exceeds 4294967295 electrons (uint32 charge type; "
+                                      "use int64)");
         }
         if (h.err & wsb::kErrPool) {
             c->pool_hint = std::max<size_t>(c->pool_hint, (size_t)h.pool_ctr + 4096);
@@ -888,6 +950,7 @@ int ws_ctx_destroy(ws_ctx* c)
     c->depos.release();
     c->frames.release();
     c->charges.release();
+    c->counts.release();
     c->ro_scratch.release();
     c->out_stage.release();
     c->noise_amp.release();
@@ -956,7 +1019,79 @@ int ws_ctx_set_direct_kappa(ws_ctx* c, double kappa)
 }
 uint64_t ws_ctx_launch_count(const ws_ctx* c) { return c ? c->launches : 0; }
 
+}  // extern "C"
+
+namespace {
+int plane_create(ws_ctx* ctx, const ws_grid_spec* grid, const ws_response* response, double n_sigma, ws_plane** out);
+}
+
+extern "C" {
+
 int ws_plane_create(ws_ctx* ctx, const ws_grid_spec* grid, const ws_response* response, double n_sigma, ws_plane** out)
+{
+    return plane_create(ctx, grid, response, n_sigma, out);
+}
+
+static bool same_response(const ws_response& a, const ws_response& b)
+{
+    if (a.plane_kind != b.plane_kind || a.shaper_order != b.shaper_order || a.field_sigma_t != b.field_sigma_t ||
+        a.shaper_peaking != b.shaper_peaking || a.gain != b.gain || a.n_wire_weights != b.n_wire_weights)
+        return false;
+    for (uint64_t i = 0; i < a.n_wire_weights; ++i)
+        if (a.wire_weights[i] != b.wire_weights[i]) return false;
+    return true;
+}
+
+int ws_plane_create_impacts(ws_ctx* ctx, const ws_grid_spec* grid, const ws_response* responses,
+                            uint32_t impacts_per_pitch, double n_sigma, ws_plane** out)
+{
+    if (!ctx || !out || !responses) return set_err(WS_EINVAL, "null argument");
+    *out = nullptr;
+    if (impacts_per_pitch < 1 || impacts_per_pitch > 32)
+        return set_err(WS_EINVAL, "impacts_per_pitch must be in [1, 32] (got %u)", impacts_per_pitch);
+    for (uint32_t i = 0; i < impacts_per_pitch; ++i)
+        if (!responses[i].wire_weights) return set_err(WS_EINVAL, "impact %u: null wire_weights", i);
+    // response classes: impacts with identical responses share one
+    std::vector<uint32_t> masks;
+    std::vector<uint32_t> first;
+    for (uint32_t i = 0; i < impacts_per_pitch; ++i) {
+        size_t c = 0;
+        while (c < first.size() && !same_response(responses[first[c]], responses[i])) ++c;
+        if (c == first.size()) {
+            first.push_back(i);
+            masks.push_back(0u);
+        }
+        masks[c] |= 1u << i;
+    }
+    if (masks.size() > (size_t)wsb::kMaxPlanes)
+        return set_err(WS_EINVAL, "at most %d distinct impact responses per plane (got %zu)", wsb::kMaxPlanes,
+                       masks.size());
+    std::vector<ws_plane*> made;
+    for (size_t c = 0; c < masks.size(); ++c) {
+        ws_plane* p = nullptr;
+        if (int rc = plane_create(ctx, grid, &responses[first[c]], n_sigma, &p)) {
+            for (ws_plane* q : made) ws_plane_destroy(q);
+            return rc;
+        }
+        p->impacts = (int)impacts_per_pitch;
+        p->imp_mask = masks[c];
+        made.push_back(p);
+        if (masks.size() > 1 && !p->direct_ok) {
+            for (ws_plane* q : made) ws_plane_destroy(q);
+            return set_err(WS_EINVAL, "impact responses: distinct per-impact responses run on the time-domain path, "
+                                      "which this geometry / kernel length does not support");
+        }
+    }
+    for (size_t c = 1; c < made.size(); ++c) made[0]->classes.push_back(made[c]);
+    *out = made[0];
+    return WS_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+int plane_create(ws_ctx* ctx, const ws_grid_spec* grid, const ws_response* response, double n_sigma, ws_plane** out)
 {
     if (!ctx || !out || !response) return set_err(WS_EINVAL, "null argument");
     *out = nullptr;
@@ -1123,9 +1258,14 @@ int ws_plane_create(ws_ctx* ctx, const ws_grid_spec* grid, const ws_response* re
     return WS_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
 int ws_plane_destroy(ws_plane* p)
 {
     if (!p) return WS_OK;
+    for (ws_plane* c : p->classes) ws_plane_destroy(c);
     cudaSetDevice(p->device);
     if (p->d_H) cudaFree(p->d_H);
     if (p->d_kern) cudaFree(p->d_kern);
@@ -1149,6 +1289,8 @@ int ws_plane_get_info(const ws_plane* p, ws_plane_info* info)
     info->support_wires = p->support_wires;
     info->lo_lag = p->lo_lag;
     info->n_lags = p->n_lags;
+    info->impacts_per_pitch = p->impacts;
+    info->n_response_classes = 1 + (int32_t)p->classes.size();
     return WS_OK;
 }
 
@@ -1206,23 +1348,23 @@ int event_device(ws_ctx* ctx, uint32_t n_planes, ws_plane* const* planes, const 
                  void* const* adcs, float* const* charges, ws_timing* timing)
 {
     std::vector<float*> ch(n_planes, nullptr);
+    std::vector<unsigned long long*> cnt(n_planes, nullptr);
     bool user_charge = false;
     if (charges)
-        for (uint32_t i = 0; i < n_planes; ++i) user_charge = user_charge || charges[i];
-    if (opt->fluctuate || user_charge) {
-        // fluctuation: the integer grid of the walk (internal unless the caller wants it)
+        for (uint32_t i = 0; i < n_planes; ++i) {
+            ch[i] = charges[i];
+            user_charge = user_charge || charges[i];
+        }
+    if (opt->fluctuate) {
+        // the walk's integer grids (u64 counts, internal; copied out in the
+        // caller's charge type when asked)
         size_t total = 0;
-        for (uint32_t i = 0; i < n_planes; ++i)
-            if (!(charges && charges[i])) total += (size_t)planes[i]->W * planes[i]->N;
-        if (opt->fluctuate) WS_CUDA(ctx->charges.reserve(total));
+        for (uint32_t i = 0; i < n_planes; ++i) total += (size_t)planes[i]->W * planes[i]->N;
+        WS_CUDA(ctx->counts.reserve(total));
         size_t off = 0;
         for (uint32_t i = 0; i < n_planes; ++i) {
-            if (charges && charges[i]) {
-                ch[i] = charges[i];
-            } else if (opt->fluctuate) {
-                ch[i] = ctx->charges.p + off;
-                off += (size_t)planes[i]->W * planes[i]->N;
-            }
+            cnt[i] = ctx->counts.p + off;
+            off += (size_t)planes[i]->W * planes[i]->N;
         }
     }
     const bool f64 = spec && spec->frame_type == WS_FRAME_F64;
@@ -1235,14 +1377,21 @@ int event_device(ws_ctx* ctx, uint32_t n_planes, ws_plane* const* planes, const 
         else fr[i] = static_cast<float*>(f);
         ad[i] = adcs ? adcs[i] : nullptr;
     }
-    for (uint32_t g = 0; g < n_planes; g += wsb::kMaxPlanes) {
-        const uint32_t n = std::min<uint32_t>(wsb::kMaxPlanes, n_planes - g);
+    for (uint32_t g = 0, n = 0; g < n_planes; g += n) {
+        // launch groups of at most kMaxPlanes plane descriptors (a plane with
+        // impact positions takes one per response class)
+        uint32_t slots = 0;
+        for (n = 0; g + n < n_planes; ++n) {
+            const uint32_t k = 1u + (uint32_t)planes[g + n]->classes.size();
+            if (n && slots + k > (uint32_t)wsb::kMaxPlanes) break;
+            slots += k;
+        }
         const Readout ro{spec, ad.data() + g, fr64.data() + g};
         bool any_charge = false;
         for (uint32_t i = g; i < g + n; ++i) any_charge = any_charge || ch[i];
         const int rc = run_group(ctx, n, planes + g, depos + g, n_depos + g, opt, fr.data() + g,
                                  any_charge ? ch.data() + g : nullptr, nullptr, g == 0 ? timing : nullptr,
-                                 spec ? &ro : nullptr, user_charge);
+                                 spec ? &ro : nullptr, opt->fluctuate ? cnt.data() + g : nullptr);
         if (rc) return rc;
     }
     return WS_OK;
@@ -1293,7 +1442,7 @@ int events_host(ws_ctx* ctx, uint32_t n_events, uint32_t n_planes, ws_plane* con
         };
         off_f[i] = put(want_f, frame_elem(spec));
         off_a[i] = put(want_a, adc_elem(spec));
-        off_c[i] = put(want_c, 4);
+        off_c[i] = put(want_c, opt->fluctuate && opt->charge_type == WS_CHARGE_I64 ? 8 : 4);
     }
     size_t max_units = 0;
     for (uint32_t e = 0; e < n_events; ++e) {
@@ -1348,8 +1497,9 @@ int events_host(ws_ctx* ctx, uint32_t n_events, uint32_t n_planes, ws_plane* con
                         WS_CUDA(cudaMemcpyAsync(adcs[k], da[i], cells * adc_elem(spec), cudaMemcpyDeviceToHost,
                                                 ctx->copy_stream));
                     if (dc[i])
-                        WS_CUDA(cudaMemcpyAsync(charges[k], dc[i], cells * 4, cudaMemcpyDeviceToHost,
-                                                ctx->copy_stream));
+                        WS_CUDA(cudaMemcpyAsync(charges[k], dc[i],
+                                                cells * (opt->fluctuate && opt->charge_type == WS_CHARGE_I64 ? 8 : 4),
+                                                cudaMemcpyDeviceToHost, ctx->copy_stream));
                 }
                 WS_CUDA(cudaEventRecord(ctx->slot_copied[slot], ctx->copy_stream));
                 return WS_OK;
@@ -1444,7 +1594,12 @@ int ws_rasterize_device(ws_plane* p, const ws_depo* depos, uint64_t n, const ws_
     const ws_depo* dp[1] = {depos};
     uint64_t nd[1] = {n};
     float* chs[1] = {charge};
-    return run_group(p->ctx, 1, planes, dp, nd, opt, nullptr, chs, nullptr, timing, nullptr, true);
+    unsigned long long* cnt[1] = {nullptr};
+    if (opt->fluctuate) {
+        WS_CUDA(p->ctx->counts.reserve((size_t)p->W * p->N));
+        cnt[0] = p->ctx->counts.p;
+    }
+    return run_group(p->ctx, 1, planes, dp, nd, opt, nullptr, chs, nullptr, timing, nullptr, cnt);
 }
 
 int ws_convolve_device(ws_plane* p, const float* charge, float* frame)

@@ -74,6 +74,12 @@ struct PlaneDesc {
     float kern_absmax;         // max |kernel tap| (rounded up)
     int32_t n_windows;         // direct: tick windows of kTileTicks per row band
     uint32_t direct_cap;       // direct: k_direct stages at most this many entries at a time
+    // impact positions (ws_plane_create_impacts): the wire pitch is split into
+    // `impacts` sub-bins; this plane (class) takes the charge of the sub-bins
+    // whose bit is set in imp_mask, normalised over all of them
+    int32_t impacts;           // 1 = the reference's wire binning (core.cpp:31-32)
+    uint32_t imp_mask;
+    int32_t stats_owner;       // counts clipped charge / patches (the first class of a plane only)
     // per call
     const ws_depo* depos;
     uint32_t n_units;
@@ -86,7 +92,7 @@ struct PlaneDesc {
     void* adc;                 // out: digitized codes, int32 or uint16 per EventDesc::adc_u16 (readout, nullable)
     float* charge_out;         // out: S (nullable)
     const float* charge_in;    // in: S (mode "grid")
-    uint32_t* charge_u32;      // fluctuation on: the integer charge grid (exact sums, mode 1 reads it)
+    unsigned long long* charge_cnt;  // fluctuation on: the integer charge grid (u64 counts, mode 1 reads it)
     long long* stats;          // [0] clipped_charge, [1] clipped_patches
     uint32_t* tile_need;       // fixed tile lists: the largest slot + 1 that did not fit (atomicMax, 0 = none)
 };

@@ -65,11 +65,24 @@ __global__ void k_noise_pairs(const NoiseArgs a)
     if (has1) sink_put(a.out, base + 1, a.noise ? __dadd_rn(v1, __dmul_rn(a.sigma, n1)) : v1);
 }
 
-// integer charge grid (fluctuation on) -> float32 in place
-__global__ void k_u32_to_f32(uint32_t* __restrict__ g, size_t n)
+// integer charge grid (fluctuation on, u64 counts) -> the caller's charge
+// output: float32 (type 0), uint32 (1; a count past 2^32 - 1 flags
+// kErrCellOvf) or int64 (2, the reference's ChargeGrid)
+__global__ void k_counts_out(const unsigned long long* __restrict__ g, void* out, int type, size_t n, unsigned* err)
 {
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-        reinterpret_cast<float*>(g)[i] = (float)g[i];
+    bool ovf = false;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const unsigned long long v = g[i];
+        if (type == 0) {
+            static_cast<float*>(out)[i] = (float)v;
+        } else if (type == 1) {
+            ovf |= v > 0xffffffffull;
+            static_cast<uint32_t*>(out)[i] = (uint32_t)v;
+        } else {
+            static_cast<long long*>(out)[i] = (long long)v;
+        }
+    }
+    if (__any_sync(0xffffffffu, ovf) && (threadIdx.x & 31) == 0) atomicOr(err, kErrCellOvf);
 }
 
 }  // namespace wsb
@@ -89,9 +102,10 @@ extern "C" cudaError_t wsb_launch_noise(const float* in, const wsb::Sink& out, i
     return cudaGetLastError();
 }
 
-extern "C" cudaError_t wsb_launch_u32_to_f32(uint32_t* g, size_t n, cudaStream_t s)
+extern "C" cudaError_t wsb_launch_counts_out(const unsigned long long* g, void* out, int type, size_t n, unsigned* err,
+                                             cudaStream_t s)
 {
     if (!n) return cudaSuccess;
-    wsb::k_u32_to_f32<<<(unsigned)std::min<size_t>((n + 255) / 256, 148 * 16), 256, 0, s>>>(g, n);
+    wsb::k_counts_out<<<(unsigned)std::min<size_t>((n + 255) / 256, 148 * 16), 256, 0, s>>>(g, out, type, n, err);
     return cudaGetLastError();
 }

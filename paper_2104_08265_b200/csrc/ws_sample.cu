@@ -112,6 +112,84 @@ __device__ __forceinline__ void bin_integrals_f32(double center, double sigma, d
     vmax = m;
 }
 
+// Wire-direction integrals at impact resolution (ws_plane_create_impacts):
+// the footprint's n_w wires are split into `imp` sub-bins each (impact i of
+// wire j spans [lo + (j imp + i) pitch / imp, + pitch / imp)), each sub-bin
+// the Gaussian's integral (gauss_bin_integrals' rule at the finer spacing;
+// sigma <= 0 puts the delta in its containing sub-bin). out[j] = the sum over
+// the sub-bins of wire j whose impact is in `mask` (this response class);
+// all4 = {sum, max} over the class's wires and {sum, max} over every
+// sub-bin (the normalisation and the emptiness test of sample_patch,
+// rasterize.cpp:101-118, run over all impacts). The sub-bin integrals of a
+// wire telescope to its wire-bin integral: with one class the result is the
+// reference's wire profile up to rounding.
+template <typename T, typename Put>
+__device__ __noinline__ void impact_integrals(double center, double sigma, double lo_edge, double pitch, int n_w, int imp,
+                                              uint32_t mask, Put&& put, double* all4)
+{
+    double sc = 0.0, mc = 0.0, sa = 0.0, ma = 0.0;
+    const int nk = n_w * imp;
+    const double sub = pitch / (double)imp;
+    if (sigma <= 0.0) {
+        long idx = (long)floor((center - lo_edge) / sub);
+        idx = idx < 0 ? 0 : (idx > nk - 1 ? nk - 1 : idx);
+        for (int j = 0; j < n_w; ++j) put(j, (T)0);
+        const bool in = (mask >> (idx % imp)) & 1u;
+        if (in) put((int)(idx / imp), (T)1);
+        sc = mc = in ? 1.0 : 0.0;
+        sa = ma = 1.0;
+    } else if constexpr (sizeof(T) == 8) {
+        const double inv = kInvSqrt2 / sigma;
+        double prev = erf((lo_edge - center) * inv);
+        for (int j = 0; j < n_w; ++j) {
+            double w = 0.0;
+            for (int i = 0; i < imp; ++i) {
+                const double next = erf((lo_edge + (double)(j * imp + i + 1) * sub - center) * inv);
+                const double v = 0.5 * (next - prev);
+                prev = next;
+                sa += v;
+                ma = v > ma ? v : ma;
+                if ((mask >> i) & 1u) w += v;
+            }
+            put(j, (T)w);
+            sc += w;
+            mc = w > mc ? w : mc;
+        }
+    } else {
+        // fp32 (fluctuation off): one erfcf per edge, each difference on the
+        // side of the centre where it does not cancel (bin_integrals_f32)
+        const double inv = kInvSqrt2 / sigma;
+        const float x0 = (float)((lo_edge - center) * inv), dx = (float)(sub * inv);
+        float xp = x0, cp = erfcf(fabsf(x0)), fi = 1.0f;
+        float fsa = 0.0f, fma = 0.0f, fsc = 0.0f, fmc = 0.0f;
+        for (int j = 0; j < n_w; ++j) {
+            float w = 0.0f;
+            for (int i = 0; i < imp; ++i, fi += 1.0f) {
+                const float xn = fmaf(fi, dx, x0);
+                const float cn = erfcf(fabsf(xn));
+                const float diff = xp >= 0.0f ? cp - cn : (xn <= 0.0f ? cn - cp : 2.0f - cn - cp);
+                const float v = 0.5f * diff;
+                fsa += v;
+                fma = fmaxf(fma, v);
+                if ((mask >> i) & 1u) w += v;
+                xp = xn;
+                cp = cn;
+            }
+            put(j, (T)w);
+            fsc += w;
+            fmc = fmaxf(fmc, w);
+        }
+        sc = fsc;
+        mc = fmc;
+        sa = fsa;
+        ma = fma;
+    }
+    all4[0] = sc;
+    all4[1] = mc;
+    all4[2] = sa;
+    all4[3] = ma;
+}
+
 // fp64 bin integrals out of line (fluctuation on, and narrow depos with it
 // off): their register demand stays out of the common fp32 path.
 // out = {sum_w, max_w, sum_t, max_t}
@@ -138,6 +216,31 @@ __device__ __noinline__ void sample_f64_ool(const ws_depo* d, double wire_edge, 
                                             double tick, int n_t, float* wv32, float* tv32, double* out)
 {
     sample_f64_body<false>(d, wire_edge, pitch, n_w, tick_edge, tick, n_t, nullptr, nullptr, wv32, tv32, out);
+}
+
+// Fluctuation-off sampling of a plane with impact positions (out of line):
+// the class's wire profile at impact resolution (fp32 for wide depos, fp64
+// for narrow ones, as the wire-binned path), the tick profile as usual.
+// out6 = {sum, max} of the class's wire profile, {sum, max} over all
+// impacts, {sum, max} of the tick profile.
+// (scalars only: a PlaneDesc reference would copy the kernel parameters to the stack)
+__device__ __noinline__ void sample_impacts_ool(const ws_depo* d, double pitch, double tick, int imp, uint32_t mask,
+                                                double wire_edge, double tick_edge, int n_w, int n_t, bool fast,
+                                                float* wv, float* tv, double* out6)
+{
+    double a4[4], st, mt;
+    if (fast) {
+        impact_integrals<float>(d->x, d->sigma_x, wire_edge, pitch, n_w, imp, mask, [&](int i, float v) { wv[i] = v; },
+                                a4);
+        bin_integrals_f32(d->t, d->sigma_t, tick_edge, tick, n_t, [&](int i, float v) { tv[i] = v; }, st, mt);
+    } else {
+        impact_integrals<double>(d->x, d->sigma_x, wire_edge, pitch, n_w, imp, mask,
+                                 [&](int i, double v) { wv[i] = (float)v; }, a4);
+        bin_integrals(d->t, d->sigma_t, tick_edge, tick, n_t, [&](int i, double v) { tv[i] = (float)v; }, st, mt);
+    }
+    for (int k = 0; k < 4; ++k) out6[k] = a4[k];
+    out6[4] = st;
+    out6[5] = mt;
 }
 
 // One thread per unit: footprint (map_depo_to_grid + clip), bin integrals
@@ -181,9 +284,9 @@ __global__ void __launch_bounds__(128, kFluct ? 1 : 8) k_sample(const EventDesc 
     }
     if (d.q < 0) atomicOr(err, kErrCharge);
     const Footprint f = footprint(P, d);
-    if (f.clipped) atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[1]), 1ULL);
+    if (f.clipped && P.stats_owner) atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[1]), 1ULL);
     if (f.empty) {
-        atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[0]), (unsigned long long)d.q);
+        if (P.stats_owner) atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[0]), (unsigned long long)d.q);
         recs[u] = rec;
         return;
     }
@@ -207,12 +310,24 @@ __global__ void __launch_bounds__(128, kFluct ? 1 : 8) k_sample(const EventDesc 
         double o4[4];
         off += off & 1u;  // 8-byte alignment
         double* wv = reinterpret_cast<double*>(pool + off);
-        sample_f64_body<true>(&d, wire_edge, P.pitch, f.n_w, tick_edge, P.tick, f.n_t, wv, wv + f.n_w, nullptr, nullptr,
-                              o4);
-        sw = o4[0];
-        mw = o4[1];
-        st = o4[2];
-        mt = o4[3];
+        if (P.impacts > 1) {
+            // one response class (the host allows fluctuation only then):
+            // the wire profile summed over the impact sub-bins
+            double a4[4];
+            impact_integrals<double>(d.x, d.sigma_x, wire_edge, P.pitch, f.n_w, P.impacts, P.imp_mask,
+                                     [&](int i, double v) { wv[i] = v; }, a4);
+            bin_integrals(d.t, d.sigma_t, tick_edge, P.tick, f.n_t, [&](int i, double v) { wv[f.n_w + i] = v; }, st,
+                          mt);
+            sw = a4[0];
+            mw = a4[1];
+        } else {
+            sample_f64_body<true>(&d, wire_edge, P.pitch, f.n_w, tick_edge, P.tick, f.n_t, wv, wv + f.n_w, nullptr,
+                                  nullptr, o4);
+            sw = o4[0];
+            mw = o4[1];
+            st = o4[2];
+            mt = o4[3];
+        }
     } else if (!(d.sigma_x * 4.0 >= P.pitch && d.sigma_t * 4.0 >= P.tick)) {
         double o4[4];
         float* raw = reinterpret_cast<float*>(pool + off);
@@ -230,7 +345,7 @@ __global__ void __launch_bounds__(128, kFluct ? 1 : 8) k_sample(const EventDesc 
     // sum_w sum_t wv*tv > 0  <=>  max(wv)*max(tv) > 0 (all terms >= 0, products monotone)
     if (!(mw * mt > 0.0)) {
         // numerically empty (rasterize.cpp:111-116) -> clipped charge (pipeline.cpp:339-340)
-        atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[0]), (unsigned long long)d.q);
+        if (P.stats_owner) atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[0]), (unsigned long long)d.q);
         recs[u] = rec;
         return;
     }
@@ -399,6 +514,9 @@ __device__ __forceinline__ void emit_tile_entries(const PlaneDesc& P, const Unit
 constexpr int kSampleThreads = 128;
 constexpr int kStageWarp = 32 * 52;  // staged profile words per warp
 
+// kImp: some plane of the call has impact positions (a separate
+// instantiation: the wire-binned hot path keeps its registers)
+template <bool kImp>
 __global__ void __launch_bounds__(kSampleThreads, 8)
 k_sample_off(const EventDesc ev, UnitRec* __restrict__ recs, uint32_t* __restrict__ pool, uint32_t pool_cap,
              uint32_t* __restrict__ pool_ctr, uint32_t* __restrict__ band_count, unsigned* __restrict__ err)
@@ -430,9 +548,9 @@ k_sample_off(const EventDesc ev, UnitRec* __restrict__ recs, uint32_t* __restric
     if (live) {
         if (d.q < 0) atomicOr(err, kErrCharge);
         f = footprint(P, d);
-        if (f.clipped) atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[1]), 1ULL);
+        if (f.clipped && P.stats_owner) atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[1]), 1ULL);
         if (f.empty) {
-            atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[0]), (unsigned long long)d.q);
+            if (P.stats_owner) atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[0]), (unsigned long long)d.q);
             live = false;
         }
     }
@@ -475,13 +593,24 @@ k_sample_off(const EventDesc ev, UnitRec* __restrict__ recs, uint32_t* __restric
     const bool staged = live && wex + words <= (uint32_t)kStageWarp;  // a prefix of the lanes
     float* stage = s_stage + warp * kStageWarp;
     double sw = 0.0, mw = 0.0, st = 0.0, mt = 0.0;
+    double sw_all = 0.0, mw_all = 0.0;  // over every impact (== sw, mw without impact positions)
     float* raw = reinterpret_cast<float*>(pool + off);
     if (live) {
         rec.goff = gneed ? gbase + gex + 4u : 0u;
         const double wire_edge = P.origin_x + ((double)f.w0 - (double)P.pad_w) * P.pitch;
         const double tick_edge = P.origin_t + ((double)f.t0 - (double)P.pad_t) * P.tick;
         float* dst = staged ? stage + wex : raw;
-        if (fast) {
+        if (kImp && P.impacts > 1) {
+            double o6[6];
+            sample_impacts_ool(&d, P.pitch, P.tick, P.impacts, P.imp_mask, wire_edge, tick_edge, f.n_w, f.n_t, fast, dst,
+                               dst + f.n_w + n_eff, o6);
+            sw = o6[0];
+            mw = o6[1];
+            sw_all = o6[2];
+            mw_all = o6[3];
+            st = o6[4];
+            mt = o6[5];
+        } else if (fast) {
             float* tv = dst + f.n_w + n_eff;
             bin_integrals_f32(d.x, d.sigma_x, wire_edge, P.pitch, f.n_w, [&](int i, float v) { dst[i] = v; }, sw,
                               mw);
@@ -493,6 +622,10 @@ k_sample_off(const EventDesc ev, UnitRec* __restrict__ recs, uint32_t* __restric
             mw = o4[1];
             st = o4[2];
             mt = o4[3];
+        }
+        if (!kImp || P.impacts == 1) {
+            sw_all = sw;
+            mw_all = mw;
         }
         if (n_eff) {
             float* eff = dst + f.n_w;
@@ -516,13 +649,16 @@ k_sample_off(const EventDesc ev, UnitRec* __restrict__ recs, uint32_t* __restric
     // sum_w sum_t wv*tv > 0  <=>  max(wv)*max(tv) > 0; numerically empty
     // (rasterize.cpp:111-116) -> clipped charge (pipeline.cpp:339-340)
     bool emit = live;
-    if (live && !(mw * mt > 0.0)) {
-        atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[0]), (unsigned long long)d.q);
+    if (live && !(mw_all * mt > 0.0)) {
+        if (P.stats_owner) atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats[0]), (unsigned long long)d.q);
         emit = false;
+    } else if (kImp && live && !(mw * mt > 0.0)) {
+        emit = false;  // impact positions: none of the depo's charge falls in this class's sub-bins
     }
     if (emit) {
-        // S = q * p = a * wv[w] * tv[t] with a = q / total (applied by the consumers)
-        rec.a = (float)((double)d.q / (sw * st));
+        // S = q * p = a * wv[w] * tv[t] with a = q / total (applied by the consumers);
+        // the total runs over every impact sub-bin
+        rec.a = (float)((double)d.q / (sw_all * st));
         rec.tsum = __double2float_ru(st);
         rec.w0 = f.w0;
         rec.t0 = f.t0;
@@ -647,18 +783,11 @@ __global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ rec
 }
 
 // Electron counts into the integer charge grid (the reference's ChargeGrid is
-// int64, core.hpp:94-99): u32 atomics, exact and order independent; a cell
-// past 2^32 - 1 electrons (or a single draw past it) flags kErrCellOvf, an
-// error of the call, never a silently wrapped sum.
-__device__ __forceinline__ void add_count(uint32_t* cell, int64_t k, unsigned* err)
+// int64, core.hpp:94-99): 64-bit reductions (fire and forget: the walk never
+// waits on them), exact and order independent.
+__device__ __forceinline__ void add_count(unsigned long long* cell, int64_t k)
 {
-    if (k <= 0) return;
-    if (k > 0xffffffffll) {
-        atomicOr(err, kErrCellOvf);
-        return;
-    }
-    const uint32_t old = atomicAdd(cell, (uint32_t)k);
-    if ((uint32_t)(old + (uint32_t)k) < old) atomicOr(err, kErrCellOvf);
+    if (k > 0) atomicAdd(cell, (unsigned long long)k);
 }
 
 // Fluctuation walk, one thread per unit: sample_patch's exact probabilities
@@ -686,7 +815,7 @@ __global__ void k_fluctuate(const EventDesc ev, const UnitRec* __restrict__ recs
     const double norm = 1.0 / total;
     Rng src;
     src.init(ev.rng_mode, ev.seed, (uint64_t)d.id);
-    uint32_t* grid = P.charge_u32;
+    unsigned long long* grid = P.charge_cnt;
     const int N = P.N;
     int64_t remaining = d.q;
     double p_rem = 1.0;
@@ -701,12 +830,12 @@ __global__ void k_fluctuate(const EventDesc ev, const UnitRec* __restrict__ recs
             p = p < 0.0 ? 0.0 : (p > 1.0 ? 1.0 : p);
         }
         const int64_t k = ev.approx ? binomial_approx(remaining, p, src) : binomial(remaining, p, src);
-        add_count(&grid[(size_t)(rec.w0 + w) * N + rec.t0 + t], k, ev.err);
+        add_count(&grid[(size_t)(rec.w0 + w) * N + rec.t0 + t], k);
         remaining -= k;
         p_rem -= pi;
     }
     if (remaining)
-        add_count(&grid[(size_t)(rec.w0 + n_w - 1) * N + rec.t0 + n_t - 1], remaining, ev.err);
+        add_count(&grid[(size_t)(rec.w0 + n_w - 1) * N + rec.t0 + n_t - 1], remaining);
 }
 
 // Exact fluctuation (fluctuate_sequential with the reference binomial), the
@@ -757,7 +886,7 @@ __global__ void __launch_bounds__(128) k_fluctuate_exact(const EventDesc ev, con
     }
     Rng src;
     src.init(ev.rng_mode, ev.seed, (uint64_t)d.id);
-    uint32_t* grid = P.charge_u32;
+    unsigned long long* grid = P.charge_cnt;
     const int N = P.N;
     const int last = rec.n_w * n_t - 1;
     int64_t remaining = d.q;
@@ -770,9 +899,9 @@ __global__ void __launch_bounds__(128) k_fluctuate_exact(const EventDesc ev, con
 
     // bin b = (bw, bt), tracked incrementally (no integer division per draw)
     int bw = 0, bt = 0;
-    uint32_t* cellp = grid + (size_t)rec.w0 * N + rec.t0;  // &grid[w0 + bw][t0 + bt]
+    unsigned long long* cellp = grid + (size_t)rec.w0 * N + rec.t0;  // &grid[w0 + bw][t0 + bt]
     auto commit = [&](int64_t k) {  // bin b drew k electrons
-        add_count(cellp, k, ev.err);
+        add_count(cellp, k);
         remaining -= k;
         p_rem -= pi;
         ++b;
@@ -789,7 +918,7 @@ __global__ void __launch_bounds__(128) k_fluctuate_exact(const EventDesc ev, con
         while (!done && !walking) {
             if (remaining == 0 || b >= last) {
                 if (remaining)  // the last bin takes the rest
-                    add_count(&grid[(size_t)(rec.w0 + rec.n_w - 1) * N + rec.t0 + n_t - 1], remaining, ev.err);
+                    add_count(&grid[(size_t)(rec.w0 + rec.n_w - 1) * N + rec.t0 + n_t - 1], remaining);
                 done = true;
                 break;
             }
@@ -892,9 +1021,11 @@ extern "C" cudaError_t wsb_launch_sample(const wsb::EventDesc& ev, wsb::UnitRec*
     } else {
         constexpr size_t smem = sizeof(float) * (wsb::kSampleThreads / 32) * wsb::kStageWarp;
         const unsigned grid = (ev.total_units + wsb::kSampleThreads - 1) / wsb::kSampleThreads;
+        bool imp = false;
+        for (int i = 0; i < ev.n_planes; ++i) imp = imp || ev.p[i].impacts > 1;
+        const auto kfn = imp ? wsb::k_sample_off<true> : wsb::k_sample_off<false>;
         if (!pdl) {
-            wsb::k_sample_off<<<grid, wsb::kSampleThreads, smem, s>>>(ev, recs, pool, pool_cap, pool_ctr, band_count,
-                                                                       err);
+            kfn<<<grid, wsb::kSampleThreads, smem, s>>>(ev, recs, pool, pool_cap, pool_ctr, band_count, err);
             return cudaGetLastError();
         }
         // programmatic launch behind the previous call's k_direct (footprints
@@ -909,7 +1040,7 @@ extern "C" cudaError_t wsb_launch_sample(const wsb::EventDesc& ev, wsb::UnitRec*
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        return cudaLaunchKernelEx(&cfg, wsb::k_sample_off, ev, recs, pool, pool_cap, pool_ctr, band_count, err);
+        return cudaLaunchKernelEx(&cfg, kfn, ev, recs, pool, pool_cap, pool_ctr, band_count, err);
     }
     return cudaGetLastError();
 }

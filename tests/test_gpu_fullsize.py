@@ -61,7 +61,7 @@ def test_c2_all_planes_vs_oracle(c2, path):
     for i, p in enumerate(planes):
         r = p.simulate(ev[i], SimConfig(fluctuate=False), want_charge=True)
         s_ref, clipped, _ = refs[i]
-        assert relL2_per_channel(r.charge, s_ref) < TOL_CHARGE
+        assert relL2_per_channel(r.charge, s_ref) < TOL_FRAME  # per cell: the fp32 path's tolerance
         q = float(ev[i]["q"].sum()) - clipped
         assert abs(float(r.charge.astype(np.float64).sum()) - q) <= TOL_CHARGE * q
     ctx.close()
@@ -81,7 +81,7 @@ def test_c3_full_event_fluctuation_exact(oracle):
         dd = torch.from_numpy(d.view(np.uint8).copy()).cuda()
         ch = torch.empty(p.shape, dtype=torch.int32, device="cuda")
         fr = torch.empty(p.shape, dtype=torch.float32, device="cuda")
-        p.simulate_device(dd, len(d), cfg, fr, ch, charge_u32=True)
+        p.simulate_device(dd, len(d), cfg, fr, ch, charge_type="u32")
         ctx.synchronize()
         got.append((ch.cpu().numpy().view(np.uint32).astype(np.int64), fr.cpu().numpy()))
 

@@ -145,7 +145,7 @@ def _fluct_u32(grid, resp, d, seed):
     dd = torch.from_numpy(d.view(np.uint8).copy()).cuda()
     ch = torch.empty(plane.shape, dtype=torch.int32, device="cuda")
     fr = torch.empty(plane.shape, dtype=torch.float32, device="cuda")
-    plane.simulate_device(dd, len(d), cfg, fr, ch, charge_u32=True)
+    plane.simulate_device(dd, len(d), cfg, fr, ch, charge_type="u32")
     ctx.synchronize()
     out = ch.cpu().numpy().view(np.uint32).astype(np.int64), fr.cpu().numpy()
     ctx.close()

@@ -223,3 +223,21 @@ def test_spec_ac1_ac5_conservation_and_mass(oracle):
                 ft = 0.5 * (erf((tl + 0.5 * (b + 1) - d["t"][i]) / (np.sqrt(2) * d["sigma_t"][i])) -
                             erf((tl + 0.5 * b - d["t"][i]) / (np.sqrt(2) * d["sigma_t"][i])))
                 assert abs(unnorm[a, b] - fx * ft) <= 1e-9
+
+
+def test_impact_restatement_pins_to_wire_binning(oracle):
+    """oracle.impact_charge (sampling at impact resolution, the checker of
+    ws_plane_create_impacts) with one class equals the oracle's wire binning,
+    which is pinned to the reference: the telescoping the degenerate case
+    relies on."""
+    from oracle.oracle import impact_charge
+    from paper_2104_08265_b200 import GridSpec
+    from paper_2104_08265_b200.workloads import line_tracks
+    from .helpers import oracle_grid
+    grid = GridSpec(n_wires=96, n_ticks=900, pad_wires=20, pad_ticks=100, pitch=5.0, tick=0.5)
+    d = line_tracks(300, grid, seed=5)
+    d["sigma_x"][:10] = 0.0  # delta depos: the containing sub-bin
+    (s,), clipped = impact_charge(oracle_grid(grid), d, 10, [(1 << 10) - 1])
+    s_ref, clipped_ref = oracle.charge_fluct_off(oracle_grid(grid), d)
+    assert clipped == clipped_ref
+    np.testing.assert_allclose(s, s_ref, rtol=0, atol=1e-9 * s_ref.max())
