@@ -218,6 +218,19 @@ def run_reference_arm(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def pipe_summary(kernel: str):
+    """North star: rasterization (k_sample_off's erfc + FMA work) as a fraction
+    of the FP32 / SFU (XU) peaks; % of peak over active cycles from the
+    committed ncu capture (inst-executed rates per pipe)."""
+    p = profile_facts(kernel).get("pipes") or {}
+    keys = {"fp32_fma": "inst_fma", "sfu_xu": "inst_xu", "fp64": "inst_fp64", "alu": "inst_alu", "lsu": "inst_lsu"}
+    out = {k: round(p[v] / 100.0, 4) for k, v in keys.items() if v in p}
+    if out:
+        out["kernel"] = kernel
+        out["source"] = profile_facts(kernel).get("source")
+    return out or None
+
+
 def profile_facts(kernel: str):
     """Per-launch counters of `kernel` from the committed ncu captures
     (profiles/traffic_<kernel>.json): DRAM bytes, warp instructions, pipes."""
@@ -380,7 +393,23 @@ C5_ROTATE = 8          # distinct events per size (rotating over the 64 of a ste
 C5_SIZES = (1_000, 10_000, 100_000, 1_000_000)
 
 
+C1_DEPOS = 10_000
+C1_IMPACTS = 10
+
+
+def c1_plane():
+    """configs[0]: one plane of 480 wires x 6000 ticks (pad 100/100, pitch 5 mm,
+    tick 0.5 us: 680 x 6200 padded), collection response."""
+    from paper_2104_08265_b200 import GridSpec, ResponseParams
+    return GridSpec(n_wires=480, n_ticks=6000, pad_wires=100, pad_ticks=100, pitch=5.0, tick=0.5), \
+        ResponseParams(plane_kind="collection")
+
+
 def workload_desc(args):
+    if args.workload == "c1":
+        return (f"single plane (configs[0]): {C1_DEPOS} line-track depos, 480 wires x 6000 ticks (680 x 6200 padded), "
+                f"{C1_IMPACTS} impacts/pitch (identical per-impact responses: the case the reference pins), "
+                f"fluct off")
     if args.workload == "c3":
         return ("microboone_event with fluctuation (configs[2]): 100k depos, U/V/W 2400/2400/3456 wires x 9600 "
                 "ticks, exact binomial walk on the shared Philox stream (seed 12345), field + electronics response "
@@ -430,6 +459,12 @@ def reference_sample(args, cores):
     from paper_2104_08265_b200.workloads import microboone_event, microboone_grids, protodune_event, protodune_specs
     if args.workload == "c3":
         return c3_reference(cores)
+    if args.workload == "c1":
+        from paper_2104_08265_b200.workloads import line_tracks
+        g, r = c1_plane()
+        t = cpu_reference_units([(g, r, line_tracks(C1_DEPOS, g, seed=1))] * 3, cores)
+        return C1_DEPOS / min(t), (f"the C1 plane (10k depos) through the unmodified reference at {cores} threads, "
+                                   f"best of 3; the reference bins per wire (the degenerate impact case)")
     if args.workload == "c4":
         specs = protodune_specs()
         plane_of, depos = protodune_event(C4_DEPOS, seed=1)
@@ -490,7 +525,15 @@ def run_sim(args, world, rank, local):
                     adc=AdcConfig(1.0, 2048.0, 12))
     # calls[r] = list of (planes, [host depo arrays]) for rotation slot r; one
     # step runs every call of one slot
-    if args.workload in ("event", "c3"):
+    if args.workload == "c1":
+        from paper_2104_08265_b200.workloads import line_tracks
+        g, r = c1_plane()
+        planes = [Plane(ctx, g, r, impacts_per_pitch=C1_IMPACTS)]
+        calls = [[(planes, [line_tracks(C1_DEPOS, g, seed=1000 * rank + e + 1)])] for e in range(N_EVENTS_ROTATE)]
+        scaling = "weak"
+        step_depos_all = world * C1_DEPOS
+        parallel = f"plane-sharded x{world}"
+    elif args.workload in ("event", "c3"):
         grids, resps = microboone_grids()
         planes = [Plane(ctx, g, r) for g, r in zip(grids, resps)]
         calls = [[(planes, ev)] for ev in make_events(rank)]
@@ -548,16 +591,33 @@ def run_sim(args, world, rank, local):
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clocks:
-        start.record(stream)
-        for i in range(args.steps):
-            step(i)
-        end.record(stream)
-        ctx.synchronize()
-        torch.cuda.synchronize()
+    if args.workload == "c1":
+        # the step's working set (5 MB of depos, 17 MB of frame) fits in L2:
+        # each step timed alone, L2 flushed (256 MB written) between steps
+        flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        with ClockSampler(local) as clocks:
+            for i in range(args.steps):
+                with torch.cuda.stream(stream):
+                    flush.fill_(float(i))
+                evs[i][0].record(stream)
+                step(i)
+                evs[i][1].record(stream)
+            ctx.synchronize()
+            torch.cuda.synchronize()
+        ms_local = sum(a.elapsed_time(b) for a, b in evs)
+    else:
+        with ClockSampler(local) as clocks:
+            start.record(stream)
+            for i in range(args.steps):
+                step(i)
+            end.record(stream)
+            ctx.synchronize()
+            torch.cuda.synchronize()
+        ms_local = start.elapsed_time(end)
     barrier()
     gpu_launches = ctx.launch_count - launches0
-    ms = max_over_ranks(start.elapsed_time(end))
+    ms = max_over_ranks(ms_local)
     ms_per_step = ms / args.steps
     value = step_depos_all * args.steps / (ms * 1e-3)
     clk = clocks.summary()
@@ -601,7 +661,7 @@ def run_sim(args, world, rank, local):
                     row.append(t.numpy().view(d.dtype))
                 host_events.append(row)
         per_step = len(calls[0])
-        k_e2e = max(3, min(args.steps, 20)) if args.workload in ("event", "c3") else max(1, min(args.steps, 3))
+        k_e2e = max(3, min(args.steps, 20)) if args.workload in ("event", "c3", "c1") else max(1, min(args.steps, 3))
         batch = [host_events[i % len(host_events)] for i in range(k_e2e * per_step)]
         adc_bufs = [[torch.empty(p.shape, dtype=torch.uint16).pin_memory().numpy() for p in slot_planes]
                     for _ in range(2)]
@@ -641,8 +701,8 @@ def run_sim(args, world, rank, local):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         if args.workload == "event":
             cpu = cpu_baseline_event([calls[0][0][1]], cores)
-        elif args.workload == "c3":
-            v, sample = c3_reference(cores)
+        elif args.workload in ("c3", "c1"):
+            v, sample = reference_sample(args, cores)
             cpu = {"value": v, "unit": "depos/s", "cores": cores, "kind": "reference", "sample": sample}
         else:
             v, sample = reference_sample(args, cores)
@@ -653,7 +713,7 @@ def run_sim(args, world, rank, local):
             "metric": "depositions_per_sec", "value": value, "unit": "depos/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (straight line tracks, fixed seeds)",
-            "config": {"workload": workload_desc(args), "events_per_sec": None if args.workload == "c4" else
+            "config": {"workload": workload_desc(args), "events_per_sec": None if args.workload in ("c4", "c1") else
                        (world if args.workload in ("event", "c3") else C5_EVENTS) * 1e3 / ms_per_step,
                        "depos_per_step": step_depos_all, "cells_per_call": call_cells,
                        "l2": "inputs rotate over distinct events (> 126 MB L2); every step writes the frames",
@@ -666,11 +726,11 @@ def run_sim(args, world, rank, local):
                          "frac": achieved / peak, "traffic": facts.get("dram_bytes_per_launch"),
                          "kernel": conv_kernel, "kernel_ms": conv_ms, "algorithmic_bytes": alg_bytes,
                          "peak_kind": peak_kind, "binding": binding,
-                         "raster_pipes": profile_facts("k_sample_off").get("pipes")},
+                         "raster_pipes": pipe_summary("k_sample_off")},
             "fluctuation": None if args.workload != "c3" else {
                 "kernel": "k_fluctuate_exact", "stage_ms": float(stage.fluctuate_ms),
                 "share_of_event": float(stage.fluctuate_ms) / float(stage.total_ms),
-                "pipes": profile_facts("k_fluctuate_exact").get("pipes")},
+                "pipes": pipe_summary("k_fluctuate_exact")},
             "clocks": clk,
             "gpu_launches": gpu_launches,
             "e2e": e2e,
@@ -690,8 +750,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="event", choices=["event", "sigproc", "c3", "c4", "c5"],
-                    help="event: the headline metric (configs[1]); c3: configs[2]; c4: configs[3]; c5: configs[4]; "
+    ap.add_argument("--workload", default="event", choices=["event", "sigproc", "c1", "c3", "c4", "c5"],
+                    help="event: the headline metric (configs[1]); c1: configs[0] (10 impacts/pitch); c3: configs[2]; "
+                         "c4: configs[3]; c5: configs[4]; "
                          "sigproc: the Listing 1 chain (§8(f))")
     ap.add_argument("--depos", type=int, default=100_000, help="c5: depositions per event (1k-1M sweep)")
     args = ap.parse_args()

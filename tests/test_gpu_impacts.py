@@ -70,7 +70,7 @@ def test_c1_impacts_charge_and_fluctuation(ctx, c1_ref, oracle):
 
 def _two_class_responses():
     a = ResponseParams(plane_kind="induction", field_sigma_t=1.0, wire_weights=(0.1, 1.0, 0.1))
-    b = ResponseParams(plane_kind="induction", field_sigma_t=1.3, wire_weights=(0.25, 1.0, 0.25))
+    b = ResponseParams(plane_kind="induction", field_sigma_t=1.1, wire_weights=(0.25, 1.0, 0.25))
     return [a, b, b, a], (0b1001, 0b0110), (a, b)  # edges vs centre of the pitch
 
 

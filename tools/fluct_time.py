@@ -1,4 +1,5 @@
 """Device time of the MicroBooNE event with fluctuation on (C3: Philox, shaper on)."""
+import sys, pathlib; sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[1]))
 import numpy as np
 import torch
 from paper_2104_08265_b200 import Context, Plane, RngConfig, SimConfig, simulate_event_device
