@@ -154,6 +154,7 @@ struct ws_ctx {
     DevBuf<ws_depo> depos;
     DevBuf<float> frames, charges, ro_scratch;
     DevBuf<unsigned long long> counts;  // fluctuation on: the integer charge grids (u64 counts)
+    DevBuf<double> recip;               // RN(1/j), j < kRecipN: the exact walk's divisions
     DevBuf<unsigned char> out_stage;  // ws_run_*: device staging of the readout outputs (ADC / fp64 frames)
     DevBuf<double> noise_amp;  // spectrum-mode amplitudes of the last ws_noise_digitize_device
     ScratchHeader* host_slots = nullptr;  // pinned, kStatSlots
@@ -682,6 +683,14 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
     }
     if (timing) WS_CUDA(cudaEventRecord(pc.ev[1], s));  // stage timing only
     if (ev.fluctuate && !from_grid) {
+        if (!c->recip.p) {
+            std::vector<double> r(wsb::kRecipN);
+            r[0] = 0.0;
+            for (int j = 1; j < wsb::kRecipN; ++j) r[j] = 1.0 / (double)j;  // IEEE division: RN(1/j)
+            WS_CUDA(c->recip.reserve(r.size()));
+            WS_CUDA(cudaMemcpy(c->recip.p, r.data(), sizeof(double) * r.size(), cudaMemcpyHostToDevice));
+        }
+        ev.recip = c->recip.p;
         WS_CUDA(wsb_launch_fluctuate(ev, c->recs.p, c->pool.p, nullptr, s));
         c->launches += units ? (ev.approx ? 1 : 2) : 0;  // exact: key kernel + walk (the CUB sort between is library code)
     }
@@ -951,6 +960,7 @@ int ws_ctx_destroy(ws_ctx* c)
     c->frames.release();
     c->charges.release();
     c->counts.release();
+    c->recip.release();
     c->ro_scratch.release();
     c->out_stage.release();
     c->noise_amp.release();

@@ -26,6 +26,7 @@ constexpr int kTileTicks = 2048;
 constexpr int kSegShiftD = 6;        // direct path fixed-point bounds per 64-tick segment
 constexpr int kSegs = kTileTicks >> kSegShiftD;
 constexpr double kFixScale = 4294967296.0;          // 2^32: fixed-point electrons
+constexpr int kRecipN = 16384;                      // reciprocal table of the exact fluctuation walk
 constexpr double kFixInv = 1.0 / 4294967296.0;
 
 // Per-unit footprint record written by the sample kernel.
@@ -117,6 +118,7 @@ struct EventDesc {
     uint32_t* tile_count;
     uint32_t* list_need;       // CSR lists: the entry total when it exceeded list_cap (k_fill_bands)
     unsigned* err;             // the call's error flags
+    const double* recip;       // recip[j] = RN(1 / j), j < kRecipN (the exact walk's divisions, ws_sample.cu)
     // readout fused into the frame-store epilogues (add_noise + digitize,
     // spectral.cpp:177-196, 228-238): ro = 0 -> plain fp32 frame stores
     int32_t ro;

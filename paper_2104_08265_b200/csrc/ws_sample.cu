@@ -782,6 +782,25 @@ __global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ rec
                             [&](uint32_t b, uint32_t slot, const TEnt& e) { tlist[off[b] + slot] = e; });
 }
 
+// RN(t / d) for the walk's pmf recursion (rng.cpp:165-168: pmf *= odds * (n -
+// k) / (k + 1)), d = k + 1 an integer: with y = RN(1/d) from a table, q =
+// RN(t y) is within one ulp of t/d, the residual r = t - q d is exact (one
+// FMA), and RN(q + r y) is the correctly rounded quotient (Markstein's
+// theorem, round-to-nearest, no under/overflow: t is a moderate odds ratio
+// times n - k). Three dependent fp64 operations instead of the IEEE division
+// sequence; the same bits as the reference's division (checked on the full
+// configs[2] event, tests/test_gpu_fullsize.py). Larger d: the division.
+__device__ __forceinline__ double div_rn(double t, double d, const double* __restrict__ recip)
+{
+    if (d < (double)kRecipN) {
+        const double y = __ldg(&recip[(int)d]);
+        const double q = __dmul_rn(t, y);
+        const double r = __fma_rn(-q, d, t);
+        return __fma_rn(r, y, q);
+    }
+    return __ddiv_rn(t, d);
+}
+
 // Electron counts into the integer charge grid (the reference's ChargeGrid is
 // int64, core.hpp:94-99): 64-bit reductions (fire and forget: the walk never
 // waits on them), exact and order independent.
@@ -990,7 +1009,7 @@ __global__ void __launch_bounds__(128) k_fluctuate_exact(const EventDesc ev, con
 #pragma unroll 1
         for (;;) {
             if (walking) {
-                pmf = __dmul_rn(pmf, __ddiv_rn(__dmul_rn(odds, nk), k1));
+                pmf = __dmul_rn(pmf, div_rn(__dmul_rn(odds, nk), k1, ev.recip));
                 kd += 1.0;
                 cdf = __dadd_rn(cdf, pmf);
                 nk -= 1.0;

@@ -190,18 +190,32 @@ def test_fluctuation_extreme_depo_charge(oracle):
     assert relL2_per_channel(m, m_ref) < 1e-5
 
 
-def test_fluctuation_cell_overflow_is_an_error():
-    """A cell past 2^32 - 1 electrons is an error, never a wrapped sum."""
+def test_fluctuation_charge_types_past_2_32():
+    """The count grid is u64 (the reference's is int64): 4 delta depos of 3e10
+    electrons on one cell sum exactly; the int64 charge output carries it,
+    the uint32 output is an error (never a wrapped count)."""
+    import torch
+    from paper_2104_08265_b200 import RngConfig
     grid = GridSpec(n_wires=20, n_ticks=300, pad_wires=10, pad_ticks=100)
     resp = ResponseParams()
     d = line_tracks(4, grid, seed=3)
     d["q"] = np.int64(30_000_000_000)
     d["sigma_t"] = 0.0
-    d["sigma_x"] = 0.0  # one cell takes all 3e10 electrons of each depo
-    from paper_2104_08265_b200 import RngConfig
+    d["sigma_x"] = 0.0
+    d["x"], d["t"] = 50.0, 75.0  # one cell takes all 1.2e11 electrons
+    cfg = SimConfig(grid=grid, response=resp, fluctuate=True, rng=RngConfig(mode="philox"))
     ctx = Context(0)
+    plane = Plane(ctx, grid, resp)
+    dd = torch.from_numpy(d.view(np.uint8).copy()).cuda()
+    fr = torch.empty(plane.shape, dtype=torch.float32, device="cuda")
+    ch64 = torch.zeros(plane.shape, dtype=torch.int64, device="cuda")
+    plane.simulate_device(dd, len(d), cfg, fr, ch64, charge_type="i64")
+    ctx.synchronize()
+    c = ch64.cpu().numpy()
+    assert c.max() == 120_000_000_000 and c.sum() == 120_000_000_000
+    ch32 = torch.zeros(plane.shape, dtype=torch.int32, device="cuda")
+    plane.simulate_device(dd, len(d), cfg, fr, ch32, charge_type="u32")
     with pytest.raises(WsError) as e:
-        Plane(ctx, grid, resp).simulate(d, SimConfig(grid=grid, response=resp, fluctuate=True,
-                                                     rng=RngConfig(mode="philox")))
+        ctx.synchronize()
     assert e.value.code == 4 and "4294967295" in str(e.value)
     ctx.close()
