@@ -691,6 +691,11 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
             WS_CUDA(cudaMemcpy(c->recip.p, r.data(), sizeof(double) * r.size(), cudaMemcpyHostToDevice));
         }
         ev.recip = c->recip.p;
+        static const int quorum = [] {
+            const char* v = getenv("WS_FLUCT_QUORUM");  // tuning only
+            return v ? std::max(1, std::min(16, atoi(v))) : 6;
+        }();
+        ev.fl_quorum = quorum;
         WS_CUDA(wsb_launch_fluctuate(ev, c->recs.p, c->pool.p, nullptr, s));
         c->launches += units ? (ev.approx ? 1 : 2) : 0;  // exact: key kernel + walk (the CUB sort between is library code)
     }

@@ -119,6 +119,7 @@ struct EventDesc {
     uint32_t* list_need;       // CSR lists: the entry total when it exceeded list_cap (k_fill_bands)
     unsigned* err;             // the call's error flags
     const double* recip;       // recip[j] = RN(1 / j), j < kRecipN (the exact walk's divisions, ws_sample.cu)
+    int32_t fl_quorum;         // exact walk: set up new draws once this many 16ths of the live lanes are idle
     // readout fused into the frame-store epilogues (add_noise + digitize,
     // spectral.cpp:177-196, 228-238): ro = 0 -> plain fp32 frame stores
     int32_t ro;

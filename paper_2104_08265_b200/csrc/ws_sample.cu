@@ -790,15 +790,11 @@ __global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ rec
 // times n - k). Three dependent fp64 operations instead of the IEEE division
 // sequence; the same bits as the reference's division (checked on the full
 // configs[2] event, tests/test_gpu_fullsize.py). Larger d: the division.
-__device__ __forceinline__ double div_rn(double t, double d, const double* __restrict__ recip)
+__device__ __forceinline__ double div_rn_y(double t, double d, double y)
 {
-    if (d < (double)kRecipN) {
-        const double y = __ldg(&recip[(int)d]);
-        const double q = __dmul_rn(t, y);
-        const double r = __fma_rn(-q, d, t);
-        return __fma_rn(r, y, q);
-    }
-    return __ddiv_rn(t, d);
+    const double q = __dmul_rn(t, y);
+    const double r = __fma_rn(-q, d, t);
+    return __fma_rn(r, y, q);
 }
 
 // Electron counts into the integer charge grid (the reference's ChargeGrid is
@@ -915,6 +911,7 @@ __global__ void __launch_bounds__(128) k_fluctuate_exact(const EventDesc ev, con
     bool walking = false, flip = false;
     int64_t n = 0;
     double odds = 0.0, pmf = 0.0, cdf = 0.0, uu = 0.0, kd = 0.0, nd = 0.0, nk = 0.0, k1 = 0.0;
+    int kr = 0;
 
     // bin b = (bw, bt), tracked incrementally (no integer division per draw)
     int bw = 0, bt = 0;
@@ -994,6 +991,7 @@ __global__ void __launch_bounds__(128) k_fluctuate_exact(const EventDesc ev, con
                 nd = (double)n;
                 nk = (double)(n - k);  // exact integers below 2^53: the reference's casts
                 k1 = (double)(k + 1);
+                kr = k + 1 < (int64_t)kRecipN ? (int)(k + 1) : kRecipN;  // table index of the next divisor
             } else {
                 commit(flip ? n - k : k);
             }
@@ -1005,16 +1003,45 @@ __global__ void __launch_bounds__(128) k_fluctuate_exact(const EventDesc ev, con
         setup();
         const unsigned alive = __ballot_sync(0xffffffffu, !done);
         if (!alive) break;
-        const int quorum = max(1, __popc(alive) >> 1);  // half the live lanes idle: set up together
+        const int quorum = max(1, (__popc(alive) * ev.fl_quorum) >> 4);  // this share of the live lanes idle: set up together
 #pragma unroll 1
         for (;;) {
             if (walking) {
-                pmf = __dmul_rn(pmf, div_rn(__dmul_rn(odds, nk), k1, ev.recip));
-                kd += 1.0;
-                cdf = __dadd_rn(cdf, pmf);
-                nk -= 1.0;
-                k1 += 1.0;
-                if (!(cdf <= uu && kd < nd)) {
+                // kWalk CDF steps per iteration. The recursion factor
+                // f_i = RN(RN(odds (n - k - i)) / (k + i + 1)) does not depend
+                // on the pmf: the kWalk factors are independent (pipelined),
+                // and only pmf *= f, cdf += pmf and the stop test (the
+                // reference's loop condition, evaluated after every step)
+                // form the serial chain. Steps past the stop are discarded.
+                constexpr int kWalk = 4;
+                double f[kWalk];
+                if (kr + kWalk <= kRecipN) {  // divisors k + 1 .. k + kWalk from the table
+#pragma unroll
+                    for (int i = 0; i < kWalk; ++i)
+                        f[i] = div_rn_y(__dmul_rn(odds, nk - (double)i), k1 + (double)i, __ldg(&ev.recip[kr + i]));
+                } else {
+#pragma unroll
+                    for (int i = 0; i < kWalk; ++i) f[i] = __ddiv_rn(__dmul_rn(odds, nk - (double)i), k1 + (double)i);
+                }
+                double p = pmf, c = cdf, kk = kd;
+                bool go = true;
+#pragma unroll
+                for (int i = 0; i < kWalk; ++i) {
+                    if (go) {
+                        p = __dmul_rn(p, f[i]);
+                        c = __dadd_rn(c, p);
+                        kk += 1.0;
+                        go = c <= uu && kk < nd;
+                    }
+                }
+                const double adv = kk - kd;
+                pmf = p;
+                cdf = c;
+                kd = kk;
+                nk -= adv;
+                k1 += adv;
+                kr += (int)adv;
+                if (!go) {
                     walking = false;
                     const int64_t k = (int64_t)kd;
                     commit(flip ? n - k : k);
