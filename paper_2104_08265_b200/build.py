@@ -28,7 +28,6 @@ SOURCES = {
     "ws_sample.cu": ["--fmad=false"],
     "ws_conv.cu": [],
     "ws_direct.cu": [],
-    "ws_direct_mma.cu": [],
     "ws_gprof.cu": [],
     "ws_gprof_umma.cu": [],
     "ws_noise.cu": ["--fmad=false"],

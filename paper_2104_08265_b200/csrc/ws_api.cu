@@ -42,8 +42,6 @@ extern "C" size_t wsb_direct_smem(int cap);
 extern "C" int wsb_direct_cap();
 extern "C" cudaError_t wsb_launch_direct(const EventDesc& ev, const uint32_t* pool, const uint32_t* band_off,
                                          const wsb::TEnt* tlist, size_t smem_bytes, cudaStream_t stream, int pdl);
-extern "C" cudaError_t wsb_launch_direct_mma(const EventDesc& ev, const uint32_t* pool, const uint32_t* band_off,
-                                             const wsb::TEnt* tlist, cudaStream_t stream, int pdl);
 extern "C" cudaError_t wsb_launch_fluctuate(const EventDesc& ev, const UnitRec* recs, const uint32_t* pool,
                                             const uint32_t* order, cudaStream_t s);
 extern "C" size_t wsb_sigproc_smem(int n);
@@ -752,17 +750,8 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
             // releases its dependents at its start, before it has consumed
             // (and zeroed) the tile counts this launch reads.
             const int pdl = ev.tile_cap != 0 && !(ev.mode == 0 && charges) && direct_units > 0 ? 1 : 0;
-            // tensor-core tiles (ws_direct_mma.cu) by default; WS_DIRECT_MMA=0
-            // selects the shared-memory-atomic kernel (ws_direct.cu)
-            static const bool mma = [] {
-                const char* v = getenv("WS_DIRECT_MMA");
-                return !(v && v[0] == '0');
-            }();
-            if (mma)
-                WS_CUDA(wsb_launch_direct_mma(ev, c->pool.p, c->band_off.p, c->tile_list.p, s, pdl));
-            else
-                WS_CUDA(wsb_launch_direct(ev, c->pool.p, c->band_off.p, c->tile_list.p,
-                                          wsb_direct_smem(wsb_direct_cap()), s, pdl));
+            WS_CUDA(wsb_launch_direct(ev, c->pool.p, c->band_off.p, c->tile_list.p, wsb_direct_smem(wsb_direct_cap()),
+                                      s, pdl));
             c->launches += bands ? 1 : 0;
         }
         if (any_fft) {
