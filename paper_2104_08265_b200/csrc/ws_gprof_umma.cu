@@ -301,5 +301,4 @@ extern "C" cudaError_t wsb_launch_gprof_umma(const wsb::EventDesc& ev, const wsb
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, wsb::k_gprof_umma, ev, recs, pool, N);
-    return cudaGetLastError();
 }
