@@ -115,6 +115,7 @@ struct ScratchHeader {
     uint32_t pad;
     long long stats[2 * wsb::kMaxPlanes];
     uint32_t tile_need[wsb::kMaxPlanes];
+    unsigned long long fl_ctr;  // exact walk: draw records allocated (the need after a kErrFluct)
 };
 
 struct PendingCall {
@@ -155,6 +156,8 @@ struct ws_ctx {
     DevBuf<float> frames, charges, ro_scratch;
     DevBuf<unsigned long long> counts;  // fluctuation on: the integer charge grids (u64 counts)
     DevBuf<double> recip;               // RN(1/j), j < kRecipN: the exact walk's divisions
+    DevBuf<double> fl_bins;             // exact walk: per-bin draw records (32 B each, ws_sample.cu FlRec)
+    size_t fl_hint = 0;                 // records needed by the last overflowing call
     DevBuf<unsigned char> out_stage;  // ws_run_*: device staging of the readout outputs (ADC / fp64 frames)
     DevBuf<double> noise_amp;  // spectrum-mode amplitudes of the last ws_noise_digitize_device
     ScratchHeader* host_slots = nullptr;  // pinned, kStatSlots
@@ -696,8 +699,16 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
             return v ? std::max(1, std::min(16, atoi(v))) : 6;
         }();
         ev.fl_quorum = quorum;
+        if (!ev.approx) {
+            // one record per drawn bin; the need is known after an overflow
+            const size_t recs_need = std::max<size_t>(c->fl_hint, (size_t)units * 160 + 4096);
+            WS_CUDA(c->fl_bins.reserve(4 * recs_need));  // 32-byte records
+            ev.fl_bins = c->fl_bins.p;
+            ev.fl_cap = c->fl_bins.cap / 4;
+            ev.fl_ctr = &hdr->fl_ctr;
+        }
         WS_CUDA(wsb_launch_fluctuate(ev, c->recs.p, c->pool.p, nullptr, s));
-        c->launches += units ? (ev.approx ? 1 : 2) : 0;  // exact: key kernel + walk (the CUB sort between is library code)
+        c->launches += units ? (ev.approx ? 1 : 4) : 0;  // exact: keys, records, walk, normal-branch units (the CUB sort is library code)
     }
     if (timing) WS_CUDA(cudaEventRecord(pc.ev[2], s));  // stage timing only
     if (ev.mode == 0) {
@@ -831,6 +842,9 @@ int finish_pending(ws_ctx* c)
                          h.pool_ctr);
             }
         }
+        // fluctuation records beyond the buffer: those units took the one-pass
+        // walk (complete result); the next call gets room for all of them
+        if (h.err & wsb::kErrFluct) c->fl_hint = std::max<size_t>(c->fl_hint, (size_t)h.fl_ctr + 4096);
         if (h.err & wsb::kErrTileCap) {
             // the real per-tile counts: size the fixed lists from them, or
             // (beyond the budget) take exact-size CSR lists; under AUTO the
@@ -966,6 +980,7 @@ int ws_ctx_destroy(ws_ctx* c)
     c->charges.release();
     c->counts.release();
     c->recip.release();
+    c->fl_bins.release();
     c->ro_scratch.release();
     c->out_stage.release();
     c->noise_amp.release();

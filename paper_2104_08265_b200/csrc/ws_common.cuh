@@ -120,6 +120,12 @@ struct EventDesc {
     unsigned* err;             // the call's error flags
     const double* recip;       // recip[j] = RN(1 / j), j < kRecipN (the exact walk's divisions, ws_sample.cu)
     int32_t fl_quorum;         // exact walk: set up new draws once this many 16ths of the live lanes are idle
+    // exact walk, per-bin draw records (k_fluct_prep -> k_fluct_walk, 32 B:
+    // ws_sample.cu FlRec), allocated from fl_ctr; more than fl_cap ->
+    // kErrFluct: those units take the one-pass walk, the host grows the buffer
+    double* fl_bins;
+    unsigned long long fl_cap;
+    unsigned long long* fl_ctr;
     // readout fused into the frame-store epilogues (add_noise + digitize,
     // spectral.cpp:177-196, 228-238): ro = 0 -> plain fp32 frame stores
     int32_t ro;
@@ -133,7 +139,7 @@ struct EventDesc {
 
 // Error / overflow flags shared by kernels (device scalar words).
 enum : unsigned { kErrPool = 1u, kErrDomain = 2u, kErrCharge = 4u, kErrRange = 8u, kErrTileCap = 16u,
-                  kErrCellOvf = 32u };
+                  kErrCellOvf = 32u, kErrFluct = 64u };
 
 __device__ __forceinline__ int band_plane(const EventDesc& ev, uint32_t gb)
 {
@@ -316,10 +322,10 @@ struct Rng {
     }
 
     // Philox4x32-10; draw i -> ctr (i>>1, id lo, id hi, 0), words 2(i&1), 2(i&1)+1.
-    __device__ __forceinline__ uint64_t next_philox()
+    // philox_block: both draws of block j (draws 2j, 2j + 1).
+    __device__ __forceinline__ void philox_block(uint32_t j, uint64_t& w01, uint64_t& w23) const
     {
-        const uint32_t i = draw++;
-        uint32_t c0 = i >> 1, c1 = id0, c2 = id1, c3 = 0u;
+        uint32_t c0 = j, c1 = id0, c2 = id1, c3 = 0u;
         uint32_t k0 = key0, k1 = key1;
 #pragma unroll
         for (int r = 0; r < 10; ++r) {
@@ -330,7 +336,15 @@ struct Rng {
             k0 += 0x9E3779B9u;
             k1 += 0xBB67AE85u;
         }
-        return (i & 1u) ? ((uint64_t)c2 << 32 | c3) : ((uint64_t)c0 << 32 | c1);
+        w01 = (uint64_t)c0 << 32 | c1;
+        w23 = (uint64_t)c2 << 32 | c3;
+    }
+    __device__ __forceinline__ uint64_t next_philox()
+    {
+        const uint32_t i = draw++;
+        uint64_t a, b;
+        philox_block(i >> 1, a, b);
+        return (i & 1u) ? b : a;
     }
 
     // uniform01 (rng.cpp:51-54)

@@ -7,6 +7,8 @@
 // reproduces its integer draws.
 #include "ws_common.cuh"
 
+#include <algorithm>
+
 #include <cub/device/device_radix_sort.cuh>
 
 namespace wsb {
@@ -790,6 +792,7 @@ __global__ void k_fill_bands(const EventDesc ev, const UnitRec* __restrict__ rec
 // times n - k). Three dependent fp64 operations instead of the IEEE division
 // sequence; the same bits as the reference's division (checked on the full
 // configs[2] event, tests/test_gpu_fullsize.py). Larger d: the division.
+constexpr double kMarksteinMin = 0x1p-900;  // t >= this: q and the residual stay normal
 __device__ __forceinline__ double div_rn_y(double t, double d, double y)
 {
     const double q = __dmul_rn(t, y);
@@ -874,12 +877,14 @@ __global__ void k_fluct_keys(const EventDesc ev, const UnitRec* __restrict__ rec
     vals[u] = u;
 }
 
+// n_list (nullable): the number of entries of `order` (device), else total_units
 __global__ void __launch_bounds__(128) k_fluctuate_exact(const EventDesc ev, const UnitRec* __restrict__ recs,
                                                           const uint32_t* __restrict__ pool,
-                                                          const uint32_t* __restrict__ order)
+                                                          const uint32_t* __restrict__ order,
+                                                          const uint32_t* __restrict__ n_list)
 {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    bool done = i >= ev.total_units;
+    bool done = i >= (n_list ? *n_list : ev.total_units);
     const uint32_t u = done ? 0u : (order ? order[i] : i);
     UnitRec rec{};
     if (!done) rec = recs[u];
@@ -991,7 +996,9 @@ __global__ void __launch_bounds__(128) k_fluctuate_exact(const EventDesc ev, con
                 nd = (double)n;
                 nk = (double)(n - k);  // exact integers below 2^53: the reference's casts
                 k1 = (double)(k + 1);
-                kr = k + 1 < (int64_t)kRecipN ? (int)(k + 1) : kRecipN;  // table index of the next divisor
+                // table index of the next divisor; tiny odds (t = odds (n - k)
+                // near the subnormal range) keep the IEEE division
+                kr = k + 1 < (int64_t)kRecipN && odds >= kMarksteinMin ? (int)(k + 1) : kRecipN;
             } else {
                 commit(flip ? n - k : k);
             }
@@ -1045,6 +1052,360 @@ __global__ void __launch_bounds__(128) k_fluctuate_exact(const EventDesc ev, con
                     walking = false;
                     const int64_t k = (int64_t)kd;
                     commit(flip ? n - k : k);
+                }
+            }
+            const unsigned wk = __ballot_sync(0xffffffffu, walking);
+            if (wk == 0 || __popc(alive & ~wk) >= quorum) break;
+        }
+    }
+}
+
+
+// ---- exact walk, two passes -------------------------------------------------
+// The draws of a depo are sequential only through n = remaining: every other
+// input of bin b's draw - its conditional probability p_b (the running p_rem
+// subtraction, rasterize.cpp:141-147), pp = min(p, 1 - p), log1p(-pp) and the
+// uniform it consumes (bins with p in (0, 1) consume one each, in bin order,
+// as long as no draw can take binomial's normal branch: q min(p, 1 - p) <=
+// 1e6 for every bin, since n <= q) - is fixed by the patch. k_fluct_prep
+// computes them for all bins, one lane per unit with the same work per bin;
+// k_fluct_walk then runs only what depends on n: n log1p(-pp), the pmf seed
+// exp(n log1p(-pp)) (lgamma seed past -700) and the CDF walk. The reference's
+// operations and their order are unchanged (the same values are computed,
+// some earlier). Units that could reach the normal branch, and units whose
+// records do not fit the buffer, take the one-pass walk (k_fluctuate_exact)
+// whole (kErrFluct only tells the host to grow the buffer).
+constexpr uint32_t kFlNone = 0xffffffffu;
+enum : uint32_t { kFlDraw = 0u, kFlDrawFlip = 1u, kFlZero = 2u, kFlAll = 3u };
+
+// One bin's draw inputs, 32 B (one sector).
+struct __align__(32) FlRec {
+    double pp;   // min(p, 1 - p) (the walk's p, rng.cpp:191-192)
+    double lg;   // log1p(-pp)
+    double u;    // the draw's uniform
+    float lnu;   // log(u) rounded to float (|error| < 2.3e-6): k = 0 test without exp
+    uint32_t cls;  // kFlDraw / kFlDrawFlip (p > 0.5) / kFlZero (p == 0) / kFlAll (p == 1)
+};
+static_assert(sizeof(FlRec) == 32, "one sector per record");
+
+__global__ void __launch_bounds__(128) k_fluct_prep(const EventDesc ev, const UnitRec* __restrict__ recs,
+                                                     const uint32_t* __restrict__ pool,
+                                                     const uint32_t* __restrict__ order, uint32_t* __restrict__ offs,
+                                                     uint32_t* __restrict__ slow, uint32_t* __restrict__ n_slow,
+                                                     uint32_t* __restrict__ cursor, uint32_t first)
+{
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    if (i == 0) *cursor = first;  // k_fluct_walk's unit cursor (its lanes start with units [0, first))
+    const bool in = i < ev.total_units;
+    const uint32_t u = in ? order[i] : 0u;
+    UnitRec rec{};
+    rec.w0 = -1;
+    if (in) rec = recs[u];
+    const bool live = in && rec.w0 >= 0;
+    const uint32_t need = live ? (uint32_t)(rec.n_w * rec.n_t - 1) : 0u;  // draws: every bin but the last
+    // warp-aggregated allocation of the records
+    uint32_t incl = need;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+    unsigned long long base = 0;
+    if (lane == 31 && tot) base = atomicAdd(ev.fl_ctr, (unsigned long long)tot);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    if (!in) return;
+    if (!live) {
+        offs[i] = kFlNone;
+        return;
+    }
+    const unsigned long long off = base + incl - need;
+    if (off + need > ev.fl_cap || off + need > 0xfffffffeull) {
+        atomicOr(ev.err, kErrFluct);
+        offs[i] = kFlNone;
+        slow[atomicAdd(n_slow, 1u)] = u;
+        return;
+    }
+    const PlaneDesc& P = ev.p[plane_of_unit(ev, u)];
+    const ws_depo d = P.depos[u - P.unit_base];
+    const double* wv = reinterpret_cast<const double*>(pool + rec.pool);
+    const double* tv = wv + rec.n_w;
+    const int n_t = rec.n_t;
+    double total = 0.0;
+    for (int w = 0; w < rec.n_w; ++w) {
+        const double pw = wv[w];
+        for (int t = 0; t < n_t; ++t) total += pw * tv[t];
+    }
+    const double norm = 1.0 / total;
+    Rng src;
+    src.init(ev.rng_mode, ev.seed, (uint64_t)d.id);
+    // uniform01 (rng.cpp:51-54); Philox: each block computed once for its two draws
+    uint64_t odd_half = 0;
+    auto uniform = [&]() -> double {
+        if (ev.rng_mode == WS_RNG_SUBSTREAM) return src.uniform();
+        const uint32_t k = src.draw++;
+        uint64_t x = odd_half;
+        if (!(k & 1u)) src.philox_block(k >> 1, x, odd_half);
+        return (double)(x >> 11) * 0x1.0p-53;
+    };
+    const double qd = (double)d.q;
+    FlRec* out = reinterpret_cast<FlRec*>(ev.fl_bins) + off;
+    double p_rem = 1.0;
+    bool slow_unit = false;
+    int bw = 0, bt = 0;
+#pragma unroll 1
+    for (uint32_t b = 0; b < need; ++b) {
+        const double pi = (wv[bw] * tv[bt]) * norm;
+        double p = 1.0;
+        if (p_rem > 0.0) {
+            p = pi / p_rem;
+            p = p < 0.0 ? 0.0 : (p > 1.0 ? 1.0 : p);
+        }
+        FlRec r;
+        r.pp = 0.0;
+        r.lg = 0.0;
+        r.u = 0.0;
+        r.lnu = 0.0f;
+        r.cls = p == 0.0 ? kFlZero : kFlAll;
+        if (p > 0.0 && p < 1.0) {
+            const double q1 = __dsub_rn(1.0, p);
+            const double mn = (q1 < p) ? q1 : p;
+            slow_unit |= __dmul_rn(qd, mn) > 1e6;
+            r.cls = p > 0.5 ? kFlDrawFlip : kFlDraw;
+            r.pp = p > 0.5 ? q1 : p;
+            r.lg = log1p(-r.pp);
+            r.u = uniform();
+            r.lnu = r.u > 0.0 ? (float)log(r.u) : -INFINITY;
+        }
+        double4 v0 = make_double4(r.pp, r.lg, r.u, 0.0);
+        reinterpret_cast<uint32_t*>(&v0.w)[0] = __float_as_uint(r.lnu);
+        reinterpret_cast<uint32_t*>(&v0.w)[1] = r.cls;
+        reinterpret_cast<double2*>(out + b)[0] = make_double2(v0.x, v0.y);
+        reinterpret_cast<double2*>(out + b)[1] = make_double2(v0.z, v0.w);
+        p_rem -= pi;
+        if (++bt == n_t) {
+            bt = 0;
+            ++bw;
+        }
+    }
+    if (slow_unit) {
+        offs[i] = kFlNone;
+        slow[atomicAdd(n_slow, 1u)] = u;
+    } else {
+        offs[i] = (uint32_t)off;
+    }
+}
+
+// The walk over k_fluct_prep's records: persistent lanes (a grid that fills
+// the GPU once) take units from a shared cursor over the charge-sorted
+// order, so a lane whose depo is finished takes the next one instead of
+// idling until its warp's longest depo ends. Per lane the state machine of
+// k_fluctuate_exact: setting up draws is a loop over the records that settles
+// the cheap ones without exp (p == 0, p == 1, and k = 0 when n log1p(-pp) >
+// log(u) + 1e-5: then (1 - pp)^n > u for the reference's exp as for ours) and
+// stops at the first draw that needs its pmf seed; the warp's seeds are then
+// computed together, and the warp walks until a quorum of its lanes is idle.
+// The walk takes kWalk CDF steps per iteration: the recursion factors are
+// independent, the serial chain is pmf *= f, cdf += pmf, and as the CDF never
+// decreases the stop is the first step with cdf > u.
+__global__ void __launch_bounds__(128) k_fluct_walk(const EventDesc ev, const UnitRec* __restrict__ recs,
+                                                     const uint32_t* __restrict__ order,
+                                                     const uint32_t* __restrict__ offs, uint32_t* __restrict__ cursor)
+{
+    const int lane = threadIdx.x & 31;
+    // the lane's unit
+    bool has = false, exhausted = false;
+    int64_t remaining = 0;
+    int n_t = 0, last = 0, b = 0, bt = 0, N = 0;
+    unsigned long long* cellp = nullptr;
+    unsigned long long* lastp = nullptr;
+    const FlRec* rp = nullptr;
+    // the draw in progress
+    bool walking = false, flip = false;
+    int64_t n = 0;
+    double odds = 0.0, pmf = 0.0, cdf = 0.0, uu = 0.0, kd = 0.0, nd = 0.0, nk = 0.0, k1 = 0.0;
+    int kr = 0;
+
+    auto take = [&](uint32_t idx) {  // start unit order[idx] (if it has records)
+        if (idx >= ev.total_units) {
+            exhausted = true;
+            return;
+        }
+        const uint32_t off = offs[idx];
+        if (off == kFlNone) return;  // empty, or the one-pass walk's
+        const uint32_t u = order[idx];
+        const UnitRec rec = recs[u];
+        const PlaneDesc& P = ev.p[plane_of_unit(ev, u)];
+        remaining = P.depos[u - P.unit_base].q;
+        N = P.N;
+        n_t = rec.n_t;
+        last = rec.n_w * n_t - 1;
+        b = 0;
+        bt = 0;
+        cellp = P.charge_cnt + (size_t)rec.w0 * N + rec.t0;
+        lastp = cellp + (size_t)(rec.n_w - 1) * N + n_t - 1;
+        rp = reinterpret_cast<const FlRec*>(ev.fl_bins) + off;
+        has = true;
+    };
+    auto commit = [&](int64_t k) {
+        add_count(cellp, k);
+        remaining -= k;
+        ++b;
+        ++rp;
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(rp + 3));
+        if (++bt == n_t) {
+            bt = 0;
+            cellp += N - (n_t - 1);
+        } else {
+            ++cellp;
+        }
+    };
+    take(blockIdx.x * blockDim.x + threadIdx.x);
+
+    auto setup = [&]() {
+        bool seed = false;  // the current draw needs its pmf seed
+        double pp = 0.0, lg = 0.0, x = 0.0;
+#pragma unroll 1
+        for (;;) {
+            // lanes without a unit take the next ones (one atomic per warp)
+            const unsigned want = __ballot_sync(0xffffffffu, !has && !exhausted);
+            if (want) {
+                uint32_t base = 0;
+                if (lane == __ffs(want) - 1) base = atomicAdd(cursor, (uint32_t)__popc(want));
+                base = __shfl_sync(0xffffffffu, base, __ffs(want) - 1);
+                if (want & (1u << lane)) take(base + __popc(want & ((1u << lane) - 1u)));
+                continue;
+            }
+            // cheap draws until one needs its seed, the unit ends, or the lane walks
+            while (has && !walking && !seed) {
+                if (remaining == 0 || b >= last) {
+                    if (remaining) add_count(lastp, remaining);  // the last bin takes the rest
+                    has = false;
+                    break;
+                }
+                const double2 ra = __ldg(reinterpret_cast<const double2*>(rp));
+                const double2 rb = __ldg(reinterpret_cast<const double2*>(rp) + 1);
+                const uint32_t cls = __double2hiint(rb.y);
+                n = remaining;
+                if (cls == kFlZero) {
+                    commit(0);
+                    continue;
+                }
+                if (cls == kFlAll) {
+                    commit(n);
+                    continue;
+                }
+                flip = cls == kFlDrawFlip;
+                pp = ra.x;
+                lg = ra.y;
+                x = __dmul_rn((double)n, lg);
+                if (x > -700.0 && x > (double)__int_as_float(__double2loint(rb.y)) + 1e-5) {
+                    commit(flip ? n : 0);  // (1 - pp)^n > u: k = 0
+                    continue;
+                }
+                uu = rb.x;
+                seed = true;
+            }
+            if (!__any_sync(0xffffffffu, !has && !exhausted)) break;
+        }
+        if (seed) {
+            // invert_binomial_cdf (rng.cpp:146-170): the pmf seed
+            odds = __ddiv_rn(pp, __dsub_rn(1.0, pp));
+            int64_t k = 0;
+            if (x > -700.0) {
+                pmf = exp_ref(x);
+            } else {
+                const double m2 = __dmul_rn((double)n, pp);
+                const double sd = sqrt(__dmul_rn(m2, __dsub_rn(1.0, pp)));
+                const int64_t k0 = (int64_t)__dsub_rn(m2, __dmul_rn(30.0, sd));
+                k = k0 > 0 ? k0 : 0;
+                const double nn = (double)n, kk = (double)k;
+                double e = __dsub_rn(lgamma(__dadd_rn(nn, 1.0)), lgamma(__dadd_rn(kk, 1.0)));
+                e = __dsub_rn(e, lgamma(__dadd_rn(__dsub_rn(nn, kk), 1.0)));
+                e = __dadd_rn(e, __dmul_rn(kk, log(pp)));
+                e = __dadd_rn(e, __dmul_rn(__dsub_rn(nn, kk), lg));
+                pmf = exp_ref(e);
+            }
+            cdf = pmf;
+            if (cdf <= uu && k < n) {
+                walking = true;
+                kd = (double)k;
+                nd = (double)n;
+                nk = (double)(n - k);
+                k1 = (double)(k + 1);
+                kr = k + 1 < (int64_t)kRecipN && odds >= kMarksteinMin ? (int)(k + 1) : kRecipN;
+            } else {
+                commit(flip ? n - k : k);
+            }
+        }
+    };
+
+    constexpr int kWalk = 4;
+#pragma unroll 1
+    for (;;) {
+        setup();
+        const unsigned alive = __ballot_sync(0xffffffffu, has);  // (lanes without a unit are exhausted)
+        if (!alive) break;
+        const int quorum = max(1, (__popc(alive) * ev.fl_quorum) >> 4);
+#pragma unroll 1
+        for (;;) {
+            if (walking) {
+                double f[kWalk];
+                if (kr + kWalk <= kRecipN) {
+#pragma unroll
+                    for (int j = 0; j < kWalk; ++j)
+                        f[j] = div_rn_y(__dmul_rn(odds, nk - (double)j), k1 + (double)j, __ldg(&ev.recip[kr + j]));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < kWalk; ++j) f[j] = __ddiv_rn(__dmul_rn(odds, nk - (double)j), k1 + (double)j);
+                }
+                if (nk >= (double)kWalk) {
+                    // k + kWalk <= n: only the cdf test can stop these steps
+                    double pm = pmf, c = cdf;
+                    int adv = 0;
+#pragma unroll
+                    for (int j = 0; j < kWalk; ++j) {
+                        pm = __dmul_rn(pm, f[j]);
+                        c = __dadd_rn(c, pm);
+                        adv += c <= uu ? 1 : 0;  // monotone: counts the steps before the stop
+                    }
+                    if (adv == kWalk && nk > (double)kWalk) {  // (k + kWalk == n ends the walk too)
+                        pmf = pm;
+                        cdf = c;
+                        kd += (double)kWalk;
+                        nk -= (double)kWalk;
+                        k1 += (double)kWalk;
+                        kr += kWalk;
+                    } else {
+                        walking = false;
+                        const int64_t k = (int64_t)kd + min(adv + 1, kWalk);
+                        commit(flip ? n - k : k);
+                    }
+                } else {
+                    double pm = pmf, c = cdf, kk = kd;
+                    bool go = true;
+#pragma unroll
+                    for (int j = 0; j < kWalk; ++j) {
+                        if (go) {
+                            pm = __dmul_rn(pm, f[j]);
+                            c = __dadd_rn(c, pm);
+                            kk += 1.0;
+                            go = c <= uu && kk < nd;
+                        }
+                    }
+                    const double adv = kk - kd;
+                    pmf = pm;
+                    cdf = c;
+                    kd = kk;
+                    nk -= adv;
+                    k1 += adv;
+                    kr += (int)adv;
+                    if (!go) {
+                        walking = false;
+                        const int64_t k = (int64_t)kd;
+                        commit(flip ? n - k : k);
+                    }
                 }
             }
             const unsigned wk = __ballot_sync(0xffffffffu, walking);
@@ -1114,7 +1475,9 @@ extern "C" cudaError_t wsb_launch_fluctuate(const wsb::EventDesc& ev, const wsb:
         wsb::k_fluctuate<<<(ev.total_units + 127) / 128, 128, 0, s>>>(ev, recs, pool, order);
         return cudaGetLastError();
     }
-    // exact walk: units in descending charge (CUB radix sort, stream-ordered scratch)
+    // exact walk: units in descending charge (CUB radix sort, stream-ordered
+    // scratch), the per-bin records (k_fluct_prep), the walk (k_fluct_walk),
+    // then the units that could take binomial's normal branch (k_fluctuate_exact)
     const uint32_t n = ev.total_units;
     uint32_t* buf = nullptr;
     size_t temp = 0;
@@ -1122,14 +1485,29 @@ extern "C" cudaError_t wsb_launch_fluctuate(const wsb::EventDesc& ev, const wsb:
                                                               (uint32_t*)nullptr, (const uint32_t*)nullptr,
                                                               (uint32_t*)nullptr, (int)n, 0, 32, s);
     if (e != cudaSuccess) return e;
-    e = cudaMallocAsync(reinterpret_cast<void**>(&buf), sizeof(uint32_t) * 4 * (size_t)n + temp, s);
+    temp = (temp + 15) & ~(size_t)15;
+    e = cudaMallocAsync(reinterpret_cast<void**>(&buf), sizeof(uint32_t) * (6 * (size_t)n + 4) + temp, s);
     if (e != cudaSuccess) return e;
     uint32_t *k_in = buf, *k_out = buf + n, *v_in = buf + 2 * (size_t)n, *v_out = buf + 3 * (size_t)n;
+    uint32_t *offs = buf + 4 * (size_t)n, *slow = buf + 5 * (size_t)n, *n_slow = buf + 6 * (size_t)n;
+    uint32_t* cursor = n_slow + 1;
+    void* sort_tmp = reinterpret_cast<unsigned char*>(buf + 6 * (size_t)n + 4);
+    const unsigned blocks = (n + 127) / 128;
     wsb::k_fluct_keys<<<(n + 255) / 256, 256, 0, s>>>(ev, recs, k_in, v_in);
-    e = cub::DeviceRadixSort::SortPairsDescending(buf + 4 * (size_t)n, temp, k_in, k_out, v_in, v_out, (int)n, 0, 32,
-                                                  s);
+    e = cudaMemsetAsync(n_slow, 0, sizeof(uint32_t), s);
     if (e == cudaSuccess)
-        wsb::k_fluctuate_exact<<<(n + 127) / 128, 128, 0, s>>>(ev, recs, pool, v_out);
+        e = cub::DeviceRadixSort::SortPairsDescending(sort_tmp, temp, k_in, k_out, v_in, v_out, (int)n, 0, 32, s);
+    if (e == cudaSuccess) {
+        // persistent walk: one resident wave of lanes pulling units from a cursor
+        int dev = 0, sms = 148, per_sm = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wsb::k_fluct_walk, 128, 0);
+        const unsigned wblocks = std::min<unsigned>(blocks, (unsigned)(sms * std::max(per_sm, 1)));
+        wsb::k_fluct_prep<<<blocks, 128, 0, s>>>(ev, recs, pool, v_out, offs, slow, n_slow, cursor, wblocks * 128u);
+        wsb::k_fluct_walk<<<wblocks, 128, 0, s>>>(ev, recs, v_out, offs, cursor);
+        wsb::k_fluctuate_exact<<<blocks, 128, 0, s>>>(ev, recs, pool, slow, n_slow);
+    }
     const cudaError_t e2 = cudaFreeAsync(buf, s);
     if (e != cudaSuccess) return e;
     if (e2 != cudaSuccess) return e2;
