@@ -867,14 +867,16 @@ __global__ void k_fluctuate(const EventDesc ev, const UnitRec* __restrict__ recs
 // walk-length key of every unit (the walk is ~q steps): warps of similar
 // charge keep their lanes busy together
 __global__ void k_fluct_keys(const EventDesc ev, const UnitRec* __restrict__ recs, uint32_t* __restrict__ keys,
-                             uint32_t* __restrict__ vals)
+                             uint32_t* __restrict__ vals, uint32_t* __restrict__ bins)
 {
     const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
     if (u >= ev.total_units) return;
     const PlaneDesc& P = ev.p[plane_of_unit(ev, u)];
-    const int64_t q = recs[u].w0 >= 0 ? P.depos[u - P.unit_base].q : 0;
+    const UnitRec r = recs[u];
+    const int64_t q = r.w0 >= 0 ? P.depos[u - P.unit_base].q : 0;
     keys[u] = (uint32_t)(q < 0 ? 0 : (q > 0xffffffffll ? 0xffffffffll : q));
     vals[u] = u;
+    if (bins) bins[u] = r.w0 >= 0 ? (uint32_t)(r.n_w * r.n_t) : 0u;  // k_fluct_prep's per-lane work
 }
 
 // n_list (nullable): the number of entries of `order` (device), else total_units
@@ -1076,6 +1078,15 @@ __global__ void __launch_bounds__(128) k_fluctuate_exact(const EventDesc ev, con
 // records do not fit the buffer, take the one-pass walk (k_fluctuate_exact)
 // whole (kErrFluct only tells the host to grow the buffer).
 constexpr uint32_t kFlNone = 0xffffffffu;
+#ifndef WS_FLWALK_MINB
+#define WS_FLWALK_MINB 8  // 64 registers, 32 warps per SM (r2: 6.67 vs 7.25 ms per C3 event at 78 registers)
+#endif
+#ifndef WS_FLWALK_PF
+#define WS_FLWALK_PF 3
+#endif
+#ifndef WS_FLWALK_PF2
+#define WS_FLWALK_PF2 0
+#endif
 enum : uint32_t { kFlDraw = 0u, kFlDrawFlip = 1u, kFlZero = 2u, kFlAll = 3u };
 
 // One bin's draw inputs, 32 B (one sector).
@@ -1083,7 +1094,7 @@ struct __align__(32) FlRec {
     double pp;   // min(p, 1 - p) (the walk's p, rng.cpp:191-192)
     double lg;   // log1p(-pp)
     double u;    // the draw's uniform
-    float lnu;   // log(u) rounded to float (|error| < 2.3e-6): k = 0 test without exp
+    float lnu;   // logf(u) (|error| < 7.7e-6; +inf below u = 1e-30): k = 0 test without exp
     uint32_t cls;  // kFlDraw / kFlDrawFlip (p > 0.5) / kFlZero (p == 0) / kFlAll (p == 1)
 };
 static_assert(sizeof(FlRec) == 32, "one sector per record");
@@ -1098,7 +1109,7 @@ __global__ void __launch_bounds__(128) k_fluct_prep(const EventDesc ev, const Un
     const int lane = threadIdx.x & 31;
     if (i == 0) *cursor = first;  // k_fluct_walk's unit cursor (its lanes start with units [0, first))
     const bool in = i < ev.total_units;
-    const uint32_t u = in ? order[i] : 0u;
+    const uint32_t u = in ? order[i] : 0u;  // units by bin count: the lanes of a warp do similar work
     UnitRec rec{};
     rec.w0 = -1;
     if (in) rec = recs[u];
@@ -1117,13 +1128,13 @@ __global__ void __launch_bounds__(128) k_fluct_prep(const EventDesc ev, const Un
     base = __shfl_sync(0xffffffffu, base, 31);
     if (!in) return;
     if (!live) {
-        offs[i] = kFlNone;
+        offs[u] = kFlNone;
         return;
     }
     const unsigned long long off = base + incl - need;
     if (off + need > ev.fl_cap || off + need > 0xfffffffeull) {
         atomicOr(ev.err, kErrFluct);
-        offs[i] = kFlNone;
+        offs[u] = kFlNone;
         slow[atomicAdd(n_slow, 1u)] = u;
         return;
     }
@@ -1176,7 +1187,10 @@ __global__ void __launch_bounds__(128) k_fluct_prep(const EventDesc ev, const Un
             r.pp = p > 0.5 ? q1 : p;
             r.lg = log1p(-r.pp);
             r.u = uniform();
-            r.lnu = r.u > 0.0 ? (float)log(r.u) : -INFINITY;
+            // log(u) for the walk's k = 0 test: |logf - ln u| <= 1 ulp (<= 7.6e-6
+            // at u >= 1e-30) + the float rounding of u (6e-8); +inf disables the
+            // test for smaller u
+            r.lnu = r.u >= 1e-30 ? logf((float)r.u) : INFINITY;
         }
         double4 v0 = make_double4(r.pp, r.lg, r.u, 0.0);
         reinterpret_cast<uint32_t*>(&v0.w)[0] = __float_as_uint(r.lnu);
@@ -1190,10 +1204,10 @@ __global__ void __launch_bounds__(128) k_fluct_prep(const EventDesc ev, const Un
         }
     }
     if (slow_unit) {
-        offs[i] = kFlNone;
+        offs[u] = kFlNone;
         slow[atomicAdd(n_slow, 1u)] = u;
     } else {
-        offs[i] = (uint32_t)off;
+        offs[u] = (uint32_t)off;
     }
 }
 
@@ -1203,13 +1217,13 @@ __global__ void __launch_bounds__(128) k_fluct_prep(const EventDesc ev, const Un
 // idling until its warp's longest depo ends. Per lane the state machine of
 // k_fluctuate_exact: setting up draws is a loop over the records that settles
 // the cheap ones without exp (p == 0, p == 1, and k = 0 when n log1p(-pp) >
-// log(u) + 1e-5: then (1 - pp)^n > u for the reference's exp as for ours) and
+// log(u) + 4e-5: then (1 - pp)^n > u for the reference's exp as for ours) and
 // stops at the first draw that needs its pmf seed; the warp's seeds are then
 // computed together, and the warp walks until a quorum of its lanes is idle.
 // The walk takes kWalk CDF steps per iteration: the recursion factors are
 // independent, the serial chain is pmf *= f, cdf += pmf, and as the CDF never
 // decreases the stop is the first step with cdf > u.
-__global__ void __launch_bounds__(128) k_fluct_walk(const EventDesc ev, const UnitRec* __restrict__ recs,
+__global__ void __launch_bounds__(128, WS_FLWALK_MINB) k_fluct_walk(const EventDesc ev, const UnitRec* __restrict__ recs,
                                                      const uint32_t* __restrict__ order,
                                                      const uint32_t* __restrict__ offs, uint32_t* __restrict__ cursor)
 {
@@ -1232,9 +1246,9 @@ __global__ void __launch_bounds__(128) k_fluct_walk(const EventDesc ev, const Un
             exhausted = true;
             return;
         }
-        const uint32_t off = offs[idx];
-        if (off == kFlNone) return;  // empty, or the one-pass walk's
         const uint32_t u = order[idx];
+        const uint32_t off = offs[u];
+        if (off == kFlNone) return;  // empty, or the one-pass walk's
         const UnitRec rec = recs[u];
         const PlaneDesc& P = ev.p[plane_of_unit(ev, u)];
         remaining = P.depos[u - P.unit_base].q;
@@ -1253,7 +1267,8 @@ __global__ void __launch_bounds__(128) k_fluct_walk(const EventDesc ev, const Un
         remaining -= k;
         ++b;
         ++rp;
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(rp + 3));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(rp + WS_FLWALK_PF));
+        if (WS_FLWALK_PF2 > 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + WS_FLWALK_PF2));
         if (++bt == n_t) {
             bt = 0;
             cellp += N - (n_t - 1);
@@ -1263,7 +1278,12 @@ __global__ void __launch_bounds__(128) k_fluct_walk(const EventDesc ev, const Un
     };
     take(blockIdx.x * blockDim.x + threadIdx.x);
 
+    int64_t kdone = -1;  // a draw the walk finished, committed by the next setup (all idle lanes together)
     auto setup = [&]() {
+        if (kdone >= 0) {
+            commit(kdone);
+            kdone = -1;
+        }
         bool seed = false;  // the current draw needs its pmf seed
         double pp = 0.0, lg = 0.0, x = 0.0;
 #pragma unroll 1
@@ -1300,7 +1320,7 @@ __global__ void __launch_bounds__(128) k_fluct_walk(const EventDesc ev, const Un
                 pp = ra.x;
                 lg = ra.y;
                 x = __dmul_rn((double)n, lg);
-                if (x > -700.0 && x > (double)__int_as_float(__double2loint(rb.y)) + 1e-5) {
+                if (x > -700.0 && x > (double)__int_as_float(__double2loint(rb.y)) + 4e-5) {
                     commit(flip ? n : 0);  // (1 - pp)^n > u: k = 0
                     continue;
                 }
@@ -1380,7 +1400,7 @@ __global__ void __launch_bounds__(128) k_fluct_walk(const EventDesc ev, const Un
                     } else {
                         walking = false;
                         const int64_t k = (int64_t)kd + min(adv + 1, kWalk);
-                        commit(flip ? n - k : k);
+                        kdone = flip ? n - k : k;
                     }
                 } else {
                     double pm = pmf, c = cdf, kk = kd;
@@ -1404,7 +1424,7 @@ __global__ void __launch_bounds__(128) k_fluct_walk(const EventDesc ev, const Un
                     if (!go) {
                         walking = false;
                         const int64_t k = (int64_t)kd;
-                        commit(flip ? n - k : k);
+                        kdone = flip ? n - k : k;
                     }
                 }
             }
@@ -1475,9 +1495,10 @@ extern "C" cudaError_t wsb_launch_fluctuate(const wsb::EventDesc& ev, const wsb:
         wsb::k_fluctuate<<<(ev.total_units + 127) / 128, 128, 0, s>>>(ev, recs, pool, order);
         return cudaGetLastError();
     }
-    // exact walk: units in descending charge (CUB radix sort, stream-ordered
-    // scratch), the per-bin records (k_fluct_prep), the walk (k_fluct_walk),
-    // then the units that could take binomial's normal branch (k_fluctuate_exact)
+    // exact walk: the units in descending charge for the walk and by bin count
+    // for the records (CUB radix sorts, stream-ordered scratch), the per-bin
+    // records (k_fluct_prep), the walk (k_fluct_walk), then the units that
+    // could take binomial's normal branch (k_fluctuate_exact)
     const uint32_t n = ev.total_units;
     uint32_t* buf = nullptr;
     size_t temp = 0;
@@ -1486,17 +1507,19 @@ extern "C" cudaError_t wsb_launch_fluctuate(const wsb::EventDesc& ev, const wsb:
                                                               (uint32_t*)nullptr, (int)n, 0, 32, s);
     if (e != cudaSuccess) return e;
     temp = (temp + 15) & ~(size_t)15;
-    e = cudaMallocAsync(reinterpret_cast<void**>(&buf), sizeof(uint32_t) * (6 * (size_t)n + 4) + temp, s);
+    e = cudaMallocAsync(reinterpret_cast<void**>(&buf), sizeof(uint32_t) * (8 * (size_t)n + 4) + temp, s);
     if (e != cudaSuccess) return e;
     uint32_t *k_in = buf, *k_out = buf + n, *v_in = buf + 2 * (size_t)n, *v_out = buf + 3 * (size_t)n;
-    uint32_t *offs = buf + 4 * (size_t)n, *slow = buf + 5 * (size_t)n, *n_slow = buf + 6 * (size_t)n;
-    uint32_t* cursor = n_slow + 1;
-    void* sort_tmp = reinterpret_cast<unsigned char*>(buf + 6 * (size_t)n + 4);
+    uint32_t *offs = buf + 4 * (size_t)n, *slow = buf + 5 * (size_t)n, *b_in = buf + 6 * (size_t)n;
+    uint32_t *b_order = buf + 7 * (size_t)n, *n_slow = buf + 8 * (size_t)n, *cursor = n_slow + 1;
+    void* sort_tmp = reinterpret_cast<unsigned char*>(buf + 8 * (size_t)n + 4);
     const unsigned blocks = (n + 127) / 128;
-    wsb::k_fluct_keys<<<(n + 255) / 256, 256, 0, s>>>(ev, recs, k_in, v_in);
+    wsb::k_fluct_keys<<<(n + 255) / 256, 256, 0, s>>>(ev, recs, k_in, v_in, b_in);
     e = cudaMemsetAsync(n_slow, 0, sizeof(uint32_t), s);
     if (e == cudaSuccess)
         e = cub::DeviceRadixSort::SortPairsDescending(sort_tmp, temp, k_in, k_out, v_in, v_out, (int)n, 0, 32, s);
+    if (e == cudaSuccess)  // (k_out is free again: the bin-count keys' sorted output)
+        e = cub::DeviceRadixSort::SortPairsDescending(sort_tmp, temp, b_in, k_out, v_in, b_order, (int)n, 0, 32, s);
     if (e == cudaSuccess) {
         // persistent walk: one resident wave of lanes pulling units from a cursor
         int dev = 0, sms = 148, per_sm = 1;
@@ -1504,7 +1527,7 @@ extern "C" cudaError_t wsb_launch_fluctuate(const wsb::EventDesc& ev, const wsb:
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wsb::k_fluct_walk, 128, 0);
         const unsigned wblocks = std::min<unsigned>(blocks, (unsigned)(sms * std::max(per_sm, 1)));
-        wsb::k_fluct_prep<<<blocks, 128, 0, s>>>(ev, recs, pool, v_out, offs, slow, n_slow, cursor, wblocks * 128u);
+        wsb::k_fluct_prep<<<blocks, 128, 0, s>>>(ev, recs, pool, b_order, offs, slow, n_slow, cursor, wblocks * 128u);
         wsb::k_fluct_walk<<<wblocks, 128, 0, s>>>(ev, recs, v_out, offs, cursor);
         wsb::k_fluctuate_exact<<<blocks, 128, 0, s>>>(ev, recs, pool, slow, n_slow);
     }
