@@ -27,6 +27,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", str(INC
 SOURCES = {
     "ws_sample.cu": ["--fmad=false"],
     "ws_conv.cu": [],
+    "ws_conv_tc.cu": [],
     "ws_direct.cu": [],
     "ws_gprof.cu": [],
     "ws_gprof_umma.cu": [],

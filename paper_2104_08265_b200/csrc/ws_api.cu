@@ -42,6 +42,8 @@ extern "C" size_t wsb_direct_smem(int cap);
 extern "C" int wsb_direct_cap();
 extern "C" cudaError_t wsb_launch_direct(const EventDesc& ev, const uint32_t* pool, const uint32_t* band_off,
                                          const wsb::TEnt* tlist, size_t smem_bytes, cudaStream_t stream, int pdl);
+extern "C" int wsb_conv_tc_nb(const PlaneDesc& P);
+extern "C" cudaError_t wsb_launch_conv_tc(const EventDesc& ev, int nb, cudaStream_t s);
 extern "C" cudaError_t wsb_launch_fluctuate(const EventDesc& ev, const UnitRec* recs, const uint32_t* pool,
                                             const uint32_t* order, cudaStream_t s);
 extern "C" size_t wsb_sigproc_smem(int n);
@@ -766,7 +768,21 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
             c->launches += bands ? 1 : 0;
         }
         if (any_fft) {
-            WS_CUDA(wsb_launch_conv(ev, c->pool.p, c->band_off.p, c->band_list.p, 1, smem, c->conv_variant, s));
+            // a given grid (fluctuation counts / ws_convolve_device): the
+            // tensor-core direct convolution when every plane is eligible,
+            // else the row FFT
+            int nb = 0;
+            if (ev.mode == 1) {
+                nb = 4;
+                for (uint32_t i = 0; i < nd && nb; ++i)
+                    if (!ev.p[i].direct) nb = std::min(nb, wsb_conv_tc_nb(ev.p[i]));
+            }
+            cudaError_t te = nb ? wsb_launch_conv_tc(ev, nb, s) : cudaErrorNotSupported;
+            if (te == cudaErrorNotSupported) {
+                (void)cudaGetLastError();
+                te = wsb_launch_conv(ev, c->pool.p, c->band_off.p, c->band_list.p, 1, smem, c->conv_variant, s);
+            }
+            WS_CUDA(te);
             c->launches += bands ? 1 : 0;
         }
     }
