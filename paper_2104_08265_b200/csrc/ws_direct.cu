@@ -109,6 +109,46 @@ __device__ __forceinline__ void scatter_rows(const float* __restrict__ c, int rl
     }
 }
 
+// The same with the row loop unrolled for a known row count (the common
+// profile lengths): per row one LDS with an immediate offset and one
+// widening, then the taps' DFMA + RED with immediate row / tap offsets; no
+// loop counter, no per-row address arithmetic.
+#if !defined(WS_DIRECT_MAGIC) && !defined(WS_DIRECT_F2I)
+template <int NQ, int R, int NR>
+struct RowsUnrolled {
+    static __device__ __forceinline__ void run(const float* __restrict__ c, uint32_t ar, const gtap_t* gv)
+    {
+        if constexpr (R < NR) {
+            constexpr int RB = 4 * kRowStride * R;
+            const double cs = (double)c[R];
+            red_shared_off<RB>(ar, fix_rn_d(cs, gv[0]));
+            if constexpr (NQ > 1) red_shared_off<RB + 128>(ar, fix_rn_d(cs, gv[1]));
+            if constexpr (NQ > 2) red_shared_off<RB + 256>(ar, fix_rn_d(cs, gv[2]));
+            if constexpr (NQ > 3) red_shared_off<RB + 384>(ar, fix_rn_d(cs, gv[3]));
+            if constexpr (NQ > 4) red_shared_off<RB + 512>(ar, fix_rn_d(cs, gv[4]));
+            RowsUnrolled<NQ, R + 1, NR>::run(c, ar, gv);
+        }
+    }
+};
+template <int NQ>
+__device__ __forceinline__ void scatter_rows_unrolled(const float* __restrict__ c, int rlo, int rhi, uint32_t a0,
+                                                      const gtap_t* gv)
+{
+    const uint32_t ar = a0 + (uint32_t)rlo * (4u * kRowStride);
+    const float* cr = c + rlo;
+    switch (rhi - rlo) {
+        case 8: RowsUnrolled<NQ, 0, 8>::run(cr, ar, gv); break;
+        case 7: RowsUnrolled<NQ, 0, 7>::run(cr, ar, gv); break;
+        case 6: RowsUnrolled<NQ, 0, 6>::run(cr, ar, gv); break;
+        case 5: RowsUnrolled<NQ, 0, 5>::run(cr, ar, gv); break;
+        case 4: RowsUnrolled<NQ, 0, 4>::run(cr, ar, gv); break;
+        case 3: RowsUnrolled<NQ, 0, 3>::run(cr, ar, gv); break;
+        case 2: RowsUnrolled<NQ, 0, 2>::run(cr, ar, gv); break;
+        default: RowsUnrolled<NQ, 0, 1>::run(cr, ar, gv); break;
+    }
+}
+#endif
+
 __device__ __forceinline__ void cp_async16(uint32_t saddr, const void* gptr)
 {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(gptr) : "memory");
@@ -273,8 +313,13 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
             const uint32_t a0 = sacc + 4u * (uint32_t)(kMargin + ts - ws + lane);
             static_assert(kQ == 5, "scatter_rows handles up to 5 taps per lane");
             switch ((L + 31) >> 5) {  // 32-tap groups in g's 0-filled length (warp-uniform)
+#if !defined(WS_DIRECT_MAGIC) && !defined(WS_DIRECT_F2I) && !defined(WS_DIRECT_ROWLOOP)
+                case 5: scatter_rows_unrolled<5>(d.c, rlo, rhi, a0, gv); break;
+                case 4: scatter_rows_unrolled<4>(d.c, rlo, rhi, a0, gv); break;
+#else
                 case 5: scatter_rows<5>(d.c, rlo, rhi, a0, gv); break;
                 case 4: scatter_rows<4>(d.c, rlo, rhi, a0, gv); break;
+#endif
                 case 3: scatter_rows<3>(d.c, rlo, rhi, a0, gv); break;
                 case 2: scatter_rows<2>(d.c, rlo, rhi, a0, gv); break;
                 default: scatter_rows<1>(d.c, rlo, rhi, a0, gv); break;
