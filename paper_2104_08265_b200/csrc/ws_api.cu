@@ -44,6 +44,7 @@ extern "C" cudaError_t wsb_launch_direct(const EventDesc& ev, const uint32_t* po
                                          const wsb::TEnt* tlist, size_t smem_bytes, cudaStream_t stream, int pdl);
 extern "C" int wsb_conv_tc_nb(const PlaneDesc& P);
 extern "C" cudaError_t wsb_launch_conv_tc(const EventDesc& ev, int nb, cudaStream_t s);
+extern "C" cudaError_t wsb_launch_conv_tc2(const EventDesc& ev, cudaStream_t s);
 extern "C" cudaError_t wsb_launch_fluctuate(const EventDesc& ev, const UnitRec* recs, const uint32_t* pool,
                                             const uint32_t* order, cudaStream_t s);
 extern "C" size_t wsb_sigproc_smem(int n);
@@ -772,12 +773,17 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
             // tensor-core direct convolution when every plane is eligible,
             // else the row FFT
             int nb = 0;
+            cudaError_t te = cudaErrorNotSupported;
             if (ev.mode == 1) {
-                nb = 4;
-                for (uint32_t i = 0; i < nd && nb; ++i)
-                    if (!ev.p[i].direct) nb = std::min(nb, wsb_conv_tc_nb(ev.p[i]));
+                te = wsb_launch_conv_tc2(ev, s);  // the pipelined kernel, where every plane is eligible
+                if (te == cudaErrorNotSupported) {
+                    (void)cudaGetLastError();
+                    nb = 4;
+                    for (uint32_t i = 0; i < nd && nb; ++i)
+                        if (!ev.p[i].direct) nb = std::min(nb, wsb_conv_tc_nb(ev.p[i]));
+                    te = nb ? wsb_launch_conv_tc(ev, nb, s) : cudaErrorNotSupported;
+                }
             }
-            cudaError_t te = nb ? wsb_launch_conv_tc(ev, nb, s) : cudaErrorNotSupported;
             if (te == cudaErrorNotSupported) {
                 (void)cudaGetLastError();
                 te = wsb_launch_conv(ev, c->pool.p, c->band_off.p, c->band_list.p, 1, smem, c->conv_variant, s);

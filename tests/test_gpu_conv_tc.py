@@ -15,6 +15,19 @@ from .helpers import oracle_grid, oracle_response, relL2_per_channel
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=["tc2", "tc2_cpasync", "tc1"], autouse=True)
+def tc_kernel(request, monkeypatch):
+    """Every case through the pipelined kernel (k_conv_tc2: TMA slab loads where
+    the plane allows them, else cp.async), its cp.async loader forced
+    (WS_CONV_TC2_TMA=0), and the one-tile-at-a-time kernel (k_conv_tc,
+    WS_CONV_TC2=0)."""
+    if request.param == "tc1":
+        monkeypatch.setenv("WS_CONV_TC2", "0")
+    if request.param == "tc2_cpasync":
+        monkeypatch.setenv("WS_CONV_TC2_TMA", "0")
+    return request.param
+
+
 def _conv(ctx, oracle, grid, resp, s):
     import torch
     plane = Plane(ctx, grid, resp)
@@ -63,3 +76,27 @@ def test_grid_convolution_delta_response_and_large_values(ctx, oracle):
     for fs, sp in [(0.0, 0.0), (0.0, 2.0), (1.0, 0.0)]:
         resp = ResponseParams(plane_kind="collection", field_sigma_t=fs, shaper_peaking=sp)
         assert _conv(ctx, oracle, grid, resp, s) < 1e-5
+
+
+def test_fluctuation_counts_past_2_11_and_2_22(ctx, oracle):
+    """Fluctuation-on frames (the walk's integer counts into the grid
+    convolution) with cells far past 2^11 and 2^22 electrons: counts below
+    2^22 enter exactly as two TF32 halves, larger ones within 2^-22."""
+    from paper_2104_08265_b200 import RngConfig, SimConfig
+    from paper_2104_08265_b200.workloads import line_tracks
+    grid = GridSpec(n_wires=180, n_ticks=900, pad_wires=20, pad_ticks=100, pitch=5.0, tick=0.5)
+    d = line_tracks(600, grid, seed=3)
+    d["q"][:40] = 60_000_000  # narrow, hot depos: cells of ~1e7 electrons
+    d["sigma_t"][:40] = 0.3
+    d["sigma_x"][:40] = 2.0
+    d["q"][40:200] = 200_000
+    resp = ResponseParams(plane_kind="induction", wire_weights=(1.0,), shaper_peaking=2.0)
+    cfg = SimConfig(grid=grid, response=resp, fluctuate=True, rng=RngConfig(mode="philox", seed=8))
+    res = Plane(ctx, grid, resp).simulate(d, cfg, want_charge=True)
+    # (the draws of these depos take binomial's normal branch, where libm ulps
+    # may move a count by a few electrons: test_gpu_overflow pins those; here
+    # the convolution of the grid the walk produced is checked)
+    s = res.charge.astype(np.int64)
+    assert s.max() > 2 ** 22 and ((s > 2 ** 11) & (s < 2 ** 22)).any()
+    m_ref = oracle.convolve(oracle_grid(grid), oracle_response(resp), s.astype(np.float64))
+    assert relL2_per_channel(res.frame, m_ref) < 1e-5
