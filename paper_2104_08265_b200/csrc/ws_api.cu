@@ -595,7 +595,7 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
     ev.total_bands = bands;
 
     // workspace
-    const size_t pool_need = std::max<size_t>(c->pool_hint, (size_t)units * (96 + (any_direct ? max_lags + 36 : 0)) + 4096);
+    const size_t pool_need = std::max<size_t>(c->pool_hint, (size_t)units * (96 + (any_direct ? max_lags + 40 : 0)) + 4096);
     WS_CUDA(c->recs.reserve(units));
     WS_CUDA(c->pool.reserve(pool_need));
     {

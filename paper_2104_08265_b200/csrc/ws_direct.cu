@@ -134,6 +134,11 @@ template <int NQ>
 __device__ __forceinline__ void scatter_rows_unrolled(const float* __restrict__ c, int rlo, int rhi, uint32_t a0,
                                                       const gtap_t* gv)
 {
+    static_assert(kTileRows <= 16, "row groups of at most 8, twice");
+    if (rhi - rlo > 8) {  // (16-row tiles) the first 8 rows, then the rest
+        RowsUnrolled<NQ, 0, 8>::run(c + rlo, a0 + (uint32_t)rlo * (4u * kRowStride), gv);
+        rlo += 8;
+    }
     const uint32_t ar = a0 + (uint32_t)rlo * (4u * kRowStride);
     const float* cr = c + rlo;
     switch (rhi - rlo) {
@@ -169,7 +174,7 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
 {
     constexpr int R = kTileRows;
     constexpr int NW = NT / 32;
-    static_assert(NW >= R && kSegs == 32 && (R & (R - 1)) == 0, "one warp per row computes the scales");
+    static_assert(NW >= R && kSegs <= 32 && (R & (R - 1)) == 0, "one warp per row computes the scales");
     constexpr int kRShift = R == 16 ? 4 : R == 8 ? 3 : R == 4 ? 2 : 1;
     const uint32_t gb = blockIdx.x;
     const PlaneDesc& P = ev.p[band_plane(ev, gb)];
@@ -224,17 +229,39 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
         __syncthreads();
     };
 
+    // the first chunk's profiles -> L2 while the bounds and scales are
+    // worked out (the warps' one-entry-ahead loads then hit L2, not DRAM)
+#ifndef WS_DIRECT_NOPF
+    if (n > 0) {
+        const int cnt0 = min(cap, n);
+        stage(0, cnt0);
+        for (int i = tid; i < cnt0 * kQ; i += NT) {
+            const int e = i / kQ, q = i - e * kQ;
+            const TEnt& d = ent[e];
+            if (32 * q < (int)(d.tsL >> 16))
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const float*>(pool + d.goff) + 32 * q));
+        }
+    }
+#endif
     // bounds of every row, one thread per (entry, row): per 64-tick segment
     // of the window the sum of |a eff g| in units of 2^ue (rounded up) over the
     // entries whose span touches it, and the largest single term; ue grows if
     // a 32-bit bound overflows (extreme charges only)
     int ue = 0;
 #pragma unroll 1
+#ifdef WS_DIRECT_NOBOUNDS  // (timing decomposition only: results wrong)
+    for (; false;) {
+#else
     for (;;) {
+#endif
 #pragma unroll 1
         for (int c0 = 0; c0 < n; c0 += cap) {
             const int cnt = min(cap, n - c0);
+#ifndef WS_DIRECT_NOPF
+            if (n > cap && !(c0 == 0 && ue == 0)) stage(c0, cnt);  // (chunk 0 staged above)
+#else
             if (n > cap || (c0 == 0 && ue == 0)) stage(c0, cnt);
+#endif
 #pragma unroll 1
             for (int i = tid; i < cnt * R; i += NT) {
                 const TEnt& d = ent[i >> kRShift];
@@ -277,7 +304,7 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
     // one-FFMA rounding, every single term below 2^22), so partial sums
     // (bound + rounding of <= 2^28 terms) stay inside int32
     if (warp < R) {
-        unsigned mx = segb[warp * kSegs + lane];
+        unsigned mx = lane < kSegs ? segb[warp * kSegs + lane] : 0u;
 #pragma unroll
         for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         if (lane == 0) {
@@ -344,7 +371,11 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
     };
 
 #pragma unroll 1
+#ifdef WS_DIRECT_NOLOOP  // (timing decomposition only: results wrong)
+    for (int c0 = 0; c0 < 0; c0 += cap) {
+#else
     for (int c0 = 0; c0 < n; c0 += cap) {
+#endif
         const int cnt = min(cap, n - c0);
         if (n > cap) stage(c0, cnt);
         // coefficients -> fixed-point units of their row
@@ -371,7 +402,11 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
 #pragma unroll
             for (int q = 0; q < kQ; ++q) gv[q] = (gtap_t)gn[q];
             load_g(e + NW, gn);
+#ifndef WS_DIRECT_NOSCATTER  // (timing decomposition only: results wrong)
             scatter(ent[e], gv);
+#else
+            if (gv[0] == (gtap_t)12345.0) scatter(ent[e], gv);
+#endif
         }
     }
     __syncthreads();
@@ -379,6 +414,10 @@ k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* 
     // frame rows of the window (convolve's real part, spectral.cpp:172-173),
     // streaming stores; one flattened (row, 16-byte word) loop. With a
     // readout (ev.ro) the same words go through noise + digitize instead.
+#ifdef WS_DIRECT_NOSTORE  // (timing decomposition only: results wrong)
+    if (acc[tid] == 0x7fffffff) P.frame[tid] = 1.0f;
+    return;
+#endif
     if constexpr (kRO) {
         if ((N & 3) == 0) {
             constexpr int kW = kTileTicks / 4;

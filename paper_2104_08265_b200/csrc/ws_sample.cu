@@ -560,9 +560,11 @@ k_sample_off(const EventDesc ev, UnitRec* __restrict__ recs, uint32_t* __restric
     const int n_eff = live && !P.ww_is_one ? f.n_w + 2 * h : 0;
     // warp-contiguous allocation, one atomic per warp: the 32 units' profiles
     // back to back [base, base + W), then their g regions (direct planes:
-    // 4 header words, g[-1] = max|g|, then ceil32(L) taps)
+    // 8 header words, g[-1] = max|g|, then ceil32(L) taps: every g starts on a
+    // 32-byte DRAM sector, so the profile writes never leave a partial sector
+    // (a read-modify-write under HBM3's ECC; r2: 72 -> see DESIGN)
     const uint32_t words = live ? (uint32_t)(f.n_w + n_eff + f.n_t) : 0u;
-    const uint32_t gneed = (live && ev.mode == 0 && P.direct) ? (((uint32_t)(f.n_t + P.n_lags - 1) + 31u) & ~31u) + 4u
+    const uint32_t gneed = (live && ev.mode == 0 && P.direct) ? (((uint32_t)(f.n_t + P.n_lags - 1) + 31u) & ~31u) + 8u
                                                                : 0u;
     uint32_t wex = words, gex = gneed;  // inclusive scans -> exclusive below
 #pragma unroll
@@ -578,10 +580,10 @@ k_sample_off(const EventDesc ev, UnitRec* __restrict__ recs, uint32_t* __restric
     gex -= gneed;
     const uint32_t w_pad = (w_tot + 3u) & ~3u;
     uint32_t base = 0;
-    if (lane == 0 && w_tot + g_tot) base = atomicAdd(pool_ctr, w_pad + g_tot + 4u);
+    if (lane == 0 && w_tot + g_tot) base = atomicAdd(pool_ctr, w_pad + g_tot + 8u);
     base = __shfl_sync(0xffffffffu, base, 0);
-    const uint32_t gbase = (base + w_pad + 3u) & ~3u;  // 16-byte aligned
-    if ((uint64_t)base + w_pad + g_tot + 4u > pool_cap && (w_tot + g_tot)) {
+    const uint32_t gbase = (base + w_pad + 7u) & ~7u;  // 32-byte aligned
+    if ((uint64_t)base + w_pad + g_tot + 8u > pool_cap && (w_tot + g_tot)) {
         if (live) atomicOr(err, kErrPool);
         live = false;
     }
@@ -598,7 +600,7 @@ k_sample_off(const EventDesc ev, UnitRec* __restrict__ recs, uint32_t* __restric
     double sw_all = 0.0, mw_all = 0.0;  // over every impact (== sw, mw without impact positions)
     float* raw = reinterpret_cast<float*>(pool + off);
     if (live) {
-        rec.goff = gneed ? gbase + gex + 4u : 0u;
+        rec.goff = gneed ? gbase + gex + 8u : 0u;
         const double wire_edge = P.origin_x + ((double)f.w0 - (double)P.pad_w) * P.pitch;
         const double tick_edge = P.origin_t + ((double)f.t0 - (double)P.pad_t) * P.tick;
         float* dst = staged ? stage + wex : raw;
