@@ -45,8 +45,10 @@ extern "C" cudaError_t wsb_launch_direct(const EventDesc& ev, const uint32_t* po
 extern "C" int wsb_conv_tc_nb(const PlaneDesc& P);
 extern "C" cudaError_t wsb_launch_conv_tc(const EventDesc& ev, int nb, cudaStream_t s);
 extern "C" cudaError_t wsb_launch_conv_tc2(const EventDesc& ev, cudaStream_t s);
+extern "C" size_t wsb_fluct_scratch_bytes(uint32_t n);
+extern "C" cudaError_t wsb_launch_zero(void* p, size_t bytes, cudaStream_t s);
 extern "C" cudaError_t wsb_launch_fluctuate(const EventDesc& ev, const UnitRec* recs, const uint32_t* pool,
-                                            const uint32_t* order, cudaStream_t s);
+                                            const uint32_t* order, void* scratch, cudaStream_t s);
 extern "C" size_t wsb_sigproc_smem(int n);
 extern "C" int wsb_sigproc_max_n();
 extern "C" int wsb_sigproc_dft_max_n();
@@ -160,6 +162,7 @@ struct ws_ctx {
     DevBuf<unsigned long long> counts;  // fluctuation on: the integer charge grids (u64 counts)
     DevBuf<double> recip;               // RN(1/j), j < kRecipN: the exact walk's divisions
     DevBuf<double> fl_bins;             // exact walk: per-bin draw records (32 B each, ws_sample.cu FlRec)
+    DevBuf<unsigned char> fl_scratch;   // exact walk: sort keys / values, offsets, CUB temporaries
     size_t fl_hint = 0;                 // records needed by the last overflowing call
     DevBuf<unsigned char> out_stage;  // ws_run_*: device staging of the readout outputs (ADC / fp64 frames)
     DevBuf<double> noise_amp;  // spectrum-mode amplitudes of the last ws_noise_digitize_device
@@ -177,6 +180,7 @@ struct ws_ctx {
     cudaEvent_t aux_fork = nullptr, aux_join = nullptr;
     cudaEvent_t slot_computed[2] = {nullptr, nullptr};
     cudaEvent_t slot_copied[2] = {nullptr, nullptr};
+    cudaEvent_t slot_loaded[2] = {nullptr, nullptr};  // ws_run_events: the slot's depos are on the device
     // sigproc chain: plan of the last row length + staging of the host path
     uint64_t sp_n = 0;
     bool sp_dft = false;  // direct-DFT plan (a prime factor > 13)
@@ -461,7 +465,12 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
 {
     cudaStream_t s = c->stream;
     EventDesc ev{};
-    const bool ro_fused = ro && readout_fused(ro->spec);
+    // the readout is fused into the frame stores of the fluctuation-off
+    // kernels; behind a given grid's convolution (k_conv_tc2: four epilogue
+    // warps per SM) the fp64 noise math would run at a fraction of the GPU,
+    // so that path writes the fp32 frame and the full-GPU pair kernel follows
+    const bool grid_conv = charge_in != nullptr || (opt && opt->fluctuate);
+    const bool ro_fused = ro && readout_fused(ro->spec) && !grid_conv;
     if (ro_fused) {
         const ws_readout& r = *ro->spec;
         ev.ro = 1;
@@ -679,9 +688,11 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
 
     if (ev.fluctuate && !from_grid)
         for (uint32_t i = 0; i < nd; ++i)
-            if (ev.p[i].charge_cnt)
-                WS_CUDA(cudaMemsetAsync(ev.p[i].charge_cnt, 0, sizeof(unsigned long long) * (size_t)ev.p[i].W * ev.p[i].N,
+            if (ev.p[i].charge_cnt) {
+                WS_CUDA(wsb_launch_zero(ev.p[i].charge_cnt, sizeof(unsigned long long) * (size_t)ev.p[i].W * ev.p[i].N,
                                         s));
+                c->launches += 1;
+            }
     if (!from_grid) {
         WS_CUDA(wsb_launch_sample(ev, c->recs.p, c->pool.p, (uint32_t)std::min<size_t>(c->pool.cap, 0xffffffffu),
                                   &hdr->pool_ctr, c->band_count.p, &hdr->err, s, timing ? 0 : 1));
@@ -710,8 +721,13 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
             ev.fl_cap = c->fl_bins.cap / 4;
             ev.fl_ctr = &hdr->fl_ctr;
         }
-        WS_CUDA(wsb_launch_fluctuate(ev, c->recs.p, c->pool.p, nullptr, s));
-        c->launches += units ? (ev.approx ? 1 : 4) : 0;  // exact: keys, records, walk, normal-branch units (the CUB sort is library code)
+        void* scratch = nullptr;
+        if (!ev.approx && units) {
+            WS_CUDA(c->fl_scratch.reserve(wsb_fluct_scratch_bytes(units)));
+            scratch = c->fl_scratch.p;
+        }
+        WS_CUDA(wsb_launch_fluctuate(ev, c->recs.p, c->pool.p, nullptr, scratch, s));
+        c->launches += units ? (ev.approx ? 1 : 7) : 0;  // exact: 4 scheduling-sort kernels, records, walk, normal-branch units
     }
     if (timing) WS_CUDA(cudaEventRecord(pc.ev[2], s));  // stage timing only
     if (ev.mode == 0) {
@@ -808,7 +824,8 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
                 WS_CUDA(wsb_launch_noise_spectrum(d, c->noise_amp.p, r.noise.seed, r.noise.rng_mode, d.frame, sk,
                                                   c->conv_variant, s));
             } else {
-                WS_CUDA(wsb_launch_noise(d.frame, sk, d.W, d.N, 1, r.noise.rng_mode, r.noise.sigma, r.noise.seed, s));
+                const int noisy = r.noise.mode == WS_NOISE_WHITE && r.noise.sigma != 0.0 ? 1 : 0;  // else digitize only
+                WS_CUDA(wsb_launch_noise(d.frame, sk, d.W, d.N, noisy, r.noise.rng_mode, r.noise.sigma, r.noise.seed, s));
             }
             c->launches += 1;
         }
@@ -1003,6 +1020,7 @@ int ws_ctx_destroy(ws_ctx* c)
     c->counts.release();
     c->recip.release();
     c->fl_bins.release();
+    c->fl_scratch.release();
     c->ro_scratch.release();
     c->out_stage.release();
     c->noise_amp.release();
@@ -1022,6 +1040,7 @@ int ws_ctx_destroy(ws_ctx* c)
     if (c->aux_join) cudaEventDestroy(c->aux_join);
     for (int s = 0; s < 2; ++s) {
         if (c->slot_computed[s]) cudaEventDestroy(c->slot_computed[s]);
+        if (c->slot_loaded[s]) cudaEventDestroy(c->slot_loaded[s]);
         if (c->slot_copied[s]) cudaEventDestroy(c->slot_copied[s]);
     }
     c->sp_tw.release();
@@ -1468,9 +1487,11 @@ int events_host(ws_ctx* ctx, uint32_t n_events, uint32_t n_planes, ws_plane* con
     WS_CUDA(cudaSetDevice(ctx->device));
     if (int rc = finish_pending(ctx)) return rc;
     if (!ctx->copy_stream) WS_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    if (!ctx->h2d_stream) WS_CUDA(cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking));
     for (int s = 0; s < 2; ++s) {
         if (!ctx->slot_computed[s]) WS_CUDA(cudaEventCreateWithFlags(&ctx->slot_computed[s], cudaEventDisableTiming));
         if (!ctx->slot_copied[s]) WS_CUDA(cudaEventCreateWithFlags(&ctx->slot_copied[s], cudaEventDisableTiming));
+        if (!ctx->slot_loaded[s]) WS_CUDA(cudaEventCreateWithFlags(&ctx->slot_loaded[s], cudaEventDisableTiming));
     }
     const size_t total = (size_t)n_events * n_planes;
     auto any = [&](void* const* a) {
@@ -1519,6 +1540,10 @@ int events_host(ws_ctx* ctx, uint32_t n_events, uint32_t n_planes, ws_plane* con
             const int slot = (int)(j & 1u);
             rc = [&]() -> int {
                 if (j >= 2) WS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->slot_copied[slot], 0));
+                // the depos go in on their own stream (a copy engine of their
+                // own): this event's H2D overlaps the previous event's compute,
+                // once the slot's last user (two events back) has computed
+                if (j >= 2) WS_CUDA(cudaStreamWaitEvent(ctx->h2d_stream, ctx->slot_computed[slot], 0));
                 size_t uo = (size_t)slot * max_units;
                 unsigned char* base = stage + (size_t)slot * slot_bytes;
                 for (uint32_t i = 0; i < n_planes; ++i) {
@@ -1526,12 +1551,14 @@ int events_host(ws_ctx* ctx, uint32_t n_events, uint32_t n_planes, ws_plane* con
                     dd[i] = ctx->depos.p + uo;
                     if (n_depos[k])
                         WS_CUDA(cudaMemcpyAsync(ctx->depos.p + uo, depos[k], sizeof(ws_depo) * n_depos[k],
-                                                cudaMemcpyHostToDevice, ctx->stream));
+                                                cudaMemcpyHostToDevice, ctx->h2d_stream));
                     uo += n_depos[k];
                     df[i] = frames && frames[k] ? base + off_f[i] : nullptr;
                     da[i] = want_a && adcs[k] ? base + off_a[i] : nullptr;
                     dc[i] = want_c && charges[k] ? reinterpret_cast<float*>(base + off_c[i]) : nullptr;
                 }
+                WS_CUDA(cudaEventRecord(ctx->slot_loaded[slot], ctx->h2d_stream));
+                WS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->slot_loaded[slot], 0));
                 ctx->call_tag = (int)e;
                 const int r = event_device(ctx, n_planes, planes, dd.data(), n_depos + (size_t)e * n_planes, opt, spec,
                                            df.data(), da.data(), want_c ? dc.data() : nullptr,
@@ -1558,7 +1585,9 @@ int events_host(ws_ctx* ctx, uint32_t n_events, uint32_t n_planes, ws_plane* con
             }();
         }
         // every copy has landed before this returns, whatever happened
-        const cudaError_t ce = cudaStreamSynchronize(ctx->copy_stream);
+        const cudaError_t he = cudaStreamSynchronize(ctx->h2d_stream);  // (host depos no longer read)
+        cudaError_t ce = cudaStreamSynchronize(ctx->copy_stream);
+        if (ce == cudaSuccess) ce = he;
         if (rc == WS_OK && ce != cudaSuccess)
             rc = set_err(WS_ECUDA, "copy stream: %s", cudaGetErrorString(ce));
         const int frc = finish_pending(ctx);

@@ -851,14 +851,27 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_conv_tc2(const EventDesc ev, 
                             if (tv && col >= 2 * H && col < cmax) __stcs(frame + off, out);
                         }
                     } else {
-#pragma unroll 1
+                        // fused readout (noise + digitize) on tick pairs: even lanes
+                        // take their odd neighbour's value; stencil unrolled over
+                        // the chunk's columns, the readout call kept out of line
+                        float outv[32];
+#pragma unroll
                         for (int cc = 0; cc < 32; ++cc) {
-                            const int col = 32 * ck + cc, o = col - 2 * H;
                             float out = 0.0f;
+#pragma unroll
                             for (int e = 0; e <= 2 * H; ++e)
                                 out = __fmaf_rn(ww[e], cc - e >= 0 ? __uint_as_float(x[cc - e]) : carry[2 * H + cc - e], out);
-                            const float nxt = __shfl_down_sync(0xffffffffu, out, 1);
-                            if (o >= 0 && o < I.nr && !(lane & 1) && tv) readout_pair(ev, P, I.r0 + o, t, out, nxt, t + 1 < Nt);
+                            outv[cc] = out;
+                        }
+                        float nxtv[32];
+#pragma unroll
+                        for (int cc = 0; cc < 32; ++cc) nxtv[cc] = __shfl_down_sync(0xffffffffu, outv[cc], 1);
+                        if (!(lane & 1) && tv) {
+#pragma unroll 1
+                            for (int cc = 0; cc < 32; ++cc) {
+                                const int o = 32 * ck + cc - 2 * H;
+                                if (o >= 0 && o < I.nr) readout_pair(ev, P, I.r0 + o, t, outv[cc], nxtv[cc], t + 1 < Nt);
+                            }
                         }
                     }
                     // the last 2H columns feed the next chunk's first outputs

@@ -9,7 +9,6 @@
 
 #include <algorithm>
 
-#include <cub/device/device_radix_sort.cuh>
 
 namespace wsb {
 
@@ -866,19 +865,95 @@ __global__ void k_fluctuate(const EventDesc ev, const UnitRec* __restrict__ recs
 // quarter of the warp's live lanes have finished their draws does the warp
 // set up the next draws (RNG, pmf seed) together. The integer grid is
 // unchanged (same draws, same order per depo; exact integer atomics).
-// walk-length key of every unit (the walk is ~q steps): warps of similar
-// charge keep their lanes busy together
-__global__ void k_fluct_keys(const EventDesc ev, const UnitRec* __restrict__ recs, uint32_t* __restrict__ keys,
-                             uint32_t* __restrict__ vals, uint32_t* __restrict__ bins)
+// Scheduling orders of the exact walk, by bucket (counting) sort: units by
+// descending charge (the walk is ~q steps: warps of similar charge keep their
+// lanes busy together) and by descending bin count (k_fluct_prep's per-lane
+// work). Only the schedule depends on these orders, never the counts (each
+// unit's draws come from its own stream), so buckets need not be exact and
+// the order inside a bucket may vary. No memsets: a large CUB sort's
+// cudaMemsetAsync calls queue on a copy engine behind the previous event's
+// frame copies (end-to-end calls).
+constexpr int kFlBq = 1056;  // charge buckets: 0 (q <= 0), then log2 x 32 sub-buckets
+constexpr int kFlBb = 4096;  // bin-count buckets (counts >= 4095 share the last)
+__device__ __forceinline__ uint32_t fl_bucket_q(int64_t q)
+{
+    if (q <= 0) return 0u;
+    const uint64_t v = (uint64_t)q;
+    const int l = 63 - __clzll((long long)v);
+    const uint32_t frac = l >= 5 ? (uint32_t)(v >> (l - 5)) & 31u : (uint32_t)(v << (5 - l)) & 31u;
+    return min(1u + 32u * (uint32_t)l + frac, (uint32_t)kFlBq - 1u);
+}
+__global__ void k_fluct_hist_zero(uint32_t* __restrict__ hist, uint32_t* __restrict__ n_slow)
+{
+    for (int i = threadIdx.x; i < kFlBq + kFlBb; i += blockDim.x) hist[i] = 0u;
+    if (threadIdx.x == 0) n_slow[0] = 0u;
+}
+__global__ void k_fluct_keys(const EventDesc ev, const UnitRec* __restrict__ recs, uint32_t* __restrict__ bq,
+                             uint32_t* __restrict__ bb, uint32_t* __restrict__ hist)
 {
     const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
     if (u >= ev.total_units) return;
     const PlaneDesc& P = ev.p[plane_of_unit(ev, u)];
     const UnitRec r = recs[u];
     const int64_t q = r.w0 >= 0 ? P.depos[u - P.unit_base].q : 0;
-    keys[u] = (uint32_t)(q < 0 ? 0 : (q > 0xffffffffll ? 0xffffffffll : q));
-    vals[u] = u;
-    if (bins) bins[u] = r.w0 >= 0 ? (uint32_t)(r.n_w * r.n_t) : 0u;  // k_fluct_prep's per-lane work
+    const uint32_t kq = (uint32_t)kFlBq - 1u - fl_bucket_q(q);  // descending
+    const uint32_t kb = (uint32_t)kFlBb - 1u - (r.w0 >= 0 ? min((uint32_t)(r.n_w * r.n_t), (uint32_t)kFlBb - 1u) : 0u);
+    bq[u] = kq;
+    bb[u] = kb;
+    // one atomic per distinct bucket of the warp (neighbouring depos of a
+    // track share buckets)
+    const unsigned act = __activemask();
+    const unsigned pq = __match_any_sync(act, kq), pb = __match_any_sync(act, kb);
+    const int lane = threadIdx.x & 31;
+    if (lane == __ffs(pq) - 1) atomicAdd(&hist[kq], (uint32_t)__popc(pq));
+    if (lane == __ffs(pb) - 1) atomicAdd(&hist[kFlBq + kb], (uint32_t)__popc(pb));
+}
+// exclusive scans of both histograms, in place (one block)
+__global__ void __launch_bounds__(1024) k_fluct_hist_scan(uint32_t* __restrict__ hist)
+{
+    __shared__ uint32_t part[1024];
+    for (int h = 0; h < 2; ++h) {
+        uint32_t* a = hist + (h ? kFlBq : 0);
+        const int n = h ? kFlBb : kFlBq;
+        const int per = (n + 1023) / 1024, i0 = threadIdx.x * per;
+        uint32_t sum = 0;
+        for (int i = i0; i < min(i0 + per, n); ++i) sum += a[i];
+        part[threadIdx.x] = sum;
+        __syncthreads();
+        for (int o = 1; o < 1024; o <<= 1) {
+            const uint32_t v = threadIdx.x >= o ? part[threadIdx.x - o] : 0u;
+            __syncthreads();
+            part[threadIdx.x] += v;
+            __syncthreads();
+        }
+        uint32_t run = part[threadIdx.x] - sum;
+        for (int i = i0; i < min(i0 + per, n); ++i) {
+            const uint32_t c = a[i];
+            a[i] = run;
+            run += c;
+        }
+        __syncthreads();
+    }
+}
+__global__ void k_fluct_scatter(uint32_t n, const uint32_t* __restrict__ bq, const uint32_t* __restrict__ bb,
+                                uint32_t* __restrict__ hist, uint32_t* __restrict__ by_q, uint32_t* __restrict__ by_b)
+{
+    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= n) return;
+    const uint32_t kq = bq[u], kb = kFlBq + bb[u];
+    const unsigned act = __activemask();
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    // warp-aggregated slot claims: the bucket's leader claims for its peers
+    const unsigned pq = __match_any_sync(act, kq), pb = __match_any_sync(act, kb);
+    const int lq = __ffs(pq) - 1, lb = __ffs(pb) - 1;
+    uint32_t baseq = 0, baseb = 0;
+    if (lane == lq) baseq = atomicAdd(&hist[kq], (uint32_t)__popc(pq));
+    if (lane == lb) baseb = atomicAdd(&hist[kb], (uint32_t)__popc(pb));
+    baseq = __shfl_sync(act, baseq, lq);
+    baseb = __shfl_sync(act, baseb, lb);
+    by_q[baseq + __popc(pq & lt)] = u;
+    by_b[baseb + __popc(pb & lt)] = u;
 }
 
 // n_list (nullable): the number of entries of `order` (device), else total_units
@@ -1478,6 +1553,29 @@ extern "C" cudaError_t wsb_launch_sample(const wsb::EventDesc& ev, wsb::UnitRec*
     return cudaGetLastError();
 }
 
+// Zero n 16-byte words on the SMs (a large cudaMemsetAsync may run on a copy
+// engine, where it queues behind the previous event's frame copies)
+namespace wsb {
+__global__ void k_zero16(uint4* __restrict__ p, size_t n)
+{
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        p[i] = make_uint4(0u, 0u, 0u, 0u);
+}
+}  // namespace wsb
+
+extern "C" cudaError_t wsb_launch_zero(void* p, size_t bytes, cudaStream_t s)
+{
+    if (bytes == 0) return cudaSuccess;
+    if ((reinterpret_cast<uintptr_t>(p) | bytes) & 15) return cudaMemsetAsync(p, 0, bytes, s);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t n = bytes / 16;
+    const unsigned blocks = (unsigned)std::min<size_t>((n + 255) / 256, (size_t)sms * 8);
+    wsb::k_zero16<<<blocks, 256, 0, s>>>(static_cast<uint4*>(p), n);
+    return cudaGetLastError();
+}
+
 extern "C" cudaError_t wsb_launch_scan(uint32_t* count, uint32_t* off, uint32_t* fill, uint32_t n, cudaStream_t s)
 {
     wsb::k_scan_bands<<<1, 1024, 0, s>>>(count, off, fill, n);
@@ -1493,8 +1591,17 @@ extern "C" cudaError_t wsb_launch_fill(const wsb::EventDesc& ev, const wsb::Unit
     return cudaGetLastError();
 }
 
+// Scratch of the exact walk for n units: bucket keys, the two schedules,
+// record offsets, the normal-branch list, counters and the bucket histograms.
+extern "C" size_t wsb_fluct_scratch_bytes(uint32_t n)
+{
+    return sizeof(uint32_t) * (6 * (size_t)n + 4 + wsb::kFlBq + wsb::kFlBb);
+}
+
+// scratch: wsb_fluct_scratch_bytes(ev.total_units) bytes of device memory the
+// caller keeps (a context buffer: no allocation per call)
 extern "C" cudaError_t wsb_launch_fluctuate(const wsb::EventDesc& ev, const wsb::UnitRec* recs, const uint32_t* pool,
-                                            const uint32_t* order, cudaStream_t s)
+                                            const uint32_t* order, void* scratch, cudaStream_t s)
 {
     if (ev.total_units == 0) return cudaSuccess;
     if (ev.approx) {
@@ -1502,30 +1609,20 @@ extern "C" cudaError_t wsb_launch_fluctuate(const wsb::EventDesc& ev, const wsb:
         return cudaGetLastError();
     }
     // exact walk: the units in descending charge for the walk and by bin count
-    // for the records (CUB radix sorts, stream-ordered scratch), the per-bin
+    // for the records (bucket sorts in the caller's scratch), the per-bin
     // records (k_fluct_prep), the walk (k_fluct_walk), then the units that
     // could take binomial's normal branch (k_fluctuate_exact)
     const uint32_t n = ev.total_units;
-    uint32_t* buf = nullptr;
-    size_t temp = 0;
-    cudaError_t e = cub::DeviceRadixSort::SortPairsDescending(nullptr, temp, (const uint32_t*)nullptr,
-                                                              (uint32_t*)nullptr, (const uint32_t*)nullptr,
-                                                              (uint32_t*)nullptr, (int)n, 0, 32, s);
-    if (e != cudaSuccess) return e;
-    temp = (temp + 15) & ~(size_t)15;
-    e = cudaMallocAsync(reinterpret_cast<void**>(&buf), sizeof(uint32_t) * (8 * (size_t)n + 4) + temp, s);
-    if (e != cudaSuccess) return e;
-    uint32_t *k_in = buf, *k_out = buf + n, *v_in = buf + 2 * (size_t)n, *v_out = buf + 3 * (size_t)n;
-    uint32_t *offs = buf + 4 * (size_t)n, *slow = buf + 5 * (size_t)n, *b_in = buf + 6 * (size_t)n;
-    uint32_t *b_order = buf + 7 * (size_t)n, *n_slow = buf + 8 * (size_t)n, *cursor = n_slow + 1;
-    void* sort_tmp = reinterpret_cast<unsigned char*>(buf + 8 * (size_t)n + 4);
+    uint32_t* buf = static_cast<uint32_t*>(scratch);
+    uint32_t *bq = buf, *bb = buf + n, *v_out = buf + 2 * (size_t)n, *b_order = buf + 3 * (size_t)n;
+    uint32_t *offs = buf + 4 * (size_t)n, *slow = buf + 5 * (size_t)n;
+    uint32_t *n_slow = buf + 6 * (size_t)n, *cursor = n_slow + 1, *hist = n_slow + 4;
     const unsigned blocks = (n + 127) / 128;
-    wsb::k_fluct_keys<<<(n + 255) / 256, 256, 0, s>>>(ev, recs, k_in, v_in, b_in);
-    e = cudaMemsetAsync(n_slow, 0, sizeof(uint32_t), s);
-    if (e == cudaSuccess)
-        e = cub::DeviceRadixSort::SortPairsDescending(sort_tmp, temp, k_in, k_out, v_in, v_out, (int)n, 0, 32, s);
-    if (e == cudaSuccess)  // (k_out is free again: the bin-count keys' sorted output)
-        e = cub::DeviceRadixSort::SortPairsDescending(sort_tmp, temp, b_in, k_out, v_in, b_order, (int)n, 0, 32, s);
+    cudaError_t e = cudaSuccess;
+    wsb::k_fluct_hist_zero<<<1, 1024, 0, s>>>(hist, n_slow);
+    wsb::k_fluct_keys<<<(n + 255) / 256, 256, 0, s>>>(ev, recs, bq, bb, hist);
+    wsb::k_fluct_hist_scan<<<1, 1024, 0, s>>>(hist);
+    wsb::k_fluct_scatter<<<(n + 255) / 256, 256, 0, s>>>(n, bq, bb, hist, v_out, b_order);
     if (e == cudaSuccess) {
         // persistent walk: one resident wave of lanes pulling units from a cursor
         int dev = 0, sms = 148, per_sm = 1;
@@ -1537,8 +1634,6 @@ extern "C" cudaError_t wsb_launch_fluctuate(const wsb::EventDesc& ev, const wsb:
         wsb::k_fluct_walk<<<wblocks, 128, 0, s>>>(ev, recs, v_out, offs, cursor);
         wsb::k_fluctuate_exact<<<blocks, 128, 0, s>>>(ev, recs, pool, slow, n_slow);
     }
-    const cudaError_t e2 = cudaFreeAsync(buf, s);
     if (e != cudaSuccess) return e;
-    if (e2 != cudaSuccess) return e2;
     return cudaGetLastError();
 }
