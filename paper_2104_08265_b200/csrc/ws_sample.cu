@@ -1156,7 +1156,7 @@ __global__ void __launch_bounds__(128) k_fluctuate_exact(const EventDesc ev, con
 // whole (kErrFluct only tells the host to grow the buffer).
 constexpr uint32_t kFlNone = 0xffffffffu;
 #ifndef WS_FLWALK_MINB
-#define WS_FLWALK_MINB 8  // 64 registers, 32 warps per SM (r2: 6.67 vs 7.25 ms per C3 event at 78 registers)
+#define WS_FLWALK_MINB 7  // 72 registers, 28 warps per SM (with 7 CDF steps per iteration; 64 registers spilled)
 #endif
 #ifndef WS_FLWALK_PF
 #define WS_FLWALK_PF 3
@@ -1450,7 +1450,10 @@ __global__ void __launch_bounds__(128, WS_FLWALK_MINB) k_fluct_walk(const EventD
         }
     };
 
-    constexpr int kWalk = 4;
+#ifndef WS_FL_KWALK
+#define WS_FL_KWALK 7  // CDF steps per iteration (r2 sweep 2-12 at 64 / 72 / 80 registers: 7 at 72, 4.12 -> 3.6 ms)
+#endif
+    constexpr int kWalk = WS_FL_KWALK;
 #pragma unroll 1
     for (;;) {
         setup();
