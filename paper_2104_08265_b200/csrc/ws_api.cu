@@ -710,7 +710,7 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
         ev.recip = c->recip.p;
         static const int quorum = [] {
             const char* v = getenv("WS_FLUCT_QUORUM");  // tuning only
-            return v ? std::max(1, std::min(16, atoi(v))) : 8;  // (r2 sweep with one settled draw per pass: 6-8 best)
+            return v ? std::max(1, std::min(16, atoi(v))) : 6;  // (r2 sweeps: 6 best with 7 steps and one settled draw per pass)
         }();
         ev.fl_quorum = quorum;
         if (!ev.approx) {
