@@ -34,7 +34,7 @@ extern "C" cudaError_t wsb_launch_gprof(const EventDesc& ev, const UnitRec* recs
 extern "C" cudaError_t wsb_launch_noise(const float* in, const wsb::Sink& out, int W, int N, int noise, int rng_mode,
                                         double sigma, uint64_t seed, cudaStream_t s);
 extern "C" cudaError_t wsb_launch_counts_out(const unsigned long long* g, void* out, int type, size_t n, unsigned* err,
-                                             cudaStream_t s);
+                                             const unsigned long long* qsum, cudaStream_t s);
 extern "C" cudaError_t wsb_launch_noise_spectrum(const wsb::PlaneDesc& P, const double* amp, uint64_t seed, int rng_mode,
                                                  const float* in, const wsb::Sink& out, int variant,
                                                  cudaStream_t stream);
@@ -47,6 +47,7 @@ extern "C" cudaError_t wsb_launch_conv_tc(const EventDesc& ev, int nb, cudaStrea
 extern "C" cudaError_t wsb_launch_conv_tc2(const EventDesc& ev, cudaStream_t s);
 extern "C" size_t wsb_fluct_scratch_bytes(uint32_t n);
 extern "C" cudaError_t wsb_launch_zero(void* p, size_t bytes, cudaStream_t s);
+extern "C" cudaError_t wsb_launch_zero_counts(void* p, size_t cells, const unsigned long long* qsum, cudaStream_t s);
 extern "C" cudaError_t wsb_launch_fluctuate(const EventDesc& ev, const UnitRec* recs, const uint32_t* pool,
                                             const uint32_t* order, void* scratch, cudaStream_t s);
 extern "C" size_t wsb_sigproc_smem(int n);
@@ -121,6 +122,7 @@ struct ScratchHeader {
     long long stats[2 * wsb::kMaxPlanes];
     uint32_t tile_need[wsb::kMaxPlanes];
     unsigned long long fl_ctr;  // exact walk: draw records allocated (the need after a kErrFluct)
+    unsigned long long qsum[wsb::kMaxPlanes];  // fluctuation on: each plane's electrons (count-grid cell width)
 };
 
 struct PendingCall {
@@ -665,6 +667,7 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
     for (uint32_t i = 0; i < nd; ++i) {
         ev.p[i].stats = &hdr->stats[2 * i];
         ev.p[i].tile_need = &hdr->tile_need[i];
+        ev.p[i].cnt_qsum = ev.p[i].charge_cnt ? &hdr->qsum[i] : nullptr;
     }
     ev.list_need = &hdr->list_need;
     ev.err = &hdr->err;
@@ -686,18 +689,19 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
 
     if (timing) WS_CUDA(cudaEventRecord(pc.ev[0], s));  // stage timing only
 
-    if (ev.fluctuate && !from_grid)
-        for (uint32_t i = 0; i < nd; ++i)
-            if (ev.p[i].charge_cnt) {
-                WS_CUDA(wsb_launch_zero(ev.p[i].charge_cnt, sizeof(unsigned long long) * (size_t)ev.p[i].W * ev.p[i].N,
-                                        s));
-                c->launches += 1;
-            }
     if (!from_grid) {
         WS_CUDA(wsb_launch_sample(ev, c->recs.p, c->pool.p, (uint32_t)std::min<size_t>(c->pool.cap, 0xffffffffu),
                                   &hdr->pool_ctr, c->band_count.p, &hdr->err, s, timing ? 0 : 1));
         c->launches += units ? 1 : 0;
     }
+    // the count grids at the cell width the sampler's electron sums chose (u32
+    // below 2^32 electrons per plane), zeroed on the SMs
+    if (ev.fluctuate && !from_grid)
+        for (uint32_t i = 0; i < nd; ++i)
+            if (ev.p[i].charge_cnt) {
+                WS_CUDA(wsb_launch_zero_counts(ev.p[i].charge_cnt, (size_t)ev.p[i].W * ev.p[i].N, ev.p[i].cnt_qsum, s));
+                c->launches += 1;
+            }
     if (timing) WS_CUDA(cudaEventRecord(pc.ev[1], s));  // stage timing only
     if (ev.fluctuate && !from_grid) {
         if (!c->recip.p) {
@@ -834,7 +838,8 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
         for (uint32_t i = 0; i < n; ++i) {  // the caller's charge output: the counts in its type
             const PlaneDesc& d = ev.p[desc_of[i]];
             if (!charges[i]) continue;
-            WS_CUDA(wsb_launch_counts_out(d.charge_cnt, charges[i], opt->charge_type, (size_t)d.W * d.N, &hdr->err, s));
+            WS_CUDA(wsb_launch_counts_out(d.charge_cnt, charges[i], opt->charge_type, (size_t)d.W * d.N, &hdr->err,
+                                          d.cnt_qsum, s));
             c->launches += 1;
         }
     if (timing) WS_CUDA(cudaEventRecord(pc.ev[4], s));  // stage timing only

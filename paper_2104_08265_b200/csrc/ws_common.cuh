@@ -102,10 +102,44 @@ struct PlaneDesc {
     void* adc;                 // out: digitized codes, int32 or uint16 per EventDesc::adc_u16 (readout, nullable)
     float* charge_out;         // out: S (nullable)
     const float* charge_in;    // in: S (mode "grid")
-    unsigned long long* charge_cnt;  // fluctuation on: the integer charge grid (u64 counts, mode 1 reads it)
+    unsigned long long* charge_cnt;  // fluctuation on: the integer charge grid (mode 1 reads it): u64 counts, or
+                                     // u32 counts when the plane's depos carry < 2^32 electrons in all (cnt_wide)
+    const unsigned long long* cnt_qsum;  // fluctuation on: the plane's sum of min(q, 2^32), set by k_sample
     long long* stats;          // [0] clipped_charge, [1] clipped_patches
     uint32_t* tile_need;       // fixed tile lists: the largest slot + 1 that did not fit (atomicMax, 0 = none)
 };
+
+// The count grid's cell width: a cell never holds more electrons than the
+// plane's depos carry in all, so below 2^32 electrons u32 cells are exact (the
+// reference's ChargeGrid is int64; half the zeroing and the convolution's reads)
+__device__ __forceinline__ bool cnt_wide(const PlaneDesc& P)
+{
+    return !P.cnt_qsum || *P.cnt_qsum >= (1ull << 32);
+}
+
+// A cell of the count grid (u64 or u32 cells)
+struct CellPtr {
+    unsigned char* p;
+    int shift;  // 3: u64 cells, 2: u32
+    __device__ __forceinline__ void advance(long long n) { p += n << shift; }
+    __device__ __forceinline__ void add(int64_t k) const
+    {
+        if (k <= 0) return;
+        if (shift == 3) atomicAdd(reinterpret_cast<unsigned long long*>(p), (unsigned long long)k);
+        else atomicAdd(reinterpret_cast<unsigned*>(p), (unsigned)k);
+    }
+};
+__device__ __forceinline__ CellPtr cell_at(const PlaneDesc& P, size_t i, bool wide)
+{
+    CellPtr c;
+    c.shift = wide ? 3 : 2;
+    c.p = reinterpret_cast<unsigned char*>(P.charge_cnt) + (i << c.shift);
+    return c;
+}
+__device__ __forceinline__ unsigned long long count_at(const PlaneDesc& P, size_t i, bool wide)
+{
+    return wide ? __ldg(P.charge_cnt + i) : (unsigned long long)__ldg(reinterpret_cast<const unsigned*>(P.charge_cnt) + i);
+}
 
 struct EventDesc {
     int32_t n_planes;

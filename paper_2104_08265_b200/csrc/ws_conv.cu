@@ -228,7 +228,7 @@ k_conv(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* __
                         int src = (w - dw) % W;
                         if (src < 0) src += W;
                         // the integer grid of the fluctuation walk, or a float grid (ws_convolve_device)
-                        const float q = P.charge_cnt ? (float)__ldg(&P.charge_cnt[(size_t)src * N + t])
+                        const float q = P.charge_cnt ? (float)count_at(P, (size_t)src * N + t, cnt_wide(P))
                                                      : __ldg(&P.charge_in[(size_t)src * N + t]);
                         s += (float)P.ww[dw + P.h] * q;
                     }

@@ -157,6 +157,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_conv_tc(const EventDesc ev, i
     if (sw < 0) sw += W;
     const int nk4 = g.kwin >> 2;
     const bool vec = (Nt & 3) == 0;
+    const bool wide = KSRC == 0 && cnt_wide(P);  // u64 or u32 count cells
     auto load_round = [&](int rho) {
         unsigned long long mx = 0ull;
         // items k4 = warp + 8 i, four ticks each; kB items' loads in flight per batch
@@ -174,9 +175,16 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_conv_tc(const EventDesc ev, i
                 sv[b] = (row_live && k4 < nk4) ? ((vec && s + 3 < Nt) ? s : -1 - s) : INT_MIN;
                 if (sv[b] >= 0) {
                     if constexpr (KSRC == 0) {
-                        const ulonglong2* src = reinterpret_cast<const ulonglong2*>(P.charge_cnt + (size_t)sw * Nt + s);
-                        ra[b] = __ldg(src);
-                        rb[b] = __ldg(src + 1);
+                        if (wide) {
+                            const ulonglong2* src = reinterpret_cast<const ulonglong2*>(P.charge_cnt + (size_t)sw * Nt + s);
+                            ra[b] = __ldg(src);
+                            rb[b] = __ldg(src + 1);
+                        } else {  // u32 cells: four in one 16-byte load
+                            const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(
+                                reinterpret_cast<const unsigned*>(P.charge_cnt) + (size_t)sw * Nt + s));
+                            ra[b] = make_ulonglong2(w4.x, w4.y);
+                            rb[b] = make_ulonglong2(w4.z, w4.w);
+                        }
                     } else {
                         ra[b] = __ldg(reinterpret_cast<const float4*>(P.charge_in + (size_t)sw * Nt + s));
                     }
@@ -194,9 +202,8 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_conv_tc(const EventDesc ev, i
                             c4[0] = ra[b].x; c4[1] = ra[b].y; c4[2] = rb[b].x; c4[3] = rb[b].y;
                         } else {  // unaligned / wrapping: scalar loads
                             const int s = -1 - sv[b];
-                            const unsigned long long* src = P.charge_cnt + (size_t)sw * Nt;
 #pragma unroll
-                            for (int q = 0; q < 4; ++q) c4[q] = __ldg(src + (s + q) % Nt);
+                            for (int q = 0; q < 4; ++q) c4[q] = count_at(P, (size_t)sw * Nt + (s + q) % Nt, wide);
                         }
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
@@ -408,7 +415,8 @@ struct alignas(64) T2Plan {
     int chunks[kMaxPlanes];       // work items per strip
     uint32_t eoff[kMaxPlanes];    // shared byte offset of the plane's E (hi; lo at + RE * 32)
     int tma;                      // 1: slab halves are TMA box loads (8 ticks x 128 rows) through tm[]
-    CUtensorMap tm[kMaxPlanes];   // the planes' input grids as 2D tensors (ticks, wire rows)
+    CUtensorMap tm[kMaxPlanes];   // the planes' input grids as 2D tensors (ticks, wire rows): u64 counts / floats
+    CUtensorMap tm32[kMaxPlanes]; // the count grids viewed as u32 cells (cnt_wide false)
 };
 
 #ifdef WS_T2_PROF
@@ -489,8 +497,6 @@ __device__ __forceinline__ T2Item t2_item(const EventDesc& ev, const T2Plan& pla
 template <int H, int KSRC>
 __global__ void __launch_bounds__(kT2Threads, 1) k_conv_tc2(const EventDesc ev, const __grid_constant__ T2Plan plan)
 {
-    constexpr int RAWQ = KSRC == 0 ? 4 : 2;     // 16-byte words of one row's 8 ticks
-    constexpr uint32_t kT2RawRow = 16u * RAWQ;  // bytes per wire row of a raw K step (dense: the TMA box layout)
     constexpr int kSlabsPerSub = kTcM / (8 * kT2SK);  // 8: a sub-block starts every 8 slabs
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n_items = plan.item0[plan.np];
@@ -502,7 +508,7 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_conv_tc2(const EventDesc ev, 
     __shared__ uint32_t s_tmem;
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(t2_buf);
     const uint32_t ring = sbase;  // kT2Slots x [hi part | lo part], a part = kT2SK K steps of 4 KB
-    const uint32_t raw = sbase + kT2Slots * kT2SlotBytes;  // kT2Raw x kT2SK x 128 rows x kT2RawRow
+    const uint32_t raw = sbase + kT2Slots * kT2SlotBytes;  // kT2Raw x kT2SK x 128 rows x (8 ticks of u64 / u32 / f32)
     auto bar = [](unsigned long long* b) { return (uint32_t)__cvta_generic_to_shared(b); };
     // shared addresses of the barrier arrays, once (cvta reads the CTA id register)
     const uint32_t a_full = bar(s_full), a_empty = bar(s_empty), a_accf = bar(s_accf), a_acce = bar(s_acce);
@@ -579,7 +585,8 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_conv_tc2(const EventDesc ev, 
                 for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
                     const T2Item I = t2_item<H>(ev, plan, it);
                     const int Nt = ev.p[plan.pl[I.k]].N;
-                    const uint64_t tmap = reinterpret_cast<uint64_t>(&plan.tm[I.k]);
+                    const bool wide = KSRC == 0 && cnt_wide(ev.p[plan.pl[I.k]]);
+                    const uint64_t tmap = reinterpret_cast<uint64_t>(KSRC == 0 && !wide ? &plan.tm32[I.k] : &plan.tm[I.k]);
                     int st = I.S0 % Nt;
                     st = st < 0 ? st + Nt : st;
                     for (int s = 0; s < I.nslab; ++s, ++gs) {
@@ -587,7 +594,7 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_conv_tc2(const EventDesc ev, 
                         if (use > 0) T2_WAIT((a_rempty + 8u * (rs)), (use - 1) & 1u, 0);
                         const uint32_t fb = (a_rfull + 8u * (rs));
                         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb),
-                                     "r"(kT2SK * kT2N * 8u * (KSRC == 0 ? 8u : 4u))
+                                     "r"(kT2SK * kT2N * 8u * (wide ? 8u : 4u))
                                      : "memory");
 #pragma unroll
                         for (int h = 0; h < kT2SK; ++h) {  // (N % 8 == 0: a K step never wraps; steps may)
@@ -609,8 +616,12 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_conv_tc2(const EventDesc ev, 
                 int sw = (I.r0 - H + n) % W;
                 sw = sw < 0 ? sw + W : sw;
                 const bool live = n < I.nr + 2 * H;
+                const bool wide = KSRC == 0 && cnt_wide(P);
+                const int E = wide ? 8 : 4;  // bytes per cell
+                const int rawq = E / 2;      // 16-byte words per 8-tick row
+                const uint32_t rowb = 16u * (uint32_t)rawq;
                 const size_t off = (size_t)sw * Nt;
-                const unsigned char* row = KSRC == 0 ? reinterpret_cast<const unsigned char*>(P.charge_cnt + off)
+                const unsigned char* row = KSRC == 0 ? reinterpret_cast<const unsigned char*>(P.charge_cnt) + off * E
                                                      : reinterpret_cast<const unsigned char*>(P.charge_in + off);
                 int st = I.S0 % Nt;
                 st = st < 0 ? st + Nt : st;
@@ -620,36 +631,37 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_conv_tc2(const EventDesc ev, 
                     bool async = false;
 #pragma unroll
                     for (int h = 0; h < kT2SK; ++h) {
-                        const uint32_t dst = raw + rs * kT2RawSlot + h * kT2RawHalf + (uint32_t)n * kT2RawRow;
-                        constexpr int E = KSRC == 0 ? 8 : 4;  // bytes per cell
+                        const uint32_t dst = raw + rs * kT2RawSlot + h * kT2RawHalf + (uint32_t)n * rowb;
                         if (live && st + 8 <= Nt && ((st | Nt) & (16 / E - 1)) == 0) {
 #pragma unroll
-                            for (int q = 0; q < RAWQ; ++q)
-                                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * q),
-                                             "l"(row + (size_t)st * E + 16 * q)
-                                             : "memory");
+                            for (int q = 0; q < 4; ++q)
+                                if (q < rawq)
+                                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * q),
+                                                 "l"(row + (size_t)st * E + 16 * q)
+                                                 : "memory");
                             async = true;
                         } else {
                             // wrapping / unaligned / dead rows: plain loads and stores
-                            uint32_t v[4 * RAWQ];
+                            uint32_t v[16];
 #pragma unroll
                             for (int i = 0; i < 8; ++i) {
                                 int t = st + i;
                                 while (t >= Nt) t -= Nt;
-                                if constexpr (KSRC == 0) {
+                                if (KSRC == 0 && wide) {
                                     const unsigned long long x =
                                         live ? __ldg(reinterpret_cast<const unsigned long long*>(row) + t) : 0ull;
                                     v[2 * i] = (uint32_t)x;
                                     v[2 * i + 1] = (uint32_t)(x >> 32);
-                                } else {
-                                    v[i] = live ? __float_as_uint(__ldg(reinterpret_cast<const float*>(row) + t)) : 0u;
+                                } else {  // u32 counts or floats: the 32-bit word
+                                    v[i] = live ? __ldg(reinterpret_cast<const unsigned*>(row) + t) : 0u;
                                 }
                             }
 #pragma unroll
-                            for (int q = 0; q < RAWQ; ++q)
-                                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst + 16u * q),
-                                             "r"(v[4 * q]), "r"(v[4 * q + 1]), "r"(v[4 * q + 2]), "r"(v[4 * q + 3])
-                                             : "memory");
+                            for (int q = 0; q < 4; ++q)
+                                if (q < rawq)
+                                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst + 16u * q),
+                                                 "r"(v[4 * q]), "r"(v[4 * q + 1]), "r"(v[4 * q + 2]), "r"(v[4 * q + 3])
+                                                 : "memory");
                         }
                         st += 8;
                         while (st >= Nt) st -= Nt;
@@ -669,22 +681,28 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_conv_tc2(const EventDesc ev, 
         // n converts wire row n to TF32 (hi part, plus a lo part where a value
         // does not fit 11 bits) into the MMA ring
         const int n = tid & (kT2N - 1), gp = (warp - 4) >> 2;
-        uint32_t total = 0;  // slabs of the CTA's items
-        for (int it = blockIdx.x; it < n_items; it += gridDim.x) total += (uint32_t)t2_item<H>(ev, plan, it).nslab;
         uint32_t dirty = 0u;  // slots whose lo part this warp wrote non-zero
-        for (uint32_t gs = gp; gs < total; gs += kT2Groups) {
+        uint32_t gs = 0;
+        for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+          const T2Item I = t2_item<H>(ev, plan, it);
+          // u64 or u32 count cells (cnt_wide), or floats: a raw row is 8 ticks
+          const bool wide = KSRC == 0 && cnt_wide(ev.p[plan.pl[I.k]]);
+          const uint32_t rowb = wide ? 64u : 32u;
+          for (int s = 0; s < I.nslab; ++s, ++gs) {
+            if ((int)(gs % kT2Groups) != gp) continue;
             const uint32_t rs = gs % kT2Raw;
             T2_WAIT((a_rfull + 8u * (rs)), (gs / kT2Raw) & 1u, 0);
-            uint4 rw[kT2SK][RAWQ];
+            uint4 rw[kT2SK][4];
 #pragma unroll
             for (int h = 0; h < kT2SK; ++h) {
-                const uint32_t src = raw + rs * kT2RawSlot + h * kT2RawHalf + (uint32_t)n * kT2RawRow;
+                const uint32_t src = raw + rs * kT2RawSlot + h * kT2RawHalf + (uint32_t)n * rowb;
 #pragma unroll
-                for (int q = 0; q < RAWQ; ++q)
-                    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                                 : "=r"(rw[h][q].x), "=r"(rw[h][q].y), "=r"(rw[h][q].z), "=r"(rw[h][q].w)
-                                 : "r"(src + 16u * q)
-                                 : "memory");
+                for (int q = 0; q < 4; ++q)
+                    if (q < 2 || wide)
+                        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                     : "=r"(rw[h][q].x), "=r"(rw[h][q].y), "=r"(rw[h][q].z), "=r"(rw[h][q].w)
+                                     : "r"(src + 16u * q)
+                                     : "memory");
             }
             __syncwarp();
             if (lane == 0) t2_arrive((a_rempty + 8u * (rs)));
@@ -693,11 +711,19 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_conv_tc2(const EventDesc ev, 
 #pragma unroll
             for (int h = 0; h < kT2SK; ++h) {
                 float x[8];
-                if constexpr (KSRC == 0) {
+                if (KSRC == 0 && wide) {
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         x[2 * q] = (float)(((unsigned long long)rw[h][q].y << 32) | rw[h][q].x);
                         x[2 * q + 1] = (float)(((unsigned long long)rw[h][q].w << 32) | rw[h][q].z);
+                    }
+                } else if (KSRC == 0) {
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        x[4 * q] = (float)rw[h][q].x;
+                        x[4 * q + 1] = (float)rw[h][q].y;
+                        x[4 * q + 2] = (float)rw[h][q].z;
+                        x[4 * q + 3] = (float)rw[h][q].w;
                     }
                 } else {
 #pragma unroll
@@ -747,6 +773,7 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_conv_tc2(const EventDesc ev, 
                 if (need) atomicMax(&s_tag[slot], (use << 1) | 1u);
                 t2_arrive((a_full + 8u * (slot)));
             }
+          }
         }
     } else if (warp == kT2MmaWarp) {
         // ---- MMA issuer: the whole warp runs the loop, one elected lane issues
@@ -1009,6 +1036,13 @@ extern "C" cudaError_t wsb_launch_conv_tc2(const wsb::EventDesc& ev, cudaStream_
         if (encode(&plan.tm[k], src == 0 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                    const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            plan.tma = 0;
+        const cuuint64_t strides32[1] = {(cuuint64_t)P.N * 4};
+        if (src == 0 && ((size_t)P.N * 4) % 16) plan.tma = 0;
+        if (src == 0 && plan.tma &&
+            encode(&plan.tm32[k], CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(base), dims, strides32, box,
+                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             plan.tma = 0;
     }

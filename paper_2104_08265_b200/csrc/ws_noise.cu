@@ -68,11 +68,13 @@ __global__ void k_noise_pairs(const NoiseArgs a)
 // integer charge grid (fluctuation on, u64 counts) -> the caller's charge
 // output: float32 (type 0), uint32 (1; a count past 2^32 - 1 flags
 // kErrCellOvf) or int64 (2, the reference's ChargeGrid)
-__global__ void k_counts_out(const unsigned long long* __restrict__ g, void* out, int type, size_t n, unsigned* err)
+__global__ void k_counts_out(const unsigned long long* __restrict__ g, void* out, int type, size_t n, unsigned* err,
+                             const unsigned long long* __restrict__ qsum)
 {
     bool ovf = false;
+    const bool wide = !qsum || *qsum >= (1ull << 32);  // the grid's cell width (cnt_wide)
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-        const unsigned long long v = g[i];
+        const unsigned long long v = wide ? g[i] : (unsigned long long)reinterpret_cast<const unsigned*>(g)[i];
         if (type == 0) {
             static_cast<float*>(out)[i] = (float)v;
         } else if (type == 1) {
@@ -103,9 +105,9 @@ extern "C" cudaError_t wsb_launch_noise(const float* in, const wsb::Sink& out, i
 }
 
 extern "C" cudaError_t wsb_launch_counts_out(const unsigned long long* g, void* out, int type, size_t n, unsigned* err,
-                                             cudaStream_t s)
+                                             const unsigned long long* qsum, cudaStream_t s)
 {
     if (!n) return cudaSuccess;
-    wsb::k_counts_out<<<(unsigned)std::min<size_t>((n + 255) / 256, 148 * 16), 256, 0, s>>>(g, out, type, n, err);
+    wsb::k_counts_out<<<(unsigned)std::min<size_t>((n + 255) / 256, 148 * 16), 256, 0, s>>>(g, out, type, n, err, qsum);
     return cudaGetLastError();
 }

@@ -269,6 +269,26 @@ __global__ void __launch_bounds__(128, kFluct ? 1 : 8) k_sample(const EventDesc 
     const int pi = plane_of_unit(ev, u);
     const PlaneDesc& P = ev.p[pi];
     ws_depo d = P.depos[u - P.unit_base];
+    if constexpr (kFluct) {
+        // the plane's electrons in all, each depo capped at 2^32 (cnt_wide:
+        // below 2^32 the count grid takes u32 cells); one atomic per warp when
+        // the warp's units share a plane
+        if (P.cnt_qsum) {
+            unsigned long long qq = d.q > 0 ? min((unsigned long long)d.q, 1ull << 32) : 0ull;
+            const unsigned act = __activemask();
+            const int lead = __ffs(act) - 1;
+            if (__all_sync(act, pi == __shfl_sync(act, pi, lead))) {
+                for (int o = 16; o; o >>= 1) {
+                    const unsigned long long t = __shfl_down_sync(act, qq, o);
+                    if ((threadIdx.x & 31) + o < 32 && (act >> ((threadIdx.x & 31) + o)) & 1u) qq += t;
+                }
+                if ((int)(threadIdx.x & 31) == lead && qq)
+                    atomicAdd(const_cast<unsigned long long*>(P.cnt_qsum), qq);
+            } else if (qq) {
+                atomicAdd(const_cast<unsigned long long*>(P.cnt_qsum), qq);
+            }
+        }
+    }
     UnitRec rec;
     rec.w0 = -1;
     rec.t0 = 0;
@@ -802,17 +822,14 @@ __device__ __forceinline__ double div_rn_y(double t, double d, double y)
 }
 
 // Electron counts into the integer charge grid (the reference's ChargeGrid is
-// int64, core.hpp:94-99): 64-bit reductions (fire and forget: the walk never
-// waits on them), exact and order independent.
-__device__ __forceinline__ void add_count(unsigned long long* cell, int64_t k)
-{
-    if (k > 0) atomicAdd(cell, (unsigned long long)k);
-}
+// int64, core.hpp:94-99): integer reductions (fire and forget: the walk never
+// waits on them), exact and order independent, into u64 cells or - when the
+// plane's depos carry fewer than 2^32 electrons - u32 cells (CellPtr).
 
 // Fluctuation walk, one thread per unit: sample_patch's exact probabilities
 // (rasterize.cpp:101-118) then fluctuate_sequential (rasterize.cpp:124-149)
 // with the reference binomial (rng.cpp:146-193) or the Gaussian approximation
-// (rasterize.cpp:159-170); counts scattered with integer atomics (add_count).
+// (rasterize.cpp:159-170); counts scattered with integer atomics (CellPtr).
 __global__ void k_fluctuate(const EventDesc ev, const UnitRec* __restrict__ recs, const uint32_t* __restrict__ pool,
                             const uint32_t* __restrict__ order)
 {
@@ -834,7 +851,7 @@ __global__ void k_fluctuate(const EventDesc ev, const UnitRec* __restrict__ recs
     const double norm = 1.0 / total;
     Rng src;
     src.init(ev.rng_mode, ev.seed, (uint64_t)d.id);
-    unsigned long long* grid = P.charge_cnt;
+    const bool wide = cnt_wide(P);
     const int N = P.N;
     int64_t remaining = d.q;
     double p_rem = 1.0;
@@ -849,12 +866,11 @@ __global__ void k_fluctuate(const EventDesc ev, const UnitRec* __restrict__ recs
             p = p < 0.0 ? 0.0 : (p > 1.0 ? 1.0 : p);
         }
         const int64_t k = ev.approx ? binomial_approx(remaining, p, src) : binomial(remaining, p, src);
-        add_count(&grid[(size_t)(rec.w0 + w) * N + rec.t0 + t], k);
+        cell_at(P, (size_t)(rec.w0 + w) * N + rec.t0 + t, wide).add(k);
         remaining -= k;
         p_rem -= pi;
     }
-    if (remaining)
-        add_count(&grid[(size_t)(rec.w0 + n_w - 1) * N + rec.t0 + n_t - 1], remaining);
+    if (remaining) cell_at(P, (size_t)(rec.w0 + n_w - 1) * N + rec.t0 + n_t - 1, wide).add(remaining);
 }
 
 // Exact fluctuation (fluctuate_sequential with the reference binomial), the
@@ -985,7 +1001,6 @@ __global__ void __launch_bounds__(128) k_fluctuate_exact(const EventDesc ev, con
     }
     Rng src;
     src.init(ev.rng_mode, ev.seed, (uint64_t)d.id);
-    unsigned long long* grid = P.charge_cnt;
     const int N = P.N;
     const int last = rec.n_w * n_t - 1;
     int64_t remaining = d.q;
@@ -999,18 +1014,19 @@ __global__ void __launch_bounds__(128) k_fluctuate_exact(const EventDesc ev, con
 
     // bin b = (bw, bt), tracked incrementally (no integer division per draw)
     int bw = 0, bt = 0;
-    unsigned long long* cellp = grid + (size_t)rec.w0 * N + rec.t0;  // &grid[w0 + bw][t0 + bt]
+    const bool wide = cnt_wide(P);
+    CellPtr cellp = cell_at(P, (size_t)rec.w0 * N + rec.t0, wide);  // grid[w0 + bw][t0 + bt]
     auto commit = [&](int64_t k) {  // bin b drew k electrons
-        add_count(cellp, k);
+        cellp.add(k);
         remaining -= k;
         p_rem -= pi;
         ++b;
         if (++bt == n_t) {
             bt = 0;
             ++bw;
-            cellp += N - (n_t - 1);
+            cellp.advance(N - (n_t - 1));
         } else {
-            ++cellp;
+            cellp.advance(1);
         }
     };
     // draws until one needs a CDF walk (or the depo is finished)
@@ -1018,7 +1034,7 @@ __global__ void __launch_bounds__(128) k_fluctuate_exact(const EventDesc ev, con
         while (!done && !walking) {
             if (remaining == 0 || b >= last) {
                 if (remaining)  // the last bin takes the rest
-                    add_count(&grid[(size_t)(rec.w0 + rec.n_w - 1) * N + rec.t0 + n_t - 1], remaining);
+                    cell_at(P, (size_t)(rec.w0 + rec.n_w - 1) * N + rec.t0 + n_t - 1, wide).add(remaining);
                 done = true;
                 break;
             }
@@ -1316,8 +1332,7 @@ __global__ void __launch_bounds__(128, WS_FLWALK_MINB) k_fluct_walk(const EventD
     bool has = false, exhausted = false;
     int64_t remaining = 0;
     int n_t = 0, last = 0, b = 0, bt = 0, N = 0;
-    unsigned long long* cellp = nullptr;
-    unsigned long long* lastp = nullptr;
+    CellPtr cellp{nullptr, 3}, lastp{nullptr, 3};
     const FlRec* rp = nullptr;
     // the draw in progress
     bool walking = false, flip = false;
@@ -1341,13 +1356,14 @@ __global__ void __launch_bounds__(128, WS_FLWALK_MINB) k_fluct_walk(const EventD
         last = rec.n_w * n_t - 1;
         b = 0;
         bt = 0;
-        cellp = P.charge_cnt + (size_t)rec.w0 * N + rec.t0;
-        lastp = cellp + (size_t)(rec.n_w - 1) * N + n_t - 1;
+        const bool wide = cnt_wide(P);
+        cellp = cell_at(P, (size_t)rec.w0 * N + rec.t0, wide);
+        lastp = cell_at(P, (size_t)(rec.w0 + rec.n_w - 1) * N + rec.t0 + n_t - 1, wide);
         rp = reinterpret_cast<const FlRec*>(ev.fl_bins) + off;
         has = true;
     };
     auto commit = [&](int64_t k) {
-        add_count(cellp, k);
+        cellp.add(k);
         remaining -= k;
         ++b;
         ++rp;
@@ -1355,9 +1371,9 @@ __global__ void __launch_bounds__(128, WS_FLWALK_MINB) k_fluct_walk(const EventD
         if (WS_FLWALK_PF2 > 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + WS_FLWALK_PF2));
         if (++bt == n_t) {
             bt = 0;
-            cellp += N - (n_t - 1);
+            cellp.advance(N - (n_t - 1));
         } else {
-            ++cellp;
+            cellp.advance(1);
         }
     };
     take(blockIdx.x * blockDim.x + threadIdx.x);
@@ -1389,7 +1405,7 @@ __global__ void __launch_bounds__(128, WS_FLWALK_MINB) k_fluct_walk(const EventD
             int cheap = 0;
             while (has && !walking && !seed && cheap++ < WS_FL_CHEAPMAX) {
                 if (remaining == 0 || b >= last) {
-                    if (remaining) add_count(lastp, remaining);  // the last bin takes the rest
+                    if (remaining) lastp.add(remaining);  // the last bin takes the rest
                     has = false;
                     break;
                 }
@@ -1573,6 +1589,29 @@ __global__ void k_zero16(uint4* __restrict__ p, size_t n)
         p[i] = make_uint4(0u, 0u, 0u, 0u);
 }
 }  // namespace wsb
+
+// Zero a count grid of `cells` cells at the width cnt_wide chose (after k_sample)
+namespace wsb {
+__global__ void k_zero_counts(uint4* __restrict__ p, size_t cells, const unsigned long long* __restrict__ qsum)
+{
+    const bool wide = !qsum || *qsum >= (1ull << 32);
+    const size_t n = ((cells << (wide ? 3 : 2)) + 15) / 16;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        p[i] = make_uint4(0u, 0u, 0u, 0u);
+}
+}  // namespace wsb
+
+extern "C" cudaError_t wsb_launch_zero_counts(void* p, size_t cells, const unsigned long long* qsum, cudaStream_t s)
+{
+    if (cells == 0) return cudaSuccess;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t n = (cells * 8 + 15) / 16;
+    const unsigned blocks = (unsigned)std::min<size_t>((n + 255) / 256, (size_t)sms * 8);
+    wsb::k_zero_counts<<<blocks, 256, 0, s>>>(static_cast<uint4*>(p), cells, qsum);
+    return cudaGetLastError();
+}
 
 extern "C" cudaError_t wsb_launch_zero(void* p, size_t bytes, cudaStream_t s)
 {
