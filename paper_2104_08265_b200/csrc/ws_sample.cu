@@ -1199,7 +1199,10 @@ struct __align__(32) FlRec {
 };
 static_assert(sizeof(FlRec) == 32, "one sector per record");
 
-__global__ void __launch_bounds__(128) k_fluct_prep(const EventDesc ev, const UnitRec* __restrict__ recs,
+#ifndef WS_PREP_MINB
+#define WS_PREP_MINB 1
+#endif
+__global__ void __launch_bounds__(128, WS_PREP_MINB) k_fluct_prep(const EventDesc ev, const UnitRec* __restrict__ recs,
                                                      const uint32_t* __restrict__ pool,
                                                      const uint32_t* __restrict__ order, uint32_t* __restrict__ offs,
                                                      uint32_t* __restrict__ slow, uint32_t* __restrict__ n_slow,
