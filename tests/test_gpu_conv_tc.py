@@ -78,15 +78,18 @@ def test_grid_convolution_delta_response_and_large_values(ctx, oracle):
         assert _conv(ctx, oracle, grid, resp, s) < 1e-5
 
 
-def test_fluctuation_counts_past_2_11_and_2_22(ctx, oracle):
+@pytest.mark.parametrize("q_hot", [60_000_000, 150_000_000])
+def test_fluctuation_counts_past_2_11_and_2_22(ctx, oracle, q_hot):
     """Fluctuation-on frames (the walk's integer counts into the grid
     convolution) with cells far past 2^11 and 2^22 electrons: counts below
-    2^22 enter exactly as two TF32 halves, larger ones within 2^-22."""
+    2^22 enter exactly as two TF32 halves, larger ones within 2^-22. With
+    1.5e8-electron depos the plane carries more than 2^32 electrons, so the
+    count grid takes u64 cells (u32 otherwise): both widths, every loader."""
     from paper_2104_08265_b200 import RngConfig, SimConfig
     from paper_2104_08265_b200.workloads import line_tracks
     grid = GridSpec(n_wires=180, n_ticks=900, pad_wires=20, pad_ticks=100, pitch=5.0, tick=0.5)
     d = line_tracks(600, grid, seed=3)
-    d["q"][:40] = 60_000_000  # narrow, hot depos: cells of ~1e7 electrons
+    d["q"][:40] = q_hot  # narrow, hot depos: cells of ~1e7 (or ~3e8) electrons
     d["sigma_t"][:40] = 0.3
     d["sigma_x"][:40] = 2.0
     d["q"][40:200] = 200_000
