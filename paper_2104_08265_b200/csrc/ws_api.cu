@@ -176,7 +176,9 @@ struct ws_ctx {
     int sm_count = 0;
     int conv_variant = 25;                       // k_conv: 25 (3 CTAs/SM, radix <= 25) or 8 (4 CTAs/SM, radix <= 8)
     int conv_path = WS_CONV_AUTO;                // ws_ctx_set_conv_path
-    double direct_kappa = 16.0;                  // AUTO: direct if est. depo-row-taps <= kappa x cells (per plane)
+    double direct_kappa = 128.0;                 // AUTO: direct if est. depo-row-taps <= kappa x cells (per plane);
+                                                 // r2: direct is 2.3x faster than the row FFT at 1M depos per
+                                                 // MicroBooNE plane (ratio 43), so only very long kernels take the FFT
     cudaStream_t copy_stream = nullptr;          // D2H of the pipelined batch path
     cudaStream_t aux_stream = nullptr;           // k_gprof, concurrent with binning
     cudaEvent_t aux_fork = nullptr, aux_join = nullptr;
@@ -214,7 +216,6 @@ struct ws_plane {
     float2* d_tw = nullptr;
     uint16_t* d_rev = nullptr;
     int ww_is_one = 0;
-    bool route_fft_next = false;  // AUTO: a tile overflowed (dense, e.g. a shower): the row FFT on the re-run
     // impact positions (ws_plane_create_impacts): sub-bins per pitch and the
     // impacts of this plane's response class; further classes (distinct
     // responses) are child planes run alongside this one into the same frame
@@ -547,11 +548,9 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
         // grid request: that pass bins by FFT bands). AUTO estimates the
         // work as depos x ~12 wire rows x profile taps against the plane's
         // cells (ws_ctx_set_direct_kappa).
-        // A plane whose tile list overflowed in the previous call (a local
-        // density far above the plane average, e.g. a shower) takes the row
-        // FFT once under AUTO: its cost does not depend on the depo density.
-        const bool dense = p->route_fft_next && c->conv_path == WS_CONV_AUTO;
-        p->route_fft_next = false;
+        // (A tile list that overflowed - a local density far above the plane
+        // average, e.g. a shower - is re-run on the same kernel with the grown
+        // lists, so a call's result never depends on the workspace's history.)
         const bool classes = !p->classes.empty();
         if (classes) {
             // distinct per-impact responses: the classes' profiles are summed
@@ -563,8 +562,7 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
             if (c->conv_path == WS_CONV_FFT)
                 return set_err(WS_EINVAL, "impact planes with distinct responses run on the time-domain path only");
         }
-        if (ev.mode == 0 && has_out && !d.charge_out && p->direct_ok && c->conv_path != WS_CONV_FFT &&
-            (!dense || classes)) {
+        if (ev.mode == 0 && has_out && !d.charge_out && p->direct_ok && c->conv_path != WS_CONV_FFT) {
             const double work = (double)d.n_units * 12.0 * (double)(p->n_lags + 16);
             if (classes || c->conv_path == WS_CONV_DIRECT || work <= c->direct_kappa * (double)p->W * (double)p->Np) {
                 d.direct = 1;
@@ -577,7 +575,7 @@ int run_group(ws_ctx* c, uint32_t n, ws_plane* const* planes, const ws_depo* con
             return set_err(WS_EINVAL, "launch group: more than %d plane descriptors", wsb::kMaxPlanes);
         any_fft = any_fft || !d.direct;
         desc_of[i] = nd;
-        desc_plane.push_back(classes ? nullptr : p);  // (dense re-routing only for single-class planes)
+        desc_plane.push_back(classes ? nullptr : p);
         ev.p[nd++] = d;
         units += d.n_units;
         bands += (uint32_t)d.n_bands;
@@ -891,17 +889,15 @@ int finish_pending(ws_ctx* c)
         if (h.err & wsb::kErrFluct) c->fl_hint = std::max<size_t>(c->fl_hint, (size_t)h.fl_ctr + 4096);
         if (h.err & wsb::kErrTileCap) {
             // the real per-tile counts: size the fixed lists from them, or
-            // (beyond the budget) take exact-size CSR lists; under AUTO the
-            // overflowing (dense) planes take the row FFT on the re-run
+            // (beyond the budget) take exact-size CSR lists
             uint32_t need = 0;
-            for (int i = 0; i < pc.n_planes; ++i) {
-                need = std::max(need, h.tile_need[i]);
-                if (h.tile_need[i] && pc.planes[i]) pc.planes[i]->route_fft_next = true;
-            }
+            for (int i = 0; i < pc.n_planes; ++i) need = std::max(need, h.tile_need[i]);
             uint32_t cap = c->tile_cap_hint;
             while (cap < need && cap < (1u << 30)) cap *= 2;
-            if ((size_t)pc.tiles * cap * sizeof(wsb::TEnt) <= kFixedTileBudget) c->tile_cap_hint = cap;
-            else c->csr_next = true;
+            // past the fixed-list budget the calls take exact-size CSR lists
+            // from now on (fixed_fits is false for the grown hint)
+            c->tile_cap_hint = cap;
+            if ((size_t)pc.tiles * cap * sizeof(wsb::TEnt) > kFixedTileBudget) c->csr_next = true;
             if (!prc) {
                 prc = WS_ERANGE;
                 snprintf(msg, sizeof msg,

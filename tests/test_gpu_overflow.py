@@ -3,7 +3,7 @@
 The direct path's fixed-capacity tile lists (and the CSR lists, and the
 profile pool) are sized by estimate; a localized shower can overflow them.
 The device records the size it needed, the host entry points re-run with it
-(or route the dense plane to the row FFT), and the asynchronous _device path
+(on the same kernel, the lists grown to the real counts), and the asynchronous _device path
 reports WS_ERANGE at synchronize. Each test starts from a FRESH context so
 no earlier test has grown its workspace. The reference never truncates
 (scatter.cpp:27-36): every frame here matches the oracle."""
@@ -53,7 +53,7 @@ def test_shower_plane_fresh_context(reference, path):
     res = Plane(ctx, GRID, RESP).simulate(d, CFG)
     assert relL2_per_channel(res.frame, m_ref) < 1e-5
     if path == "auto":
-        assert res.timing["direct_planes"] == 0  # the dense plane was re-run on the row FFT
+        assert res.timing["direct_planes"] == 1  # re-run on the same (time-domain) kernel, lists grown
     ctx.close()
 
 
