@@ -328,7 +328,7 @@ uint32_t ws_multi_device_count(const ws_multi* m);
 ws_ctx* ws_multi_context(ws_multi* m, uint32_t device_index);
 ws_plane* ws_multi_plane(ws_multi* m, uint32_t device_index, uint32_t plane);
 int ws_multi_set_conv_path(ws_multi* m, int path);
-/* cost model of one plane run: cells + 150 x depos */
+/* cost model of one plane run: cells + 900 x depos (fitted to the 1k-1M depo sweep) */
 double ws_multi_cost(uint64_t cells, uint64_t n_depos);
 /* Whole events over the devices: depos / n_depos / adcs / frames are
  * [n_events * n_planes] (as ws_run_events). readout NULL: fp32 frames (as

@@ -34,7 +34,7 @@ struct ws_multi {
 
 namespace {
 
-constexpr double kDepoCost = 150.0;  // cells-equivalent of one depo on one plane (k_direct: ~12 rows x ~160 taps vs 4 B/cell)
+constexpr double kDepoCost = 900.0;  // cells-equivalent of one depo on one plane (fitted to the r2 C5 sweep: ~0.9-1.3 ns per depo-plane vs ~1 ps per cell)
 
 int fail(int code, const std::string& msg) { return ws_set_error_message(code, msg.c_str()); }
 

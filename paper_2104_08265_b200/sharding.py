@@ -11,14 +11,15 @@ from __future__ import annotations
 from typing import Sequence
 
 
-DEPO_COST = 150.0  # cells-equivalent of one depo on one plane (ws_multi_cost in csrc/ws_multi.cu)
+DEPO_COST = 900.0  # cells-equivalent of one depo on one plane (ws_multi_cost in csrc/ws_multi.cu)
 
 
 def unit_cost(padded_wires: int, padded_ticks: int, n_depos: int) -> float:
     """Device-time model of one plane run, the same as the C ABI's
-    ws_multi_cost: the time-domain path (k_direct, the default for sparse
-    planes) writes every cell once and adds each depo's response profile
-    (~12 wire rows x ~160 taps) to its rows, so cost = cells + 150 x depos."""
+    ws_multi_cost: the time-domain path (k_direct) writes every cell once and
+    adds each depo's response profile (~12 wire rows x ~130 taps) to its rows;
+    fitted to the C5 sweep (1k-1M depos per MicroBooNE event, round 2: 0.9-1.3
+    ns per depo-plane vs 1.0 ps per cell): cost = cells + 900 x depos."""
     return float(padded_wires) * padded_ticks + DEPO_COST * n_depos
 
 
