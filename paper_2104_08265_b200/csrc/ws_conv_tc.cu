@@ -355,23 +355,28 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_conv_tc(const EventDesc ev, i
 // another, so the tensor pipe idles while a tile loads and shared-memory
 // bandwidth caps it when it runs (r2c: 0.79 ms per C3 event, 24% of warps
 // active). Here one CTA per SM walks a list of work items (plane, strip of
-// 128 wire rows, chunk of kT2Chunk 128-tick sub-blocks), N = 128 wire rows per
-// MMA (the A operand is amortised over 4x the columns), and three roles
-// overlap:
-//   warps 0-3 (loaders, one thread per wire row): cp.async copies of the input
-//     window as "slabs" of 8 ticks x 128 rows (one MMA K step) into a raw
-//     ring, eight slabs in flight, completion signalled on mbarriers;
-//   warps 4-11 (converters, two groups taking alternate slabs): raw counts /
-//     floats -> TF32 (hi part, plus a lo part when a value does not fit 11
-//     bits) in the MMA ring. Loading and converting are separate warps because
-//     the generic -> async proxy fence the converters need (MEMBAR.ALL.CTA)
-//     waits for every load the thread has in flight;
+// 128 wire rows, chunk of eight 128-tick sub-blocks), N = 128 wire rows per
+// MMA (tools/ubench_umma.cu: 64 cycles per 128x128x8 TF32 MMA, 46 at N = 32),
+// and four roles overlap, connected by mbarriers:
+//   warp 0 (loader): per "slab" (16 ticks x 128 rows = two MMA K steps) two
+//     TMA 2D boxes of the count grid (u64 or u32 cells) or float grid into a
+//     4-deep raw ring; planes whose layout rules TMA out (a wire stencil wraps
+//     rows, N % 8 != 0, an unaligned base) take cp.async per wire row (warps
+//     0-3) instead;
+//   warps 4-11 (converters, two groups taking alternate slabs, one wire row
+//     per thread): raw values -> TF32 hi (plus a lo part where a value does
+//     not fit 11 bits) in a 4-slot MMA ring. Loading and converting are
+//     separate warps because the generic -> async proxy fence the converters
+//     need compiles to MEMBAR.ALL.CTA, which waits for every load the thread
+//     has in flight;
 //   warp 16 (one elected lane): per slab, the MMAs of every sub-block whose K
-//     range contains it (<= 3 for J <= 48), into a ring of four 128-column TMEM
+//     range contains it (<= 3 for J <= 48) into a ring of four 128-column TMEM
 //     accumulators; tcgen05.commit releases the slab and, after a sub-block's
 //     last K step, hands its accumulator to the epilogue;
 //   warps 12-15 (epilogue, one TMEM lane quadrant each): tcgen05.ld, the
-//     cross-wire stencil in registers, coalesced stores (or the fused readout).
+//     cross-wire stencil in registers, predicated coalesced stores with a
+//     running offset (or the fused readout; the end-to-end calls digitize
+//     with the full-GPU pair kernel instead, ws_api.cu).
 // Exactness as in k_conv_tc: taps split TF32 hi + lo; counts below 2^11 are
 // one TF32 value, below 2^22 exactly hi + lo (the 11-bit halves), above that
 // hi + lo within 2^-22 relative (the frame tolerance is 1e-5); float grids hi
