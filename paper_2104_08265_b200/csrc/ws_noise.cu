@@ -65,6 +65,33 @@ __global__ void k_noise_pairs(const NoiseArgs a)
     if (has1) sink_put(a.out, base + 1, a.noise ? __dadd_rn(v1, __dmul_rn(a.sigma, n1)) : v1);
 }
 
+// Digitize only (no noise), a float4 of samples per thread: the frame's
+// samples -> fp32 / fp64 frame and ADC codes (the reference's fp64 rounding,
+// adc_code), 16-byte loads and 8-/16-byte stores. n4: the samples / 4 (the
+// frame is contiguous: W x N padded samples).
+__global__ void k_digitize4(const float4* __restrict__ in, const Sink k, size_t n4)
+{
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+        const float4 v = __ldcs(in + i);
+        const double x[4] = {(double)v.x, (double)v.y, (double)v.z, (double)v.w};
+        if (k.frame && k.frame != reinterpret_cast<const float*>(in)) reinterpret_cast<float4*>(k.frame)[i] = v;
+        if (k.frame64) {
+            reinterpret_cast<double2*>(k.frame64)[2 * i] = make_double2(x[0], x[1]);
+            reinterpret_cast<double2*>(k.frame64)[2 * i + 1] = make_double2(x[2], x[3]);
+        }
+        if (k.adc) {
+            int c[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) c[j] = adc_code(x[j], k.scale, k.offset, k.max_code);
+            if (k.adc_u16)
+                reinterpret_cast<uint2*>(k.adc)[i] =
+                    make_uint2((uint32_t)c[0] | ((uint32_t)c[1] << 16), (uint32_t)c[2] | ((uint32_t)c[3] << 16));
+            else
+                reinterpret_cast<int4*>(k.adc)[i] = make_int4(c[0], c[1], c[2], c[3]);
+        }
+    }
+}
+
 // integer charge grid (fluctuation on, u64 counts) -> the caller's charge
 // output: float32 (type 0), uint32 (1; a count past 2^32 - 1 flags
 // kErrCellOvf) or int64 (2, the reference's ChargeGrid)
@@ -95,7 +122,16 @@ extern "C" cudaError_t wsb_launch_noise(const float* in, const wsb::Sink& out, i
                                         double sigma, uint64_t seed, cudaStream_t s)
 {
     const wsb::NoiseArgs a{in, out, W, N, noise, rng_mode, sigma, seed};
-    if (noise && rng_mode == WS_RNG_SUBSTREAM) {
+    const size_t n = (size_t)W * N;
+    const auto aligned = [](const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    if (!noise && n % 4 == 0 && aligned(in) && aligned(out.frame) && aligned(out.frame64) && aligned(out.adc)) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const size_t n4 = n / 4;
+        wsb::k_digitize4<<<(unsigned)std::min<size_t>((n4 + 255) / 256, (size_t)sms * 16), 256, 0, s>>>(
+            reinterpret_cast<const float4*>(in), out, n4);
+    } else if (noise && rng_mode == WS_RNG_SUBSTREAM) {
         wsb::k_noise_rows<<<(W + 63) / 64, 64, 0, s>>>(a);
     } else {
         const size_t pairs = (size_t)W * ((N + 1) / 2);
