@@ -36,7 +36,14 @@ constexpr int kQ = 5;                          // profile taps per lane in regis
 constexpr int kSlot = 32 * kQ;                 // taps of the register fast path
 constexpr int kMargin = kSlot;                 // discard margins either side of every row
 constexpr int kRowStride = kMargin + kTileTicks + kMargin;  // ints per tile row
-constexpr int kDirectThreads = 640;  // two CTAs per SM
+#ifndef WS_DIRECT_THREADS
+#define WS_DIRECT_THREADS 640
+#endif
+#ifndef WS_DIRECT_MINB
+#define WS_DIRECT_MINB 2
+#endif
+constexpr int kDirectThreads = WS_DIRECT_THREADS;  // x kDirectMinB CTAs per SM
+constexpr int kDirectMinB = WS_DIRECT_MINB;
 
 // Fixed-point term round(c g). WS_DIRECT_MAGIC: one FFMA with the magic
 // 1.5 * 2^23 (the mantissa bits hold the rounded value; needs |c g| < 2^22,
@@ -168,7 +175,7 @@ __device__ __forceinline__ void cp_wait()
 // kRO: the fused readout (noise + digitize, fp64 frame) in the frame store;
 // a separate instantiation so the plain fp32 store keeps its registers
 template <int NT, bool kRO>
-__global__ void __launch_bounds__(NT, 2)
+__global__ void __launch_bounds__(NT, kDirectMinB)
 k_direct(const EventDesc ev, const uint32_t* __restrict__ pool, const uint32_t* __restrict__ band_off,
          const TEnt* __restrict__ tlist)
 {
@@ -472,7 +479,7 @@ extern "C" size_t wsb_direct_smem(int cap)
 
 extern "C" int wsb_direct_cap()
 {
-    const size_t limit = 112 * 1024;  // two CTAs per SM (228 KB, 1 KB reserved per CTA, static smem)
+    const size_t limit = (228 * 1024) / wsb::kDirectMinB - 2 * 1024;  // kDirectMinB CTAs per SM (1 KB reserved per CTA, static smem)
     return (int)((limit - wsb_direct_smem(0)) / sizeof(wsb::TEnt));
 }
 
