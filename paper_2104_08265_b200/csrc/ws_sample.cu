@@ -1206,7 +1206,10 @@ constexpr uint32_t kFlNone = 0xffffffffu;
 #ifndef WS_FLWALK_PF2
 #define WS_FLWALK_PF2 0
 #endif
-enum : uint32_t { kFlDraw = 0u, kFlDrawFlip = 1u, kFlZero = 2u, kFlAll = 3u };
+enum : uint32_t { kFlDraw = 0u, kFlDrawFlip = 1u, kFlZero = 2u, kFlAll = 3u, kFlSkip = 4u };
+#ifndef WS_FL_SKIP
+#define WS_FL_SKIP 2  // shortest run of certain-zero draws k_fluct_prep marks for one skip (0: off)
+#endif
 #ifndef WS_FL_CHEAPMAX
 #define WS_FL_CHEAPMAX 1
 #endif
@@ -1294,6 +1297,7 @@ __global__ void __launch_bounds__(128, WS_PREP_MINB) k_fluct_prep(const EventDes
     double p_rem = 1.0;
     bool slow_unit = false;
     int bw = 0, bt = 0;
+    int zs = -1;  // first record of the current run of certain-zero draws
     // the bin's weights are loaded one bin ahead (bin need, the last, is in
     // range): the L1 latency hides behind the previous bin's draw (r2: prep
     // 0.89 -> 0.85 ms per C3 event)
@@ -1336,12 +1340,28 @@ __global__ void __launch_bounds__(128, WS_PREP_MINB) k_fluct_prep(const EventDes
         reinterpret_cast<uint32_t*>(&v0.w)[1] = r.cls;
         reinterpret_cast<double2*>(out + b)[0] = make_double2(v0.x, v0.y);
         reinterpret_cast<double2*>(out + b)[1] = make_double2(v0.z, v0.w);
+        if (WS_FL_SKIP > 0) {
+            // a draw that takes 0 electrons for any n <= q (n log1p(-pp) >=
+            // q log1p(-pp) passes the walk's k = 0 test) or p == 0: runs of
+            // them become one skip in the walk (the run's first record)
+            const double xq = __dmul_rn(qd, r.lg);
+            const bool cz = r.cls == kFlZero || (r.cls == kFlDraw && xq > -700.0 && xq > (double)r.lnu + 4e-5);
+            if (cz) {
+                if (zs < 0) zs = (int)b;
+            } else if (zs >= 0) {
+                if ((int)b - zs >= WS_FL_SKIP)
+                    *reinterpret_cast<uint2*>(reinterpret_cast<char*>(out + zs) + 24) = make_uint2((uint32_t)((int)b - zs), kFlSkip);
+                zs = -1;
+            }
+        }
         p_rem -= pi;
         if (++bt == n_t) {
             bt = 0;
             ++bw;
         }
     }
+    if (WS_FL_SKIP > 0 && zs >= 0 && (int)need - zs >= WS_FL_SKIP)
+        *reinterpret_cast<uint2*>(reinterpret_cast<char*>(out + zs) + 24) = make_uint2((uint32_t)((int)need - zs), kFlSkip);
     if (slow_unit) {
         offs[u] = kFlNone;
         slow[atomicAdd(n_slow, 1u)] = u;
@@ -1452,6 +1472,16 @@ __global__ void __launch_bounds__(128, WS_FLWALK_MINB) k_fluct_walk(const EventD
                 const double2 rb = __ldg(reinterpret_cast<const double2*>(rp) + 1);
                 const uint32_t cls = __double2hiint(rb.y);
                 n = remaining;
+                if (cls == kFlSkip) {  // a run of m draws that take 0 electrons
+                    const int m = __double2loint(rb.y);
+                    const int nb = bt + m, dw = nb / n_t, nbt = nb - dw * n_t;
+                    cellp.advance((long long)dw * N + (nbt - bt));
+                    bt = nbt;
+                    b += m;
+                    rp += m;
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(rp + WS_FLWALK_PF));
+                    continue;
+                }
                 if (cls == kFlZero) {
                     commit(0);
                     continue;
