@@ -1208,7 +1208,7 @@ constexpr uint32_t kFlNone = 0xffffffffu;
 #endif
 enum : uint32_t { kFlDraw = 0u, kFlDrawFlip = 1u, kFlZero = 2u, kFlAll = 3u, kFlSkip = 4u };
 #ifndef WS_FL_SKIP
-#define WS_FL_SKIP 2  // shortest run of certain-zero draws k_fluct_prep marks for one skip (0: off)
+#define WS_FL_SKIP 1  // runs of certain-zero draws as one skip record (0: off)
 #endif
 #ifndef WS_FL_CHEAPMAX
 #define WS_FL_CHEAPMAX 1
@@ -1227,6 +1227,12 @@ struct __align__(32) FlRec {
     uint32_t cls;  // kFlDraw / kFlDrawFlip (p > 0.5) / kFlZero (p == 0) / kFlAll (p == 1)
 };
 static_assert(sizeof(FlRec) == 32, "one sector per record");
+// a run of m draws that take 0 electrons: class kFlSkip, m in the lnu slot
+__device__ __forceinline__ void fl_skip_record(FlRec* r, uint32_t m)
+{
+    reinterpret_cast<double2*>(r)[0] = make_double2(0.0, 0.0);
+    reinterpret_cast<double2*>(r)[1] = make_double2(0.0, __hiloint2double((int)kFlSkip, (int)m));
+}
 
 #ifndef WS_PREP_MINB
 #define WS_PREP_MINB 1
@@ -1338,30 +1344,36 @@ __global__ void __launch_bounds__(128, WS_PREP_MINB) k_fluct_prep(const EventDes
         double4 v0 = make_double4(r.pp, r.lg, r.u, 0.0);
         reinterpret_cast<uint32_t*>(&v0.w)[0] = __float_as_uint(r.lnu);
         reinterpret_cast<uint32_t*>(&v0.w)[1] = r.cls;
-        reinterpret_cast<double2*>(out + b)[0] = make_double2(v0.x, v0.y);
-        reinterpret_cast<double2*>(out + b)[1] = make_double2(v0.z, v0.w);
-        if (WS_FL_SKIP > 0) {
-            // a draw that takes 0 electrons for any n <= q (n log1p(-pp) >=
-            // q log1p(-pp) passes the walk's k = 0 test) or p == 0: runs of
-            // them become one skip in the walk (the run's first record)
-            const double xq = __dmul_rn(qd, r.lg);
-            const bool cz = r.cls == kFlZero || (r.cls == kFlDraw && xq > -700.0 && xq > (double)r.lnu + 4e-5);
-            if (cz) {
-                if (zs < 0) zs = (int)b;
-            } else if (zs >= 0) {
-                if ((int)b - zs >= WS_FL_SKIP)
-                    *reinterpret_cast<uint2*>(reinterpret_cast<char*>(out + zs) + 24) = make_uint2((uint32_t)((int)b - zs), kFlSkip);
+#if WS_FL_SKIP
+        // a draw that takes 0 electrons for any n <= q (n log1p(-pp) >=
+        // q log1p(-pp) passes the walk's k = 0 test) or p == 0: a run of them
+        // is one skip record (the run's first slot; the others are never read
+        // and never written)
+        const double xq = __dmul_rn(qd, r.lg);
+        const bool cz = r.cls == kFlZero || (r.cls == kFlDraw && xq > -700.0 && xq > (double)r.lnu + 4e-5);
+        if (cz) {
+            if (zs < 0) zs = (int)b;
+        } else {
+            if (zs >= 0) {
+                fl_skip_record(out + zs, (uint32_t)((int)b - zs));
                 zs = -1;
             }
+            reinterpret_cast<double2*>(out + b)[0] = make_double2(v0.x, v0.y);
+            reinterpret_cast<double2*>(out + b)[1] = make_double2(v0.z, v0.w);
         }
+#else
+        reinterpret_cast<double2*>(out + b)[0] = make_double2(v0.x, v0.y);
+        reinterpret_cast<double2*>(out + b)[1] = make_double2(v0.z, v0.w);
+#endif
         p_rem -= pi;
         if (++bt == n_t) {
             bt = 0;
             ++bw;
         }
     }
-    if (WS_FL_SKIP > 0 && zs >= 0 && (int)need - zs >= WS_FL_SKIP)
-        *reinterpret_cast<uint2*>(reinterpret_cast<char*>(out + zs) + 24) = make_uint2((uint32_t)((int)need - zs), kFlSkip);
+#if WS_FL_SKIP
+    if (zs >= 0) fl_skip_record(out + zs, (uint32_t)((int)need - zs));
+#endif
     if (slow_unit) {
         offs[u] = kFlNone;
         slow[atomicAdd(n_slow, 1u)] = u;
