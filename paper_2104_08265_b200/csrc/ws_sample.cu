@@ -1394,6 +1394,9 @@ __global__ void __launch_bounds__(128, WS_PREP_MINB) k_fluct_prep(const EventDes
 // The walk takes kWalk CDF steps per iteration: the recursion factors are
 // independent, the serial chain is pmf *= f, cdf += pmf, and as the CDF never
 // decreases the stop is the first step with cdf > u.
+#ifdef WS_WALK_PROF
+__device__ unsigned long long g_walkprof[16];
+#endif
 __global__ void __launch_bounds__(128, WS_FLWALK_MINB) k_fluct_walk(const EventDesc ev, const UnitRec* __restrict__ recs,
                                                      const uint32_t* __restrict__ order,
                                                      const uint32_t* __restrict__ offs, uint32_t* __restrict__ cursor)
@@ -1450,17 +1453,32 @@ __global__ void __launch_bounds__(128, WS_FLWALK_MINB) k_fluct_walk(const EventD
     take(blockIdx.x * blockDim.x + threadIdx.x);
 
     int64_t kdone = -1;  // a draw the walk finished, committed by the next setup (all idle lanes together)
+#ifdef WS_WALK_PROF
+    unsigned long long wp[16] = {};
+#endif
     auto setup = [&]() {
+#ifdef WS_WALK_PROF
+        const long long wp_c = clock64();
+#endif
         if (kdone >= 0) {
             commit(kdone);
             kdone = -1;
         }
+#ifdef WS_WALK_PROF
+        __syncwarp();
+        wp[11] += clock64() - wp_c;
+        const long long wp_l = clock64();
+#endif
         bool seed = false;  // the current draw needs its pmf seed
         double pp = 0.0, lg = 0.0, x = 0.0;
 #pragma unroll 1
         for (;;) {
             // lanes without a unit take the next ones (one atomic per warp)
             const unsigned want = __ballot_sync(0xffffffffu, !has && !exhausted);
+#ifdef WS_WALK_PROF
+            wp[13] += 1;
+            if (want) wp[8] += 1;
+#endif
             if (want) {
                 uint32_t base = 0;
                 if (lane == __ffs(want) - 1) base = atomicAdd(cursor, (uint32_t)__popc(want));
@@ -1475,6 +1493,9 @@ __global__ void __launch_bounds__(128, WS_FLWALK_MINB) k_fluct_walk(const EventD
             // (r2: walk 4.40 -> 4.13 ms per C3 event with quorum 8/16)
             int cheap = 0;
             while (has && !walking && !seed && cheap++ < WS_FL_CHEAPMAX) {
+#ifdef WS_WALK_PROF
+                wp[14] += 1;
+#endif
                 if (remaining == 0 || b >= last) {
                     if (remaining) lastp.add(remaining);  // the last bin takes the rest
                     has = false;
@@ -1515,6 +1536,12 @@ __global__ void __launch_bounds__(128, WS_FLWALK_MINB) k_fluct_walk(const EventD
             }
             if (!__any_sync(0xffffffffu, !has && !exhausted)) break;
         }
+#ifdef WS_WALK_PROF
+        __syncwarp();
+        wp[12] += clock64() - wp_l;
+        const long long wp_sd = clock64();
+        wp[10] += __popc(__ballot_sync(0xffffffffu, seed));
+#endif
         if (seed) {
             // invert_binomial_cdf (rng.cpp:146-170): the pmf seed
             odds = __ddiv_rn(pp, __dsub_rn(1.0, pp));
@@ -1545,20 +1572,43 @@ __global__ void __launch_bounds__(128, WS_FLWALK_MINB) k_fluct_walk(const EventD
                 commit(flip ? n - k : k);
             }
         }
+#ifdef WS_WALK_PROF
+        __syncwarp();
+        wp[9] += clock64() - wp_sd;
+#endif
     };
 
 #ifndef WS_FL_KWALK
 #define WS_FL_KWALK 7  // CDF steps per iteration (r2 sweep 2-12 at 64 / 72 / 80 registers: 7 at 72, 4.12 -> 3.6 ms)
 #endif
     constexpr int kWalk = WS_FL_KWALK;
+#ifdef WS_WALK_PROF
+    const long long wp_t0 = clock64();
+#endif
 #pragma unroll 1
     for (;;) {
+#ifdef WS_WALK_PROF
+        const long long wp_s = clock64();
         setup();
+        wp[0] += clock64() - wp_s;
+        wp[4] += 1;
+#else
+        setup();
+#endif
         const unsigned alive = __ballot_sync(0xffffffffu, has);  // (lanes without a unit are exhausted)
         if (!alive) break;
         const int quorum = max(1, (__popc(alive) * ev.fl_quorum) >> 4);
+#ifdef WS_WALK_PROF
+        wp[5] += __popc(alive);
+        wp[7] += __popc(__ballot_sync(0xffffffffu, walking));
+        const long long wp_w = clock64();
+#endif
 #pragma unroll 1
         for (;;) {
+#ifdef WS_WALK_PROF
+            wp[2] += 1;
+            wp[3] += __popc(__ballot_sync(0xffffffffu, walking));
+#endif
             if (walking) {
                 double f[kWalk];
                 if (kr + kWalk <= kRecipN) {
@@ -1620,10 +1670,36 @@ __global__ void __launch_bounds__(128, WS_FLWALK_MINB) k_fluct_walk(const EventD
             const unsigned wk = __ballot_sync(0xffffffffu, walking);
             if (wk == 0 || __popc(alive & ~wk) >= quorum) break;
         }
+#ifdef WS_WALK_PROF
+        wp[1] += clock64() - wp_w;
+#endif
     }
+#ifdef WS_WALK_PROF
+    wp[6] = clock64() - wp_t0;
+    if (lane == 0)
+        for (int i = 0; i < 16; ++i) atomicAdd(&g_walkprof[i], wp[i]);
+#endif
 }
 
 }  // namespace wsb
+
+#ifdef WS_WALK_PROF
+#include <cstdio>
+// tools/walkprof.py (a -DWS_WALK_PROF build): where the walk's warps spend their cycles
+extern "C" void wsb_walk_prof_dump()
+{
+    unsigned long long h[16];
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(h, wsb::g_walkprof, sizeof(h));
+    fprintf(stderr, "walkprof setup_cyc %llu walk_cyc %llu total_cyc %llu | walk_iters %llu walking_lanes/iter %.2f | setups %llu alive/setup %.2f walking_after_setup %.2f\n",
+            h[0], h[1], h[6], h[2], h[2] ? (double)h[3] / h[2] : 0.0, h[4], h[4] ? (double)h[5] / h[4] : 0.0,
+            h[4] ? (double)h[7] / h[4] : 0.0);
+    fprintf(stderr, "walkprof take_passes %llu seed_cyc %llu seeding_lanes/setup %.2f commit_cyc %llu loop_cyc %llu loop_passes %llu cheap_lane_iters %llu\n",
+            h[8], h[9], h[4] ? (double)h[10] / h[4] : 0.0, h[11], h[12], h[13], h[14]);
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(wsb::g_walkprof, z, sizeof(z));
+}
+#endif
 
 extern "C" cudaError_t wsb_launch_sample(const wsb::EventDesc& ev, wsb::UnitRec* recs, uint32_t* pool, uint32_t pool_cap,
                                          uint32_t* pool_ctr, uint32_t* band_count, unsigned* err, cudaStream_t s,
