@@ -1228,9 +1228,10 @@ struct __align__(32) FlRec {
 };
 static_assert(sizeof(FlRec) == 32, "one sector per record");
 // a run of m draws that take 0 electrons: class kFlSkip, m in the lnu slot
-__device__ __forceinline__ void fl_skip_record(FlRec* r, uint32_t m)
+// and, in the first slot, the cell advance over the run and the tick the run ends on
+__device__ __forceinline__ void fl_skip_record(FlRec* r, uint32_t m, int adv, int bt_end)
 {
-    reinterpret_cast<double2*>(r)[0] = make_double2(0.0, 0.0);
+    reinterpret_cast<double2*>(r)[0] = make_double2(__hiloint2double(bt_end, adv), 0.0);
     reinterpret_cast<double2*>(r)[1] = make_double2(0.0, __hiloint2double((int)kFlSkip, (int)m));
 }
 
@@ -1303,7 +1304,7 @@ __global__ void __launch_bounds__(128, WS_PREP_MINB) k_fluct_prep(const EventDes
     double p_rem = 1.0;
     bool slow_unit = false;
     int bw = 0, bt = 0;
-    int zs = -1;  // first record of the current run of certain-zero draws
+    int zs = -1, zbw = 0, zbt = 0;  // first record of the current run of certain-zero draws, its bin
     // the bin's weights are loaded one bin ahead (bin need, the last, is in
     // range): the L1 latency hides behind the previous bin's draw (r2: prep
     // 0.89 -> 0.85 ms per C3 event)
@@ -1352,10 +1353,14 @@ __global__ void __launch_bounds__(128, WS_PREP_MINB) k_fluct_prep(const EventDes
         const double xq = __dmul_rn(qd, r.lg);
         const bool cz = r.cls == kFlZero || (r.cls == kFlDraw && xq > -700.0 && xq > (double)r.lnu + 4e-5);
         if (cz) {
-            if (zs < 0) zs = (int)b;
+            if (zs < 0) {
+                zs = (int)b;
+                zbw = bw;
+                zbt = bt;
+            }
         } else {
             if (zs >= 0) {
-                fl_skip_record(out + zs, (uint32_t)((int)b - zs));
+                fl_skip_record(out + zs, (uint32_t)((int)b - zs), (bw - zbw) * P.N + (bt - zbt), bt);
                 zs = -1;
             }
             reinterpret_cast<double2*>(out + b)[0] = make_double2(v0.x, v0.y);
@@ -1372,7 +1377,7 @@ __global__ void __launch_bounds__(128, WS_PREP_MINB) k_fluct_prep(const EventDes
         }
     }
 #if WS_FL_SKIP
-    if (zs >= 0) fl_skip_record(out + zs, (uint32_t)((int)need - zs));
+    if (zs >= 0) fl_skip_record(out + zs, (uint32_t)((int)need - zs), (bw - zbw) * P.N + (bt - zbt), bt);
 #endif
     if (slow_unit) {
         offs[u] = kFlNone;
@@ -1507,9 +1512,8 @@ __global__ void __launch_bounds__(128, WS_FLWALK_MINB) k_fluct_walk(const EventD
                 n = remaining;
                 if (cls == kFlSkip) {  // a run of m draws that take 0 electrons
                     const int m = __double2loint(rb.y);
-                    const int nb = bt + m, dw = nb / n_t, nbt = nb - dw * n_t;
-                    cellp.advance((long long)dw * N + (nbt - bt));
-                    bt = nbt;
+                    cellp.advance((long long)__double2loint(ra.x));  // (prep: rows x N + ticks)
+                    bt = __double2hiint(ra.x);
                     b += m;
                     rp += m;
                     asm volatile("prefetch.global.L1 [%0];" ::"l"(rp + WS_FLWALK_PF));
