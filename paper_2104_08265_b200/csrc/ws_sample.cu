@@ -1198,7 +1198,7 @@ __global__ void __launch_bounds__(128) k_fluctuate_exact(const EventDesc ev, con
 // whole (kErrFluct only tells the host to grow the buffer).
 constexpr uint32_t kFlNone = 0xffffffffu;
 #ifndef WS_FLWALK_MINB
-#define WS_FLWALK_MINB 7  // 72 registers, 28 warps per SM (with 7 CDF steps per iteration; 64 registers spilled)
+#define WS_FLWALK_MINB 6  // 80 registers, 24 warps per SM (r2 re-sweep with skip records: 6 x 10 steps 3.20 ms, 7 x 7 3.36, 7 x 9 3.30, 8 x 7 3.52)
 #endif
 #ifndef WS_FLWALK_PF
 #define WS_FLWALK_PF 3
@@ -1583,7 +1583,7 @@ __global__ void __launch_bounds__(128, WS_FLWALK_MINB) k_fluct_walk(const EventD
     };
 
 #ifndef WS_FL_KWALK
-#define WS_FL_KWALK 7  // CDF steps per iteration (r2 sweep 2-12 at 64 / 72 / 80 registers: 7 at 72, 4.12 -> 3.6 ms)
+#define WS_FL_KWALK 10  // CDF steps per iteration (sweeps: 7 at 72 registers before skip records, 10 at 80 after: 9 / 10 / 11 / 12 = 3.24 / 3.20 / 3.22 / 3.27 ms)
 #endif
     constexpr int kWalk = WS_FL_KWALK;
 #ifdef WS_WALK_PROF
