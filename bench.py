@@ -128,7 +128,24 @@ def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("WS_BENCH_SHARED_GPU") == "1":
+        # test mode for the multi-rank path on a box with fewer GPUs than
+        # ranks: ranks share devices (use WS_BENCH_BACKEND=gloo: NCCL refuses
+        # two ranks on one GPU); never for a reported number
+        import torch
+        local = local % max(1, torch.cuda.device_count())
     return world, rank, local
+
+
+def init_dist(local: int):
+    import torch
+    import torch.distributed as dist
+    backend = os.environ.get("WS_BENCH_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
+    return backend
 
 
 def relaunch_distributed(n: int) -> int:
@@ -504,8 +521,7 @@ def run_sim(args, world, rank, local):
         return
 
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    backend = init_dist(local) if world > 1 else "nccl"
 
     def barrier():
         if world > 1:
@@ -514,7 +530,7 @@ def run_sim(args, world, rank, local):
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        t = torch.tensor([x], device="cuda" if backend == "nccl" else "cpu", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
