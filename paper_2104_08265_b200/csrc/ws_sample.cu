@@ -1305,6 +1305,7 @@ __global__ void __launch_bounds__(128, WS_PREP_MINB) k_fluct_prep(const EventDes
     bool slow_unit = false;
     int bw = 0, bt = 0;
     int zs = -1, zbw = 0, zbt = 0;  // first record of the current run of certain-zero draws, its bin
+    const bool can_skip = (long long)rec.n_w * P.N < (1ll << 31);  // a skip's cell advance fits its int32 slot
     // the bin's weights are loaded one bin ahead (bin need, the last, is in
     // range): the L1 latency hides behind the previous bin's draw (r2: prep
     // 0.89 -> 0.85 ms per C3 event)
@@ -1351,7 +1352,7 @@ __global__ void __launch_bounds__(128, WS_PREP_MINB) k_fluct_prep(const EventDes
         // is one skip record (the run's first slot; the others are never read
         // and never written)
         const double xq = __dmul_rn(qd, r.lg);
-        const bool cz = r.cls == kFlZero || (r.cls == kFlDraw && xq > -700.0 && xq > (double)r.lnu + 4e-5);
+        const bool cz = can_skip && (r.cls == kFlZero || (r.cls == kFlDraw && xq > -700.0 && xq > (double)r.lnu + 4e-5));
         if (cz) {
             if (zs < 0) {
                 zs = (int)b;
