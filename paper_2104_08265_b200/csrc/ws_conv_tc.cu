@@ -991,7 +991,11 @@ extern "C" cudaError_t wsb_launch_conv_tc2(const wsb::EventDesc& ev, cudaStream_
     const char* off = getenv("WS_CONV_TC2");  // 0: the one-tile-at-a-time kernel (A/B, tests)
     if (off && atoi(off) == 0) return cudaErrorNotSupported;
     T2Plan plan{};
-    plan.chunk = 8;
+    static const int chunk = [] {
+        const char* v = getenv("WS_CONV_TC2_CHUNK");  // sub-blocks per work item (tuning only)
+        return v ? std::max(1, std::min(64, atoi(v))) : 8;
+    }();
+    plan.chunk = chunk;
     uint32_t eoff = kT2Slots * kT2SlotBytes + kT2Raw * kT2RawSlot;
     int h = -1, src = -1;
     for (int i = 0; i < ev.n_planes; ++i) {
