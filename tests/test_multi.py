@@ -84,3 +84,23 @@ def test_cost_model_matches_c_abi():
     lib = _lib.load()
     for w, t, n in ((2600, 9800, 100_000), (1000, 6200, 0), (680, 6200, 10_000)):
         assert lib.ws_multi_cost(w * t, n) == unit_cost(w, t, n)
+
+
+def test_bench_rank_device_mapping(monkeypatch):
+    """bench.py's rank -> device mapping: LOCAL_RANK as is (one GPU per rank),
+    or modulo the visible devices in the shared-GPU test mode (a path check on
+    a box with fewer GPUs than ranks; never a reported number)."""
+    import importlib
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    bench = importlib.import_module("bench")
+    monkeypatch.setenv("WORLD_SIZE", "4")
+    monkeypatch.setenv("RANK", "3")
+    monkeypatch.setenv("LOCAL_RANK", "3")
+    monkeypatch.delenv("WS_BENCH_SHARED_GPU", raising=False)
+    assert bench.dist_setup() == (4, 3, 3)
+    monkeypatch.setenv("WS_BENCH_SHARED_GPU", "1")
+    import torch
+    n = max(1, torch.cuda.device_count())
+    assert bench.dist_setup() == (4, 3, 3 % n)
